@@ -1,0 +1,354 @@
+/*
+ * dd_oracle.c -- CPU restatement of the reference dd Rgemm / Rsyrk.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the checker for the CUDA path:
+ * only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load it.  The product path never calls it.
+ *
+ * It restates, element by element, what the reference package computes
+ * (/root/reference/pkg/src/mpkit), so a GPU result in `exact` mode can be
+ * compared bit for bit:
+ *
+ *   two_sum            elem.py:32-35      (ddarith.py:37-41)
+ *   quick_two_sum      elem.py:38-40      (ddarith.py:44-47)
+ *   two_prod (Dekker)  elem.py:43-51      (ddarith.py:50-62), splitter elem.py:25
+ *   add2 (accurate)    elem.py:54-66      -- vectorised variant: only s0 is checked
+ *   mul2               elem.py:69-78      -- vectorised variant: (p, e) checked
+ *   Rgemm order        level23.py:107-149 (_gemm_core), :163-177 (_scale_full,
+ *                      _combine), :180-198 (Rgemm validation / early exit)
+ *   Rsyrk order        level23.py:226-285
+ *
+ * Validation returns the reference argument index (level23.py:84-96,
+ * :233-239); 0 means success.
+ *
+ * Parity of this restatement with the reference is pinned by
+ * tests/test_oracle.py against tests/golden/ (npz fixtures), which
+ * oracle/gen_golden.py produced by running the reference itself.
+ *
+ * Build: see oracle/Makefile (-ffp-contract=off: no FMA contraction).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define SPLITTER 134217729.0 /* 2**27 + 1, elem.py:25 */
+
+typedef struct { double h, l; } dd;
+
+#if defined(__GNUC__) && !defined(__clang__)
+#define CLONES __attribute__((target_clones("avx512f", "avx2", "default")))
+#else
+#define CLONES
+#endif
+
+static inline void two_sum(double a, double b, double *s, double *e) {
+    double ss = a + b;
+    double bb = ss - a;
+    *e = (a - (ss - bb)) + (b - bb);
+    *s = ss;
+}
+
+static inline void quick_two_sum(double a, double b, double *s, double *e) {
+    double ss = a + b;
+    *e = b - (ss - a);
+    *s = ss;
+}
+
+static inline void two_prod(double a, double b, double *p, double *e) {
+    double pp = a * b;
+    double t = SPLITTER * a;
+    double ah = t - (t - a);
+    double al = a - ah;
+    t = SPLITTER * b;
+    double bh = t - (t - b);
+    double bl = b - bh;
+    *e = (((ah * bh - pp) + ah * bl) + al * bh) + al * bl;
+    *p = pp;
+}
+
+/* elem.py:54-66 */
+static inline dd add2(dd x, dd y) {
+    double s0 = x.h + y.h;
+    double sh, sl, th, tl;
+    two_sum(x.h, y.h, &sh, &sl);
+    two_sum(x.l, y.l, &th, &tl);
+    sl = sl + th;
+    quick_two_sum(sh, sl, &sh, &sl);
+    sl = sl + tl;
+    quick_two_sum(sh, sl, &sh, &sl);
+    dd r;
+    if (!isfinite(s0)) { r.h = s0; r.l = 0.0; }
+    else { r.h = sh; r.l = sl; }
+    return r;
+}
+
+/* elem.py:69-78 */
+static inline dd mul2(dd x, dd y) {
+    double p, e;
+    two_prod(x.h, y.h, &p, &e);
+    int bad = !(isfinite(p) && isfinite(e));
+    e = e + (x.h * y.l + x.l * y.h);
+    double rh, rl;
+    quick_two_sum(p, e, &rh, &rl);
+    dd r;
+    if (bad) { r.h = p; r.l = 0.0; }
+    else { r.h = rh; r.l = rl; }
+    return r;
+}
+
+static inline int is_zero(dd v) { return v.h == 0.0 && v.l == 0.0; }     /* DDouble.__bool__ */
+static inline int is_one(dd v) { return v.h == 1.0 && v.l == 0.0; }      /* _cmp2 == 0 vs 1 */
+
+static int upflag(char c) { return (c >= 'a' && c <= 'z') ? c - 32 : c; }
+
+/* level23.py:84-96 */
+int oracle_gemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                         int64_t lda, int64_t ldb, int64_t ldc) {
+    int ta = upflag(transa), tb = upflag(transb);
+    if (ta != 'N' && ta != 'T' && ta != 'C') return 1;
+    if (tb != 'N' && tb != 'T' && tb != 'C') return 2;
+    if (m < 0) return 3;
+    if (n < 0) return 4;
+    if (k < 0) return 5;
+    int64_t nrowa = ta == 'N' ? m : k;
+    int64_t nrowb = tb == 'N' ? k : n;
+    if (lda < (nrowa > 1 ? nrowa : 1)) return 8;
+    if (ldb < (nrowb > 1 ? nrowb : 1)) return 10;
+    if (ldc < (m > 1 ? m : 1)) return 13;
+    return 0;
+}
+
+/* level23.py:233-239 */
+int oracle_syrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc) {
+    int u = upflag(uplo), t = upflag(trans);
+    if (u != 'U' && u != 'L') return 1;
+    if (t != 'N' && t != 'T' && t != 'C') return 2;
+    if (n < 0) return 3;
+    if (k < 0) return 4;
+    int64_t nrowa = t == 'N' ? n : k;
+    if (lda < (nrowa > 1 ? nrowa : 1)) return 7;
+    if (ldc < (n > 1 ? n : 1)) return 10;
+    return 0;
+}
+
+static inline dd ld_(const double *h, const double *l, int64_t idx) {
+    dd v; v.h = h[idx]; v.l = l[idx]; return v;
+}
+
+/* beta rule of _scale_full (level23.py:163-169) applied to one element */
+static inline dd scale_beta(dd beta, dd c) {
+    if (is_zero(beta)) { dd z = {0.0, 0.0}; return z; }
+    if (is_one(beta)) return c;
+    return mul2(beta, c);
+}
+
+/* One column j of NN / NT Rgemm (level23.py:120-125, :134-140).  t is a
+ * k-scratch; the per-element order is exactly c = add2(c, mul2(A(i,l), t_l))
+ * for l ascending after the beta rule. */
+CLONES
+static void gemm_col_notrans_a(int tb, int64_t m, int64_t k, dd alpha,
+                               const double *Ah, const double *Al, int64_t lda,
+                               const double *Bh, const double *Bl, int64_t ldb,
+                               dd beta, double *Ch, double *Cl, int64_t ldc,
+                               int64_t j, dd *t, dd *c) {
+    for (int64_t l = 0; l < k; ++l) {
+        int64_t bidx = tb == 'N' ? l + j * ldb : j + l * ldb;
+        t[l] = mul2(alpha, ld_(Bh, Bl, bidx));
+    }
+    for (int64_t i = 0; i < m; ++i) c[i] = scale_beta(beta, ld_(Ch, Cl, i + j * ldc));
+    for (int64_t l = 0; l < k; ++l) {
+        const double *ah = Ah + l * lda, *al = Al + l * lda;
+        dd tl = t[l];
+        for (int64_t i = 0; i < m; ++i) {
+            dd a; a.h = ah[i]; a.l = al[i];
+            c[i] = add2(c[i], mul2(a, tl));
+        }
+    }
+    for (int64_t i = 0; i < m; ++i) { Ch[i + j * ldc] = c[i].h; Cl[i + j * ldc] = c[i].l; }
+}
+
+/* _combine (level23.py:172-177) */
+static inline dd combine(dd alpha, dd acc, dd beta, dd c0) {
+    dd at = mul2(alpha, acc);
+    if (is_zero(beta)) return at;
+    return add2(at, mul2(beta, c0));
+}
+
+/* One column j of TN / TT Rgemm (level23.py:126-133, :141-149). */
+CLONES
+static void gemm_col_trans_a(int tb, int64_t m, int64_t k, dd alpha,
+                             const double *Ah, const double *Al, int64_t lda,
+                             const double *Bh, const double *Bl, int64_t ldb,
+                             dd beta, double *Ch, double *Cl, int64_t ldc,
+                             int64_t j, dd *t, dd *c) {
+    for (int64_t l = 0; l < k; ++l) {
+        int64_t bidx = tb == 'N' ? l + j * ldb : j + l * ldb;
+        t[l] = ld_(Bh, Bl, bidx);
+    }
+    for (int64_t i = 0; i < m; ++i) {
+        const double *ah = Ah + i * lda, *al = Al + i * lda;
+        dd acc = {0.0, 0.0};
+        for (int64_t l = 0; l < k; ++l) {
+            dd a; a.h = ah[l]; a.l = al[l];
+            acc = add2(acc, mul2(a, t[l]));
+        }
+        c[i] = combine(alpha, acc, beta, ld_(Ch, Cl, i + j * ldc));
+    }
+    for (int64_t i = 0; i < m; ++i) { Ch[i + j * ldc] = c[i].h; Cl[i + j * ldc] = c[i].l; }
+}
+
+/* ---- host threading: columns of C are independent (the disjoint-panel
+ * argument of parallel.py:102-125), so workers pull column indices from an
+ * atomic counter.  Results do not depend on the thread count. */
+#include <pthread.h>
+#include <unistd.h>
+
+typedef struct {
+    void (*col)(void *ctx, int64_t j, dd *t, dd *c);
+    void *ctx;
+    int64_t n, k, m;
+    int64_t next;       /* atomic */
+    int err;            /* atomic */
+} pool_job;
+
+static void *pool_worker(void *arg) {
+    pool_job *job = (pool_job *)arg;
+    dd *t = (dd *)malloc(sizeof(dd) * (size_t)(job->k > 0 ? job->k : 1));
+    dd *c = (dd *)malloc(sizeof(dd) * (size_t)(job->m > 0 ? job->m : 1));
+    if (!t || !c) {
+        __atomic_store_n(&job->err, -1, __ATOMIC_SEQ_CST);
+    } else {
+        for (;;) {
+            int64_t j = __atomic_fetch_add(&job->next, 1, __ATOMIC_SEQ_CST);
+            if (j >= job->n) break;
+            job->col(job->ctx, j, t, c);
+        }
+    }
+    free(t);
+    free(c);
+    return NULL;
+}
+
+int oracle_max_threads(void) {
+    long v = sysconf(_SC_NPROCESSORS_ONLN);
+    return v > 0 ? (int)v : 1;
+}
+
+static int run_columns(void (*col)(void *, int64_t, dd *, dd *), void *ctx,
+                       int64_t n, int64_t k, int64_t m, int nthreads) {
+    pool_job job = {col, ctx, n, k, m, 0, 0};
+    if (nthreads <= 0) nthreads = oracle_max_threads();
+    if (nthreads > n) nthreads = (int)(n > 0 ? n : 1);
+    if (nthreads <= 1) { pool_worker(&job); return job.err; }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    if (!th) return -1;
+    int started = 0;
+    for (int i = 0; i < nthreads; ++i)
+        if (pthread_create(&th[i], NULL, pool_worker, &job) == 0) ++started;
+    if (started == 0) pool_worker(&job);
+    for (int i = 0; i < started; ++i) pthread_join(th[i], NULL);
+    free(th);
+    return job.err;
+}
+
+typedef struct {
+    int ta, tb, up, tn;
+    int64_t m, k;
+    dd alpha, beta;
+    const double *Ah, *Al, *Bh, *Bl;
+    double *Ch, *Cl;
+    int64_t lda, ldb, ldc, n;
+} call_ctx;
+
+static void gemm_col(void *p, int64_t j, dd *t, dd *c) {
+    call_ctx *x = (call_ctx *)p;
+    if (x->ta == 'N')
+        gemm_col_notrans_a(x->tb, x->m, x->k, x->alpha, x->Ah, x->Al, x->lda, x->Bh, x->Bl,
+                           x->ldb, x->beta, x->Ch, x->Cl, x->ldc, j, t, c);
+    else
+        gemm_col_trans_a(x->tb, x->m, x->k, x->alpha, x->Ah, x->Al, x->lda, x->Bh, x->Bl,
+                         x->ldb, x->beta, x->Ch, x->Cl, x->ldc, j, t, c);
+}
+
+/* level23.py:180-198 + _gemm_core. */
+int oracle_rgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                 double alpha_hi, double alpha_lo,
+                 const double *Ah, const double *Al, int64_t lda,
+                 const double *Bh, const double *Bl, int64_t ldb,
+                 double beta_hi, double beta_lo,
+                 double *Ch, double *Cl, int64_t ldc, int nthreads) {
+    int rc = oracle_gemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+    if (rc) return rc;
+    dd alpha = {alpha_hi, alpha_lo}, beta = {beta_hi, beta_lo};
+    if (m == 0 || n == 0 || ((is_zero(alpha) || k == 0) && is_one(beta))) return 0;
+    if (is_zero(alpha)) {                       /* _gemm_core :110-115 */
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < m; ++i) {
+                dd c = scale_beta(beta, ld_(Ch, Cl, i + j * ldc));
+                Ch[i + j * ldc] = c.h; Cl[i + j * ldc] = c.l;
+            }
+        return 0;
+    }
+    call_ctx x = {upflag(transa), upflag(transb), 0, 0, m, k, alpha, beta,
+                  Ah, Al, Bh, Bl, Ch, Cl, lda, ldb, ldc, n};
+    return run_columns(gemm_col, &x, n, k, m, nthreads);
+}
+
+static void syrk_col(void *p, int64_t j, dd *t, dd *cs) {
+    call_ctx *x = (call_ctx *)p;
+    (void)cs;
+    const double *Ah = x->Ah, *Al = x->Al;
+    double *Ch = x->Ch, *Cl = x->Cl;
+    int64_t lda = x->lda, ldc = x->ldc, k = x->k;
+    int64_t i0 = x->up ? 0 : j, i1 = x->up ? j + 1 : x->n;
+    if (is_zero(x->alpha)) {                    /* _scale_masked, :247-249 */
+        for (int64_t i = i0; i < i1; ++i) {
+            dd c = scale_beta(x->beta, ld_(Ch, Cl, i + j * ldc));
+            Ch[i + j * ldc] = c.h; Cl[i + j * ldc] = c.l;
+        }
+        return;
+    }
+    if (x->tn) {                                /* :250-258, == NT Rgemm with B = A */
+        for (int64_t l = 0; l < k; ++l) t[l] = mul2(x->alpha, ld_(Ah, Al, j + l * lda));
+        for (int64_t i = i0; i < i1; ++i) {
+            dd c = scale_beta(x->beta, ld_(Ch, Cl, i + j * ldc));
+            for (int64_t l = 0; l < k; ++l)
+                c = add2(c, mul2(ld_(Ah, Al, i + l * lda), t[l]));
+            Ch[i + j * ldc] = c.h; Cl[i + j * ldc] = c.l;
+        }
+    } else {                                    /* :259-270, == TN Rgemm with B = A */
+        for (int64_t i = i0; i < i1; ++i) {
+            dd acc = {0.0, 0.0};
+            for (int64_t l = 0; l < k; ++l)
+                acc = add2(acc, mul2(ld_(Ah, Al, l + i * lda), ld_(Ah, Al, l + j * lda)));
+            dd c = combine(x->alpha, acc, x->beta, ld_(Ch, Cl, i + j * ldc));
+            Ch[i + j * ldc] = c.h; Cl[i + j * ldc] = c.l;
+        }
+    }
+}
+
+/* level23.py:226-285.  Only (i, j) in the uplo triangle are written. */
+int oracle_rsyrk(char uplo, char trans, int64_t n, int64_t k,
+                 double alpha_hi, double alpha_lo,
+                 const double *Ah, const double *Al, int64_t lda,
+                 double beta_hi, double beta_lo,
+                 double *Ch, double *Cl, int64_t ldc, int nthreads) {
+    int rc = oracle_syrk_validate(uplo, trans, n, k, lda, ldc);
+    if (rc) return rc;
+    dd alpha = {alpha_hi, alpha_lo}, beta = {beta_hi, beta_lo};
+    if (n == 0 || ((is_zero(alpha) || k == 0) && is_one(beta))) return 0;
+    call_ctx x = {0, 0, upflag(uplo) == 'U', upflag(trans) == 'N', n, k, alpha, beta,
+                  Ah, Al, NULL, NULL, Ch, Cl, lda, 0, ldc, n};
+    return run_columns(syrk_col, &x, n, k, n, nthreads);
+}
+
+/* Scalar EFT entry points, for pinning the restatement against the
+ * reference's scalar kernels (tests/test_oracle.py). */
+void oracle_add2(double xh, double xl, double yh, double yl, double *out) {
+    dd x = {xh, xl}, y = {yh, yl}, r = add2(x, y); out[0] = r.h; out[1] = r.l;
+}
+void oracle_mul2(double xh, double xl, double yh, double yl, double *out) {
+    dd x = {xh, xl}, y = {yh, yl}, r = mul2(x, y); out[0] = r.h; out[1] = r.l;
+}
+void oracle_two_prod(double a, double b, double *out) { two_prod(a, b, &out[0], &out[1]); }

@@ -1,0 +1,202 @@
+"""Generate tests/golden/ fixtures by running the REFERENCE itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python oracle/gen_golden.py
+
+It imports the reference package from /root/reference/pkg/src, runs its own
+``mpkit.mpblas.Rgemm`` / ``Rsyrk`` (level23.py:180, :226) and its vectorised dd
+element kernels (elem.py:43-78) on seeded inputs, and stores inputs + outputs
+as compressed npz fixtures plus a JSON manifest.  The GPU parity tests and the
+C oracle are pinned against these bytes; nothing at test time reads
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+OUT = os.path.join(REPO, "tests", "golden")
+sys.path.insert(0, REPO)
+
+from oracle.golden import case_inputs, input_digest  # noqa: E402
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import mpkit.mpblas as mb
+    from mpkit.mpblas import elem
+    from mpkit.ddarith import DDouble
+    return mb, elem, DDouble
+
+
+def _matrix(mb, m, n, ld, planes):
+    mat = mb.Matrix(m, n, "dd", ld)
+    mat.store = (planes[0].copy(), planes[1].copy())
+    return mat
+
+
+ALPHAS = {
+    "a15": (1.5, 0.0),
+    "a15lo": (1.5, 1.5 * 2.0 ** -60),
+    "aneg": (-0.75, 2.0 ** -58),
+    "a0": (0.0, 0.0),
+}
+BETAS = {
+    "b05lo": (0.5, 2.0 ** -58),
+    "b1": (1.0, 0.0),
+    "b0": (0.0, 0.0),
+    "bneg": (-0.5, 0.0),
+}
+
+
+def gemm_cases():
+    cases = []
+    seed = 100
+    # every trans pair incl. 'C' and lower case, every beta rule, padded lds
+    for ta in ("N", "T", "C", "n", "t"):
+        for tb in ("N", "T", "C", "n", "t"):
+            for bname in ("b05lo", "b1", "b0"):
+                if ta in "nt" or tb in "nt":
+                    if bname != "b05lo":
+                        continue
+                m, n, k = 13, 11, 17
+                cases.append(dict(routine="Rgemm", transa=ta, transb=tb, m=m, n=n, k=k,
+                                  pad=(3, 2, 5), alpha="a15lo", beta=bname, seed=seed))
+                seed += 1
+    # tile-boundary crossing shapes (> 128 rows / cols, ragged)
+    for ta, tb in (("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")):
+        cases.append(dict(routine="Rgemm", transa=ta, transb=tb, m=133, n=70, k=41,
+                          pad=(1, 0, 3), alpha="a15", beta="b05lo", seed=seed))
+        seed += 1
+    # alpha = 0, k = 0, negative alpha
+    for ta in ("N", "T"):
+        cases.append(dict(routine="Rgemm", transa=ta, transb="N", m=7, n=5, k=6,
+                          pad=(0, 0, 0), alpha="a0", beta="bneg", seed=seed)); seed += 1
+        cases.append(dict(routine="Rgemm", transa=ta, transb="N", m=7, n=5, k=0,
+                          pad=(0, 0, 0), alpha="a15", beta="bneg", seed=seed)); seed += 1
+        cases.append(dict(routine="Rgemm", transa=ta, transb="T", m=9, n=6, k=8,
+                          pad=(2, 2, 2), alpha="aneg", beta="b0", seed=seed)); seed += 1
+    # special values routed to the checked path: inf / nan / huge / tiny
+    for special in ("nan_c_beta0", "inf_a", "huge", "tiny", "mixed_scale"):
+        for ta in ("N", "T"):
+            cases.append(dict(routine="Rgemm", transa=ta, transb="N", m=9, n=7, k=10,
+                              pad=(1, 1, 1), alpha="a15lo",
+                              beta="b0" if special == "nan_c_beta0" else "b05lo",
+                              seed=seed, special=special))
+            seed += 1
+    return cases
+
+
+def syrk_cases():
+    cases = []
+    seed = 500
+    for uplo in ("U", "L", "u", "l"):
+        for trans in ("N", "T", "C", "n"):
+            for bname in ("b05lo", "b1", "b0"):
+                if (uplo in "ul" or trans == "n") and bname != "b05lo":
+                    continue
+                cases.append(dict(routine="Rsyrk", uplo=uplo, trans=trans, n=13, k=9,
+                                  pad=(2, 0, 3), alpha="a15lo", beta=bname, seed=seed))
+                seed += 1
+    for uplo in ("U", "L"):
+        for trans in ("N", "T"):
+            cases.append(dict(routine="Rsyrk", uplo=uplo, trans=trans, n=137, k=33,
+                              pad=(1, 0, 2), alpha="a15", beta="b05lo", seed=seed)); seed += 1
+            cases.append(dict(routine="Rsyrk", uplo=uplo, trans=trans, n=6, k=4,
+                              pad=(0, 0, 0), alpha="a0", beta="bneg", seed=seed)); seed += 1
+            cases.append(dict(routine="Rsyrk", uplo=uplo, trans=trans, n=6, k=0,
+                              pad=(0, 0, 0), alpha="a15", beta="bneg", seed=seed)); seed += 1
+    for special in ("inf_a", "huge", "tiny"):
+        for trans in ("N", "T"):
+            cases.append(dict(routine="Rsyrk", uplo="U", trans=trans, n=8, k=7,
+                              pad=(1, 0, 1), alpha="a15lo", beta="b05lo", seed=seed,
+                              special=special))
+            seed += 1
+    return cases
+
+
+def run_case(mb, DDouble, case, store):
+    alpha = ALPHAS[case["alpha"]]
+    beta = BETAS[case["beta"]]
+    case["alpha_v"] = list(alpha)
+    case["beta_v"] = list(beta)
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    if case["routine"] == "Rgemm":
+        ta, tb = case["transa"].upper(), case["transb"].upper()
+        m, n, k = case["m"], case["n"], case["k"]
+        nra, nca = (m, k) if ta == "N" else (k, m)
+        nrb, ncb = (k, n) if tb == "N" else (n, k)
+        a = _matrix(mb, nra, nca, lds["lda"], (arrays["A_hi"], arrays["A_lo"]))
+        b = _matrix(mb, nrb, ncb, lds["ldb"], (arrays["B_hi"], arrays["B_lo"]))
+        c = _matrix(mb, m, n, lds["ldc"], (arrays["C_hi"], arrays["C_lo"]))
+        with np.errstate(all="ignore"):
+            mb.Rgemm(case["transa"], case["transb"], m, n, k, DDouble(*alpha), a, lds["lda"],
+                     b, lds["ldb"], DDouble._raw(*beta), c, lds["ldc"])
+    else:
+        n, k = case["n"], case["k"]
+        nra, nca = (n, k) if case["trans"].upper() == "N" else (k, n)
+        a = _matrix(mb, nra, nca, lds["lda"], (arrays["A_hi"], arrays["A_lo"]))
+        c = _matrix(mb, n, n, lds["ldc"], (arrays["C_hi"], arrays["C_lo"]))
+        with np.errstate(all="ignore"):
+            mb.Rsyrk(case["uplo"], case["trans"], n, k, DDouble(*alpha), a, lds["lda"],
+                     DDouble._raw(*beta), c, lds["ldc"])
+    arrays["out_hi"], arrays["out_lo"] = c.store
+    cid = len(store["cases"])
+    case["id"] = cid
+    # inputs are regenerated at test time by the same seeded recipe
+    # (case_inputs below); only their digest is stored, outputs in full.
+    case["input_sha256"] = input_digest(arrays)
+    for name in ("out_hi", "out_lo"):
+        store["arrays"][f"c{cid}_{name}"] = np.asarray(arrays[name], dtype=np.float64)
+    store["cases"].append(case)
+
+
+def eft_vectors(elem):
+    """Scalar EFT golden vectors through the reference's vectorised kernels."""
+    g = np.random.default_rng(np.random.SeedSequence([9, 9, 9]))
+    n = 4000
+    xh = g.uniform(-1, 1, n) * 2.0 ** g.integers(-60, 60, n)
+    yh = g.uniform(-1, 1, n) * 2.0 ** g.integers(-60, 60, n)
+    xl = xh * g.uniform(-1, 1, n) * 2.0 ** -53
+    yl = yh * g.uniform(-1, 1, n) * 2.0 ** -53
+    # edge lanes: zeros of both signs, exact cancellation, huge, tiny, inf, nan
+    edge = [(0.0, 0.0, -0.0, 0.0), (-0.0, 0.0, -0.0, -0.0), (1.0, 0.0, -1.0, 0.0),
+            (2.0 ** 1000, 0.0, 3.0, 0.0), (2.0 ** -1000, 0.0, 2.0 ** -60, 0.0),
+            (math.inf, 0.0, 1.0, 0.0), (math.nan, 0.0, 1.0, 0.0),
+            (1.7e308, 0.0, 1.7e308, 0.0), (1.0, 2.0 ** -53, 1.0, -2.0 ** -54)]
+    for i, e in enumerate(edge):
+        xh[i], xl[i], yh[i], yl[i] = e
+    with np.errstate(all="ignore"):
+        ah, al = elem._v_add2(xh, xl, yh, yl)
+        mh, ml = elem._v_mul2(xh, xl, yh, yl)
+        p, e = elem._v_two_prod(xh, yh)
+    return dict(xh=xh, xl=xl, yh=yh, yl=yl, add_h=ah, add_l=al, mul_h=mh, mul_l=ml,
+                tp_p=p, tp_e=e)
+
+
+def main():
+    mb, elem, DDouble = _ref()
+    os.makedirs(OUT, exist_ok=True)
+    store = {"cases": [], "arrays": {}}
+    for case in gemm_cases() + syrk_cases():
+        run_case(mb, DDouble, case, store)
+    np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
+    with open(os.path.join(OUT, "cases.json"), "w") as f:
+        json.dump(store["cases"], f, indent=0)
+    np.savez_compressed(os.path.join(OUT, "eft.npz"), **eft_vectors(elem))
+    # known-answer instance of cli.py:160-186 / test_acceptance.py:121-139
+    print(f"wrote {len(store['cases'])} cases to {OUT}")
+
+
+if __name__ == "__main__":
+    main()

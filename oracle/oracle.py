@@ -1,0 +1,119 @@
+"""ctypes front end of the C oracle (``dd_oracle.c``) -- TEST INFRASTRUCTURE ONLY.
+
+See ``oracle/__init__.py`` for who may import this.  Operands are numpy
+float64 planes in the reference's column-major flat layout: element (i, j)
+of a matrix with leading dimension ``ld`` lives at ``i + j*ld``
+(``/root/reference/pkg/src/mpkit/mpblas/matrix.py:1-7``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libdd_oracle.so")
+_lib = None
+
+_dp = ctypes.POINTER(ctypes.c_double)
+_i64 = ctypes.c_int64
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with its Makefile (gcc, -ffp-contract=off)."""
+    src = os.path.join(_HERE, "dd_oracle.c")
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        L.oracle_rgemm.restype = ctypes.c_int
+        L.oracle_rgemm.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64, _i64,
+                                   ctypes.c_double, ctypes.c_double,
+                                   _dp, _dp, _i64, _dp, _dp, _i64,
+                                   ctypes.c_double, ctypes.c_double,
+                                   _dp, _dp, _i64, ctypes.c_int]
+        L.oracle_rsyrk.restype = ctypes.c_int
+        L.oracle_rsyrk.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64,
+                                   ctypes.c_double, ctypes.c_double,
+                                   _dp, _dp, _i64,
+                                   ctypes.c_double, ctypes.c_double,
+                                   _dp, _dp, _i64, ctypes.c_int]
+        for name in ("oracle_add2", "oracle_mul2"):
+            f = getattr(L, name)
+            f.restype = None
+            f.argtypes = [ctypes.c_double] * 4 + [_dp]
+        L.oracle_two_prod.restype = None
+        L.oracle_two_prod.argtypes = [ctypes.c_double, ctypes.c_double, _dp]
+        L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_gemm_validate.restype = ctypes.c_int
+        L.oracle_gemm_validate.argtypes = [ctypes.c_char, ctypes.c_char] + [_i64] * 6
+        L.oracle_syrk_validate.restype = ctypes.c_int
+        L.oracle_syrk_validate.argtypes = [ctypes.c_char, ctypes.c_char] + [_i64] * 4
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_dp)
+
+
+def _flag(c):
+    return c.encode() if isinstance(c, str) else bytes([c])
+
+
+def rgemm(transa, transb, m, n, k, alpha, a_hi, a_lo, lda, b_hi, b_lo, ldb,
+          beta, c_hi, c_lo, ldc, threads=0):
+    """In-place C <- alpha*op(A)*op(B) + beta*C with the reference's rounding.
+
+    ``alpha``/``beta`` are (hi, lo) pairs.  Returns 0 or the reference
+    argument index of the first invalid argument."""
+    return lib().oracle_rgemm(_flag(transa), _flag(transb), m, n, k,
+                              float(alpha[0]), float(alpha[1]),
+                              _ptr(a_hi), _ptr(a_lo), lda, _ptr(b_hi), _ptr(b_lo), ldb,
+                              float(beta[0]), float(beta[1]),
+                              _ptr(c_hi), _ptr(c_lo), ldc, int(threads))
+
+
+def rsyrk(uplo, trans, n, k, alpha, a_hi, a_lo, lda, beta, c_hi, c_lo, ldc,
+          threads=0):
+    return lib().oracle_rsyrk(_flag(uplo), _flag(trans), n, k,
+                              float(alpha[0]), float(alpha[1]),
+                              _ptr(a_hi), _ptr(a_lo), lda,
+                              float(beta[0]), float(beta[1]),
+                              _ptr(c_hi), _ptr(c_lo), ldc, int(threads))
+
+
+def add2(x, y):
+    out = np.zeros(2)
+    lib().oracle_add2(x[0], x[1], y[0], y[1], _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def mul2(x, y):
+    out = np.zeros(2)
+    lib().oracle_mul2(x[0], x[1], y[0], y[1], _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def two_prod(a, b):
+    out = np.zeros(2)
+    lib().oracle_two_prod(a, b, _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def max_threads():
+    return lib().oracle_max_threads()

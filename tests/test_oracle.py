@@ -1,0 +1,75 @@
+"""The C oracle is pinned against the reference's own outputs (tests/golden)."""
+
+import numpy as np
+import pytest
+
+from oracle import golden, oracle
+
+
+def bits_equal(a, b):
+    """Bitwise equality, NaN payload-insensitive, -0.0 != +0.0."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    both_nan = np.isnan(a) & np.isnan(b)
+    same = a.view(np.uint64) == b.view(np.uint64)
+    return bool(np.all(same | both_nan))
+
+
+CASES = list(golden.load_cases())
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)))
+def test_oracle_matches_reference_bitwise(idx):
+    case, arr, out_hi, out_lo = CASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"], "input regeneration drifted"
+    ch, cl = arr["C_hi"].copy(), arr["C_lo"].copy()
+    with np.errstate(all="ignore"):
+        if case["routine"] == "Rgemm":
+            rc = oracle.rgemm(case["transa"], case["transb"], case["m"], case["n"], case["k"],
+                              case["alpha_v"], arr["A_hi"], arr["A_lo"], case["lda"],
+                              arr["B_hi"], arr["B_lo"], case["ldb"], case["beta_v"],
+                              ch, cl, case["ldc"], threads=2)
+        else:
+            rc = oracle.rsyrk(case["uplo"], case["trans"], case["n"], case["k"],
+                              case["alpha_v"], arr["A_hi"], arr["A_lo"], case["lda"],
+                              case["beta_v"], ch, cl, case["ldc"], threads=2)
+    assert rc == 0
+    assert bits_equal(ch, out_hi), case
+    assert bits_equal(cl, out_lo), case
+
+
+def test_oracle_scalar_efts_match_reference():
+    v = golden.load_eft()
+    for i in range(len(v["xh"])):
+        x = (v["xh"][i], v["xl"][i])
+        y = (v["yh"][i], v["yl"][i])
+        assert bits_equal(oracle.add2(x, y), (v["add_h"][i], v["add_l"][i])), i
+        assert bits_equal(oracle.mul2(x, y), (v["mul_h"][i], v["mul_l"][i])), i
+        assert bits_equal(oracle.two_prod(x[0], y[0]), (v["tp_p"][i], v["tp_e"][i])), i
+
+
+def test_oracle_known_answer_integer_instance():
+    """cli.py:160-186 / test_acceptance.py:121-139: exact at dd, lo == 0."""
+    A = np.array([[1, 8, 3], [0, 10, 8], [9, -5, -1]], float)
+    B = np.array([[9, 8, 3], [3, -11, 0], [-8, 6, 1]], float)
+    C = np.array([[3, 3, 0], [8, 4, 8], [6, 1, -2]], float)
+    col = lambda M: np.ascontiguousarray(M.T.reshape(-1))
+    ch, cl = col(C), np.zeros(9)
+    rc = oracle.rgemm("N", "N", 3, 3, 3, (3.0, 0.0), col(A), np.zeros(9), 3,
+                      col(B), np.zeros(9), 3, (-2.0, 0.0), ch, cl, 3)
+    assert rc == 0
+    expect = np.array([[21, -192, 18], [-118, -194, 8], [210, 361, 82]], float)
+    assert np.array_equal(ch.reshape(3, 3).T, expect)
+    assert np.all(cl == 0.0)
+
+
+@pytest.mark.parametrize("args,idx", [
+    (("X", "N", 1, 1, 1, 1, 1, 1), 1), (("N", "Q", 1, 1, 1, 1, 1, 1), 2),
+    (("N", "N", -1, 1, 1, 1, 1, 1), 3), (("N", "N", 1, -1, 1, 1, 1, 1), 4),
+    (("N", "N", 1, 1, -1, 1, 1, 1), 5), (("N", "N", 4, 1, 1, 3, 4, 4), 8),
+    (("N", "N", 1, 1, 4, 1, 3, 1), 10), (("N", "N", 4, 1, 1, 4, 1, 3), 13),
+    (("T", "N", 4, 1, 2, 1, 2, 4), 8),
+])
+def test_oracle_validation_indices(args, idx):
+    ta, tb, m, n, k, lda, ldb, ldc = args
+    assert oracle.lib().oracle_gemm_validate(ta.encode(), tb.encode(), m, n, k, lda, ldb, ldc) == idx
