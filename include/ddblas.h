@@ -1,0 +1,100 @@
+/*
+ * ddblas.h -- C ABI of the B200-native double-double Rgemm / Rsyrk.
+ *
+ * Drop-in for the reference's dd path (arXiv 2109.13406, MPLAPACK; Python
+ * reference package "mpkit"):
+ *
+ *   ddb_rgemm  replaces  mpkit.mpblas.Rgemm(transa, transb, m, n, k, alpha,
+ *                        a, lda, b, ldb, beta, c, ldc)
+ *                        /root/reference/pkg/src/mpkit/mpblas/level23.py:180-198
+ *   ddb_rsyrk  replaces  mpkit.mpblas.Rsyrk(uplo, trans, n, k, alpha, a, lda,
+ *                        beta, c, ldc)            level23.py:226-285
+ *
+ * A dd matrix is two float64 planes (hi, lo) in the reference's column-major
+ * flat layout: element (i, j) at index i + j*ld (mpblas/matrix.py:1-7,
+ * elem.py DDBackend store = (hi, lo)).  alpha / beta are (hi, lo) pairs
+ * (ddarith.DDouble).  Flags are single characters, case-insensitive,
+ * 'C' == 'T' for real data (level23.py:23-26, :116-117).
+ *
+ * Return value: DDB_OK (0); a positive reference argument index (the
+ * BlasError.index the reference would raise, level23.py:84-96 / :233-239);
+ * or a negative DDB_E* code with text in ddb_last_error().
+ *
+ * Device entry points (ddb_rgemm / ddb_rsyrk) take DEVICE pointers and run
+ * asynchronously on `stream` (a cudaStream_t, NULL = legacy default stream).
+ * Host entry points (*_host) take HOST pointers, stage through device
+ * memory, and return after C has been copied back (synchronous).
+ * Thread safety: reentrant; concurrent calls on distinct streams are safe.
+ */
+#ifndef DDBLAS_H
+#define DDBLAS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DDB_VERSION 100
+
+#define DDB_OK 0
+#define DDB_EINVAL (-1)   /* bad mode / internal argument */
+#define DDB_ECUDA (-2)    /* CUDA runtime failure */
+#define DDB_ENOMEM (-3)   /* device allocation failed */
+
+/* mode: DDB_MODE_EXACT     bit-identical to the reference (29 FP64 instr / MAC)
+ *       DDB_MODE_FAST      anchored accumulation, error <= c*k*2^-104*sum|a*b|
+ *                          (6 FP64 instr / MAC)
+ *       DDB_MODE_REFERENCE one thread per element, checked arithmetic (debug) */
+#define DDB_MODE_EXACT 0
+#define DDB_MODE_FAST 1
+#define DDB_MODE_REFERENCE 2
+
+int ddb_rgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+              double alpha_hi, double alpha_lo,
+              const double* a_hi, const double* a_lo, int64_t lda,
+              const double* b_hi, const double* b_lo, int64_t ldb,
+              double beta_hi, double beta_lo,
+              double* c_hi, double* c_lo, int64_t ldc,
+              int mode, void* stream);
+
+int ddb_rsyrk(char uplo, char trans, int64_t n, int64_t k,
+              double alpha_hi, double alpha_lo,
+              const double* a_hi, const double* a_lo, int64_t lda,
+              double beta_hi, double beta_lo,
+              double* c_hi, double* c_lo, int64_t ldc,
+              int mode, void* stream);
+
+int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                   double alpha_hi, double alpha_lo,
+                   const double* a_hi, const double* a_lo, int64_t lda,
+                   const double* b_hi, const double* b_lo, int64_t ldb,
+                   double beta_hi, double beta_lo,
+                   double* c_hi, double* c_lo, int64_t ldc,
+                   int mode, void* stream);
+
+int ddb_rsyrk_host(char uplo, char trans, int64_t n, int64_t k,
+                   double alpha_hi, double alpha_lo,
+                   const double* a_hi, const double* a_lo, int64_t lda,
+                   double beta_hi, double beta_lo,
+                   double* c_hi, double* c_lo, int64_t ldc,
+                   int mode, void* stream);
+
+/* Argument checks alone (no device work): reference index or 0. */
+int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                       int64_t lda, int64_t ldb, int64_t ldc);
+int ddb_rsyrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc);
+
+const char* ddb_last_error(void);
+int ddb_version(void);
+/* Number of kernels this library has launched in this process. */
+long long ddb_launch_count(void);
+/* Route of this thread's last call when DDB_DEBUG_SYNC=1 (0 exact tiled,
+ * 1 fast tiled, 2 reference-semantics kernel), else -1. */
+int ddb_last_route(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DDBLAS_H */

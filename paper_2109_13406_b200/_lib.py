@@ -1,0 +1,75 @@
+"""ctypes binding of the in-tree CUDA library ``libddblas.so`` (include/ddblas.h).
+
+There is no CPU fallback: if the library is missing or cannot load, every
+call raises.  Build it with ``python -c "import __graft_entry__ as g; g.build()"``
+or ``make -C paper_2109_13406_b200/csrc``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libddblas.so")
+
+MODES = {"exact": 0, "fast": 1, "reference": 2}
+
+_dp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_d = ctypes.c_double
+_c = ctypes.c_char
+
+EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
+           "ddb_rgemm_validate", "ddb_rsyrk_validate", "ddb_last_error",
+           "ddb_version", "ddb_launch_count", "ddb_last_route")
+
+_lib = None
+
+
+class LibraryMissing(RuntimeError):
+    pass
+
+
+def load():
+    """Load libddblas.so (once).  Raises LibraryMissing if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise LibraryMissing(
+            f"{LIB_PATH} is not built: the dd kernels exist only as CUDA code "
+            "(run __graft_entry__.build()); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    gemm_args = [_c, _c, _i64, _i64, _i64, _d, _d, _dp, _dp, _i64, _dp, _dp, _i64,
+                 _d, _d, _dp, _dp, _i64, ctypes.c_int, _dp]
+    syrk_args = [_c, _c, _i64, _i64, _d, _d, _dp, _dp, _i64, _d, _d, _dp, _dp, _i64,
+                 ctypes.c_int, _dp]
+    for name, args in (("ddb_rgemm", gemm_args), ("ddb_rgemm_host", gemm_args),
+                       ("ddb_rsyrk", syrk_args), ("ddb_rsyrk_host", syrk_args)):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = args
+    L.ddb_rgemm_validate.restype = ctypes.c_int
+    L.ddb_rgemm_validate.argtypes = [_c, _c] + [_i64] * 6
+    L.ddb_rsyrk_validate.restype = ctypes.c_int
+    L.ddb_rsyrk_validate.argtypes = [_c, _c] + [_i64] * 4
+    L.ddb_last_error.restype = ctypes.c_char_p
+    L.ddb_last_error.argtypes = []
+    L.ddb_version.restype = ctypes.c_int
+    L.ddb_launch_count.restype = ctypes.c_longlong
+    L.ddb_last_route.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def last_error():
+    return load().ddb_last_error().decode(errors="replace")
+
+
+def launch_count():
+    return int(load().ddb_launch_count())
+
+
+def last_route():
+    return int(load().ddb_last_route())

@@ -1,0 +1,281 @@
+// capi.cu -- the drop-in C ABI (include/ddblas.h).
+//
+// Each entry point restates the reference routine's argument checking and
+// early exits before touching the device:
+//   ddb_rgemm  <- mpkit.mpblas.Rgemm  (level23.py:180-198; checks :84-96)
+//   ddb_rsyrk  <- mpkit.mpblas.Rsyrk  (level23.py:226-285; checks :233-239)
+// Return 0 on success, the reference argument index (1..13) of the first
+// invalid argument, or a negative DDB_E* code on a CUDA failure
+// (ddb_last_error() has the text).  Calls are asynchronous on `stream`.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "../../include/ddblas.h"
+#include "internal.h"
+
+using namespace ddb;
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_last_route = -1;
+std::atomic<long long> g_launches{0};
+
+int fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? DDB_ENOMEM : DDB_ECUDA;
+}
+
+int upflag(char c) { return (c >= 'a' && c <= 'z') ? c - 32 : c; }
+bool is_zero(double h, double l) { return h == 0.0 && l == 0.0; }
+bool is_one(double h, double l) { return h == 1.0 && l == 0.0; }
+
+int bexp(double x) {
+  long long b;
+  std::memcpy(&b, &x, sizeof b);
+  return (int)((b >> 52) & 0x7ff);
+}
+// scalar safe-window test (same window as dd_prescan.cu)
+bool in_window(double h, double l) {
+  const int eh = bexp(h), el = bexp(l);
+  return !((h != 0.0 && eh < WIN_LO) || eh > WIN_HI || el > WIN_HI);
+}
+
+bool debug_sync() {
+  static const bool on = [] {
+    const char* v = std::getenv("DDB_DEBUG_SYNC");
+    return v != nullptr && v[0] != '\0' && v[0] != '0';
+  }();
+  return on;
+}
+
+// Runs one validated, non-trivial call: prescan -> tiled (gated on the
+// flag) -> reference-semantics kernel (gated on the opposite).
+int run(const GemmArgs& g, int mode, cudaStream_t s) {
+  int nl = 0;
+  cudaError_t e;
+  const bool trivial_ref = mode == MODE_REFERENCE || is_zero(g.alpha.h, g.alpha.l) || g.k == 0;
+  bool scalars_ok = true;
+  if (mode == MODE_EXACT)
+    scalars_ok = in_window(g.alpha.h, g.alpha.l) && in_window(g.beta.h, g.beta.l);
+  if (trivial_ref || !scalars_ok) {
+    e = launch_reference(g, nullptr, GATE_ALWAYS, s, &nl);
+    g_launches += nl;
+    if (e != cudaSuccess) return fail(e, "reference kernel launch");
+    g_last_route = 2;
+    return DDB_OK;
+  }
+  const int64_t nrow = g.m, ncol = g.n;
+  const size_t ws_bytes = sizeof(int) * (size_t)(1 + nrow + ncol) + 64;
+  void* ws = nullptr;
+  e = cudaMallocAsync(&ws, ws_bytes, s);
+  if (e != cudaSuccess) return fail(e, "workspace allocation");
+  int* flag = static_cast<int*>(ws);
+  int* row_exp = flag + 16;
+  int* col_exp = g.syrk ? row_exp : row_exp + nrow;
+  e = cudaMemsetAsync(ws, 0, ws_bytes, s);
+  if (e == cudaSuccess) e = launch_prescan(g, mode, row_exp, col_exp, flag, s, &nl);
+  if (e == cudaSuccess) e = launch_tiled(g, mode, row_exp, col_exp, flag, s, &nl);
+  if (e == cudaSuccess) e = launch_reference(g, flag, GATE_IF_UNSAFE, s, &nl);
+  g_launches += nl;
+  int route = -1;
+  if (e == cudaSuccess && debug_sync()) {
+    int f = 0;
+    e = cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    route = f == ROUTE_SAFE ? (mode == MODE_FAST ? 1 : 0) : 2;
+  }
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return fail(e, "dd kernel launch");
+  if (e2 != cudaSuccess) return fail(e2, "workspace free");
+  g_last_route = route;
+  return DDB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ddb_version(void) { return DDB_VERSION; }
+
+const char* ddb_last_error(void) { return g_last_error.c_str(); }
+
+long long ddb_launch_count(void) { return g_launches.load(); }
+
+int ddb_last_route(void) { return g_last_route; }
+
+int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                       int64_t lda, int64_t ldb, int64_t ldc) {
+  const int ta = upflag(transa), tb = upflag(transb);
+  if (ta != 'N' && ta != 'T' && ta != 'C') return 1;
+  if (tb != 'N' && tb != 'T' && tb != 'C') return 2;
+  if (m < 0) return 3;
+  if (n < 0) return 4;
+  if (k < 0) return 5;
+  const int64_t nrowa = ta == 'N' ? m : k, nrowb = tb == 'N' ? k : n;
+  if (lda < (nrowa > 1 ? nrowa : 1)) return 8;
+  if (ldb < (nrowb > 1 ? nrowb : 1)) return 10;
+  if (ldc < (m > 1 ? m : 1)) return 13;
+  return 0;
+}
+
+int ddb_rsyrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc) {
+  const int u = upflag(uplo), t = upflag(trans);
+  if (u != 'U' && u != 'L') return 1;
+  if (t != 'N' && t != 'T' && t != 'C') return 2;
+  if (n < 0) return 3;
+  if (k < 0) return 4;
+  const int64_t nrowa = t == 'N' ? n : k;
+  if (lda < (nrowa > 1 ? nrowa : 1)) return 7;
+  if (ldc < (n > 1 ? n : 1)) return 10;
+  return 0;
+}
+
+int ddb_rgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
+              double alpha_hi, double alpha_lo,
+              const double* a_hi, const double* a_lo, int64_t lda,
+              const double* b_hi, const double* b_lo, int64_t ldb,
+              double beta_hi, double beta_lo,
+              double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
+  const int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_REFERENCE) {
+    g_last_error = "unknown mode";
+    return DDB_EINVAL;
+  }
+  // level23.py:191-192
+  if (m == 0 || n == 0 || ((is_zero(alpha_hi, alpha_lo) || k == 0) && is_one(beta_hi, beta_lo)))
+    return DDB_OK;
+  GemmArgs g{};
+  g.ta = upflag(transa) == 'N' ? 0 : 1;
+  g.tb = upflag(transb) == 'N' ? 0 : 1;
+  g.syrk = 0;
+  g.m = m; g.n = n; g.k = k;
+  g.a_hi = a_hi; g.a_lo = a_lo; g.lda = lda;
+  g.b_hi = b_hi; g.b_lo = b_lo; g.ldb = ldb;
+  g.c_hi = c_hi; g.c_lo = c_lo; g.ldc = ldc;
+  g.alpha = dd{alpha_hi, alpha_lo};
+  g.beta = dd{beta_hi, beta_lo};
+  return run(g, mode, static_cast<cudaStream_t>(stream));
+}
+
+int ddb_rsyrk(char uplo, char trans, int64_t n, int64_t k,
+              double alpha_hi, double alpha_lo,
+              const double* a_hi, const double* a_lo, int64_t lda,
+              double beta_hi, double beta_lo,
+              double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
+  const int rc = ddb_rsyrk_validate(uplo, trans, n, k, lda, ldc);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_REFERENCE) {
+    g_last_error = "unknown mode";
+    return DDB_EINVAL;
+  }
+  // level23.py:242-243
+  if (n == 0 || ((is_zero(alpha_hi, alpha_lo) || k == 0) && is_one(beta_hi, beta_lo)))
+    return DDB_OK;
+  GemmArgs g{};
+  const bool tn = upflag(trans) == 'N';
+  g.ta = tn ? 0 : 1;            // trans 'N': C = A A^T  == NT Rgemm with B = A
+  g.tb = tn ? 1 : 0;            // trans 'T': C = A^T A  == TN Rgemm with B = A
+  g.syrk = upflag(uplo) == 'U' ? 1 : 2;
+  g.m = n; g.n = n; g.k = k;
+  g.a_hi = a_hi; g.a_lo = a_lo; g.lda = lda;
+  g.b_hi = a_hi; g.b_lo = a_lo; g.ldb = lda;
+  g.c_hi = c_hi; g.c_lo = c_lo; g.ldc = ldc;
+  g.alpha = dd{alpha_hi, alpha_lo};
+  g.beta = dd{beta_hi, beta_lo};
+  return run(g, mode, static_cast<cudaStream_t>(stream));
+}
+
+// ---- host-buffer entry points: stage operands through device memory ----
+
+namespace {
+
+int64_t span(int64_t nrow, int64_t ncol, int64_t ld) {
+  return (nrow <= 0 || ncol <= 0) ? 0 : (ncol - 1) * ld + nrow;
+}
+
+struct DevBuf {
+  double* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~DevBuf() { if (p) cudaFreeAsync(p, s); }
+};
+
+int stage_in(DevBuf& b, const double* hi, const double* lo, int64_t n, cudaStream_t s) {
+  b.s = s;
+  if (n == 0) return DDB_OK;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b.p), sizeof(double) * 2 * n, s);
+  if (e != cudaSuccess) return fail(e, "host staging allocation");
+  e = cudaMemcpyAsync(b.p, hi, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(b.p + n, lo, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail(e, "host to device copy");
+  return DDB_OK;
+}
+
+}  // namespace
+
+int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                   double alpha_hi, double alpha_lo,
+                   const double* a_hi, const double* a_lo, int64_t lda,
+                   const double* b_hi, const double* b_lo, int64_t ldb,
+                   double beta_hi, double beta_lo,
+                   double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
+  int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  if (m == 0 || n == 0 || ((is_zero(alpha_hi, alpha_lo) || k == 0) && is_one(beta_hi, beta_lo)))
+    return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool na = upflag(transa) == 'N', nb = upflag(transb) == 'N';
+  const int64_t sa = span(na ? m : k, na ? k : m, lda);
+  const int64_t sb = span(nb ? k : n, nb ? n : k, ldb);
+  const int64_t sc = span(m, n, ldc);
+  DevBuf A, B, C;
+  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
+  if ((rc = stage_in(B, b_hi, b_lo, sb, s))) return rc;
+  if ((rc = stage_in(C, c_hi, c_lo, sc, s))) return rc;
+  rc = ddb_rgemm(transa, transb, m, n, k, alpha_hi, alpha_lo, A.p, A.p ? A.p + sa : nullptr, lda,
+                 B.p, B.p ? B.p + sb : nullptr, ldb, beta_hi, beta_lo, C.p, C.p + sc, ldc, mode,
+                 stream);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(c_hi, C.p, sizeof(double) * sc, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c_lo, C.p + sc, sizeof(double) * sc, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
+int ddb_rsyrk_host(char uplo, char trans, int64_t n, int64_t k,
+                   double alpha_hi, double alpha_lo,
+                   const double* a_hi, const double* a_lo, int64_t lda,
+                   double beta_hi, double beta_lo,
+                   double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
+  int rc = ddb_rsyrk_validate(uplo, trans, n, k, lda, ldc);
+  if (rc) return rc;
+  if (n == 0 || ((is_zero(alpha_hi, alpha_lo) || k == 0) && is_one(beta_hi, beta_lo)))
+    return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool tn = upflag(trans) == 'N';
+  // A is only read when alpha != 0 (level23.py:247-249 never views it)
+  const int64_t sa = is_zero(alpha_hi, alpha_lo) ? 0 : span(tn ? n : k, tn ? k : n, lda);
+  const int64_t sc = span(n, n, ldc);
+  DevBuf A, C;
+  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
+  if ((rc = stage_in(C, c_hi, c_lo, sc, s))) return rc;
+  rc = ddb_rsyrk(uplo, trans, n, k, alpha_hi, alpha_lo, A.p, A.p ? A.p + sa : nullptr, lda,
+                 beta_hi, beta_lo, C.p, C.p + sc, ldc, mode, stream);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(c_hi, C.p, sizeof(double) * sc, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c_lo, C.p + sc, sizeof(double) * sc, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// dd_reference.cu -- reference-semantics kernel: one thread per C element,
+// operands read straight from HBM, every dd operation in its checked form
+// (Dekker TwoProd + the reference's finiteness fix-ups).
+//
+// It is the complete per-element restatement of the reference:
+//   alpha == 0        level23.py:110-115  (_gemm_core) / :247-249 (Rsyrk)
+//   transa = 'N'      level23.py:120-125, :134-140  (beta rule, then
+//                     c = add2(c, mul2(A(i,l), mul2(alpha, op(B)(l,j)))))
+//   transa = 'T'/'C'  level23.py:126-133, :141-149  (acc from 0, _combine)
+//   Rsyrk             level23.py:226-285 == NT / TN Rgemm with B = A, only
+//                     the uplo triangle written
+// and runs whenever the prescan found a value outside the safe window
+// (inf, nan, |x| >= 2**301, 0 < |hi| < 2**-300), for alpha == 0, for k == 0,
+// and for mode DDB_MODE_REFERENCE.  It is not the fast path: throughput is a
+// few percent of the tiled kernels (dd_gemm.cu).
+#include "internal.h"
+
+namespace ddb {
+
+__global__ void __launch_bounds__(256)
+reference_kernel(GemmArgs g, const int* __restrict__ flag, int gate) {
+  if (gate != GATE_ALWAYS) {
+    const int f = *flag;
+    if (gate == GATE_IF_UNSAFE && f == ROUTE_SAFE) return;
+    if (gate == GATE_IF_SAFE && f != ROUTE_SAFE) return;
+  }
+  const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (i >= g.m) return;
+  const bool alpha_zero = dd_is_zero(g.alpha);
+  for (int64_t j = (int64_t)blockIdx.y * 8 + threadIdx.y; j < g.n; j += (int64_t)gridDim.y * 8) {
+    if (g.syrk == 1 && i > j) continue;
+    if (g.syrk == 2 && i < j) continue;
+    const int64_t ci = i + j * g.ldc;
+    const dd c0{g.c_hi[ci], g.c_lo[ci]};
+    dd out;
+    if (alpha_zero) {
+      if (dd_is_one(g.beta)) continue;
+      out = scale_beta(g.beta, c0);
+    } else if (g.ta == 0) {
+      dd c = scale_beta(g.beta, c0);
+      for (int64_t l = 0; l < g.k; ++l) {
+        const int64_t bi = g.tb == 0 ? l + j * g.ldb : j + l * g.ldb;
+        const dd t = mul2_chk(g.alpha, dd{g.b_hi[bi], g.b_lo[bi]});
+        const int64_t ai = i + l * g.lda;
+        c = add2_chk(c, mul2_chk(dd{g.a_hi[ai], g.a_lo[ai]}, t));
+      }
+      out = c;
+    } else {
+      dd acc{0.0, 0.0};
+      for (int64_t l = 0; l < g.k; ++l) {
+        const int64_t bi = g.tb == 0 ? l + j * g.ldb : j + l * g.ldb;
+        const int64_t ai = l + i * g.lda;
+        acc = add2_chk(acc, mul2_chk(dd{g.a_hi[ai], g.a_lo[ai]}, dd{g.b_hi[bi], g.b_lo[bi]}));
+      }
+      out = combine(g.alpha, acc, g.beta, c0);
+    }
+    g.c_hi[ci] = out.h;
+    g.c_lo[ci] = out.l;
+  }
+}
+
+cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaStream_t s,
+                             int* nlaunch) {
+  if (g.m <= 0 || g.n <= 0) return cudaSuccess;
+  const int64_t gx = (g.m + 31) / 32;
+  int64_t gy = (g.n + 7) / 8;
+  if (gy > 65535) gy = 65535;
+  dim3 grid((unsigned)gx, (unsigned)gy), block(32, 8);
+  reference_kernel<<<grid, block, 0, s>>>(g, flag, gate);
+  ++*nlaunch;
+  return cudaGetLastError();
+}
+
+}  // namespace ddb

@@ -1,0 +1,42 @@
+// internal.h -- declarations shared by the kernels and the C ABI (capi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "dd_arith.cuh"
+
+namespace ddb {
+
+enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2 };
+
+// Route flag written by the prescan: 0 = every operand inside the safe
+// window (tiled kernels run), nonzero = some value outside it (non-finite,
+// |x| > 2**301, or a nonzero hi word below 2**-300): the tiled kernels exit
+// and the reference-semantics kernel runs instead.
+enum RouteFlag { ROUTE_SAFE = 0, ROUTE_UNSAFE = 1 };
+
+// Safe window in biased-exponent terms (see dd_prescan.cu).
+constexpr int WIN_LO = 1023 - 300;   // hi words: zero or biased exp >= WIN_LO
+constexpr int WIN_HI = 1023 + 300;   // hi and lo words: biased exp <= WIN_HI
+
+struct GemmArgs {
+  int ta, tb;                 // 0 = 'N', 1 = 'T'/'C' (real: conj is identity)
+  int syrk;                   // 0 = Rgemm, 1 = Rsyrk upper, 2 = Rsyrk lower
+  int64_t m, n, k;
+  const double *a_hi, *a_lo; int64_t lda;
+  const double *b_hi, *b_lo; int64_t ldb;
+  double *c_hi, *c_lo; int64_t ldc;
+  dd alpha, beta;
+};
+
+// Which kernel should run, decided on the device by the prescan flag.
+enum Gate { GATE_ALWAYS = 0, GATE_IF_SAFE = 1, GATE_IF_UNSAFE = 2 };
+
+cudaError_t launch_prescan(const GemmArgs& g, int mode, int* row_exp, int* col_exp,
+                           int* flag, cudaStream_t s, int* nlaunch);
+cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaStream_t s,
+                             int* nlaunch);
+cudaError_t launch_tiled(const GemmArgs& g, int mode, const int* row_exp, const int* col_exp,
+                         const int* flag, cudaStream_t s, int* nlaunch);
+
+}  // namespace ddb

@@ -1,0 +1,224 @@
+"""Containers, scalar coercion and argument errors of the drop-in surface.
+
+Mirrors the parts of the reference the dd Rgemm / Rsyrk path touches:
+
+* ``BlasError``           mpkit/mpblas/matrix.py:18-26 (message and attributes)
+* ``same_precision``      mpkit/mpblas/matrix.py:235-239
+* ``to_dd``               the ``_scalar_for('dd', v)`` -> ``DDouble(v)`` coercion
+                          of alpha / beta (matrix.py:29-37, ddarith.py:192-214,
+                          decimal strings: ddarith.py:504-532)
+* ``HostMatrix``          the reference ``Matrix`` layout: column-major, element
+                          (i, j) at ``i + j*ld``, dd store = (hi, lo) float64
+                          planes (matrix.py:100-195, elem.py DDBackend)
+* ``DeviceMatrix``        the same layout with the planes resident in HBM as
+                          torch CUDA tensors (no host staging per call)
+
+Any object with ``m, n, ld, precision, store`` attributes is accepted by
+``Rgemm`` / ``Rsyrk`` -- in particular the reference's own ``mpkit`` Matrix.
+"""
+
+from __future__ import annotations
+
+import math
+import re
+from fractions import Fraction
+
+import numpy as np
+
+
+class BlasError(ValueError):
+    """Invalid argument, reported with the reference argument index."""
+
+    def __init__(self, routine, index):
+        self.routine = routine
+        self.index = index
+        super().__init__(
+            f"on entry to {routine} parameter number {index} "
+            "had an illegal value")
+
+
+def require(routine, cond, index):
+    if not cond:
+        raise BlasError(routine, index)
+
+
+def same_precision(routine, *objs):
+    tags = {o.precision for o in objs}
+    if len(tags) > 1:
+        raise ValueError(f"{routine}: mixed precisions {sorted(tags)}")
+    return tags.pop()
+
+
+# --------------------------------------------------------------------------
+# dd scalars (alpha, beta)
+
+_DECIMAL_RE = re.compile(
+    r"^\s*([+-]?)(?:(\d+)(?:\.(\d*))?|\.(\d+))(?:[eE]([+-]?\d+))?\s*$")
+
+
+def _two_sum(a, b):
+    s = a + b
+    bb = s - a
+    return s, (a - (s - bb)) + (b - bb)
+
+
+def _norm(hi, lo):
+    s, e = _two_sum(hi, lo)
+    return (s, e) if math.isfinite(s) else (s, 0.0)
+
+
+def _round_fraction(v):
+    try:
+        hi = float(v)
+    except OverflowError:
+        return (math.inf if v > 0 else -math.inf), 0.0
+    if math.isinf(hi):
+        return hi, 0.0
+    return _norm(hi, float(v - Fraction(hi)))
+
+
+def _parse_decimal(s):
+    m = _DECIMAL_RE.match(s)
+    if not m:
+        raise ValueError(f"not a decimal number: {s!r}")
+    sign, ip, fp1, fp2, ex = m.groups()
+    frac = (fp1 if fp1 is not None else fp2) or ""
+    v = Fraction(int((ip or "") + frac), 1) * Fraction(10) ** (int(ex or 0) - len(frac))
+    return _round_fraction(-v if sign == "-" else v)
+
+
+def to_dd(value):
+    """Coerce alpha / beta exactly as ``DDouble(value)`` does; returns (hi, lo)."""
+    if hasattr(value, "hi") and hasattr(value, "lo") and not isinstance(value, (int, float, str)):
+        return float(value.hi), float(value.lo)
+    if isinstance(value, str):
+        return _parse_decimal(value)
+    if isinstance(value, float):
+        return float(value), 0.0
+    if isinstance(value, int):
+        try:
+            hi = float(value)
+        except OverflowError:
+            return (math.inf if value > 0 else -math.inf), 0.0
+        if math.isfinite(hi):
+            return _norm(hi, float(value - int(hi)))
+        return hi, 0.0
+    raise TypeError(f"cannot make DDouble from {type(value).__name__}")
+
+
+def dd_truthy(v):
+    """``DDouble.__bool__`` (ddarith.py:290-291)."""
+    return v[0] != 0.0 or v[1] != 0.0
+
+
+def dd_is_one(v):
+    """``DDouble == 1`` via ``_cmp2`` (ddarith.py:166-176)."""
+    return v[0] == 1.0 and v[1] == 0.0
+
+
+# --------------------------------------------------------------------------
+# containers
+
+class HostMatrix:
+    """m x n dd matrix in host memory, column-major (hi, lo) numpy planes.
+
+    Same attributes as the reference ``mpkit.mpblas.Matrix`` for the dd
+    precision (``m, n, ld, precision, store``)."""
+
+    def __init__(self, m, n, precision="dd", ld=None, pinned=False):
+        if m < 0 or n < 0:
+            raise ValueError("matrix dimensions must be >= 0")
+        ld = max(1, m) if ld is None else ld
+        if ld < max(1, m):
+            raise ValueError("leading dimension too small")
+        if precision != "dd":
+            raise NotImplementedError(f"precision {precision!r}: only 'dd' is on the B200 path")
+        self.m, self.n, self.ld, self.precision = m, n, ld, precision
+        size = ld * n
+        if pinned:
+            import torch
+            self.store = tuple(torch.zeros(size, dtype=torch.float64, pin_memory=True).numpy()
+                               for _ in range(2))
+        else:
+            self.store = (np.zeros(size), np.zeros(size))
+
+    @classmethod
+    def from_planes(cls, m, n, hi, lo, ld=None):
+        a = cls(0, 0)
+        a.m, a.n = m, n
+        a.ld = max(1, m) if ld is None else ld
+        a.store = (np.ascontiguousarray(hi, dtype=np.float64),
+                   np.ascontiguousarray(lo, dtype=np.float64))
+        return a
+
+    def to_device(self, device=None):
+        return DeviceMatrix.from_host(self, device)
+
+    def __repr__(self):
+        return f"HostMatrix({self.m}x{self.n}, ld={self.ld}, precision='dd')"
+
+
+class DeviceMatrix:
+    """m x n dd matrix resident in HBM: ``store = (hi, lo)`` torch float64
+    CUDA tensors of length ``ld*n`` in the reference's column-major layout."""
+
+    def __init__(self, m, n, precision="dd", ld=None, device=None, store=None):
+        import torch
+        if m < 0 or n < 0:
+            raise ValueError("matrix dimensions must be >= 0")
+        ld = max(1, m) if ld is None else ld
+        if ld < max(1, m):
+            raise ValueError("leading dimension too small")
+        if precision != "dd":
+            raise NotImplementedError(f"precision {precision!r}: only 'dd' is on the B200 path")
+        self.m, self.n, self.ld, self.precision = m, n, ld, precision
+        if store is None:
+            dev = torch.device("cuda" if device is None else device)
+            store = (torch.zeros(ld * n, dtype=torch.float64, device=dev),
+                     torch.zeros(ld * n, dtype=torch.float64, device=dev))
+        self.store = store
+
+    @classmethod
+    def from_host(cls, mat, device=None):
+        import torch
+        dev = torch.device("cuda" if device is None else device)
+        hi, lo = (torch.as_tensor(np.ascontiguousarray(p, dtype=np.float64)).to(dev)
+                  for p in mat.store[:2])
+        return cls(mat.m, mat.n, "dd", mat.ld, store=(hi, lo))
+
+    @property
+    def device(self):
+        return self.store[0].device
+
+    def to_host(self):
+        return HostMatrix.from_planes(self.m, self.n, self.store[0].cpu().numpy(),
+                                      self.store[1].cpu().numpy(), self.ld)
+
+    def copy(self):
+        return DeviceMatrix(self.m, self.n, "dd", self.ld,
+                            store=(self.store[0].clone(), self.store[1].clone()))
+
+    def __repr__(self):
+        return f"DeviceMatrix({self.m}x{self.n}, ld={self.ld}, precision='dd', device={self.device})"
+
+
+def is_device(mat):
+    try:
+        import torch
+    except ImportError:
+        return False
+    return isinstance(mat.store[0], torch.Tensor) and mat.store[0].is_cuda
+
+
+def storage_len(mat):
+    s = mat.store[0]
+    return int(s.shape[0])
+
+
+def check_storage(mat, nrow, ncol, ld):
+    """``Matrix.view2d``'s length rule (matrix.py:140-155)."""
+    need = ld * ncol
+    if storage_len(mat) < need:
+        raise ValueError(
+            f"storage of length {storage_len(mat)} too short for "
+            f"{nrow}x{ncol} with ld={ld}")

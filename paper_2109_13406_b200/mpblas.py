@@ -1,0 +1,192 @@
+"""Drop-in ``Rgemm`` / ``Rsyrk`` over dd (hi, lo) planes, computed on the B200.
+
+Same call surface, defaults, validation order, error types / indices and
+early exits as the reference (``/root/reference/pkg/src/mpkit/mpblas/``):
+
+  Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
+        beta=1.0, c=None, ldc=None)                          level23.py:180-198
+  Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None)
+                                                             level23.py:226-270
+
+plus one keyword, ``mode``:
+
+  "fast"   (default; env ``DDBLAS_MODE`` overrides) anchored accumulation on
+           the FP64 pipe, componentwise error <= c*k*2**-104*(|alpha| sum|a*b|
+           + |beta||c|) -- the north-star tolerance
+  "exact"  bit-identical to the reference's result
+  "reference"  the one-thread-per-element checked kernel (debugging)
+
+C is updated in place; A and B are read only; nothing is returned.
+Operands are either all ``DeviceMatrix`` (planes resident in HBM; the call is
+asynchronous on torch's current stream) or all host matrices (numpy planes:
+``HostMatrix`` or the reference's own ``mpkit`` Matrix; the call stages
+through device memory and returns after C is back on the host).  Only the
+'dd' precision is on the B200 path; other precisions raise
+NotImplementedError -- there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+from . import _lib
+from .matrix import (BlasError, check_storage, dd_is_one, dd_truthy, is_device, require,
+                     same_precision, to_dd)
+
+__all__ = ["Rgemm", "Rsyrk", "BlasError", "default_mode"]
+
+
+def default_mode():
+    return os.environ.get("DDBLAS_MODE", "fast")
+
+
+def _flag(routine, value, allowed, index):
+    """level23.py:23-26."""
+    ok = isinstance(value, str) and len(value) == 1 and value.upper() in allowed
+    require(routine, ok, index)
+    return value.upper()
+
+
+def _ld_of(mat, ld):
+    return mat.ld if ld is None else ld
+
+
+def _mode_code(mode):
+    mode = default_mode() if mode is None else mode
+    try:
+        return _lib.MODES[mode]
+    except KeyError:
+        raise ValueError(f"unknown mode {mode!r}; expected one of {sorted(_lib.MODES)}") from None
+
+
+def _raise_rc(routine, rc):
+    if rc > 0:
+        raise BlasError(routine, rc)
+    if rc < 0:
+        raise RuntimeError(f"{routine}: CUDA failure ({rc}): {_lib.last_error()}")
+
+
+def _precision_gate(routine, tag):
+    if tag != "dd":
+        raise NotImplementedError(
+            f"{routine}: precision {tag!r} is not on the B200 dd path (only 'dd')")
+
+
+class _HostPlanes:
+    """Contiguous float64 views of a host store; writes back on ``commit``."""
+
+    def __init__(self, store):
+        self.src = store
+        self.planes = [p if (isinstance(p, np.ndarray) and p.dtype == np.float64
+                             and p.flags.c_contiguous)
+                       else np.ascontiguousarray(p, dtype=np.float64) for p in store[:2]]
+
+    def ptr(self, i):
+        return self.planes[i].ctypes.data
+
+    def commit(self):
+        for dst, src in zip(self.src[:2], self.planes):
+            if dst is not src:
+                dst[...] = src
+
+
+def _dev_ptr(mat, i):
+    return mat.store[i].data_ptr()
+
+
+def _placement(routine, *mats):
+    kinds = {is_device(m) for m in mats}
+    if len(kinds) > 1:
+        raise ValueError(f"{routine}: operands must all be device or all be host matrices")
+    if kinds.pop():
+        devs = {m.store[0].device for m in mats}
+        if len(devs) > 1:
+            raise ValueError(f"{routine}: operands on different devices {sorted(map(str, devs))}")
+        return devs.pop()
+    return None
+
+
+def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
+          beta=1.0, c=None, ldc=None, *, mode=None):
+    """C <- alpha*op(A)*op(B) + beta*C on the B200 (level23.py:180-198)."""
+    routine = "Rgemm"
+    tag = same_precision(routine, a, b, c)
+    _precision_gate(routine, tag)
+    lda, ldb, ldc = _ld_of(a, lda), _ld_of(b, ldb), _ld_of(c, ldc)
+    transa = _flag(routine, transa, ("N", "T", "C"), 1)
+    transb = _flag(routine, transb, ("N", "T", "C"), 2)
+    require(routine, m >= 0, 3)
+    require(routine, n >= 0, 4)
+    require(routine, k >= 0, 5)
+    nrowa, ncola = (m, k) if transa == "N" else (k, m)
+    nrowb, ncolb = (k, n) if transb == "N" else (n, k)
+    require(routine, lda >= max(1, nrowa), 8)
+    require(routine, ldb >= max(1, nrowb), 10)
+    require(routine, ldc >= max(1, m), 13)
+    al = to_dd(alpha)
+    be = to_dd(beta)
+    code = _mode_code(mode)
+    if m == 0 or n == 0 or ((not dd_truthy(al) or k == 0) and dd_is_one(be)):
+        return
+    check_storage(a, nrowa, ncola, lda)
+    check_storage(b, nrowb, ncolb, ldb)
+    check_storage(c, m, n, ldc)
+    L = _lib.load()
+    dev = _placement(routine, a, b, c)
+    args_head = (transa.encode(), transb.encode(), m, n, k, al[0], al[1])
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_rgemm(*args_head, _dev_ptr(a, 0), _dev_ptr(a, 1), lda,
+                             _dev_ptr(b, 0), _dev_ptr(b, 1), ldb, be[0], be[1],
+                             _dev_ptr(c, 0), _dev_ptr(c, 1), ldc, code, stream)
+        _raise_rc(routine, rc)
+        return
+    ha, hb, hc = _HostPlanes(a.store), _HostPlanes(b.store), _HostPlanes(c.store)
+    rc = L.ddb_rgemm_host(*args_head, ha.ptr(0), ha.ptr(1), lda, hb.ptr(0), hb.ptr(1), ldb,
+                          be[0], be[1], hc.ptr(0), hc.ptr(1), ldc, code, None)
+    _raise_rc(routine, rc)
+    hc.commit()
+
+
+def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, mode=None):
+    """C <- alpha*A*A^T + beta*C (trans='N') or alpha*A^T*A + beta*C on the
+    uplo triangle only (level23.py:226-270)."""
+    routine = "Rsyrk"
+    tag = same_precision(routine, a, c)
+    _precision_gate(routine, tag)
+    lda, ldc = _ld_of(a, lda), _ld_of(c, ldc)
+    uplo = _flag(routine, uplo, ("U", "L"), 1)
+    trans = _flag(routine, trans, ("N", "T", "C"), 2)
+    require(routine, n >= 0, 3)
+    require(routine, k >= 0, 4)
+    nrowa, ncola = (n, k) if trans == "N" else (k, n)
+    require(routine, lda >= max(1, nrowa), 7)
+    require(routine, ldc >= max(1, n), 10)
+    al = to_dd(alpha)
+    be = to_dd(beta)
+    code = _mode_code(mode)
+    if n == 0 or ((not dd_truthy(al) or k == 0) and dd_is_one(be)):
+        return
+    check_storage(c, n, n, ldc)
+    if dd_truthy(al):
+        check_storage(a, nrowa, ncola, lda)   # view2d of A only when alpha != 0 (:250-260)
+    L = _lib.load()
+    dev = _placement(routine, a, c)
+    args_head = (uplo.encode(), trans.encode(), n, k, al[0], al[1])
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_rsyrk(*args_head, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, be[0], be[1],
+                             _dev_ptr(c, 0), _dev_ptr(c, 1), ldc, code, stream)
+        _raise_rc(routine, rc)
+        return
+    ha, hc = _HostPlanes(a.store), _HostPlanes(c.store)
+    rc = L.ddb_rsyrk_host(*args_head, ha.ptr(0), ha.ptr(1), lda, be[0], be[1],
+                          hc.ptr(0), hc.ptr(1), ldc, code, None)
+    _raise_rc(routine, rc)
+    hc.commit()
