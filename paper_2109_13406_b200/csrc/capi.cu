@@ -88,7 +88,7 @@ int run(const GemmArgs& g, int mode, cudaStream_t s) {
     int f = 0;
     e = cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    route = f == ROUTE_SAFE ? (mode == MODE_FAST ? 1 : 0) : 2;
+    route = f == ROUTE_SAFE ? (mode == MODE_EXACT ? 0 : (mode == MODE_FAST ? 1 : 3)) : 2;
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   if (e != cudaSuccess) return fail(e, "dd kernel launch");
@@ -144,7 +144,7 @@ int ddb_rgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
               double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
   const int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
   if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_REFERENCE) {
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_ANCHORED) {
     g_last_error = "unknown mode";
     return DDB_EINVAL;
   }
@@ -171,7 +171,7 @@ int ddb_rsyrk(char uplo, char trans, int64_t n, int64_t k,
               double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
   const int rc = ddb_rsyrk_validate(uplo, trans, n, k, lda, ldc);
   if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_REFERENCE) {
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_ANCHORED) {
     g_last_error = "unknown mode";
     return DDB_EINVAL;
   }

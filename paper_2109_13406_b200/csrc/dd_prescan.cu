@@ -96,7 +96,8 @@ static cudaError_t scan(const double* hi, const double* lo, int64_t ld, int64_t 
 // it as its starting accumulator).
 cudaError_t launch_prescan(const GemmArgs& g, int mode, int* row_exp, int* col_exp,
                            int* flag, cudaStream_t s, int* nlaunch) {
-  const bool fast = mode == MODE_FAST;
+  // only the anchored algorithm consumes the exponent maxima
+  const bool fast = mode == MODE_ANCHORED || (mode == MODE_FAST && fast_alg() == 3);
   cudaError_t e;
   // op(A) is m x k: stored m x k (N) or k x m (T)
   if (g.ta == 0)

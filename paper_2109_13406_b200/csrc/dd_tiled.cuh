@@ -1,0 +1,392 @@
+// dd_tiled.cuh -- tiled sm_100a dd GEMM / SYRK kernel template (FP64 pipe).
+//
+// One CTA computes a BM x BN = 128 x 64 tile of C with 256 threads, each
+// owning an 8 x 4 register micro-tile (rows g*32 + tx*2 + q, cols
+// g*32 + ty*2 + q).  op(A) / op(B) k-slices of BK = 16 are staged (hi and lo
+// planes) through shared memory by a 3-stage cp.async pipeline.  8-byte
+// copies handle any lda / ldb / alignment / transpose: each double lands in
+// its k-major smem slot, so every trans variant reads smem identically with
+// 16-byte LDS.  Tensor cores are not used: tcgen05 has no fp64 kind and DMMA
+// rounds away the per-product error terms dd needs.
+//
+// Accumulation algorithms (template ALG), per output element:
+//
+//  ALG_EXACT  -- the reference's own sequence, bit for bit (level23.py:120-149):
+//      transa='N': c = beta-rule(C); c = add2(c, mul2(A(i,l), t_l)),
+//                  t = mul2(alpha, op(B)(l,j)) formed once per smem tile;
+//      transa='T': acc = add2(acc, mul2(A(l,i), op(B)(l,j))) from 0, _combine.
+//      add2_nc(mul2_nc) = 29 FP64-pipe instructions per MAC.
+//
+//  ALG_TWOSUM -- error-bounded dd accumulation, (S, L) per element:
+//      p = ah*bh; e = fma(ah,bh,-p) + ah*bl + al*bh (two more fma);
+//      (S, t) = TwoSum(S, p) [Knuth, 6 ops]; L += t + e;
+//      every RN = 8 steps (S, L) = QuickTwoSum(S, L).   ~12.4 FP64 / MAC.
+//
+//  ALG_SELECT -- as TWOSUM but the sum error comes from a Fast2Sum whose
+//      operands are ordered by an integer compare of |S| and |p| (the ALU
+//      pipe, which the FP64-bound loop leaves idle): s = S + p;
+//      t = small - (s - big).  ~9.4 FP64 + 8 ALU / MAC.
+//      Both fast variants: |L| <= (RN + 4) u sum|ab|, so the rounding error
+//      per step is <= (RN + 4) u^2 sum|ab| < 16 u^2 sum|ab| = 2^-102 sum|ab|,
+//      i.e. inside c*k*2^-104*sum|ab| with c = 4 for every in-window input.
+//
+//  ALG_ANCHOR -- offset-anchored accumulation, 6 FP64 / MAC (opt-in mode
+//      "anchored"): T = sigma + running sum on a fixed grid, Tn = fma(ah,bh,T),
+//      r = fma(ah,bh,T-Tn) is the rounding residual; re-anchored every 32
+//      steps from per-row / per-column exponent maxima.  Its error scales with
+//      max|a|*max|b| rather than sum|a*b|, so it is data
+//      dependent and is not the default.
+//
+// Rsyrk (SYRK = 1 upper / 2 lower) is NT (trans='N') or TN (trans='T') Rgemm
+// with B = A: tiles fully outside the triangle exit at once, diagonal tiles
+// mask their stores (level23.py:245-285).
+#pragma once
+#include "internal.h"
+
+namespace ddb {
+
+enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_ANCHOR = 3 };
+
+namespace tiled {
+
+constexpr int BM = 128, BN = 64, BK = 16, NT = 256, STAGES = 3;
+constexpr int ASTR = BM + 2, BSTR = BN + 2;        // smem row strides (doubles)
+constexpr int A_STAGE = 2 * BK * ASTR, B_STAGE = 2 * BK * BSTR;
+constexpr size_t SMEM_BYTES =
+    (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + (BM + BN) * sizeof(int);
+constexpr int RN = 8;                              // fast: renormalise every RN steps
+constexpr int RB = 2;                              // anchored: k-tiles per anchor block
+constexpr int LG_KB = 5;                           // log2(RB * BK)
+constexpr int GROUP_M = 8;                         // raster group (L2 reuse)
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ long long dbits(double x) { return __double_as_longlong(x); }
+__device__ __forceinline__ double bitsd(long long x) { return __longlong_as_double(x); }
+
+// anchored: sigma = 1.5 * 2**E for the binade T lives in (T > 0 always)
+__device__ __forceinline__ double anchor_of(double T) {
+  return bitsd((dbits(T) & 0x7ff0000000000000LL) | 0x0008000000000000LL);
+}
+__device__ __forceinline__ double anchor_from_bexp(int eb) {
+  eb = eb < 64 ? 64 : (eb > 2000 ? 2000 : eb);
+  return bitsd(((long long)eb << 52) | 0x0008000000000000LL);
+}
+
+// |x| >= |y| on the bit patterns (integer pipe): IEEE order of magnitudes.
+// The sign bit is cleared with a 32-bit LOP3 in inline PTX: written in C the
+// 64-bit mask is recognised as fabs and lowered to a DADD on the FP64 pipe.
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  unsigned long long r;
+  asm("{\n\t.reg .b32 lo, hi;\n\tmov.b64 {lo, hi}, %1;\n\t"
+      "and.b32 hi, hi, 0x7fffffff;\n\tmov.b64 %0, {lo, hi};\n\t}"
+      : "=l"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ bool abs_ge(double x, double y) { return abs_bits(x) >= abs_bits(y); }
+
+template <int TA, int TB>
+__device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double* sB,
+                                           int64_t i0, int64_t j0, int64_t l0, int tid) {
+  // op(A) tile: BM x BK -> sA[plane][kk][ii]
+#pragma unroll
+  for (int r = 0; r < BM * BK / NT; ++r) {
+    const int idx = tid + r * NT;
+    int ii, kk;
+    if (TA == 0) { ii = idx % BM; kk = idx / BM; } else { kk = idx % BK; ii = idx / BK; }
+    const int64_t gi = i0 + ii, gl = l0 + kk;
+    const bool v = gi < g.m && gl < g.k;
+    const int64_t off = v ? (TA == 0 ? gi + gl * g.lda : gl + gi * g.lda) : 0;
+    cp_async8(sA + kk * ASTR + ii, g.a_hi + off, v);
+    cp_async8(sA + BK * ASTR + kk * ASTR + ii, g.a_lo + off, v);
+  }
+  // op(B) tile: BK x BN -> sB[plane][kk][jj]
+#pragma unroll
+  for (int r = 0; r < BN * BK / NT; ++r) {
+    const int idx = tid + r * NT;
+    int jj, kk;
+    if (TB == 0) { kk = idx % BK; jj = idx / BK; } else { jj = idx % BN; kk = idx / BN; }
+    const int64_t gj = j0 + jj, gl = l0 + kk;
+    const bool v = gj < g.n && gl < g.k;
+    const int64_t off = v ? (TB == 0 ? gl + gj * g.ldb : gj + gl * g.ldb) : 0;
+    cp_async8(sB + kk * BSTR + jj, g.b_hi + off, v);
+    cp_async8(sB + BK * BSTR + kk * BSTR + jj, g.b_lo + off, v);
+  }
+}
+
+template <int ALG>
+__device__ __forceinline__ void mac_step(double (&H)[8][4], double (&L)[8][4],
+                                         const double (&ah)[8], const double (&al)[8],
+                                         const double (&bh)[4], const double (&bl)[4]) {
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      if (ALG == ALG_EXACT) {
+        const dd p = mul2_nc(dd{ah[a], al[a]}, dd{bh[b], bl[b]});
+        const dd c = add2_nc(dd{H[a][b], L[a][b]}, p);
+        H[a][b] = c.h;
+        L[a][b] = c.l;
+      } else if (ALG == ALG_ANCHOR) {
+        const double T = H[a][b];
+        const double Tn = dfma(ah[a], bh[b], T);
+        const double r = dfma(ah[a], bh[b], dsub(T, Tn));
+        double l = dfma(ah[a], bl[b], L[a][b]);
+        l = dfma(al[a], bh[b], l);
+        L[a][b] = dadd(l, r);
+        H[a][b] = Tn;
+      } else {
+        const double p = dmul(ah[a], bh[b]);
+        double e = dfma(ah[a], bh[b], -p);
+        e = dfma(ah[a], bl[b], e);
+        e = dfma(al[a], bh[b], e);
+        const double S = H[a][b];
+        const double s = dadd(S, p);
+        double t;
+        if (ALG == ALG_TWOSUM) {
+          const double bb = dsub(s, S);
+          t = dadd(dsub(S, dsub(s, bb)), dsub(p, bb));
+        } else {
+          const bool ge = abs_ge(S, p);
+          const double big = ge ? S : p, small = ge ? p : S;
+          t = dsub(small, dsub(s, big));
+        }
+        L[a][b] = dadd(L[a][b], dadd(t, e));
+        H[a][b] = s;
+      }
+    }
+}
+
+template <int TA, int TB, int ALG, int SYRK>
+__global__ void __launch_bounds__(NT, 1)
+dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restrict__ col_exp,
+                const int* __restrict__ flag, int tiles_m, int tiles_n) {
+  if (*flag != ROUTE_SAFE) return;  // dd_reference.cu handles this call
+
+  // grouped raster over the tile grid
+  const int bid = blockIdx.x;
+  const int group_size = GROUP_M * tiles_n;
+  const int first_m = (bid / group_size) * GROUP_M;
+  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int local = bid % group_size;
+  const int bm = first_m + local % gm, bn = local / gm;
+  const int64_t i0 = (int64_t)bm * BM, j0 = (int64_t)bn * BN;
+  if (SYRK == 1 && i0 > j0 + BN - 1) return;   // tile entirely below the diagonal
+  if (SYRK == 2 && i0 + BM - 1 < j0) return;   // tile entirely above the diagonal
+
+  extern __shared__ __align__(16) double smem[];
+  double* sA = smem;
+  double* sB = smem + STAGES * A_STAGE;
+  int* sRowExp = reinterpret_cast<int*>(sB + STAGES * B_STAGE);
+  int* sColExp = sRowExp + BM;
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+
+  double H[8][4], L[8][4];   // exact: (c_h, c_l); twosum/select: (S, L); anchor: (T, L)
+
+  if (ALG == ALG_ANCHOR) {
+    for (int r = tid; r < BM + BN; r += NT) {
+      if (r < BM) {
+        const int64_t gi = i0 + r;
+        sRowExp[r] = gi < g.m ? row_exp[gi] : 0;
+      } else {
+        const int64_t gj = j0 + (r - BM);
+        sColExp[r - BM] = gj < g.n ? col_exp[gj] : 0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int e = sRowExp[(a >> 1) * 32 + tx * 2 + (a & 1)] +
+                      sColExp[(b >> 1) * 32 + ty * 2 + (b & 1)];
+        H[a][b] = anchor_from_bexp(e - 1018 + LG_KB);
+        L[a][b] = 0.0;
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 8; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        H[a][b] = 0.0;
+        L[a][b] = 0.0;
+        if (ALG == ALG_EXACT && TA == 0) {  // axpy form: start from beta-scaled C
+          const int64_t gi = i0 + (a >> 1) * 32 + tx * 2 + (a & 1);
+          const int64_t gj = j0 + (b >> 1) * 32 + ty * 2 + (b & 1);
+          if (gi < g.m && gj < g.n) {
+            const dd c = scale_beta(g.beta, dd{g.c_hi[gi + gj * g.ldc], g.c_lo[gi + gj * g.ldc]});
+            H[a][b] = c.h;
+            L[a][b] = c.l;
+          }
+        }
+      }
+  }
+
+  const int ktiles = (int)((g.k + BK - 1) / BK);
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load_stage<TA, TB>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, (int64_t)s * BK, tid);
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nk = kt + STAGES - 1;
+      const int ns = nk % STAGES;
+      if (nk < ktiles) load_stage<TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, (int64_t)nk * BK, tid);
+      cp_async_commit();
+    }
+    const int st = kt % STAGES;
+    const double* a_h = sA + st * A_STAGE;
+    const double* a_l = a_h + BK * ASTR;
+    double* b_h = sB + st * B_STAGE;
+    double* b_l = b_h + BK * BSTR;
+
+    if (ALG == ALG_EXACT && TA == 0) {
+      // t = mul2(alpha, op(B)(l, j)) once per tile element (level23.py:122, :137)
+#pragma unroll
+      for (int r = 0; r < BN * BK / NT; ++r) {
+        const int idx = tid + r * NT;
+        const int kk = idx / BN, jj = idx % BN;
+        const dd t = mul2_chk(g.alpha, dd{b_h[kk * BSTR + jj], b_l[kk * BSTR + jj]});
+        b_h[kk * BSTR + jj] = t.h;
+        b_l[kk * BSTR + jj] = t.l;
+      }
+      __syncthreads();
+    }
+
+    int kcount = BK;
+    if (ALG == ALG_EXACT) {
+      const int64_t rem = g.k - (int64_t)kt * BK;
+      kcount = rem < BK ? (int)rem : BK;   // exact: never run a padded k-step
+    }
+
+#pragma unroll 1
+    for (int kk = 0; kk < kcount; ++kk) {
+      double ah[8], al[8], bh[4], bl[4];
+#pragma unroll
+      for (int gq = 0; gq < 4; ++gq) {
+        const double2 vh = *reinterpret_cast<const double2*>(a_h + kk * ASTR + gq * 32 + tx * 2);
+        const double2 vl = *reinterpret_cast<const double2*>(a_l + kk * ASTR + gq * 32 + tx * 2);
+        ah[2 * gq] = vh.x; ah[2 * gq + 1] = vh.y;
+        al[2 * gq] = vl.x; al[2 * gq + 1] = vl.y;
+      }
+#pragma unroll
+      for (int gq = 0; gq < 2; ++gq) {
+        const double2 vh = *reinterpret_cast<const double2*>(b_h + kk * BSTR + gq * 32 + ty * 2);
+        const double2 vl = *reinterpret_cast<const double2*>(b_l + kk * BSTR + gq * 32 + ty * 2);
+        bh[2 * gq] = vh.x; bh[2 * gq + 1] = vh.y;
+        bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
+      }
+      mac_step<ALG>(H, L, ah, al, bh, bl);
+      if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && (kk % RN) == RN - 1) {
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            double s, e;
+            quick_two_sum(H[a][b], L[a][b], s, e);
+            H[a][b] = s;
+            L[a][b] = e;
+          }
+      }
+    }
+
+    if (ALG == ALG_ANCHOR && ((kt + 1) % RB) == 0 && kt + 1 < ktiles) {
+      // re-anchor: fold (T - sigma) and L onto a grid sized for the running
+      // sum plus the next KB-step block
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double T = H[a][b];
+          const double h = dsub(T, anchor_of(T));          // exact
+          const int eh = (int)((dbits(h) >> 52) & 0x7ff);
+          const int e_blk = sRowExp[(a >> 1) * 32 + tx * 2 + (a & 1)] +
+                            sColExp[(b >> 1) * 32 + ty * 2 + (b & 1)] - 1018 + LG_KB;
+          const double sg = anchor_from_bexp(max(eh + 4, e_blk));
+          const double T2 = dadd(sg, h);
+          const double e1 = dsub(h, dsub(T2, sg));          // exact (Fast2Sum)
+          const double l = L[a][b];
+          const double T3 = dadd(T2, l);
+          const double e2 = dsub(l, dsub(T3, T2));          // exact (Fast2Sum)
+          H[a][b] = T3;
+          L[a][b] = dadd(e1, e2);
+        }
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int64_t gi = i0 + (a >> 1) * 32 + tx * 2 + (a & 1);
+      const int64_t gj = j0 + (b >> 1) * 32 + ty * 2 + (b & 1);
+      if (gi >= g.m || gj >= g.n) continue;
+      if (SYRK == 1 && gi > gj) continue;
+      if (SYRK == 2 && gi < gj) continue;
+      const int64_t ci = gi + gj * g.ldc;
+      dd out;
+      if (ALG == ALG_EXACT) {
+        if (TA == 0) out = dd{H[a][b], L[a][b]};
+        else out = combine(g.alpha, dd{H[a][b], L[a][b]}, g.beta, dd{g.c_hi[ci], g.c_lo[ci]});
+      } else {
+        double s, e;
+        const double hv = ALG == ALG_ANCHOR ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
+        two_sum(hv, L[a][b], s, e);
+        const dd at = mul2_chk(g.alpha, dd{s, e});
+        out = add2_chk(at, scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
+      }
+      g.c_hi[ci] = out.h;
+      g.c_lo[ci] = out.l;
+    }
+}
+
+template <int TA, int TB, int ALG, int SYRK>
+cudaError_t launch_one(const GemmArgs& g, const int* row_exp, const int* col_exp,
+                       const int* flag, cudaStream_t s) {
+  auto kern = dd_tiled_kernel<TA, TB, ALG, SYRK>;
+  // per-device attribute: set on every call (cheap, idempotent, thread-safe)
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
+  kern<<<tiles_m * tiles_n, NT, SMEM_BYTES, s>>>(g, row_exp, col_exp, flag, tiles_m, tiles_n);
+  return cudaGetLastError();
+}
+
+// All trans / uplo variants of one algorithm (instantiated per .cu file).
+template <int ALG>
+cudaError_t launch_alg(const GemmArgs& g, const int* row_exp, const int* col_exp,
+                       const int* flag, cudaStream_t s) {
+  if (g.syrk == 0) {
+    switch (g.ta * 2 + g.tb) {
+      case 0: return launch_one<0, 0, ALG, 0>(g, row_exp, col_exp, flag, s);
+      case 1: return launch_one<0, 1, ALG, 0>(g, row_exp, col_exp, flag, s);
+      case 2: return launch_one<1, 0, ALG, 0>(g, row_exp, col_exp, flag, s);
+      default: return launch_one<1, 1, ALG, 0>(g, row_exp, col_exp, flag, s);
+    }
+  }
+  // Rsyrk: trans 'N' == NT with B = A, trans 'T' == TN with B = A
+  if (g.ta == 0)
+    return g.syrk == 1 ? launch_one<0, 1, ALG, 1>(g, row_exp, col_exp, flag, s)
+                       : launch_one<0, 1, ALG, 2>(g, row_exp, col_exp, flag, s);
+  return g.syrk == 1 ? launch_one<1, 0, ALG, 1>(g, row_exp, col_exp, flag, s)
+                     : launch_one<1, 0, ALG, 2>(g, row_exp, col_exp, flag, s);
+}
+
+}  // namespace tiled
+}  // namespace ddb

@@ -1,0 +1,10 @@
+// dd_tiled_twosum.cu -- instantiates the tiled kernel (dd_tiled.cuh) for ALG_TWOSUM;
+// one algorithm per translation unit so the variants compile in parallel.
+#include "dd_tiled.cuh"
+
+namespace ddb {
+cudaError_t launch_tiled_twosum(const GemmArgs& g, const int* row_exp, const int* col_exp,
+                            const int* flag, cudaStream_t s) {
+  return tiled::launch_alg<ALG_TWOSUM>(g, row_exp, col_exp, flag, s);
+}
+}  // namespace ddb

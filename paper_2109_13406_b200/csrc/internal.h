@@ -7,7 +7,10 @@
 
 namespace ddb {
 
-enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2 };
+enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2, MODE_ANCHORED = 3 };
+
+// fast-mode algorithm in use (dd_gemm.cu): needs the exponent prescan?
+int fast_alg();
 
 // Route flag written by the prescan: 0 = every operand inside the safe
 // window (tiled kernels run), nonzero = some value outside it (non-finite,
