@@ -1,0 +1,395 @@
+"""Benchmark: dd GFlops of Rgemm (2mnk) / Rsyrk (n(n+1)k) at n = 8192 on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--n 8192] [--mode fast|exact|anchored]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU, NCCL)
+
+Metric (BASELINE.json): "dd GFlops (Rgemm 2mnk, Rsyrk n(n+1)k) at n=8192,
+1/2/4/8 B200 vs FP64 roof".  One step = one dd Rgemm NN, m = n = k = 8192,
+alpha = 1.5, beta = 0.5, seeded random dd operands (hi ~ U(-1,1), lo ~ 2^-53
+hi; paper_2109_13406_b200/synth.py) resident in HBM: 3 GiB of operands, far
+larger than the 126 MB L2, so no flush is needed between steps.  At N > 1 the
+same total problem is split by column blocks of C over the ranks (strong
+scaling): A is broadcast from rank 0 over NCCL, B / C column blocks are
+scattered and C gathered back, all inside the timed region
+(paper_2109_13406_b200/parallel.py).
+
+Printed keys beyond the driver contract:
+  roofline      FP64-pipe roofline of the dominant kernel (20 fp64 flops per
+                dd MAC, the north star's convention; peak = DFMA rate measured
+                live on this GPU by ddb_fp64_peak_probe)
+  cpu_baseline  the reference algorithm on this box's host cores (the C port
+                in oracle/, bit-identical to the reference), sampled
+  e2e           the same Rgemm through the public API with pinned HOST
+                buffers (H2D of A, B, C and D2H of C inside the timed region)
+  rsyrk         Rsyrk U/N at n = k = 8192 (the metric's second routine)
+  modes         exact (bit-identical) and anchored (opt-in) at the same shape
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "dd GFlops (Rgemm 2mnk, Rsyrk n(n+1)k) at n=8192, 1/2/4/8 B200 vs FP64 roof"
+UNIT = "dd GFlops"
+ALPHA, BETA = 1.5, 0.5
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=8192)
+    p.add_argument("--mode", default="fast", choices=["fast", "exact", "anchored"])
+    p.add_argument("--quick", action="store_true", help="skip the secondary measurements")
+    return p.parse_args()
+
+
+# --------------------------------------------------------------------------
+# clocks during the timed region
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "power_w_max": max(pw) if pw else None,
+                "samples": len(self.rows), "reasons": reasons}
+
+
+# --------------------------------------------------------------------------
+# reference arm and CPU baseline: the oracle port of the reference algorithm
+
+def cpu_sample_rate(n, k, cols, threads):
+    """Time the reference algorithm (bit-exact C port, oracle/dd_oracle.c) on
+    an m = n x cols x k sub-problem of the Rgemm NN workload; returns
+    (dd GFlops, seconds, description)."""
+    from oracle import oracle
+    from paper_2109_13406_b200.synth import random_dd
+    m = n
+    A = random_dd(m, k, m, 0, 1)
+    B = random_dd(k, cols, k, 0, 2)
+    C = random_dd(m, cols, m, 0, 3)
+    ch, cl = C[0].copy(), C[1].copy()
+    t0 = time.perf_counter()
+    rc = oracle.rgemm("N", "N", m, cols, k, (ALPHA, 0.0), A[0], A[1], m, B[0], B[1], k,
+                      (BETA, 0.0), ch, cl, m, threads=threads)
+    dt = time.perf_counter() - t0
+    assert rc == 0
+    return 2.0 * m * cols * k / dt / 1e9, dt, f"Rgemm NN m={m} n={cols} k={k} (columns of the n={n} workload)"
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle
+    threads = oracle.max_threads()
+    n = args.n
+    cols = max(threads, 8)
+    for _ in range(args.warmup):
+        cpu_sample_rate(n, n, cols, threads)
+    rates, secs = [], []
+    for _ in range(args.steps):
+        r, dt, desc = cpu_sample_rate(n, n, cols, threads)
+        rates.append(r)
+        secs.append(dt)
+    value = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64x2 (double-double)",
+        "data": "synthetic", "config": {"workload": f"dd Rgemm NN m=n=k={n}", "n": n,
+                                        "sample": desc, "flush": "inputs > L2 (CPU)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# our arm
+
+def device_operands(n, k, dev):
+    import torch
+    from paper_2109_13406_b200 import DeviceMatrix
+    from paper_2109_13406_b200.synth import random_dd
+    mats = []
+    for rows, cols, tag in ((n, k, 1), (k, n, 2), (n, n, 3)):
+        hi, lo = random_dd(rows, cols, rows, 0, tag)
+        mats.append(DeviceMatrix(rows, cols, "dd", rows, store=(
+            torch.from_numpy(hi).to(dev), torch.from_numpy(lo).to(dev))))
+    return mats
+
+
+def timed(fn, steps, warmup, stream, reset=None):
+    import torch
+    for _ in range(warmup):
+        if reset:
+            reset()
+        fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        if reset:
+            reset()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    return times
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2109_13406_b200 import HostMatrix, Rgemm, Rsyrk, _lib, flop_count
+    from paper_2109_13406_b200 import parallel
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=dev)
+    n = k = args.n
+    mode = args.mode
+    stream = torch.cuda.current_stream(dev)
+    flops = flop_count("Rgemm", n, k=k, m=n)
+
+    if rank == 0 or not distributed:
+        A, B, C0 = device_operands(n, k, dev)
+        C = C0.copy()
+    else:
+        A = B = C0 = C = None
+
+    def reset():
+        if C is not None:
+            C.store[0].copy_(C0.store[0])
+            C.store[1].copy_(C0.store[1])
+
+    if distributed:
+        plan = parallel.RgemmPlan(n, n, k, world, rank, dev)
+
+        def step():
+            parallel.rgemm_columns(plan, "N", "N", ALPHA, A, B, BETA, C, mode=mode)
+    else:
+        def step():
+            Rgemm("N", "N", n, n, k, ALPHA, A, n, B, k, BETA, C, n, mode=mode)
+
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clocks:
+        if distributed:
+            dist.barrier()
+        times = timed(step, args.steps, args.warmup, stream, reset)
+    launches = _lib.launch_count() - launches0
+    t_local = statistics.median(times)
+    t = t_local
+    if distributed:
+        tt = torch.tensor([t_local], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    value = flops / t / 1e9
+
+    extra = {}
+    if rank == 0:
+        # ---- roofline of the dominant kernel (tiled dd GEMM) ----
+        peak = _lib.fp64_peak_probe()        # DFMA lane-ops/s * 2, measured live
+        kernel_t = t if not distributed else t_local
+        achieved = 20.0 * n * n * k / kernel_t / 1e12 / (world if distributed else 1)
+        prof = _profile_traffic()
+        extra["roofline"] = {
+            "bound": "fp64", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
+            "frac": achieved * 1e12 / peak,
+            "traffic": prof.get("dram_bytes_per_launch"),
+            "convention": "20 fp64 flops per dd MAC (north star); peak = live DFMA probe",
+            "algorithmic_bytes": 16.0 * (2 * n * k + 2 * n * n),
+            "fp64_instr_per_mac": {"fast": 12.375, "exact": 29, "anchored": 6.25}[mode],
+        }
+    if rank == 0 and not args.quick:
+        # ---- e2e through the public API with pinned host buffers ----
+        extra["e2e"] = _e2e(n, k, mode, distributed, world, rank, dev)
+        # ---- Rsyrk U/N at n = k ----
+        if not distributed:
+            extra["rsyrk"] = _rsyrk(n, k, mode, dev, stream, max(1, args.steps // 2))
+            extra["modes"] = _modes(n, k, dev, stream, A, B, C, C0, mode)
+        cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, 16, 0)
+        from oracle import oracle
+        extra["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": oracle.max_threads(),
+                                 "kind": "port", "sample": desc, "seconds": cpu_s}
+    elif distributed and not args.quick:
+        _e2e(n, k, mode, distributed, world, rank, dev)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64x2 (double-double)", "data": "synthetic",
+            "config": {"workload": f"dd Rgemm NN m=n=k={n}", "m": n, "n": n, "k": k,
+                       "alpha": ALPHA, "beta": BETA, "mode": mode,
+                       "parallelism": f"columns{world}" if distributed else "single",
+                       "flush": "operands 3 GiB > 126 MB L2"},
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "step_ms_all": [x * 1e3 for x in times],
+        }
+        line.update(extra)
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _profile_traffic():
+    """dram bytes per launch of the tiled kernel from the committed ncu
+    capture (profiles/), if present."""
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _e2e(n, k, mode, distributed, world, rank, dev):
+    import torch
+    from paper_2109_13406_b200 import HostMatrix, Rgemm
+    from paper_2109_13406_b200 import parallel
+    from paper_2109_13406_b200.synth import random_dd
+    hm = []
+    if rank == 0:
+        for rows, cols, tag in ((n, k, 1), (k, n, 2), (n, n, 3)):
+            m = HostMatrix(rows, cols, "dd", rows, pinned=True)
+            hi, lo = random_dd(rows, cols, rows, 0, tag)
+            m.store[0][:] = hi
+            m.store[1][:] = lo
+            hm.append(m)
+    steps = 2
+    times = []
+    for it in range(steps + 1):
+        torch.cuda.synchronize()
+        if distributed:
+            import torch.distributed as dist
+            dist.barrier()
+        t0 = time.perf_counter()
+        if distributed:
+            parallel.rgemm_host_columns("N", "N", n, n, k, ALPHA, *(hm if hm else (None,) * 3),
+                                        BETA, world, rank, dev, mode=mode)
+        else:
+            Rgemm("N", "N", n, n, k, ALPHA, hm[0], n, hm[1], k, BETA, hm[2], n, mode=mode)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if it:
+            times.append(dt)
+    t = statistics.median(times)
+    if distributed:
+        import torch.distributed as dist
+        tt = torch.tensor([t], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": 2.0 * n * n * k / t / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": 16 * (n * k + k * n + n * n), "d2h_bytes_per_step": 16 * n * n,
+            "ms_per_step": t * 1e3, "host_buffers": "pinned numpy planes, ddb_rgemm_host"}
+
+
+def _rsyrk(n, k, mode, dev, stream, steps):
+    import torch
+    from paper_2109_13406_b200 import DeviceMatrix, Rsyrk, flop_count
+    from paper_2109_13406_b200.synth import random_dd
+    hi, lo = random_dd(n, k, n, 0, 1)
+    A = DeviceMatrix(n, k, "dd", n, store=(torch.from_numpy(hi).to(dev), torch.from_numpy(lo).to(dev)))
+    hi, lo = random_dd(n, n, n, 0, 3)
+    C = DeviceMatrix(n, n, "dd", n, store=(torch.from_numpy(hi).to(dev), torch.from_numpy(lo).to(dev)))
+    times = timed(lambda: Rsyrk("U", "N", n, k, ALPHA, A, n, BETA, C, n, mode=mode), steps, 1, stream)
+    t = statistics.median(times)
+    return {"workload": f"dd Rsyrk U N n=k={n}", "value": flop_count("Rsyrk", n, k=k) / t / 1e9,
+            "unit": UNIT, "ms_per_step": t * 1e3, "mode": mode}
+
+
+def _modes(n, k, dev, stream, A, B, C, C0, mode):
+    from paper_2109_13406_b200 import Rgemm
+    out = {}
+    for other in ("exact", "anchored", "fast"):
+        if other == mode:
+            continue
+        times = timed(lambda: Rgemm("N", "N", n, n, k, ALPHA, A, n, B, k, BETA, C, n, mode=other),
+                      1, 1, stream)
+        t = min(times)
+        out[other] = {"ms": t * 1e3, "value": 2.0 * n * n * k / t / 1e9, "unit": UNIT}
+    C.store[0].copy_(C0.store[0])
+    C.store[1].copy_(C0.store[1])
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

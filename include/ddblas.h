@@ -96,6 +96,11 @@ long long ddb_launch_count(void);
  * 1 fast tiled, 2 reference-semantics kernel, 3 anchored tiled), else -1. */
 int ddb_last_route(void);
 
+/* Diagnostic: FP64 FMA throughput of the current GPU in FLOP/s (FMA = 2),
+ * measured with a DFMA burn kernel on `stream` (synchronous; ~10 ms). The
+ * bench's roofline denominator. */
+double ddb_fp64_peak_probe(void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -22,7 +22,7 @@ _c = ctypes.c_char
 
 EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rgemm_validate", "ddb_rsyrk_validate", "ddb_last_error",
-           "ddb_version", "ddb_launch_count", "ddb_last_route")
+           "ddb_version", "ddb_launch_count", "ddb_last_route", "ddb_fp64_peak_probe")
 
 _lib = None
 
@@ -59,6 +59,8 @@ def load():
     L.ddb_version.restype = ctypes.c_int
     L.ddb_launch_count.restype = ctypes.c_longlong
     L.ddb_last_route.restype = ctypes.c_int
+    L.ddb_fp64_peak_probe.restype = ctypes.c_double
+    L.ddb_fp64_peak_probe.argtypes = [_dp]
     _lib = L
     return L
 
@@ -73,3 +75,14 @@ def launch_count():
 
 def last_route():
     return int(load().ddb_last_route())
+
+
+def fp64_peak_probe(stream=None):
+    """Measured FP64 FLOP/s of the current device (DFMA burn, FMA = 2)."""
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream().cuda_stream
+    v = load().ddb_fp64_peak_probe(stream)
+    if v <= 0:
+        raise RuntimeError(f"fp64 peak probe failed: {last_error()}")
+    return v

@@ -109,8 +109,11 @@ def _placement(routine, *mats):
 
 
 def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
-          beta=1.0, c=None, ldc=None, *, mode=None):
-    """C <- alpha*op(A)*op(B) + beta*C on the B200 (level23.py:180-198)."""
+          beta=1.0, c=None, ldc=None, *, mode=None, _check_storage=True):
+    """C <- alpha*op(A)*op(B) + beta*C on the B200 (level23.py:180-198).
+
+    (``_check_storage=False`` is for sub-matrix views made by parallel.py,
+    whose storage ends before ``ld*ncol``; the kernels never touch it.)"""
     routine = "Rgemm"
     tag = same_precision(routine, a, b, c)
     _precision_gate(routine, tag)
@@ -130,9 +133,10 @@ def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
     code = _mode_code(mode)
     if m == 0 or n == 0 or ((not dd_truthy(al) or k == 0) and dd_is_one(be)):
         return
-    check_storage(a, nrowa, ncola, lda)
-    check_storage(b, nrowb, ncolb, ldb)
-    check_storage(c, m, n, ldc)
+    if _check_storage:
+        check_storage(a, nrowa, ncola, lda)
+        check_storage(b, nrowb, ncolb, ldb)
+        check_storage(c, m, n, ldc)
     L = _lib.load()
     dev = _placement(routine, a, b, c)
     args_head = (transa.encode(), transb.encode(), m, n, k, al[0], al[1])
@@ -152,7 +156,8 @@ def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
     hc.commit()
 
 
-def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, mode=None):
+def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, mode=None,
+          _check_storage=True):
     """C <- alpha*A*A^T + beta*C (trans='N') or alpha*A^T*A + beta*C on the
     uplo triangle only (level23.py:226-270)."""
     routine = "Rsyrk"
@@ -171,9 +176,10 @@ def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, 
     code = _mode_code(mode)
     if n == 0 or ((not dd_truthy(al) or k == 0) and dd_is_one(be)):
         return
-    check_storage(c, n, n, ldc)
-    if dd_truthy(al):
-        check_storage(a, nrowa, ncola, lda)   # view2d of A only when alpha != 0 (:250-260)
+    if _check_storage:
+        check_storage(c, n, n, ldc)
+        if dd_truthy(al):
+            check_storage(a, nrowa, ncola, lda)   # A viewed only when alpha != 0 (:250-260)
     L = _lib.load()
     dev = _placement(routine, a, c)
     args_head = (uplo.encode(), trans.encode(), n, k, al[0], al[1])

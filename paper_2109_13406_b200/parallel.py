@@ -1,0 +1,276 @@
+"""Multi-GPU dd Rgemm / Rsyrk: one process per GPU, torch.distributed (NCCL).
+
+The partition is the reference's own thread decomposition lifted to GPUs:
+``Rgemm_par`` splits C into contiguous column panels and runs the sequential
+kernel on each (``/root/reference/pkg/src/mpkit/mpblas/parallel.py:102-157``,
+``_chunks`` :37-47).  Every C(i, j) still sees exactly the same sequence of dd
+operations, so the P-GPU result is bitwise equal to the 1-GPU result in every
+mode (the reference pins this for threads: test_acceptance.py:431-468).
+
+Data movement (operands start on rank 0, the root, and C ends there):
+
+  Rgemm  broadcast op(A)'s storage (every rank needs all rows of op(A));
+         send rank r the columns J_r of op(B) (packed on the root when
+         transb = 'T') and, unless beta == 0, the column slab C[:, J_r];
+         each rank runs the single-GPU kernel on its slab; the slabs come back.
+  Rsyrk  broadcast A; column slabs with triangle-balanced boundaries
+         (j_r ~ n*sqrt(r/P) for 'U'), each rank computes its slab of the
+         triangle as one Rgemm rectangle + one Rsyrk diagonal block -- the
+         same per-element operation sequence as a full Rsyrk (Rsyrk 'N' is NT
+         Rgemm with B = A, level23.py:250-258).
+
+The compute callable is injectable so the host logic is testable on CPU with
+the gloo backend (tests/test_parallel_gloo.py); the default is the CUDA path.
+"""
+
+from __future__ import annotations
+
+import functools
+import math
+
+import torch
+import torch.distributed as dist
+
+from .matrix import DeviceMatrix, to_dd
+from .mpblas import Rgemm, Rsyrk
+
+TILE = 64   # column boundaries are multiples of the kernel's BN
+
+
+def column_split(n, world, tile=TILE):
+    """Contiguous column blocks, sizes within one tile of each other."""
+    ntiles = -(-n // tile) if n else 0
+    out = []
+    for r in range(world):
+        t0 = ntiles * r // world
+        t1 = ntiles * (r + 1) // world
+        out.append((min(n, t0 * tile), min(n, t1 * tile)))
+    return out
+
+
+def triangle_split(n, world, uplo="U", tile=16):
+    """Column blocks with equal triangle area (U: area of [0, j) ~ j^2)."""
+    ntiles = -(-n // tile) if n else 0
+    bounds = [0]
+    for r in range(1, world):
+        frac = math.sqrt(r / world) if uplo == "U" else 1.0 - math.sqrt((world - r) / world)
+        t = int(round(frac * ntiles))
+        bounds.append(max(bounds[-1], min(ntiles, t)))
+    bounds.append(ntiles)
+    return [(min(n, bounds[r] * tile), min(n, bounds[r + 1] * tile)) for r in range(world)]
+
+
+class _Ops:
+    """Collective helpers over torch.distributed (NCCL or gloo)."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def bcast(self, t, src=0):
+        dist.broadcast(t, src=src, group=self.group)
+
+    def exchange(self, ops):
+        ops = [op for op in ops if op is not None]
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    @staticmethod
+    def send(t, peer, group=None):
+        return dist.P2POp(dist.isend, t, peer, group=group)
+
+    @staticmethod
+    def recv(t, peer, group=None):
+        return dist.P2POp(dist.irecv, t, peer, group=group)
+
+
+class RgemmPlan:
+    """Column split and cached receive buffers for one (m, n, k, world) shape."""
+
+    def __init__(self, m, n, k, world, rank, device, tile=TILE):
+        self.m, self.n, self.k = m, n, k
+        self.world, self.rank, self.device = world, rank, device
+        self.blocks = column_split(n, world, tile)
+        self._bufs = {}
+
+    def buf(self, name, numel, dtype=torch.float64):
+        b = self._bufs.get(name)
+        if b is None or b[0].numel() < numel:
+            b = (torch.empty(numel, dtype=dtype, device=self.device),
+                 torch.empty(numel, dtype=dtype, device=self.device))
+            self._bufs[name] = b
+        return b[0][:numel], b[1][:numel]
+
+
+def _slab(store, start, length):
+    return store[0][start:start + length], store[1][start:start + length]
+
+
+def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=None,
+                  compute=None):
+    """C <- alpha op(A) op(B) + beta C with C split by column blocks over ranks.
+
+    On the root, ``a``/``b``/``c`` are the full operands (leading dimensions
+    tight: lda = rows); on the other ranks they are ignored (None).  Returns
+    nothing; on the root C holds the result, bitwise equal to ``Rgemm``."""
+    ops = _Ops(group)
+    compute = functools.partial(Rgemm, _check_storage=False) if compute is None else compute
+    m, n, k = plan.m, plan.n, plan.k
+    rank, world = plan.rank, plan.world
+    ta, tb = transa.upper(), transb.upper()
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    lda = max(1, nra)
+    be = to_dd(beta)
+    beta_zero = be[0] == 0.0 and be[1] == 0.0
+
+    # 1. op(A) to every rank
+    if rank == 0:
+        a_store = (a.store[0][:lda * nca], a.store[1][:lda * nca])
+    else:
+        a_store = plan.buf("A", lda * nca)
+    ops.bcast(a_store[0])
+    ops.bcast(a_store[1])
+    A = DeviceMatrix(nra, nca, "dd", lda, store=a_store)
+
+    # 2. B and C column slabs to their owners
+    j0, j1 = plan.blocks[rank]
+    nb = j1 - j0
+    ldb_loc = max(1, k) if tb == "N" else max(1, nb)
+    sends, recvs = [], []
+    if rank == 0:
+        for r in range(1, world):
+            r0, r1 = plan.blocks[r]
+            if r1 == r0:
+                continue
+            if tb == "N":
+                bs = _slab(b.store, r0 * k, (r1 - r0) * k)
+            else:   # rows r0:r1 of the stored n x k matrix, packed column-major
+                bs = tuple(p[:n * k].view(k, n)[:, r0:r1].contiguous().view(-1) for p in b.store)
+            sends += [ops.send(bs[0], r, group), ops.send(bs[1], r, group)]
+            if not beta_zero:
+                cs = _slab(c.store, r0 * m, (r1 - r0) * m)
+                sends += [ops.send(cs[0], r, group), ops.send(cs[1], r, group)]
+        if tb == "N":
+            b_loc = _slab(b.store, j0 * k, nb * k)
+        else:
+            b_loc = tuple(p[:n * k].view(k, n)[:, j0:j1].contiguous().view(-1) for p in b.store)
+        c_loc = _slab(c.store, j0 * m, nb * m)
+    elif nb:
+        b_loc = plan.buf("B", nb * k)
+        c_loc = plan.buf("C", nb * m)
+        recvs += [ops.recv(b_loc[0], 0, group), ops.recv(b_loc[1], 0, group)]
+        if not beta_zero:
+            recvs += [ops.recv(c_loc[0], 0, group), ops.recv(c_loc[1], 0, group)]
+        else:
+            c_loc[0].zero_()
+            c_loc[1].zero_()
+    ops.exchange(sends + recvs)
+
+    # 3. local slab
+    if nb:
+        nrb_loc, ncb_loc = (k, nb) if tb == "N" else (nb, k)
+        B = DeviceMatrix(nrb_loc, ncb_loc, "dd", ldb_loc, store=b_loc)
+        C = DeviceMatrix(m, nb, "dd", max(1, m), store=c_loc)
+        compute(ta, tb, m, nb, k, alpha, A, lda, B, ldb_loc, beta, C, max(1, m), mode=mode)
+
+    # 4. slabs back to the root
+    sends, recvs = [], []
+    if rank == 0:
+        for r in range(1, world):
+            r0, r1 = plan.blocks[r]
+            if r1 == r0:
+                continue
+            cs = _slab(c.store, r0 * m, (r1 - r0) * m)
+            recvs += [ops.recv(cs[0], r, group), ops.recv(cs[1], r, group)]
+    elif nb:
+        sends += [ops.send(c_loc[0], 0, group), ops.send(c_loc[1], 0, group)]
+    ops.exchange(sends + recvs)
+
+
+def rsyrk_columns(n, k, world, rank, device, uplo, trans, alpha, a, beta, c, mode=None,
+                  group=None, compute_gemm=None, compute_syrk=None):
+    """Rsyrk with the uplo triangle split into triangle-balanced column slabs.
+
+    Root holds A (lda = rows) and C (ldc = n); the result lands in the root's
+    C, bitwise equal to ``Rsyrk``; the opposite triangle is never changed."""
+    ops = _Ops(group)
+    gemm = functools.partial(Rgemm, _check_storage=False) if compute_gemm is None else compute_gemm
+    syrk = functools.partial(Rsyrk, _check_storage=False) if compute_syrk is None else compute_syrk
+    up, tr = uplo.upper(), trans.upper()
+    nra, nca = (n, k) if tr == "N" else (k, n)
+    lda = max(1, nra)
+    blocks = triangle_split(n, world, up)
+    bufs = {}
+
+    def buf(name, numel):
+        if name not in bufs:
+            bufs[name] = (torch.empty(numel, dtype=torch.float64, device=device),
+                          torch.empty(numel, dtype=torch.float64, device=device))
+        return bufs[name]
+
+    a_store = (a.store[0][:lda * nca], a.store[1][:lda * nca]) if rank == 0 else buf("A", lda * nca)
+    ops.bcast(a_store[0])
+    ops.bcast(a_store[1])
+
+    j0, j1 = blocks[rank]
+    nb = j1 - j0
+    sends, recvs = [], []
+    if rank == 0:
+        for r in range(1, world):
+            r0, r1 = blocks[r]
+            if r1 > r0:
+                cs = _slab(c.store, r0 * n, (r1 - r0) * n)
+                sends += [ops.send(cs[0], r, group), ops.send(cs[1], r, group)]
+        c_loc = _slab(c.store, j0 * n, nb * n)
+    elif nb:
+        c_loc = buf("C", nb * n)
+        recvs += [ops.recv(c_loc[0], 0, group), ops.recv(c_loc[1], 0, group)]
+    ops.exchange(sends + recvs)
+
+    if nb:
+        def sub(store, off):
+            return store[0][off:], store[1][off:]
+
+        # rows of op(A) [r0, r1) as a stored matrix view
+        def a_rows(r0, r1):
+            if tr == "N":   # rows r0.. of the n x k matrix: offset r0, same lda
+                return DeviceMatrix(r1 - r0, k, "dd", lda, store=sub(a_store, r0))
+            return DeviceMatrix(k, r1 - r0, "dd", lda, store=sub(a_store, r0 * lda))
+
+        diag = DeviceMatrix(nb, nb, "dd", n, store=sub(c_loc, j0))
+        syrk(up, tr, nb, k, alpha, a_rows(j0, j1), lda, beta, diag, n, mode=mode)
+        ta, tb = ("N", "T") if tr == "N" else ("T", "N")
+        if up == "U" and j0 > 0:        # rectangle rows [0, j0) x cols J
+            rect = DeviceMatrix(j0, nb, "dd", n, store=c_loc)
+            gemm(ta, tb, j0, nb, k, alpha, a_rows(0, j0), lda, a_rows(j0, j1), lda, beta,
+                 rect, n, mode=mode)
+        if up == "L" and j1 < n:        # rectangle rows [j1, n) x cols J
+            rect = DeviceMatrix(n - j1, nb, "dd", n, store=sub(c_loc, j1))
+            gemm(ta, tb, n - j1, nb, k, alpha, a_rows(j1, n), lda, a_rows(j0, j1), lda, beta,
+                 rect, n, mode=mode)
+
+    sends, recvs = [], []
+    if rank == 0:
+        for r in range(1, world):
+            r0, r1 = blocks[r]
+            if r1 > r0:
+                cs = _slab(c.store, r0 * n, (r1 - r0) * n)
+                recvs += [ops.recv(cs[0], r, group), ops.recv(cs[1], r, group)]
+    elif nb:
+        sends += [ops.send(c_loc[0], 0, group), ops.send(c_loc[1], 0, group)]
+    ops.exchange(sends + recvs)
+
+
+def rgemm_host_columns(transa, transb, m, n, k, alpha, a, b, beta, c, world, rank, device,
+                       mode=None, group=None):
+    """End-to-end variant: host (numpy) operands on the root are staged to its
+    GPU, the column-split Rgemm runs, and C is copied back to the host."""
+    plan = RgemmPlan(m, n, k, world, rank, device)
+    if rank == 0:
+        A, B, C = (DeviceMatrix.from_host(x, device) for x in (a, b, c))
+    else:
+        A = B = C = None
+    rgemm_columns(plan, transa, transb, alpha, A, B, beta, C, mode=mode, group=group)
+    if rank == 0:
+        c.store[0][:] = C.store[0].cpu().numpy()
+        c.store[1][:] = C.store[1].cpu().numpy()

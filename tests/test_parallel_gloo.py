@@ -1,0 +1,143 @@
+"""Multi-rank host logic on CPU: world_size 2 over gloo.  The per-slab compute
+is the bit-exact oracle (test infrastructure), so the test checks that the
+column / triangle decomposition, broadcasts, scatters and gathers reproduce
+the single-process result bit for bit -- the GPU analogue of the reference's
+thread-count invariance (test_acceptance.py:431-468)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle
+from paper_2109_13406_b200 import parallel
+from paper_2109_13406_b200.matrix import DeviceMatrix, to_dd
+from paper_2109_13406_b200.synth import random_dd
+
+
+def _np(t):
+    return t.numpy()
+
+
+def oracle_gemm(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, mode=None):
+    """compute callable: the oracle on CPU-tensor views (shares memory)."""
+    ch, cl = _np(c.store[0]), _np(c.store[1])
+    ah, al = np.ascontiguousarray(_np(a.store[0])), np.ascontiguousarray(_np(a.store[1]))
+    bh, bl = np.ascontiguousarray(_np(b.store[0])), np.ascontiguousarray(_np(b.store[1]))
+    rc = oracle.rgemm(ta, tb, m, n, k, to_dd(alpha), ah, al, lda, bh, bl, ldb, to_dd(beta),
+                      ch, cl, ldc, threads=1)
+    assert rc == 0
+
+
+def oracle_syrk(up, tr, n, k, alpha, a, lda, beta, c, ldc, mode=None):
+    ch, cl = _np(c.store[0]), _np(c.store[1])
+    ah, al = np.ascontiguousarray(_np(a.store[0])), np.ascontiguousarray(_np(a.store[1]))
+    rc = oracle.rsyrk(up, tr, n, k, to_dd(alpha), ah, al, lda, to_dd(beta), ch, cl, ldc, threads=1)
+    assert rc == 0
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cpu_mat(rows, cols, seed, tag):
+    hi, lo = random_dd(rows, cols, rows, seed, tag)
+    return DeviceMatrix(rows, cols, "dd", max(1, rows),
+                        store=(torch.from_numpy(hi.copy()), torch.from_numpy(lo.copy())))
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if case[0] == "gemm":
+            _, ta, tb, m, n, k, beta = case
+            nra, nca = (m, k) if ta == "N" else (k, m)
+            nrb, ncb = (k, n) if tb == "N" else (n, k)
+            if rank == 0:
+                A, B, C = _cpu_mat(nra, nca, 3, 1), _cpu_mat(nrb, ncb, 3, 2), _cpu_mat(m, n, 3, 3)
+            else:
+                A = B = C = None
+            plan = parallel.RgemmPlan(m, n, k, world, rank, torch.device("cpu"))
+            parallel.rgemm_columns(plan, ta, tb, 1.5, A, B, beta, C, compute=oracle_gemm)
+            if rank == 0:
+                q.put((C.store[0].numpy().copy(), C.store[1].numpy().copy()))
+        else:
+            _, up, tr, n, k = case
+            nra, nca = (n, k) if tr == "N" else (k, n)
+            if rank == 0:
+                A, C = _cpu_mat(nra, nca, 4, 1), _cpu_mat(n, n, 4, 3)
+            else:
+                A = C = None
+            parallel.rsyrk_columns(n, k, world, rank, torch.device("cpu"), up, tr, 1.5, A, 0.5, C,
+                                   compute_gemm=oracle_gemm, compute_syrk=oracle_syrk)
+            if rank == 0:
+                q.put((C.store[0].numpy().copy(), C.store[1].numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(case, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("ta,tb,beta", [("N", "N", 0.5), ("N", "T", 0.0), ("T", "N", 1.0),
+                                        ("T", "T", 0.5)])
+def test_rgemm_columns_bitwise_equal_single_process(ta, tb, beta):
+    m, n, k = 70, 150, 33
+    got = _run(("gemm", ta, tb, m, n, k, beta))
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A = random_dd(nra, nca, nra, 3, 1)
+    B = random_dd(nrb, ncb, nrb, 3, 2)
+    ch, cl = (x.copy() for x in random_dd(m, n, m, 3, 3))
+    oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra, B[0], B[1], nrb, to_dd(beta),
+                 ch, cl, m)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+@pytest.mark.parametrize("up,tr", [("U", "N"), ("L", "N"), ("U", "T"), ("L", "T")])
+def test_rsyrk_triangle_split_bitwise_equal_single_process(up, tr):
+    n, k = 200, 17
+    got = _run(("syrk", up, tr, n, k))
+    nra, nca = (n, k) if tr == "N" else (k, n)
+    A = random_dd(nra, nca, nra, 4, 1)
+    ch, cl = (x.copy() for x in random_dd(n, n, n, 4, 3))
+    oracle.rsyrk(up, tr, n, k, (1.5, 0.0), A[0], A[1], nra, (0.5, 0.0), ch, cl, n)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+def test_splits_cover_and_balance():
+    for n in (1, 63, 64, 1000, 8192):
+        for world in (1, 2, 3, 4, 8):
+            b = parallel.column_split(n, world)
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            t = parallel.triangle_split(n, world, "U")
+            assert t[0][0] == 0 and t[-1][1] == n
+            assert all(t[i][1] == t[i + 1][0] for i in range(world - 1))
+    # triangle areas within a tile-row of each other at n = 8192, P = 8
+    t = parallel.triangle_split(8192, 8, "U")
+    areas = [(j1 * j1 - j0 * j0) / 2 for j0, j1 in t]
+    assert max(areas) / min(areas) < 1.05
+    t = parallel.triangle_split(8192, 8, "L")
+    areas = [((8192 - j0) ** 2 - (8192 - j1) ** 2) / 2 for j0, j1 in t]
+    assert max(areas) / min(areas) < 1.05
