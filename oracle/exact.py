@@ -94,9 +94,10 @@ def exact_entries(transa, transb, k, alpha, a_hi, a_lo, lda, b_hi, b_lo, ldb,
         for y, j in enumerate(J):
             bj = B_int[y]
             dot = sum(p * q for p, q in zip(ai, bj))
-            cij = Fraction(float(c_hi[i + j * ldc])) + Fraction(float(c_lo[i + j * ldc]))
             v = al * Fraction(dot, den)
-            if be != 0:
+            cij = 0
+            if be != 0:   # beta == 0 never reads C (it may hold NaN: level23.py:163-169)
+                cij = Fraction(float(c_hi[i + j * ldc])) + Fraction(float(c_lo[i + j * ldc]))
                 v += be * cij
             row_v.append(v)
             s = abs(float(al)) * float(np.dot(absA[x], absB[y]))

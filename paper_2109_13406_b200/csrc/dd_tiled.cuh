@@ -49,15 +49,25 @@ enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_ANCHOR = 3 };
 
 namespace tiled {
 
-constexpr int BM = 128, BN = 64, BK = 16, NT = 256, STAGES = 3;
-constexpr int ASTR = BM + 2, BSTR = BN + 2;        // smem row strides (doubles)
-constexpr int A_STAGE = 2 * BK * ASTR, B_STAGE = 2 * BK * BSTR;
-constexpr size_t SMEM_BYTES =
-    (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + (BM + BN) * sizeof(int);
+// Tile configuration: 16 x 16 threads, each owning a TM x TN micro-tile
+// (TM, TN even); MINB CTAs resident per SM (register budget 65536/(256*MINB)).
+template <int TM_, int TN_, int MINB_>
+struct Cfg {
+  static constexpr int TM = TM_, TN = TN_, MINB = MINB_;
+  static constexpr int BM = 16 * TM, BN = 16 * TN, BK = 16, NT = 256, STAGES = 3;
+  static constexpr int ASTR = BM + 2, BSTR = BN + 2;   // smem row strides (doubles)
+  static constexpr int A_STAGE = 2 * BK * ASTR, B_STAGE = 2 * BK * BSTR;
+  static constexpr size_t SMEM_BYTES =
+      (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + (BM + BN) * sizeof(int);
+};
+using CfgBig = Cfg<8, 4, 1>;     // 128 x 64 tile, 1 CTA / SM
+using CfgSmall = Cfg<4, 4, 2>;   // 64 x 64 tile, 2 CTAs / SM
+
+constexpr int BK = 16;
 constexpr int RN = 8;                              // fast: renormalise every RN steps
 constexpr int RB = 2;                              // anchored: k-tiles per anchor block
 constexpr int LG_KB = 5;                           // log2(RB * BK)
-constexpr int GROUP_M = 8;                         // raster group (L2 reuse)
+constexpr int GROUP_M = 12;                        // raster group (L2 reuse)
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -92,9 +102,10 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 }
 __device__ __forceinline__ bool abs_ge(double x, double y) { return abs_bits(x) >= abs_bits(y); }
 
-template <int TA, int TB>
+template <class C, int TA, int TB>
 __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double* sB,
                                            int64_t i0, int64_t j0, int64_t l0, int tid) {
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT, ASTR = C::ASTR, BSTR = C::BSTR;
   // op(A) tile: BM x BK -> sA[plane][kk][ii]
 #pragma unroll
   for (int r = 0; r < BM * BK / NT; ++r) {
@@ -121,14 +132,14 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double
   }
 }
 
-template <int ALG>
-__device__ __forceinline__ void mac_step(double (&H)[8][4], double (&L)[8][4],
-                                         const double (&ah)[8], const double (&al)[8],
-                                         const double (&bh)[4], const double (&bl)[4]) {
+template <int ALG, int TM, int TN>
+__device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN],
+                                         const double (&ah)[TM], const double (&al)[TM],
+                                         const double (&bh)[TN], const double (&bl)[TN]) {
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < TM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < TN; ++b) {
       if (ALG == ALG_EXACT) {
         const dd p = mul2_nc(dd{ah[a], al[a]}, dd{bh[b], bl[b]});
         const dd c = add2_nc(dd{H[a][b], L[a][b]}, p);
@@ -164,10 +175,13 @@ __device__ __forceinline__ void mac_step(double (&H)[8][4], double (&L)[8][4],
     }
 }
 
-template <int TA, int TB, int ALG, int SYRK>
-__global__ void __launch_bounds__(NT, 1)
+template <class C, int TA, int TB, int ALG, int SYRK>
+__global__ void __launch_bounds__(C::NT, C::MINB)
 dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restrict__ col_exp,
                 const int* __restrict__ flag, int tiles_m, int tiles_n) {
+  constexpr int TM = C::TM, TN = C::TN, BM = C::BM, BN = C::BN, NT = C::NT;
+  constexpr int STAGES = C::STAGES, ASTR = C::ASTR, BSTR = C::BSTR;
+  constexpr int A_STAGE = C::A_STAGE, B_STAGE = C::B_STAGE;
   if (*flag != ROUTE_SAFE) return;  // dd_reference.cu handles this call
 
   // grouped raster over the tile grid
@@ -190,7 +204,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
 
-  double H[8][4], L[8][4];   // exact: (c_h, c_l); twosum/select: (S, L); anchor: (T, L)
+  double H[TM][TN], L[TM][TN];   // exact: (c_h, c_l); twosum/select: (S, L); anchor: (T, L)
 
   if (ALG == ALG_ANCHOR) {
     for (int r = tid; r < BM + BN; r += NT) {
@@ -204,9 +218,9 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     }
     __syncthreads();
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < TM; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < TN; ++b) {
         const int e = sRowExp[(a >> 1) * 32 + tx * 2 + (a & 1)] +
                       sColExp[(b >> 1) * 32 + ty * 2 + (b & 1)];
         H[a][b] = anchor_from_bexp(e - 1018 + LG_KB);
@@ -214,9 +228,9 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       }
   } else {
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < TM; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < TN; ++b) {
         H[a][b] = 0.0;
         L[a][b] = 0.0;
         if (ALG == ALG_EXACT && TA == 0) {  // axpy form: start from beta-scaled C
@@ -234,7 +248,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   const int ktiles = (int)((g.k + BK - 1) / BK);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage<TA, TB>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, (int64_t)s * BK, tid);
+    if (s < ktiles) load_stage<C, TA, TB>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, (int64_t)s * BK, tid);
     cp_async_commit();
   }
 
@@ -244,7 +258,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     {
       const int nk = kt + STAGES - 1;
       const int ns = nk % STAGES;
-      if (nk < ktiles) load_stage<TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, (int64_t)nk * BK, tid);
+      if (nk < ktiles) load_stage<C, TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, (int64_t)nk * BK, tid);
       cp_async_commit();
     }
     const int st = kt % STAGES;
@@ -274,27 +288,27 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
 
 #pragma unroll 1
     for (int kk = 0; kk < kcount; ++kk) {
-      double ah[8], al[8], bh[4], bl[4];
+      double ah[TM], al[TM], bh[TN], bl[TN];
 #pragma unroll
-      for (int gq = 0; gq < 4; ++gq) {
+      for (int gq = 0; gq < TM / 2; ++gq) {
         const double2 vh = *reinterpret_cast<const double2*>(a_h + kk * ASTR + gq * 32 + tx * 2);
         const double2 vl = *reinterpret_cast<const double2*>(a_l + kk * ASTR + gq * 32 + tx * 2);
         ah[2 * gq] = vh.x; ah[2 * gq + 1] = vh.y;
         al[2 * gq] = vl.x; al[2 * gq + 1] = vl.y;
       }
 #pragma unroll
-      for (int gq = 0; gq < 2; ++gq) {
+      for (int gq = 0; gq < TN / 2; ++gq) {
         const double2 vh = *reinterpret_cast<const double2*>(b_h + kk * BSTR + gq * 32 + ty * 2);
         const double2 vl = *reinterpret_cast<const double2*>(b_l + kk * BSTR + gq * 32 + ty * 2);
         bh[2 * gq] = vh.x; bh[2 * gq + 1] = vh.y;
         bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
       }
-      mac_step<ALG>(H, L, ah, al, bh, bl);
+      mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
       if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && (kk % RN) == RN - 1) {
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
+        for (int a = 0; a < TM; ++a)
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
+          for (int b = 0; b < TN; ++b) {
             double s, e;
             quick_two_sum(H[a][b], L[a][b], s, e);
             H[a][b] = s;
@@ -307,9 +321,9 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       // re-anchor: fold (T - sigma) and L onto a grid sized for the running
       // sum plus the next KB-step block
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < TM; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < TN; ++b) {
           const double T = H[a][b];
           const double h = dsub(T, anchor_of(T));          // exact
           const int eh = (int)((dbits(h) >> 52) & 0x7ff);
@@ -330,9 +344,9 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
 
   // epilogue
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < TM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < TN; ++b) {
       const int64_t gi = i0 + (a >> 1) * 32 + tx * 2 + (a & 1);
       const int64_t gj = j0 + (b >> 1) * 32 + ty * 2 + (b & 1);
       if (gi >= g.m || gj >= g.n) continue;
@@ -355,10 +369,12 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     }
 }
 
-template <int TA, int TB, int ALG, int SYRK>
+template <class C, int TA, int TB, int ALG, int SYRK>
 cudaError_t launch_one(const GemmArgs& g, const int* row_exp, const int* col_exp,
                        const int* flag, cudaStream_t s) {
-  auto kern = dd_tiled_kernel<TA, TB, ALG, SYRK>;
+  constexpr int BM = C::BM, BN = C::BN, NT = C::NT;
+  constexpr size_t SMEM_BYTES = C::SMEM_BYTES;
+  auto kern = dd_tiled_kernel<C, TA, TB, ALG, SYRK>;
   // per-device attribute: set on every call (cheap, idempotent, thread-safe)
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SMEM_BYTES);
@@ -369,23 +385,23 @@ cudaError_t launch_one(const GemmArgs& g, const int* row_exp, const int* col_exp
 }
 
 // All trans / uplo variants of one algorithm (instantiated per .cu file).
-template <int ALG>
+template <class C, int ALG>
 cudaError_t launch_alg(const GemmArgs& g, const int* row_exp, const int* col_exp,
                        const int* flag, cudaStream_t s) {
   if (g.syrk == 0) {
     switch (g.ta * 2 + g.tb) {
-      case 0: return launch_one<0, 0, ALG, 0>(g, row_exp, col_exp, flag, s);
-      case 1: return launch_one<0, 1, ALG, 0>(g, row_exp, col_exp, flag, s);
-      case 2: return launch_one<1, 0, ALG, 0>(g, row_exp, col_exp, flag, s);
-      default: return launch_one<1, 1, ALG, 0>(g, row_exp, col_exp, flag, s);
+      case 0: return launch_one<C, 0, 0, ALG, 0>(g, row_exp, col_exp, flag, s);
+      case 1: return launch_one<C, 0, 1, ALG, 0>(g, row_exp, col_exp, flag, s);
+      case 2: return launch_one<C, 1, 0, ALG, 0>(g, row_exp, col_exp, flag, s);
+      default: return launch_one<C, 1, 1, ALG, 0>(g, row_exp, col_exp, flag, s);
     }
   }
   // Rsyrk: trans 'N' == NT with B = A, trans 'T' == TN with B = A
   if (g.ta == 0)
-    return g.syrk == 1 ? launch_one<0, 1, ALG, 1>(g, row_exp, col_exp, flag, s)
-                       : launch_one<0, 1, ALG, 2>(g, row_exp, col_exp, flag, s);
-  return g.syrk == 1 ? launch_one<1, 0, ALG, 1>(g, row_exp, col_exp, flag, s)
-                     : launch_one<1, 0, ALG, 2>(g, row_exp, col_exp, flag, s);
+    return g.syrk == 1 ? launch_one<C, 0, 1, ALG, 1>(g, row_exp, col_exp, flag, s)
+                       : launch_one<C, 0, 1, ALG, 2>(g, row_exp, col_exp, flag, s);
+  return g.syrk == 1 ? launch_one<C, 1, 0, ALG, 1>(g, row_exp, col_exp, flag, s)
+                     : launch_one<C, 1, 0, ALG, 2>(g, row_exp, col_exp, flag, s);
 }
 
 }  // namespace tiled

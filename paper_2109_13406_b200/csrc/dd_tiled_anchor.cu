@@ -3,8 +3,9 @@
 #include "dd_tiled.cuh"
 
 namespace ddb {
-cudaError_t launch_tiled_anchor(const GemmArgs& g, const int* row_exp, const int* col_exp,
+cudaError_t launch_tiled_anchor(int cfg, const GemmArgs& g, const int* row_exp, const int* col_exp,
                             const int* flag, cudaStream_t s) {
-  return tiled::launch_alg<ALG_ANCHOR>(g, row_exp, col_exp, flag, s);
+  if (cfg == 1) return tiled::launch_alg<tiled::CfgSmall, ALG_ANCHOR>(g, row_exp, col_exp, flag, s);
+  return tiled::launch_alg<tiled::CfgBig, ALG_ANCHOR>(g, row_exp, col_exp, flag, s);
 }
 }  // namespace ddb
