@@ -286,8 +286,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       kcount = rem < BK ? (int)rem : BK;   // exact: never run a padded k-step
     }
 
-#pragma unroll 1
-    for (int kk = 0; kk < kcount; ++kk) {
+    auto k_step = [&](int kk) {
       double ah[TM], al[TM], bh[TN], bl[TN];
 #pragma unroll
       for (int gq = 0; gq < TM / 2; ++gq) {
@@ -304,16 +303,28 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
         bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
       }
       mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
-      if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && (kk % RN) == RN - 1) {
+    };
+    auto renorm = [&]() {
 #pragma unroll
-        for (int a = 0; a < TM; ++a)
+      for (int a = 0; a < TM; ++a)
 #pragma unroll
-          for (int b = 0; b < TN; ++b) {
-            double s, e;
-            quick_two_sum(H[a][b], L[a][b], s, e);
-            H[a][b] = s;
-            L[a][b] = e;
-          }
+        for (int b = 0; b < TN; ++b) {
+          double s, e;
+          quick_two_sum(H[a][b], L[a][b], s, e);
+          H[a][b] = s;
+          L[a][b] = e;
+        }
+    };
+    if (ALG == ALG_EXACT) {
+#pragma unroll 1
+      for (int kk = 0; kk < kcount; ++kk) k_step(kk);
+    } else {
+      // fast modes: the whole k-tile unrolled (kcount == BK), renormalisation
+      // every RN steps placed at compile time
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        k_step(kk);
+        if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && (kk % RN) == RN - 1) renorm();
       }
     }
 
