@@ -54,6 +54,21 @@ bool debug_sync() {
   return on;
 }
 
+// The per-call workspace and host staging buffers come from the device's
+// stream-ordered pool; keep freed blocks cached instead of returning them to
+// the driver at every synchronisation (release threshold = unlimited).
+void retain_pool_memory() {
+  static thread_local int done_mask = 0;   // bit per device id < 32
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32 || (done_mask >> dev) & 1) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ULL;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done_mask |= 1 << dev;
+}
+
 // Runs one validated, non-trivial call: prescan -> tiled (gated on the
 // flag) -> reference-semantics kernel (gated on the opposite).
 int run(const GemmArgs& g, int mode, cudaStream_t s) {
@@ -70,6 +85,7 @@ int run(const GemmArgs& g, int mode, cudaStream_t s) {
     g_last_route = 2;
     return DDB_OK;
   }
+  retain_pool_memory();
   const int64_t nrow = g.m, ncol = g.n;
   const size_t ws_bytes = sizeof(int) * (size_t)(1 + nrow + ncol) + 64;
   void* ws = nullptr;
@@ -208,6 +224,7 @@ struct DevBuf {
 
 int stage_in(DevBuf& b, const double* hi, const double* lo, int64_t n, cudaStream_t s) {
   b.s = s;
+  retain_pool_memory();
   if (n == 0) return DDB_OK;
   cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b.p), sizeof(double) * 2 * n, s);
   if (e != cudaSuccess) return fail(e, "host staging allocation");
