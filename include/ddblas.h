@@ -43,15 +43,16 @@ extern "C" {
 #define DDB_ENOMEM (-3)   /* device allocation failed */
 
 /* mode: DDB_MODE_EXACT     bit-identical to the reference (29 FP64 instr / MAC)
- *       DDB_MODE_FAST      dd accumulation with deferred renormalisation,
- *                          error <= c*k*2^-104*sum|a*b| (c = 4) for every input
+ *       DDB_MODE_FAST      certified-anchor accumulation (7.5 FP64 instr / MAC
+ *                          + a bf16 tensor-core bound GEMM), error
+ *                          <= c*k*2^-104*sum|a*b| (c = 4) for every input
  *       DDB_MODE_REFERENCE one thread per element, checked arithmetic (debug)
- *       DDB_MODE_ANCHORED  offset-anchored accumulation, 6 FP64 instr / MAC;
- *                          data-dependent error (scales with max|a|*max|b|) */
+ *       DDB_MODE_TWOSUM    TwoSum dd accumulation, same bound, no bound GEMM
+ *                          (12.4 FP64 instr / MAC) */
 #define DDB_MODE_EXACT 0
 #define DDB_MODE_FAST 1
 #define DDB_MODE_REFERENCE 2
-#define DDB_MODE_ANCHORED 3
+#define DDB_MODE_TWOSUM 3
 
 int ddb_rgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
               double alpha_hi, double alpha_lo,
@@ -93,7 +94,7 @@ int ddb_version(void);
 /* Number of kernels this library has launched in this process. */
 long long ddb_launch_count(void);
 /* Route of this thread's last call when DDB_DEBUG_SYNC=1 (0 exact tiled,
- * 1 fast tiled, 2 reference-semantics kernel, 3 anchored tiled), else -1. */
+ * 1 fast tiled, 2 reference-semantics kernel, 3 twosum tiled), else -1. */
 int ddb_last_route(void);
 
 /* Diagnostic: FP64 FMA throughput of the current GPU in FLOP/s (FMA = 2),

@@ -13,7 +13,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libddblas.so")
 
-MODES = {"exact": 0, "fast": 1, "reference": 2, "anchored": 3}
+MODES = {"exact": 0, "fast": 1, "reference": 2, "twosum": 3}
 
 _dp = ctypes.c_void_p
 _i64 = ctypes.c_int64

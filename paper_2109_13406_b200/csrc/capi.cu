@@ -71,9 +71,10 @@ void retain_pool_memory() {
 
 // Runs one validated, non-trivial call: prescan -> tiled (gated on the
 // flag) -> reference-semantics kernel (gated on the opposite).
-int run(const GemmArgs& g, int mode, cudaStream_t s) {
+int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   int nl = 0;
   cudaError_t e;
+  GemmArgs g = g0;
   const bool trivial_ref = mode == MODE_REFERENCE || is_zero(g.alpha.h, g.alpha.l) || g.k == 0;
   bool scalars_ok = true;
   if (mode == MODE_EXACT)
@@ -86,17 +87,30 @@ int run(const GemmArgs& g, int mode, cudaStream_t s) {
     return DDB_OK;
   }
   retain_pool_memory();
+  const int alg = alg_for_mode(mode);
   const int64_t nrow = g.m, ncol = g.n;
-  const size_t ws_bytes = sizeof(int) * (size_t)(1 + nrow + ncol) + 64;
+  const size_t head = ((sizeof(int) * (size_t)(16 + nrow + ncol) + 255) / 256) * 256;
+  const size_t ws_bytes = head + (alg == ALG_CERT ? bound_workspace_bytes(g) : 0);
   void* ws = nullptr;
   e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "workspace allocation");
   int* flag = static_cast<int*>(ws);
   int* row_exp = flag + 16;
   int* col_exp = g.syrk ? row_exp : row_exp + nrow;
-  e = cudaMemsetAsync(ws, 0, ws_bytes, s);
-  if (e == cudaSuccess) e = launch_prescan(g, mode, row_exp, col_exp, flag, s, &nl);
-  if (e == cudaSuccess) e = launch_tiled(g, mode, row_exp, col_exp, flag, s, &nl);
+  const char* what = "dd kernel launch";
+  e = cudaMemsetAsync(ws, 0, head, s);
+  if (e == cudaSuccess) e = launch_prescan(g, alg, row_exp, col_exp, flag, s, &nl);
+  if (e == cudaSuccess && alg == ALG_CERT) {
+    char* bw = static_cast<char*>(ws) + head;
+    const size_t conv = ((2 * (size_t)g.m * g.k + 255) / 256) * 256 +
+                        (g.syrk ? 0 : ((2 * (size_t)g.k * g.n + 255) / 256) * 256);
+    float* bound = reinterpret_cast<float*>(bw + conv);
+    g.bound = bound;
+    g.bnd_fac = 1.0 + (double)g.k * 0x1p-20;
+    g.bnd_floor = (double)g.k * 0x1p-120;
+    e = launch_bound(g, row_exp, col_exp, bw, bound, s, &nl, &what);
+  }
+  if (e == cudaSuccess) e = launch_tiled(g, alg, row_exp, col_exp, flag, s, &nl);
   if (e == cudaSuccess) e = launch_reference(g, flag, GATE_IF_UNSAFE, s, &nl);
   g_launches += nl;
   int route = -1;
@@ -104,10 +118,10 @@ int run(const GemmArgs& g, int mode, cudaStream_t s) {
     int f = 0;
     e = cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    route = f == ROUTE_SAFE ? (mode == MODE_EXACT ? 0 : (mode == MODE_FAST ? 1 : 3)) : 2;
+    route = f != ROUTE_SAFE ? 2 : (mode == MODE_EXACT ? 0 : (mode == MODE_FAST ? 1 : 3));
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
-  if (e != cudaSuccess) return fail(e, "dd kernel launch");
+  if (e != cudaSuccess) return fail(e, what);
   if (e2 != cudaSuccess) return fail(e2, "workspace free");
   g_last_route = route;
   return DDB_OK;
@@ -160,7 +174,7 @@ int ddb_rgemm(char transa, char transb, int64_t m, int64_t n, int64_t k,
               double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
   const int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
   if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_ANCHORED) {
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM) {
     g_last_error = "unknown mode";
     return DDB_EINVAL;
   }
@@ -187,7 +201,7 @@ int ddb_rsyrk(char uplo, char trans, int64_t n, int64_t k,
               double* c_hi, double* c_lo, int64_t ldc, int mode, void* stream) {
   const int rc = ddb_rsyrk_validate(uplo, trans, n, k, lda, ldc);
   if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_ANCHORED) {
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM) {
     g_last_error = "unknown mode";
     return DDB_EINVAL;
   }

@@ -4,8 +4,7 @@
 // It produces, in a per-call workspace:
 //   * row_exp[i]  max biased exponent of the hi words of row i of op(A)
 //   * col_exp[j]  max biased exponent of the hi words of column j of op(B)
-//     (fast mode only: they bound |a_il * b_lj| by 2**(row_exp+col_exp-2044),
-//     which fixes the anchor exponent of the fast accumulator, dd_gemm.cu)
+//     (fast mode only: the scales of the certified bound GEMM, dd_bound.cu)
 //   * flag        nonzero if any word lies outside the safe window:
 //       hi: zero, or 2**-300 <= |hi| < 2**301;   lo: finite and |lo| < 2**301.
 //     Inside the window the tiled kernels' check-free dd arithmetic is
@@ -94,10 +93,10 @@ static cudaError_t scan(const double* hi, const double* lo, int64_t ld, int64_t 
 
 // Scans op(A) rows and op(B) columns (and C when the exact kernel will use
 // it as its starting accumulator).
-cudaError_t launch_prescan(const GemmArgs& g, int mode, int* row_exp, int* col_exp,
+cudaError_t launch_prescan(const GemmArgs& g, int alg, int* row_exp, int* col_exp,
                            int* flag, cudaStream_t s, int* nlaunch) {
-  // only the anchored algorithm consumes the exponent maxima
-  const bool fast = mode == MODE_ANCHORED || (mode == MODE_FAST && fast_alg() == 3);
+  // only the certified-anchor algorithm consumes the exponent maxima
+  const bool fast = alg == ALG_CERT;
   cudaError_t e;
   // op(A) is m x k: stored m x k (N) or k x m (T)
   if (g.ta == 0)
@@ -115,7 +114,7 @@ cudaError_t launch_prescan(const GemmArgs& g, int mode, int* row_exp, int* col_e
   }
   // The exact kernel's axpy form (transa = 'N') starts its unchecked
   // accumulation from beta*C, so C must be in the window too.
-  if (mode == MODE_EXACT && g.ta == 0 && !(g.beta.h == 0.0 && g.beta.l == 0.0)) {
+  if (alg == ALG_EXACT && g.ta == 0 && !(g.beta.h == 0.0 && g.beta.l == 0.0)) {
     // Rsyrk: only the uplo triangle is ever read (level23.py:245-246)
     e = scan(g.c_hi, g.c_lo, g.ldc, g.m, g.n, nullptr, nullptr, flag, s, nlaunch, g.syrk);
     if (e != cudaSuccess) return e;

@@ -1,0 +1,11 @@
+// dd_tiled_cert.cu -- instantiates the tiled kernel (dd_tiled.cuh) for ALG_CERT;
+// one algorithm per translation unit so the variants compile in parallel.
+#include "dd_tiled.cuh"
+
+namespace ddb {
+cudaError_t launch_tiled_cert(int cfg, const GemmArgs& g, const int* row_exp, const int* col_exp,
+                            const int* flag, cudaStream_t s) {
+  if (cfg == 1) return tiled::launch_alg<tiled::CfgSmall, ALG_CERT>(g, row_exp, col_exp, flag, s);
+  return tiled::launch_alg<tiled::CfgBig, ALG_CERT>(g, row_exp, col_exp, flag, s);
+}
+}  // namespace ddb

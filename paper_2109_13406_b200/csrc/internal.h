@@ -7,10 +7,11 @@
 
 namespace ddb {
 
-enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2, MODE_ANCHORED = 3 };
+enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2, MODE_TWOSUM = 3 };
 
-// fast-mode algorithm in use (dd_gemm.cu): needs the exponent prescan?
-int fast_alg();
+// Tiled accumulation algorithm for a mode (dd_gemm.cu).
+enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_CERT = 3 };
+int alg_for_mode(int mode);
 
 // Route flag written by the prescan: 0 = every operand inside the safe
 // window (tiled kernels run), nonzero = some value outside it (non-finite,
@@ -30,16 +31,23 @@ struct GemmArgs {
   const double *b_hi, *b_lo; int64_t ldb;
   double *c_hi, *c_lo; int64_t ldc;
   dd alpha, beta;
+  // fast mode (ALG_CERT): certified magnitude bound, m x n fp32, ld = m,
+  // in units of 2^(row_exp + col_exp - 2044); see dd_bound.cu
+  const float* bound;
+  double bnd_fac, bnd_floor;
 };
 
 // Which kernel should run, decided on the device by the prescan flag.
 enum Gate { GATE_ALWAYS = 0, GATE_IF_SAFE = 1, GATE_IF_UNSAFE = 2 };
 
-cudaError_t launch_prescan(const GemmArgs& g, int mode, int* row_exp, int* col_exp,
+cudaError_t launch_prescan(const GemmArgs& g, int alg, int* row_exp, int* col_exp,
                            int* flag, cudaStream_t s, int* nlaunch);
 cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaStream_t s,
                              int* nlaunch);
-cudaError_t launch_tiled(const GemmArgs& g, int mode, const int* row_exp, const int* col_exp,
+cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,
                          const int* flag, cudaStream_t s, int* nlaunch);
+size_t bound_workspace_bytes(const GemmArgs& g);
+cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
+                         float* bound, cudaStream_t s, int* nlaunch, const char** what);
 
 }  // namespace ddb

@@ -10,9 +10,11 @@ early exits as the reference (``/root/reference/pkg/src/mpkit/mpblas/``):
 
 plus one keyword, ``mode``:
 
-  "fast"   (default; env ``DDBLAS_MODE`` overrides) anchored accumulation on
-           the FP64 pipe, componentwise error <= c*k*2**-104*(|alpha| sum|a*b|
-           + |beta||c|) -- the north-star tolerance
+  "fast"   (default; env ``DDBLAS_MODE`` overrides) certified-anchor dd
+           accumulation on the FP64 pipe, componentwise error
+           <= c*k*2**-104*(|alpha| sum|a*b| + |beta||c|), c = 4 -- the
+           north-star tolerance -- for every input
+  "twosum" the same bound with TwoSum accumulation (no bound GEMM; slower)
   "exact"  bit-identical to the reference's result
   "reference"  the one-thread-per-element checked kernel (debugging)
 

@@ -44,7 +44,7 @@ def child(alg, n, k, trans):
     a, b = dev(nra, nca, A), dev(nrb, ncb, B)
     c0 = dev(m, n, C)
     c = c0.copy()
-    mode = "exact" if alg == "exact" else "fast"
+    mode = "exact" if alg == "exact" else "fast"   # DDB_FAST_ALG picks the fast kernel
     alpha, beta = 1.5, 0.5
     Rgemm(ta, tb, m, n, k, alpha, a, nra, b, nrb, beta, c, m, mode=mode)
     torch.cuda.synchronize()
@@ -76,7 +76,7 @@ if __name__ == "__main__":
     else:
         n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
         k = int(sys.argv[2]) if len(sys.argv) > 2 else n
-        algs = sys.argv[3].split(",") if len(sys.argv) > 3 else ["select", "twosum", "anchor", "exact"]
+        algs = sys.argv[3].split(",") if len(sys.argv) > 3 else ["cert", "twosum", "exact"]
         trans = sys.argv[4] if len(sys.argv) > 4 else "NN"
         for alg in algs:
             run_child(alg, n, k, trans)

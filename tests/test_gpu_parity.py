@@ -216,3 +216,56 @@ def test_fast_mode_error_bound_deep_k(m, n, k):
                                        beta, C[0], C[1], m, I, J)
     worst = exact.error_ratios(gh, gl, m, I, J, vals, scales, k)
     assert worst < 1e-2, worst   # typically ~1e-5 of the bound
+
+
+# ---- fast modes on adversarial magnitude patterns --------------------------
+
+def _pattern(kind, m, n, k, seed):
+    A = [x.copy() for x in random_dd(m, k, m, seed, 1)]
+    B = [x.copy() for x in random_dd(k, n, k, seed, 2)]
+    g = np.random.default_rng(seed)
+    if kind == "disjoint" and k > 1:   # big A entries at l = 0, big B entries at l = 1
+        A[0][:m] *= 2.0 ** 40
+        A[1][:m] *= 2.0 ** 40
+        B[0][1::k] *= 2.0 ** 40
+        B[1][1::k] *= 2.0 ** 40
+    elif kind == "graded":      # magnitudes decay along k
+        scale = 2.0 ** (-np.arange(k) / 4.0)
+        A[0] = (A[0].reshape(k, m) * scale[:, None]).reshape(-1)
+        A[1] = (A[1].reshape(k, m) * scale[:, None]).reshape(-1)
+    elif kind == "rows":        # wildly different row / column scales
+        rs = 2.0 ** g.integers(-80, 80, m)
+        A[0] = (A[0].reshape(k, m) * rs[None, :]).reshape(-1)
+        A[1] = (A[1].reshape(k, m) * rs[None, :]).reshape(-1)
+        cs = 2.0 ** g.integers(-80, 80, n)
+        B[0] = (B[0].reshape(n, k) * cs[:, None]).reshape(-1)
+        B[1] = (B[1].reshape(n, k) * cs[:, None]).reshape(-1)
+    elif kind == "cancel":      # B column j = -(B column j-1): heavy cancellation
+        B[0] = B[0].reshape(n, k)
+        B[1] = B[1].reshape(n, k)
+        B[0][1::2] = -B[0][0::2][: n // 2]
+        B[1][1::2] = -B[1][0::2][: n // 2]
+        A[0][::3] = A[0][::3] * 2.0 ** 30
+        A[1][::3] = A[1][::3] * 2.0 ** 30
+        B[0] = B[0].reshape(-1)
+        B[1] = B[1].reshape(-1)
+    return A, B
+
+
+@pytest.mark.parametrize("mode", ["fast", "twosum"])
+@pytest.mark.parametrize("kind", ["uniform", "disjoint", "graded", "rows", "cancel"])
+@pytest.mark.parametrize("k", [1, 2, 3, 17, 300])
+def test_fast_modes_bound_on_adversarial_patterns(mode, kind, k):
+    m, n = 70, 66
+    A, B = _pattern(kind, m, n, k, 5 + k)
+    C = random_dd(m, n, m, 5, 3)
+    alpha, beta = (1.5, 0.0), (0.5, 0.0)
+    a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
+    Rgemm("N", "N", m, n, k, _Scalar(alpha), a, m, b, k, _Scalar(beta), c, m, mode=mode)
+    assert _lib.last_route() == (1 if mode == "fast" else 3)
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    I, J = list(range(0, m, 7)), list(range(0, n, 5))
+    vals, scales = exact.exact_entries("N", "N", k, alpha, A[0], A[1], m, B[0], B[1], k,
+                                       beta, C[0], C[1], m, I, J)
+    worst = exact.error_ratios(gh, gl, m, I, J, vals, scales, k)
+    assert worst <= 1.0, worst
