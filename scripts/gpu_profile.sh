@@ -13,7 +13,7 @@ $CMD > gpurun_out/${TAG}_bench_quick.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
 echo "launches rc=$?"
-for ALG in twosum anchor; do
+for ALG in cert twosum; do
   CMD1="python bench.py --steps 1 --warmup 0 --quick"
   DDB_FAST_ALG=$ALG $CMD1 > gpurun_out/${TAG}_${ALG}_plain.log 2>&1 && \
   DDB_FAST_ALG=$ALG ncu --set full --clock-control none --import-source on -k regex:dd_tiled -c 1 \
