@@ -138,6 +138,36 @@ template <int ALG, int TM, int TN>
 __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN],
                                          const double (&ah)[TM], const double (&al)[TM],
                                          const double (&bh)[TN], const double (&bl)[TN]) {
+  if (ALG == ALG_CERT) {
+    // phase-ordered so that consecutive FP64 instructions are independent
+    // (each phase touches all TM*TN elements before the next phase starts)
+    double D[TM][TN];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) {
+        const double Tn = dfma(ah[a], bh[b], H[a][b]);
+        D[a][b] = dsub(H[a][b], Tn);
+        H[a][b] = Tn;
+      }
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) L[a][b] = dfma(ah[a], bl[b], L[a][b]);
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) D[a][b] = dfma(ah[a], bh[b], D[a][b]);
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) L[a][b] = dfma(al[a], bh[b], L[a][b]);
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) L[a][b] = dadd(L[a][b], D[a][b]);
+    return;
+  }
 #pragma unroll
   for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -147,14 +177,6 @@ __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN
         const dd c = add2_nc(dd{H[a][b], L[a][b]}, p);
         H[a][b] = c.h;
         L[a][b] = c.l;
-      } else if (ALG == ALG_CERT) {
-        const double T = H[a][b];
-        const double Tn = dfma(ah[a], bh[b], T);
-        const double r = dfma(ah[a], bh[b], dsub(T, Tn));
-        double l = dfma(ah[a], bl[b], L[a][b]);
-        l = dfma(al[a], bh[b], l);
-        L[a][b] = dadd(l, r);
-        H[a][b] = Tn;
       } else {
         const double p = dmul(ah[a], bh[b]);
         double e = dfma(ah[a], bh[b], -p);
