@@ -11,7 +11,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libddblas.so")
+# DDBLAS_LIB points at an alternative build (kernel experiments); default in-tree
+LIB_PATH = os.environ.get("DDBLAS_LIB") or os.path.join(HERE, "libddblas.so")
 
 MODES = {"exact": 0, "fast": 1, "reference": 2, "twosum": 3}
 

@@ -67,6 +67,12 @@ using CfgBig = Cfg<8, 4, 1>;     // 128 x 64 tile, 1 CTA / SM
 using CfgSmall = Cfg<4, 4, 2>;   // 64 x 64 tile, 2 CTAs / SM
 
 constexpr int BK = 16;
+#ifndef DDB_PHASE
+#define DDB_PHASE 0      // phase-ordered CERT MAC step (experiment switch)
+#endif
+#ifndef DDB_PREFETCH
+#define DDB_PREFETCH 1   // fast modes: load step kk+1's operands before step kk's math
+#endif
 constexpr int RN = 8;                              // fast: renormalise every RN steps
 constexpr int RF = 2;                              // cert: fold L into T every RF steps
 constexpr int GROUP_M = 12;                        // raster group (L2 reuse)
@@ -138,7 +144,7 @@ template <int ALG, int TM, int TN>
 __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN],
                                          const double (&ah)[TM], const double (&al)[TM],
                                          const double (&bh)[TN], const double (&bl)[TN]) {
-  if (ALG == ALG_CERT) {
+  if (ALG == ALG_CERT && DDB_PHASE) {
     // phase-ordered so that consecutive FP64 instructions are independent
     // (each phase touches all TM*TN elements before the next phase starts)
     double D[TM][TN];
@@ -172,7 +178,15 @@ __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN
   for (int a = 0; a < TM; ++a)
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
-      if (ALG == ALG_EXACT) {
+      if (ALG == ALG_CERT) {
+        const double T = H[a][b];
+        const double Tn = dfma(ah[a], bh[b], T);
+        const double r = dfma(ah[a], bh[b], dsub(T, Tn));
+        double l = dfma(ah[a], bl[b], L[a][b]);
+        l = dfma(al[a], bh[b], l);
+        L[a][b] = dadd(l, r);
+        H[a][b] = Tn;
+      } else if (ALG == ALG_EXACT) {
         const dd p = mul2_nc(dd{ah[a], al[a]}, dd{bh[b], bl[b]});
         const dd c = add2_nc(dd{H[a][b], L[a][b]}, p);
         H[a][b] = c.h;
@@ -315,8 +329,8 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       kcount = rem < BK ? (int)rem : BK;   // exact: never run a padded k-step
     }
 
-    auto k_step = [&](int kk) {
-      double ah[TM], al[TM], bh[TN], bl[TN];
+    auto load_ops = [&](int kk, double (&ah)[TM], double (&al)[TM], double (&bh)[TN],
+                        double (&bl)[TN]) {
 #pragma unroll
       for (int gq = 0; gq < TM / 2; ++gq) {
         const double2 vh = *reinterpret_cast<const double2*>(a_h + kk * ASTR + gq * 32 + tx * 2);
@@ -331,6 +345,10 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
         bh[2 * gq] = vh.x; bh[2 * gq + 1] = vh.y;
         bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
       }
+    };
+    auto k_step = [&](int kk) {
+      double ah[TM], al[TM], bh[TN], bl[TN];
+      load_ops(kk, ah, al, bh, bl);
       mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
     };
     auto renorm = [&]() {
@@ -359,10 +377,17 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       for (int kk = 0; kk < kcount; ++kk) k_step(kk);
     } else {
       // fast modes: the whole k-tile unrolled (kcount == BK), renormalisation
-      // every RN steps placed at compile time
+      // / folding placed at compile time, operands double-buffered in registers
+      double ah[2][TM], al[2][TM], bh[2][TN], bl[2][TN];
+      if (DDB_PREFETCH) load_ops(0, ah[0], al[0], bh[0], bl[0]);
 #pragma unroll
       for (int kk = 0; kk < BK; ++kk) {
-        k_step(kk);
+        if (DDB_PREFETCH) {
+          if (kk + 1 < BK) load_ops(kk + 1, ah[(kk + 1) & 1], al[(kk + 1) & 1], bh[(kk + 1) & 1], bl[(kk + 1) & 1]);
+          mac_step<ALG, TM, TN>(H, L, ah[kk & 1], al[kk & 1], bh[kk & 1], bl[kk & 1]);
+        } else {
+          k_step(kk);
+        }
         if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && (kk % RN) == RN - 1) renorm();
         if (ALG == ALG_CERT && (kk % RF) == RF - 1) fold();
       }

@@ -17,9 +17,12 @@ import torch  # noqa: E402
 
 def run_child(alg, n, k, trans):
     env = dict(os.environ)
-    tile = "big"
-    if alg.endswith("@small"):
-        alg, tile = alg[:-6], "small"
+    parts = alg.split("@")          # alg[@tile[@libvariant]]
+    alg = parts[0]
+    tile = parts[1] if len(parts) > 1 and parts[1] else "big"
+    if len(parts) > 2:
+        env["DDBLAS_LIB"] = os.path.join(REPO, "scripts", "libs", f"libddblas_{parts[2]}.so")
+        env["DDB_LIBTAG"] = parts[2]
     env["DDB_TILE"] = tile
     env["DDB_FAST_ALG"] = alg
     out = subprocess.run([sys.executable, __file__, "--child", alg, str(n), str(k), trans],
@@ -66,7 +69,7 @@ def child(alg, n, k, trans):
     vals, scales = exact.exact_entries(ta, tb, k, (1.5, 0.0), A[0], A[1], nra, B[0], B[1], nrb,
                                        (0.5, 0.0), C[0], C[1], m, I, J)
     worst = exact.error_ratios(gh, gl, m, I, J, vals, scales, k)
-    print(f"{alg:8s} {os.environ.get('DDB_TILE','big'):5s} {trans} n={n} k={k}: {t*1e3:9.2f} ms  {gf:9.1f} dd GFlops  "
+    print(f"{alg:8s} {os.environ.get('DDB_TILE','big'):5s} {os.environ.get('DDB_LIBTAG','main'):5s} {trans} n={n} k={k}: {t*1e3:9.2f} ms  {gf:9.1f} dd GFlops  "
           f"({gf/3720*100:5.1f}% of 3.72 TF roof)  err/bound {worst:.3e}", flush=True)
 
 
