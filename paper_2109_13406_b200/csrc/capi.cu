@@ -90,7 +90,12 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   const int alg = alg_for_mode(mode);
   const int64_t nrow = g.m, ncol = g.n;
   const size_t head = ((sizeof(int) * (size_t)(16 + nrow + ncol) + 255) / 256) * 256;
-  const size_t ws_bytes = head + (alg == ALG_CERT ? bound_workspace_bytes(g) : 0);
+  int64_t kchunk = g.k;
+  const int splits = choose_ksplit(g, alg, &kchunk);
+  g.kchunk = kchunk;
+  const size_t part_bytes = splits > 1 ? (size_t)splits * 2 * g.m * g.n * sizeof(double) : 0;
+  const size_t bnd_bytes = alg == ALG_CERT ? ((bound_workspace_bytes(g) + 255) / 256) * 256 : 0;
+  const size_t ws_bytes = head + bnd_bytes + part_bytes;
   void* ws = nullptr;
   e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "workspace allocation");
@@ -110,7 +115,9 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
     g.bnd_floor = (double)g.k * 0x1p-120;
     e = launch_bound(g, row_exp, col_exp, bw, bound, s, &nl, &what);
   }
+  if (splits > 1) g.part = reinterpret_cast<double*>(static_cast<char*>(ws) + head + bnd_bytes);
   if (e == cudaSuccess) e = launch_tiled(g, alg, row_exp, col_exp, flag, s, &nl);
+  if (e == cudaSuccess && splits > 1) e = launch_splitk_reduce(g, splits, flag, s, &nl);
   if (e == cudaSuccess) e = launch_reference(g, flag, GATE_IF_UNSAFE, s, &nl);
   g_launches += nl;
   int route = -1;

@@ -4,6 +4,7 @@
 //   fast     -> ALG_CERT    (certified-anchor accumulation; env
 //                            DDB_FAST_ALG=twosum|select overrides, for measurement)
 //   twosum   -> ALG_TWOSUM  (error-bounded without the bound GEMM)
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 
@@ -42,6 +43,88 @@ static int tile_cfg() {
     return (v != nullptr && !std::strcmp(v, "small")) ? 1 : 0;
   }();
   return cfg;
+}
+
+// ---- split-K (fast modes only: exact keeps the reference's single sequential
+// accumulation per element) -------------------------------------------------
+
+static int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// Picks a k-chunk that fills the GPU when the tile grid alone leaves a wave
+// mostly empty (e.g. m = n = 2048, k = 65536: 512 tiles on 148 SMs).
+int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk) {
+  *kchunk = g.k;
+  if (alg == ALG_EXACT || g.k < 1024) return 1;
+  const int bm = tile_cfg() == 1 ? 64 : 128, bn = 64;
+  const int64_t tm = (g.m + bm - 1) / bm, tn = (g.n + bn - 1) / bn;
+  int64_t tiles = 0;
+  if (g.syrk == 0) {
+    tiles = tm * tn;
+  } else {
+    for (int64_t j = 0; j < tn; ++j)
+      for (int64_t i = 0; i < tm; ++i) {
+        const int64_t i0 = i * bm, j0 = j * bn;
+        if (g.syrk == 1 ? i0 <= j0 + bn - 1 : i0 + bm - 1 >= j0) ++tiles;
+      }
+  }
+  const int sms = sm_count();
+  auto eff = [&](int64_t t) {
+    const double waves = (double)t / sms;
+    return waves / std::ceil(waves);
+  };
+  double best = eff(tiles);
+  int best_s = 1;
+  int64_t best_chunk = g.k;
+  for (int s = 2; s <= 16; ++s) {
+    int64_t chunk = (g.k + s - 1) / s;
+    chunk = ((chunk + 31) / 32) * 32;
+    if (chunk < 512) break;
+    const int real = (int)((g.k + chunk - 1) / chunk);
+    const double e = eff(tiles * real);
+    if (e > best + 0.03) {
+      best = e;
+      best_s = real;
+      best_chunk = chunk;
+    }
+  }
+  *kchunk = best_chunk;
+  return best_s;
+}
+
+__global__ void __launch_bounds__(256)
+splitk_reduce_kernel(GemmArgs g, int splits, const int* __restrict__ flag) {
+  if (*flag != ROUTE_SAFE) return;
+  const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (i >= g.m) return;
+  const size_t plane = (size_t)g.m * g.n;
+  for (int64_t j = (int64_t)blockIdx.y * 8 + threadIdx.y; j < g.n; j += (int64_t)gridDim.y * 8) {
+    if (g.syrk == 1 && i > j) continue;
+    if (g.syrk == 2 && i < j) continue;
+    const size_t pi = i + j * g.m;
+    dd acc{g.part[pi], g.part[plane + pi]};
+    for (int z = 1; z < splits; ++z) {
+      const double* pz = g.part + (size_t)z * 2 * plane;
+      acc = add2_chk(acc, dd{pz[pi], pz[plane + pi]});
+    }
+    const int64_t ci = i + j * g.ldc;
+    const dd out = add2_chk(mul2_chk(g.alpha, acc), scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
+    g.c_hi[ci] = out.h;
+    g.c_lo[ci] = out.l;
+  }
+}
+
+cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag, cudaStream_t s,
+                                 int* nlaunch) {
+  int64_t gy = (g.n + 7) / 8;
+  if (gy > 65535) gy = 65535;
+  dim3 grid((unsigned)((g.m + 31) / 32), (unsigned)gy), block(32, 8);
+  splitk_reduce_kernel<<<grid, block, 0, s>>>(g, splits, flag);
+  ++*nlaunch;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,

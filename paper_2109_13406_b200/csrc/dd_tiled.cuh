@@ -112,7 +112,8 @@ __device__ __forceinline__ bool abs_ge(double x, double y) { return abs_bits(x) 
 
 template <class C, int TA, int TB>
 __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double* sB,
-                                           int64_t i0, int64_t j0, int64_t l0, int tid) {
+                                           int64_t i0, int64_t j0, int64_t l0, int64_t kend,
+                                           int tid) {
   constexpr int BM = C::BM, BN = C::BN, NT = C::NT, ASTR = C::ASTR, BSTR = C::BSTR;
   // op(A) tile: BM x BK -> sA[plane][kk][ii]
 #pragma unroll
@@ -121,7 +122,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double
     int ii, kk;
     if (TA == 0) { ii = idx % BM; kk = idx / BM; } else { kk = idx % BK; ii = idx / BK; }
     const int64_t gi = i0 + ii, gl = l0 + kk;
-    const bool v = gi < g.m && gl < g.k;
+    const bool v = gi < g.m && gl < kend;
     const int64_t off = v ? (TA == 0 ? gi + gl * g.lda : gl + gi * g.lda) : 0;
     cp_async8(sA + kk * ASTR + ii, g.a_hi + off, v);
     cp_async8(sA + BK * ASTR + kk * ASTR + ii, g.a_lo + off, v);
@@ -133,7 +134,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double
     int jj, kk;
     if (TB == 0) { kk = idx % BK; jj = idx / BK; } else { jj = idx % BN; kk = idx / BN; }
     const int64_t gj = j0 + jj, gl = l0 + kk;
-    const bool v = gj < g.n && gl < g.k;
+    const bool v = gj < g.n && gl < kend;
     const int64_t off = v ? (TB == 0 ? gl + gj * g.ldb : gj + gl * g.ldb) : 0;
     cp_async8(sB + kk * BSTR + jj, g.b_hi + off, v);
     cp_async8(sB + BK * BSTR + kk * BSTR + jj, g.b_lo + off, v);
@@ -288,10 +289,13 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       }
   }
 
-  const int ktiles = (int)((g.k + BK - 1) / BK);
+  // split-K (fast modes): blockIdx.y owns k in [kbeg, kend), a multiple of BK
+  const int64_t kbeg = (int64_t)blockIdx.y * g.kchunk;
+  const int64_t kend = g.kchunk >= g.k ? g.k : min(g.k, kbeg + g.kchunk);
+  const int ktiles = (int)((kend - kbeg + BK - 1) / BK);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage<C, TA, TB>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, (int64_t)s * BK, tid);
+    if (s < ktiles) load_stage<C, TA, TB>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, kbeg + (int64_t)s * BK, kend, tid);
     cp_async_commit();
   }
 
@@ -301,7 +305,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     {
       const int nk = kt + STAGES - 1;
       const int ns = nk % STAGES;
-      if (nk < ktiles) load_stage<C, TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, (int64_t)nk * BK, tid);
+      if (nk < ktiles) load_stage<C, TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, kbeg + (int64_t)nk * BK, kend, tid);
       cp_async_commit();
     }
     const int st = kt % STAGES;
@@ -325,7 +329,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
 
     int kcount = BK;
     if (ALG == ALG_EXACT) {
-      const int64_t rem = g.k - (int64_t)kt * BK;
+      const int64_t rem = kend - kbeg - (int64_t)kt * BK;
       kcount = rem < BK ? (int)rem : BK;   // exact: never run a padded k-step
     }
 
@@ -415,6 +419,12 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
         double s, e;
         const double hv = ALG == ALG_CERT ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
         two_sum(hv, L[a][b], s, e);
+        if (g.part != nullptr) {   // split-K: this slice's sum, combined by splitk_reduce
+          double* ph = g.part + (size_t)blockIdx.y * 2 * g.m * g.n;
+          ph[gi + gj * g.m] = s;
+          ph[(size_t)g.m * g.n + gi + gj * g.m] = e;
+          continue;
+        }
         const dd at = mul2_chk(g.alpha, dd{s, e});
         out = add2_chk(at, scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
       }
@@ -434,7 +444,9 @@ cudaError_t launch_one(const GemmArgs& g, const int* row_exp, const int* col_exp
                                        (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
-  kern<<<tiles_m * tiles_n, NT, SMEM_BYTES, s>>>(g, row_exp, col_exp, flag, tiles_m, tiles_n);
+  const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
+  kern<<<dim3(tiles_m * tiles_n, splits), NT, SMEM_BYTES, s>>>(g, row_exp, col_exp, flag,
+                                                                tiles_m, tiles_n);
   return cudaGetLastError();
 }
 

@@ -35,6 +35,11 @@ struct GemmArgs {
   // in units of 2^(row_exp + col_exp - 2044); see dd_bound.cu
   const float* bound;
   double bnd_fac, bnd_floor;
+  // split-K (fast modes): k is cut into chunks of kchunk (a multiple of the
+  // k-tile); each chunk's (hi, lo) sum goes to part[z] (2 planes of m x n) and
+  // splitk_reduce adds them in order.  kchunk >= k: no split, part == nullptr.
+  int64_t kchunk;
+  double* part;
 };
 
 // Which kernel should run, decided on the device by the prescan flag.
@@ -47,6 +52,9 @@ cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaS
 cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,
                          const int* flag, cudaStream_t s, int* nlaunch);
 size_t bound_workspace_bytes(const GemmArgs& g);
+int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk);
+cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag, cudaStream_t s,
+                                 int* nlaunch);
 cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
                          float* bound, cudaStream_t s, int* nlaunch, const char** what);
 

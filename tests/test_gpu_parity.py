@@ -269,3 +269,42 @@ def test_fast_modes_bound_on_adversarial_patterns(mode, kind, k):
                                        beta, C[0], C[1], m, I, J)
     worst = exact.error_ratios(gh, gl, m, I, J, vals, scales, k)
     assert worst <= 1.0, worst
+
+
+# ---- split-K (fast modes fill the GPU when the tile grid is small) ----------
+
+@pytest.mark.parametrize("mode", ["fast", "twosum"])
+@pytest.mark.parametrize("shape", [(200, 130, 4096), (64, 64, 20000), (300, 70, 1500)])
+def test_fast_split_k_within_bound(mode, shape):
+    m, n, k = shape
+    A = random_dd(m, k, m, 21, 1)
+    B = random_dd(k, n, k, 21, 2)
+    C = random_dd(m, n, m, 21, 3)
+    alpha, beta = (1.5, 2 ** -60), (0.5, 0.0)
+    a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
+    Rgemm("N", "N", m, n, k, _Scalar(alpha), a, m, b, k, _Scalar(beta), c, m, mode=mode)
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    I, J = list(range(0, m, max(1, m // 6))), list(range(0, n, max(1, n // 6)))
+    vals, scales = exact.exact_entries("N", "N", k, alpha, A[0], A[1], m, B[0], B[1], k,
+                                       beta, C[0], C[1], m, I, J)
+    assert exact.error_ratios(gh, gl, m, I, J, vals, scales, k) < 1e-2
+
+
+@pytest.mark.parametrize("uplo", ["U", "L"])
+def test_fast_split_k_rsyrk_triangle_only(uplo):
+    n, k = 150, 6000
+    A = random_dd(n, k, n, 22, 1)
+    C = random_dd(n, n, n, 22, 3)
+    a, c = dev(n, k, n, A), dev(n, n, n, C)
+    Rsyrk(uplo, "N", n, k, 1.5, a, n, 0.5, c, n, mode="fast")
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    iu = np.array([[(i <= j) if uplo == "U" else (i >= j) for j in range(n)] for i in range(n)])
+    mask = iu.T.reshape(-1)          # column-major flat index i + j*n
+    assert bits_equal(gh[~mask], C[0][~mask]) and bits_equal(gl[~mask], C[1][~mask])
+    I = [0, 37, 74, 149]
+    vals, scales = exact.exact_entries("N", "T", k, (1.5, 0.0), A[0], A[1], n, A[0], A[1], n,
+                                       (0.5, 0.0), C[0], C[1], n, I, I)
+    for x, i in enumerate(I):
+        for y, j in enumerate(I):
+            if (i <= j) if uplo == "U" else (i >= j):
+                assert exact.error_ratios(gh, gl, n, [i], [j], [[vals[x][y]]], [[scales[x][y]]], k) < 1e-2
