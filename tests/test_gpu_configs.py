@@ -1,0 +1,205 @@
+"""GPU parity at the BASELINE.json configurations (full sizes).
+
+Full-size outputs are checked on sampled entries: every C(i, j) depends only
+on row i of op(A), column j of op(B) and C(i, j), so the C oracle run on the
+sampled rows / columns with the full k is the reference's result for exactly
+those entries (bitwise in exact mode), and the exact-rational checker bounds
+the fast mode's error there ("Large shapes").
+"""
+
+import numpy as np
+import pytest
+
+from oracle import exact, oracle
+from paper_2109_13406_b200 import DeviceMatrix, Rgemm, Rsyrk, _lib
+from paper_2109_13406_b200.synth import hashed_dd_device, hashed_entries, random_dd
+
+pytestmark = pytest.mark.gpu
+
+ALPHA, BETA = (1.5, 0.0), (0.5, 0.0)
+
+
+def bits_equal(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return bool(np.all((a.view(np.uint64) == b.view(np.uint64)) | (np.isnan(a) & np.isnan(b))))
+
+
+def dev(rows, cols, planes):
+    import torch
+    return DeviceMatrix(rows, cols, "dd", rows,
+                        store=tuple(torch.from_numpy(np.ascontiguousarray(p)).cuda() for p in planes))
+
+
+def sub_cols(planes, rows, cols_idx):
+    """Columns cols_idx of a column-major rows x * matrix, as a rows x |J| matrix."""
+    return tuple(np.ascontiguousarray(p.reshape(-1, rows)[cols_idx].reshape(-1)) for p in planes)
+
+
+def sub_rows(planes, rows, ncols, rows_idx):
+    """Rows rows_idx of a column-major rows x ncols matrix, as |I| x ncols."""
+    return tuple(np.ascontiguousarray(p.reshape(ncols, rows)[:, rows_idx].reshape(-1))
+                 for p in planes)
+
+
+def oracle_entries(ta, tb, m, n, k, A, B, C, I, J):
+    """The reference's values of C(I, J) (C oracle on the sampled slabs)."""
+    nra = m if ta == "N" else k
+    nrb = k if tb == "N" else n
+    As = sub_rows(A, nra, k if ta == "N" else m, I) if ta == "N" else sub_cols(A, nra, I)
+    Bs = sub_cols(B, nrb, J) if tb == "N" else sub_rows(B, nrb, k, J)
+    Cs = sub_rows(sub_cols(C, m, J), m, len(J), I)
+    ch, cl = Cs[0].copy(), Cs[1].copy()
+    lda_s = len(I) if ta == "N" else k
+    ldb_s = k if tb == "N" else len(J)
+    assert oracle.rgemm(ta, tb, len(I), len(J), k, ALPHA, As[0], As[1], lda_s, Bs[0], Bs[1],
+                        ldb_s, BETA, ch, cl, len(I)) == 0
+    return ch, cl
+
+
+def gather(planes, m, I, J):
+    h, l = planes
+    idx = np.array([[i + j * m for i in I] for j in J]).reshape(-1)   # column-major |I| x |J|
+    return h[idx], l[idx]
+
+
+def test_config1_rgemm_nn_256_full_bitwise():
+    """configs[0]: dd Rgemm NN m=n=k=256, alpha=1.5, beta=0.5 -- every entry."""
+    n = 256
+    A, B, C = random_dd(n, n, n, 0, 1), random_dd(n, n, n, 0, 2), random_dd(n, n, n, 0, 3)
+    ch, cl = C[0].copy(), C[1].copy()
+    assert oracle.rgemm("N", "N", n, n, n, ALPHA, A[0], A[1], n, B[0], B[1], n, BETA, ch, cl, n) == 0
+    for mode in ("exact", "fast", "twosum"):
+        c = dev(n, n, C)
+        Rgemm("N", "N", n, n, n, 1.5, dev(n, n, A), n, dev(n, n, B), n, 0.5, c, n, mode=mode)
+        gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+        if mode == "exact":
+            assert bits_equal(gh, ch) and bits_equal(gl, cl)
+        else:
+            I = J = list(range(0, n, 17))
+            vals, scales = exact.exact_entries("N", "N", n, ALPHA, A[0], A[1], n, B[0], B[1], n,
+                                               BETA, C[0], C[1], n, I, J)
+            assert exact.error_ratios(gh, gl, n, I, J, vals, scales, n) < 1e-2
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+def test_config2_rgemm_4096_all_trans(ta, tb):
+    n = k = m = 4096
+    A = random_dd(m if ta == "N" else k, k if ta == "N" else m, None, 2, 1)
+    B = random_dd(k if tb == "N" else n, n if tb == "N" else k, None, 2, 2)
+    C = random_dd(m, n, m, 2, 3)
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    a, b = dev(nra, nca, A), dev(nrb, ncb, B)
+    I = [0, 1, 777, 2048, 4095]
+    J = [0, 63, 64, 3001, 4095]
+    ref = oracle_entries(ta, tb, m, n, k, A, B, C, I, J)
+    vals, scales = exact.exact_entries(ta, tb, k, ALPHA, A[0], A[1], nra, B[0], B[1], nrb,
+                                       BETA, C[0], C[1], m, I, J)
+    for mode in ("exact", "fast"):
+        c = dev(m, n, C)
+        Rgemm(ta, tb, m, n, k, 1.5, a, nra, b, nrb, 0.5, c, m, mode=mode)
+        got = gather((c.store[0].cpu().numpy(), c.store[1].cpu().numpy()), m, I, J)
+        if mode == "exact":
+            assert _lib.last_route() in (-1, 0)
+            assert bits_equal(got[0], ref[0]) and bits_equal(got[1], ref[1])
+        else:
+            full = (c.store[0].cpu().numpy(), c.store[1].cpu().numpy())
+            assert exact.error_ratios(full[0], full[1], m, I, J, vals, scales, k) < 1e-2
+
+
+@pytest.mark.parametrize("uplo", ["U", "L"])
+@pytest.mark.parametrize("trans", ["N", "T"])
+def test_config3_rsyrk_4096(uplo, trans):
+    n = k = 4096
+    A = random_dd(n, k, n, 3, 1)
+    C = random_dd(n, n, n, 3, 3)
+    a = dev(n, k, A)
+    I = [0, 5, 1000, 2047, 4095]
+    # Rsyrk N == NT Rgemm with B = A, T == TN with B = A (level23.py:250-270)
+    ta, tb = ("N", "T") if trans == "N" else ("T", "N")
+    ref = oracle_entries(ta, tb, n, n, k, A, A, C, I, I)
+    vals, scales = exact.exact_entries(ta, tb, k, ALPHA, A[0], A[1], n, A[0], A[1], n,
+                                       BETA, C[0], C[1], n, I, I)
+    inside = np.array([[(i <= j) if uplo == "U" else (i >= j) for i in I] for j in I]).reshape(-1)
+    for mode in ("exact", "fast"):
+        c = dev(n, n, C)
+        Rsyrk(uplo, trans, n, k, 1.5, a, n, 0.5, c, n, mode=mode)
+        full = (c.store[0].cpu().numpy(), c.store[1].cpu().numpy())
+        got = gather(full, n, I, I)
+        orig = gather(C, n, I, I)
+        assert bits_equal(got[0][~inside], orig[0][~inside])   # other triangle untouched
+        if mode == "exact":
+            assert bits_equal(got[0][inside], ref[0][inside])
+            assert bits_equal(got[1][inside], ref[1][inside])
+        else:
+            for x, i in enumerate(I):
+                for y, j in enumerate(I):
+                    if (i <= j) if uplo == "U" else (i >= j):
+                        r = exact.error_ratios(full[0], full[1], n, [i], [j], [[vals[x][y]]],
+                                               [[scales[x][y]]], k)
+                        assert r < 1e-2
+
+
+def test_config4_deep_k_2048_65536():
+    m = n = 2048
+    k = 65536
+    A, B, C = random_dd(m, k, m, 4, 1), random_dd(k, n, k, 4, 2), random_dd(m, n, m, 4, 3)
+    a, b = dev(m, k, A), dev(k, n, B)
+    I, J = [0, 1023, 2047], [0, 1500, 2047]
+    ref = oracle_entries("N", "N", m, n, k, A, B, C, I, J)
+    vals, scales = exact.exact_entries("N", "N", k, ALPHA, A[0], A[1], m, B[0], B[1], k,
+                                       BETA, C[0], C[1], m, I, J)
+    for mode in ("exact", "fast", "twosum"):
+        c = dev(m, n, C)
+        Rgemm("N", "N", m, n, k, 1.5, a, m, b, k, 0.5, c, m, mode=mode)
+        full = (c.store[0].cpu().numpy(), c.store[1].cpu().numpy())
+        if mode == "exact":
+            got = gather(full, m, I, J)
+            assert bits_equal(got[0], ref[0]) and bits_equal(got[1], ref[1])
+        else:
+            assert exact.error_ratios(full[0], full[1], m, I, J, vals, scales, k) < 1e-2
+
+
+def test_config5_n32768_single_gpu_fast():
+    """configs[4] shape (n = 32768; 48 GiB of operands) on one B200, fast mode,
+    counter-based operands generated on the GPU, sampled exact check."""
+    import torch
+    n = 32768
+    free, _ = torch.cuda.mem_get_info()
+    if free < 64 * 2 ** 30:
+        pytest.skip("needs ~60 GiB of free HBM")
+    mats = [DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 5, t, "cuda")) for t in (1, 2, 3)]
+    I = J = [0, 4097, 32767]
+    # host copies of the sampled rows of A, columns of B, and C(I, J)
+    ks = np.arange(n)
+    Arows = [hashed_entries(5, 1, np.full(n, i), ks) for i in I]
+    Bcols = [hashed_entries(5, 2, ks, np.full(n, j)) for j in J]
+    Cij = hashed_entries(5, 3, np.repeat(I, len(J)), np.tile(J, len(I)))
+    Ah = np.zeros(len(I) * n); Al = np.zeros(len(I) * n)
+    for x, (h, l) in enumerate(Arows):          # |I| x n column-major
+        Ah[x::len(I)] = h
+        Al[x::len(I)] = l
+    Bh = np.concatenate([h for h, _ in Bcols]); Bl = np.concatenate([l for _, l in Bcols])
+    Ch = np.zeros(len(I) * len(J)); Cl = np.zeros(len(I) * len(J))
+    for x in range(len(I)):
+        for y in range(len(J)):
+            Ch[x + y * len(I)] = Cij[0][x * len(J) + y]
+            Cl[x + y * len(I)] = Cij[1][x * len(J) + y]
+    II = list(range(len(I)))
+    vals, scales = exact.exact_entries("N", "N", n, ALPHA, Ah, Al, len(I), Bh, Bl, n,
+                                       BETA, Ch, Cl, len(I), II, II)
+    Rgemm("N", "N", n, n, n, 1.5, mats[0], n, mats[1], n, 0.5, mats[2], n, mode="fast")
+    torch.cuda.synchronize()
+    idx = torch.tensor([i + j * n for j in J for i in I], device="cuda")
+    gh = mats[2].store[0][idx].cpu().numpy()
+    gl = mats[2].store[1][idx].cpu().numpy()
+    assert exact.error_ratios(gh, gl, len(I), II, II, vals, scales, n) < 1e-2
+
+
+def test_hashed_operands_device_equals_host():
+    h, l = hashed_dd_device(100, 50, 5, 2, "cuda", chunk_cols=16)
+    ii = np.arange(100 * 50) % 100
+    jj = np.arange(100 * 50) // 100
+    eh, el = hashed_entries(5, 2, ii, jj)
+    assert bits_equal(h.cpu().numpy(), eh) and bits_equal(l.cpu().numpy(), el)
