@@ -17,6 +17,11 @@ from paper_2109_13406_b200.synth import hashed_dd_device, hashed_entries, random
 pytestmark = pytest.mark.gpu
 
 ALPHA, BETA = (1.5, 0.0), (0.5, 0.0)
+# Error / bound ceilings asserted for the fast modes.  The contract is 1.0
+# (c = 4 in c*k*2^-104*sum|ab|); the certified-anchor mode typically sits at
+# 1e-3 .. 3e-2 of it (its error scales with sum|ab| rather than |running sum|),
+# TwoSum at ~1e-5.  0.25 keeps a 4x margin under the contract.
+FAST_TOL = 0.25
 
 
 def bits_equal(a, b):
@@ -79,7 +84,7 @@ def test_config1_rgemm_nn_256_full_bitwise():
             I = J = list(range(0, n, 17))
             vals, scales = exact.exact_entries("N", "N", n, ALPHA, A[0], A[1], n, B[0], B[1], n,
                                                BETA, C[0], C[1], n, I, J)
-            assert exact.error_ratios(gh, gl, n, I, J, vals, scales, n) < 1e-2
+            assert exact.error_ratios(gh, gl, n, I, J, vals, scales, n) < FAST_TOL
 
 
 @pytest.mark.parametrize("ta,tb", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
@@ -105,7 +110,7 @@ def test_config2_rgemm_4096_all_trans(ta, tb):
             assert bits_equal(got[0], ref[0]) and bits_equal(got[1], ref[1])
         else:
             full = (c.store[0].cpu().numpy(), c.store[1].cpu().numpy())
-            assert exact.error_ratios(full[0], full[1], m, I, J, vals, scales, k) < 1e-2
+            assert exact.error_ratios(full[0], full[1], m, I, J, vals, scales, k) < FAST_TOL
 
 
 @pytest.mark.parametrize("uplo", ["U", "L"])
@@ -138,7 +143,7 @@ def test_config3_rsyrk_4096(uplo, trans):
                     if (i <= j) if uplo == "U" else (i >= j):
                         r = exact.error_ratios(full[0], full[1], n, [i], [j], [[vals[x][y]]],
                                                [[scales[x][y]]], k)
-                        assert r < 1e-2
+                        assert r < FAST_TOL
 
 
 def test_config4_deep_k_2048_65536():
@@ -158,7 +163,7 @@ def test_config4_deep_k_2048_65536():
             got = gather(full, m, I, J)
             assert bits_equal(got[0], ref[0]) and bits_equal(got[1], ref[1])
         else:
-            assert exact.error_ratios(full[0], full[1], m, I, J, vals, scales, k) < 1e-2
+            assert exact.error_ratios(full[0], full[1], m, I, J, vals, scales, k) < FAST_TOL
 
 
 def test_config5_n32768_single_gpu_fast():
@@ -194,7 +199,7 @@ def test_config5_n32768_single_gpu_fast():
     idx = torch.tensor([i + j * n for j in J for i in I], device="cuda")
     gh = mats[2].store[0][idx].cpu().numpy()
     gl = mats[2].store[1][idx].cpu().numpy()
-    assert exact.error_ratios(gh, gl, len(I), II, II, vals, scales, n) < 1e-2
+    assert exact.error_ratios(gh, gl, len(I), II, II, vals, scales, n) < FAST_TOL
 
 
 def test_hashed_operands_device_equals_host():
