@@ -3,9 +3,11 @@
 The partition is the reference's own thread decomposition lifted to GPUs:
 ``Rgemm_par`` splits C into contiguous column panels and runs the sequential
 kernel on each (``/root/reference/pkg/src/mpkit/mpblas/parallel.py:102-157``,
-``_chunks`` :37-47).  Every C(i, j) still sees exactly the same sequence of dd
-operations, so the P-GPU result is bitwise equal to the 1-GPU result in every
-mode (the reference pins this for threads: test_acceptance.py:431-468).
+``_chunks`` :37-47).  In exact mode every C(i, j) still sees exactly the same
+sequence of dd operations, so the P-GPU result is bitwise equal to the 1-GPU
+result (the reference pins this for threads: test_acceptance.py:431-468); the
+fast modes keep their error bound under any split but may differ in the last
+bits (the bound GEMM and the split-K choice depend on the slab shape).
 
 Data movement (operands start on rank 0, the root, and C ends there):
 
@@ -112,7 +114,8 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
 
     On the root, ``a``/``b``/``c`` are the full operands (leading dimensions
     tight: lda = rows); on the other ranks they are ignored (None).  Returns
-    nothing; on the root C holds the result, bitwise equal to ``Rgemm``."""
+    nothing; on the root C holds the result (bitwise equal to ``Rgemm`` in
+    exact mode)."""
     ops = _Ops(group)
     compute = functools.partial(Rgemm, _check_storage=False) if compute is None else compute
     m, n, k = plan.m, plan.n, plan.k
@@ -192,7 +195,8 @@ def rsyrk_columns(n, k, world, rank, device, uplo, trans, alpha, a, beta, c, mod
     """Rsyrk with the uplo triangle split into triangle-balanced column slabs.
 
     Root holds A (lda = rows) and C (ldc = n); the result lands in the root's
-    C, bitwise equal to ``Rsyrk``; the opposite triangle is never changed."""
+    C (bitwise equal to ``Rsyrk`` in exact mode); the opposite triangle is
+    never changed."""
     ops = _Ops(group)
     gemm = functools.partial(Rgemm, _check_storage=False) if compute_gemm is None else compute_gemm
     syrk = functools.partial(Rsyrk, _check_storage=False) if compute_syrk is None else compute_syrk
