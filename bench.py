@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--n", type=int, default=8192)
     p.add_argument("--mode", default="fast", choices=["fast", "exact", "twosum"])
     p.add_argument("--quick", action="store_true", help="skip the secondary measurements")
+    p.add_argument("--force-dist", action="store_true",
+                   help="use the distributed (NCCL) path even with one rank (testing)")
     return p.parse_args()
 
 
@@ -210,8 +212,12 @@ def run_ours(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    distributed = world > 1
+    distributed = world > 1 or args.force_dist
     if distributed:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     n = k = args.n
     mode = args.mode

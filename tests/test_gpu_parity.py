@@ -308,3 +308,15 @@ def test_fast_split_k_rsyrk_triangle_only(uplo):
         for y, j in enumerate(I):
             if (i <= j) if uplo == "U" else (i >= j):
                 assert exact.error_ratios(gh, gl, n, [i], [j], [[vals[x][y]]], [[scales[x][y]]], k) < 0.25
+
+
+def test_nccl_path_single_rank_selftest():
+    """The NCCL code path of parallel.py (broadcast, P2P slabs, gather) on one
+    rank, bit-exact against the single-GPU routines (scripts/dist_selftest.py)."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(repo, "scripts", "dist_selftest.py")],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr[-2000:]
+    assert "MISMATCH" not in out.stdout and out.stdout.count("OK") == 5
