@@ -36,11 +36,14 @@ int alg_for_mode(int mode) {
   }
 }
 
-// tile configuration: 0 = 128 x 64 tiles, 1 CTA / SM; 1 = 64 x 64, 2 CTAs / SM
+// tile configuration: 0 = 128 x 64 tiles, 8 warps / SM; 1 = 64 x 64, 2 CTAs / SM;
+// 2 = 128 x 64 with 512 threads (4 x 4 micro-tiles), 16 warps / SM
 static int tile_cfg() {
   static const int cfg = [] {
     const char* v = std::getenv("DDB_TILE");
-    return (v != nullptr && !std::strcmp(v, "small")) ? 1 : 0;
+    if (v != nullptr && !std::strcmp(v, "small")) return 1;
+    if (v != nullptr && !std::strcmp(v, "wide")) return 2;
+    return 0;
   }();
   return cfg;
 }

@@ -52,19 +52,23 @@ namespace ddb {
 
 namespace tiled {
 
-// Tile configuration: 16 x 16 threads, each owning a TM x TN micro-tile
-// (TM, TN even); MINB CTAs resident per SM (register budget 65536/(256*MINB)).
-template <int TM_, int TN_, int MINB_>
+// Tile configuration: NT threads as NX (along m) x NT/NX (along n), each
+// owning a TM x TN micro-tile (TM, TN even) at rows g*2NX + tx*2 + q and
+// columns g*2NY + ty*2 + q; MINB CTAs per SM (registers 65536/(NT*MINB)).
+// PF: double-buffer the next k-step's operands in registers.
+template <int TM_, int TN_, int MINB_, int NT_ = 256, int NX_ = 16, int PF_ = 1>
 struct Cfg {
-  static constexpr int TM = TM_, TN = TN_, MINB = MINB_;
-  static constexpr int BM = 16 * TM, BN = 16 * TN, BK = 16, NT = 256, STAGES = 3;
+  static constexpr int TM = TM_, TN = TN_, MINB = MINB_, NT = NT_, NX = NX_, NY = NT_ / NX_;
+  static constexpr int PF = PF_;
+  static constexpr int BM = NX * TM, BN = NY * TN, BK = 16, STAGES = 3;
   static constexpr int ASTR = BM + 2, BSTR = BN + 2;   // smem row strides (doubles)
   static constexpr int A_STAGE = 2 * BK * ASTR, B_STAGE = 2 * BK * BSTR;
   static constexpr size_t SMEM_BYTES =
       (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + (BM + BN) * sizeof(int);
 };
-using CfgBig = Cfg<8, 4, 1>;     // 128 x 64 tile, 1 CTA / SM
-using CfgSmall = Cfg<4, 4, 2>;   // 64 x 64 tile, 2 CTAs / SM
+using CfgBig = Cfg<8, 4, 1>;                 // 128 x 64 tile, 8 warps / SM
+using CfgSmall = Cfg<4, 4, 2, 256, 16, 0>;   // 64 x 64 tile, 2 CTAs: 16 warps / SM
+using CfgWide = Cfg<4, 4, 1, 512, 32, 0>;    // 128 x 64 tile, 16 warps / SM
 
 constexpr int BK = 16;
 #ifndef DDB_PHASE
@@ -219,6 +223,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB)
 dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restrict__ col_exp,
                 const int* __restrict__ flag, int tiles_m, int tiles_n) {
   constexpr int TM = C::TM, TN = C::TN, BM = C::BM, BN = C::BN, NT = C::NT;
+  constexpr int RX = 2 * C::NX, RY = 2 * C::NY;   // row / column group strides
   constexpr int STAGES = C::STAGES, ASTR = C::ASTR, BSTR = C::BSTR;
   constexpr int A_STAGE = C::A_STAGE, B_STAGE = C::B_STAGE;
   if (*flag != ROUTE_SAFE) return;  // dd_reference.cu handles this call
@@ -241,7 +246,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   int* sColExp = sRowExp + BM;
 
   const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
+  const int tx = tid % C::NX, ty = tid / C::NX;
 
   double H[TM][TN], L[TM][TN];   // exact: (c_h, c_l); twosum/select: (S, L); anchor: (T, L)
 
@@ -260,7 +265,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     for (int a = 0; a < TM; ++a)
 #pragma unroll
       for (int b = 0; b < TN; ++b) {
-        const int ri = (a >> 1) * 32 + tx * 2 + (a & 1), cj = (b >> 1) * 32 + ty * 2 + (b & 1);
+        const int ri = (a >> 1) * RX + tx * 2 + (a & 1), cj = (b >> 1) * RY + ty * 2 + (b & 1);
         const int64_t gi = i0 + ri, gj = j0 + cj;
         const float sb = (gi < g.m && gj < g.n) ? g.bound[gi + gj * g.m] : 0.f;
         // Sigma' = sd * 2^(rowexp + colexp - 2044), sd < 2^(es - 1022);
@@ -278,8 +283,8 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
         H[a][b] = 0.0;
         L[a][b] = 0.0;
         if (ALG == ALG_EXACT && TA == 0) {  // axpy form: start from beta-scaled C
-          const int64_t gi = i0 + (a >> 1) * 32 + tx * 2 + (a & 1);
-          const int64_t gj = j0 + (b >> 1) * 32 + ty * 2 + (b & 1);
+          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
           if (gi < g.m && gj < g.n) {
             const dd c = scale_beta(g.beta, dd{g.c_hi[gi + gj * g.ldc], g.c_lo[gi + gj * g.ldc]});
             H[a][b] = c.h;
@@ -337,15 +342,15 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
                         double (&bl)[TN]) {
 #pragma unroll
       for (int gq = 0; gq < TM / 2; ++gq) {
-        const double2 vh = *reinterpret_cast<const double2*>(a_h + kk * ASTR + gq * 32 + tx * 2);
-        const double2 vl = *reinterpret_cast<const double2*>(a_l + kk * ASTR + gq * 32 + tx * 2);
+        const double2 vh = *reinterpret_cast<const double2*>(a_h + kk * ASTR + gq * RX + tx * 2);
+        const double2 vl = *reinterpret_cast<const double2*>(a_l + kk * ASTR + gq * RX + tx * 2);
         ah[2 * gq] = vh.x; ah[2 * gq + 1] = vh.y;
         al[2 * gq] = vl.x; al[2 * gq + 1] = vl.y;
       }
 #pragma unroll
       for (int gq = 0; gq < TN / 2; ++gq) {
-        const double2 vh = *reinterpret_cast<const double2*>(b_h + kk * BSTR + gq * 32 + ty * 2);
-        const double2 vl = *reinterpret_cast<const double2*>(b_l + kk * BSTR + gq * 32 + ty * 2);
+        const double2 vh = *reinterpret_cast<const double2*>(b_h + kk * BSTR + gq * RY + ty * 2);
+        const double2 vl = *reinterpret_cast<const double2*>(b_l + kk * BSTR + gq * RY + ty * 2);
         bh[2 * gq] = vh.x; bh[2 * gq + 1] = vh.y;
         bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
       }
@@ -383,10 +388,10 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       // fast modes: the whole k-tile unrolled (kcount == BK), renormalisation
       // / folding placed at compile time, operands double-buffered in registers
       double ah[2][TM], al[2][TM], bh[2][TN], bl[2][TN];
-      if (DDB_PREFETCH) load_ops(0, ah[0], al[0], bh[0], bl[0]);
+      if (DDB_PREFETCH && C::PF) load_ops(0, ah[0], al[0], bh[0], bl[0]);
 #pragma unroll
       for (int kk = 0; kk < BK; ++kk) {
-        if (DDB_PREFETCH) {
+        if (DDB_PREFETCH && C::PF) {
           if (kk + 1 < BK) load_ops(kk + 1, ah[(kk + 1) & 1], al[(kk + 1) & 1], bh[(kk + 1) & 1], bl[(kk + 1) & 1]);
           mac_step<ALG, TM, TN>(H, L, ah[kk & 1], al[kk & 1], bh[kk & 1], bl[kk & 1]);
         } else {
@@ -405,8 +410,8 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   for (int a = 0; a < TM; ++a)
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
-      const int64_t gi = i0 + (a >> 1) * 32 + tx * 2 + (a & 1);
-      const int64_t gj = j0 + (b >> 1) * 32 + ty * 2 + (b & 1);
+      const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+      const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
       if (gi >= g.m || gj >= g.n) continue;
       if (SYRK == 1 && gi > gj) continue;
       if (SYRK == 2 && gi < gj) continue;

@@ -1,0 +1,87 @@
+// cert_mix.cu -- ceiling of the fast mode's instruction mix on the FP64
+// pipe: the certified-anchor MAC step (6 FP64 ops) + a 3-op fold every 2
+// steps on a TM x TN register micro-tile, operands from registers (no smem),
+// at 256 threads x MINB CTAs per SM.
+#include <cstdio>
+#include <cuda_runtime.h>
+
+template <int TM, int TN, int MINB>
+__global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double s0) {
+  double T[TM][TN], L[TM][TN], ah[TM], al[TM], bh[TN], bl[TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i) { ah[i] = 1.0 + i * 1e-3 + threadIdx.x * 1e-7; al[i] = ah[i] * 1e-17; }
+#pragma unroll
+  for (int j = 0; j < TN; ++j) { bh[j] = 0.5 + j * 1e-3; bl[j] = bh[j] * 1e-17; }
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) { T[i][j] = s0; L[i][j] = 0.0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+          const double t = T[i][j];
+          const double tn = __fma_rn(ah[i], bh[j], t);
+          const double r = __fma_rn(ah[i], bh[j], __dsub_rn(t, tn));
+          double l = __fma_rn(ah[i], bl[j], L[i][j]);
+          l = __fma_rn(al[i], bh[j], l);
+          L[i][j] = __dadd_rn(l, r);
+          T[i][j] = tn;
+        }
+      if (kk & 1) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            const double t2 = __dadd_rn(T[i][j], L[i][j]);
+            L[i][j] = __dsub_rn(L[i][j], __dsub_rn(t2, T[i][j]));
+            T[i][j] = t2;
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < TM; ++i) ah[i] = -ah[i];   // keep the sum bounded
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) s += T[i][j] + L[i][j];
+  if (s == 12345.0) out[0] = s;
+}
+
+template <int TM, int TN, int MINB>
+void run(int sms, double* out) {
+  const int iters = 400;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0);
+    mix<TM, TN, MINB><<<sms * MINB, 256>>>(out, iters, 1.5 * 1024);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  const double dp = (double)sms * MINB * 256 * iters * 16 * TM * TN * 7.5;
+  printf("%dx%d micro-tile, %d CTA/SM: %.1f%% of DP peak\n", TM, TN, MINB,
+         dp / (best * 1e-3) / ((double)sms * 64 * 1.965e9) * 100);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out;
+  cudaMalloc(&out, 8);
+  run<8, 4, 1>(sms, out);
+  run<4, 4, 2>(sms, out);
+  run<4, 2, 3>(sms, out);
+  run<2, 2, 4>(sms, out);
+  return 0;
+}
