@@ -74,6 +74,11 @@ constexpr int BK = 16;
 #ifndef DDB_PHASE
 #define DDB_PHASE 0      // phase-ordered CERT MAC step (experiment switch)
 #endif
+#ifndef DDB_ABLATE
+#define DDB_ABLATE 0     // measurement-only ablations (wrong results): 1 = operands of
+                         // step 0 reused for the whole k-tile, 2 = skip the k-tile
+                         // loads + barrier after the first tile
+#endif
 #ifndef DDB_PREFETCH
 #define DDB_PREFETCH 1   // fast modes: load step kk+1's operands before step kk's math
 #endif
@@ -305,9 +310,11 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   }
 
   for (int kt = 0; kt < ktiles; ++kt) {
+    if (DDB_ABLATE != 2 || kt == 0) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
+    }
+    if (DDB_ABLATE != 2 || kt == 0) {
       const int nk = kt + STAGES - 1;
       const int ns = nk % STAGES;
       if (nk < ktiles) load_stage<C, TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, kbeg + (int64_t)nk * BK, kend, tid);
@@ -391,7 +398,9 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       if (DDB_PREFETCH && C::PF) load_ops(0, ah[0], al[0], bh[0], bl[0]);
 #pragma unroll
       for (int kk = 0; kk < BK; ++kk) {
-        if (DDB_PREFETCH && C::PF) {
+        if (DDB_ABLATE == 1) {
+          mac_step<ALG, TM, TN>(H, L, ah[0], al[0], bh[0], bl[0]);
+        } else if (DDB_PREFETCH && C::PF) {
           if (kk + 1 < BK) load_ops(kk + 1, ah[(kk + 1) & 1], al[(kk + 1) & 1], bh[(kk + 1) & 1], bl[(kk + 1) & 1]);
           mac_step<ALG, TM, TN>(H, L, ah[kk & 1], al[kk & 1], bh[kk & 1], bl[kk & 1]);
         } else {
