@@ -392,22 +392,26 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
 #pragma unroll 1
       for (int kk = 0; kk < kcount; ++kk) k_step(kk);
     } else {
-      // fast modes: the whole k-tile unrolled (kcount == BK), renormalisation
-      // / folding placed at compile time, operands double-buffered in registers
-      double ah[2][TM], al[2][TM], bh[2][TN], bl[2][TN];
-      if (DDB_PREFETCH && C::PF) load_ops(0, ah[0], al[0], bh[0], bl[0]);
-#pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        if (DDB_ABLATE == 1) {
-          mac_step<ALG, TM, TN>(H, L, ah[0], al[0], bh[0], bl[0]);
-        } else if (DDB_PREFETCH && C::PF) {
-          if (kk + 1 < BK) load_ops(kk + 1, ah[(kk + 1) & 1], al[(kk + 1) & 1], bh[(kk + 1) & 1], bl[(kk + 1) & 1]);
-          mac_step<ALG, TM, TN>(H, L, ah[kk & 1], al[kk & 1], bh[kk & 1], bl[kk & 1]);
+      // fast modes: the k-tile runs as BK/2 iterations of a 2-step body.
+      // Unrolling the whole 16-step tile (~66 KB of SASS for the 8 x 4 tile)
+      // overflows the instruction cache: measured 63 % of the FP64 pipe vs
+      // 99 % for a 2- or 4-step body (scripts/cert_mix.cu).  Operands are
+      // double-buffered in registers across the two steps; CERT folds every 2
+      // steps, TWOSUM renormalises every RN = 8.
+#pragma unroll 1
+      for (int kk = 0; kk < BK; kk += 2) {
+        if (C::PF) {   // both steps' operands loaded up front (nothing live across the back-edge)
+          double ah0[TM], al0[TM], bh0[TN], bl0[TN], ah1[TM], al1[TM], bh1[TN], bl1[TN];
+          load_ops(kk, ah0, al0, bh0, bl0);
+          load_ops(kk + 1, ah1, al1, bh1, bl1);
+          mac_step<ALG, TM, TN>(H, L, ah0, al0, bh0, bl0);
+          mac_step<ALG, TM, TN>(H, L, ah1, al1, bh1, bl1);
         } else {
           k_step(kk);
+          k_step(kk + 1);
         }
-        if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && (kk % RN) == RN - 1) renorm();
-        if (ALG == ALG_CERT && (kk % RF) == RF - 1) fold();
+        if (ALG == ALG_CERT) fold();
+        if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && ((kk + 2) % RN) == 0) renorm();
       }
     }
 

@@ -5,7 +5,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int TM, int TN, int MINB>
+template <int TM, int TN, int MINB, int UNR>
 __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double s0) {
   double T[TM][TN], L[TM][TN], ah[TM], al[TM], bh[TN], bl[TN];
 #pragma unroll
@@ -16,9 +16,9 @@ __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double 
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) { T[i][j] = s0; L[i][j] = 0.0; }
-  for (int it = 0; it < iters; ++it) {
+  for (int it = 0; it < iters * (16 / UNR); ++it) {
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
+    for (int kk = 0; kk < UNR; ++kk) {
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double 
   if (s == 12345.0) out[0] = s;
 }
 
-template <int TM, int TN, int MINB>
+template <int TM, int TN, int MINB, int UNR = 16>
 void run(int sms, double* out) {
   const int iters = 400;
   cudaEvent_t e0, e1;
@@ -62,7 +62,7 @@ void run(int sms, double* out) {
   float best = 1e30f;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    mix<TM, TN, MINB><<<sms * MINB, 256>>>(out, iters, 1.5 * 1024);
+    mix<TM, TN, MINB, UNR><<<sms * MINB, 256>>>(out, iters, 1.5 * 1024);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -70,7 +70,7 @@ void run(int sms, double* out) {
     if (ms < best) best = ms;
   }
   const double dp = (double)sms * MINB * 256 * iters * 16 * TM * TN * 7.5;
-  printf("%dx%d micro-tile, %d CTA/SM: %.1f%% of DP peak\n", TM, TN, MINB,
+  printf("%dx%d micro-tile, %d CTA/SM, unroll %d: %.1f%% of DP peak\n", TM, TN, MINB, UNR,
          dp / (best * 1e-3) / ((double)sms * 64 * 1.965e9) * 100);
 }
 
@@ -80,7 +80,10 @@ int main() {
   double* out;
   cudaMalloc(&out, 8);
   run<8, 4, 1>(sms, out);
+  run<8, 4, 1, 2>(sms, out);
+  run<8, 4, 1, 4>(sms, out);
   run<4, 4, 2>(sms, out);
+  run<4, 4, 2, 2>(sms, out);
   run<4, 2, 3>(sms, out);
   run<2, 2, 4>(sms, out);
   return 0;
