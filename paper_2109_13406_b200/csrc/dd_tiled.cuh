@@ -79,6 +79,9 @@ constexpr int BK = 16;
                          // step 0 reused for the whole k-tile, 2 = skip the k-tile
                          // loads + barrier after the first tile
 #endif
+#ifndef DDB_UNR
+#define DDB_UNR 16       // fast modes: k-steps per loop body (divides BK, multiple of RF)
+#endif
 #ifndef DDB_PREFETCH
 #define DDB_PREFETCH 1   // fast modes: load step kk+1's operands before step kk's math
 #endif
@@ -399,19 +402,27 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       // double-buffered in registers across the two steps; CERT folds every 2
       // steps, TWOSUM renormalises every RN = 8.
 #pragma unroll 1
-      for (int kk = 0; kk < BK; kk += 2) {
-        if (C::PF) {   // both steps' operands loaded up front (nothing live across the back-edge)
-          double ah0[TM], al0[TM], bh0[TN], bl0[TN], ah1[TM], al1[TM], bh1[TN], bl1[TN];
-          load_ops(kk, ah0, al0, bh0, bl0);
-          load_ops(kk + 1, ah1, al1, bh1, bl1);
-          mac_step<ALG, TM, TN>(H, L, ah0, al0, bh0, bl0);
-          mac_step<ALG, TM, TN>(H, L, ah1, al1, bh1, bl1);
+      for (int kk = 0; kk < BK; kk += DDB_UNR) {
+        if (C::PF) {   // step j+1's operands load while step j computes; nothing
+                       // stays live across the back-edge but H and L
+          double ah[2][TM], al[2][TM], bh[2][TN], bl[2][TN];
+          load_ops(kk, ah[0], al[0], bh[0], bl[0]);
+#pragma unroll
+          for (int j = 0; j < DDB_UNR; ++j) {
+            if (j + 1 < DDB_UNR)
+              load_ops(kk + j + 1, ah[(j + 1) & 1], al[(j + 1) & 1], bh[(j + 1) & 1], bl[(j + 1) & 1]);
+            mac_step<ALG, TM, TN>(H, L, ah[j & 1], al[j & 1], bh[j & 1], bl[j & 1]);
+            if (ALG == ALG_CERT && (j % RF) == RF - 1) fold();
+            if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && ((kk + j + 1) % RN) == 0) renorm();
+          }
         } else {
-          k_step(kk);
-          k_step(kk + 1);
+#pragma unroll
+          for (int j = 0; j < DDB_UNR; ++j) {
+            k_step(kk + j);
+            if (ALG == ALG_CERT && (j % RF) == RF - 1) fold();
+            if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && ((kk + j + 1) % RN) == 0) renorm();
+          }
         }
-        if (ALG == ALG_CERT) fold();
-        if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && ((kk + 2) % RN) == 0) renorm();
       }
     }
 
