@@ -84,6 +84,20 @@ int ddb_rsyrk_host(char uplo, char trans, int64_t n, int64_t k,
                    double* c_hi, double* c_lo, int64_t ldc,
                    int mode, void* stream);
 
+/* Binary64 precision (the reference's 'f64' Matrix, one plane per matrix):
+ * the same routines over the reference's F64 backend (elem.py:149-197),
+ * bit-identical for every input.  Same argument indices and early exits. */
+int ddb_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+              double* c, int64_t ldc, void* stream);
+int ddb_dsyrk(char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
+              int64_t lda, double beta, double* c, int64_t ldc, void* stream);
+int ddb_dgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                   const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                   double* c, int64_t ldc, void* stream);
+int ddb_dsyrk_host(char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
+                   int64_t lda, double beta, double* c, int64_t ldc, void* stream);
+
 /* Argument checks alone (no device work): reference index or 0. */
 int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
                        int64_t lda, int64_t ldb, int64_t ldc);
@@ -94,7 +108,8 @@ int ddb_version(void);
 /* Number of kernels this library has launched in this process. */
 long long ddb_launch_count(void);
 /* Route of this thread's last call when DDB_DEBUG_SYNC=1 (0 exact tiled,
- * 1 fast tiled, 2 reference-semantics kernel, 3 twosum tiled), else -1. */
+ * 1 fast tiled, 2 reference-semantics kernel, 3 twosum tiled, 4 f64 tiled),
+ * else -1. */
 int ddb_last_route(void);
 
 /* Diagnostic: FP64 FMA throughput of the current GPU in FLOP/s (FMA = 2),

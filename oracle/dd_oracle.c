@@ -343,6 +343,71 @@ int oracle_rsyrk(char uplo, char trans, int64_t n, int64_t k,
     return run_columns(syrk_col, &x, n, k, n, nthreads);
 }
 
+/* ---- binary64 precision: the same routines over the reference's F64
+ * backend (elem.py:149-197: add / mul are plain numpy float64 ops), same loop
+ * orders (level23.py:107-177, :226-285).  Single-threaded (test use). */
+
+static inline double f64_beta_rule(double beta, double c) {       /* _scale_full */
+    if (beta == 0.0) return 0.0;
+    if (beta == 1.0) return c;
+    return beta * c;
+}
+
+int oracle_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, double beta,
+                 double *C, int64_t ldc) {
+    int rc = oracle_gemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+    if (rc) return rc;
+    int ta = upflag(transa), tb = upflag(transb);
+    if (m == 0 || n == 0 || ((alpha == 0.0 || k == 0) && beta == 1.0)) return 0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) {
+            double *c = &C[i + j * ldc];
+            if (alpha == 0.0) { *c = f64_beta_rule(beta, *c); continue; }
+            if (ta == 'N') {
+                double acc = f64_beta_rule(beta, *c);
+                for (int64_t l = 0; l < k; ++l) {
+                    double t = alpha * (tb == 'N' ? B[l + j * ldb] : B[j + l * ldb]);
+                    acc = acc + A[i + l * lda] * t;
+                }
+                *c = acc;
+            } else {
+                double acc = 0.0;
+                for (int64_t l = 0; l < k; ++l)
+                    acc = acc + A[l + i * lda] * (tb == 'N' ? B[l + j * ldb] : B[j + l * ldb]);
+                double at = alpha * acc;
+                *c = beta == 0.0 ? at : at + beta * *c;
+            }
+        }
+    return 0;
+}
+
+int oracle_dsyrk(char uplo, char trans, int64_t n, int64_t k, double alpha, const double *A,
+                 int64_t lda, double beta, double *C, int64_t ldc) {
+    int rc = oracle_syrk_validate(uplo, trans, n, k, lda, ldc);
+    if (rc) return rc;
+    int up = upflag(uplo) == 'U', tn = upflag(trans) == 'N';
+    if (n == 0 || ((alpha == 0.0 || k == 0) && beta == 1.0)) return 0;
+    for (int64_t j = 0; j < n; ++j) {
+        int64_t i0 = up ? 0 : j, i1 = up ? j + 1 : n;
+        for (int64_t i = i0; i < i1; ++i) {
+            double *c = &C[i + j * ldc];
+            if (alpha == 0.0) { *c = f64_beta_rule(beta, *c); continue; }
+            if (tn) {
+                double acc = f64_beta_rule(beta, *c);
+                for (int64_t l = 0; l < k; ++l) acc = acc + A[i + l * lda] * (alpha * A[j + l * lda]);
+                *c = acc;
+            } else {
+                double acc = 0.0;
+                for (int64_t l = 0; l < k; ++l) acc = acc + A[l + i * lda] * A[l + j * lda];
+                double at = alpha * acc;
+                *c = beta == 0.0 ? at : at + beta * *c;
+            }
+        }
+    }
+    return 0;
+}
+
 /* Scalar EFT entry points, for pinning the restatement against the
  * reference's scalar kernels (tests/test_oracle.py). */
 void oracle_add2(double xh, double xl, double yh, double yl, double *out) {

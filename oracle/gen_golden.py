@@ -51,6 +51,7 @@ ALPHAS = {
     "a0": (0.0, 0.0),
 }
 BETAS = {
+    "b05": (0.5, 0.0),
     "b05lo": (0.5, 2.0 ** -58),
     "b1": (1.0, 0.0),
     "b0": (0.0, 0.0),
@@ -96,6 +97,42 @@ def gemm_cases():
     return cases
 
 
+def f64_cases():
+    """The same routines on the reference's binary64 Matrix (F64 backend)."""
+    cases = []
+    seed = 900
+    for ta in ("N", "T", "C"):
+        for tb in ("N", "T", "C"):
+            for bname in ("b05", "b1", "b0"):
+                cases.append(dict(routine="Rgemm", precision="f64", transa=ta, transb=tb, m=13,
+                                  n=11, k=17, pad=(3, 2, 5), alpha="a15", beta=bname, seed=seed))
+                seed += 1
+    for ta, tb in (("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")):
+        cases.append(dict(routine="Rgemm", precision="f64", transa=ta, transb=tb, m=133, n=70,
+                          k=41, pad=(1, 0, 3), alpha="a15", beta="b05", seed=seed)); seed += 1
+    for ta in ("N", "T"):
+        cases.append(dict(routine="Rgemm", precision="f64", transa=ta, transb="N", m=7, n=5, k=6,
+                          pad=(0, 0, 0), alpha="a0", beta="bneg", seed=seed)); seed += 1
+        cases.append(dict(routine="Rgemm", precision="f64", transa=ta, transb="N", m=7, n=5, k=0,
+                          pad=(0, 0, 0), alpha="a15", beta="bneg", seed=seed)); seed += 1
+        for special in ("nan_c_beta0", "inf_a", "huge", "tiny"):
+            cases.append(dict(routine="Rgemm", precision="f64", transa=ta, transb="T", m=9, n=7,
+                              k=10, pad=(1, 1, 1), alpha="aneg",
+                              beta="b0" if special == "nan_c_beta0" else "b05", seed=seed,
+                              special=special)); seed += 1
+    for uplo in ("U", "L"):
+        for trans in ("N", "T", "C"):
+            for bname in ("b05", "b1", "b0"):
+                cases.append(dict(routine="Rsyrk", precision="f64", uplo=uplo, trans=trans, n=13,
+                                  k=9, pad=(2, 0, 3), alpha="a15", beta=bname, seed=seed))
+                seed += 1
+        cases.append(dict(routine="Rsyrk", precision="f64", uplo=uplo, trans="N", n=137, k=33,
+                          pad=(1, 0, 2), alpha="a15", beta="b05", seed=seed)); seed += 1
+        cases.append(dict(routine="Rsyrk", precision="f64", uplo=uplo, trans="T", n=6, k=4,
+                          pad=(0, 0, 0), alpha="a0", beta="bneg", seed=seed)); seed += 1
+    return cases
+
+
 def syrk_cases():
     cases = []
     seed = 500
@@ -127,6 +164,8 @@ def syrk_cases():
 def run_case(mb, DDouble, case, store):
     alpha = ALPHAS[case["alpha"]]
     beta = BETAS[case["beta"]]
+    if case.get("precision") == "f64":
+        return run_case_f64(mb, case, store, alpha[0], beta[0])
     case["alpha_v"] = list(alpha)
     case["beta_v"] = list(beta)
     arrays, lds = case_inputs(case)
@@ -161,6 +200,43 @@ def run_case(mb, DDouble, case, store):
     store["cases"].append(case)
 
 
+def _f64_matrix(mb, m, n, ld, hi):
+    mat = mb.Matrix(m, n, "f64", ld)
+    mat.store = (hi.copy(),)
+    return mat
+
+
+def run_case_f64(mb, case, store, alpha, beta):
+    case["alpha_v"] = [alpha, 0.0]
+    case["beta_v"] = [beta, 0.0]
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    if case["routine"] == "Rgemm":
+        ta, tb = case["transa"].upper(), case["transb"].upper()
+        m, n, k = case["m"], case["n"], case["k"]
+        nra, nca = (m, k) if ta == "N" else (k, m)
+        nrb, ncb = (k, n) if tb == "N" else (n, k)
+        a = _f64_matrix(mb, nra, nca, lds["lda"], arrays["A_hi"])
+        b = _f64_matrix(mb, nrb, ncb, lds["ldb"], arrays["B_hi"])
+        c = _f64_matrix(mb, m, n, lds["ldc"], arrays["C_hi"])
+        with np.errstate(all="ignore"):
+            mb.Rgemm(case["transa"], case["transb"], m, n, k, alpha, a, lds["lda"], b, lds["ldb"],
+                     beta, c, lds["ldc"])
+    else:
+        n, k = case["n"], case["k"]
+        nra, nca = (n, k) if case["trans"].upper() == "N" else (k, n)
+        a = _f64_matrix(mb, nra, nca, lds["lda"], arrays["A_hi"])
+        c = _f64_matrix(mb, n, n, lds["ldc"], arrays["C_hi"])
+        with np.errstate(all="ignore"):
+            mb.Rsyrk(case["uplo"], case["trans"], n, k, alpha, a, lds["lda"], beta, c, lds["ldc"])
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    store["arrays"][f"c{cid}_out_hi"] = np.asarray(c.store[0], dtype=np.float64)
+    store["arrays"][f"c{cid}_out_lo"] = np.zeros(0)
+    store["cases"].append(case)
+
+
 def eft_vectors(elem):
     """Scalar EFT golden vectors through the reference's vectorised kernels."""
     g = np.random.default_rng(np.random.SeedSequence([9, 9, 9]))
@@ -188,7 +264,7 @@ def main():
     mb, elem, DDouble = _ref()
     os.makedirs(OUT, exist_ok=True)
     store = {"cases": [], "arrays": {}}
-    for case in gemm_cases() + syrk_cases():
+    for case in gemm_cases() + syrk_cases() + f64_cases():
         run_case(mb, DDouble, case, store)
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
     with open(os.path.join(OUT, "cases.json"), "w") as f:

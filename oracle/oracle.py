@@ -55,6 +55,12 @@ def lib():
             f.argtypes = [ctypes.c_double] * 4 + [_dp]
         L.oracle_two_prod.restype = None
         L.oracle_two_prod.argtypes = [ctypes.c_double, ctypes.c_double, _dp]
+        L.oracle_dgemm.restype = ctypes.c_int
+        L.oracle_dgemm.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64, _i64, ctypes.c_double,
+                                   _dp, _i64, _dp, _i64, ctypes.c_double, _dp, _i64]
+        L.oracle_dsyrk.restype = ctypes.c_int
+        L.oracle_dsyrk.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64, ctypes.c_double,
+                                   _dp, _i64, ctypes.c_double, _dp, _i64]
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_gemm_validate.restype = ctypes.c_int
         L.oracle_gemm_validate.argtypes = [ctypes.c_char, ctypes.c_char] + [_i64] * 6
@@ -95,6 +101,17 @@ def rsyrk(uplo, trans, n, k, alpha, a_hi, a_lo, lda, beta, c_hi, c_lo, ldc,
                               _ptr(a_hi), _ptr(a_lo), lda,
                               float(beta[0]), float(beta[1]),
                               _ptr(c_hi), _ptr(c_lo), ldc, int(threads))
+
+
+def dgemm(transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc):
+    """binary64 Rgemm with the reference's order (F64 backend)."""
+    return lib().oracle_dgemm(_flag(transa), _flag(transb), m, n, k, float(alpha), _ptr(a), lda,
+                              _ptr(b), ldb, float(beta), _ptr(c), ldc)
+
+
+def dsyrk(uplo, trans, n, k, alpha, a, lda, beta, c, ldc):
+    return lib().oracle_dsyrk(_flag(uplo), _flag(trans), n, k, float(alpha), _ptr(a), lda,
+                              float(beta), _ptr(c), ldc)
 
 
 def add2(x, y):

@@ -23,7 +23,8 @@ _c = ctypes.c_char
 
 EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rgemm_validate", "ddb_rsyrk_validate", "ddb_last_error",
-           "ddb_version", "ddb_launch_count", "ddb_last_route", "ddb_fp64_peak_probe")
+           "ddb_version", "ddb_launch_count", "ddb_last_route", "ddb_fp64_peak_probe",
+           "ddb_dgemm", "ddb_dsyrk", "ddb_dgemm_host", "ddb_dsyrk_host")
 
 _lib = None
 
@@ -48,6 +49,13 @@ def load():
                  ctypes.c_int, _dp]
     for name, args in (("ddb_rgemm", gemm_args), ("ddb_rgemm_host", gemm_args),
                        ("ddb_rsyrk", syrk_args), ("ddb_rsyrk_host", syrk_args)):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = args
+    dgemm_args = [_c, _c, _i64, _i64, _i64, _d, _dp, _i64, _dp, _i64, _d, _dp, _i64, _dp]
+    dsyrk_args = [_c, _c, _i64, _i64, _d, _dp, _i64, _d, _dp, _i64, _dp]
+    for name, args in (("ddb_dgemm", dgemm_args), ("ddb_dgemm_host", dgemm_args),
+                       ("ddb_dsyrk", dsyrk_args), ("ddb_dsyrk_host", dsyrk_args)):
         f = getattr(L, name)
         f.restype = ctypes.c_int
         f.argtypes = args

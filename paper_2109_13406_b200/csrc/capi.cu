@@ -75,6 +75,28 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   int nl = 0;
   cudaError_t e;
   GemmArgs g = g0;
+  if (g.f64) {   // binary64: bit-exact tiled kernel for every input (no window)
+    if (g.alpha.h == 0.0 || g.k == 0 || mode == MODE_REFERENCE) {
+      e = launch_reference(g, nullptr, GATE_ALWAYS, s, &nl);
+      g_launches += nl;
+      if (e != cudaSuccess) return fail(e, "reference kernel launch");
+      g_last_route = 2;
+      return DDB_OK;
+    }
+    retain_pool_memory();
+    void* ws = nullptr;
+    e = cudaMallocAsync(&ws, 256, s);
+    if (e != cudaSuccess) return fail(e, "workspace allocation");
+    e = cudaMemsetAsync(ws, 0, 256, s);
+    g.kchunk = g.k;
+    if (e == cudaSuccess) e = launch_tiled(g, ALG_F64, nullptr, nullptr, static_cast<int*>(ws), s, &nl);
+    g_launches += nl;
+    cudaError_t e2 = cudaFreeAsync(ws, s);
+    if (e != cudaSuccess) return fail(e, "f64 kernel launch");
+    if (e2 != cudaSuccess) return fail(e2, "workspace free");
+    g_last_route = debug_sync() ? 4 : -1;
+    return DDB_OK;
+  }
   const bool trivial_ref = mode == MODE_REFERENCE || is_zero(g.alpha.h, g.alpha.l) || g.k == 0;
   bool scalars_ok = true;
   if (mode == MODE_EXACT)
@@ -229,6 +251,47 @@ int ddb_rsyrk(char uplo, char trans, int64_t n, int64_t k,
   return run(g, mode, static_cast<cudaStream_t>(stream));
 }
 
+// ---- binary64 precision (the reference's 'f64' Matrix) ----------------------
+
+int ddb_dgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+              const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+              double* c, int64_t ldc, void* stream) {
+  const int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  if (m == 0 || n == 0 || ((alpha == 0.0 || k == 0) && beta == 1.0)) return DDB_OK;
+  GemmArgs g{};
+  g.f64 = 1;
+  g.ta = upflag(transa) == 'N' ? 0 : 1;
+  g.tb = upflag(transb) == 'N' ? 0 : 1;
+  g.m = m; g.n = n; g.k = k;
+  g.a_hi = a; g.lda = lda;
+  g.b_hi = b; g.ldb = ldb;
+  g.c_hi = c; g.ldc = ldc;
+  g.alpha = dd{alpha, 0.0};
+  g.beta = dd{beta, 0.0};
+  return run(g, MODE_EXACT, static_cast<cudaStream_t>(stream));
+}
+
+int ddb_dsyrk(char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
+              int64_t lda, double beta, double* c, int64_t ldc, void* stream) {
+  const int rc = ddb_rsyrk_validate(uplo, trans, n, k, lda, ldc);
+  if (rc) return rc;
+  if (n == 0 || ((alpha == 0.0 || k == 0) && beta == 1.0)) return DDB_OK;
+  GemmArgs g{};
+  g.f64 = 1;
+  const bool tn = upflag(trans) == 'N';
+  g.ta = tn ? 0 : 1;
+  g.tb = tn ? 1 : 0;
+  g.syrk = upflag(uplo) == 'U' ? 1 : 2;
+  g.m = n; g.n = n; g.k = k;
+  g.a_hi = a; g.lda = lda;
+  g.b_hi = a; g.ldb = lda;
+  g.c_hi = c; g.ldc = ldc;
+  g.alpha = dd{alpha, 0.0};
+  g.beta = dd{beta, 0.0};
+  return run(g, MODE_EXACT, static_cast<cudaStream_t>(stream));
+}
+
 // ---- host-buffer entry points: stage operands through device memory ----
 
 namespace {
@@ -314,6 +377,62 @@ int ddb_rsyrk_host(char uplo, char trans, int64_t n, int64_t k,
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail(e, "device to host copy");
   return DDB_OK;
+}
+
+namespace {
+int stage_in1(DevBuf& b, const double* x, int64_t n, cudaStream_t s) {
+  b.s = s;
+  retain_pool_memory();
+  if (n == 0) return DDB_OK;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b.p), sizeof(double) * n, s);
+  if (e != cudaSuccess) return fail(e, "host staging allocation");
+  e = cudaMemcpyAsync(b.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail(e, "host to device copy");
+  return DDB_OK;
+}
+int stage_out1(double* x, const DevBuf& b, int64_t n, cudaStream_t s) {
+  cudaError_t e = cudaMemcpyAsync(x, b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+}  // namespace
+
+int ddb_dgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
+                   const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
+                   double* c, int64_t ldc, void* stream) {
+  int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  if (m == 0 || n == 0 || ((alpha == 0.0 || k == 0) && beta == 1.0)) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool na = upflag(transa) == 'N', nb = upflag(transb) == 'N';
+  const int64_t sa = alpha == 0.0 ? 0 : span(na ? m : k, na ? k : m, lda);
+  const int64_t sb = alpha == 0.0 ? 0 : span(nb ? k : n, nb ? n : k, ldb);
+  const int64_t sc = span(m, n, ldc);
+  DevBuf A, B, C;
+  if ((rc = stage_in1(A, a, sa, s))) return rc;
+  if ((rc = stage_in1(B, b, sb, s))) return rc;
+  if ((rc = stage_in1(C, c, sc, s))) return rc;
+  rc = ddb_dgemm(transa, transb, m, n, k, alpha, A.p, lda, B.p, ldb, beta, C.p, ldc, stream);
+  if (rc) return rc;
+  return stage_out1(c, C, sc, s);
+}
+
+int ddb_dsyrk_host(char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
+                   int64_t lda, double beta, double* c, int64_t ldc, void* stream) {
+  int rc = ddb_rsyrk_validate(uplo, trans, n, k, lda, ldc);
+  if (rc) return rc;
+  if (n == 0 || ((alpha == 0.0 || k == 0) && beta == 1.0)) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool tn = upflag(trans) == 'N';
+  const int64_t sa = alpha == 0.0 ? 0 : span(tn ? n : k, tn ? k : n, lda);
+  const int64_t sc = span(n, n, ldc);
+  DevBuf A, C;
+  if ((rc = stage_in1(A, a, sa, s))) return rc;
+  if ((rc = stage_in1(C, c, sc, s))) return rc;
+  rc = ddb_dsyrk(uplo, trans, n, k, alpha, A.p, lda, beta, C.p, ldc, stream);
+  if (rc) return rc;
+  return stage_out1(c, C, sc, s);
 }
 
 }  // extern "C"

@@ -18,6 +18,8 @@ cudaError_t launch_tiled_twosum(int, const GemmArgs&, const int*, const int*, co
                               cudaStream_t);
 cudaError_t launch_tiled_select(int, const GemmArgs&, const int*, const int*, const int*,
                               cudaStream_t);
+cudaError_t launch_tiled_f64(int, const GemmArgs&, const int*, const int*, const int*,
+                             cudaStream_t);
 cudaError_t launch_tiled_cert(int, const GemmArgs&, const int*, const int*, const int*,
                               cudaStream_t);
 
@@ -140,6 +142,7 @@ cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const i
     case ALG_TWOSUM: return launch_tiled_twosum(cfg, g, row_exp, col_exp, flag, s);
     case ALG_SELECT: return launch_tiled_select(cfg, g, row_exp, col_exp, flag, s);
     case ALG_CERT: return launch_tiled_cert(cfg, g, row_exp, col_exp, flag, s);
+    case ALG_F64: return launch_tiled_f64(cfg, g, row_exp, col_exp, flag, s);
     default: return launch_tiled_exact(cfg, g, row_exp, col_exp, flag, s);
   }
 }

@@ -59,9 +59,52 @@ reference_kernel(GemmArgs g, const int* __restrict__ flag, int gate) {
   }
 }
 
+// Binary64 precision (the F64 backend, elem.py:149-197): the same loop orders
+// with plain IEEE operations; used for alpha == 0 and k == 0.
+__global__ void __launch_bounds__(256) reference_f64_kernel(GemmArgs g) {
+  const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (i >= g.m) return;
+  const double alpha = g.alpha.h, beta = g.beta.h;
+  for (int64_t j = (int64_t)blockIdx.y * 8 + threadIdx.y; j < g.n; j += (int64_t)gridDim.y * 8) {
+    if (g.syrk == 1 && i > j) continue;
+    if (g.syrk == 2 && i < j) continue;
+    const int64_t ci = i + j * g.ldc;
+    const double c0 = g.c_hi[ci];
+    double out;
+    if (alpha == 0.0) {
+      if (beta == 1.0) continue;
+      out = beta == 0.0 ? 0.0 : dmul(beta, c0);
+    } else if (g.ta == 0) {
+      double c = beta == 0.0 ? 0.0 : (beta == 1.0 ? c0 : dmul(beta, c0));
+      for (int64_t l = 0; l < g.k; ++l) {
+        const int64_t bi = g.tb == 0 ? l + j * g.ldb : j + l * g.ldb;
+        c = dadd(c, dmul(g.a_hi[i + l * g.lda], dmul(alpha, g.b_hi[bi])));
+      }
+      out = c;
+    } else {
+      double acc = 0.0;
+      for (int64_t l = 0; l < g.k; ++l) {
+        const int64_t bi = g.tb == 0 ? l + j * g.ldb : j + l * g.ldb;
+        acc = dadd(acc, dmul(g.a_hi[l + i * g.lda], g.b_hi[bi]));
+      }
+      const double at = dmul(alpha, acc);
+      out = beta == 0.0 ? at : dadd(at, dmul(beta, c0));
+    }
+    g.c_hi[ci] = out;
+  }
+}
+
 cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaStream_t s,
                              int* nlaunch) {
   if (g.m <= 0 || g.n <= 0) return cudaSuccess;
+  if (g.f64) {
+    const int64_t gx = (g.m + 31) / 32;
+    int64_t gy = (g.n + 7) / 8;
+    if (gy > 65535) gy = 65535;
+    reference_f64_kernel<<<dim3((unsigned)gx, (unsigned)gy), dim3(32, 8), 0, s>>>(g);
+    ++*nlaunch;
+    return cudaGetLastError();
+  }
   const int64_t gx = (g.m + 31) / 32;
   int64_t gy = (g.n + 7) / 8;
   if (gy > 65535) gy = 65535;

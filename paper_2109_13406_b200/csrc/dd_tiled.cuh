@@ -123,7 +123,7 @@ __device__ __forceinline__ unsigned long long abs_bits(double x) {
 }
 __device__ __forceinline__ bool abs_ge(double x, double y) { return abs_bits(x) >= abs_bits(y); }
 
-template <class C, int TA, int TB>
+template <class C, int TA, int TB, bool LO = true>
 __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double* sB,
                                            int64_t i0, int64_t j0, int64_t l0, int64_t kend,
                                            int tid) {
@@ -138,7 +138,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double
     const bool v = gi < g.m && gl < kend;
     const int64_t off = v ? (TA == 0 ? gi + gl * g.lda : gl + gi * g.lda) : 0;
     cp_async8(sA + kk * ASTR + ii, g.a_hi + off, v);
-    cp_async8(sA + BK * ASTR + kk * ASTR + ii, g.a_lo + off, v);
+    if (LO) cp_async8(sA + BK * ASTR + kk * ASTR + ii, g.a_lo + off, v);
   }
   // op(B) tile: BK x BN -> sB[plane][kk][jj]
 #pragma unroll
@@ -150,7 +150,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double
     const bool v = gj < g.n && gl < kend;
     const int64_t off = v ? (TB == 0 ? gl + gj * g.ldb : gj + gl * g.ldb) : 0;
     cp_async8(sB + kk * BSTR + jj, g.b_hi + off, v);
-    cp_async8(sB + BK * BSTR + kk * BSTR + jj, g.b_lo + off, v);
+    if (LO) cp_async8(sB + BK * BSTR + kk * BSTR + jj, g.b_lo + off, v);
   }
 }
 
@@ -192,7 +192,9 @@ __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN
   for (int a = 0; a < TM; ++a)
 #pragma unroll
     for (int b = 0; b < TN; ++b) {
-      if (ALG == ALG_CERT) {
+      if (ALG == ALG_F64) {     // f64: c = c + a*t (NN) / acc = acc + a*b (TN), unfused
+        H[a][b] = dadd(H[a][b], dmul(ah[a], bh[b]));
+      } else if (ALG == ALG_CERT) {
         const double T = H[a][b];
         const double Tn = dfma(ah[a], bh[b], T);
         const double r = dfma(ah[a], bh[b], dsub(T, Tn));
@@ -291,6 +293,14 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       for (int b = 0; b < TN; ++b) {
         H[a][b] = 0.0;
         L[a][b] = 0.0;
+        if (ALG == ALG_F64 && TA == 0) {    // _scale_full in binary64
+          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+          if (gi < g.m && gj < g.n) {
+            const double c = g.c_hi[gi + gj * g.ldc];
+            H[a][b] = g.beta.h == 0.0 ? 0.0 : (g.beta.h == 1.0 ? c : dmul(g.beta.h, c));
+          }
+        }
         if (ALG == ALG_EXACT && TA == 0) {  // axpy form: start from beta-scaled C
           const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
           const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
@@ -309,7 +319,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   const int ktiles = (int)((kend - kbeg + BK - 1) / BK);
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage<C, TA, TB>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, kbeg + (int64_t)s * BK, kend, tid);
+    if (s < ktiles) load_stage<C, TA, TB, ALG != ALG_F64>(g, sA + s * A_STAGE, sB + s * B_STAGE, i0, j0, kbeg + (int64_t)s * BK, kend, tid);
     cp_async_commit();
   }
 
@@ -321,7 +331,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     if (DDB_ABLATE != 2 || kt == 0) {
       const int nk = kt + STAGES - 1;
       const int ns = nk % STAGES;
-      if (nk < ktiles) load_stage<C, TA, TB>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, kbeg + (int64_t)nk * BK, kend, tid);
+      if (nk < ktiles) load_stage<C, TA, TB, ALG != ALG_F64>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, kbeg + (int64_t)nk * BK, kend, tid);
       cp_async_commit();
     }
     const int st = kt % STAGES;
@@ -330,6 +340,16 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     double* b_h = sB + st * B_STAGE;
     double* b_l = b_h + BK * BSTR;
 
+    if (ALG == ALG_F64 && TA == 0) {
+      // temp = alpha * op(B)(l, j) in binary64 (level23.py:122, :137)
+#pragma unroll
+      for (int r = 0; r < BN * BK / NT; ++r) {
+        const int idx = tid + r * NT;
+        const int kk = idx / BN, jj = idx % BN;
+        b_h[kk * BSTR + jj] = dmul(g.alpha.h, b_h[kk * BSTR + jj]);
+      }
+      __syncthreads();
+    }
     if (ALG == ALG_EXACT && TA == 0) {
       // t = mul2(alpha, op(B)(l, j)) once per tile element (level23.py:122, :137)
 #pragma unroll
@@ -344,7 +364,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     }
 
     int kcount = BK;
-    if (ALG == ALG_EXACT) {
+    if (ALG == ALG_EXACT || ALG == ALG_F64) {
       const int64_t rem = kend - kbeg - (int64_t)kt * BK;
       kcount = rem < BK ? (int)rem : BK;   // exact: never run a padded k-step
     }
@@ -354,16 +374,20 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
 #pragma unroll
       for (int gq = 0; gq < TM / 2; ++gq) {
         const double2 vh = *reinterpret_cast<const double2*>(a_h + kk * ASTR + gq * RX + tx * 2);
-        const double2 vl = *reinterpret_cast<const double2*>(a_l + kk * ASTR + gq * RX + tx * 2);
         ah[2 * gq] = vh.x; ah[2 * gq + 1] = vh.y;
-        al[2 * gq] = vl.x; al[2 * gq + 1] = vl.y;
+        if (ALG != ALG_F64) {
+          const double2 vl = *reinterpret_cast<const double2*>(a_l + kk * ASTR + gq * RX + tx * 2);
+          al[2 * gq] = vl.x; al[2 * gq + 1] = vl.y;
+        }
       }
 #pragma unroll
       for (int gq = 0; gq < TN / 2; ++gq) {
         const double2 vh = *reinterpret_cast<const double2*>(b_h + kk * BSTR + gq * RY + ty * 2);
-        const double2 vl = *reinterpret_cast<const double2*>(b_l + kk * BSTR + gq * RY + ty * 2);
         bh[2 * gq] = vh.x; bh[2 * gq + 1] = vh.y;
-        bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
+        if (ALG != ALG_F64) {
+          const double2 vl = *reinterpret_cast<const double2*>(b_l + kk * BSTR + gq * RY + ty * 2);
+          bl[2 * gq] = vl.x; bl[2 * gq + 1] = vl.y;
+        }
       }
     };
     auto k_step = [&](int kk) {
@@ -392,7 +416,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
           H[a][b] = T2;
         }
     };
-    if (ALG == ALG_EXACT) {
+    if (ALG == ALG_EXACT || ALG == ALG_F64) {
 #pragma unroll 1
       for (int kk = 0; kk < kcount; ++kk) k_step(kk);
     } else {
@@ -441,6 +465,15 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       if (SYRK == 1 && gi > gj) continue;
       if (SYRK == 2 && gi < gj) continue;
       const int64_t ci = gi + gj * g.ldc;
+      if (ALG == ALG_F64) {    // level23.py:120-149 with the F64 backend (elem.py:149-197)
+        if (TA == 0) {
+          g.c_hi[ci] = H[a][b];
+        } else {                // _combine: at = alpha*acc; beta == 0 ? at : at + beta*C
+          const double at = dmul(g.alpha.h, H[a][b]);
+          g.c_hi[ci] = g.beta.h == 0.0 ? at : dadd(at, dmul(g.beta.h, g.c_hi[ci]));
+        }
+        continue;
+      }
       dd out;
       if (ALG == ALG_EXACT) {
         if (TA == 0) out = dd{H[a][b], L[a][b]};

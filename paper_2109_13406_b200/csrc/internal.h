@@ -10,7 +10,7 @@ namespace ddb {
 enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2, MODE_TWOSUM = 3 };
 
 // Tiled accumulation algorithm for a mode (dd_gemm.cu).
-enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_CERT = 3 };
+enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_CERT = 3, ALG_F64 = 4 };
 int alg_for_mode(int mode);
 
 // Route flag written by the prescan: 0 = every operand inside the safe
@@ -40,6 +40,9 @@ struct GemmArgs {
   // splitk_reduce adds them in order.  kchunk >= k: no split, part == nullptr.
   int64_t kchunk;
   double* part;
+  // binary64 precision (the reference's 'f64' Matrix): only the hi planes
+  // exist; a_lo / b_lo / c_lo are unused (dd_reference.cu, ALG_F64)
+  int f64;
 };
 
 // Which kernel should run, decided on the device by the prescan flag.

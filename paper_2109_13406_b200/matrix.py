@@ -119,6 +119,17 @@ def dd_is_one(v):
 # --------------------------------------------------------------------------
 # containers
 
+PRECISIONS = {"dd": 2, "f64": 1}   # planes per matrix; c64 / cdd are not on the path
+
+
+def _planes(precision):
+    try:
+        return PRECISIONS[precision]
+    except KeyError:
+        raise NotImplementedError(
+            f"precision {precision!r}: only 'dd' and 'f64' are on the B200 path") from None
+
+
 class HostMatrix:
     """m x n dd matrix in host memory, column-major (hi, lo) numpy planes.
 
@@ -131,31 +142,31 @@ class HostMatrix:
         ld = max(1, m) if ld is None else ld
         if ld < max(1, m):
             raise ValueError("leading dimension too small")
-        if precision != "dd":
-            raise NotImplementedError(f"precision {precision!r}: only 'dd' is on the B200 path")
+        planes = _planes(precision)
         self.m, self.n, self.ld, self.precision = m, n, ld, precision
         size = ld * n
         if pinned:
             import torch
             self.store = tuple(torch.zeros(size, dtype=torch.float64, pin_memory=True).numpy()
-                               for _ in range(2))
+                               for _ in range(planes))
         else:
-            self.store = (np.zeros(size), np.zeros(size))
+            self.store = tuple(np.zeros(size) for _ in range(planes))
 
     @classmethod
-    def from_planes(cls, m, n, hi, lo, ld=None):
-        a = cls(0, 0)
+    def from_planes(cls, m, n, hi, lo=None, ld=None):
+        """dd from (hi, lo); binary64 ('f64') when lo is None."""
+        a = cls(0, 0, "dd" if lo is not None else "f64")
         a.m, a.n = m, n
         a.ld = max(1, m) if ld is None else ld
-        a.store = (np.ascontiguousarray(hi, dtype=np.float64),
-                   np.ascontiguousarray(lo, dtype=np.float64))
+        a.store = tuple(np.ascontiguousarray(p, dtype=np.float64)
+                        for p in ((hi, lo) if lo is not None else (hi,)))
         return a
 
     def to_device(self, device=None):
         return DeviceMatrix.from_host(self, device)
 
     def __repr__(self):
-        return f"HostMatrix({self.m}x{self.n}, ld={self.ld}, precision='dd')"
+        return f"HostMatrix({self.m}x{self.n}, ld={self.ld}, precision={self.precision!r})"
 
 
 class DeviceMatrix:
@@ -169,37 +180,39 @@ class DeviceMatrix:
         ld = max(1, m) if ld is None else ld
         if ld < max(1, m):
             raise ValueError("leading dimension too small")
-        if precision != "dd":
-            raise NotImplementedError(f"precision {precision!r}: only 'dd' is on the B200 path")
+        planes = _planes(precision)
         self.m, self.n, self.ld, self.precision = m, n, ld, precision
         if store is None:
             dev = torch.device("cuda" if device is None else device)
-            store = (torch.zeros(ld * n, dtype=torch.float64, device=dev),
-                     torch.zeros(ld * n, dtype=torch.float64, device=dev))
+            store = tuple(torch.zeros(ld * n, dtype=torch.float64, device=dev)
+                          for _ in range(planes))
         self.store = store
 
     @classmethod
     def from_host(cls, mat, device=None):
         import torch
         dev = torch.device("cuda" if device is None else device)
-        hi, lo = (torch.as_tensor(np.ascontiguousarray(p, dtype=np.float64)).to(dev)
-                  for p in mat.store[:2])
-        return cls(mat.m, mat.n, "dd", mat.ld, store=(hi, lo))
+        planes = _planes(mat.precision)
+        store = tuple(torch.as_tensor(np.ascontiguousarray(p, dtype=np.float64)).to(dev)
+                      for p in mat.store[:planes])
+        return cls(mat.m, mat.n, mat.precision, mat.ld, store=store)
 
     @property
     def device(self):
         return self.store[0].device
 
     def to_host(self):
-        return HostMatrix.from_planes(self.m, self.n, self.store[0].cpu().numpy(),
-                                      self.store[1].cpu().numpy(), self.ld)
+        planes = [p.cpu().numpy() for p in self.store]
+        return HostMatrix.from_planes(self.m, self.n, planes[0],
+                                      planes[1] if len(planes) > 1 else None, self.ld)
 
     def copy(self):
-        return DeviceMatrix(self.m, self.n, "dd", self.ld,
-                            store=(self.store[0].clone(), self.store[1].clone()))
+        return DeviceMatrix(self.m, self.n, self.precision, self.ld,
+                            store=tuple(p.clone() for p in self.store))
 
     def __repr__(self):
-        return f"DeviceMatrix({self.m}x{self.n}, ld={self.ld}, precision='dd', device={self.device})"
+        return (f"DeviceMatrix({self.m}x{self.n}, ld={self.ld}, precision={self.precision!r}, "
+                f"device={self.device})")
 
 
 def is_device(mat):

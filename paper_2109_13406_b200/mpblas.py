@@ -19,12 +19,13 @@ plus one keyword, ``mode``:
   "reference"  the one-thread-per-element checked kernel (debugging)
 
 C is updated in place; A and B are read only; nothing is returned.
+Precision 'f64' (the reference's binary64 Matrix, one plane) runs the same
+routines over the reference's F64 backend bit for bit (``mode`` is ignored).
 Operands are either all ``DeviceMatrix`` (planes resident in HBM; the call is
 asynchronous on torch's current stream) or all host matrices (numpy planes:
 ``HostMatrix`` or the reference's own ``mpkit`` Matrix; the call stages
-through device memory and returns after C is back on the host).  Only the
-'dd' precision is on the B200 path; other precisions raise
-NotImplementedError -- there is no CPU fallback.
+through device memory and returns after C is back on the host).  The complex
+precisions raise NotImplementedError -- there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -71,19 +72,27 @@ def _raise_rc(routine, rc):
 
 
 def _precision_gate(routine, tag):
-    if tag != "dd":
+    if tag not in ("dd", "f64"):
         raise NotImplementedError(
-            f"{routine}: precision {tag!r} is not on the B200 dd path (only 'dd')")
+            f"{routine}: precision {tag!r} is not on the B200 path (only 'dd' and 'f64')")
+
+
+def _scalar(tag, v):
+    """``_scalar_for`` (matrix.py:29-37): DDouble for dd, float() for f64."""
+    if tag == "f64":
+        f = float(v)
+        return f, 0.0
+    return to_dd(v)
 
 
 class _HostPlanes:
     """Contiguous float64 views of a host store; writes back on ``commit``."""
 
-    def __init__(self, store):
+    def __init__(self, store, nplanes=2):
         self.src = store
         self.planes = [p if (isinstance(p, np.ndarray) and p.dtype == np.float64
                              and p.flags.c_contiguous)
-                       else np.ascontiguousarray(p, dtype=np.float64) for p in store[:2]]
+                       else np.ascontiguousarray(p, dtype=np.float64) for p in store[:nplanes]]
 
     def ptr(self, i):
         return self.planes[i].ctypes.data
@@ -130,8 +139,8 @@ def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
     require(routine, lda >= max(1, nrowa), 8)
     require(routine, ldb >= max(1, nrowb), 10)
     require(routine, ldc >= max(1, m), 13)
-    al = to_dd(alpha)
-    be = to_dd(beta)
+    al = _scalar(tag, alpha)
+    be = _scalar(tag, beta)
     code = _mode_code(mode)
     if m == 0 or n == 0 or ((not dd_truthy(al) or k == 0) and dd_is_one(be)):
         return
@@ -141,6 +150,21 @@ def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
         check_storage(c, m, n, ldc)
     L = _lib.load()
     dev = _placement(routine, a, b, c)
+    if tag == "f64":
+        head = (transa.encode(), transb.encode(), m, n, k, al[0])
+        if dev is not None:
+            import torch
+            with torch.cuda.device(dev):
+                stream = torch.cuda.current_stream(dev).cuda_stream
+                rc = L.ddb_dgemm(*head, _dev_ptr(a, 0), lda, _dev_ptr(b, 0), ldb, be[0],
+                                 _dev_ptr(c, 0), ldc, stream)
+            _raise_rc(routine, rc)
+            return
+        ha, hb, hc = _HostPlanes(a.store, 1), _HostPlanes(b.store, 1), _HostPlanes(c.store, 1)
+        rc = L.ddb_dgemm_host(*head, ha.ptr(0), lda, hb.ptr(0), ldb, be[0], hc.ptr(0), ldc, None)
+        _raise_rc(routine, rc)
+        hc.commit()
+        return
     args_head = (transa.encode(), transb.encode(), m, n, k, al[0], al[1])
     if dev is not None:
         import torch
@@ -173,8 +197,8 @@ def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, 
     nrowa, ncola = (n, k) if trans == "N" else (k, n)
     require(routine, lda >= max(1, nrowa), 7)
     require(routine, ldc >= max(1, n), 10)
-    al = to_dd(alpha)
-    be = to_dd(beta)
+    al = _scalar(tag, alpha)
+    be = _scalar(tag, beta)
     code = _mode_code(mode)
     if n == 0 or ((not dd_truthy(al) or k == 0) and dd_is_one(be)):
         return
@@ -184,6 +208,20 @@ def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, 
             check_storage(a, nrowa, ncola, lda)   # A viewed only when alpha != 0 (:250-260)
     L = _lib.load()
     dev = _placement(routine, a, c)
+    if tag == "f64":
+        head = (uplo.encode(), trans.encode(), n, k, al[0])
+        if dev is not None:
+            import torch
+            with torch.cuda.device(dev):
+                stream = torch.cuda.current_stream(dev).cuda_stream
+                rc = L.ddb_dsyrk(*head, _dev_ptr(a, 0), lda, be[0], _dev_ptr(c, 0), ldc, stream)
+            _raise_rc(routine, rc)
+            return
+        ha, hc = _HostPlanes(a.store, 1), _HostPlanes(c.store, 1)
+        rc = L.ddb_dsyrk_host(*head, ha.ptr(0), lda, be[0], hc.ptr(0), ldc, None)
+        _raise_rc(routine, rc)
+        hc.commit()
+        return
     args_head = (uplo.encode(), trans.encode(), n, k, al[0], al[1])
     if dev is not None:
         import torch

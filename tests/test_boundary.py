@@ -79,10 +79,28 @@ def test_mixed_precision_is_value_error_before_blas_error():
         Rgemm("X", "N", 2, 2, 2, 1.0, a, 2, b, 2, 0.0, a, 2)
 
 
-def test_non_dd_precision_is_not_silently_run_on_cpu():
+def test_complex_precision_is_not_silently_run_on_cpu():
     a = HostMatrix(2, 2)
-    a.precision = "f64"
+    a.precision = "cdd"
     with pytest.raises(NotImplementedError):
+        Rgemm("N", "N", 2, 2, 2, 1.0, a, 2, a, 2, 0.0, a, 2)
+    with pytest.raises(NotImplementedError):
+        HostMatrix(2, 2, "c64")
+
+
+def test_f64_without_gpu_fails_loudly():
+    """binary64 goes to the GPU too; with no device the call raises."""
+    import os
+    a = HostMatrix(2, 2, "f64")
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libddblas.so not built")
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    with pytest.raises(RuntimeError):
         Rgemm("N", "N", 2, 2, 2, 1.0, a, 2, a, 2, 0.0, a, 2)
 
 

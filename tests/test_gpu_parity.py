@@ -37,7 +37,18 @@ def host(m, n, ld, planes):
 CASES = list(golden.load_cases())
 
 
+def dev64(m, n, ld, hi):
+    import torch
+    return DeviceMatrix(m, n, "f64", ld, store=(torch.from_numpy(np.ascontiguousarray(hi)).cuda(),))
+
+
+def host64(m, n, ld, hi):
+    return HostMatrix.from_planes(m, n, hi.copy(), None, ld)
+
+
 def _run_case(case, arr, mode, on_device=True):
+    if case.get("precision") == "f64":
+        return _run_case_f64(case, arr, on_device)
     mk = dev if on_device else host
     if case["routine"] == "Rgemm":
         ta, tb = case["transa"].upper(), case["transb"].upper()
@@ -64,6 +75,31 @@ def _run_case(case, arr, mode, on_device=True):
     return c.store[0], c.store[1]
 
 
+def _run_case_f64(case, arr, on_device):
+    mk = dev64 if on_device else host64
+    al, be = case["alpha_v"][0], case["beta_v"][0]
+    if case["routine"] == "Rgemm":
+        ta, tb = case["transa"].upper(), case["transb"].upper()
+        m, n, k = case["m"], case["n"], case["k"]
+        nra, nca = (m, k) if ta == "N" else (k, m)
+        nrb, ncb = (k, n) if tb == "N" else (n, k)
+        a = mk(nra, nca, case["lda"], arr["A_hi"])
+        b = mk(nrb, ncb, case["ldb"], arr["B_hi"])
+        c = mk(m, n, case["ldc"], arr["C_hi"])
+        with np.errstate(all="ignore"):
+            Rgemm(case["transa"], case["transb"], m, n, k, al, a, case["lda"], b, case["ldb"],
+                  be, c, case["ldc"])
+    else:
+        n, k = case["n"], case["k"]
+        nra, nca = (n, k) if case["trans"].upper() == "N" else (k, n)
+        a = mk(nra, nca, case["lda"], arr["A_hi"])
+        c = mk(n, n, case["ldc"], arr["C_hi"])
+        with np.errstate(all="ignore"):
+            Rsyrk(case["uplo"], case["trans"], n, k, al, a, case["lda"], be, c, case["ldc"])
+    h = c.store[0].cpu().numpy() if on_device else c.store[0]
+    return h, np.zeros(0)
+
+
 class _Scalar:
     """A DDouble-like (hi, lo) scalar, as the reference's DDouble."""
 
@@ -84,6 +120,9 @@ def test_golden_bitwise(idx, mode):
 def test_golden_fast_within_bound(idx):
     case, arr, out_hi, out_lo = CASES[idx]
     got_h, got_l = _run_case(case, arr, "fast")
+    if case.get("precision") == "f64":     # binary64: bit-exact in every mode
+        assert bits_equal(got_h, out_hi), case
+        return
     if case.get("special") in ("inf_a", "huge", "tiny"):
         # outside the safe window the call is routed to the reference-semantics
         # kernel, so even fast mode reproduces the reference bit for bit
@@ -131,6 +170,13 @@ def test_golden_fast_within_bound(idx):
                                    max(k, 1))
             worst = max(worst, r)
     assert worst <= 1.0, (case, worst)
+
+
+@pytest.mark.parametrize("idx", [i for i, c in enumerate(CASES) if c[0].get("precision") == "f64"][:6])
+def test_f64_host_path_bitwise(idx):
+    case, arr, out_hi, _ = CASES[idx]
+    got, _ = _run_case(case, arr, "exact", on_device=False)
+    assert bits_equal(got, out_hi), case
 
 
 @pytest.mark.parametrize("mode", ["exact", "fast"])
