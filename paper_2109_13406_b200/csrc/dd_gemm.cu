@@ -45,7 +45,6 @@ static int tile_cfg() {
     const char* v = std::getenv("DDB_TILE");
     if (v != nullptr && !std::strcmp(v, "small")) return 1;
     if (v != nullptr && !std::strcmp(v, "wide")) return 2;
-    if (v != nullptr && !std::strcmp(v, "tall")) return 3;
     return 0;
   }();
   return cfg;

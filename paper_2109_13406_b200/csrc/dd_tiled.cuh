@@ -69,7 +69,6 @@ struct Cfg {
 using CfgBig = Cfg<8, 4, 1>;                 // 128 x 64 tile, 8 warps / SM
 using CfgSmall = Cfg<4, 4, 2, 256, 16, 0>;   // 64 x 64 tile, 2 CTAs: 16 warps / SM
 using CfgWide = Cfg<4, 4, 1, 512, 32, 0>;    // 128 x 64 tile, 16 warps / SM
-using CfgTall = Cfg<4, 8, 1, 256, 32, 1>;    // 128 x 64 tile, 4 x 8 micro-tiles
 
 constexpr int BK = 16;
 #ifndef DDB_PHASE

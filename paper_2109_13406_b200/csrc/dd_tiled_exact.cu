@@ -7,7 +7,6 @@ cudaError_t launch_tiled_exact(int cfg, const GemmArgs& g, const int* row_exp, c
                             const int* flag, cudaStream_t s) {
   if (cfg == 1) return tiled::launch_alg<tiled::CfgSmall, ALG_EXACT>(g, row_exp, col_exp, flag, s);
   if (cfg == 2) return tiled::launch_alg<tiled::CfgWide, ALG_EXACT>(g, row_exp, col_exp, flag, s);
-  if (cfg == 3) return tiled::launch_alg<tiled::CfgTall, ALG_EXACT>(g, row_exp, col_exp, flag, s);
   return tiled::launch_alg<tiled::CfgBig, ALG_EXACT>(g, row_exp, col_exp, flag, s);
 }
 }  // namespace ddb

@@ -5,8 +5,12 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-template <int TM, int TN, int MINB, int UNR>
+template <int TM, int TN, int MINB, int UNR, int LDS = 0>
 __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double s0) {
+  __shared__ __align__(16) double sm[4][16][64];
+  for (int i = threadIdx.x; i < 4 * 16 * 64; i += 256) (&sm[0][0][0])[i] = 1.0 + (i & 63) * 1e-6;
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   double T[TM][TN], L[TM][TN], ah[TM], al[TM], bh[TN], bl[TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i) { ah[i] = 1.0 + i * 1e-3 + threadIdx.x * 1e-7; al[i] = ah[i] * 1e-17; }
@@ -16,9 +20,71 @@ __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double 
   for (int i = 0; i < TM; ++i)
 #pragma unroll
     for (int j = 0; j < TN; ++j) { T[i][j] = s0; L[i][j] = 0.0; }
+  if (LDS == 2) {   // operands for step s+1 loaded while step s computes
+    double ah2[2][TM], bh2[2][TN], al2[2][TM], bl2[2][TN];
+    auto ld = [&](int k2, double (&xa)[TM], double (&xal)[TM], double (&xb)[TN], double (&xbl)[TN]) {
+#pragma unroll
+      for (int g = 0; g < TM / 2; ++g) {
+        const double2 h = *reinterpret_cast<const double2*>(&sm[0][k2][(g * 32 + tx * 2) & 63]);
+        const double2 l = *reinterpret_cast<const double2*>(&sm[1][k2][(g * 32 + tx * 2) & 63]);
+        xa[2 * g] = h.x; xa[2 * g + 1] = h.y; xal[2 * g] = l.x; xal[2 * g + 1] = l.y;
+      }
+#pragma unroll
+      for (int g = 0; g < TN / 2; ++g) {
+        const double2 h = *reinterpret_cast<const double2*>(&sm[2][k2][g * 32 + ty * 2]);
+        const double2 l = *reinterpret_cast<const double2*>(&sm[3][k2][g * 32 + ty * 2]);
+        xb[2 * g] = h.x; xb[2 * g + 1] = h.y; xbl[2 * g] = l.x; xbl[2 * g + 1] = l.y;
+      }
+    };
+    ld(0, ah2[0], al2[0], bh2[0], bl2[0]);
+    for (int it = 0; it < iters * (16 / UNR); ++it) {
+#pragma unroll
+      for (int kk = 0; kk < UNR; ++kk) {
+        const int c = kk & 1;
+        ld((it * UNR + kk + 1) & 15, ah2[c ^ 1], al2[c ^ 1], bh2[c ^ 1], bl2[c ^ 1]);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            const double t = T[i][j];
+            const double tn = __fma_rn(ah2[c][i], bh2[c][j], t);
+            const double r = __fma_rn(ah2[c][i], bh2[c][j], __dsub_rn(t, tn));
+            double l = __fma_rn(ah2[c][i], bl2[c][j], L[i][j]);
+            l = __fma_rn(al2[c][i], bh2[c][j], l);
+            L[i][j] = __dadd_rn(l, r);
+            T[i][j] = tn;
+          }
+        if (kk & 1) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+              const double t2 = __dadd_rn(T[i][j], L[i][j]);
+              L[i][j] = __dsub_rn(L[i][j], __dsub_rn(t2, T[i][j]));
+              T[i][j] = t2;
+            }
+        }
+      }
+    }
+  } else
   for (int it = 0; it < iters * (16 / UNR); ++it) {
 #pragma unroll
     for (int kk = 0; kk < UNR; ++kk) {
+      if (LDS) {
+        const int k2 = (it * UNR + kk) & 15;
+#pragma unroll
+        for (int g = 0; g < TM / 2; ++g) {
+          const double2 h = *reinterpret_cast<const double2*>(&sm[0][k2][(g * 32 + tx * 2) & 63]);
+          const double2 l = *reinterpret_cast<const double2*>(&sm[1][k2][(g * 32 + tx * 2) & 63]);
+          ah[2 * g] = h.x; ah[2 * g + 1] = h.y; al[2 * g] = l.x * 1e-17; al[2 * g + 1] = l.y * 1e-17;
+        }
+#pragma unroll
+        for (int g = 0; g < TN / 2; ++g) {
+          const double2 h = *reinterpret_cast<const double2*>(&sm[2][k2][g * 32 + ty * 2]);
+          const double2 l = *reinterpret_cast<const double2*>(&sm[3][k2][g * 32 + ty * 2]);
+          bh[2 * g] = h.x; bh[2 * g + 1] = h.y; bl[2 * g] = l.x * 1e-17; bl[2 * g + 1] = l.y * 1e-17;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
@@ -41,8 +107,10 @@ __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double 
             T[i][j] = t2;
           }
       }
+      if (!LDS) {
 #pragma unroll
-      for (int i = 0; i < TM; ++i) ah[i] = -ah[i];   // keep the sum bounded
+        for (int i = 0; i < TM; ++i) ah[i] = -ah[i];   // keep the sum bounded
+      }
     }
   }
   double s = 0;
@@ -53,7 +121,7 @@ __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double 
   if (s == 12345.0) out[0] = s;
 }
 
-template <int TM, int TN, int MINB, int UNR = 16>
+template <int TM, int TN, int MINB, int UNR = 16, int LDS = 0>
 void run(int sms, double* out) {
   const int iters = 400;
   cudaEvent_t e0, e1;
@@ -62,7 +130,7 @@ void run(int sms, double* out) {
   float best = 1e30f;
   for (int rep = 0; rep < 3; ++rep) {
     cudaEventRecord(e0);
-    mix<TM, TN, MINB, UNR><<<sms * MINB, 256>>>(out, iters, 1.5 * 1024);
+    mix<TM, TN, MINB, UNR, LDS><<<sms * MINB, 256>>>(out, iters, 1.5 * 1024);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -70,7 +138,7 @@ void run(int sms, double* out) {
     if (ms < best) best = ms;
   }
   const double dp = (double)sms * MINB * 256 * iters * 16 * TM * TN * 7.5;
-  printf("%dx%d micro-tile, %d CTA/SM, unroll %d: %.1f%% of DP peak\n", TM, TN, MINB, UNR,
+  printf("%dx%d micro-tile, %d CTA/SM, unroll %d, lds %d: %.1f%% of DP peak\n", TM, TN, MINB, UNR, LDS,
          dp / (best * 1e-3) / ((double)sms * 64 * 1.965e9) * 100);
 }
 
@@ -79,12 +147,12 @@ int main() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* out;
   cudaMalloc(&out, 8);
-  run<8, 4, 1>(sms, out);
   run<8, 4, 1, 2>(sms, out);
-  run<8, 4, 1, 4>(sms, out);
-  run<4, 4, 2>(sms, out);
-  run<4, 4, 2, 2>(sms, out);
-  run<4, 2, 3>(sms, out);
-  run<2, 2, 4>(sms, out);
+  run<8, 4, 1, 2, 1>(sms, out);
+  run<8, 4, 1, 2, 2>(sms, out);
+  run<8, 4, 1, 4, 2>(sms, out);
+  run<8, 4, 1, 8, 2>(sms, out);
+  run<4, 4, 2, 2, 2>(sms, out);
+  run<4, 4, 2, 4, 2>(sms, out);
   return 0;
 }
