@@ -323,11 +323,11 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   }
 
   for (int kt = 0; kt < ktiles; ++kt) {
-    if (DDB_ABLATE != 2 || kt == 0) {
+    if ((DDB_ABLATE & 2) == 0 || kt == 0) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
     }
-    if (DDB_ABLATE != 2 || kt == 0) {
+    if ((DDB_ABLATE & 2) == 0 || kt == 0) {
       const int nk = kt + STAGES - 1;
       const int ns = nk % STAGES;
       if (nk < ktiles) load_stage<C, TA, TB, ALG != ALG_F64>(g, sA + ns * A_STAGE, sB + ns * B_STAGE, i0, j0, kbeg + (int64_t)nk * BK, kend, tid);
@@ -425,6 +425,16 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       // 99 % for a 2- or 4-step body (scripts/cert_mix.cu).  Operands are
       // double-buffered in registers across the two steps; CERT folds every 2
       // steps, TWOSUM renormalises every RN = 8.
+      if (DDB_ABLATE & 1) {   // ablation: operands loaded once per k-tile (no LDS in the steps)
+        double ah[TM], al[TM], bh[TN], bl[TN];
+        load_ops(0, ah, al, bh, bl);
+#pragma unroll 1
+        for (int kk = 0; kk < BK; kk += 2) {
+          mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
+          mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
+          if (ALG == ALG_CERT) fold();
+        }
+      } else
 #pragma unroll 1
       for (int kk = 0; kk < BK; kk += DDB_UNR) {
         if (C::PF) {   // step j+1's operands load while step j computes; nothing
