@@ -20,6 +20,9 @@ cudaError_t launch_tiled_select(int, const GemmArgs&, const int*, const int*, co
                               cudaStream_t);
 cudaError_t launch_tiled_f64(int, const GemmArgs&, const int*, const int*, const int*,
                              cudaStream_t);
+bool tma_eligible(const GemmArgs& g, int alg);
+cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,
+                          const int* flag, cudaStream_t s);
 cudaError_t launch_tiled_cert(int, const GemmArgs&, const int*, const int*, const int*,
                               cudaStream_t);
 
@@ -137,6 +140,11 @@ cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const i
   if (g.m <= 0 || g.n <= 0) return cudaSuccess;
   ++*nlaunch;
   const int cfg = tile_cfg();
+  if (cfg == 0 && tma_eligible(g, alg)) {   // NN, aligned: TMA + mbarrier feed (dd_tma.cu)
+    const cudaError_t e = launch_tma_nn(g, alg, row_exp, col_exp, flag, s);
+    if (e != cudaErrorNotSupported) return e;
+    cudaGetLastError();
+  }
   switch (alg) {
     case ALG_TWOSUM: return launch_tiled_twosum(cfg, g, row_exp, col_exp, flag, s);
     case ALG_SELECT: return launch_tiled_select(cfg, g, row_exp, col_exp, flag, s);

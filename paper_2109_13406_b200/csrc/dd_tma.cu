@@ -1,0 +1,299 @@
+// dd_tma.cu -- TMA + mbarrier pipeline variant of the fast-mode tiled kernel
+// for the NN layout (the benchmark case) with 16-byte aligned operands.
+//
+// Same arithmetic as dd_tiled.cuh (mac_step / fold / renorm / epilogue), a
+// different feed: a dedicated producer warp issues cp.async.bulk.tensor (TMA)
+// copies of the A hi/lo (128 x 16, m-major) and B hi/lo (16 x 64, k-major) tiles
+// into a 4-stage ring; 8 consumer warps wait on per-stage "full" mbarriers
+// (transaction-counted) and release stages through "empty" mbarriers, so there
+// is no __syncthreads, no per-thread address arithmetic and no cp.async issue
+// in the k-loop.  TMA zero-fills the ragged edges.  A is read m-major exactly
+// as before; B is read k-major: one 16-byte LDS gives a column's operands for
+// two consecutive k-steps, so the 2-step loop body needs the same number of
+// LDS as the cp.async kernel.
+//
+// Used when transa = transb = 'N', both planes 16-byte aligned, lda and ldb
+// even (TMA global strides are multiples of 16 bytes); anything else runs
+// dd_tiled.cuh.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "dd_tiled.cuh"
+
+namespace ddb {
+namespace tma {
+
+using tiled::anchor_from_bexp;
+using tiled::anchor_of;
+using tiled::dbits;
+
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+constexpr int NT = 256;       // 8 warps; thread 0 doubles as the TMA producer
+constexpr int TM = 8, TN = 4, RX = 32, RY = 32;
+constexpr int A_PLANE = BK * BM, B_PLANE = BN * BK;          // doubles
+constexpr int STAGE_DOUBLES = 2 * A_PLANE + 2 * B_PLANE;     // 6144 doubles = 48 KB
+constexpr uint32_t STAGE_BYTES = STAGE_DOUBLES * 8;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + (BM + BN) * 4 + 1024;
+
+__device__ __forceinline__ uint32_t saddr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(saddr(b)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar))
+      : "memory");
+}
+
+template <int ALG>
+__global__ void __launch_bounds__(NT, 1)
+dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
+                 const __grid_constant__ CUtensorMap mAl, const __grid_constant__ CUtensorMap mBh,
+                 const __grid_constant__ CUtensorMap mBl, const int* __restrict__ row_exp,
+                 const int* __restrict__ col_exp, const int* __restrict__ flag, int tiles_m,
+                 int tiles_n) {
+  if (*flag != ROUTE_SAFE) return;   // dd_reference.cu handles this call
+
+  const int bid = blockIdx.x;
+  const int group_size = tiled::GROUP_M * tiles_n;
+  const int first_m = (bid / group_size) * tiled::GROUP_M;
+  const int gm = min(tiles_m - first_m, tiled::GROUP_M);
+  const int local = bid % group_size;
+  const int64_t i0 = (int64_t)(first_m + local % gm) * BM, j0 = (int64_t)(local / gm) * BN;
+
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * STAGE_DOUBLES);
+  uint64_t* empty = full + STAGES;
+  int* sRowExp = reinterpret_cast<int*>(empty + STAGES);
+  int* sColExp = sRowExp + BM;
+
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (ALG == ALG_CERT) {
+    for (int r = tid; r < BM + BN; r += NT) {
+      if (r < BM) sRowExp[r] = i0 + r < g.m ? row_exp[i0 + r] : 0;
+      else sColExp[r - BM] = j0 + (r - BM) < g.n ? col_exp[j0 + (r - BM)] : 0;
+    }
+  }
+  __syncthreads();
+
+  const int64_t kbeg = (int64_t)blockIdx.y * g.kchunk;
+  const int64_t kend = g.kchunk >= g.k ? g.k : min(g.k, kbeg + g.kchunk);
+  const int ktiles = (int)((kend - kbeg + BK - 1) / BK);
+
+  // Thread 0 is the producer: it keeps STAGES - 1 tiles in flight, refilling a
+  // stage once all 8 warps have released it (empty barrier).  A dedicated
+  // producer warp would cost the consumers registers (allocation granularity).
+  auto produce = [&](int kt) {
+    const int s = kt % STAGES;
+    if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+    double* st = ring + s * STAGE_DOUBLES;
+    mbar_expect_tx(&full[s], STAGE_BYTES);
+    const int kc = (int)(kbeg + (int64_t)kt * BK);
+    tma_load_2d(st, &mAh, (int)i0, kc, &full[s]);
+    tma_load_2d(st + A_PLANE, &mAl, (int)i0, kc, &full[s]);
+    tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)j0, &full[s]);
+    tma_load_2d(st + 2 * A_PLANE + B_PLANE, &mBl, kc, (int)j0, &full[s]);
+  };
+  if (tid == 0)
+    for (int kt = 0; kt < STAGES - 1 && kt < ktiles; ++kt) produce(kt);
+
+  // ---- consumers: the dd_tiled.cuh arithmetic on the TMA-fed ring ----
+  const int tx = tid % 16, ty = tid / 16;
+  double H[TM][TN], L[TM][TN];
+  if (ALG == ALG_CERT) {
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) {
+        const int ri = (a >> 1) * RX + tx * 2 + (a & 1), cj = (b >> 1) * RY + ty * 2 + (b & 1);
+        const int64_t gi = i0 + ri, gj = j0 + cj;
+        const float sb = (gi < g.m && gj < g.n) ? g.bound[gi + gj * g.m] : 0.f;
+        const double sd = dfma((double)sb, g.bnd_fac, g.bnd_floor);
+        const int es = (int)((dbits(sd) >> 52) & 0x7ff);
+        H[a][b] = anchor_from_bexp(es + sRowExp[ri] + sColExp[cj] - 2042);
+        L[a][b] = 0.0;
+      }
+  } else {
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
+  }
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int s = kt % STAGES;
+    if (tid == 0 && kt + STAGES - 1 < ktiles) produce(kt + STAGES - 1);
+    mbar_wait(&full[s], (kt / STAGES) & 1);
+    const double* a_h = ring + s * STAGE_DOUBLES;
+    const double* a_l = a_h + A_PLANE;
+    const double* b_h = a_h + 2 * A_PLANE;
+    const double* b_l = b_h + B_PLANE;
+#pragma unroll 1
+    for (int kk = 0; kk < BK; kk += 2) {
+      double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TN], bl0[TN], bh1[TN], bl1[TN];
+#pragma unroll
+      for (int gq = 0; gq < TM / 2; ++gq) {
+        const double2 h0 = *reinterpret_cast<const double2*>(a_h + kk * BM + gq * RX + tx * 2);
+        const double2 l0 = *reinterpret_cast<const double2*>(a_l + kk * BM + gq * RX + tx * 2);
+        const double2 h1 = *reinterpret_cast<const double2*>(a_h + (kk + 1) * BM + gq * RX + tx * 2);
+        const double2 l1 = *reinterpret_cast<const double2*>(a_l + (kk + 1) * BM + gq * RX + tx * 2);
+        ah0[2 * gq] = h0.x; ah0[2 * gq + 1] = h0.y; al0[2 * gq] = l0.x; al0[2 * gq + 1] = l0.y;
+        ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y; al1[2 * gq] = l1.x; al1[2 * gq + 1] = l1.y;
+      }
+#pragma unroll
+      for (int b = 0; b < TN; ++b) {   // k-major B: (kk, kk+1) of column cj in one LDS
+        const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
+        const double2 h = *reinterpret_cast<const double2*>(b_h + cj * BK + kk);
+        const double2 l = *reinterpret_cast<const double2*>(b_l + cj * BK + kk);
+        bh0[b] = h.x; bh1[b] = h.y; bl0[b] = l.x; bl1[b] = l.y;
+      }
+      tiled::mac_step<ALG, TM, TN>(H, L, ah0, al0, bh0, bl0);
+      tiled::mac_step<ALG, TM, TN>(H, L, ah1, al1, bh1, bl1);
+      if (ALG == ALG_CERT) {
+#pragma unroll
+        for (int a = 0; a < TM; ++a)
+#pragma unroll
+          for (int b = 0; b < TN; ++b) {
+            const double T2 = dadd(H[a][b], L[a][b]);
+            L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
+            H[a][b] = T2;
+          }
+      } else if (((kk + 2) % tiled::RN) == 0) {
+#pragma unroll
+        for (int a = 0; a < TM; ++a)
+#pragma unroll
+          for (int b = 0; b < TN; ++b) {
+            double sx, ex;
+            quick_two_sum(H[a][b], L[a][b], sx, ex);
+            H[a][b] = sx;
+            L[a][b] = ex;
+          }
+      }
+    }
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+  }
+
+  // epilogue (as dd_tiled.cuh's fast modes)
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) {
+      const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+      const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+      if (gi >= g.m || gj >= g.n) continue;
+      double sx, ex;
+      const double hv = ALG == ALG_CERT ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
+      two_sum(hv, L[a][b], sx, ex);
+      if (g.part != nullptr) {
+        double* ph = g.part + (size_t)blockIdx.y * 2 * g.m * g.n;
+        ph[gi + gj * g.m] = sx;
+        ph[(size_t)g.m * g.n + gi + gj * g.m] = ex;
+        continue;
+      }
+      const int64_t ci = gi + gj * g.ldc;
+      const dd out = add2_chk(mul2_chk(g.alpha, dd{sx, ex}),
+                              scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
+      g.c_hi[ci] = out.h;
+      g.c_lo[ci] = out.l;
+    }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeFn) nullptr;
+    return reinterpret_cast<EncodeFn>(p);
+  }();
+  return fn;
+}
+
+static bool encode(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t ld,
+                   uint32_t box_inner, uint32_t box_outer) {
+  EncodeFn fn = encode_fn();
+  if (fn == nullptr) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace tma
+
+bool tma_eligible(const GemmArgs& g, int alg) {
+  if (std::getenv("DDB_NO_TMA") != nullptr) return false;
+  if (!(alg == ALG_CERT || alg == ALG_TWOSUM)) return false;
+  if (g.syrk != 0 || g.ta != 0 || g.tb != 0 || g.f64) return false;
+  if ((g.lda & 1) || (g.ldb & 1)) return false;
+  if (!tma::aligned16(g.a_hi) || !tma::aligned16(g.a_lo) || !tma::aligned16(g.b_hi) ||
+      !tma::aligned16(g.b_lo))
+    return false;
+  if (g.m >= (1ll << 31) || g.n >= (1ll << 31) || g.k >= (1ll << 31)) return false;
+  return tma::encode_fn() != nullptr;
+}
+
+cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,
+                          const int* flag, cudaStream_t s) {
+  using namespace tma;
+  alignas(64) CUtensorMap mAh, mAl, mBh, mBl;
+  // A: m x k, m contiguous -> box {BM (m), BK (k)}; B: k x n, k contiguous -> box {BK, BN}
+  if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, BK) || !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, BK) ||
+      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, BK, BN) || !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, BK, BN))
+    return cudaErrorNotSupported;
+  const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
+  const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
+  auto kern = alg == ALG_CERT ? dd_tma_nn_kernel<ALG_CERT> : dd_tma_nn_kernel<ALG_TWOSUM>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  kern<<<dim3(tiles_m * tiles_n, splits), NT, SMEM_BYTES, s>>>(g, mAh, mAl, mBh, mBl, row_exp,
+                                                                col_exp, flag, tiles_m, tiles_n);
+  return cudaGetLastError();
+}
+
+}  // namespace ddb
