@@ -32,6 +32,7 @@ using tiled::dbits;
 #define DDB_TMA_UNROLL 8   // 2-step bodies per k-tile unrolled (8 = the whole tile)
 #endif
 
+constexpr int kTmaUnroll = DDB_TMA_UNROLL;
 constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
 constexpr int NT = 256;       // 8 warps; thread 0 doubles as the TMA producer
 constexpr int TM = 8, TN = 4, RX = 32, RY = 32;
@@ -163,7 +164,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     const double* a_l = a_h + A_PLANE;
     const double* b_h = a_h + 2 * A_PLANE;
     const double* b_l = b_h + B_PLANE;
-#pragma unroll DDB_TMA_UNROLL
+#pragma unroll (kTmaUnroll)
     for (int kk = 0; kk < BK; kk += 2) {
       double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TN], bl0[TN], bh1[TN], bl1[TN];
 #pragma unroll
