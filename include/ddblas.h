@@ -98,6 +98,26 @@ int ddb_dgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, do
 int ddb_dsyrk_host(char uplo, char trans, int64_t n, int64_t k, double alpha, const double* a,
                    int64_t lda, double beta, double* c, int64_t ldc, void* stream);
 
+/* Complex GEMM: mpkit.mpblas.Cgemm (level23.py:201-221).  'cdd' operands are
+ * four planes {re_hi, re_lo, im_hi, im_lo} (arrays of 4 pointers), alpha /
+ * beta four doubles in the same order; 'C' flags conjugate.  Modes as for
+ * ddb_rgemm (exact = the reference's CDD backend bit for bit, fast = four
+ * real fast-mode GEMMs + a complex dd epilogue).  'c64' (ddb_zgemm) takes
+ * interleaved complex128 arrays and alpha / beta as {re, im}; bit-exact. */
+int ddb_cgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double* alpha,
+              const double* const* a, int64_t lda, const double* const* b, int64_t ldb,
+              const double* beta, double* const* c, int64_t ldc, int mode, void* stream);
+int ddb_cgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                   const double* alpha, const double* const* a, int64_t lda,
+                   const double* const* b, int64_t ldb, const double* beta, double* const* c,
+                   int64_t ldc, int mode, void* stream);
+int ddb_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double* alpha,
+              const double* a, int64_t lda, const double* b, int64_t ldb, const double* beta,
+              double* c, int64_t ldc, void* stream);
+int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, const double* alpha,
+                   const double* a, int64_t lda, const double* b, int64_t ldb, const double* beta,
+                   double* c, int64_t ldc, void* stream);
+
 /* Argument checks alone (no device work): reference index or 0. */
 int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
                        int64_t lda, int64_t ldb, int64_t ldc);

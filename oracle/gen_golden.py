@@ -133,6 +133,67 @@ def f64_cases():
     return cases
 
 
+CALPHAS = {"z1": (complex(1.5, -0.25),), "z0": (0j,), "zr": (2.0,)}
+CBETAS = {"w05": complex(0.5, 0.125), "w1": complex(1.0, 0.0), "w0": 0j}
+
+
+def complex_cases():
+    """Cgemm (level23.py:201-221) on 'cdd' and 'c64' matrices."""
+    cases = []
+    seed = 1200
+    for prec in ("cdd", "c64"):
+        for ta in ("N", "T", "C"):
+            for tb in ("N", "T", "C"):
+                cases.append(dict(routine="Cgemm", precision=prec, transa=ta, transb=tb, m=9,
+                                  n=7, k=11, pad=(2, 1, 3), alpha="z1", beta="w05", seed=seed))
+                seed += 1
+        for ta, tb, al, be, k, sp in (("N", "N", "z1", "w1", 6, None), ("T", "N", "z1", "w1", 6, None),
+                                      ("N", "N", "z1", "w0", 6, "nan_c"),
+                                      ("C", "N", "z1", "w0", 6, "nan_c"),
+                                      ("N", "N", "z0", "w05", 6, None), ("T", "C", "z0", "w05", 6, None),
+                                      ("N", "N", "z1", "w05", 0, None), ("T", "N", "zr", "w05", 0, None),
+                                      ("N", "T", "zr", "w05", 5, None)):
+            cases.append(dict(routine="Cgemm", precision=prec, transa=ta, transb=tb, m=5, n=4,
+                              k=k, pad=(0, 0, 1), alpha=al, beta=be, seed=seed, special=sp))
+            seed += 1
+        cases.append(dict(routine="Cgemm", precision=prec, transa="N", transb="N", m=70, n=66,
+                          k=40, pad=(0, 0, 0), alpha="z1", beta="w05", seed=seed)); seed += 1
+    return cases
+
+
+def run_case_complex(mb, case, store):
+    from mpkit.ddarith import DDComplex, DDouble
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    al = CALPHAS[case["alpha"]][0]
+    be = CBETAS[case["beta"]]
+    case["alpha_v"] = [al.real, al.imag] if isinstance(al, complex) else [al, 0.0]
+    case["beta_v"] = [be.real, be.imag]
+    ta, tb = case["transa"].upper(), case["transb"].upper()
+    m, n, k = case["m"], case["n"], case["k"]
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    prec = case["precision"]
+    mats = {}
+    for name, (r, c, ld) in (("A", (nra, nca, lds["lda"])), ("B", (nrb, ncb, lds["ldb"])),
+                             ("C", (m, n, lds["ldc"]))):
+        mat = mb.Matrix(r, c, prec, ld)
+        if prec == "cdd":
+            mat.store = tuple(arrays[f"{name}_{p}"].copy() for p in ("rh", "rl", "ih", "il"))
+        else:
+            mat.store = (arrays[f"{name}_z"].copy(),)
+        mats[name] = mat
+    with np.errstate(all="ignore"):
+        mb.Cgemm(case["transa"], case["transb"], m, n, k, al, mats["A"], lds["lda"], mats["B"],
+                 lds["ldb"], be, mats["C"], lds["ldc"])
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    for i, plane in enumerate(mats["C"].store):
+        store["arrays"][f"c{cid}_out{i}"] = np.asarray(plane)
+    store["cases"].append(case)
+
+
 def syrk_cases():
     cases = []
     seed = 500
@@ -162,6 +223,8 @@ def syrk_cases():
 
 
 def run_case(mb, DDouble, case, store):
+    if case["routine"] == "Cgemm":
+        return run_case_complex(mb, case, store)
     alpha = ALPHAS[case["alpha"]]
     beta = BETAS[case["beta"]]
     if case.get("precision") == "f64":
@@ -264,7 +327,7 @@ def main():
     mb, elem, DDouble = _ref()
     os.makedirs(OUT, exist_ok=True)
     store = {"cases": [], "arrays": {}}
-    for case in gemm_cases() + syrk_cases() + f64_cases():
+    for case in gemm_cases() + syrk_cases() + f64_cases() + complex_cases():
         run_case(mb, DDouble, case, store)
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
     with open(os.path.join(OUT, "cases.json"), "w") as f:

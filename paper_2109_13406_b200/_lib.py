@@ -24,7 +24,8 @@ _c = ctypes.c_char
 EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rgemm_validate", "ddb_rsyrk_validate", "ddb_last_error",
            "ddb_version", "ddb_launch_count", "ddb_last_route", "ddb_fp64_peak_probe",
-           "ddb_dgemm", "ddb_dsyrk", "ddb_dgemm_host", "ddb_dsyrk_host")
+           "ddb_dgemm", "ddb_dsyrk", "ddb_dgemm_host", "ddb_dsyrk_host",
+           "ddb_cgemm", "ddb_cgemm_host", "ddb_zgemm", "ddb_zgemm_host")
 
 _lib = None
 
@@ -56,6 +57,13 @@ def load():
     dsyrk_args = [_c, _c, _i64, _i64, _d, _dp, _i64, _d, _dp, _i64, _dp]
     for name, args in (("ddb_dgemm", dgemm_args), ("ddb_dgemm_host", dgemm_args),
                        ("ddb_dsyrk", dsyrk_args), ("ddb_dsyrk_host", dsyrk_args)):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = args
+    cg = [_c, _c, _i64, _i64, _i64, _dp, _dp, _i64, _dp, _i64, _dp, _dp, _i64, ctypes.c_int, _dp]
+    zg = [_c, _c, _i64, _i64, _i64, _dp, _dp, _i64, _dp, _i64, _dp, _dp, _i64, _dp]
+    for name, args in (("ddb_cgemm", cg), ("ddb_cgemm_host", cg), ("ddb_zgemm", zg),
+                       ("ddb_zgemm_host", zg)):
         f = getattr(L, name)
         f.restype = ctypes.c_int
         f.argtypes = args

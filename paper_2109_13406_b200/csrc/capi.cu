@@ -292,6 +292,91 @@ int ddb_dsyrk(char uplo, char trans, int64_t n, int64_t k, double alpha, const d
   return run(g, MODE_EXACT, static_cast<cudaStream_t>(stream));
 }
 
+// ---- Cgemm: complex precisions ('cdd' planes, 'c64' interleaved) ----------
+
+int ddb_cgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double* alpha,
+              const double* const* a, int64_t lda, const double* const* b, int64_t ldb,
+              const double* beta, double* const* c, int64_t ldc, int mode, void* stream) {
+  const int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM) {
+    g_last_error = "unknown mode";
+    return DDB_EINVAL;
+  }
+  const bool beta_one = is_one(beta[0], beta[1]) && is_zero(beta[2], beta[3]);
+  // level23.py:214-215 with a DDComplex alpha: `not alpha` is never true
+  if (m == 0 || n == 0 || (k == 0 && beta_one)) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CgemmArgs g{};
+  g.ta = upflag(transa) == 'N' ? 0 : 1;
+  g.tb = upflag(transb) == 'N' ? 0 : 1;
+  g.conja = upflag(transa) == 'C';
+  g.conjb = upflag(transb) == 'C';
+  g.m = m; g.n = n; g.k = k;
+  for (int p = 0; p < 4; ++p) { g.a[p] = a[p]; g.b[p] = b[p]; g.c[p] = c[p]; }
+  g.lda = lda; g.ldb = ldb; g.ldc = ldc;
+  g.alpha = cdd{dd{alpha[0], alpha[1]}, dd{alpha[2], alpha[3]}};
+  g.beta = cdd{dd{beta[0], beta[1]}, dd{beta[2], beta[3]}};
+  if (mode == DDB_MODE_EXACT || mode == DDB_MODE_REFERENCE || k == 0) {
+    cudaError_t e = launch_cgemm_exact(g, s);
+    g_launches += 1;
+    if (e != cudaSuccess) return fail(e, "cgemm kernel launch");
+    return DDB_OK;
+  }
+  // fast / twosum: P = op(A) op(B) from four real dd GEMMs on the planes,
+  //   Re P = Ar Br - (sa sb) Ai Bi,  Im P = sb Ar Bi + sa Ai Br
+  // (sa, sb = -1 for a conjugated operand), then C = alpha P + beta C.
+  retain_pool_memory();
+  double* pw = nullptr;
+  const size_t plane = (size_t)m * n;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&pw), 4 * plane * sizeof(double), s);
+  if (e != cudaSuccess) return fail(e, "cgemm workspace");
+  const double sa = g.conja ? -1.0 : 1.0, sb = g.conjb ? -1.0 : 1.0;
+  double* pr[2] = {pw, pw + plane};
+  double* pim[2] = {pw + 2 * plane, pw + 3 * plane};
+  struct Term { int ai, bi; double coef; double** dst; double beta; };
+  const Term terms[4] = {{0, 0, 1.0, pr, 0.0}, {1, 1, -sa * sb, pr, 1.0},
+                         {0, 1, sb, pim, 0.0}, {1, 0, sa, pim, 1.0}};
+  int rc2 = DDB_OK;
+  for (const Term& t : terms) {
+    rc2 = ddb_rgemm(transa == 'C' || transa == 'c' ? 'T' : transa,
+                    transb == 'C' || transb == 'c' ? 'T' : transb, m, n, k, t.coef, 0.0,
+                    a[2 * t.ai], a[2 * t.ai + 1], lda, b[2 * t.bi], b[2 * t.bi + 1], ldb,
+                    t.beta, 0.0, t.dst[0], t.dst[1], m, mode, stream);
+    if (rc2 != DDB_OK) break;
+  }
+  if (rc2 == DDB_OK) {
+    e = launch_cgemm_combine(g, pr[0], pr[1], pim[0], pim[1], s);
+    g_launches += 1;
+    if (e != cudaSuccess) rc2 = fail(e, "cgemm combine launch");
+  }
+  cudaFreeAsync(pw, s);
+  return rc2;
+}
+
+int ddb_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double* alpha,
+              const double* a, int64_t lda, const double* b, int64_t ldb, const double* beta,
+              double* c, int64_t ldc, void* stream) {
+  const int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  const bool alpha_zero = alpha[0] == 0.0 && alpha[1] == 0.0;
+  const bool beta_one = beta[0] == 1.0 && beta[1] == 0.0;
+  if (m == 0 || n == 0 || ((alpha_zero || k == 0) && beta_one)) return DDB_OK;
+  ZgemmArgs g{};
+  g.ta = upflag(transa) == 'N' ? 0 : 1;
+  g.tb = upflag(transb) == 'N' ? 0 : 1;
+  g.conja = upflag(transa) == 'C';
+  g.conjb = upflag(transb) == 'C';
+  g.m = m; g.n = n; g.k = k;
+  g.a = a; g.lda = lda; g.b = b; g.ldb = ldb; g.c = c; g.ldc = ldc;
+  g.alpha = z64{alpha[0], alpha[1]};
+  g.beta = z64{beta[0], beta[1]};
+  cudaError_t e = launch_zgemm(g, static_cast<cudaStream_t>(stream));
+  g_launches += 1;
+  if (e != cudaSuccess) return fail(e, "zgemm kernel launch");
+  return DDB_OK;
+}
+
 // ---- host-buffer entry points: stage operands through device memory ----
 
 namespace {
@@ -431,6 +516,56 @@ int ddb_dsyrk_host(char uplo, char trans, int64_t n, int64_t k, double alpha, co
   if ((rc = stage_in1(A, a, sa, s))) return rc;
   if ((rc = stage_in1(C, c, sc, s))) return rc;
   rc = ddb_dsyrk(uplo, trans, n, k, alpha, A.p, lda, beta, C.p, ldc, stream);
+  if (rc) return rc;
+  return stage_out1(c, C, sc, s);
+}
+
+int ddb_cgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                   const double* alpha, const double* const* a, int64_t lda,
+                   const double* const* b, int64_t ldb, const double* beta, double* const* c,
+                   int64_t ldc, int mode, void* stream) {
+  int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool na = upflag(transa) == 'N', nb = upflag(transb) == 'N';
+  const int64_t sa = span(na ? m : k, na ? k : m, lda);
+  const int64_t sb = span(nb ? k : n, nb ? n : k, ldb);
+  const int64_t sc = span(m, n, ldc);
+  DevBuf A[2], B[2], C[2];
+  for (int p = 0; p < 2; ++p) {
+    if ((rc = stage_in(A[p], a[2 * p], a[2 * p + 1], sa, s))) return rc;
+    if ((rc = stage_in(B[p], b[2 * p], b[2 * p + 1], sb, s))) return rc;
+    if ((rc = stage_in(C[p], c[2 * p], c[2 * p + 1], sc, s))) return rc;
+  }
+  const double* ad[4] = {A[0].p, A[0].p ? A[0].p + sa : nullptr, A[1].p, A[1].p ? A[1].p + sa : nullptr};
+  const double* bd[4] = {B[0].p, B[0].p ? B[0].p + sb : nullptr, B[1].p, B[1].p ? B[1].p + sb : nullptr};
+  double* cd[4] = {C[0].p, C[0].p ? C[0].p + sc : nullptr, C[1].p, C[1].p ? C[1].p + sc : nullptr};
+  rc = ddb_cgemm(transa, transb, m, n, k, alpha, ad, lda, bd, ldb, beta, cd, ldc, mode, stream);
+  if (rc) return rc;
+  for (int p = 0; p < 4 && sc > 0; ++p) {
+    cudaError_t e = cudaMemcpyAsync(c[p], cd[p], sizeof(double) * sc, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return fail(e, "device to host copy");
+  }
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
+int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, const double* alpha,
+                   const double* a, int64_t lda, const double* b, int64_t ldb, const double* beta,
+                   double* c, int64_t ldc, void* stream) {
+  int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool na = upflag(transa) == 'N', nb = upflag(transb) == 'N';
+  const int64_t sa = 2 * span(na ? m : k, na ? k : m, lda);
+  const int64_t sb = 2 * span(nb ? k : n, nb ? n : k, ldb);
+  const int64_t sc = 2 * span(m, n, ldc);
+  DevBuf A, B, C;
+  if ((rc = stage_in1(A, a, sa, s))) return rc;
+  if ((rc = stage_in1(B, b, sb, s))) return rc;
+  if ((rc = stage_in1(C, c, sc, s))) return rc;
+  rc = ddb_zgemm(transa, transb, m, n, k, alpha, A.p, lda, B.p, ldb, beta, C.p, ldc, stream);
   if (rc) return rc;
   return stage_out1(c, C, sc, s);
 }

@@ -61,4 +61,31 @@ cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag,
 cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
                          float* bound, cudaStream_t s, int* nlaunch, const char** what);
 
+// complex GEMM (dd_complex.cu)
+struct cdd { dd re, im; };
+struct z64 { double re, im; };
+
+struct CgemmArgs {            // 'cdd': planes re_hi, re_lo, im_hi, im_lo
+  int ta, tb, conja, conjb;
+  int64_t m, n, k;
+  const double* a[4]; int64_t lda;
+  const double* b[4]; int64_t ldb;
+  double* c[4]; int64_t ldc;
+  cdd alpha, beta;
+};
+
+struct ZgemmArgs {            // 'c64': interleaved complex128
+  int ta, tb, conja, conjb;
+  int64_t m, n, k;
+  const double* a; int64_t lda;
+  const double* b; int64_t ldb;
+  double* c; int64_t ldc;
+  z64 alpha, beta;
+};
+
+cudaError_t launch_cgemm_exact(const CgemmArgs& g, cudaStream_t s);
+cudaError_t launch_cgemm_combine(const CgemmArgs& g, const double* pr_h, const double* pr_l,
+                                 const double* pi_h, const double* pi_l, cudaStream_t s);
+cudaError_t launch_zgemm(const ZgemmArgs& g, cudaStream_t s);
+
 }  // namespace ddb

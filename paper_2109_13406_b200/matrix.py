@@ -106,6 +106,21 @@ def to_dd(value):
     raise TypeError(f"cannot make DDouble from {type(value).__name__}")
 
 
+def to_cdd(value):
+    """``_scalar_for('cdd', v)`` (matrix.py:36-37): DDComplex(value) as
+    (re_hi, re_lo, im_hi, im_lo)."""
+    if hasattr(value, "re") and hasattr(value, "im"):
+        return to_dd(value.re) + to_dd(value.im)
+    if isinstance(value, complex):
+        return to_dd(value.real) + to_dd(value.imag)
+    return to_dd(value) + (0.0, 0.0)
+
+
+def to_c64(value):
+    """``_scalar_for('c64', v)``: complex(value)."""
+    return complex(value)
+
+
 def dd_truthy(v):
     """``DDouble.__bool__`` (ddarith.py:290-291)."""
     return v[0] != 0.0 or v[1] != 0.0
@@ -119,7 +134,7 @@ def dd_is_one(v):
 # --------------------------------------------------------------------------
 # containers
 
-PRECISIONS = {"dd": 2, "f64": 1}   # planes per matrix; c64 / cdd are not on the path
+PRECISIONS = {"dd": 2, "f64": 1, "cdd": 4, "c64": 1}   # planes per matrix (c64: complex128)
 
 
 def _planes(precision):
@@ -127,7 +142,11 @@ def _planes(precision):
         return PRECISIONS[precision]
     except KeyError:
         raise NotImplementedError(
-            f"precision {precision!r}: only 'dd' and 'f64' are on the B200 path") from None
+            f"precision {precision!r} is not on the B200 path") from None
+
+
+def _plane_dtype(precision):
+    return np.complex128 if precision == "c64" else np.float64
 
 
 class HostMatrix:
@@ -147,10 +166,11 @@ class HostMatrix:
         size = ld * n
         if pinned:
             import torch
-            self.store = tuple(torch.zeros(size, dtype=torch.float64, pin_memory=True).numpy()
+            tdt = torch.complex128 if precision == "c64" else torch.float64
+            self.store = tuple(torch.zeros(size, dtype=tdt, pin_memory=True).numpy()
                                for _ in range(planes))
         else:
-            self.store = tuple(np.zeros(size) for _ in range(planes))
+            self.store = tuple(np.zeros(size, dtype=_plane_dtype(precision)) for _ in range(planes))
 
     @classmethod
     def from_planes(cls, m, n, hi, lo=None, ld=None):
@@ -184,8 +204,8 @@ class DeviceMatrix:
         self.m, self.n, self.ld, self.precision = m, n, ld, precision
         if store is None:
             dev = torch.device("cuda" if device is None else device)
-            store = tuple(torch.zeros(ld * n, dtype=torch.float64, device=dev)
-                          for _ in range(planes))
+            tdt = torch.complex128 if precision == "c64" else torch.float64
+            store = tuple(torch.zeros(ld * n, dtype=tdt, device=dev) for _ in range(planes))
         self.store = store
 
     @classmethod
@@ -193,8 +213,8 @@ class DeviceMatrix:
         import torch
         dev = torch.device("cuda" if device is None else device)
         planes = _planes(mat.precision)
-        store = tuple(torch.as_tensor(np.ascontiguousarray(p, dtype=np.float64)).to(dev)
-                      for p in mat.store[:planes])
+        store = tuple(torch.as_tensor(np.ascontiguousarray(p, dtype=_plane_dtype(mat.precision)))
+                      .to(dev) for p in mat.store[:planes])
         return cls(mat.m, mat.n, mat.precision, mat.ld, store=store)
 
     @property

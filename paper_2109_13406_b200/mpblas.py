@@ -30,15 +30,16 @@ precisions raise NotImplementedError -- there is no CPU fallback.
 
 from __future__ import annotations
 
+import ctypes
 import os
 
 import numpy as np
 
 from . import _lib
 from .matrix import (BlasError, check_storage, dd_is_one, dd_truthy, is_device, require,
-                     same_precision, to_dd)
+                     same_precision, to_c64, to_cdd, to_dd)
 
-__all__ = ["Rgemm", "Rsyrk", "BlasError", "default_mode"]
+__all__ = ["Rgemm", "Rsyrk", "Cgemm", "BlasError", "default_mode"]
 
 
 def default_mode():
@@ -88,11 +89,11 @@ def _scalar(tag, v):
 class _HostPlanes:
     """Contiguous float64 views of a host store; writes back on ``commit``."""
 
-    def __init__(self, store, nplanes=2):
+    def __init__(self, store, nplanes=2, dtype=np.float64):
         self.src = store
-        self.planes = [p if (isinstance(p, np.ndarray) and p.dtype == np.float64
+        self.planes = [p if (isinstance(p, np.ndarray) and p.dtype == dtype
                              and p.flags.c_contiguous)
-                       else np.ascontiguousarray(p, dtype=np.float64) for p in store[:nplanes]]
+                       else np.ascontiguousarray(p, dtype=dtype) for p in store[:nplanes]]
 
     def ptr(self, i):
         return self.planes[i].ctypes.data
@@ -127,6 +128,9 @@ def Rgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
     whose storage ends before ``ld*ncol``; the kernels never touch it.)"""
     routine = "Rgemm"
     tag = same_precision(routine, a, b, c)
+    if tag in ("cdd", "c64"):   # the reference's Rgemm runs any backend (level23.py:180-198)
+        return _complex_gemm(routine, transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c,
+                             ldc, mode)
     _precision_gate(routine, tag)
     lda, ldb, ldc = _ld_of(a, lda), _ld_of(b, ldb), _ld_of(c, ldc)
     transa = _flag(routine, transa, ("N", "T", "C"), 1)
@@ -234,5 +238,92 @@ def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, 
     ha, hc = _HostPlanes(a.store), _HostPlanes(c.store)
     rc = L.ddb_rsyrk_host(*args_head, ha.ptr(0), ha.ptr(1), lda, be[0], be[1],
                           hc.ptr(0), hc.ptr(1), ldc, code, None)
+    _raise_rc(routine, rc)
+    hc.commit()
+
+
+def Cgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,
+          beta=1.0, c=None, ldc=None, *, mode=None):
+    """Complex GEMM, 'C' flags conjugate (level23.py:201-221).
+
+    'cdd' (complex double-double, four planes) and 'c64' (complex128).
+    Reference quirks kept: a DDComplex has no truth value, so for 'cdd' the
+    alpha == 0 shortcut never fires and beta == 0 multiplies C."""
+    routine = "Cgemm"
+    tag = same_precision(routine, a, b, c)
+    if tag not in ("cdd", "c64"):
+        if tag in ("dd", "f64"):
+            raise ValueError("Cgemm requires complex matrices")
+        raise NotImplementedError(f"{routine}: precision {tag!r} is not on the B200 path")
+    return _complex_gemm(routine, transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc,
+                         mode)
+
+
+def _complex_gemm(routine, transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, mode):
+    tag = a.precision
+    lda, ldb, ldc = _ld_of(a, lda), _ld_of(b, ldb), _ld_of(c, ldc)
+    transa = _flag(routine, transa, ("N", "T", "C"), 1)
+    transb = _flag(routine, transb, ("N", "T", "C"), 2)
+    require(routine, m >= 0, 3)
+    require(routine, n >= 0, 4)
+    require(routine, k >= 0, 5)
+    nrowa, ncola = (m, k) if transa == "N" else (k, m)
+    nrowb, ncolb = (k, n) if transb == "N" else (n, k)
+    require(routine, lda >= max(1, nrowa), 8)
+    require(routine, ldb >= max(1, nrowb), 10)
+    require(routine, ldc >= max(1, m), 13)
+    if tag == "cdd":
+        al, be = to_cdd(alpha), to_cdd(beta)
+        alpha_zero = False                       # DDComplex is always truthy
+        beta_one = be[0] == 1.0 and be[1] == 0.0 and be[2] == 0.0 and be[3] == 0.0
+    else:
+        al, be = to_c64(alpha), to_c64(beta)
+        alpha_zero = al == 0
+        beta_one = be == 1
+    code = _mode_code(mode)
+    if m == 0 or n == 0 or ((alpha_zero or k == 0) and beta_one):
+        return
+    check_storage(a, nrowa, ncola, lda)
+    check_storage(b, nrowb, ncolb, ldb)
+    check_storage(c, m, n, ldc)
+    L = _lib.load()
+    dev = _placement(routine, a, b, c)
+    fl = (transa.encode(), transb.encode(), m, n, k)
+    if tag == "c64":
+        av = ctypes.cast((ctypes.c_double * 2)(al.real, al.imag), ctypes.c_void_p)
+        bv = ctypes.cast((ctypes.c_double * 2)(be.real, be.imag), ctypes.c_void_p)
+        if dev is not None:
+            import torch
+            with torch.cuda.device(dev):
+                stream = torch.cuda.current_stream(dev).cuda_stream
+                rc = L.ddb_zgemm(*fl, av, _dev_ptr(a, 0), lda, _dev_ptr(b, 0), ldb, bv,
+                                 _dev_ptr(c, 0), ldc, stream)
+            _raise_rc(routine, rc)
+            return
+        ha, hb, hc = (_HostPlanes(x.store, 1, np.complex128) for x in (a, b, c))
+        rc = L.ddb_zgemm_host(*fl, av, ha.ptr(0), lda, hb.ptr(0), ldb, bv, hc.ptr(0), ldc, None)
+        _raise_rc(routine, rc)
+        hc.commit()
+        return
+    keep = [(ctypes.c_double * 4)(*al), (ctypes.c_double * 4)(*be)]
+    av, bv = (ctypes.cast(x, ctypes.c_void_p) for x in keep)
+
+    def P4(*ptrs):
+        arr = (ctypes.c_void_p * 4)(*ptrs)
+        keep.append(arr)
+        return ctypes.cast(arr, ctypes.c_void_p)
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_cgemm(*fl, av, P4(*(_dev_ptr(a, i) for i in range(4))), lda,
+                             P4(*(_dev_ptr(b, i) for i in range(4))), ldb, bv,
+                             P4(*(_dev_ptr(c, i) for i in range(4))), ldc, code, stream)
+        _raise_rc(routine, rc)
+        return
+    ha, hb, hc = (_HostPlanes(x.store, 4) for x in (a, b, c))
+    rc = L.ddb_cgemm_host(*fl, av, P4(*(ha.ptr(i) for i in range(4))), lda,
+                          P4(*(hb.ptr(i) for i in range(4))), ldb, bv,
+                          P4(*(hc.ptr(i) for i in range(4))), ldc, code, None)
     _raise_rc(routine, rc)
     hc.commit()

@@ -79,13 +79,21 @@ def test_mixed_precision_is_value_error_before_blas_error():
         Rgemm("X", "N", 2, 2, 2, 1.0, a, 2, b, 2, 0.0, a, 2)
 
 
-def test_complex_precision_is_not_silently_run_on_cpu():
+def test_unknown_precision_is_not_silently_run_on_cpu():
     a = HostMatrix(2, 2)
-    a.precision = "cdd"
+    a.precision = "qd"
     with pytest.raises(NotImplementedError):
         Rgemm("N", "N", 2, 2, 2, 1.0, a, 2, a, 2, 0.0, a, 2)
     with pytest.raises(NotImplementedError):
-        HostMatrix(2, 2, "c64")
+        HostMatrix(2, 2, "qd")
+
+
+def test_cgemm_rejects_real_matrices():
+    """level23.py:207-208."""
+    from paper_2109_13406_b200 import Cgemm
+    a = HostMatrix(2, 2)
+    with pytest.raises(ValueError, match="requires complex"):
+        Cgemm("N", "N", 2, 2, 2, 1.0, a, 2, a, 2, 0.0, a, 2)
 
 
 def test_f64_without_gpu_fails_loudly():

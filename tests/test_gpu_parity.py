@@ -34,7 +34,9 @@ def host(m, n, ld, planes):
     return HostMatrix.from_planes(m, n, planes[0].copy(), planes[1].copy(), ld)
 
 
-CASES = list(golden.load_cases())
+ALL_CASES = list(golden.load_cases())
+CASES = [c for c in ALL_CASES if c[0]["routine"] != "Cgemm"]
+CCASES = [c for c in ALL_CASES if c[0]["routine"] == "Cgemm"]
 
 
 def dev64(m, n, ld, hi):
@@ -366,3 +368,79 @@ def test_nccl_path_single_rank_selftest():
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr[-2000:]
     assert "MISMATCH" not in out.stdout and out.stdout.count("OK") == 5
+
+
+# ---- Cgemm ('cdd', 'c64') against the reference's outputs -------------------
+
+def _cmat(prec, rows, cols, ld, arr, name, on_device=True):
+    import torch
+    from paper_2109_13406_b200.matrix import HostMatrix as HM
+    if prec == "cdd":
+        planes = [np.ascontiguousarray(arr[f"{name}_{p}"]) for p in ("rh", "rl", "ih", "il")]
+    else:
+        planes = [np.ascontiguousarray(arr[f"{name}_z"])]
+    if on_device:
+        return DeviceMatrix(rows, cols, prec, ld, store=tuple(torch.from_numpy(p.copy()).cuda()
+                                                            for p in planes))
+    h = HM(0, 0, prec)
+    h.m, h.n, h.ld = rows, cols, ld
+    h.store = tuple(p.copy() for p in planes)
+    return h
+
+
+def _run_cgemm(case, arr, mode, on_device=True):
+    from paper_2109_13406_b200 import Cgemm
+    prec = case["precision"]
+    ta, tb = case["transa"].upper(), case["transb"].upper()
+    m, n, k = case["m"], case["n"], case["k"]
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    a = _cmat(prec, nra, nca, case["lda"], arr, "A", on_device)
+    b = _cmat(prec, nrb, ncb, case["ldb"], arr, "B", on_device)
+    c = _cmat(prec, m, n, case["ldc"], arr, "C", on_device)
+    al = complex(*case["alpha_v"]) if case["alpha"] != "zr" else case["alpha_v"][0]
+    be = complex(*case["beta_v"])
+    with np.errstate(all="ignore"):
+        Cgemm(case["transa"], case["transb"], m, n, k, al, a, case["lda"], b, case["ldb"], be,
+              c, case["ldc"], mode=mode)
+    if on_device:
+        return tuple(p.cpu().numpy() for p in c.store)
+    return c.store
+
+
+def _bits_equal_c(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.dtype.kind == "c":
+        return bits_equal(a.real.copy(), b.real.copy()) and bits_equal(a.imag.copy(), b.imag.copy())
+    return bits_equal(a, b)
+
+
+@pytest.mark.parametrize("idx", range(len(CCASES)))
+def test_cgemm_golden_bitwise_exact(idx):
+    case, arr, outs, _ = CCASES[idx]
+    got = _run_cgemm(case, arr, "exact")
+    for g_, o_ in zip(got, outs):
+        assert _bits_equal_c(g_, o_), case
+
+
+@pytest.mark.parametrize("idx", [i for i, c in enumerate(CCASES) if c[0]["precision"] == "cdd"])
+def test_cgemm_cdd_fast_close_to_reference(idx):
+    case, arr, outs, _ = CCASES[idx]
+    got = _run_cgemm(case, arr, "fast")
+    k = max(case["k"], 1)
+    ref_re = outs[0] + outs[1]
+    ref_im = outs[2] + outs[3]
+    got_re, got_im = got[0] + got[1], got[2] + got[3]
+    with np.errstate(all="ignore"):
+        scale = np.maximum(1.0, np.abs(ref_re) + np.abs(ref_im))
+        ok = (np.abs(got_re - ref_re) <= 1e-28 * k * scale) | (np.isnan(ref_re) & np.isnan(got_re))
+        ok &= (np.abs(got_im - ref_im) <= 1e-28 * k * scale) | (np.isnan(ref_im) & np.isnan(got_im))
+    assert ok.all(), case
+
+
+@pytest.mark.parametrize("idx", [0, 9, 20])
+def test_cgemm_host_path_bitwise(idx):
+    case, arr, outs, _ = CCASES[idx]
+    got = _run_cgemm(case, arr, "exact", on_device=False)
+    for g_, o_ in zip(got, outs):
+        assert _bits_equal_c(g_, o_), case

@@ -15,7 +15,7 @@ def bits_equal(a, b):
     return bool(np.all(same | both_nan))
 
 
-CASES = list(golden.load_cases())
+CASES = [c for c in golden.load_cases() if c[0]["routine"] != "Cgemm"]
 
 
 @pytest.mark.parametrize("idx", range(len(CASES)))
