@@ -280,6 +280,8 @@ def run_ours(args):
         if not distributed:
             extra["rsyrk"] = _rsyrk(n, k, mode, dev, stream, max(1, args.steps // 2))
             extra["modes"] = _modes(n, k, dev, stream, A, B, C, C0, mode)
+            extra["f64"] = _f64(n, dev, stream)
+            extra["cgemm"] = _cgemm(n // 2, dev, stream, mode)
         cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, 16, 0)
         from oracle import oracle
         extra["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": oracle.max_threads(),
@@ -372,6 +374,36 @@ def _rsyrk(n, k, mode, dev, stream, steps):
     t = statistics.median(times)
     return {"workload": f"dd Rsyrk U N n=k={n}", "value": flop_count("Rsyrk", n, k=k) / t / 1e9,
             "unit": UNIT, "ms_per_step": t * 1e3, "mode": mode}
+
+
+def _f64(n, dev, stream):
+    """binary64 Rgemm NN (the reference's 'f64' precision, bit-exact path)."""
+    import torch
+    from paper_2109_13406_b200 import DeviceMatrix, Rgemm
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    mats = [DeviceMatrix(n, n, "f64", n, store=(hashed_dd_device(n, n, 0, t, dev)[0],))
+            for t in (1, 2, 3)]
+    times = timed(lambda: Rgemm("N", "N", n, n, n, ALPHA, mats[0], n, mats[1], n, BETA,
+                                mats[2], n), 2, 1, stream)
+    t = min(times)
+    return {"workload": f"f64 Rgemm NN m=n=k={n}", "value": 2.0 * n ** 3 / t / 1e9,
+            "unit": "GFlops (binary64)", "ms": t * 1e3}
+
+
+def _cgemm(n, dev, stream, mode):
+    """complex double-double Cgemm NN ('cdd'), 8mnk real dd flops per call."""
+    from paper_2109_13406_b200 import Cgemm, DeviceMatrix
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    mats = []
+    for t in (1, 2, 3):
+        re = hashed_dd_device(n, n, 0, t, dev)
+        im = hashed_dd_device(n, n, 0, t + 10, dev)
+        mats.append(DeviceMatrix(n, n, "cdd", n, store=(re[0], re[1], im[0], im[1])))
+    times = timed(lambda: Cgemm("N", "N", n, n, n, complex(1.5, -0.25), mats[0], n, mats[1], n,
+                                complex(0.5, 0.125), mats[2], n, mode=mode), 2, 1, stream)
+    t = min(times)
+    return {"workload": f"cdd Cgemm NN m=n=k={n}", "value": 8.0 * n ** 3 / t / 1e9,
+            "unit": "dd GFlops (8mnk)", "ms": t * 1e3, "mode": mode}
 
 
 def _modes(n, k, dev, stream, A, B, C, C0, mode):

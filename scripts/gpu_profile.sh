@@ -16,7 +16,7 @@ echo "launches rc=$?"
 for ALG in cert twosum; do
   CMD1="python bench.py --steps 1 --warmup 0 --quick"
   DDB_FAST_ALG=$ALG $CMD1 > gpurun_out/${TAG}_${ALG}_plain.log 2>&1 && \
-  DDB_FAST_ALG=$ALG ncu --set full --clock-control none --import-source on -k regex:dd_tiled -c 1 \
+  DDB_FAST_ALG=$ALG ncu --set full --clock-control none --import-source on -k regex:"dd_(tiled|tma)" -c 1 \
       -o gpurun_out/${TAG}_prof_${ALG} $CMD1 > gpurun_out/${TAG}_ncu_${ALG}.log 2>&1
   echo "ncu $ALG rc=$?"
 done
