@@ -254,7 +254,7 @@ static EncodeFn encode_fn() {
 }
 
 static bool encode(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t ld,
-                   uint32_t box_inner, uint32_t box_outer) {
+                   uint32_t box_inner, uint32_t box_outer, CUtensorMapL2promotion promo) {
   EncodeFn fn = encode_fn();
   if (fn == nullptr) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -263,7 +263,7 @@ static bool encode(CUtensorMap* m, const double* base, int64_t inner, int64_t ou
   const cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -286,9 +286,15 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
                           const int* flag, cudaStream_t s) {
   using namespace tma;
   alignas(64) CUtensorMap mAh, mAl, mBh, mBl;
-  // A: m x k, m contiguous -> box {BM (m), BK (k)}; B: k x n, k contiguous -> box {BK, BN}
-  if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, BK) || !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, BK) ||
-      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, BK, BN) || !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, BK, BN))
+  // A: m x k, m contiguous -> box {BM (m), BK (k)}: 1 KB rows, 256-byte L2 promotion.
+  // B: k x n, k contiguous -> box {BK, BN}: 128-byte rows; promoting them to
+  // 256 bytes doubled the DRAM reads (ncu, round 1), so B uses 128-byte lines.
+  const CUtensorMapL2promotion pa = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  const CUtensorMapL2promotion pb = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+  if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, BK, pa) ||
+      !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, BK, pa) ||
+      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, BK, BN, pb) ||
+      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, BK, BN, pb))
     return cudaErrorNotSupported;
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
