@@ -39,7 +39,7 @@ constexpr int TM = 8, TN = 4, RX = 32, RY = 32;
 constexpr int A_PLANE = BK * BM, B_PLANE = BN * BK;          // doubles
 constexpr int STAGE_DOUBLES = 2 * A_PLANE + 2 * B_PLANE;     // 6144 doubles = 48 KB
 constexpr uint32_t STAGE_BYTES = STAGE_DOUBLES * 8;
-constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + (BM + BN) * 4 + 1024;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -71,29 +71,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// Work unit = one (tile, k-slice).  PERSISTENT: gridDim.x CTAs (one per SM)
+// walk the units u = blockIdx.x + i * gridDim.x in raster order, so all SMs
+// work on the same wave of tiles at nearly the same k (the wave's A / B panel
+// k-slices are read from DRAM once and shared through L2); the producer runs
+// ahead across unit boundaries, overlapping the epilogue with the next loads.
 template <int ALG>
 __global__ void __launch_bounds__(NT, 1)
 dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                  const __grid_constant__ CUtensorMap mAl, const __grid_constant__ CUtensorMap mBh,
                  const __grid_constant__ CUtensorMap mBl, const int* __restrict__ row_exp,
                  const int* __restrict__ col_exp, const int* __restrict__ flag, int tiles_m,
-                 int tiles_n) {
+                 int tiles_n, int splits) {
   if (*flag != ROUTE_SAFE) return;   // dd_reference.cu handles this call
-
-  const int bid = blockIdx.x;
-  const int group_size = tiled::GROUP_M * tiles_n;
-  const int first_m = (bid / group_size) * tiled::GROUP_M;
-  const int gm = min(tiles_m - first_m, tiled::GROUP_M);
-  const int local = bid % group_size;
-  const int64_t i0 = (int64_t)(first_m + local % gm) * BM, j0 = (int64_t)(local / gm) * BN;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * STAGE_DOUBLES);
   uint64_t* empty = full + STAGES;
-  int* sRowExp = reinterpret_cast<int*>(empty + STAGES);
-  int* sColExp = sRowExp + BM;
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -104,135 +100,161 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
-  if (ALG == ALG_CERT) {
-    for (int r = tid; r < BM + BN; r += NT) {
-      if (r < BM) sRowExp[r] = i0 + r < g.m ? row_exp[i0 + r] : 0;
-      else sColExp[r - BM] = j0 + (r - BM) < g.n ? col_exp[j0 + (r - BM)] : 0;
-    }
-  }
   __syncthreads();
 
-  const int64_t kbeg = (int64_t)blockIdx.y * g.kchunk;
-  const int64_t kend = g.kchunk >= g.k ? g.k : min(g.k, kbeg + g.kchunk);
-  const int ktiles = (int)((kend - kbeg + BK - 1) / BK);
+  const int tiles = tiles_m * tiles_n;
+  const int units = tiles * splits;
+  // every unit has the same number of k-tiles except possibly the last slice
+  const int64_t kchunk = g.kchunk >= g.k ? g.k : g.kchunk;
+  auto unit_origin = [&](int u, int64_t& i0, int64_t& j0, int64_t& kbeg, int& ktiles) {
+    const int tile = u % tiles, split = u / tiles;
+    const int group_size = tiled::GROUP_M * tiles_n;
+    const int first_m = (tile / group_size) * tiled::GROUP_M;
+    const int gm = min(tiles_m - first_m, tiled::GROUP_M);
+    const int local = tile % group_size;
+    i0 = (int64_t)(first_m + local % gm) * BM;
+    j0 = (int64_t)(local / gm) * BN;
+    kbeg = (int64_t)split * kchunk;
+    const int64_t kend = min(g.k, kbeg + kchunk);
+    ktiles = (int)((kend - kbeg + BK - 1) / BK);
+  };
 
-  // Thread 0 is the producer: it keeps STAGES - 1 tiles in flight, refilling a
-  // stage once all 8 warps have released it (empty barrier).  A dedicated
-  // producer warp would cost the consumers registers (allocation granularity).
-  auto produce = [&](int kt) {
-    const int s = kt % STAGES;
-    if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+  // ---- producer state (thread 0): walks (unit, k-tile) items ahead ----
+  int p_unit = blockIdx.x, p_kt = 0, p_ktiles = 0;
+  int64_t p_i0 = 0, p_j0 = 0, p_kbeg = 0;
+  uint32_t p_item = 0;
+  if (tid == 0 && p_unit < units) unit_origin(p_unit, p_i0, p_j0, p_kbeg, p_ktiles);
+  auto produce_next = [&]() {   // issue the next item if any; false when exhausted
+    if (p_unit >= units) return false;
+    const int s = p_item % STAGES;
+    if (p_item >= STAGES) mbar_wait(&empty[s], ((p_item / STAGES) - 1) & 1);
     double* st = ring + s * STAGE_DOUBLES;
     mbar_expect_tx(&full[s], STAGE_BYTES);
-    const int kc = (int)(kbeg + (int64_t)kt * BK);
-    tma_load_2d(st, &mAh, (int)i0, kc, &full[s]);
-    tma_load_2d(st + A_PLANE, &mAl, (int)i0, kc, &full[s]);
-    tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)j0, &full[s]);
-    tma_load_2d(st + 2 * A_PLANE + B_PLANE, &mBl, kc, (int)j0, &full[s]);
+    const int kc = (int)(p_kbeg + (int64_t)p_kt * BK);
+    tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
+    tma_load_2d(st + A_PLANE, &mAl, (int)p_i0, kc, &full[s]);
+    tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)p_j0, &full[s]);
+    tma_load_2d(st + 2 * A_PLANE + B_PLANE, &mBl, kc, (int)p_j0, &full[s]);
+    ++p_item;
+    if (++p_kt == p_ktiles) {
+      p_kt = 0;
+      p_unit += gridDim.x;
+      if (p_unit < units) unit_origin(p_unit, p_i0, p_j0, p_kbeg, p_ktiles);
+    }
+    return true;
   };
   if (tid == 0)
-    for (int kt = 0; kt < STAGES - 1 && kt < ktiles; ++kt) produce(kt);
+    for (int i = 0; i < STAGES - 1; ++i) produce_next();
 
-  // ---- consumers: the dd_tiled.cuh arithmetic on the TMA-fed ring ----
   const int tx = tid % 16, ty = tid / 16;
-  double H[TM][TN], L[TM][TN];
-  if (ALG == ALG_CERT) {
+  uint32_t c_item = 0;
+  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    int64_t i0, j0, kbeg;
+    int ktiles;
+    unit_origin(u, i0, j0, kbeg, ktiles);
+
+    double H[TM][TN], L[TM][TN];
+    if (ALG == ALG_CERT) {
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) {
+          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+          const bool in = gi < g.m && gj < g.n;
+          const float sb = in ? g.bound[gi + gj * g.m] : 0.f;
+          const int er = gi < g.m ? row_exp[gi] : 0, ec = gj < g.n ? col_exp[gj] : 0;
+          const double sd = dfma((double)sb, g.bnd_fac, g.bnd_floor);
+          const int es = (int)((dbits(sd) >> 52) & 0x7ff);
+          H[a][b] = anchor_from_bexp(es + er + ec - 2042);
+          L[a][b] = 0.0;
+        }
+    } else {
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
+    }
+
+    for (int kt = 0; kt < ktiles; ++kt, ++c_item) {
+      const int s = c_item % STAGES;
+      if (tid == 0) produce_next();
+      mbar_wait(&full[s], (c_item / STAGES) & 1);
+      const double* a_h = ring + s * STAGE_DOUBLES;
+      const double* a_l = a_h + A_PLANE;
+      const double* b_h = a_h + 2 * A_PLANE;
+      const double* b_l = b_h + B_PLANE;
+#pragma unroll (kTmaUnroll)
+      for (int kk = 0; kk < BK; kk += 2) {
+        double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TN], bl0[TN], bh1[TN], bl1[TN];
+#pragma unroll
+        for (int gq = 0; gq < TM / 2; ++gq) {
+          const double2 h0 = *reinterpret_cast<const double2*>(a_h + kk * BM + gq * RX + tx * 2);
+          const double2 l0 = *reinterpret_cast<const double2*>(a_l + kk * BM + gq * RX + tx * 2);
+          const double2 h1 = *reinterpret_cast<const double2*>(a_h + (kk + 1) * BM + gq * RX + tx * 2);
+          const double2 l1 = *reinterpret_cast<const double2*>(a_l + (kk + 1) * BM + gq * RX + tx * 2);
+          ah0[2 * gq] = h0.x; ah0[2 * gq + 1] = h0.y; al0[2 * gq] = l0.x; al0[2 * gq + 1] = l0.y;
+          ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y; al1[2 * gq] = l1.x; al1[2 * gq + 1] = l1.y;
+        }
+#pragma unroll
+        for (int b = 0; b < TN; ++b) {   // k-major B: (kk, kk+1) of column cj in one LDS
+          const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
+          const double2 h = *reinterpret_cast<const double2*>(b_h + cj * BK + kk);
+          const double2 l = *reinterpret_cast<const double2*>(b_l + cj * BK + kk);
+          bh0[b] = h.x; bh1[b] = h.y; bl0[b] = l.x; bl1[b] = l.y;
+        }
+        tiled::mac_step<ALG, TM, TN>(H, L, ah0, al0, bh0, bl0);
+        tiled::mac_step<ALG, TM, TN>(H, L, ah1, al1, bh1, bl1);
+        if (ALG == ALG_CERT) {
+#pragma unroll
+          for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b) {
+              const double T2 = dadd(H[a][b], L[a][b]);
+              L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
+              H[a][b] = T2;
+            }
+        } else if (((kk + 2) % tiled::RN) == 0) {
+#pragma unroll
+          for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b) {
+              double sx, ex;
+              quick_two_sum(H[a][b], L[a][b], sx, ex);
+              H[a][b] = sx;
+              L[a][b] = ex;
+            }
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+
+    // epilogue (as dd_tiled.cuh's fast modes)
+    const int split = u / tiles;
 #pragma unroll
     for (int a = 0; a < TM; ++a)
 #pragma unroll
       for (int b = 0; b < TN; ++b) {
-        const int ri = (a >> 1) * RX + tx * 2 + (a & 1), cj = (b >> 1) * RY + ty * 2 + (b & 1);
-        const int64_t gi = i0 + ri, gj = j0 + cj;
-        const float sb = (gi < g.m && gj < g.n) ? g.bound[gi + gj * g.m] : 0.f;
-        const double sd = dfma((double)sb, g.bnd_fac, g.bnd_floor);
-        const int es = (int)((dbits(sd) >> 52) & 0x7ff);
-        H[a][b] = anchor_from_bexp(es + sRowExp[ri] + sColExp[cj] - 2042);
-        L[a][b] = 0.0;
+        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+        if (gi >= g.m || gj >= g.n) continue;
+        double sx, ex;
+        const double hv = ALG == ALG_CERT ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
+        two_sum(hv, L[a][b], sx, ex);
+        if (g.part != nullptr) {
+          double* ph = g.part + (size_t)split * 2 * g.m * g.n;
+          ph[gi + gj * g.m] = sx;
+          ph[(size_t)g.m * g.n + gi + gj * g.m] = ex;
+          continue;
+        }
+        const int64_t ci = gi + gj * g.ldc;
+        const dd out = add2_chk(mul2_chk(g.alpha, dd{sx, ex}),
+                                scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
+        g.c_hi[ci] = out.h;
+        g.c_lo[ci] = out.l;
       }
-  } else {
-#pragma unroll
-    for (int a = 0; a < TM; ++a)
-#pragma unroll
-      for (int b = 0; b < TN; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
   }
-
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const int s = kt % STAGES;
-    if (tid == 0 && kt + STAGES - 1 < ktiles) produce(kt + STAGES - 1);
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const double* a_h = ring + s * STAGE_DOUBLES;
-    const double* a_l = a_h + A_PLANE;
-    const double* b_h = a_h + 2 * A_PLANE;
-    const double* b_l = b_h + B_PLANE;
-#pragma unroll (kTmaUnroll)
-    for (int kk = 0; kk < BK; kk += 2) {
-      double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TN], bl0[TN], bh1[TN], bl1[TN];
-#pragma unroll
-      for (int gq = 0; gq < TM / 2; ++gq) {
-        const double2 h0 = *reinterpret_cast<const double2*>(a_h + kk * BM + gq * RX + tx * 2);
-        const double2 l0 = *reinterpret_cast<const double2*>(a_l + kk * BM + gq * RX + tx * 2);
-        const double2 h1 = *reinterpret_cast<const double2*>(a_h + (kk + 1) * BM + gq * RX + tx * 2);
-        const double2 l1 = *reinterpret_cast<const double2*>(a_l + (kk + 1) * BM + gq * RX + tx * 2);
-        ah0[2 * gq] = h0.x; ah0[2 * gq + 1] = h0.y; al0[2 * gq] = l0.x; al0[2 * gq + 1] = l0.y;
-        ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y; al1[2 * gq] = l1.x; al1[2 * gq + 1] = l1.y;
-      }
-#pragma unroll
-      for (int b = 0; b < TN; ++b) {   // k-major B: (kk, kk+1) of column cj in one LDS
-        const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
-        const double2 h = *reinterpret_cast<const double2*>(b_h + cj * BK + kk);
-        const double2 l = *reinterpret_cast<const double2*>(b_l + cj * BK + kk);
-        bh0[b] = h.x; bh1[b] = h.y; bl0[b] = l.x; bl1[b] = l.y;
-      }
-      tiled::mac_step<ALG, TM, TN>(H, L, ah0, al0, bh0, bl0);
-      tiled::mac_step<ALG, TM, TN>(H, L, ah1, al1, bh1, bl1);
-      if (ALG == ALG_CERT) {
-#pragma unroll
-        for (int a = 0; a < TM; ++a)
-#pragma unroll
-          for (int b = 0; b < TN; ++b) {
-            const double T2 = dadd(H[a][b], L[a][b]);
-            L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
-            H[a][b] = T2;
-          }
-      } else if (((kk + 2) % tiled::RN) == 0) {
-#pragma unroll
-        for (int a = 0; a < TM; ++a)
-#pragma unroll
-          for (int b = 0; b < TN; ++b) {
-            double sx, ex;
-            quick_two_sum(H[a][b], L[a][b], sx, ex);
-            H[a][b] = sx;
-            L[a][b] = ex;
-          }
-      }
-    }
-    __syncwarp();
-    if ((tid & 31) == 0) mbar_arrive(&empty[s]);
-  }
-
-  // epilogue (as dd_tiled.cuh's fast modes)
-#pragma unroll
-  for (int a = 0; a < TM; ++a)
-#pragma unroll
-    for (int b = 0; b < TN; ++b) {
-      const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-      const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-      if (gi >= g.m || gj >= g.n) continue;
-      double sx, ex;
-      const double hv = ALG == ALG_CERT ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
-      two_sum(hv, L[a][b], sx, ex);
-      if (g.part != nullptr) {
-        double* ph = g.part + (size_t)blockIdx.y * 2 * g.m * g.n;
-        ph[gi + gj * g.m] = sx;
-        ph[(size_t)g.m * g.n + gi + gj * g.m] = ex;
-        continue;
-      }
-      const int64_t ci = gi + gj * g.ldc;
-      const dd out = add2_chk(mul2_chk(g.alpha, dd{sx, ex}),
-                              scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
-      g.c_hi[ci] = out.h;
-      g.c_lo[ci] = out.l;
-    }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -302,8 +324,14 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  kern<<<dim3(tiles_m * tiles_n, splits), NT, SMEM_BYTES, s>>>(g, mAh, mAl, mBh, mBl, row_exp,
-                                                                col_exp, flag, tiles_m, tiles_n);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t units = (int64_t)tiles_m * tiles_n * splits;
+  const int grid = std::getenv("DDB_TMA_NONPERSISTENT") ? (int)units
+                                                        : (int)(units < sms ? units : sms);
+  kern<<<grid, NT, SMEM_BYTES, s>>>(g, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
+                                    tiles_n, splits);
   return cudaGetLastError();
 }
 
