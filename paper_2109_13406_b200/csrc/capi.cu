@@ -75,6 +75,13 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   int nl = 0;
   cudaError_t e;
   GemmArgs g = g0;
+  {
+    static const int gm_env = [] {
+      const char* v = std::getenv("DDB_GROUP_M");
+      return v ? std::atoi(v) : 0;
+    }();
+    g.group_m = gm_env;
+  }
   if (g.f64) {   // binary64: bit-exact tiled kernel for every input (no window)
     if (g.alpha.h == 0.0 || g.k == 0 || mode == MODE_REFERENCE) {
       e = launch_reference(g, nullptr, GATE_ALWAYS, s, &nl);

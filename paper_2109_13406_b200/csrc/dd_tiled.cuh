@@ -240,9 +240,10 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
 
   // grouped raster over the tile grid
   const int bid = blockIdx.x;
-  const int group_size = GROUP_M * tiles_n;
-  const int first_m = (bid / group_size) * GROUP_M;
-  const int gm = min(tiles_m - first_m, GROUP_M);
+  const int GM_ = g.group_m > 0 ? g.group_m : GROUP_M;
+  const int group_size = GM_ * tiles_n;
+  const int first_m = (bid / group_size) * GM_;
+  const int gm = min(tiles_m - first_m, GM_);
   const int local = bid % group_size;
   const int bm = first_m + local % gm, bn = local / gm;
   const int64_t i0 = (int64_t)bm * BM, j0 = (int64_t)bn * BN;

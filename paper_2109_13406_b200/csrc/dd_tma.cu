@@ -108,9 +108,10 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
   const int64_t kchunk = g.kchunk >= g.k ? g.k : g.kchunk;
   auto unit_origin = [&](int u, int64_t& i0, int64_t& j0, int64_t& kbeg, int& ktiles) {
     const int tile = u % tiles, split = u / tiles;
-    const int group_size = tiled::GROUP_M * tiles_n;
-    const int first_m = (tile / group_size) * tiled::GROUP_M;
-    const int gm = min(tiles_m - first_m, tiled::GROUP_M);
+    const int GM_ = g.group_m > 0 ? g.group_m : tiled::GROUP_M;
+    const int group_size = GM_ * tiles_n;
+    const int first_m = (tile / group_size) * GM_;
+    const int gm = min(tiles_m - first_m, GM_);
     const int local = tile % group_size;
     i0 = (int64_t)(first_m + local % gm) * BM;
     j0 = (int64_t)(local / gm) * BN;

@@ -40,6 +40,7 @@ struct GemmArgs {
   // splitk_reduce adds them in order.  kchunk >= k: no split, part == nullptr.
   int64_t kchunk;
   double* part;
+  int group_m;      // raster group height in tiles (L2 reuse); 0 = default
   // binary64 precision (the reference's 'f64' Matrix): only the hi planes
   // exist; a_lo / b_lo / c_lo are unused (dd_reference.cu, ALG_F64)
   int f64;
