@@ -329,8 +329,11 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t units = (int64_t)tiles_m * tiles_n * splits;
-  const int grid = std::getenv("DDB_TMA_NONPERSISTENT") ? (int)units
-                                                        : (int)(units < sms ? units : sms);
+  // Default: one CTA per unit (the hardware scheduler backfills SMs).  The
+  // persistent walk (one CTA per SM, DDB_TMA_PERSISTENT=1) measured the same
+  // speed but more DRAM reads (its CTAs drift apart in k across units).
+  const int grid = std::getenv("DDB_TMA_PERSISTENT") ? (int)(units < sms ? units : sms)
+                                                     : (int)units;
   kern<<<grid, NT, SMEM_BYTES, s>>>(g, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
                                     tiles_n, splits);
   return cudaGetLastError();
