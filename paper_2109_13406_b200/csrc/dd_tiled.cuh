@@ -87,7 +87,7 @@ constexpr int BK = 16;
 #endif
 constexpr int RN = 8;                              // fast: renormalise every RN steps
 constexpr int RF = 2;                              // cert: fold L into T every RF steps
-constexpr int GROUP_M = 12;                        // raster group (L2 reuse)
+constexpr int GROUP_M = 4;    // raster group height: 4 -> 34 GB of DRAM reads at 8192^3, 12 -> 81 GB (scripts/dram_sweep.sh)
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
