@@ -444,3 +444,54 @@ def test_cgemm_host_path_bitwise(idx):
     got = _run_cgemm(case, arr, "exact", on_device=False)
     for g_, o_ in zip(got, outs):
         assert _bits_equal_c(g_, o_), case
+
+
+# ---- out-of-bounds guard: NaN sentinels around and inside the operands ------
+
+def _guarded(planes, rows, cols, ld, guard=4096):
+    """Device planes embedded in NaN-filled buffers (NaN also in the ld padding)."""
+    import torch
+    out, views = [], []
+    for p in planes:
+        buf = np.full(len(p) + 2 * guard, np.nan)
+        body = p.copy()
+        for j in range(cols):
+            body[j * ld + rows:(j + 1) * ld] = np.nan        # padding rows of each column
+        buf[guard:guard + len(p)] = body
+        t = torch.from_numpy(buf).cuda()
+        out.append(t)
+        views.append(t[guard:guard + len(p)])
+    return out, tuple(views)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast", "twosum"])
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "N"), ("N", "T"), ("T", "T")])
+def test_kernels_never_touch_outside_the_operands(mode, ta, tb):
+    m, n, k, pad = 70, 45, 300, 2           # even ld: the TMA kernel takes NN
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A = random_dd(nra, nca, nra + pad, 31, 1)
+    B = random_dd(nrb, ncb, nrb + pad, 31, 2)
+    C = random_dd(m, n, m + pad, 31, 3)
+    # reference run on clean operands
+    a0, b0 = dev(nra, nca, nra + pad, A), dev(nrb, ncb, nrb + pad, B)
+    c0 = dev(m, n, m + pad, C)
+    Rgemm(ta, tb, m, n, k, 1.5, a0, nra + pad, b0, nrb + pad, 0.5, c0, m + pad, mode=mode)
+    ref = [p.cpu().numpy() for p in c0.store]
+    # guarded run: NaN everywhere the kernel must not read
+    abufs, av = _guarded(A, nra, nca, nra + pad)
+    bbufs, bv = _guarded(B, nrb, ncb, nrb + pad)
+    cbufs, cv = _guarded(C, m, n, m + pad)
+    a = DeviceMatrix(nra, nca, "dd", nra + pad, store=av)
+    b = DeviceMatrix(nrb, ncb, "dd", nrb + pad, store=bv)
+    c = DeviceMatrix(m, n, "dd", m + pad, store=cv)
+    Rgemm(ta, tb, m, n, k, 1.5, a, nra + pad, b, nrb + pad, 0.5, c, m + pad, mode=mode)
+    got = [p.cpu().numpy() for p in c.store]
+    for g_, r_ in zip(got, ref):
+        for j in range(n):
+            col = slice(j * (m + pad), j * (m + pad) + m)
+            assert bits_equal(g_[col], r_[col])
+            assert np.all(np.isnan(g_[j * (m + pad) + m:(j + 1) * (m + pad)]))  # C padding untouched
+    for buf in cbufs:
+        h = buf.cpu().numpy()
+        assert np.all(np.isnan(h[:4096])) and np.all(np.isnan(h[-4096:]))
