@@ -408,6 +408,120 @@ int oracle_dsyrk(char uplo, char trans, int64_t n, int64_t k, double alpha, cons
     return 0;
 }
 
+/* ---- complex precisions: Cgemm (level23.py:201-221 -> _gemm_core) --------
+ * 'cdd': planes re_hi, re_lo, im_hi, im_lo; CDD backend ops (elem.py:324-377):
+ *   add = (add2(re,re'), add2(im,im')), mul = (add2(mul2(xr,yr), -mul2(xi,yi)),
+ *   add2(mul2(xr,yi), mul2(xi,yr))).  A DDComplex has no __bool__, so for 'cdd'
+ *   `not alpha` / `not beta` are never true (beta == 0 multiplies C).
+ * 'c64': interleaved complex128; C64 backend mul (elem.py:313-318) evaluated
+ *   by numpy as re = (ac - bd) + (0*x - 0), im = 0 + (0 + x), x = ad + bc. */
+
+typedef struct { dd re, im; } cdd_t;
+
+static inline cdd_t c_add(cdd_t x, cdd_t y) { cdd_t r = {add2(x.re, y.re), add2(x.im, y.im)}; return r; }
+static inline dd dneg(dd x) { dd r = {-x.h, -x.l}; return r; }
+static inline cdd_t c_mul(cdd_t x, cdd_t y) {
+    cdd_t r = {add2(mul2(x.re, y.re), dneg(mul2(x.im, y.im))), add2(mul2(x.re, y.im), mul2(x.im, y.re))};
+    return r;
+}
+static inline cdd_t c_ld(const double *const *p, int64_t i) {
+    cdd_t r = {{p[0][i], p[1][i]}, {p[2][i], p[3][i]}};
+    return r;
+}
+
+int oracle_cgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double *alpha,
+                 const double *const *A, int64_t lda, const double *const *B, int64_t ldb,
+                 const double *beta, double *const *C, int64_t ldc) {
+    int rc = oracle_gemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+    if (rc) return rc;
+    int ta = upflag(transa), tb = upflag(transb);
+    int conja = ta == 'C', conjb = tb == 'C';
+    cdd_t al = {{alpha[0], alpha[1]}, {alpha[2], alpha[3]}};
+    cdd_t be = {{beta[0], beta[1]}, {beta[2], beta[3]}};
+    int beta_one = is_one(be.re) && is_zero(be.im);
+    if (m == 0 || n == 0 || (k == 0 && beta_one)) return 0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) {
+            int64_t ci = i + j * ldc;
+            cdd_t c0 = c_ld((const double *const *)C, ci), out;
+            if (ta == 'N') {
+                cdd_t c = beta_one ? c0 : c_mul(be, c0);
+                for (int64_t l = 0; l < k; ++l) {
+                    cdd_t bv = c_ld(B, tb == 'N' ? l + j * ldb : j + l * ldb);
+                    if (conjb) bv.im = dneg(bv.im);
+                    c = c_add(c, c_mul(c_ld(A, i + l * lda), c_mul(al, bv)));
+                }
+                out = c;
+            } else {
+                cdd_t acc = {{0.0, 0.0}, {0.0, 0.0}};
+                for (int64_t l = 0; l < k; ++l) {
+                    cdd_t av = c_ld(A, l + i * lda), bv = c_ld(B, tb == 'N' ? l + j * ldb : j + l * ldb);
+                    if (conja) av.im = dneg(av.im);
+                    if (conjb) bv.im = dneg(bv.im);
+                    acc = c_add(acc, c_mul(av, bv));
+                }
+                out = c_add(c_mul(al, acc), c_mul(be, c0));
+            }
+            C[0][ci] = out.re.h; C[1][ci] = out.re.l; C[2][ci] = out.im.h; C[3][ci] = out.im.l;
+        }
+    return 0;
+}
+
+typedef struct { double re, im; } z_t;
+static inline z_t z_mul(z_t x, z_t y) {
+    double r = x.re * y.re - x.im * y.im;
+    double xi = x.re * y.im + x.im * y.re;
+    z_t o = {r + (0.0 * xi - 0.0), 0.0 + (0.0 + xi)};
+    return o;
+}
+static inline z_t z_add(z_t x, z_t y) { z_t o = {x.re + y.re, x.im + y.im}; return o; }
+
+int oracle_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const double *alpha,
+                 const double *A, int64_t lda, const double *B, int64_t ldb, const double *beta,
+                 double *C, int64_t ldc) {
+    int rc = oracle_gemm_validate(transa, transb, m, n, k, lda, ldb, ldc);
+    if (rc) return rc;
+    int ta = upflag(transa), tb = upflag(transb);
+    int conja = ta == 'C', conjb = tb == 'C';
+    z_t al = {alpha[0], alpha[1]}, be = {beta[0], beta[1]};
+    int a0 = al.re == 0.0 && al.im == 0.0, b0 = be.re == 0.0 && be.im == 0.0;
+    int b1 = be.re == 1.0 && be.im == 0.0;
+    if (m == 0 || n == 0 || ((a0 || k == 0) && b1)) return 0;
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) {
+            int64_t ci = i + j * ldc;
+            z_t c0 = {C[2 * ci], C[2 * ci + 1]}, out;
+            if (a0) {
+                if (b1) continue;
+                if (b0) { out.re = 0.0; out.im = 0.0; } else out = z_mul(be, c0);
+            } else if (ta == 'N') {
+                z_t c = b1 ? c0 : (b0 ? (z_t){0.0, 0.0} : z_mul(be, c0));
+                for (int64_t l = 0; l < k; ++l) {
+                    int64_t bi = tb == 'N' ? l + j * ldb : j + l * ldb;
+                    z_t bv = {B[2 * bi], B[2 * bi + 1]};
+                    if (conjb) bv.im = -bv.im;
+                    int64_t ai = i + l * lda;
+                    z_t av = {A[2 * ai], A[2 * ai + 1]};
+                    c = z_add(c, z_mul(av, z_mul(al, bv)));
+                }
+                out = c;
+            } else {
+                z_t acc = {0.0, 0.0};
+                for (int64_t l = 0; l < k; ++l) {
+                    int64_t bi = tb == 'N' ? l + j * ldb : j + l * ldb, ai = l + i * lda;
+                    z_t av = {A[2 * ai], A[2 * ai + 1]}, bv = {B[2 * bi], B[2 * bi + 1]};
+                    if (conja) av.im = -av.im;
+                    if (conjb) bv.im = -bv.im;
+                    acc = z_add(acc, z_mul(av, bv));
+                }
+                z_t at = z_mul(al, acc);
+                out = b0 ? at : z_add(at, z_mul(be, c0));
+            }
+            C[2 * ci] = out.re; C[2 * ci + 1] = out.im;
+        }
+    return 0;
+}
+
 /* Scalar EFT entry points, for pinning the restatement against the
  * reference's scalar kernels (tests/test_oracle.py). */
 void oracle_add2(double xh, double xl, double yh, double yl, double *out) {

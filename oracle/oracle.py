@@ -61,6 +61,14 @@ def lib():
         L.oracle_dsyrk.restype = ctypes.c_int
         L.oracle_dsyrk.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64, ctypes.c_double,
                                    _dp, _i64, ctypes.c_double, _dp, _i64]
+        L.oracle_cgemm.restype = ctypes.c_int
+        L.oracle_cgemm.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64, _i64, ctypes.c_void_p,
+                                   ctypes.c_void_p, _i64, ctypes.c_void_p, _i64, ctypes.c_void_p,
+                                   ctypes.c_void_p, _i64]
+        L.oracle_zgemm.restype = ctypes.c_int
+        L.oracle_zgemm.argtypes = [ctypes.c_char, ctypes.c_char, _i64, _i64, _i64, ctypes.c_void_p,
+                                   ctypes.c_void_p, _i64, ctypes.c_void_p, _i64, ctypes.c_void_p,
+                                   ctypes.c_void_p, _i64]
         L.oracle_max_threads.restype = ctypes.c_int
         L.oracle_gemm_validate.restype = ctypes.c_int
         L.oracle_gemm_validate.argtypes = [ctypes.c_char, ctypes.c_char] + [_i64] * 6
@@ -112,6 +120,32 @@ def dgemm(transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc):
 def dsyrk(uplo, trans, n, k, alpha, a, lda, beta, c, ldc):
     return lib().oracle_dsyrk(_flag(uplo), _flag(trans), n, k, float(alpha), _ptr(a), lda,
                               float(beta), _ptr(c), ldc)
+
+
+def cgemm(transa, transb, m, n, k, alpha4, a4, lda, b4, ldb, beta4, c4, ldc):
+    """'cdd' Cgemm; a4/b4/c4 = four float64 planes, alpha4/beta4 four doubles."""
+    keep = []
+
+    def arr(vals):
+        x = (ctypes.c_double * 4)(*vals)
+        keep.append(x)
+        return ctypes.cast(x, ctypes.c_void_p)
+
+    def ptrs(planes):
+        x = (ctypes.c_void_p * 4)(*(p.ctypes.data for p in planes))
+        keep.append(x)
+        return ctypes.cast(x, ctypes.c_void_p)
+    return lib().oracle_cgemm(_flag(transa), _flag(transb), m, n, k, arr(alpha4), ptrs(a4), lda,
+                              ptrs(b4), ldb, arr(beta4), ptrs(c4), ldc)
+
+
+def zgemm(transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc):
+    """'c64' Cgemm on complex128 arrays."""
+    al = (ctypes.c_double * 2)(alpha.real, alpha.imag)
+    be = (ctypes.c_double * 2)(beta.real, beta.imag)
+    return lib().oracle_zgemm(_flag(transa), _flag(transb), m, n, k,
+                              ctypes.cast(al, ctypes.c_void_p), a.ctypes.data, lda, b.ctypes.data,
+                              ldb, ctypes.cast(be, ctypes.c_void_p), c.ctypes.data, ldc)
 
 
 def add2(x, y):

@@ -15,7 +15,9 @@ def bits_equal(a, b):
     return bool(np.all(same | both_nan))
 
 
-CASES = [c for c in golden.load_cases() if c[0]["routine"] != "Cgemm"]
+ALL = list(golden.load_cases())
+CASES = [c for c in ALL if c[0]["routine"] != "Cgemm"]
+CCASES = [c for c in ALL if c[0]["routine"] == "Cgemm"]
 
 
 @pytest.mark.parametrize("idx", range(len(CASES)))
@@ -87,3 +89,34 @@ def test_oracle_known_answer_integer_instance():
 def test_oracle_validation_indices(args, idx):
     ta, tb, m, n, k, lda, ldb, ldc = args
     assert oracle.lib().oracle_gemm_validate(ta.encode(), tb.encode(), m, n, k, lda, ldb, ldc) == idx
+
+
+@pytest.mark.parametrize("idx", range(len(CCASES)))
+def test_oracle_cgemm_matches_reference_bitwise(idx):
+    case, arr, outs, _ = CCASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"]
+    al = complex(*case["alpha_v"])
+    be = complex(*case["beta_v"])
+    with np.errstate(all="ignore"):
+        if case["precision"] == "cdd":
+            from paper_2109_13406_b200.matrix import to_cdd
+            a4 = [np.ascontiguousarray(arr[f"A_{p}"]) for p in ("rh", "rl", "ih", "il")]
+            b4 = [np.ascontiguousarray(arr[f"B_{p}"]) for p in ("rh", "rl", "ih", "il")]
+            c4 = [arr[f"C_{p}"].copy() for p in ("rh", "rl", "ih", "il")]
+            alv = to_cdd(al if case["alpha"] != "zr" else case["alpha_v"][0])
+            rc = oracle.cgemm(case["transa"], case["transb"], case["m"], case["n"], case["k"],
+                              alv, a4, case["lda"], b4, case["ldb"], to_cdd(be), c4, case["ldc"])
+            got = c4
+        else:
+            c = arr["C_z"].copy()
+            rc = oracle.zgemm(case["transa"], case["transb"], case["m"], case["n"], case["k"],
+                              al, np.ascontiguousarray(arr["A_z"]), case["lda"],
+                              np.ascontiguousarray(arr["B_z"]), case["ldb"], be, c, case["ldc"])
+            got = [c]
+    assert rc == 0
+    for g_, o_ in zip(got, outs):
+        g_, o_ = np.asarray(g_), np.asarray(o_)
+        if g_.dtype.kind == "c":
+            assert bits_equal(g_.real.copy(), o_.real.copy()) and bits_equal(g_.imag.copy(), o_.imag.copy()), case
+        else:
+            assert bits_equal(g_, o_), case
