@@ -79,6 +79,9 @@ constexpr int BK = 16;
                          // step 0 reused for the whole k-tile, 2 = skip the k-tile
                          // loads + barrier after the first tile
 #endif
+#ifndef DDB_EXACT_SEL
+#define DDB_EXACT_SEL 0  // exact mode: ordered-Fast2Sum TwoSums (bit-identical, 23 vs 29 ops)
+#endif
 #ifndef DDB_UNR
 #define DDB_UNR 16       // fast modes: k-steps per loop body (divides BK, multiple of RF)
 #endif
@@ -203,7 +206,8 @@ __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN
         H[a][b] = Tn;
       } else if (ALG == ALG_EXACT) {
         const dd p = mul2_nc(dd{ah[a], al[a]}, dd{bh[b], bl[b]});
-        const dd c = add2_nc(dd{H[a][b], L[a][b]}, p);
+        const dd c = DDB_EXACT_SEL ? add2_nc_sel(dd{H[a][b], L[a][b]}, p)
+                                   : add2_nc(dd{H[a][b], L[a][b]}, p);
         H[a][b] = c.h;
         L[a][b] = c.l;
       } else {

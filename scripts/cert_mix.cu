@@ -70,7 +70,31 @@ __global__ void __launch_bounds__(256, MINB) mix(double* out, int iters, double 
   for (int it = 0; it < iters * (16 / UNR); ++it) {
 #pragma unroll
     for (int kk = 0; kk < UNR; ++kk) {
-      if (LDS) {
+      if (LDS == 3) {
+        const int k2 = (it * UNR + kk) & 15;
+#pragma unroll
+        for (int g = 0; g < TM / 2; ++g) {
+          const double2 h = *reinterpret_cast<const double2*>(&sm[0][k2][(g * 32 + tx * 2) & 63]);
+          ah[2 * g] = h.x; ah[2 * g + 1] = h.y;
+        }
+#pragma unroll
+        for (int g = 0; g < TN / 2; ++g) {
+          const double2 h = *reinterpret_cast<const double2*>(&sm[2][k2][g * 32 + ty * 2]);
+          bh[2 * g] = h.x; bh[2 * g + 1] = h.y;
+        }
+      } else if (LDS == 4) {
+        const int k2 = (it * UNR + kk) & 15;
+#pragma unroll
+        for (int g = 0; g < TM; ++g) {
+          ah[g] = sm[0][k2][((g >> 1) * 32 + tx * 2 + (g & 1)) & 63];
+          al[g] = sm[1][k2][((g >> 1) * 32 + tx * 2 + (g & 1)) & 63];
+        }
+#pragma unroll
+        for (int g = 0; g < TN; ++g) {
+          bh[g] = sm[2][k2][(g >> 1) * 32 + ty * 2 + (g & 1)];
+          bl[g] = sm[3][k2][(g >> 1) * 32 + ty * 2 + (g & 1)];
+        }
+      } else if (LDS) {
         const int k2 = (it * UNR + kk) & 15;
 #pragma unroll
         for (int g = 0; g < TM / 2; ++g) {
@@ -149,10 +173,8 @@ int main() {
   cudaMalloc(&out, 8);
   run<8, 4, 1, 2>(sms, out);
   run<8, 4, 1, 2, 1>(sms, out);
-  run<8, 4, 1, 2, 2>(sms, out);
+  run<8, 4, 1, 2, 3>(sms, out);
+  run<8, 4, 1, 2, 4>(sms, out);
   run<8, 4, 1, 4, 2>(sms, out);
-  run<8, 4, 1, 8, 2>(sms, out);
-  run<4, 4, 2, 2, 2>(sms, out);
-  run<4, 4, 2, 4, 2>(sms, out);
   return 0;
 }
