@@ -21,7 +21,6 @@
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 
-#include <mutex>
 
 #include "internal.h"
 
@@ -54,21 +53,18 @@ static cudaError_t convert(const double* hi, int64_t ld, int64_t rows, int64_t c
   return cudaGetLastError();
 }
 
-namespace {
-std::mutex g_mu;
-cublasHandle_t g_handles[64] = {};
-}  // namespace
-
+// One cuBLAS handle per (host thread, device): cublasSetStream + GemmEx on a
+// shared handle would race between threads calling on different streams.
 static cublasHandle_t handle_for_current_device() {
+  thread_local cublasHandle_t handles[64] = {};
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(g_mu);
-  if (g_handles[dev] == nullptr) {
+  if (handles[dev] == nullptr) {
     cublasHandle_t h;
     if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) return nullptr;
-    g_handles[dev] = h;
+    handles[dev] = h;
   }
-  return g_handles[dev];
+  return handles[dev];
 }
 
 size_t bound_workspace_bytes(const GemmArgs& g) {
