@@ -495,3 +495,40 @@ def test_kernels_never_touch_outside_the_operands(mode, ta, tb):
     for buf in cbufs:
         h = buf.cpu().numpy()
         assert np.all(np.isnan(h[:4096])) and np.all(np.isnan(h[-4096:]))
+
+
+def test_concurrent_calls_on_two_streams_from_two_threads():
+    """The C ABI is reentrant: two host threads, two streams, fast mode (cuBLAS
+    bound GEMM per thread) and exact mode at once, results as if sequential."""
+    import threading
+    import torch
+    m, n, k = 200, 150, 700
+    A, B, C = random_dd(m, k, m, 41, 1), random_dd(k, n, k, 41, 2), random_dd(m, n, m, 41, 3)
+    refs = {}
+    for mode in ("fast", "exact"):
+        c = dev(m, n, m, C)
+        Rgemm("N", "N", m, n, k, 1.5, dev(m, k, m, A), m, dev(k, n, k, B), k, 0.5, c, m, mode=mode)
+        refs[mode] = [p.cpu().numpy() for p in c.store]
+    out, errs = {}, []
+
+    def worker(mode):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for _ in range(5):
+                    c = dev(m, n, m, C)
+                    Rgemm("N", "N", m, n, k, 1.5, dev(m, k, m, A), m, dev(k, n, k, B), k, 0.5,
+                          c, m, mode=mode)
+                s.synchronize()
+                out[mode] = [p.cpu().numpy() for p in c.store]
+        except Exception as e:   # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=worker, args=(md,)) for md in ("fast", "exact")]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for mode in ("fast", "exact"):
+        assert all(bits_equal(a, b) for a, b in zip(out[mode], refs[mode])), mode
