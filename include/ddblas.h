@@ -118,10 +118,26 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
                    const double* a, int64_t lda, const double* b, int64_t ldb, const double* beta,
                    double* c, int64_t ldc, void* stream);
 
+/* Cholesky: mpkit.mplapack.Rpotrf (mplapack/chol.py:21-65), dd, in place.
+ * uplo 'L': A = L L^T, 'U': A = U^T U; only that triangle is read / written.
+ * Blocked right-looking (block width nb; <= 0 = default 128 or
+ * $DDB_POTRF_NB) with the trailing updates done by ddb_rsyrk in `mode`; in
+ * exact mode the factor is bit-identical to the reference's unblocked
+ * order for operands inside the safe window.  *info (host int) = 0, or
+ * j + 1 for the first pivot that is NaN or <= 0, whose value is left in
+ * A(j, j) with the later columns as the reference leaves them (chol.py:44).
+ * Returns 0 / the reference argument index (1 uplo, 2 n, 4 lda) / DDB_E*.
+ * Synchronises `stream` (info is a host value). */
+int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
+               int mode, void* stream, int* info);
+int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
+                    int mode, void* stream, int* info);
+
 /* Argument checks alone (no device work): reference index or 0. */
 int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
                        int64_t lda, int64_t ldb, int64_t ldc);
 int ddb_rsyrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc);
+int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda);
 
 const char* ddb_last_error(void);
 int ddb_version(void);

@@ -531,3 +531,144 @@ void oracle_mul2(double xh, double xl, double yh, double yl, double *out) {
     dd x = {xh, xl}, y = {yh, yl}, r = mul2(x, y); out[0] = r.h; out[1] = r.l;
 }
 void oracle_two_prod(double a, double b, double *out) { two_prod(a, b, &out[0], &out[1]); }
+
+/* ---- Rpotrf (mplapack/chol.py:21-65), unblocked, the reference's order ----
+ * Scalar DDouble operations (ddarith.py): _canon :68-71, _add2 :79-90,
+ * _mul21 :103-110, _div2 :113-131, _sqrt2 :142-163; element-wise add / mul
+ * are the vectorised add2 / mul2 above; sum_ltr (elem.py:261-283) is add2
+ * from (0, 0). */
+static inline dd canon(double h, double l) { dd r = {h, isfinite(h) ? l : 0.0}; return r; }
+
+static dd add2_s(dd x, dd y) {
+    double s0 = x.h + y.h;
+    if (!isfinite(s0)) { dd r = {s0, 0.0}; return r; }
+    dd r = add2(x, y);
+    return canon(r.h, r.l);
+}
+
+static dd mul21_s(dd x, double y) {
+    double p, e;
+    two_prod(x.h, y, &p, &e);
+    if (!(isfinite(p) && isfinite(e))) return canon(p, 0.0);
+    e = e + x.l * y;
+    double s, t;
+    quick_two_sum(p, e, &s, &t);
+    return canon(s, t);
+}
+
+static dd div2_s(dd x, dd y) {
+    dd r;
+    if (y.h == 0.0) {
+        r.l = 0.0;
+        r.h = x.h == 0.0 ? NAN : copysign(INFINITY, x.h) * copysign(1.0, y.h);
+        return r;
+    }
+    if (!(isfinite(x.h) && isfinite(y.h))) {
+        if (isinf(y.h)) {
+            r.l = 0.0;
+            r.h = isinf(x.h) ? NAN : copysign(0.0, x.h) * copysign(1.0, y.h);
+            return r;
+        }
+        return canon(x.h * copysign(1.0, y.h), 0.0);
+    }
+    double q1 = x.h / y.h;
+    dd m = mul21_s(y, q1), nm = {-m.h, -m.l};
+    r = add2_s(x, nm);
+    double q2 = r.h / y.h;
+    m = mul21_s(y, q2); nm.h = -m.h; nm.l = -m.l;
+    r = add2_s(r, nm);
+    double q3 = r.h / y.h;
+    double a, b;
+    quick_two_sum(q1, q2, &a, &b);
+    dd ab = {a, b}, c = {q3, 0.0};
+    return add2_s(ab, c);
+}
+
+static dd sqrt2_s(dd v) {
+    dd z = {0.0, 0.0};
+    if (v.h == 0.0 && v.l == 0.0) return z;
+    if (!isfinite(v.h)) { dd r = {v.h, 0.0}; return r; }
+    double h = v.h, l = v.l;
+    int shift = 0;
+    if (h >= 0x1p996) { h = ldexp(h, -106); l = ldexp(l, -106); shift = 53; }
+    else if (h <= 0x1p-996) { h = ldexp(h, 106); l = ldexp(l, 106); shift = -53; }
+    double x = 1.0 / sqrt(h);
+    double ax = h * x;
+    double p, e;
+    two_prod(ax, ax, &p, &e);
+    dd hv = {h, l}, pe = {-p, -e};
+    dd r = add2_s(hv, pe);
+    double s, e2;
+    quick_two_sum(ax, r.h * (x * 0.5), &s, &e2);
+    if (shift) { s = ldexp(s, shift); e2 = ldexp(e2, shift); }
+    return canon(s, e2);
+}
+
+int oracle_potrf_validate(char uplo, int64_t n, int64_t lda) {
+    int u = upflag(uplo);
+    if (u != 'U' && u != 'L') return 1;
+    if (n < 0) return 2;
+    if (lda < (n > 1 ? n : 1)) return 4;
+    return 0;
+}
+
+/* Returns the reference argument index (> 0) on invalid arguments, else 0
+ * with *info = 0 or the first failing pivot + 1 (chol.py:44-46). */
+int oracle_rpotrf(char uplo, int64_t n, double *Ah, double *Al, int64_t lda, int64_t *info) {
+    int rc = oracle_potrf_validate(uplo, n, lda);
+    if (rc) return rc;
+    *info = 0;
+    const int upper = upflag(uplo) == 'U';
+#define AT(i, j) ((i) + (j) * lda)
+    for (int64_t j = 0; j < n; ++j) {
+        dd dot = {0.0, 0.0};
+        for (int64_t l = 0; l < j; ++l) {
+            int64_t x = upper ? AT(l, j) : AT(j, l);
+            dd h = {Ah[x], Al[x]};
+            dot = add2(dot, mul2(h, h));
+        }
+        dd a = {Ah[AT(j, j)], Al[AT(j, j)]}, nd = {-dot.h, -dot.l};
+        dd ajj = add2_s(a, nd);
+        int bad = isnan(ajj.h + ajj.l) || ajj.h < 0.0 || (ajj.h == 0.0 && !(ajj.l > 0.0));
+        if (bad) {
+            Ah[AT(j, j)] = ajj.h; Al[AT(j, j)] = ajj.l;
+            *info = j + 1;
+            return 0;
+        }
+        ajj = sqrt2_s(ajj);
+        Ah[AT(j, j)] = ajj.h; Al[AT(j, j)] = ajj.l;
+        if (j == n - 1) break;
+        dd one = {1.0, 0.0};
+        dd rec = div2_s(one, ajj);
+        for (int64_t q = j + 1; q < n; ++q) {
+            dd v;
+            if (upper) {
+                dd temp = {0.0, 0.0};
+                for (int64_t l = 0; l < j; ++l) {
+                    dd c = {Ah[AT(l, q)], Al[AT(l, q)]}, h = {Ah[AT(l, j)], Al[AT(l, j)]};
+                    temp = add2(temp, mul2(c, h));
+                }
+                dd elt = {Ah[AT(j, q)], Al[AT(j, q)]}, nt = {-temp.h, -temp.l};
+                v = mul2(rec, add2(elt, nt));
+                Ah[AT(j, q)] = v.h; Al[AT(j, q)] = v.l;
+            } else {
+                dd tail = {Ah[AT(q, j)], Al[AT(q, j)]};
+                for (int64_t l = 0; l < j; ++l) {
+                    dd t = {-Ah[AT(j, l)], -Al[AT(j, l)]}, c = {Ah[AT(q, l)], Al[AT(q, l)]};
+                    tail = add2(tail, mul2(t, c));
+                }
+                v = mul2(rec, tail);
+                Ah[AT(q, j)] = v.h; Al[AT(q, j)] = v.l;
+            }
+        }
+    }
+#undef AT
+    return 0;
+}
+
+void oracle_div2(double xh, double xl, double yh, double yl, double *out) {
+    dd x = {xh, xl}, y = {yh, yl}, r = div2_s(x, y); out[0] = r.h; out[1] = r.l;
+}
+void oracle_sqrt2(double h, double l, double *out) {
+    dd v = {h, l}, r = sqrt2_s(v); out[0] = r.h; out[1] = r.l;
+}

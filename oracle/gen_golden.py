@@ -222,9 +222,51 @@ def syrk_cases():
     return cases
 
 
+def potrf_cases():
+    """Rpotrf (mplapack/chol.py:21-65): both triangles, ragged sizes, padded
+    lda, binary64-valued entries, failing pivots (early / late / NaN / zero),
+    and scales that reach the scalar sqrt's pre-scaling branches."""
+    cases = []
+    seed = 1500
+    for uplo in ("L", "U", "l"):
+        for n, pad in ((1, 0), (2, 1), (7, 0), (33, 2), (70, 0), (100, 3)):
+            if uplo == "l" and n > 7:
+                continue
+            cases.append(dict(routine="Rpotrf", uplo=uplo, n=n, pad=(pad,), seed=seed))
+            seed += 1
+    for uplo in ("L", "U"):
+        for sp, n in (("lo0", 40), ("neg_pivot", 40), ("late_fail", 70), ("nan_pivot", 12),
+                      ("zero", 1), ("lo_only", 1), ("scale_up", 40), ("scale_huge", 70),
+                      ("scale_tiny", 70)):
+            cases.append(dict(routine="Rpotrf", uplo=uplo, n=n, pad=(1,), seed=seed, special=sp))
+            seed += 1
+    return cases
+
+
+def run_case_potrf(case, store):
+    sys.path.insert(0, REF)
+    import mpkit.mpblas as mb
+    from mpkit.mplapack import Rpotrf
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    n = case["n"]
+    a = _matrix(mb, n, n, lds["lda"], (arrays["A_hi"], arrays["A_lo"]))
+    with np.errstate(all="ignore"):
+        info = Rpotrf(case["uplo"], n, a, lds["lda"])
+    case["info"] = int(info)
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    store["arrays"][f"c{cid}_out_hi"] = np.asarray(a.store[0], dtype=np.float64)
+    store["arrays"][f"c{cid}_out_lo"] = np.asarray(a.store[1], dtype=np.float64)
+    store["cases"].append(case)
+
+
 def run_case(mb, DDouble, case, store):
     if case["routine"] == "Cgemm":
         return run_case_complex(mb, case, store)
+    if case["routine"] == "Rpotrf":
+        return run_case_potrf(case, store)
     alpha = ALPHAS[case["alpha"]]
     beta = BETAS[case["beta"]]
     if case.get("precision") == "f64":
@@ -319,15 +361,26 @@ def eft_vectors(elem):
         ah, al = elem._v_add2(xh, xl, yh, yl)
         mh, ml = elem._v_mul2(xh, xl, yh, yl)
         p, e = elem._v_two_prod(xh, yh)
+    # the scalar DDouble division and square root (ddarith.py:113-163) that
+    # Rpotrf uses for its pivots
+    from mpkit import ddarith
+    div = [ddarith._div2(*v) for v in zip(xh.tolist(), xl.tolist(), yh.tolist(), yl.tolist())]
+    sh = g.uniform(0.5, 1.0, n) * 2.0 ** g.integers(-1070, 1020, n)
+    sl = sh * g.uniform(-1, 1, n) * 2.0 ** -54
+    sh[:4] = (0.0, np.inf, 2.0 ** 1000, 2.0 ** -1060)
+    sl[:4] = 0.0
+    sq = [ddarith._sqrt2(h, l) for h, l in zip(sh.tolist(), sl.tolist())]
     return dict(xh=xh, xl=xl, yh=yh, yl=yl, add_h=ah, add_l=al, mul_h=mh, mul_l=ml,
-                tp_p=p, tp_e=e)
+                tp_p=p, tp_e=e, div_h=np.array([d[0] for d in div]),
+                div_l=np.array([d[1] for d in div]), sq_in_h=sh, sq_in_l=sl,
+                sq_h=np.array([q[0] for q in sq]), sq_l=np.array([q[1] for q in sq]))
 
 
 def main():
     mb, elem, DDouble = _ref()
     os.makedirs(OUT, exist_ok=True)
     store = {"cases": [], "arrays": {}}
-    for case in gemm_cases() + syrk_cases() + f64_cases() + complex_cases():
+    for case in gemm_cases() + syrk_cases() + f64_cases() + complex_cases() + potrf_cases():
         run_case(mb, DDouble, case, store)
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
     with open(os.path.join(OUT, "cases.json"), "w") as f:

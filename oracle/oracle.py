@@ -70,6 +70,15 @@ def lib():
                                    ctypes.c_void_p, _i64, ctypes.c_void_p, _i64, ctypes.c_void_p,
                                    ctypes.c_void_p, _i64]
         L.oracle_max_threads.restype = ctypes.c_int
+        L.oracle_rpotrf.restype = ctypes.c_int
+        L.oracle_rpotrf.argtypes = [ctypes.c_char, _i64, _dp, _dp, _i64,
+                                    ctypes.POINTER(ctypes.c_int64)]
+        L.oracle_potrf_validate.restype = ctypes.c_int
+        L.oracle_potrf_validate.argtypes = [ctypes.c_char, _i64, _i64]
+        L.oracle_div2.restype = None
+        L.oracle_div2.argtypes = [ctypes.c_double] * 4 + [_dp]
+        L.oracle_sqrt2.restype = None
+        L.oracle_sqrt2.argtypes = [ctypes.c_double] * 2 + [_dp]
         L.oracle_gemm_validate.restype = ctypes.c_int
         L.oracle_gemm_validate.argtypes = [ctypes.c_char, ctypes.c_char] + [_i64] * 6
         L.oracle_syrk_validate.restype = ctypes.c_int
@@ -146,6 +155,27 @@ def zgemm(transa, transb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc):
     return lib().oracle_zgemm(_flag(transa), _flag(transb), m, n, k,
                               ctypes.cast(al, ctypes.c_void_p), a.ctypes.data, lda, b.ctypes.data,
                               ldb, ctypes.cast(be, ctypes.c_void_p), c.ctypes.data, ldc)
+
+
+def rpotrf(uplo, n, a_hi, a_lo, lda):
+    """In-place unblocked dd Cholesky in the reference's order
+    (mplapack/chol.py:21-65).  Returns (rc, info): rc = reference argument
+    index of an invalid argument, else 0; info as chol.py returns it."""
+    info = ctypes.c_int64(0)
+    rc = lib().oracle_rpotrf(_flag(uplo), n, _ptr(a_hi), _ptr(a_lo), lda, ctypes.byref(info))
+    return rc, int(info.value)
+
+
+def div2(x, y):
+    out = np.zeros(2)
+    lib().oracle_div2(x[0], x[1], y[0], y[1], _ptr(out))
+    return float(out[0]), float(out[1])
+
+
+def sqrt2(x):
+    out = np.zeros(2)
+    lib().oracle_sqrt2(x[0], x[1], _ptr(out))
+    return float(out[0]), float(out[1])
 
 
 def add2(x, y):

@@ -6,19 +6,23 @@ compute runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI in
 """
 
 from .matrix import BlasError, DeviceMatrix, HostMatrix, to_dd
+from .lapack import Rpotrf
 from .mpblas import Cgemm, Rgemm, Rsyrk, default_mode
 
-__all__ = ["Rgemm", "Rsyrk", "Cgemm", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
+__all__ = ["Rgemm", "Rsyrk", "Cgemm", "Rpotrf", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
            "default_mode", "flop_count"]
 
 
 def flop_count(routine, n, k=None, m=None):
     """dd flops as the reference bench counts them (mpkit/bench.py:51-70;
-    m and k default to n): Rgemm 2mnk, Rsyrk n^2*k + n*k = n(n+1)k."""
+    m and k default to n): Rgemm 2mnk, Rsyrk n^2*k + n*k = n(n+1)k,
+    Rpotrf n^3/3."""
     m = n if m is None else m
     k = n if k is None else k
     if routine == "Rgemm":
         return 2.0 * m * n * k
     if routine == "Rsyrk":
         return float(n * n * k + n * k)
+    if routine == "Rpotrf":
+        return n ** 3 / 3.0
     raise ValueError(f"unknown routine {routine!r}")

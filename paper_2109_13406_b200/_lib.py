@@ -25,7 +25,8 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rgemm_validate", "ddb_rsyrk_validate", "ddb_last_error",
            "ddb_version", "ddb_launch_count", "ddb_last_route", "ddb_fp64_peak_probe",
            "ddb_dgemm", "ddb_dsyrk", "ddb_dgemm_host", "ddb_dsyrk_host",
-           "ddb_cgemm", "ddb_cgemm_host", "ddb_zgemm", "ddb_zgemm_host")
+           "ddb_cgemm", "ddb_cgemm_host", "ddb_zgemm", "ddb_zgemm_host",
+           "ddb_rpotrf", "ddb_rpotrf_host", "ddb_rpotrf_validate")
 
 _lib = None
 
@@ -67,6 +68,13 @@ def load():
         f = getattr(L, name)
         f.restype = ctypes.c_int
         f.argtypes = args
+    po = [_c, _i64, _dp, _dp, _i64, _i64, ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_int)]
+    for name in ("ddb_rpotrf", "ddb_rpotrf_host"):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = po
+    L.ddb_rpotrf_validate.restype = ctypes.c_int
+    L.ddb_rpotrf_validate.argtypes = [_c, _i64, _i64]
     L.ddb_rgemm_validate.restype = ctypes.c_int
     L.ddb_rgemm_validate.argtypes = [_c, _c] + [_i64] * 6
     L.ddb_rsyrk_validate.restype = ctypes.c_int

@@ -577,4 +577,137 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
   return stage_out1(c, C, sc, s);
 }
 
+// ---- blocked Cholesky (dd_potrf.cu) ----------------------------------------
+
+int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {
+  const int u = upflag(uplo);
+  if (u != 'U' && u != 'L') return 1;                 // chol.py:24-26
+  if (n < 0) return 2;                                // chol.py:28
+  if (lda < (n > 1 ? n : 1)) return 4;                // chol.py:29
+  return 0;
+}
+
+int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
+               int mode, void* stream, int* info) {
+  const int rc = ddb_rpotrf_validate(uplo, n, lda);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr) {
+    g_last_error = info == nullptr ? "info pointer is null" : "unknown mode";
+    return DDB_EINVAL;
+  }
+  *info = 0;
+  if (n == 0) return DDB_OK;                          // chol.py:30-31
+  if (nb <= 0) {
+    static const int64_t nb_env = [] {
+      const char* v = std::getenv("DDB_POTRF_NB");
+      return v ? (int64_t)std::atoll(v) : (int64_t)0;
+    }();
+    nb = nb_env > 0 ? nb_env : 128;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
+  PotrfArgs p{};
+  p.n = n; p.lda = lda; p.upper = upflag(uplo) == 'U';
+  p.a_hi = a_hi; p.a_lo = a_lo;
+  const bool blocked = n > nb;
+  const size_t head = 256, vec = sizeof(double) * (size_t)n;
+  const size_t full = blocked ? sizeof(double) * (size_t)n * n : 0;
+  const size_t tpan = blocked && p.upper ? sizeof(double) * (size_t)n * nb : 0;
+  const size_t ws_bytes = head + 4 * vec + 2 * full + 2 * tpan;
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
+  if (e != cudaSuccess) return fail(e, "workspace allocation");
+  char* w = static_cast<char*>(ws);
+  p.info = reinterpret_cast<int*>(w);
+  double* d = reinterpret_cast<double*>(w + head);
+  p.dh = d; p.dl = d + n;
+  double* d0h = d + 2 * n;
+  double* d0l = d + 3 * n;
+  p.d0_hi = d0h; p.d0_lo = d0l;
+  double* big = d + 4 * n;                            // backup (lower) or S (upper)
+  double* tp = big + 2 * (size_t)n * (blocked ? n : 0);
+  const char* what = "rpotrf";
+  int nl = 0;
+  e = cudaMemsetAsync(ws, 0, head + 2 * vec, s);
+  const size_t dpitch = sizeof(double) * (size_t)(lda + 1);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0h, 8, a_hi, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0l, 8, a_lo, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && blocked) {
+    if (p.upper) {
+      p.s_hi = big; p.s_lo = big + (size_t)n * n; p.lds = n;
+      p.t_hi = tp; p.t_lo = tp + (size_t)n * nb;
+      e = cudaMemsetAsync(big, 0, 2 * full, s);
+    } else {
+      double* bh = big;
+      double* bl = big + (size_t)n * n;
+      p.b_hi = bh; p.b_lo = bl;
+      const size_t pitch = sizeof(double) * (size_t)lda, row = sizeof(double) * (size_t)n;
+      e = cudaMemcpy2DAsync(bh, row, a_hi, pitch, row, n, cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess) e = cudaMemcpy2DAsync(bl, row, a_lo, pitch, row, n, cudaMemcpyDeviceToDevice, s);
+    }
+  }
+  int rc2 = DDB_OK;
+  for (int64_t j0 = 0; e == cudaSuccess && rc2 == DDB_OK && j0 < n; j0 += nb) {
+    const int64_t j1 = j0 + nb < n ? j0 + nb : n;
+    for (int64_t j = j0; j < j1 && e == cudaSuccess; ++j) {
+      e = launch_potrf_col(p, j0, j, s);
+      ++nl;
+    }
+    if (e != cudaSuccess || j1 >= n) break;
+    const int64_t n2 = n - j1;
+    if (!p.upper) {
+      // A22 -= L21 L21^T in place (chol.py:57-62 order, continued)
+      rc2 = ddb_rsyrk('L', 'N', n2, j1 - j0, -1.0, 0.0, a_hi + j1 + j0 * lda, a_lo + j1 + j0 * lda,
+                      lda, 1.0, 0.0, a_hi + j1 + j1 * lda, a_lo + j1 + j1 * lda, lda, mode, stream);
+    } else {
+      // S22 += U12^T U12 (chol.py:50-53 dot products, continued)
+      e = launch_potrf_transpose(p, j0, j1, (int)(j1 - j0), n2, s);
+      ++nl;
+      if (e == cudaSuccess)
+        rc2 = ddb_rsyrk('L', 'N', n2, j1 - j0, 1.0, 0.0, p.t_hi, p.t_lo, n2, 1.0, 0.0,
+                        p.s_hi + j1 + j1 * n, p.s_lo + j1 + j1 * n, n, mode, stream);
+    }
+  }
+  if (e == cudaSuccess && rc2 == DDB_OK && blocked && !p.upper) {
+    e = launch_potrf_restore(p, s);
+    ++nl;
+  }
+  g_launches += nl;
+  int hinfo = 0;
+  if (e == cudaSuccess && rc2 == DDB_OK) {
+    e = cudaMemcpyAsync(&hinfo, p.info, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  if (rc2 != DDB_OK) return rc2;
+  if (e != cudaSuccess) return fail(e, what);
+  if (e2 != cudaSuccess) return fail(e2, "workspace free");
+  *info = hinfo;
+  return DDB_OK;
+}
+
+int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
+                    int mode, void* stream, int* info) {
+  int rc = ddb_rpotrf_validate(uplo, n, lda);
+  if (rc) return rc;
+  if (info == nullptr) {
+    g_last_error = "info pointer is null";
+    return DDB_EINVAL;
+  }
+  *info = 0;
+  if (n == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t sa = span(n, n, lda);
+  DevBuf A;
+  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
+  rc = ddb_rpotrf(uplo, n, A.p, A.p + sa, lda, nb, mode, stream, info);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(a_hi, A.p, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(a_lo, A.p + sa, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
 }  // extern "C"

@@ -89,4 +89,23 @@ cudaError_t launch_cgemm_combine(const CgemmArgs& g, const double* pr_h, const d
                                  const double* pi_h, const double* pi_l, cudaStream_t s);
 cudaError_t launch_zgemm(const ZgemmArgs& g, cudaStream_t s);
 
+// blocked Cholesky (dd_potrf.cu); column-major, every plane pair (hi, lo)
+struct PotrfArgs {
+  int64_t n, lda;
+  int upper;
+  double *a_hi, *a_lo;
+  const double *d0_hi, *d0_lo;  // original diagonal
+  double *dh, *dl;              // pivot dot products accumulated so far
+  double *s_hi, *s_lo;          // upper: lower-stored accumulator S, ld = lds
+  int64_t lds;
+  double *t_hi, *t_lo;          // upper: the transposed panel U12^T
+  const double *b_hi, *b_lo;    // lower: backup of the input (ld = n)
+  int* info;                    // device: first failing pivot + 1, or 0
+};
+
+cudaError_t launch_potrf_col(const PotrfArgs& p, int64_t j0, int64_t j, cudaStream_t s);
+cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,
+                                   int64_t rows, cudaStream_t s);
+cudaError_t launch_potrf_restore(const PotrfArgs& p, cudaStream_t s);
+
 }  // namespace ddb

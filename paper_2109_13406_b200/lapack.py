@@ -1,0 +1,67 @@
+"""Drop-in ``Rpotrf`` (dd Cholesky) whose O(n^3) work runs as GPU ``Rsyrk``.
+
+Same call surface, validation order, BlasError indices and return value as
+the reference (``/root/reference/pkg/src/mpkit/mplapack/chol.py:21-65``):
+
+  info = Rpotrf(uplo, n, a, lda=None)
+
+A = L*L^T (uplo 'L') or U^T*U ('U') in place on that triangle; info = 0, or
+j + 1 for the first pivot that is NaN or <= 0, whose value is left in A(j, j)
+with the later entries as the reference leaves them.  Keywords:
+
+  mode  "exact": bit-identical to the reference (operands inside the safe
+        window), blocked, the trailing updates are exact-mode Rsyrk calls;
+        "fast" (default, env DDBLAS_MODE) / "twosum": the same blocked
+        algorithm with those modes' Rsyrk -- residual within the reference's
+        testkit threshold (testkit.residual_chol < 30); "reference": the
+        trailing updates on the checked one-thread-per-element kernel.
+  nb    block width (default 128, env DDB_POTRF_NB).
+
+``a`` is a dd ``DeviceMatrix`` (asynchronous up to the final info read) or a
+host matrix (``HostMatrix`` / the reference's Matrix; staged through HBM).
+Other precisions raise NotImplementedError; there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from .matrix import check_storage, require
+from .mpblas import _HostPlanes, _dev_ptr, _mode_code, _placement, _raise_rc
+
+__all__ = ["Rpotrf"]
+
+
+def Rpotrf(uplo, n, a, lda=None, *, mode=None, nb=0):
+    routine = "Rpotrf"
+    lda = a.ld if lda is None else lda
+    ok = isinstance(uplo, str) and uplo.upper() in ("U", "L")     # chol.py:24-26
+    require(routine, ok, 1)
+    uplo = uplo.upper()
+    require(routine, n >= 0, 2)                                     # chol.py:28
+    require(routine, lda >= max(1, n), 4)                           # chol.py:29
+    if n == 0:                                                      # chol.py:30-31
+        return 0
+    if a.precision != "dd":
+        raise NotImplementedError(
+            f"{routine}: precision {a.precision!r} is not on the B200 path (only 'dd')")
+    code = _mode_code(mode)
+    check_storage(a, n, n, lda)
+    L = _lib.load()
+    info = ctypes.c_int(0)
+    dev = _placement(routine, a)
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_rpotrf(uplo.encode(), n, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, int(nb),
+                              code, stream, ctypes.byref(info))
+        _raise_rc(routine, rc)
+        return int(info.value)
+    ha = _HostPlanes(a.store)
+    rc = L.ddb_rpotrf_host(uplo.encode(), n, ha.ptr(0), ha.ptr(1), lda, int(nb), code, None,
+                           ctypes.byref(info))
+    _raise_rc(routine, rc)
+    ha.commit()
+    return int(info.value)

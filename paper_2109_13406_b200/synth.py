@@ -39,6 +39,27 @@ def random_dd(rows: int, cols: int, ld: int | None = None, seed: int = 0,
     return np.ascontiguousarray(hi), np.ascontiguousarray(lo)
 
 
+def spd_dd(n: int, ld: int | None = None, seed: int = 0, scale: float = 1.0):
+    """Symmetric positive definite dd test matrix for Rpotrf: the triangle
+    either factorization reads is ``random_dd`` (tag 4) with ``n + 1 + U(-1, 1)``
+    on the diagonal (strictly diagonally dominant), a non-zero dd tail on
+    every entry, times ``scale`` (a power of two, exact).  Both triangles
+    are filled, as the symmetric matrix they define."""
+    ld = max(1, n) if ld is None else ld
+    hi, lo = random_dd(n, n, ld, seed, 4)
+    g = np.random.default_rng(np.random.SeedSequence([seed, 5, n, n]))
+    dh = n + 1.0 + g.uniform(-1.0, 1.0, n)
+    dl = dh * g.uniform(-1.0, 1.0, n) * 2.0 ** -55
+    dh, dl = two_sum(dh, dl)
+    idx = np.arange(n)
+    for i in range(n):          # mirror the lower triangle into the upper
+        hi[i + idx[i + 1:] * ld] = hi[idx[i + 1:] + i * ld]
+        lo[i + idx[i + 1:] * ld] = lo[idx[i + 1:] + i * ld]
+    hi[idx + idx * ld] = dh
+    lo[idx + idx * ld] = dl
+    return hi * scale, lo * scale
+
+
 # --------------------------------------------------------------------------
 # Counter-based dd operands: element (i, j) is a pure function of
 # (seed, tag, i, j) (splitmix64), so a 16 GiB matrix can be generated on the

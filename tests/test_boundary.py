@@ -161,6 +161,7 @@ def test_flop_count_matches_reference_bench():
     assert flop_count("Rgemm", 4) == 128.0
     assert flop_count("Rgemm", 3, k=5, m=2) == 60.0
     assert flop_count("Rsyrk", 4, k=3) == 60.0
+    assert flop_count("Rpotrf", 3) == 9.0
 
 
 def test_library_exports_every_header_symbol():
@@ -180,3 +181,53 @@ def test_library_exports_every_header_symbol():
     for name in declared:
         assert re.search(rf"\bT {name}$", out, re.M), name
     assert _lib.load().ddb_version() == 100
+
+
+POTRF_BAD = [(("X", 2), {}, 1), (("UU", 2), {}, 1), ((3, 2), {}, 1), (("U", -1), {}, 2),
+             (("L", 3), {"lda": 2}, 4), (("L", 0), {"lda": 0}, 4)]
+
+
+@pytest.mark.parametrize("args,lds,idx", POTRF_BAD)
+def test_rpotrf_blas_error_indices(args, lds, idx):
+    """mplapack/chol.py:21-29 (validation order uplo, n, lda)."""
+    from paper_2109_13406_b200 import Rpotrf
+    up, n = args
+    a = HostMatrix(4, 4)
+    with pytest.raises(BlasError) as e:
+        Rpotrf(up, n, a, lds.get("lda", 4))
+    assert e.value.index == idx and e.value.routine == "Rpotrf"
+    try:
+        L = _lib.load()
+    except _lib.LibraryMissing:
+        return
+    if isinstance(up, str) and len(up) == 1:
+        assert L.ddb_rpotrf_validate(up.encode(), n, lds.get("lda", 4)) == idx
+
+
+def test_rpotrf_early_exit_and_precision_gate():
+    from paper_2109_13406_b200 import Rpotrf
+    a = HostMatrix(3, 3)
+    a.store[0][:] = 7.0
+    assert Rpotrf("L", 0, a) == 0            # chol.py:30-31, no device work
+    assert Rpotrf("U", 0, a, 1) == 0
+    assert np.all(a.store[0] == 7.0)
+    b = HostMatrix(3, 3, "f64")
+    with pytest.raises(NotImplementedError):
+        Rpotrf("L", 3, b)
+
+
+def test_rpotrf_without_gpu_fails_loudly():
+    import os
+    from paper_2109_13406_b200 import Rpotrf
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libddblas.so not built")
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    a = HostMatrix(2, 2)
+    a.store[0][[0, 3]] = 2.0
+    with pytest.raises(RuntimeError):
+        Rpotrf("L", 2, a)

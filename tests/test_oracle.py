@@ -16,7 +16,8 @@ def bits_equal(a, b):
 
 
 ALL = list(golden.load_cases())
-CASES = [c for c in ALL if c[0]["routine"] != "Cgemm"]
+CASES = [c for c in ALL if c[0]["routine"] in ("Rgemm", "Rsyrk")]
+PCASES = [c for c in ALL if c[0]["routine"] == "Rpotrf"]
 CCASES = [c for c in ALL if c[0]["routine"] == "Cgemm"]
 
 
@@ -120,3 +121,35 @@ def test_oracle_cgemm_matches_reference_bitwise(idx):
             assert bits_equal(g_.real.copy(), o_.real.copy()) and bits_equal(g_.imag.copy(), o_.imag.copy()), case
         else:
             assert bits_equal(g_, o_), case
+
+
+@pytest.mark.parametrize("idx", range(len(PCASES)))
+def test_oracle_rpotrf_matches_reference_bitwise(idx):
+    """mplapack/chol.py:21-65 restated in C, against the reference's own output."""
+    case, arr, out_hi, out_lo = PCASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"]
+    ah, al = arr["A_hi"].copy(), arr["A_lo"].copy()
+    with np.errstate(all="ignore"):
+        rc, info = oracle.rpotrf(case["uplo"], case["n"], ah, al, case["lda"])
+    assert rc == 0
+    assert info == case["info"], case
+    assert bits_equal(ah, out_hi), case
+    assert bits_equal(al, out_lo), case
+
+
+def test_oracle_scalar_div_sqrt_match_reference():
+    """ddarith._div2 / _sqrt2 (the pivots of Rpotrf) through the oracle."""
+    v = golden.load_eft()
+    for i in range(len(v["xh"])):
+        x = (v["xh"][i], v["xl"][i])
+        y = (v["yh"][i], v["yl"][i])
+        assert bits_equal(oracle.div2(x, y), (v["div_h"][i], v["div_l"][i])), i
+        assert bits_equal(oracle.sqrt2((v["sq_in_h"][i], v["sq_in_l"][i])),
+                          (v["sq_h"][i], v["sq_l"][i])), i
+
+
+@pytest.mark.parametrize("args,idx", [(("X", 3, 3), 1), (("U", -1, 1), 2), (("L", 4, 3), 4),
+                                      (("l", 0, 1), 0), (("u", 1, 1), 0), (("L", 0, 0), 4)])
+def test_oracle_potrf_validation_indices(args, idx):
+    uplo, n, lda = args
+    assert oracle.lib().oracle_potrf_validate(uplo.encode(), n, lda) == idx
