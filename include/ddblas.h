@@ -120,8 +120,9 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
 
 /* Cholesky: mpkit.mplapack.Rpotrf (mplapack/chol.py:21-65), dd, in place.
  * uplo 'L': A = L L^T, 'U': A = U^T U; only that triangle is read / written.
- * Blocked right-looking (block width nb; <= 0 = default 128 or
- * $DDB_POTRF_NB) with the trailing updates done by ddb_rsyrk in `mode`; in
+ * Blocked right-looking, two levels: outer block width nb (<= 0 = default
+ * 256 or $DDB_POTRF_NB), inner width min(nb, 64); the trailing updates are
+ * ddb_rsyrk / ddb_rgemm calls in `mode`, overlapped with the next panel; in
  * exact mode the factor is bit-identical to the reference's unblocked
  * order for operands inside the safe window.  *info (host int) = 0, or
  * j + 1 for the first pivot that is NaN or <= 0, whose value is left in

@@ -69,6 +69,24 @@ void retain_pool_memory() {
   done_mask |= 1 << dev;
 }
 
+// Rpotrf's panel stream (highest priority), one per host thread and device.
+cudaError_t potrf_panel_stream(cudaStream_t* out) {
+  static thread_local cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  if (streams[dev] == nullptr) {
+    int least = 0, greatest = 0;
+    e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (e == cudaSuccess)
+      e = cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, greatest);
+    if (e != cudaSuccess) return e;
+  }
+  *out = streams[dev];
+  return cudaSuccess;
+}
+
 // Runs one validated, non-trivial call: prescan -> tiled (gated on the
 // flag) -> reference-semantics kernel (gated on the opposite).
 int run(const GemmArgs& g0, int mode, cudaStream_t s) {
@@ -597,23 +615,31 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   }
   *info = 0;
   if (n == 0) return DDB_OK;                          // chol.py:30-31
+  // two block levels: outer width NB (the trailing Rsyrk / Rgemm depth) and
+  // inner width ib <= kPotrfMaxNb (diagonal block in shared memory)
   if (nb <= 0) {
     static const int64_t nb_env = [] {
       const char* v = std::getenv("DDB_POTRF_NB");
       return v ? (int64_t)std::atoll(v) : (int64_t)0;
     }();
-    nb = nb_env > 0 ? nb_env : 128;
+    nb = nb_env > 0 ? nb_env : 256;
   }
+  const int64_t NB = nb;
+  const int64_t ib = nb < kPotrfMaxNb ? nb : kPotrfMaxNb;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   retain_pool_memory();
   PotrfArgs p{};
   p.n = n; p.lda = lda; p.upper = upflag(uplo) == 'U';
   p.a_hi = a_hi; p.a_lo = a_lo;
-  const bool blocked = n > nb;
+  // workspace: info | D, d0 (dd vectors), rec (ib dd) | backup ('L') or S
+  // ('U'), n x n dd | 'U': the inner transposed panel (n x ib) and two outer
+  // ones (n x NB; block J's is read by the trailing update while J+1's is
+  // written)
   const size_t head = 256, vec = sizeof(double) * (size_t)n;
-  const size_t full = blocked ? sizeof(double) * (size_t)n * n : 0;
-  const size_t tpan = blocked && p.upper ? sizeof(double) * (size_t)n * nb : 0;
-  const size_t ws_bytes = head + 4 * vec + 2 * full + 2 * tpan;
+  const size_t recb = ((sizeof(double) * 2 * (size_t)ib + 255) / 256) * 256;
+  const size_t full = sizeof(double) * (size_t)n * n;
+  const size_t t_in = p.upper ? (size_t)n * ib : 0, t_out = p.upper ? (size_t)n * NB : 0;
+  const size_t ws_bytes = head + 4 * vec + recb + 2 * full + sizeof(double) * 2 * (t_in + 2 * t_out);
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "workspace allocation");
@@ -624,18 +650,20 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   double* d0h = d + 2 * n;
   double* d0l = d + 3 * n;
   p.d0_hi = d0h; p.d0_lo = d0l;
-  double* big = d + 4 * n;                            // backup (lower) or S (upper)
-  double* tp = big + 2 * (size_t)n * (blocked ? n : 0);
-  const char* what = "rpotrf";
+  p.rec_hi = d + 4 * n; p.rec_lo = p.rec_hi + ib;
+  double* big = reinterpret_cast<double*>(w + head + 4 * vec + recb);
+  double* tin_h = big + 2 * (size_t)n * n;           // inner T: hi | lo
+  double* tin_l = tin_h + t_in;
+  double* tout_h = tin_l + t_in;                     // outer T: hi[2] | lo[2]
+  double* tout_l = tout_h + 2 * t_out;
   int nl = 0;
   e = cudaMemsetAsync(ws, 0, head + 2 * vec, s);
   const size_t dpitch = sizeof(double) * (size_t)(lda + 1);
   if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0h, 8, a_hi, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0l, 8, a_lo, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess && blocked) {
+  if (e == cudaSuccess) {
     if (p.upper) {
       p.s_hi = big; p.s_lo = big + (size_t)n * n; p.lds = n;
-      p.t_hi = tp; p.t_lo = tp + (size_t)n * nb;
       e = cudaMemsetAsync(big, 0, 2 * full, s);
     } else {
       double* bh = big;
@@ -646,29 +674,108 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
       if (e == cudaSuccess) e = cudaMemcpy2DAsync(bl, row, a_lo, pitch, row, n, cudaMemcpyDeviceToDevice, s);
     }
   }
+  // Streams: the panel work (diagonal blocks, panels, inner updates and the
+  // lookahead update of the next block column) runs on a high-priority
+  // stream `cs`; the bulk trailing update of each outer block runs on the
+  // caller's stream `s`, overlapping the next panel.  Per element the
+  // contributions still arrive in block order: `cs` waits for rest(J-1)
+  // before update(J -> J+1), and rest(J) follows rest(J-1) on `s`.
   int rc2 = DDB_OK;
-  for (int64_t j0 = 0; e == cudaSuccess && rc2 == DDB_OK && j0 < n; j0 += nb) {
-    const int64_t j1 = j0 + nb < n ? j0 + nb : n;
-    for (int64_t j = j0; j < j1 && e == cudaSuccess; ++j) {
-      e = launch_potrf_col(p, j0, j, s);
-      ++nl;
-    }
-    if (e != cudaSuccess || j1 >= n) break;
-    const int64_t n2 = n - j1;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  if (e == cudaSuccess) e = potrf_panel_stream(&cs);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+  // trailing update of columns [c0, c1) (rows >= c0) by factor rows / columns
+  // [j0, j1):  'L': A(r, c) -= L(r, j0:j1) L(c, j0:j1)^T in place;
+  //            'U': S(r, c) += T(r) T(c)^T, T(x) = U(j0:j1, x)^T stored from
+  //                 column tb0 with leading dimension n - tb0
+  auto update = [&](int64_t j0, int64_t j1, int64_t c0, int64_t c1, const double* th,
+                    const double* tl, int64_t tb0, cudaStream_t st) -> int {
+    const int64_t kb = j1 - j0, wd = c1 - c0, below = n - c1;
+    void* sv = static_cast<void*>(st);
+    int r;
     if (!p.upper) {
-      // A22 -= L21 L21^T in place (chol.py:57-62 order, continued)
-      rc2 = ddb_rsyrk('L', 'N', n2, j1 - j0, -1.0, 0.0, a_hi + j1 + j0 * lda, a_lo + j1 + j0 * lda,
-                      lda, 1.0, 0.0, a_hi + j1 + j1 * lda, a_lo + j1 + j1 * lda, lda, mode, stream);
+      const double *lh = a_hi + j0 * lda, *ll = a_lo + j0 * lda;
+      r = ddb_rsyrk('L', 'N', wd, kb, -1.0, 0.0, lh + c0, ll + c0, lda, 1.0, 0.0,
+                    a_hi + c0 + c0 * lda, a_lo + c0 + c0 * lda, lda, mode, sv);
+      if (r == DDB_OK && below > 0)
+        r = ddb_rgemm('N', 'T', below, wd, kb, -1.0, 0.0, lh + c1, ll + c1, lda, lh + c0, ll + c0,
+                      lda, 1.0, 0.0, a_hi + c1 + c0 * lda, a_lo + c1 + c0 * lda, lda, mode, sv);
     } else {
-      // S22 += U12^T U12 (chol.py:50-53 dot products, continued)
-      e = launch_potrf_transpose(p, j0, j1, (int)(j1 - j0), n2, s);
-      ++nl;
-      if (e == cudaSuccess)
-        rc2 = ddb_rsyrk('L', 'N', n2, j1 - j0, 1.0, 0.0, p.t_hi, p.t_lo, n2, 1.0, 0.0,
-                        p.s_hi + j1 + j1 * n, p.s_lo + j1 + j1 * n, n, mode, stream);
+      const int64_t ldt = n - tb0;
+      th -= tb0;
+      tl -= tb0;                                     // th[x] = T(x) for column x
+      r = ddb_rsyrk('L', 'N', wd, kb, 1.0, 0.0, th + c0, tl + c0, ldt, 1.0, 0.0,
+                    p.s_hi + c0 + c0 * n, p.s_lo + c0 + c0 * n, n, mode, sv);
+      if (r == DDB_OK && below > 0)
+        r = ddb_rgemm('N', 'T', below, wd, kb, 1.0, 0.0, th + c1, tl + c1, ldt, th + c0, tl + c0,
+                      ldt, 1.0, 0.0, p.s_hi + c1 + c0 * n, p.s_lo + c1 + c0 * n, n, mode, sv);
     }
+    return r;
+  };
+  auto transpose = [&](int64_t j0, int64_t j1, double* th, double* tl) -> cudaError_t {
+    PotrfArgs q = p;
+    q.t_hi = th;
+    q.t_lo = tl;
+    ++nl;
+    return launch_potrf_transpose(q, j0, j1, (int)(j1 - j0), n - j1, cs);
+  };
+  // factor the outer panel [J0, J1): inner blocks, each followed by the
+  // update of the rest of the outer panel's columns
+  auto factor_outer = [&](int64_t J0, int64_t J1) -> int {
+    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
+      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
+      cudaError_t er = launch_potrf_diag(p, i0, i1, cs);
+      ++nl;
+      if (er == cudaSuccess && i1 < n) {
+        er = launch_potrf_panel(p, i0, (int)(i1 - i0), n - i1, cs);
+        ++nl;
+      }
+      if (er != cudaSuccess) return fail(er, "rpotrf panel");
+      if (i1 < J1) {
+        if (p.upper && (er = transpose(i0, i1, tin_h, tin_l)) != cudaSuccess)
+          return fail(er, "rpotrf transpose");
+        const int r = update(i0, i1, i1, J1, tin_h, tin_l, i1, cs);
+        if (r != DDB_OK) return r;
+      }
+    }
+    return DDB_OK;
+  };
+  if (e == cudaSuccess) e = cudaEventRecord(ev_a, s);      // workspace ready
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_a, 0);
+  if (e == cudaSuccess) rc2 = factor_outer(0, NB < n ? NB : n);
+  bool have_rest = false;
+  for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
+    const int64_t J1 = J0 + NB < n ? J0 + NB : n;
+    if (J1 >= n) break;
+    const int64_t J2 = J1 + NB < n ? J1 + NB : n;
+    double* th = tout_h + ((J0 / NB) & 1) * t_out;
+    double* tl = tout_l + ((J0 / NB) & 1) * t_out;
+    if (p.upper) e = transpose(J0, J1, th, tl);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_a, cs);    // panel J (+ T) done
+    if (e == cudaSuccess && have_rest) e = cudaStreamWaitEvent(cs, ev_b, 0);   // rest(J-1)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
+    if (e != cudaSuccess) break;
+    if (J2 < n) {
+      rc2 = update(J0, J1, J2, n, th, tl, J1, s);           // rest(J)
+      if (rc2 != DDB_OK) break;
+      e = cudaEventRecord(ev_b, s);
+      have_rest = true;
+      if (e != cudaSuccess) break;
+    }
+    rc2 = update(J0, J1, J1, J2, th, tl, J1, cs);            // update(J -> J+1)
+    if (rc2 == DDB_OK) rc2 = factor_outer(J1, J2);
   }
-  if (e == cudaSuccess && rc2 == DDB_OK && blocked && !p.upper) {
+  // join the panel stream back into `s`
+  if (cs != nullptr) {
+    cudaError_t ej = cudaEventRecord(ev_a, cs);
+    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_a, 0);
+    if (e == cudaSuccess) e = ej;
+  }
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
+  if (e == cudaSuccess && rc2 == DDB_OK && !p.upper) {
     e = launch_potrf_restore(p, s);
     ++nl;
   }
@@ -680,7 +787,7 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   if (rc2 != DDB_OK) return rc2;
-  if (e != cudaSuccess) return fail(e, what);
+  if (e != cudaSuccess) return fail(e, "rpotrf");
   if (e2 != cudaSuccess) return fail(e2, "workspace free");
   *info = hinfo;
   return DDB_OK;

@@ -25,9 +25,12 @@
 //   * upper: temp accumulates from ZERO, so the trailing updates go to a
 //     separate accumulator S (lower-stored, S(jj, j) for U(j, jj)) by
 //     Rsyrk('L', 'N', alpha = 1, beta = 1) on T = U12^T;
-//   * potrf_col_kernel finishes column j of the current block: the pivot
-//     (every CTA recomputes it, CTA 0 stores it), then one thread per
-//     trailing row (column) continues the sequence over l in [j0, j).
+//   * per block: potrf_diag_kernel factors the diagonal block in one CTA
+//     (right-looking, a barrier per column; the pivots are the only serial
+//     chain), potrf_panel_kernel the rows below it ('U': the columns right of
+//     it), each row an independent sequence over the block's columns run by
+//     a group of lanes; block width <= 64 (the diagonal block lives in
+//     shared memory).
 // So in exact mode (Rsyrk exact) the factor is bit-identical to the
 // reference for operands inside the safe window; fast / twosum modes differ
 // only by their Rsyrk accumulation.  On failure the device info is set,
@@ -122,54 +125,228 @@ __device__ __forceinline__ bool bad_pivot(dd a) {
 
 }  // namespace
 
-// Column j of the block starting at j0.  d0 = original diagonal, D = pivot
-// dot products so far, S (upper only) = the lower-stored accumulator.
-__global__ void __launch_bounds__(128)
-potrf_col_kernel(PotrfArgs p, int64_t j0, int64_t j) {
+// Diagonal block [j0, j1) in one CTA, staged in shared memory, right-looking:
+// per column j the pivot (thread 0), the column inside the block, then the
+// block's trailing strictly-lower entries, each update in the reference's
+// l order.  X(q, c) (q > c) is the block entry the factor overwrites: A(q, c)
+// for 'L', A(c, q) for 'U'; for 'U' the running dot products S(q, c) are
+// staged too.  The reciprocals go to p.rec for the panel kernel.
+__global__ void __launch_bounds__(512)
+potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
+  extern __shared__ double sm[];
+  __shared__ dd rec_s;
+  __shared__ int ok_s;
   if (*p.info != 0) return;
-  const dd ajj = add2_s(dd{p.d0_hi[j], p.d0_lo[j]}, neg2(dd{p.dh[j], p.dl[j]}));
-  const int64_t djj = j + j * p.lda;
-  if (bad_pivot(ajj)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+  const int64_t lda = p.lda, lds = p.lds;
+  const int sq = nb * nb;
+  double* xh = sm;
+  double* xl = sm + sq;
+  double* sh = sm + 2 * sq;                      // 'U' only
+  double* sl = sm + 3 * sq;
+  double* dh = sm + (p.upper ? 4 : 2) * sq;
+  double* dl = dh + nb;
+  double* d0h = dl + nb;
+  double* d0l = d0h + nb;
+  for (int t = threadIdx.x; t < sq; t += blockDim.x) {
+    const int q = t % nb, c = t / nb;
+    if (q <= c) continue;
+    const int64_t x = p.upper ? (j0 + c) + (j0 + q) * lda : (j0 + q) + (j0 + c) * lda;
+    xh[t] = p.a_hi[x];
+    xl[t] = p.a_lo[x];
+    if (p.upper) {
+      const int64_t y = (j0 + q) + (j0 + c) * lds;
+      sh[t] = p.s_hi[y];
+      sl[t] = p.s_lo[y];
+    }
+  }
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    dh[t] = p.dh[j0 + t];
+    dl[t] = p.dl[j0 + t];
+    d0h[t] = p.d0_hi[j0 + t];
+    d0l[t] = p.d0_lo[j0 + t];
+  }
+  __syncthreads();
+  // thread 0 computes pivot j+1 while warps 1.. run step j's trailing
+  // update (pivot j+1 needs only D(j+1), final after step j's column phase)
+  auto pivot = [&](int j) {
+    const dd ajj = add2_s(dd{d0h[j], d0l[j]}, neg2(dd{dh[j], dl[j]}));   // chol.py:41
+    const int64_t djj = (j0 + j) * (lda + 1);
+    ok_s = !bad_pivot(ajj);
+    if (!ok_s) {
       p.a_hi[djj] = ajj.h;
       p.a_lo[djj] = ajj.l;
-      *p.info = (int)(j + 1);
+      *p.info = (int)(j0 + j + 1);
+    } else {
+      const dd s = sqrt2_s(ajj);
+      p.a_hi[djj] = s.h;
+      p.a_lo[djj] = s.l;
+      const dd rec = div2_s(dd{1.0, 0.0}, s);
+      rec_s = rec;
+      p.rec_hi[j] = rec.h;
+      p.rec_lo[j] = rec.l;
     }
-    return;
-  }
-  const dd s = sqrt2_s(ajj);
-  const dd rec = div2_s(dd{1.0, 0.0}, s);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    p.a_hi[djj] = s.h;
-    p.a_lo[djj] = s.l;
-  }
-  const int64_t q = j + 1 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= p.n) return;
-  const int64_t lda = p.lda;
-  dd v;
-  if (!p.upper) {
-    dd acc{p.a_hi[q + j * lda], p.a_lo[q + j * lda]};
-    for (int64_t l = j0; l < j; ++l) {
-      const dd t = neg2(dd{p.a_hi[j + l * lda], p.a_lo[j + l * lda]});
-      acc = add2_chk(acc, mul2_chk(t, dd{p.a_hi[q + l * lda], p.a_lo[q + l * lda]}));
+  };
+  if (threadIdx.x == 0) pivot(0);
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (!ok_s) break;
+    const dd rec = rec_s;
+    for (int q = j + 1 + threadIdx.x; q < nb; q += blockDim.x) {
+      const int t = q + j * nb;
+      dd a{xh[t], xl[t]};
+      if (p.upper) a = add2_chk(a, neg2(dd{sh[t], sl[t]}));
+      const dd v = mul2_chk(rec, a);
+      xh[t] = v.h;
+      xl[t] = v.l;
+      const dd d = add2_chk(dd{dh[q], dl[q]}, mul2_chk(v, v));
+      dh[q] = d.h;
+      dl[q] = d.l;
     }
-    v = mul2_chk(rec, acc);
-    p.a_hi[q + j * lda] = v.h;
-    p.a_lo[q + j * lda] = v.l;
-  } else {
-    dd acc{0.0, 0.0};                     // S is absent for a single block
-    if (p.s_hi != nullptr) acc = dd{p.s_hi[q + j * p.lds], p.s_lo[q + j * p.lds]};
-    for (int64_t l = j0; l < j; ++l)
-      acc = add2_chk(acc, mul2_chk(dd{p.a_hi[l + q * lda], p.a_lo[l + q * lda]},
-                                   dd{p.a_hi[l + j * lda], p.a_lo[l + j * lda]}));
-    const dd elt = add2_chk(dd{p.a_hi[j + q * lda], p.a_lo[j + q * lda]}, neg2(acc));
-    v = mul2_chk(rec, elt);
-    p.a_hi[j + q * lda] = v.h;
-    p.a_lo[j + q * lda] = v.l;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (j + 1 < nb) pivot(j + 1);
+    } else if (threadIdx.x >= 32) {
+      // pairs (q, c), j < c < q < nb, enumerated column by column; batches
+      // of kB independent updates (operands gathered before any store)
+      const int rem = nb - j - 1;
+      const int npairs = rem * (rem - 1) / 2;
+      constexpr int kB = 4;
+      const int nthr = blockDim.x - 32;
+      for (int base = threadIdx.x - 32; base < npairs; base += nthr * kB) {
+        int xs[kB];
+        dd acc[kB], f1[kB], f2[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int t = base + b * nthr;
+          xs[b] = -1;
+          if (t < npairs) {
+            // column ci (0-based within the rem trailing columns) of pair t
+            int ci = (int)((2.0f * rem - 1.0f - sqrtf((2.0f * rem - 1.0f) * (2.0f * rem - 1.0f) - 8.0f * t)) * 0.5f);
+            while (ci > 0 && ci * (2 * rem - ci - 1) / 2 > t) --ci;
+            while ((ci + 1) * (2 * rem - ci - 2) / 2 <= t) ++ci;
+            const int qi = ci + 1 + (t - ci * (2 * rem - ci - 1) / 2);
+            const int c = j + 1 + ci, q = j + 1 + qi;
+            xs[b] = q + c * nb;
+            const dd vq{xh[q + j * nb], xl[q + j * nb]}, vc{xh[c + j * nb], xl[c + j * nb]};
+            if (!p.upper) { acc[b] = dd{xh[xs[b]], xl[xs[b]]}; f1[b] = neg2(vc); f2[b] = vq; }
+            else { acc[b] = dd{sh[xs[b]], sl[xs[b]]}; f1[b] = vq; f2[b] = vc; }
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          if (xs[b] < 0) continue;
+          const dd r = add2_chk(acc[b], mul2_chk(f1[b], f2[b]));
+          if (!p.upper) { xh[xs[b]] = r.h; xl[xs[b]] = r.l; }
+          else { sh[xs[b]] = r.h; sl[xs[b]] = r.l; }
+        }
+      }
+    }
+    __syncthreads();
   }
-  const dd d = add2_chk(dd{p.dh[q], p.dl[q]}, mul2_chk(v, v));
-  p.dh[q] = d.h;
-  p.dl[q] = d.l;
+  // write the block back ('U': the untouched part is written back unchanged;
+  // 'L': entries the reference would not have touched yet are restored from
+  // the backup by potrf_restore_kernel)
+  for (int t = threadIdx.x; t < sq; t += blockDim.x) {
+    const int q = t % nb, c = t / nb;
+    if (q <= c) continue;
+    const int64_t x = p.upper ? (j0 + c) + (j0 + q) * lda : (j0 + q) + (j0 + c) * lda;
+    p.a_hi[x] = xh[t];
+    p.a_lo[x] = xl[t];
+  }
+}
+
+// Panel below ('L': rows q >= j1) / right of ('U': columns q >= j1) the
+// diagonal block.  Each q is independent: a group of G lanes owns it, lane t
+// holding the accumulators of block columns c = j0 + t + G*i.  Step c: the
+// owner finalises entry c (rec_c * acc, or rec_c * (A - acc) for 'U'),
+// broadcasts it, and every lane extends its later columns by one product --
+// the reference's per-element order (chol.py:50-64), with NPER independent
+// chains per lane.  The block's factor (strictly-lower part, transposed for
+// 'U') and the reciprocals sit in shared memory.
+constexpr int kPanelG = 32;          // lanes per row: one warp
+constexpr int kPanelThreads = 256;    // 8 rows per CTA
+
+template <int NPER>
+__global__ void __launch_bounds__(kPanelThreads)
+potrf_panel_kernel(PotrfArgs p, int64_t j0, int nb) {
+  extern __shared__ double sm[];
+  // a failure inside this block's diagonal part still leaves the columns
+  // before it complete, as the reference does (chol.py:44-46)
+  int ncols = nb;
+  const int inf = *p.info;
+  if (inf != 0) {
+    if (inf - 1 < j0) return;
+    ncols = (int)(inf - 1 - j0);
+  }
+  const int64_t lda = p.lda, lds = p.lds;
+  const int64_t j1 = j0 + nb;
+  // packed strictly-lower triangle: T(c2, c) (c < c2) at off(c) + c2 - c - 1
+  const int ntri = nb * (nb - 1) / 2;
+  double* th = sm;
+  double* tl = sm + ntri;
+  double* rh = sm + 2 * ntri;
+  double* rl = rh + nb;
+  auto off = [nb](int c) { return c * (2 * nb - c - 1) / 2; };
+  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+    const int c2 = t % nb, c = t / nb;
+    if (c2 <= c) continue;
+    const int64_t x = p.upper ? (j0 + c) + (j0 + c2) * lda : (j0 + c2) + (j0 + c) * lda;
+    th[off(c) + c2 - c - 1] = p.a_hi[x];
+    tl[off(c) + c2 - c - 1] = p.a_lo[x];
+  }
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+    rh[c] = p.rec_hi[c];
+    rl[c] = p.rec_lo[c];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x % kPanelG;
+  const int64_t q = j1 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPanelG;
+  if (q >= p.n) return;                 // whole warps exit together
+  dd acc[NPER];
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + kPanelG * i;
+    acc[i] = dd{0.0, 0.0};
+    if (c < nb) {
+      const int64_t x = p.upper ? q + (j0 + c) * lds : q + (j0 + c) * lda;
+      acc[i] = p.upper ? dd{p.s_hi[x], p.s_lo[x]} : dd{p.a_hi[x], p.a_lo[x]};
+    }
+  }
+  dd dq{0.0, 0.0};
+  if (lane == 0) dq = dd{p.dh[q], p.dl[q]};
+  for (int c = 0; c < ncols; ++c) {
+    const int owner = c % kPanelG, ic = c / kPanelG;
+    dd v{0.0, 0.0};
+    if (lane == owner) {
+      dd a{0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < NPER; ++i)
+        if (i == ic) a = acc[i];
+      const dd rec{rh[c], rl[c]};
+      const int64_t x = p.upper ? (j0 + c) + q * lda : q + (j0 + c) * lda;
+      if (p.upper) a = add2_chk(dd{p.a_hi[x], p.a_lo[x]}, neg2(a));
+      v = mul2_chk(rec, a);
+      p.a_hi[x] = v.h;
+      p.a_lo[x] = v.l;
+    }
+    v.h = __shfl_sync(0xffffffffu, v.h, owner);
+    v.l = __shfl_sync(0xffffffffu, v.l, owner);
+    if (lane == 0) dq = add2_chk(dq, mul2_chk(v, v));
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {
+      const int c2 = lane + kPanelG * i;
+      if (c2 > c && c2 < nb) {
+        const int o = off(c) + c2 - c - 1;
+        const dd t{th[o], tl[o]};
+        acc[i] = p.upper ? add2_chk(acc[i], mul2_chk(v, t))
+                         : add2_chk(acc[i], mul2_chk(neg2(t), v));
+      }
+    }
+  }
+  if (lane == 0) {
+    p.dh[q] = dq.h;
+    p.dl[q] = dq.l;
+  }
 }
 
 // T(r, l) = U(j0 + l, j1 + r), r < rows, l < nb  (ld = rows)
@@ -212,11 +389,44 @@ potrf_restore_kernel(PotrfArgs p) {
   }
 }
 
-cudaError_t launch_potrf_col(const PotrfArgs& p, int64_t j0, int64_t j, cudaStream_t s) {
-  const int64_t rows = p.n - j - 1;
-  const unsigned grid = rows > 0 ? (unsigned)((rows + 127) / 128) : 1u;
-  potrf_col_kernel<<<grid, 128, 0, s>>>(p, j0, j);
+cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaStream_t s) {
+  const int nb = (int)(j1 - j0);
+  const size_t smem = sizeof(double) * ((size_t)(p.upper ? 4 : 2) * nb * nb + 4 * (size_t)nb);
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_dev = dev;
+  }
+  potrf_diag_kernel<<<1, 512, smem, s>>>(p, j0, nb);
   return cudaGetLastError();
+}
+
+template <int NPER>
+static cudaError_t panel_launch(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
+                                cudaStream_t s) {
+  const size_t smem = sizeof(double) * ((size_t)nb * (nb - 1) + 2 * (size_t)nb);
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(potrf_panel_kernel<NPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr_dev = dev;
+  }
+  const int64_t threads = rows * kPanelG;
+  potrf_panel_kernel<NPER><<<(unsigned)((threads + kPanelThreads - 1) / kPanelThreads),
+                             kPanelThreads, smem, s>>>(p, j0, nb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_potrf_panel(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
+                               cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  const int nper = (nb + kPanelG - 1) / kPanelG;
+  (void)nper;   // nb <= 64 = 2 * kPanelG
+  return panel_launch<2>(p, j0, nb, rows, s);
 }
 
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,

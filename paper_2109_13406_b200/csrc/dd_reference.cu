@@ -24,9 +24,8 @@ reference_kernel(GemmArgs g, const int* __restrict__ flag, int gate) {
     if (gate == GATE_IF_UNSAFE && f == ROUTE_SAFE) return;
     if (gate == GATE_IF_SAFE && f != ROUTE_SAFE) return;
   }
-  const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
-  if (i >= g.m) return;
   const bool alpha_zero = dd_is_zero(g.alpha);
+  for (int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x; i < g.m; i += (int64_t)gridDim.x * 32)
   for (int64_t j = (int64_t)blockIdx.y * 8 + threadIdx.y; j < g.n; j += (int64_t)gridDim.y * 8) {
     if (g.syrk == 1 && i > j) continue;
     if (g.syrk == 2 && i < j) continue;
@@ -105,9 +104,13 @@ cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaS
     ++*nlaunch;
     return cudaGetLastError();
   }
-  const int64_t gx = (g.m + 31) / 32;
+  // a gated launch usually exits at once: keep its grid small (the loops
+  // stride over the rest when it does run)
+  const int64_t cap_x = gate == GATE_ALWAYS ? INT32_MAX : 32, cap_y = gate == GATE_ALWAYS ? 65535 : 32;
+  int64_t gx = (g.m + 31) / 32;
   int64_t gy = (g.n + 7) / 8;
-  if (gy > 65535) gy = 65535;
+  if (gx > cap_x) gx = cap_x;
+  if (gy > cap_y) gy = cap_y;
   dim3 grid((unsigned)gx, (unsigned)gy), block(32, 8);
   reference_kernel<<<grid, block, 0, s>>>(g, flag, gate);
   ++*nlaunch;

@@ -100,10 +100,14 @@ struct PotrfArgs {
   int64_t lds;
   double *t_hi, *t_lo;          // upper: the transposed panel U12^T
   const double *b_hi, *b_lo;    // lower: backup of the input (ld = n)
+  double *rec_hi, *rec_lo;      // the current block's pivot reciprocals
   int* info;                    // device: first failing pivot + 1, or 0
 };
 
-cudaError_t launch_potrf_col(const PotrfArgs& p, int64_t j0, int64_t j, cudaStream_t s);
+constexpr int kPotrfMaxNb = 64;
+cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaStream_t s);
+cudaError_t launch_potrf_panel(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
+                               cudaStream_t s);
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,
                                    int64_t rows, cudaStream_t s);
 cudaError_t launch_potrf_restore(const PotrfArgs& p, cudaStream_t s);

@@ -15,7 +15,8 @@ with the later entries as the reference leaves them.  Keywords:
         algorithm with those modes' Rsyrk -- residual within the reference's
         testkit threshold (testkit.residual_chol < 30); "reference": the
         trailing updates on the checked one-thread-per-element kernel.
-  nb    block width (default 128, env DDB_POTRF_NB).
+  nb    outer block width = the trailing updates' depth (default 256, env
+        DDB_POTRF_NB); the inner (diagonal-block) width is min(nb, 64).
 
 ``a`` is a dd ``DeviceMatrix`` (asynchronous up to the final info read) or a
 host matrix (``HostMatrix`` / the reference's Matrix; staged through HBM).

@@ -74,7 +74,7 @@ def residual_ratio(uplo, n, ld, a_hi, a_lo, f_hi, f_lo):
     return float(rnorm / (max(1, n) * anorm * EPS_DD))
 
 
-@pytest.mark.parametrize("nb", [0, 16, 5])
+@pytest.mark.parametrize("nb", [0, 16, 5, 40])
 @pytest.mark.parametrize("mode", ["exact", "reference"])
 @pytest.mark.parametrize("idx", range(len(PCASES)))
 def test_rpotrf_golden_bitwise(idx, mode, nb):
@@ -109,7 +109,7 @@ def test_rpotrf_golden_fast_modes(idx, mode):
 
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
-@pytest.mark.parametrize("n,nb", [(700, 128), (1000, 96)])
+@pytest.mark.parametrize("n,nb", [(700, 0), (1000, 100), (900, 48), (650, 130)])
 def test_rpotrf_exact_matches_oracle(uplo, n, nb):
     """Multi-block sizes, default and odd block widths: bitwise vs the C
     oracle (the reference's order, pinned by the golden tests)."""
