@@ -282,6 +282,7 @@ def run_ours(args):
             extra["modes"] = _modes(n, k, dev, stream, A, B, C, C0, mode)
             extra["f64"] = _f64(n, dev, stream)
             extra["cgemm"] = _cgemm(n // 2, dev, stream, mode)
+            extra["rpotrf"] = _rpotrf(n, dev, stream, mode)
         cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, 16, 0)
         from oracle import oracle
         extra["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": oracle.max_threads(),
@@ -404,6 +405,34 @@ def _cgemm(n, dev, stream, mode):
     t = min(times)
     return {"workload": f"cdd Cgemm NN m=n=k={n}", "value": 8.0 * n ** 3 / t / 1e9,
             "unit": "dd GFlops (8mnk)", "ms": t * 1e3, "mode": mode}
+
+
+def _rpotrf(n, dev, stream, mode):
+    """blocked dd Cholesky (lower) of an n x n SPD matrix; n^3/3 flops
+    (the reference bench's count, mpkit/bench.py:68-69)."""
+    import torch
+    from paper_2109_13406_b200 import DeviceMatrix, Rpotrf, flop_count
+    g = torch.Generator(device=dev).manual_seed(0)
+    hi = torch.rand((n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1
+    lo = hi * (torch.rand((n, n), generator=g, device=dev, dtype=torch.float64) * 2 - 1) * 2.0 ** -54
+    hi = torch.tril(hi) + torch.tril(hi, -1).T
+    lo = torch.tril(lo) + torch.tril(lo, -1).T
+    hi.diagonal().add_(n + 1.0)
+    lo.diagonal().zero_()
+    h0, l0 = hi.T.contiguous().reshape(-1), lo.T.contiguous().reshape(-1)
+    del hi, lo
+    A = DeviceMatrix(n, n, "dd", n, store=(h0.clone(), l0.clone()))
+    infos = []
+
+    def reset():
+        A.store[0].copy_(h0)
+        A.store[1].copy_(l0)
+
+    times = timed(lambda: infos.append(Rpotrf("L", n, A, n, mode=mode)), 2, 1, stream, reset=reset)
+    t = min(times)
+    return {"workload": f"dd Rpotrf L n={n} (SPD, diagonally dominant)",
+            "value": flop_count("Rpotrf", n) / t / 1e9, "unit": UNIT, "ms": t * 1e3,
+            "mode": mode, "info": max(infos)}
 
 
 def _modes(n, k, dev, stream, A, B, C, C0, mode):
