@@ -672,3 +672,212 @@ void oracle_div2(double xh, double xl, double yh, double yl, double *out) {
 void oracle_sqrt2(double h, double l, double *out) {
     dd v = {h, l}, r = sqrt2_s(v); out[0] = r.h; out[1] = r.l;
 }
+
+/* ---- vectorised dd division (elem.py:81-117): _v_mul21 / _v_div2, with
+ * the scalar _div2 for the special lanes (y.h == 0 or a non-finite hi) ---- */
+static dd v_mul21(dd y, double q) {
+    double p, e;
+    two_prod(y.h, q, &p, &e);
+    int bad = !(isfinite(p) && isfinite(e));
+    e = e + y.l * q;
+    double s, t;
+    quick_two_sum(p, e, &s, &t);
+    dd r = {s, t};
+    if (bad) { r.h = p; r.l = 0.0; }
+    return r;
+}
+
+static dd v_div2(dd x, dd y) {
+    if (y.h == 0.0 || !(isfinite(x.h) && isfinite(y.h))) return div2_s(x, y);
+    double q1 = x.h / y.h;
+    dd m = v_mul21(y, q1), nm = {-m.h, -m.l};
+    dd r = add2(x, nm);
+    double q2 = r.h / y.h;
+    m = v_mul21(y, q2); nm.h = -m.h; nm.l = -m.l;
+    r = add2(r, nm);
+    double q3 = r.h / y.h;
+    double a, b;
+    quick_two_sum(q1, q2, &a, &b);
+    dd ab = {a, b}, c = {q3, 0.0};
+    return add2(ab, c);
+}
+
+static inline dd dsub(dd x, dd y) { dd ny = {-y.h, -y.l}; return add2(x, ny); }   /* be.sub */
+
+int oracle_trsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                         int64_t lda, int64_t ldb) {
+    int s = upflag(side), u = upflag(uplo), t = upflag(transa), d = upflag(diag);
+    if (s != 'L' && s != 'R') return 1;
+    if (u != 'U' && u != 'L') return 2;
+    if (t != 'N' && t != 'T' && t != 'C') return 3;
+    if (d != 'U' && d != 'N') return 4;
+    if (m < 0) return 5;
+    if (n < 0) return 6;
+    int64_t nrowa = s == 'L' ? m : n;
+    if (lda < (nrowa > 1 ? nrowa : 1)) return 9;
+    if (ldb < (m > 1 ? m : 1)) return 11;
+    return 0;
+}
+
+/* Rtrsm (level23.py:288-380): op(A) X = alpha B or X op(A) = alpha B, X
+ * overwriting B, in the reference's loop order for each of the four
+ * (side, transa) branches. */
+int oracle_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                 double alpha_hi, double alpha_lo, const double *Ah, const double *Al,
+                 int64_t lda, double *Bh, double *Bl, int64_t ldb) {
+    int rc = oracle_trsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
+    if (rc) return rc;
+    if (m == 0 || n == 0) return 0;
+    const int left = upflag(side) == 'L', up = upflag(uplo) == 'U';
+    const int notr = upflag(transa) == 'N', nounit = upflag(diag) == 'N';
+    const dd al = {alpha_hi, alpha_lo}, one = {1.0, 0.0};
+#define A_(i, j) ld_(Ah, Al, (i) + (j) * lda)
+#define B_(i, j) ld_(Bh, Bl, (i) + (j) * ldb)
+#define SETB(i, j, v) do { dd v_ = (v); Bh[(i) + (j) * ldb] = v_.h; Bl[(i) + (j) * ldb] = v_.l; } while (0)
+    if (is_zero(al)) {                                  /* level23.py:306-308 */
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < m; ++i) { Bh[i + j * ldb] = 0.0; Bl[i + j * ldb] = 0.0; }
+        return 0;
+    }
+    const int alpha_one = is_one(al);
+    if (left && notr) {                                 /* :326-338 */
+        for (int64_t j = 0; j < n; ++j) {
+            if (!alpha_one)
+                for (int64_t i = 0; i < m; ++i) SETB(i, j, mul2(al, B_(i, j)));
+            for (int64_t s = 0; s < m; ++s) {
+                int64_t kk = up ? m - 1 - s : s;
+                if (nounit) SETB(kk, j, v_div2(B_(kk, j), A_(kk, kk)));
+                int64_t r0 = up ? 0 : kk + 1, r1 = up ? kk : m;
+                dd x = B_(kk, j);
+                for (int64_t i = r0; i < r1; ++i) SETB(i, j, dsub(B_(i, j), mul2(A_(i, kk), x)));
+            }
+        }
+    } else if (left) {                                  /* :339-350 */
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t s = 0; s < m; ++s) {
+                int64_t i = up ? s : m - 1 - s;
+                dd temp = mul2(al, B_(i, j));
+                int64_t k0 = up ? 0 : i + 1, k1 = up ? i : m;
+                for (int64_t kk = k0; kk < k1; ++kk) temp = dsub(temp, mul2(A_(kk, i), B_(kk, j)));
+                if (nounit) temp = v_div2(temp, A_(i, i));
+                SETB(i, j, temp);
+            }
+    } else if (notr) {                                  /* :351-363 */
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t s = 0; s < n; ++s) {
+                int64_t j = up ? s : n - 1 - s;
+                if (!alpha_one) SETB(i, j, mul2(al, B_(i, j)));
+                int64_t k0 = up ? 0 : j + 1, k1 = up ? j : n;
+                for (int64_t kk = k0; kk < k1; ++kk)
+                    SETB(i, j, dsub(B_(i, j), mul2(A_(kk, j), B_(i, kk))));
+                if (nounit) SETB(i, j, mul2(v_div2(one, A_(j, j)), B_(i, j)));
+            }
+    } else {                                            /* :364-380 */
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t s = 0; s < n; ++s) {
+                int64_t kk = up ? n - 1 - s : s;
+                if (nounit) SETB(i, kk, mul2(v_div2(one, A_(kk, kk)), B_(i, kk)));
+                int64_t j0 = up ? 0 : kk + 1, j1 = up ? kk : n;
+                dd x = B_(i, kk);
+                for (int64_t j = j0; j < j1; ++j) SETB(i, j, dsub(B_(i, j), mul2(A_(j, kk), x)));
+                if (!alpha_one) SETB(i, kk, mul2(al, B_(i, kk)));
+            }
+    }
+#undef A_
+#undef B_
+#undef SETB
+    return 0;
+}
+
+/* Rgetrf (mplapack/lu.py:74-114): unblocked right-looking LU with partial
+ * pivoting in the reference's order.  ipiv (1-based, length min(m, n)) and
+ * *info as the reference returns them. */
+int oracle_getrf_validate(int64_t m, int64_t n, int64_t lda) {
+    if (m < 0) return 1;
+    if (n < 0) return 2;
+    if (lda < (m > 1 ? m : 1)) return 4;
+    return 0;
+}
+
+static const dd SFMIN_DD = {0x1p-969, -0x0.0000000000006p-1022};   /* machine_params("dd").safe_min */
+
+static int cmp2(dd x, dd y) {                          /* _cmp2, ddarith.py:166-176 */
+    if (x.h < y.h) return -1;
+    if (x.h > y.h) return 1;
+    if (x.l < y.l) return -1;
+    if (x.l > y.l) return 1;
+    return 0;
+}
+
+/* DDBackend.argmax_abs (elem.py:246-259): max |hi|, ties by max lo*sign(hi),
+ * first index; a NaN |hi| anywhere gives 0 (np.max propagates it). */
+static int64_t argmax_abs_dd(const double *h, const double *l, int64_t cnt) {
+    double mx = -1.0;
+    for (int64_t i = 0; i < cnt; ++i) {
+        double a = fabs(h[i]);
+        if (isnan(a)) return 0;
+        if (a > mx) mx = a;
+    }
+    int64_t best = -1;
+    double bl = 0.0;
+    for (int64_t i = 0; i < cnt; ++i) {
+        if (fabs(h[i]) != mx) continue;
+        double al = l[i] * (h[i] < 0.0 ? -1.0 : 1.0);
+        if (best < 0 || al > bl) { best = i; bl = al; }
+    }
+    return best < 0 ? 0 : best;
+}
+
+int oracle_rgetrf(int64_t m, int64_t n, double *Ah, double *Al, int64_t lda, int64_t *ipiv,
+                  int64_t *info) {
+    int rc = oracle_getrf_validate(m, n, lda);
+    if (rc) return rc;
+    *info = 0;
+    int64_t mn = m < n ? m : n;
+    double *colh = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+    double *coll = (double *)malloc(sizeof(double) * (m > 0 ? m : 1));
+    for (int64_t j = 0; j < mn; ++j) {
+        for (int64_t i = j; i < m; ++i) { colh[i - j] = Ah[i + j * lda]; coll[i - j] = Al[i + j * lda]; }
+        int64_t jp = j + argmax_abs_dd(colh, coll, m - j);
+        ipiv[j] = jp + 1;
+        dd piv = {Ah[jp + j * lda], Al[jp + j * lda]};
+        if (!is_zero(piv)) {
+            if (jp != j)
+                for (int64_t c = 0; c < n; ++c) {
+                    double th = Ah[j + c * lda], tl = Al[j + c * lda];
+                    Ah[j + c * lda] = Ah[jp + c * lda]; Al[j + c * lda] = Al[jp + c * lda];
+                    Ah[jp + c * lda] = th; Al[jp + c * lda] = tl;
+                }
+            if (j < m - 1) {
+                dd ap = piv;
+                if (ap.h < 0.0 || (ap.h == 0.0 && ap.l < 0.0)) { ap.h = -ap.h; ap.l = -ap.l; }
+                if (cmp2(ap, SFMIN_DD) >= 0) {
+                    dd one = {1.0, 0.0}, rec = div2_s(one, piv);
+                    for (int64_t i = j + 1; i < m; ++i) {
+                        dd x = {Ah[i + j * lda], Al[i + j * lda]}, r = mul2(rec, x);
+                        Ah[i + j * lda] = r.h; Al[i + j * lda] = r.l;
+                    }
+                } else {
+                    for (int64_t i = j + 1; i < m; ++i) {
+                        dd x = {Ah[i + j * lda], Al[i + j * lda]}, r = v_div2(x, piv);
+                        Ah[i + j * lda] = r.h; Al[i + j * lda] = r.l;
+                    }
+                }
+            }
+        } else if (*info == 0) {
+            *info = j + 1;
+        }
+        if (j < mn - 1)
+            for (int64_t c = j + 1; c < n; ++c) {
+                dd y = {-Ah[j + c * lda], -Al[j + c * lda]};
+                for (int64_t i = j + 1; i < m; ++i) {
+                    dd x = {Ah[i + j * lda], Al[i + j * lda]}, a = {Ah[i + c * lda], Al[i + c * lda]};
+                    dd r = add2(a, mul2(x, y));
+                    Ah[i + c * lda] = r.h; Al[i + c * lda] = r.l;
+                }
+            }
+    }
+    free(colh);
+    free(coll);
+    return 0;
+}

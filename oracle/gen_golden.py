@@ -262,7 +262,109 @@ def run_case_potrf(case, store):
     store["cases"].append(case)
 
 
+TRSM_ALPHAS = {"a15lo": (1.5, 1.5 * 2.0 ** -60), "a1": (1.0, 0.0), "a0": (0.0, 0.0),
+               "aneg": (-0.75, 2.0 ** -58)}
+
+
+def trsm_cases():
+    """Rtrsm (level23.py:288-380): every side x uplo x transa x diag, alpha
+    = 1 and != 1, padded lds, lower-case flags, a zero diagonal entry."""
+    cases = []
+    seed = 1700
+    for side in ("L", "R"):
+        for uplo in ("U", "L"):
+            for ta in ("N", "T", "C"):
+                for diag in ("N", "U"):
+                    for al in ("a15lo", "a1"):
+                        if ta == "C" and al == "a1":
+                            continue
+                        cases.append(dict(routine="Rtrsm", side=side, uplo=uplo, transa=ta,
+                                          diag=diag, m=9, n=7, pad=(2, 1), alpha=al, seed=seed))
+                        seed += 1
+                cases.append(dict(routine="Rtrsm", side=side, uplo=uplo, transa=ta, diag="N",
+                                  m=70, n=33, pad=(0, 3), alpha="aneg", seed=seed))
+                seed += 1
+    for flags in (("l", "u", "n", "n"), ("r", "l", "t", "u")):
+        cases.append(dict(routine="Rtrsm", side=flags[0], uplo=flags[1], transa=flags[2],
+                          diag=flags[3], m=6, n=5, pad=(0, 0), alpha="a15lo", seed=seed))
+        seed += 1
+    for side in ("L", "R"):
+        cases.append(dict(routine="Rtrsm", side=side, uplo="U", transa="N", diag="N", m=6, n=5,
+                          pad=(1, 1), alpha="a0", seed=seed)); seed += 1
+        cases.append(dict(routine="Rtrsm", side=side, uplo="L", transa="N", diag="N", m=6, n=5,
+                          pad=(1, 1), alpha="a15lo", seed=seed, special="zero_diag")); seed += 1
+        cases.append(dict(routine="Rtrsm", side=side, uplo="U", transa="T", diag="N", m=12, n=10,
+                          pad=(0, 0), alpha="a1", seed=seed, special="lo0")); seed += 1
+    for m, n in ((0, 4), (4, 0)):
+        cases.append(dict(routine="Rtrsm", side="L", uplo="U", transa="N", diag="N", m=m, n=n,
+                          pad=(0, 0), alpha="a15lo", seed=seed)); seed += 1
+    return cases
+
+
+def run_case_trsm(case, store):
+    sys.path.insert(0, REF)
+    import mpkit.mpblas as mb
+    from mpkit.ddarith import DDouble
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    alpha = TRSM_ALPHAS[case["alpha"]]
+    case["alpha_v"] = list(alpha)
+    m, n = case["m"], case["n"]
+    na = m if case["side"].upper() == "L" else n
+    a = _matrix(mb, na, na, lds["lda"], (arrays["A_hi"], arrays["A_lo"]))
+    b = _matrix(mb, m, n, lds["ldb"], (arrays["B_hi"], arrays["B_lo"]))
+    with np.errstate(all="ignore"):
+        mb.Rtrsm(case["side"], case["uplo"], case["transa"], case["diag"], m, n,
+                 DDouble._raw(*alpha), a, lds["lda"], b, lds["ldb"])
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    store["arrays"][f"c{cid}_out_hi"] = np.asarray(b.store[0], dtype=np.float64)
+    store["arrays"][f"c{cid}_out_lo"] = np.asarray(b.store[1], dtype=np.float64)
+    store["cases"].append(case)
+
+
+def getrf_cases():
+    """Rgetrf (mplapack/lu.py:74-114): square / tall / wide, padded lda,
+    pivot ties, an exactly zero pivot (info), sub-safmin pivots, NaN."""
+    cases = []
+    seed = 1900
+    for m, n, pad in ((1, 1, 0), (2, 2, 1), (7, 7, 0), (33, 33, 2), (70, 70, 0), (100, 100, 1),
+                      (40, 17, 1), (17, 40, 0), (1, 5, 0), (5, 1, 2)):
+        cases.append(dict(routine="Rgetrf", m=m, n=n, pad=(pad,), seed=seed)); seed += 1
+    for sp, m, n in (("zero_col", 20, 20), ("ties", 30, 30), ("ties", 25, 12), ("tiny_pivot", 20, 20),
+                     ("singular", 12, 12), ("nan", 10, 10)):
+        cases.append(dict(routine="Rgetrf", m=m, n=n, pad=(1,), seed=seed, special=sp)); seed += 1
+    for m, n in ((0, 3), (3, 0)):
+        cases.append(dict(routine="Rgetrf", m=m, n=n, pad=(0,), seed=seed)); seed += 1
+    return cases
+
+
+def run_case_getrf(case, store):
+    sys.path.insert(0, REF)
+    import mpkit.mpblas as mb
+    from mpkit.mplapack import Rgetrf
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    m, n = case["m"], case["n"]
+    a = _matrix(mb, m, n, lds["lda"], (arrays["A_hi"], arrays["A_lo"]))
+    with np.errstate(all="ignore"):
+        ipiv, info = Rgetrf(m, n, a, lds["lda"])
+    case["info"] = int(info)
+    case["ipiv"] = [int(p) for p in ipiv]
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    store["arrays"][f"c{cid}_out_hi"] = np.asarray(a.store[0], dtype=np.float64)
+    store["arrays"][f"c{cid}_out_lo"] = np.asarray(a.store[1], dtype=np.float64)
+    store["cases"].append(case)
+
+
 def run_case(mb, DDouble, case, store):
+    if case["routine"] == "Rtrsm":
+        return run_case_trsm(case, store)
+    if case["routine"] == "Rgetrf":
+        return run_case_getrf(case, store)
     if case["routine"] == "Cgemm":
         return run_case_complex(mb, case, store)
     if case["routine"] == "Rpotrf":
@@ -380,7 +482,8 @@ def main():
     mb, elem, DDouble = _ref()
     os.makedirs(OUT, exist_ok=True)
     store = {"cases": [], "arrays": {}}
-    for case in gemm_cases() + syrk_cases() + f64_cases() + complex_cases() + potrf_cases():
+    for case in (gemm_cases() + syrk_cases() + f64_cases() + complex_cases() + potrf_cases()
+                 + trsm_cases() + getrf_cases()):
         run_case(mb, DDouble, case, store)
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
     with open(os.path.join(OUT, "cases.json"), "w") as f:

@@ -75,6 +75,16 @@ def lib():
                                     ctypes.POINTER(ctypes.c_int64)]
         L.oracle_potrf_validate.restype = ctypes.c_int
         L.oracle_potrf_validate.argtypes = [ctypes.c_char, _i64, _i64]
+        L.oracle_rtrsm.restype = ctypes.c_int
+        L.oracle_rtrsm.argtypes = [ctypes.c_char] * 4 + [_i64, _i64, ctypes.c_double, ctypes.c_double,
+                                                         _dp, _dp, _i64, _dp, _dp, _i64]
+        L.oracle_trsm_validate.restype = ctypes.c_int
+        L.oracle_trsm_validate.argtypes = [ctypes.c_char] * 4 + [_i64] * 4
+        L.oracle_rgetrf.restype = ctypes.c_int
+        L.oracle_rgetrf.argtypes = [_i64, _i64, _dp, _dp, _i64, ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_int64)]
+        L.oracle_getrf_validate.restype = ctypes.c_int
+        L.oracle_getrf_validate.argtypes = [_i64, _i64, _i64]
         L.oracle_div2.restype = None
         L.oracle_div2.argtypes = [ctypes.c_double] * 4 + [_dp]
         L.oracle_sqrt2.restype = None
@@ -164,6 +174,25 @@ def rpotrf(uplo, n, a_hi, a_lo, lda):
     info = ctypes.c_int64(0)
     rc = lib().oracle_rpotrf(_flag(uplo), n, _ptr(a_hi), _ptr(a_lo), lda, ctypes.byref(info))
     return rc, int(info.value)
+
+
+def rtrsm(side, uplo, transa, diag, m, n, alpha, a_hi, a_lo, lda, b_hi, b_lo, ldb):
+    """In-place dd triangular solve in the reference's order
+    (mpblas/level23.py:288-380); alpha = (hi, lo).  Returns the reference
+    argument index of an invalid argument, else 0."""
+    return lib().oracle_rtrsm(_flag(side), _flag(uplo), _flag(transa), _flag(diag), m, n,
+                              float(alpha[0]), float(alpha[1]), _ptr(a_hi), _ptr(a_lo), lda,
+                              _ptr(b_hi), _ptr(b_lo), ldb)
+
+
+def rgetrf(m, n, a_hi, a_lo, lda):
+    """In-place dd LU with partial pivoting (mplapack/lu.py:74-114).
+    Returns (rc, ipiv list (1-based), info)."""
+    mn = max(0, min(m, n))
+    ipiv = (ctypes.c_int64 * max(1, mn))()
+    info = ctypes.c_int64(0)
+    rc = lib().oracle_rgetrf(m, n, _ptr(a_hi), _ptr(a_lo), lda, ipiv, ctypes.byref(info))
+    return rc, [int(ipiv[i]) for i in range(mn)], int(info.value)
 
 
 def div2(x, y):

@@ -18,6 +18,8 @@ def bits_equal(a, b):
 ALL = list(golden.load_cases())
 CASES = [c for c in ALL if c[0]["routine"] in ("Rgemm", "Rsyrk")]
 PCASES = [c for c in ALL if c[0]["routine"] == "Rpotrf"]
+TCASES = [c for c in ALL if c[0]["routine"] == "Rtrsm"]
+LCASES = [c for c in ALL if c[0]["routine"] == "Rgetrf"]
 CCASES = [c for c in ALL if c[0]["routine"] == "Cgemm"]
 
 
@@ -153,3 +155,50 @@ def test_oracle_scalar_div_sqrt_match_reference():
 def test_oracle_potrf_validation_indices(args, idx):
     uplo, n, lda = args
     assert oracle.lib().oracle_potrf_validate(uplo.encode(), n, lda) == idx
+
+
+@pytest.mark.parametrize("idx", range(len(TCASES)))
+def test_oracle_rtrsm_matches_reference_bitwise(idx):
+    """mpblas/level23.py:288-380 restated in C, against the reference's output."""
+    case, arr, out_hi, out_lo = TCASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"]
+    bh, bl = arr["B_hi"].copy(), arr["B_lo"].copy()
+    with np.errstate(all="ignore"):
+        rc = oracle.rtrsm(case["side"], case["uplo"], case["transa"], case["diag"], case["m"],
+                          case["n"], case["alpha_v"], arr["A_hi"], arr["A_lo"], case["lda"],
+                          bh, bl, case["ldb"])
+    assert rc == 0
+    assert bits_equal(bh, out_hi), case
+    assert bits_equal(bl, out_lo), case
+
+
+@pytest.mark.parametrize("idx", range(len(LCASES)))
+def test_oracle_rgetrf_matches_reference_bitwise(idx):
+    """mplapack/lu.py:74-114 restated in C: factors, ipiv and info."""
+    case, arr, out_hi, out_lo = LCASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"]
+    ah, al = arr["A_hi"].copy(), arr["A_lo"].copy()
+    with np.errstate(all="ignore"):
+        rc, ipiv, info = oracle.rgetrf(case["m"], case["n"], ah, al, case["lda"])
+    assert rc == 0
+    assert ipiv == case["ipiv"] and info == case["info"], case
+    assert bits_equal(ah, out_hi), case
+    assert bits_equal(al, out_lo), case
+
+
+@pytest.mark.parametrize("args,idx", [
+    (("X", "U", "N", "N", 2, 2, 2, 2), 1), (("L", "X", "N", "N", 2, 2, 2, 2), 2),
+    (("L", "U", "X", "N", 2, 2, 2, 2), 3), (("L", "U", "N", "X", 2, 2, 2, 2), 4),
+    (("L", "U", "N", "N", -1, 2, 2, 2), 5), (("L", "U", "N", "N", 2, -1, 2, 2), 6),
+    (("L", "U", "N", "N", 3, 2, 2, 3), 9), (("R", "U", "N", "N", 2, 3, 2, 2), 9),
+    (("L", "U", "N", "N", 3, 2, 3, 2), 11), (("r", "l", "c", "u", 2, 3, 3, 2), 0)])
+def test_oracle_trsm_validation_indices(args, idx):
+    s, u, t, d, m, n, lda, ldb = args
+    assert oracle.lib().oracle_trsm_validate(s.encode(), u.encode(), t.encode(), d.encode(), m, n,
+                                             lda, ldb) == idx
+
+
+@pytest.mark.parametrize("args,idx", [((-1, 2, 2), 1), ((2, -1, 2), 2), ((3, 2, 2), 4),
+                                      ((0, 0, 0), 4), ((0, 0, 1), 0)])
+def test_oracle_getrf_validation_indices(args, idx):
+    assert oracle.lib().oracle_getrf_validate(*args) == idx
