@@ -118,6 +118,20 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
                    const double* a, int64_t lda, const double* b, int64_t ldb, const double* beta,
                    double* c, int64_t ldc, void* stream);
 
+/* Triangular solve: mpkit.mpblas.Rtrsm (level23.py:288-380), dd, X over B.
+ * side 'L': op(A) X = alpha B, 'R': X op(A) = alpha B; uplo, transa
+ * ('N', 'T', 'C'), diag ('U' unit, 'N').  Exact / reference modes are
+ * bit-identical to the reference (blocked where the reference's per-element
+ * order allows it; L,T,L and R,N,L run one sequential recurrence per
+ * vector); fast / twosum use the blocked order with fast-mode GEMM updates.
+ * Returns 0 / the reference argument index (1-6, 9, 11) / DDB_E*. */
+int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+              double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
+              int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream);
+int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                   double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
+                   int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream);
+
 /* Cholesky: mpkit.mplapack.Rpotrf (mplapack/chol.py:21-65), dd, in place.
  * uplo 'L': A = L L^T, 'U': A = U^T U; only that triangle is read / written.
  * Blocked right-looking, two levels: outer block width nb (<= 0 = default
@@ -139,6 +153,8 @@ int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k
                        int64_t lda, int64_t ldb, int64_t ldc);
 int ddb_rsyrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc);
 int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda);
+int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                       int64_t lda, int64_t ldb);
 
 const char* ddb_last_error(void);
 int ddb_version(void);

@@ -7,9 +7,9 @@ compute runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI in
 
 from .matrix import BlasError, DeviceMatrix, HostMatrix, to_dd
 from .lapack import Rpotrf
-from .mpblas import Cgemm, Rgemm, Rsyrk, default_mode
+from .mpblas import Cgemm, Rgemm, Rsyrk, Rtrsm, default_mode
 
-__all__ = ["Rgemm", "Rsyrk", "Cgemm", "Rpotrf", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
+__all__ = ["Rgemm", "Rsyrk", "Rtrsm", "Cgemm", "Rpotrf", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
            "default_mode", "flop_count"]
 
 

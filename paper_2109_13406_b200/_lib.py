@@ -26,7 +26,8 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_version", "ddb_launch_count", "ddb_last_route", "ddb_fp64_peak_probe",
            "ddb_dgemm", "ddb_dsyrk", "ddb_dgemm_host", "ddb_dsyrk_host",
            "ddb_cgemm", "ddb_cgemm_host", "ddb_zgemm", "ddb_zgemm_host",
-           "ddb_rpotrf", "ddb_rpotrf_host", "ddb_rpotrf_validate")
+           "ddb_rpotrf", "ddb_rpotrf_host", "ddb_rpotrf_validate",
+           "ddb_rtrsm", "ddb_rtrsm_host", "ddb_rtrsm_validate")
 
 _lib = None
 
@@ -73,6 +74,13 @@ def load():
         f = getattr(L, name)
         f.restype = ctypes.c_int
         f.argtypes = po
+    tr = [_c, _c, _c, _c, _i64, _i64, _d, _d, _dp, _dp, _i64, _dp, _dp, _i64, ctypes.c_int, _dp]
+    for name in ("ddb_rtrsm", "ddb_rtrsm_host"):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = tr
+    L.ddb_rtrsm_validate.restype = ctypes.c_int
+    L.ddb_rtrsm_validate.argtypes = [_c, _c, _c, _c] + [_i64] * 4
     L.ddb_rpotrf_validate.restype = ctypes.c_int
     L.ddb_rpotrf_validate.argtypes = [_c, _i64, _i64]
     L.ddb_rgemm_validate.restype = ctypes.c_int

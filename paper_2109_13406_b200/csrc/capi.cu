@@ -595,6 +595,135 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
   return stage_out1(c, C, sc, s);
 }
 
+// ---- triangular solve (dd_trsm.cu) -------------------------------------------
+
+int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                       int64_t lda, int64_t ldb) {
+  const int sd = upflag(side), u = upflag(uplo), t = upflag(transa), d = upflag(diag);
+  if (sd != 'L' && sd != 'R') return 1;               // level23.py:296-299
+  if (u != 'U' && u != 'L') return 2;
+  if (t != 'N' && t != 'T' && t != 'C') return 3;
+  if (d != 'U' && d != 'N') return 4;
+  if (m < 0) return 5;                                // :300-301
+  if (n < 0) return 6;
+  const int64_t nrowa = sd == 'L' ? m : n;            // :302-304
+  if (lda < (nrowa > 1 ? nrowa : 1)) return 9;
+  if (ldb < (m > 1 ? m : 1)) return 11;
+  return 0;
+}
+
+int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+              double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
+              int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream) {
+  const int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM) {
+    g_last_error = "unknown mode";
+    return DDB_EINVAL;
+  }
+  if (m == 0 || n == 0) return DDB_OK;                // :306-307
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (is_zero(alpha_hi, alpha_lo)) {                  // :310-312: B = 0
+    e = cudaMemset2DAsync(b_hi, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
+    if (e == cudaSuccess) e = cudaMemset2DAsync(b_lo, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
+    return e == cudaSuccess ? DDB_OK : fail(e, "rtrsm zero fill");
+  }
+  const bool left = upflag(side) == 'L', upper = upflag(uplo) == 'U';
+  const bool notr = upflag(transa) == 'N', alpha_one = is_one(alpha_hi, alpha_lo);
+  const dd alpha{alpha_hi, alpha_lo};
+  // branch table (see dd_trsm.cu): production order, T orientation, finish,
+  // alpha placement, and whether the terms arrive in reverse order
+  TrsmArgs t{};
+  t.left = left;
+  t.unit = upflag(diag) == 'U';
+  t.fin_rec = !left;
+  int trans, init_scale, post_scale, rev_terms;
+  if (left && notr) {        t.rev = upper;  trans = 0; init_scale = !alpha_one; post_scale = 0; rev_terms = 0; }
+  else if (left) {           t.rev = !upper; trans = 1; init_scale = 1;          post_scale = 0; rev_terms = !upper; }
+  else if (notr) {           t.rev = !upper; trans = 1; init_scale = !alpha_one; post_scale = 0; rev_terms = !upper; }
+  else {                     t.rev = upper;  trans = 0; init_scale = 0; post_scale = !alpha_one; rev_terms = 0; }
+  t.p = left ? m : n;
+  t.q = left ? n : m;
+  t.ldw = t.p;
+  t.ldt = t.p;
+  retain_pool_memory();
+  const size_t wsz = (size_t)t.p * t.q, tsz = (size_t)t.p * t.p;
+  void* ws = nullptr;
+  e = cudaMallocAsync(&ws, sizeof(double) * 2 * (wsz + tsz + t.p), s);
+  if (e != cudaSuccess) return fail(e, "rtrsm workspace");
+  double* w = static_cast<double*>(ws);
+  t.w_hi = w; t.w_lo = w + wsz;
+  t.t_hi = w + 2 * wsz; t.t_lo = t.t_hi + tsz;
+  t.d_hi = t.t_lo + tsz; t.d_lo = t.d_hi + t.p;
+  int nl = 0, rc2 = DDB_OK;
+  e = launch_trsm_pack(t, b_hi, b_lo, ldb, init_scale, alpha, s);
+  ++nl;
+  if (e == cudaSuccess) { e = launch_trsm_coef(t, a_hi, a_lo, lda, trans, s); ++nl; }
+  const bool exact_order = mode == MODE_EXACT || mode == MODE_REFERENCE;
+  if (e == cudaSuccess && rev_terms && exact_order) {
+    e = launch_trsm_rev(t, s);
+    ++nl;
+  } else if (e == cudaSuccess) {
+    static const int64_t nb_env = [] {
+      const char* v = std::getenv("DDB_TRSM_NB");
+      return v ? (int64_t)std::atoll(v) : (int64_t)0;
+    }();
+    const int64_t nb = nb_env > 0 && nb_env <= 96 ? nb_env : 64;
+    for (int64_t r0 = 0; r0 < t.p && e == cudaSuccess && rc2 == DDB_OK; r0 += nb) {
+      const int64_t r1 = r0 + nb < t.p ? r0 + nb : t.p;
+      e = launch_trsm_block(t, r0, (int)(r1 - r0), s);
+      ++nl;
+      if (e != cudaSuccess || r1 >= t.p) break;
+      // W(r1:p, :) -= T(r1:p, r0:r1) W(r0:r1, :), terms in production order
+      GemmArgs g{};
+      g.ta = 0; g.tb = 0; g.syrk = 0;
+      g.m = t.p - r1; g.n = t.q; g.k = r1 - r0;
+      g.a_hi = t.t_hi + r1 + r0 * t.ldt; g.a_lo = t.t_lo + r1 + r0 * t.ldt; g.lda = t.ldt;
+      g.b_hi = t.w_hi + r0; g.b_lo = t.w_lo + r0; g.ldb = t.ldw;
+      g.c_hi = t.w_hi + r1; g.c_lo = t.w_lo + r1; g.ldc = t.ldw;
+      g.beta = dd{1.0, 0.0};
+      if (exact_order) { g.sub = 1; g.alpha = dd{1.0, 0.0}; }
+      else { g.sub = 0; g.alpha = dd{-1.0, 0.0}; }
+      rc2 = run(g, mode, s);
+    }
+  }
+  if (e == cudaSuccess && rc2 == DDB_OK) {
+    e = launch_trsm_unpack(t, b_hi, b_lo, ldb, post_scale, alpha, s);
+    ++nl;
+  }
+  g_launches += nl;
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  if (rc2 != DDB_OK) return rc2;
+  if (e != cudaSuccess) return fail(e, "rtrsm");
+  if (e2 != cudaSuccess) return fail(e2, "workspace free");
+  return DDB_OK;
+}
+
+int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                   double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
+                   int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream) {
+  int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
+  if (rc) return rc;
+  if (m == 0 || n == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t na = upflag(side) == 'L' ? m : n;
+  const int64_t sa = is_zero(alpha_hi, alpha_lo) ? 0 : span(na, na, lda);
+  const int64_t sb = span(m, n, ldb);
+  DevBuf A, B;
+  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
+  if ((rc = stage_in(B, b_hi, b_lo, sb, s))) return rc;
+  rc = ddb_rtrsm(side, uplo, transa, diag, m, n, alpha_hi, alpha_lo, A.p, A.p ? A.p + sa : nullptr,
+                 lda, B.p, B.p + sb, ldb, mode, stream);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(b_hi, B.p, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(b_lo, B.p + sb, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
 // ---- blocked Cholesky (dd_potrf.cu) ----------------------------------------
 
 int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {

@@ -36,12 +36,17 @@ reference_kernel(GemmArgs g, const int* __restrict__ flag, int gate) {
       if (dd_is_one(g.beta)) continue;
       out = scale_beta(g.beta, c0);
     } else if (g.ta == 0) {
-      dd c = scale_beta(g.beta, c0);
+      dd c = g.sub ? c0 : scale_beta(g.beta, c0);
       for (int64_t l = 0; l < g.k; ++l) {
         const int64_t bi = g.tb == 0 ? l + j * g.ldb : j + l * g.ldb;
-        const dd t = mul2_chk(g.alpha, dd{g.b_hi[bi], g.b_lo[bi]});
+        const dd b{g.b_hi[bi], g.b_lo[bi]};
         const int64_t ai = i + l * g.lda;
-        c = add2_chk(c, mul2_chk(dd{g.a_hi[ai], g.a_lo[ai]}, t));
+        if (g.sub) {   // be.sub(c, be.mul(a, b)) (level23.py:334-336)
+          const dd p = mul2_chk(dd{g.a_hi[ai], g.a_lo[ai]}, b);
+          c = add2_chk(c, dd{-p.h, -p.l});
+        } else {
+          c = add2_chk(c, mul2_chk(dd{g.a_hi[ai], g.a_lo[ai]}, mul2_chk(g.alpha, b)));
+        }
       }
       out = c;
     } else {

@@ -156,7 +156,7 @@ __device__ __forceinline__ void load_stage(const GemmArgs& g, double* sA, double
   }
 }
 
-template <int ALG, int TM, int TN>
+template <int ALG, int TM, int TN, bool SUB = false>
 __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN],
                                          const double (&ah)[TM], const double (&al)[TM],
                                          const double (&bh)[TN], const double (&bl)[TN]) {
@@ -205,7 +205,8 @@ __device__ __forceinline__ void mac_step(double (&H)[TM][TN], double (&L)[TM][TN
         L[a][b] = dadd(l, r);
         H[a][b] = Tn;
       } else if (ALG == ALG_EXACT) {
-        const dd p = mul2_nc(dd{ah[a], al[a]}, dd{bh[b], bl[b]});
+        dd p = mul2_nc(dd{ah[a], al[a]}, dd{bh[b], bl[b]});
+        if (SUB) p = dd{-p.h, -p.l};
         const dd c = DDB_EXACT_SEL ? add2_nc_sel(dd{H[a][b], L[a][b]}, p)
                                    : add2_nc(dd{H[a][b], L[a][b]}, p);
         H[a][b] = c.h;
@@ -354,7 +355,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       }
       __syncthreads();
     }
-    if (ALG == ALG_EXACT && TA == 0) {
+    if (ALG == ALG_EXACT && TA == 0 && SYRK != 3) {
       // t = mul2(alpha, op(B)(l, j)) once per tile element (level23.py:122, :137)
 #pragma unroll
       for (int r = 0; r < BN * BK / NT; ++r) {
@@ -397,7 +398,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
     auto k_step = [&](int kk) {
       double ah[TM], al[TM], bh[TN], bl[TN];
       load_ops(kk, ah, al, bh, bl);
-      mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
+      mac_step<ALG, TM, TN, SYRK == 3>(H, L, ah, al, bh, bl);
     };
     auto renorm = [&]() {
 #pragma unroll
@@ -435,8 +436,8 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
         load_ops(0, ah, al, bh, bl);
 #pragma unroll 1
         for (int kk = 0; kk < BK; kk += 2) {
-          mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
-          mac_step<ALG, TM, TN>(H, L, ah, al, bh, bl);
+          mac_step<ALG, TM, TN, SYRK == 3>(H, L, ah, al, bh, bl);
+          mac_step<ALG, TM, TN, SYRK == 3>(H, L, ah, al, bh, bl);
           if (ALG == ALG_CERT) fold();
         }
       } else
@@ -450,7 +451,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
           for (int j = 0; j < DDB_UNR; ++j) {
             if (j + 1 < DDB_UNR)
               load_ops(kk + j + 1, ah[(j + 1) & 1], al[(j + 1) & 1], bh[(j + 1) & 1], bl[(j + 1) & 1]);
-            mac_step<ALG, TM, TN>(H, L, ah[j & 1], al[j & 1], bh[j & 1], bl[j & 1]);
+            mac_step<ALG, TM, TN, SYRK == 3>(H, L, ah[j & 1], al[j & 1], bh[j & 1], bl[j & 1]);
             if (ALG == ALG_CERT && (j % RF) == RF - 1) fold();
             if ((ALG == ALG_TWOSUM || ALG == ALG_SELECT) && ((kk + j + 1) % RN) == 0) renorm();
           }
@@ -531,6 +532,11 @@ cudaError_t launch_one(const GemmArgs& g, const int* row_exp, const int* col_exp
 template <class C, int ALG>
 cudaError_t launch_alg(const GemmArgs& g, const int* row_exp, const int* col_exp,
                        const int* flag, cudaStream_t s) {
+  if constexpr (ALG == ALG_EXACT) {
+    if (g.sub && g.syrk == 0 && g.ta == 0)   // SYRK = 3: the subtract-product form
+      return g.tb == 0 ? launch_one<C, 0, 0, ALG, 3>(g, row_exp, col_exp, flag, s)
+                       : launch_one<C, 0, 1, ALG, 3>(g, row_exp, col_exp, flag, s);
+  }
   if (g.syrk == 0) {
     switch (g.ta * 2 + g.tb) {
       case 0: return launch_one<C, 0, 0, ALG, 0>(g, row_exp, col_exp, flag, s);

@@ -44,6 +44,10 @@ struct GemmArgs {
   // binary64 precision (the reference's 'f64' Matrix): only the hi planes
   // exist; a_lo / b_lo / c_lo are unused (dd_reference.cu, ALG_F64)
   int f64;
+  // exact / reference modes, TA == 0 only: c = c - a*b per step with the
+  // product negated after rounding (be.sub(c, be.mul(a, b)), the reference's
+  // Rtrsm update, level23.py:334-336); alpha, beta unused (treated as 1)
+  int sub;
 };
 
 // Which kernel should run, decided on the device by the prescan flag.
@@ -111,5 +115,24 @@ cudaError_t launch_potrf_panel(const PotrfArgs& p, int64_t j0, int nb, int64_t r
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,
                                    int64_t rows, cudaStream_t s);
 cudaError_t launch_potrf_restore(const PotrfArgs& p, cudaStream_t s);
+
+// triangular solve (dd_trsm.cu): the recurrence in production order over
+// p x q work planes W (ld = ldw) with coefficients T (p x p, ld = ldt)
+struct TrsmArgs {
+  int64_t p, q;
+  int left, rev, unit, fin_rec;
+  double *w_hi, *w_lo; int64_t ldw;
+  double *t_hi, *t_lo; int64_t ldt;
+  double *d_hi, *d_lo;
+};
+
+cudaError_t launch_trsm_pack(const TrsmArgs& t, const double* bh, const double* bl, int64_t ldb,
+                             int scale, dd alpha, cudaStream_t s);
+cudaError_t launch_trsm_unpack(const TrsmArgs& t, double* bh, double* bl, int64_t ldb, int scale,
+                               dd alpha, cudaStream_t s);
+cudaError_t launch_trsm_coef(const TrsmArgs& t, const double* ah, const double* al, int64_t lda,
+                             int trans, cudaStream_t s);
+cudaError_t launch_trsm_block(const TrsmArgs& t, int64_t r0, int nb, cudaStream_t s);
+cudaError_t launch_trsm_rev(const TrsmArgs& t, cudaStream_t s);
 
 }  // namespace ddb

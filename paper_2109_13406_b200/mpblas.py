@@ -39,7 +39,7 @@ from . import _lib
 from .matrix import (BlasError, check_storage, dd_is_one, dd_truthy, is_device, require,
                      same_precision, to_c64, to_cdd, to_dd)
 
-__all__ = ["Rgemm", "Rsyrk", "Cgemm", "BlasError", "default_mode"]
+__all__ = ["Rgemm", "Rsyrk", "Rtrsm", "Cgemm", "BlasError", "default_mode"]
 
 
 def default_mode():
@@ -240,6 +240,50 @@ def Rsyrk(uplo, trans, n, k, alpha, a, lda=None, beta=1.0, c=None, ldc=None, *, 
                           hc.ptr(0), hc.ptr(1), ldc, code, None)
     _raise_rc(routine, rc)
     hc.commit()
+
+
+def Rtrsm(side, uplo, transa, diag, m, n, alpha, a, lda=None, b=None, ldb=None, *,
+          mode=None):
+    """Solve op(A)*X = alpha*B (side 'L') or X*op(A) = alpha*B ('R') in place
+    in B on the B200 (level23.py:288-380; checks :292-304).  mode "exact" /
+    "reference": bit-identical to the reference; "fast" / "twosum": blocked
+    with fast-mode GEMM updates (dd accuracy, not bit-identical)."""
+    routine = "Rtrsm"
+    tag = same_precision(routine, a, b)
+    if tag != "dd":
+        raise NotImplementedError(
+            f"{routine}: precision {tag!r} is not on the B200 path (only 'dd')")
+    lda, ldb = _ld_of(a, lda), _ld_of(b, ldb)
+    side = _flag(routine, side, ("L", "R"), 1)
+    uplo = _flag(routine, uplo, ("U", "L"), 2)
+    transa = _flag(routine, transa, ("N", "T", "C"), 3)
+    diag = _flag(routine, diag, ("U", "N"), 4)
+    require(routine, m >= 0, 5)
+    require(routine, n >= 0, 6)
+    nrowa = m if side == "L" else n
+    require(routine, lda >= max(1, nrowa), 9)
+    require(routine, ldb >= max(1, m), 11)
+    al = _scalar(tag, alpha)
+    code = _mode_code(mode)
+    if m == 0 or n == 0:
+        return
+    check_storage(a, nrowa, nrowa, lda)
+    check_storage(b, m, n, ldb)
+    L = _lib.load()
+    dev = _placement(routine, a, b)
+    head = (side.encode(), uplo.encode(), transa.encode(), diag.encode(), m, n, al[0], al[1])
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_rtrsm(*head, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, _dev_ptr(b, 0),
+                             _dev_ptr(b, 1), ldb, code, stream)
+        _raise_rc(routine, rc)
+        return
+    ha, hb = _HostPlanes(a.store), _HostPlanes(b.store)
+    rc = L.ddb_rtrsm_host(*head, ha.ptr(0), ha.ptr(1), lda, hb.ptr(0), hb.ptr(1), ldb, code, None)
+    _raise_rc(routine, rc)
+    hb.commit()
 
 
 def Cgemm(transa, transb, m, n, k, alpha, a, lda=None, b=None, ldb=None,

@@ -231,3 +231,41 @@ def test_rpotrf_without_gpu_fails_loudly():
     a.store[0][[0, 3]] = 2.0
     with pytest.raises(RuntimeError):
         Rpotrf("L", 2, a)
+
+
+TRSM_BAD = [(("X", "U", "N", "N", 2, 2), {}, 1), (("L", "X", "N", "N", 2, 2), {}, 2),
+            (("L", "U", "X", "N", 2, 2), {}, 3), (("L", "U", "N", "X", 2, 2), {}, 4),
+            (("L", "U", "N", "N", -1, 2), {}, 5), (("L", "U", "N", "N", 2, -1), {}, 6),
+            (("L", "U", "N", "N", 3, 2), {"lda": 2}, 9), (("R", "U", "N", "N", 2, 3), {"lda": 2}, 9),
+            (("L", "U", "N", "N", 3, 2), {"ldb": 2}, 11)]
+
+
+@pytest.mark.parametrize("args,lds,idx", TRSM_BAD)
+def test_rtrsm_blas_error_indices(args, lds, idx):
+    """level23.py:290-304, and the C ABI's validate agrees."""
+    from paper_2109_13406_b200 import Rtrsm
+    sd, up, tr, dg, m, n = args
+    a, b = HostMatrix(4, 4), HostMatrix(4, 4)
+    with pytest.raises(BlasError) as e:
+        Rtrsm(sd, up, tr, dg, m, n, 1.0, a, lds.get("lda", 4), b, lds.get("ldb", 4))
+    assert e.value.index == idx and e.value.routine == "Rtrsm"
+    try:
+        L = _lib.load()
+    except _lib.LibraryMissing:
+        return
+    assert L.ddb_rtrsm_validate(sd.encode(), up.encode(), tr.encode(), dg.encode(), m, n,
+                                lds.get("lda", 4), lds.get("ldb", 4)) == idx
+
+
+def test_rtrsm_early_exit_and_precision_gate():
+    from paper_2109_13406_b200 import Rtrsm
+    a, b = HostMatrix(3, 3), HostMatrix(3, 3)
+    b.store[0][:] = 7.0
+    Rtrsm("L", "U", "N", "N", 0, 3, 2.0, a, 3, b, 3)          # level23.py:306-307
+    Rtrsm("R", "L", "T", "U", 3, 0, 2.0, a, 3, b, 3)
+    assert np.all(b.store[0] == 7.0)
+    c = HostMatrix(3, 3, "f64")
+    with pytest.raises(NotImplementedError):
+        Rtrsm("L", "U", "N", "N", 3, 3, 1.0, c, 3, HostMatrix(3, 3, "f64"), 3)
+    with pytest.raises(ValueError, match="mixed precisions"):
+        Rtrsm("L", "U", "N", "N", 3, 3, 1.0, a, 3, c, 3)
