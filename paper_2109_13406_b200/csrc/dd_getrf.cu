@@ -1,0 +1,374 @@
+// dd_getrf.cu -- blocked dd LU with partial pivoting (Rgetrf, mplapack/lu.py:74-114).
+//
+// The reference is unblocked right-looking: per column j, pivot search
+// (DDBackend.argmax_abs, elem.py:246-259: max |hi|, ties by max lo*sign(hi),
+// first index), interchange of the whole rows, scaling of the column by the
+// pivot's reciprocal (or a division when |pivot| < safmin), then the rank-1
+// update a(i, c) += mul2(a(i, j), -a(j, c)) of everything right of / below.
+// Per element the updates arrive in j order, so the LAPACK blocking keeps
+// the result bit-identical in exact mode:
+//   1. getrf_panel_kernel  factors the nb-column panel over all rows below j0
+//      -- one cooperative launch, rows split over the CTAs, two grid barriers
+//      per column (after the partial pivot searches; after the interchange);
+//   2. getrf_laswp_kernel  applies the panel's interchanges to the columns
+//      left and right of it (in order, per column);
+//   3. getrf_trsm_kernel   U12 = L11^-1 A12, one thread per column, the
+//      reference's per-element order;
+//   4. the trailing update A22 += L21 (-U12) as Rgemm (alpha = -1, beta = 1)
+//      in the caller's mode: per element c = c + mul2(L, mul2(-1, U)), which
+//      equals the reference's mul2(L, -U) bit for bit (mul2(-1, u) differs
+//      from -u at most in the sign of a zero low word, which mul2 absorbs).
+// A zero pivot sets info (first one) and skips the interchange and scaling
+// but not the update, as the reference does; the pivot index is recorded
+// either way (lu.py:93-106).
+#include <cooperative_groups.h>
+
+#include "internal.h"
+
+namespace ddb {
+
+namespace {
+
+__device__ __forceinline__ dd neg_(dd x) { return dd{-x.h, -x.l}; }
+__device__ __forceinline__ bool fin(double x) { return finite_(x); }
+__device__ __forceinline__ dd canon(double h, double l) { return dd{h, fin(h) ? l : 0.0}; }
+
+__device__ dd add2_scal(dd x, dd y) {
+  const double s0 = dadd(x.h, y.h);
+  if (!fin(s0)) return dd{s0, 0.0};
+  const dd r = add2_chk(x, y);
+  return canon(r.h, r.l);
+}
+__device__ dd mul21_scal(dd x, double y) {
+  double p, e;
+  two_prod_dekker(x.h, y, p, e);
+  if (!(fin(p) && fin(e))) return canon(p, 0.0);
+  e = dadd(e, dmul(x.l, y));
+  double s, t;
+  quick_two_sum(p, e, s, t);
+  return canon(s, t);
+}
+// scalar _div2 (ddarith.py:113-131)
+__device__ dd div2_scal(dd x, dd y) {
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  if (y.h == 0.0) {
+    if (x.h == 0.0) return dd{qnan, 0.0};
+    return dd{copysign(inf, x.h) * copysign(1.0, y.h), 0.0};
+  }
+  if (!(fin(x.h) && fin(y.h))) {
+    if (!fin(y.h) && !isnan(y.h)) {
+      if (!fin(x.h) && !isnan(x.h)) return dd{qnan, 0.0};
+      return dd{dmul(copysign(0.0, x.h), copysign(1.0, y.h)), 0.0};
+    }
+    return canon(dmul(x.h, copysign(1.0, y.h)), 0.0);
+  }
+  const double q1 = x.h / y.h;
+  dd r = add2_scal(x, neg_(mul21_scal(y, q1)));
+  const double q2 = r.h / y.h;
+  r = add2_scal(r, neg_(mul21_scal(y, q2)));
+  const double q3 = r.h / y.h;
+  double a, b;
+  quick_two_sum(q1, q2, a, b);
+  return add2_scal(dd{a, b}, dd{q3, 0.0});
+}
+// vectorised _v_div2 (elem.py:93-117)
+__device__ dd vdiv2(dd x, dd y) {
+  if (y.h == 0.0 || !(fin(x.h) && fin(y.h))) return div2_scal(x, y);
+  auto m21 = [](dd yy, double q) {
+    double p, e;
+    two_prod_dekker(yy.h, q, p, e);
+    const bool bad = !(fin(p) && fin(e));
+    e = dadd(e, dmul(yy.l, q));
+    double s, t;
+    quick_two_sum(p, e, s, t);
+    return bad ? dd{p, 0.0} : dd{s, t};
+  };
+  const double q1 = x.h / y.h;
+  dd r = add2_chk(x, neg_(m21(y, q1)));
+  const double q2 = r.h / y.h;
+  r = add2_chk(r, neg_(m21(y, q2)));
+  const double q3 = r.h / y.h;
+  double a, b;
+  quick_two_sum(q1, q2, a, b);
+  return add2_chk(dd{a, b}, dd{q3, 0.0});
+}
+
+// pivot-search key: larger |hi| wins, then larger lo*sign(hi), then the
+// smaller row index; a NaN |hi| anywhere makes the search return its first
+// row (np.max propagates NaN and no entry compares equal to it)
+struct PivKey {
+  double ah, al;     // |hi|, lo * sign(hi)
+  double h, l;       // the entry itself (the pivot value, read before any interchange)
+  long long idx;
+  int nan;
+};
+__device__ __forceinline__ bool better(const PivKey& x, const PivKey& y) {
+  if (x.idx < 0) return false;
+  if (y.idx < 0) return true;
+  if (x.ah != y.ah) return x.ah > y.ah;
+  if (x.al != y.al) return x.al > y.al;
+  return x.idx < y.idx;
+}
+__device__ __forceinline__ PivKey merge(PivKey x, const PivKey& y) {
+  PivKey r = better(y, x) ? y : x;
+  r.nan = x.nan | y.nan;
+  return r;
+}
+
+__device__ __forceinline__ PivKey shfl_down(const PivKey& k, int o) {
+  PivKey y;
+  y.ah = __shfl_down_sync(0xffffffffu, k.ah, o);
+  y.al = __shfl_down_sync(0xffffffffu, k.al, o);
+  y.h = __shfl_down_sync(0xffffffffu, k.h, o);
+  y.l = __shfl_down_sync(0xffffffffu, k.l, o);
+  y.idx = __shfl_down_sync(0xffffffffu, k.idx, o);
+  y.nan = __shfl_down_sync(0xffffffffu, k.nan, o);
+  return y;
+}
+
+__device__ __forceinline__ double ldg_cg(const double* p) { return __ldcg(p); }
+
+// grid-wide barrier for a cooperative launch: arrival counter in global
+// memory, target = gridDim.x * (number of barriers so far)
+__device__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kPanelThreads = 256;
+
+// block-wide best key (all threads get it)
+__device__ PivKey block_best(PivKey k) {
+  __shared__ PivKey red[kPanelThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) k = merge(k, shfl_down(k, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = k;
+  __syncthreads();
+  PivKey r = red[0];
+  for (int i = 1; i < kPanelThreads / 32; ++i) r = merge(r, red[i]);
+  return r;
+}
+
+}  // namespace
+
+// Panel [j0, j0 + nb) over rows [j0, m).  CTA c owns rows [r0c, r1c).
+__global__ void __launch_bounds__(kPanelThreads)
+getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
+  __shared__ PivKey best_s;
+  __shared__ dd piv_s, rec_s;
+  __shared__ int use_rec_s, nonzero_s;
+  const int64_t rows = g.m - j0;
+  const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = j0 + (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = r0 + chunk < g.m ? r0 + chunk : g.m;
+  const int64_t lda = g.lda;
+  double* ah = g.a_hi;
+  double* al = g.a_lo;
+  unsigned nbar = 0;
+  auto local_search = [&](int64_t j) {
+    PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
+    for (int64_t i = (r0 > j ? r0 : j) + threadIdx.x; i < r1; i += blockDim.x) {
+      const double h = ldg_cg(ah + i + j * lda), l = ldg_cg(al + i + j * lda);
+      PivKey y{fabs(h), h < 0.0 ? -l : l, h, l, (long long)i, isnan(h) ? 1 : 0};
+      k = merge(k, y);
+    }
+    k = block_best(k);
+    if (threadIdx.x == 0) {
+      g.part_ah[blockIdx.x] = k.ah;
+      g.part_al[blockIdx.x] = k.al;
+      g.part_h[blockIdx.x] = k.h;
+      g.part_l[blockIdx.x] = k.l;
+      g.part_idx[blockIdx.x] = k.idx;
+      g.part_nan[blockIdx.x] = k.nan;
+    }
+  };
+  local_search(j0);
+  const int64_t jend = j0 + nb;
+  for (int64_t j = j0; j < jend; ++j) {
+    grid_barrier(g.bar, gridDim.x * ++nbar);
+    if (threadIdx.x < 32) {   // merge the partial searches (warp 0)
+      PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+        PivKey y{__ldcg(g.part_ah + c), __ldcg(g.part_al + c), __ldcg(g.part_h + c),
+                 __ldcg(g.part_l + c), __ldcg(g.part_idx + c), __ldcg(g.part_nan + c)};
+        k = merge(k, y);
+      }
+      for (int o = 16; o > 0; o >>= 1) k = merge(k, shfl_down(k, o));
+      if (threadIdx.x == 0) {
+        dd piv{k.h, k.l};
+        if (k.nan || k.idx < 0) {   // argmax_abs returns 0 -> the diagonal entry
+          k.idx = j;
+          piv = dd{ldg_cg(ah + j + j * lda), ldg_cg(al + j + j * lda)};
+        }
+        best_s = k;
+        const int64_t jp = k.idx;
+        piv_s = piv;
+        nonzero_s = !(piv.h == 0.0 && piv.l == 0.0);
+        // |pivot| >= safmin (lu.py:98): DDouble abs then _cmp2 order
+        dd ap = piv;
+        if (ap.h < 0.0 || (ap.h == 0.0 && ap.l < 0.0)) ap = neg_(ap);
+        const double sh = 0x1p-969, sl = -0x0.0000000000006p-1022;
+        use_rec_s = ap.h > sh || (ap.h == sh && ap.l >= sl);
+        if (nonzero_s && use_rec_s) rec_s = div2_scal(dd{1.0, 0.0}, piv);
+        if (blockIdx.x == 0) {
+          g.ipiv[j] = jp + 1;
+          g.swap[j] = nonzero_s ? jp : j;
+          if (!nonzero_s && *g.info == 0) *g.info = (int)(j + 1);
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t jp = best_s.idx;
+    const bool nonzero = nonzero_s;
+    if (blockIdx.x == 0 && nonzero && jp != j) {   // interchange within the panel
+      for (int64_t c = j0 + threadIdx.x; c < jend; c += blockDim.x) {
+        const double th = ldg_cg(ah + j + c * lda), tl = ldg_cg(al + j + c * lda);
+        ah[j + c * lda] = ldg_cg(ah + jp + c * lda);
+        al[j + c * lda] = ldg_cg(al + jp + c * lda);
+        ah[jp + c * lda] = th;
+        al[jp + c * lda] = tl;
+      }
+    }
+    grid_barrier(g.bar, gridDim.x * ++nbar);
+    // scale the column below the pivot (own rows), then the rank-1 update of
+    // the panel's later columns
+    const int64_t lo_row = r0 > j + 1 ? r0 : j + 1;
+    if (nonzero) {
+      const bool use_rec = use_rec_s;
+      const dd rec = rec_s, piv = piv_s;
+      for (int64_t i = lo_row + threadIdx.x; i < r1; i += blockDim.x) {
+        const dd x{ldg_cg(ah + i + j * lda), ldg_cg(al + i + j * lda)};
+        const dd y = use_rec ? mul2_chk(rec, x) : vdiv2(x, piv);
+        ah[i + j * lda] = y.h;
+        al[i + j * lda] = y.l;
+      }
+    }
+    __syncthreads();
+    const int64_t ncol = jend - j - 1;
+    const int64_t nrow = r1 - lo_row;
+    if (ncol > 0 && nrow > 0 && j < g.mn - 1) {
+      for (int64_t t = threadIdx.x; t < ncol * nrow; t += blockDim.x) {
+        const int64_t i = lo_row + t % nrow, c = j + 1 + t / nrow;
+        const dd x{ldg_cg(ah + i + j * lda), ldg_cg(al + i + j * lda)};
+        const dd u{ldg_cg(ah + j + c * lda), ldg_cg(al + j + c * lda)};
+        const dd r = add2_chk(dd{ldg_cg(ah + i + c * lda), ldg_cg(al + i + c * lda)},
+                              mul2_chk(x, neg_(u)));
+        ah[i + c * lda] = r.h;
+        al[i + c * lda] = r.l;
+      }
+    }
+    __syncthreads();
+    if (j + 1 < jend) local_search(j + 1);
+  }
+}
+
+// Apply the interchanges of steps [j0, j1) in order to columns [c0, c1).
+__global__ void __launch_bounds__(256)
+getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1) {
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
+  double* ah = g.a_hi + c * g.lda;
+  double* al = g.a_lo + c * g.lda;
+  for (int64_t j = j0; j < j1; ++j) {
+    const int64_t p = g.swap[j];
+    if (p == j) continue;
+    const double th = ah[j], tl = al[j];
+    ah[j] = ah[p];
+    al[j] = al[p];
+    ah[p] = th;
+    al[p] = tl;
+  }
+}
+
+// U12 = L11^-1 A12 for columns [c0, n): per column, rows r in [j0, j1):
+// a(r, c) += mul2(L(r, l), -U(l, c)) for l = j0 .. r-1 in order.
+__global__ void __launch_bounds__(128)
+getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0) {
+  extern __shared__ double sm[];
+  double* lh = sm;
+  double* ll = sm + nb * nb;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    const int r = e % nb, l = e / nb;
+    if (l < r) {
+      lh[e] = g.a_hi[(j0 + r) + (j0 + l) * g.lda];
+      ll[e] = g.a_lo[(j0 + r) + (j0 + l) * g.lda];
+    }
+  }
+  __syncthreads();
+  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= g.n) return;
+  double* uh = g.a_hi + j0 + c * g.lda;
+  double* ul = g.a_lo + j0 + c * g.lda;
+  for (int r = 1; r < nb; ++r) {
+    dd acc{uh[r], ul[r]};
+    for (int l = 0; l < r; ++l)
+      acc = add2_chk(acc, mul2_chk(dd{lh[r + l * nb], ll[r + l * nb]}, neg_(dd{uh[l], ul[l]})));
+    uh[r] = acc.h;
+    ul[r] = acc.l;
+  }
+}
+
+static int panel_grid(int64_t rows) {
+  static thread_local int cached_dev = -1, cached_max = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != cached_dev) {
+    int sms = 0, per = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrf_panel_kernel, kPanelThreads, 0);
+    cached_max = per > 0 ? sms : 1;                            // one CTA per SM
+    cached_dev = dev;
+  }
+  int64_t want = (rows + 63) / 64;                            // >= 64 rows per CTA
+  if (want < 1) want = 1;
+  return (int)(want < cached_max ? want : cached_max);
+}
+
+int getrf_max_panel_ctas() { return panel_grid(1LL << 40); }
+
+cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStream_t s) {
+  const int grid = panel_grid(g.m - j0);
+  cudaError_t e = cudaMemsetAsync(g.bar, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  GetrfArgs ga = g;
+  int nbv = nb;
+  void* args[] = {&ga, &j0, &nbv};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(getrf_panel_kernel), dim3(grid),
+                                     dim3(kPanelThreads), args, 0, s);
+}
+
+cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
+                               cudaStream_t s) {
+  if (c1 <= c0) return cudaSuccess;
+  getrf_laswp_kernel<<<(unsigned)((c1 - c0 + 255) / 256), 256, 0, s>>>(g, j0, j1, c0, c1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, cudaStream_t s) {
+  if (g.n <= c0 || nb <= 1) return cudaSuccess;
+  const size_t smem = 2 * sizeof(double) * (size_t)nb * nb;
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(getrf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr_dev = dev;
+  }
+  getrf_trsm_kernel<<<(unsigned)((g.n - c0 + 127) / 128), 128, smem, s>>>(g, j0, nb, c0);
+  return cudaGetLastError();
+}
+
+}  // namespace ddb

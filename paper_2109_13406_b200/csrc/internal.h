@@ -135,4 +135,23 @@ cudaError_t launch_trsm_coef(const TrsmArgs& t, const double* ah, const double* 
 cudaError_t launch_trsm_block(const TrsmArgs& t, int64_t r0, int nb, cudaStream_t s);
 cudaError_t launch_trsm_rev(const TrsmArgs& t, cudaStream_t s);
 
+// LU with partial pivoting (dd_getrf.cu)
+struct GetrfArgs {
+  int64_t m, n, mn, lda;
+  double *a_hi, *a_lo;
+  long long* ipiv;              // 1-based pivot rows (device)
+  long long* swap;              // interchange actually applied at step j (j = none)
+  int* info;
+  double *part_ah, *part_al, *part_h, *part_l;   // per-CTA pivot candidates
+  long long* part_idx;
+  int* part_nan;
+  unsigned* bar;                // grid barrier counter
+};
+
+int getrf_max_panel_ctas();
+cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStream_t s);
+cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
+                               cudaStream_t s);
+cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, cudaStream_t s);
+
 }  // namespace ddb
