@@ -132,6 +132,19 @@ int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int6
                    double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
                    int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream);
 
+/* LU with partial pivoting: mpkit.mplapack.Rgetrf (mplapack/lu.py:74-114),
+ * dd, in place (A = P L U, unit-lower L below the diagonal).  ipiv: host
+ * array of min(m, n) 1-based pivot rows; *info (host) = 0 or the first
+ * column with an exactly zero pivot (the factorization still completes).
+ * Blocked (width $DDB_GETRF_NB, default 64): cooperative panel kernel, row
+ * interchanges, unit-lower TRSM and an Rgemm trailing update in `mode`;
+ * exact mode is bit-identical to the reference.  Returns 0 / the reference
+ * argument index (1 m, 2 n, 4 lda) / DDB_E*.  Synchronises `stream`. */
+int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
+               int* info, int mode, void* stream);
+int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
+                    int* info, int mode, void* stream);
+
 /* Cholesky: mpkit.mplapack.Rpotrf (mplapack/chol.py:21-65), dd, in place.
  * uplo 'L': A = L L^T, 'U': A = U^T U; only that triangle is read / written.
  * Blocked right-looking, two levels: outer block width nb (<= 0 = default
@@ -153,6 +166,7 @@ int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k
                        int64_t lda, int64_t ldb, int64_t ldc);
 int ddb_rsyrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc);
 int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda);
+int ddb_rgetrf_validate(int64_t m, int64_t n, int64_t lda);
 int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
                        int64_t lda, int64_t ldb);
 

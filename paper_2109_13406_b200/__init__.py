@@ -6,17 +6,17 @@ compute runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI in
 """
 
 from .matrix import BlasError, DeviceMatrix, HostMatrix, to_dd
-from .lapack import Rpotrf
+from .lapack import PivotVector, Rgetrf, Rpotrf
 from .mpblas import Cgemm, Rgemm, Rsyrk, Rtrsm, default_mode
 
-__all__ = ["Rgemm", "Rsyrk", "Rtrsm", "Cgemm", "Rpotrf", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
+__all__ = ["Rgemm", "Rsyrk", "Rtrsm", "Cgemm", "Rpotrf", "Rgetrf", "PivotVector", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
            "default_mode", "flop_count"]
 
 
 def flop_count(routine, n, k=None, m=None):
     """dd flops as the reference bench counts them (mpkit/bench.py:51-70;
     m and k default to n): Rgemm 2mnk, Rsyrk n^2*k + n*k = n(n+1)k,
-    Rpotrf n^3/3."""
+    Rgetrf 2n^3/3, Rpotrf n^3/3."""
     m = n if m is None else m
     k = n if k is None else k
     if routine == "Rgemm":
@@ -25,4 +25,6 @@ def flop_count(routine, n, k=None, m=None):
         return float(n * n * k + n * k)
     if routine == "Rpotrf":
         return n ** 3 / 3.0
+    if routine == "Rgetrf":
+        return 2.0 * n ** 3 / 3.0
     raise ValueError(f"unknown routine {routine!r}")

@@ -27,7 +27,8 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_dgemm", "ddb_dsyrk", "ddb_dgemm_host", "ddb_dsyrk_host",
            "ddb_cgemm", "ddb_cgemm_host", "ddb_zgemm", "ddb_zgemm_host",
            "ddb_rpotrf", "ddb_rpotrf_host", "ddb_rpotrf_validate",
-           "ddb_rtrsm", "ddb_rtrsm_host", "ddb_rtrsm_validate")
+           "ddb_rtrsm", "ddb_rtrsm_host", "ddb_rtrsm_validate",
+           "ddb_rgetrf", "ddb_rgetrf_host", "ddb_rgetrf_validate")
 
 _lib = None
 
@@ -81,6 +82,14 @@ def load():
         f.argtypes = tr
     L.ddb_rtrsm_validate.restype = ctypes.c_int
     L.ddb_rtrsm_validate.argtypes = [_c, _c, _c, _c] + [_i64] * 4
+    lu = [_i64, _i64, _dp, _dp, _i64, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int),
+          ctypes.c_int, _dp]
+    for name in ("ddb_rgetrf", "ddb_rgetrf_host"):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = lu
+    L.ddb_rgetrf_validate.restype = ctypes.c_int
+    L.ddb_rgetrf_validate.argtypes = [_i64, _i64, _i64]
     L.ddb_rpotrf_validate.restype = ctypes.c_int
     L.ddb_rpotrf_validate.argtypes = [_c, _i64, _i64]
     L.ddb_rgemm_validate.restype = ctypes.c_int

@@ -724,6 +724,106 @@ int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int6
   return DDB_OK;
 }
 
+// ---- LU with partial pivoting (dd_getrf.cu) -----------------------------------
+
+int ddb_rgetrf_validate(int64_t m, int64_t n, int64_t lda) {
+  if (m < 0) return 1;                                // lu.py:83-85
+  if (n < 0) return 2;
+  if (lda < (m > 1 ? m : 1)) return 4;
+  return 0;
+}
+
+int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
+               int* info, int mode, void* stream) {
+  const int rc = ddb_rgetrf_validate(m, n, lda);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr ||
+      (ipiv == nullptr && m > 0 && n > 0)) {
+    g_last_error = info == nullptr || ipiv == nullptr ? "ipiv / info pointer is null" : "unknown mode";
+    return DDB_EINVAL;
+  }
+  *info = 0;
+  if (m == 0 || n == 0) return DDB_OK;                // lu.py:86-87
+  static const int64_t nb_env = [] {
+    const char* v = std::getenv("DDB_GETRF_NB");
+    return v ? (int64_t)std::atoll(v) : (int64_t)0;
+  }();
+  const int64_t nb = nb_env > 0 && nb_env <= 96 ? nb_env : 64;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
+  GetrfArgs g{};
+  g.m = m; g.n = n; g.mn = m < n ? m : n; g.lda = lda;
+  g.a_hi = a_hi; g.a_lo = a_lo;
+  const int G = getrf_max_panel_ctas();
+  // workspace: info, barrier | ipiv, swap (mn each) | G partial candidates
+  const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
+                          (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) + 64;
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
+  if (e != cudaSuccess) return fail(e, "rgetrf workspace");
+  char* w = static_cast<char*>(ws);
+  g.info = reinterpret_cast<int*>(w);
+  g.bar = reinterpret_cast<unsigned*>(w + 64);
+  g.ipiv = reinterpret_cast<long long*>(w + 256);
+  g.swap = g.ipiv + g.mn;
+  double* pd = reinterpret_cast<double*>(g.swap + g.mn);
+  g.part_ah = pd; g.part_al = pd + G; g.part_h = pd + 2 * G; g.part_l = pd + 3 * G;
+  g.part_idx = reinterpret_cast<long long*>(pd + 4 * G);
+  g.part_nan = reinterpret_cast<int*>(g.part_idx + G);
+  int nl = 0, rc2 = DDB_OK;
+  e = cudaMemsetAsync(ws, 0, 256, s);
+  for (int64_t j0 = 0; j0 < g.mn && e == cudaSuccess && rc2 == DDB_OK; j0 += nb) {
+    const int64_t j1 = j0 + nb < g.mn ? j0 + nb : g.mn;
+    e = launch_getrf_panel(g, j0, (int)(j1 - j0), s);
+    ++nl;
+    if (e == cudaSuccess) { e = launch_getrf_laswp(g, j0, j1, 0, j0, s); ++nl; }
+    if (e == cudaSuccess) { e = launch_getrf_laswp(g, j0, j1, j1, n, s); ++nl; }
+    if (e == cudaSuccess && j1 < n) { e = launch_getrf_trsm(g, j0, (int)(j1 - j0), j1, s); ++nl; }
+    if (e == cudaSuccess && j1 < m && j1 < n)        // A22 += L21 (-U12)  (lu.py:107-111)
+      rc2 = ddb_rgemm('N', 'N', m - j1, n - j1, j1 - j0, -1.0, 0.0, a_hi + j1 + j0 * lda,
+                      a_lo + j1 + j0 * lda, lda, a_hi + j0 + j1 * lda, a_lo + j0 + j1 * lda, lda,
+                      1.0, 0.0, a_hi + j1 + j1 * lda, a_lo + j1 + j1 * lda, lda, mode, stream);
+  }
+  g_launches += nl;
+  int hinfo = 0;
+  if (e == cudaSuccess && rc2 == DDB_OK) {
+    e = cudaMemcpyAsync(&hinfo, g.info, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ipiv, g.ipiv, sizeof(long long) * g.mn, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  }
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  if (rc2 != DDB_OK) return rc2;
+  if (e != cudaSuccess) return fail(e, "rgetrf");
+  if (e2 != cudaSuccess) return fail(e2, "workspace free");
+  *info = hinfo;
+  return DDB_OK;
+}
+
+int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
+                    int* info, int mode, void* stream) {
+  int rc = ddb_rgetrf_validate(m, n, lda);
+  if (rc) return rc;
+  if (info == nullptr) {
+    g_last_error = "info pointer is null";
+    return DDB_EINVAL;
+  }
+  *info = 0;
+  if (m == 0 || n == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t sa = span(m, n, lda);
+  DevBuf A;
+  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
+  rc = ddb_rgetrf(m, n, A.p, A.p + sa, lda, ipiv, info, mode, stream);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(a_hi, A.p, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(a_lo, A.p + sa, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
 // ---- blocked Cholesky (dd_potrf.cu) ----------------------------------------
 
 int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {

@@ -221,7 +221,8 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
         dd ap = piv;
         if (ap.h < 0.0 || (ap.h == 0.0 && ap.l < 0.0)) ap = neg_(ap);
         const double sh = 0x1p-969, sl = -0x0.0000000000006p-1022;
-        use_rec_s = ap.h > sh || (ap.h == sh && ap.l >= sl);
+        // _cmp2(ap, safmin) >= 0, NaN included (ddarith.py:166-176)
+        use_rec_s = !(ap.h < sh) && (ap.h > sh || !(ap.l < sl));
         if (nonzero_s && use_rec_s) rec_s = div2_scal(dd{1.0, 0.0}, piv);
         if (blockIdx.x == 0) {
           g.ipiv[j] = jp + 1;

@@ -1,4 +1,6 @@
-"""Drop-in ``Rpotrf`` (dd Cholesky) whose O(n^3) work runs as GPU ``Rsyrk``.
+"""Drop-in ``Rpotrf`` / ``Rgetrf`` (dd Cholesky, LU) on the B200.
+
+The O(n^3) work runs as GPU ``Rsyrk`` / ``Rgemm`` trailing updates.
 
 Same call surface, validation order, BlasError indices and return value as
 the reference (``/root/reference/pkg/src/mpkit/mplapack/chol.py:21-65``):
@@ -31,7 +33,71 @@ from . import _lib
 from .matrix import check_storage, require
 from .mpblas import _HostPlanes, _dev_ptr, _mode_code, _placement, _raise_rc
 
-__all__ = ["Rpotrf"]
+__all__ = ["Rpotrf", "Rgetrf", "PivotVector"]
+
+
+class PivotVector:
+    """1-based row interchange record (mplapack/lu.py:17-41): row k was
+    swapped with ipiv[k-1]."""
+
+    def __init__(self, ipiv=()):
+        self.ipiv = [int(p) for p in ipiv]
+
+    def __len__(self):
+        return len(self.ipiv)
+
+    def __getitem__(self, k):
+        return self.ipiv[k]
+
+    def __iter__(self):
+        return iter(self.ipiv)
+
+    def __eq__(self, other):
+        other = list(other) if not isinstance(other, PivotVector) else other.ipiv
+        return self.ipiv == other
+
+    def __repr__(self):
+        return f"PivotVector({self.ipiv})"
+
+
+def Rgetrf(m, n, a, lda=None, *, mode=None):
+    """A = P*L*U in place (mplapack/lu.py:74-114); returns (PivotVector, info).
+
+    info = k > 0 flags an exactly zero pivot U(k, k); the factorization still
+    completes.  mode "exact" / "reference": bit-identical to the reference;
+    "fast" / "twosum": the trailing updates in that mode (the pivot order can
+    then differ where two candidates agree to ~2**-100)."""
+    routine = "Rgetrf"
+    lda = a.ld if lda is None else lda
+    require(routine, m >= 0, 1)                                     # lu.py:83-85
+    require(routine, n >= 0, 2)
+    require(routine, lda >= max(1, m), 4)
+    if m == 0 or n == 0:                                            # lu.py:86-87
+        return PivotVector(), 0
+    if a.precision != "dd":
+        raise NotImplementedError(
+            f"{routine}: precision {a.precision!r} is not on the B200 path (only 'dd')")
+    code = _mode_code(mode)
+    check_storage(a, m, n, lda)
+    L = _lib.load()
+    mn = min(m, n)
+    ipiv = (ctypes.c_int64 * mn)()
+    info = ctypes.c_int(0)
+    dev = _placement(routine, a)
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_rgetrf(m, n, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, ipiv,
+                              ctypes.byref(info), code, stream)
+        _raise_rc(routine, rc)
+    else:
+        ha = _HostPlanes(a.store)
+        rc = L.ddb_rgetrf_host(m, n, ha.ptr(0), ha.ptr(1), lda, ipiv, ctypes.byref(info), code,
+                               None)
+        _raise_rc(routine, rc)
+        ha.commit()
+    return PivotVector(ipiv[:]), int(info.value)
 
 
 def Rpotrf(uplo, n, a, lda=None, *, mode=None, nb=0):

@@ -162,6 +162,7 @@ def test_flop_count_matches_reference_bench():
     assert flop_count("Rgemm", 3, k=5, m=2) == 60.0
     assert flop_count("Rsyrk", 4, k=3) == 60.0
     assert flop_count("Rpotrf", 3) == 9.0
+    assert flop_count("Rgetrf", 3) == 18.0
 
 
 def test_library_exports_every_header_symbol():
@@ -269,3 +270,29 @@ def test_rtrsm_early_exit_and_precision_gate():
         Rtrsm("L", "U", "N", "N", 3, 3, 1.0, c, 3, HostMatrix(3, 3, "f64"), 3)
     with pytest.raises(ValueError, match="mixed precisions"):
         Rtrsm("L", "U", "N", "N", 3, 3, 1.0, a, 3, c, 3)
+
+
+@pytest.mark.parametrize("args,idx", [((-1, 2, 2), 1), ((2, -1, 2), 2), ((3, 2, 2), 4),
+                                      ((0, 0, 0), 4)])
+def test_rgetrf_blas_error_indices(args, idx):
+    """mplapack/lu.py:82-85 (m, n, lda), and the C ABI's validate agrees."""
+    from paper_2109_13406_b200 import Rgetrf
+    m, n, lda = args
+    with pytest.raises(BlasError) as e:
+        Rgetrf(m, n, HostMatrix(4, 4), lda)
+    assert e.value.index == idx and e.value.routine == "Rgetrf"
+    try:
+        L = _lib.load()
+    except _lib.LibraryMissing:
+        return
+    assert L.ddb_rgetrf_validate(m, n, lda) == idx
+
+
+def test_rgetrf_early_exit_and_precision_gate():
+    from paper_2109_13406_b200 import PivotVector, Rgetrf
+    a = HostMatrix(3, 3)
+    ipiv, info = Rgetrf(0, 3, a, 3)
+    assert ipiv == [] and info == 0 and isinstance(ipiv, PivotVector)
+    assert Rgetrf(3, 0, a) == (PivotVector(), 0)
+    with pytest.raises(NotImplementedError):
+        Rgetrf(3, 3, HostMatrix(3, 3, "f64"))
