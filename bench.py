@@ -29,6 +29,7 @@ Printed keys beyond the driver contract:
 from __future__ import annotations
 
 import argparse
+import math
 import json
 import os
 import statistics
@@ -283,6 +284,8 @@ def run_ours(args):
             extra["f64"] = _f64(n, dev, stream)
             extra["cgemm"] = _cgemm(n // 2, dev, stream, mode)
             extra["rpotrf"] = _rpotrf(n, dev, stream, mode)
+            extra["rgetrf"] = _rgetrf(n, dev, stream, mode)
+            extra["rtrsm"] = _rtrsm(n, dev, stream, mode)
         cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, 16, 0)
         from oracle import oracle
         extra["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": oracle.max_threads(),
@@ -433,6 +436,53 @@ def _rpotrf(n, dev, stream, mode):
     return {"workload": f"dd Rpotrf L n={n} (SPD, diagonally dominant)",
             "value": flop_count("Rpotrf", n) / t / 1e9, "unit": UNIT, "ms": t * 1e3,
             "mode": mode, "info": max(infos)}
+
+
+def _rgetrf(n, dev, stream, mode):
+    """blocked dd LU with partial pivoting of a random n x n matrix; 2n^3/3
+    flops (mpkit/bench.py:66-67)."""
+    from paper_2109_13406_b200 import DeviceMatrix, Rgetrf, flop_count
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    h0, l0 = hashed_dd_device(n, n, 0, 1, dev)
+    A = DeviceMatrix(n, n, "dd", n, store=(h0.clone(), l0.clone()))
+    infos = []
+
+    def reset():
+        A.store[0].copy_(h0)
+        A.store[1].copy_(l0)
+
+    times = timed(lambda: infos.append(Rgetrf(n, n, A, n, mode=mode)[1]), 2, 1, stream, reset=reset)
+    t = min(times)
+    return {"workload": f"dd Rgetrf n={n} (random, partial pivoting)",
+            "value": flop_count("Rgetrf", n) / t / 1e9, "unit": UNIT, "ms": t * 1e3,
+            "mode": mode, "info": max(infos)}
+
+
+def _rtrsm(n, dev, stream, mode):
+    """dd Rtrsm L,L,N,N with an n x n lower-triangular A and n right-hand
+    sides; n^3 flops (n^2 n / 2 multiply-adds)."""
+    import torch
+    from paper_2109_13406_b200 import DeviceMatrix, Rtrsm
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    ah, al = hashed_dd_device(n, n, 0, 4, dev)
+    f = 2.0 ** -math.ceil(math.log2(n))      # off-diagonal row sums < 1 < diagonal
+    ah.mul_(f)
+    al.mul_(f)
+    ah.view(n, n).diagonal().add_(4.0)      # column-major: the diagonal either way
+    A = DeviceMatrix(n, n, "dd", n, store=(ah, al))
+    b0 = hashed_dd_device(n, n, 0, 5, dev)
+    B = DeviceMatrix(n, n, "dd", n, store=(b0[0].clone(), b0[1].clone()))
+
+    def reset():
+        B.store[0].copy_(b0[0])
+        B.store[1].copy_(b0[1])
+
+    times = timed(lambda: Rtrsm("L", "L", "N", "N", n, n, 1.5, A, n, B, n, mode=mode), 2, 1,
+                  stream, reset=reset)
+    t = min(times)
+    del torch
+    return {"workload": f"dd Rtrsm L,L,N,N m=n={n}", "value": 1.0 * n ** 3 / t / 1e9,
+            "unit": UNIT, "ms": t * 1e3, "mode": mode}
 
 
 def _modes(n, k, dev, stream, A, B, C, C0, mode):

@@ -757,7 +757,8 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   const int G = getrf_max_panel_ctas();
   // workspace: info, barrier | ipiv, swap (mn each) | G partial candidates
   const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
-                          (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) + 64;
+                          (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) + 64 +
+                          sizeof(double) * 4 * (size_t)nb + 64;
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "rgetrf workspace");
@@ -770,6 +771,8 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   g.part_ah = pd; g.part_al = pd + G; g.part_h = pd + 2 * G; g.part_l = pd + 3 * G;
   g.part_idx = reinterpret_cast<long long*>(pd + 4 * G);
   g.part_nan = reinterpret_cast<int*>(g.part_idx + G);
+  g.rowbuf = reinterpret_cast<double*>(
+      (reinterpret_cast<uintptr_t>(g.part_nan + G) + 63) & ~static_cast<uintptr_t>(63));
   int nl = 0, rc2 = DDB_OK;
   e = cudaMemsetAsync(ws, 0, 256, s);
   for (int64_t j0 = 0; j0 < g.mn && e == cudaSuccess && rc2 == DDB_OK; j0 += nb) {

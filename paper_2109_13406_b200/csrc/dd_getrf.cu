@@ -276,6 +276,158 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
   }
 }
 
+// Shared-memory panel: CTA c stages its rows [r0, r1) of the panel (all nb
+// columns) in shared memory for the whole factorization; only the pivot
+// row crosses CTAs (through g.rowbuf) -- per column: partial searches ->
+// barrier -> the owners of rows jp / j publish them -> barrier -> every CTA
+// scales and updates its own rows.  Falls back to the global-memory kernel
+// when a CTA's share would not fit (kSmemRowsMax rows).
+constexpr int kSmemRowsMax = 192;
+
+__global__ void __launch_bounds__(kPanelThreads)
+getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
+  extern __shared__ double sm[];
+  __shared__ PivKey best_s;
+  __shared__ dd rec_s;
+  __shared__ int use_rec_s, nonzero_s;
+  const int64_t r0 = j0 + (int64_t)blockIdx.x * chunk;
+  const int64_t r1 = r0 + chunk < g.m ? r0 + chunk : g.m;
+  const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
+  const int ch = (int)chunk;
+  double* xh = sm;                       // rows x nb, ld = chunk
+  double* xl = sm + (size_t)ch * nb;
+  double* ph = xl + (size_t)ch * nb;     // the pivot row (nb)
+  double* pl = ph + nb;
+  const int64_t lda = g.lda;
+  for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
+    const int r = t % nr, c = t / nr;
+    xh[r + c * ch] = g.a_hi[(r0 + r) + (j0 + c) * lda];
+    xl[r + c * ch] = g.a_lo[(r0 + r) + (j0 + c) * lda];
+  }
+  __syncthreads();
+  unsigned nbar = 0;
+  auto owner = [&](int64_t row) { return (int)((row - j0) / chunk); };
+  auto local_search = [&](int jj) {
+    const int64_t j = j0 + jj;
+    PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
+    const int rs = r0 > j ? 0 : (int)(j - r0);
+    for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) {
+      const double h = xh[r + jj * ch], l = xl[r + jj * ch];
+      PivKey y{fabs(h), h < 0.0 ? -l : l, h, l, (long long)(r0 + r), isnan(h) ? 1 : 0};
+      k = merge(k, y);
+    }
+    k = block_best(k);
+    if (threadIdx.x == 0) {
+      g.part_ah[blockIdx.x] = k.ah;
+      g.part_al[blockIdx.x] = k.al;
+      g.part_h[blockIdx.x] = k.h;
+      g.part_l[blockIdx.x] = k.l;
+      g.part_idx[blockIdx.x] = k.idx;
+      g.part_nan[blockIdx.x] = k.nan;
+    }
+  };
+  local_search(0);
+  double* pbh = g.rowbuf;                 // pivot row, then the displaced row j
+  double* pbl = g.rowbuf + nb;
+  double* sbh = g.rowbuf + 2 * nb;
+  double* sbl = g.rowbuf + 3 * nb;
+  for (int jj = 0; jj < nb; ++jj) {
+    const int64_t j = j0 + jj;
+    grid_barrier(g.bar, gridDim.x * ++nbar);
+    if (threadIdx.x < 32) {
+      PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
+      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
+        PivKey y{__ldcg(g.part_ah + c), __ldcg(g.part_al + c), __ldcg(g.part_h + c),
+                 __ldcg(g.part_l + c), __ldcg(g.part_idx + c), __ldcg(g.part_nan + c)};
+        k = merge(k, y);
+      }
+      for (int o = 16; o > 0; o >>= 1) k = merge(k, shfl_down(k, o));
+      if (threadIdx.x == 0) {
+        if (k.nan || k.idx < 0) {          // argmax_abs returns 0 -> the diagonal entry
+          k.idx = j;
+          k.nan = 1;
+        }
+        best_s = k;
+      }
+    }
+    __syncthreads();
+    const int64_t jp = best_s.idx;
+    // a NaN search keeps row j; otherwise the winner's value is the pivot
+    const bool swapped = !best_s.nan && !(best_s.h == 0.0 && best_s.l == 0.0) && jp != j;
+    const int64_t prow = swapped ? jp : j;          // the row that ends at position j
+    if (owner(prow) == (int)blockIdx.x)
+      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+        pbh[c] = xh[(prow - r0) + c * ch];
+        pbl[c] = xl[(prow - r0) + c * ch];
+      }
+    if (swapped && owner(j) == (int)blockIdx.x)
+      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+        sbh[c] = xh[(j - r0) + c * ch];
+        sbl[c] = xl[(j - r0) + c * ch];
+      }
+    grid_barrier(g.bar, gridDim.x * ++nbar);
+    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+      const double h = __ldcg(pbh + c), l = __ldcg(pbl + c);
+      ph[c] = h;
+      pl[c] = l;
+      if (owner(j) == (int)blockIdx.x) {
+        xh[(j - r0) + c * ch] = h;
+        xl[(j - r0) + c * ch] = l;
+      }
+      if (swapped && owner(jp) == (int)blockIdx.x) {
+        xh[(jp - r0) + c * ch] = __ldcg(sbh + c);
+        xl[(jp - r0) + c * ch] = __ldcg(sbl + c);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const dd piv{ph[jj], pl[jj]};
+      nonzero_s = !(piv.h == 0.0 && piv.l == 0.0);
+      dd ap = piv;
+      if (ap.h < 0.0 || (ap.h == 0.0 && ap.l < 0.0)) ap = neg_(ap);
+      const double sh = 0x1p-969, sl = -0x0.0000000000006p-1022;
+      use_rec_s = !(ap.h < sh) && (ap.h > sh || !(ap.l < sl));   // _cmp2 >= 0
+      if (nonzero_s && use_rec_s) rec_s = div2_scal(dd{1.0, 0.0}, piv);
+      if (blockIdx.x == 0) {
+        g.ipiv[j] = jp + 1;
+        g.swap[j] = swapped ? jp : j;
+        if (!nonzero_s && *g.info == 0) *g.info = (int)(j + 1);
+      }
+    }
+    __syncthreads();
+    const bool nonzero = nonzero_s;
+    const int rs = r0 > j + 1 ? 0 : (int)(j + 1 - r0);
+    if (nonzero) {
+      const bool use_rec = use_rec_s;
+      const dd rec = rec_s, piv{ph[jj], pl[jj]};
+      for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) {
+        const dd x{xh[r + jj * ch], xl[r + jj * ch]};
+        const dd y = use_rec ? mul2_chk(rec, x) : vdiv2(x, piv);
+        xh[r + jj * ch] = y.h;
+        xl[r + jj * ch] = y.l;
+      }
+    }
+    __syncthreads();
+    const int ncol = nb - jj - 1, nrow = nr - rs;
+    if (ncol > 0 && nrow > 0 && j < g.mn - 1) {
+      for (int t = threadIdx.x; t < ncol * nrow; t += blockDim.x) {
+        const int r = rs + t % nrow, c = jj + 1 + t / nrow;
+        const dd x{xh[r + jj * ch], xl[r + jj * ch]};
+        const dd rr = add2_chk(dd{xh[r + c * ch], xl[r + c * ch]}, mul2_chk(x, neg_(dd{ph[c], pl[c]})));
+        xh[r + c * ch] = rr.h;
+        xl[r + c * ch] = rr.l;
+      }
+    }
+    __syncthreads();
+    if (jj + 1 < nb) local_search(jj + 1);
+  }
+  for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
+    const int r = t % nr, c = t / nr;
+    g.a_hi[(r0 + r) + (j0 + c) * lda] = xh[r + c * ch];
+    g.a_lo[(r0 + r) + (j0 + c) * lda] = xl[r + c * ch];
+  }
+}
+
 // Apply the interchanges of steps [j0, j1) in order to columns [c0, c1).
 __global__ void __launch_bounds__(256)
 getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1) {
@@ -330,6 +482,9 @@ static int panel_grid(int64_t rows) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrf_panel_kernel, kPanelThreads, 0);
+    // the shared-memory variant at its largest share: also >= 1 CTA / SM
+    cudaFuncSetAttribute(getrf_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     cached_max = per > 0 ? sms : 1;                            // one CTA per SM
     cached_dev = dev;
   }
@@ -341,11 +496,32 @@ static int panel_grid(int64_t rows) {
 int getrf_max_panel_ctas() { return panel_grid(1LL << 40); }
 
 cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStream_t s) {
-  const int grid = panel_grid(g.m - j0);
+  const int64_t rows = g.m - j0;
+  int grid = panel_grid(rows);
   cudaError_t e = cudaMemsetAsync(g.bar, 0, sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   GetrfArgs ga = g;
   int nbv = nb;
+  int64_t chunk = (rows + grid - 1) / grid;
+  if (chunk < 32) {                       // >= 32 rows per CTA: fewer barrier arrivals
+    chunk = rows < 32 ? rows : 32;
+    grid = (int)((rows + chunk - 1) / chunk);
+  }
+  if (chunk <= kSmemRowsMax) {
+    const size_t smem = sizeof(double) * (2 * (size_t)chunk * nb + 2 * (size_t)nb);
+    static thread_local int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+      cudaFuncSetAttribute(getrf_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr_dev = dev;
+    }
+    void* args[] = {&ga, &j0, &nbv, &chunk};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(getrf_panel_smem_kernel),
+                                       dim3(grid), dim3(kPanelThreads), args, smem, s);
+  }
+  grid = panel_grid(rows);
   void* args[] = {&ga, &j0, &nbv};
   return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(getrf_panel_kernel), dim3(grid),
                                      dim3(kPanelThreads), args, 0, s);

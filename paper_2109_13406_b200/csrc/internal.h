@@ -146,6 +146,7 @@ struct GetrfArgs {
   long long* part_idx;
   int* part_nan;
   unsigned* bar;                // grid barrier counter
+  double* rowbuf;               // 4 x nb: the pivot row and the displaced row (hi, lo)
 };
 
 int getrf_max_panel_ctas();
