@@ -748,7 +748,9 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
     const char* v = std::getenv("DDB_GETRF_NB");
     return v ? (int64_t)std::atoll(v) : (int64_t)0;
   }();
-  const int64_t nb = nb_env > 0 && nb_env <= 96 ? nb_env : 64;
+  const int64_t nbo = nb_env > 0 ? nb_env : 256;          // outer width
+  const int64_t ib = nbo < 64 ? nbo : 64;                  // inner (panel kernel) width
+  const int64_t nb = ib;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   retain_pool_memory();
   GetrfArgs g{};
@@ -756,9 +758,10 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   g.a_hi = a_hi; g.a_lo = a_lo;
   const int G = getrf_max_panel_ctas();
   // workspace: info, barrier | ipiv, swap (mn each) | G partial candidates
+  // partial candidates and rows: two parities (getrf_panel_smem_kernel)
   const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
-                          (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) + 64 +
-                          sizeof(double) * 4 * (size_t)nb + 64;
+                          2 * (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) +
+                          64 + sizeof(double) * (4 * (size_t)G + 4) * (size_t)nb + 64;
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "rgetrf workspace");
@@ -768,25 +771,97 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   g.ipiv = reinterpret_cast<long long*>(w + 256);
   g.swap = g.ipiv + g.mn;
   double* pd = reinterpret_cast<double*>(g.swap + g.mn);
-  g.part_ah = pd; g.part_al = pd + G; g.part_h = pd + 2 * G; g.part_l = pd + 3 * G;
-  g.part_idx = reinterpret_cast<long long*>(pd + 4 * G);
-  g.part_nan = reinterpret_cast<int*>(g.part_idx + G);
+  g.part_ah = pd; g.part_al = pd + 2 * G; g.part_h = pd + 4 * G; g.part_l = pd + 6 * G;
+  g.part_idx = reinterpret_cast<long long*>(pd + 8 * G);
+  g.part_nan = reinterpret_cast<int*>(g.part_idx + 2 * G);
   g.rowbuf = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(g.part_nan + G) + 63) & ~static_cast<uintptr_t>(63));
+      (reinterpret_cast<uintptr_t>(g.part_nan + 2 * G) + 63) & ~static_cast<uintptr_t>(63));
   int nl = 0, rc2 = DDB_OK;
   e = cudaMemsetAsync(ws, 0, 256, s);
-  for (int64_t j0 = 0; j0 < g.mn && e == cudaSuccess && rc2 == DDB_OK; j0 += nb) {
-    const int64_t j1 = j0 + nb < g.mn ? j0 + nb : g.mn;
-    e = launch_getrf_panel(g, j0, (int)(j1 - j0), s);
+  // Two block levels (outer NB = the trailing GEMM's depth, inner ib <= 64 =
+  // the panel kernel's width) and a lookahead: the next outer panel and the
+  // update of its columns run on the high-priority stream `cs` while the
+  // rest of the trailing update runs on the caller's stream (same scheme and
+  // ordering argument as Rpotrf).
+  const int64_t NB = nbo;
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  if (e == cudaSuccess) e = potrf_panel_stream(&cs);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+  auto gemm = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t l0, int64_t l1,
+                  cudaStream_t st) -> int {   // A(r0:r1, c0:c1) += A(r0:r1, l0:l1) (-A(l0:l1, c0:c1))
+    if (r1 <= r0 || c1 <= c0 || l1 <= l0) return DDB_OK;
+    return ddb_rgemm('N', 'N', r1 - r0, c1 - c0, l1 - l0, -1.0, 0.0, a_hi + r0 + l0 * lda,
+                     a_lo + r0 + l0 * lda, lda, a_hi + l0 + c0 * lda, a_lo + l0 + c0 * lda, lda,
+                     1.0, 0.0, a_hi + r0 + c0 * lda, a_lo + r0 + c0 * lda, lda, mode,
+                     static_cast<void*>(st));
+  };
+  // block J's pending work on columns [c0, c1): interchanges, U12 (blocked
+  // by the inner width), trailing update of rows >= J1
+  auto apply_block = [&](int64_t J0, int64_t J1, int64_t c0, int64_t c1, cudaStream_t st) -> int {
+    if (c1 <= c0) return DDB_OK;
+    cudaError_t er = launch_getrf_laswp(g, J0, J1, c0, c1, st);
     ++nl;
-    if (e == cudaSuccess) { e = launch_getrf_laswp(g, j0, j1, 0, j0, s); ++nl; }
-    if (e == cudaSuccess) { e = launch_getrf_laswp(g, j0, j1, j1, n, s); ++nl; }
-    if (e == cudaSuccess && j1 < n) { e = launch_getrf_trsm(g, j0, (int)(j1 - j0), j1, s); ++nl; }
-    if (e == cudaSuccess && j1 < m && j1 < n)        // A22 += L21 (-U12)  (lu.py:107-111)
-      rc2 = ddb_rgemm('N', 'N', m - j1, n - j1, j1 - j0, -1.0, 0.0, a_hi + j1 + j0 * lda,
-                      a_lo + j1 + j0 * lda, lda, a_hi + j0 + j1 * lda, a_lo + j0 + j1 * lda, lda,
-                      1.0, 0.0, a_hi + j1 + j1 * lda, a_lo + j1 + j1 * lda, lda, mode, stream);
+    if (er != cudaSuccess) return fail(er, "rgetrf laswp");
+    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
+      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
+      if ((er = launch_getrf_trsm(g, i0, (int)(i1 - i0), c0, c1, st)) != cudaSuccess)
+        return fail(er, "rgetrf trsm");
+      ++nl;
+      const int r = gemm(i1, J1, c0, c1, i0, i1, st);
+      if (r != DDB_OK) return r;
+    }
+    return gemm(J1, m, c0, c1, J0, J1, st);
+  };
+  // factor the outer panel [J0, J1) (its columns only) on `cs`
+  auto factor_outer = [&](int64_t J0, int64_t J1) -> int {
+    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
+      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
+      cudaError_t er = launch_getrf_panel(g, i0, (int)(i1 - i0), cs);
+      ++nl;
+      if (er == cudaSuccess) { er = launch_getrf_laswp(g, i0, i1, J0, i0, cs); ++nl; }
+      if (er != cudaSuccess) return fail(er, "rgetrf panel");
+      if (i1 < J1) {
+        const int r = apply_block(i0, i1, i1, J1, cs);
+        if (r != DDB_OK) return r;
+      }
+    }
+    return DDB_OK;
+  };
+  if (e == cudaSuccess) e = cudaEventRecord(ev_a, s);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_a, 0);
+  if (e == cudaSuccess) rc2 = factor_outer(0, NB < g.mn ? NB : g.mn);
+  bool have_rest = false;
+  for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
+    const int64_t J1 = J0 + NB < g.mn ? J0 + NB : g.mn;
+    // interchanges of block J on the factored columns to its left
+    if ((e = launch_getrf_laswp(g, J0, J1, 0, J0, cs)) != cudaSuccess) break;
+    ++nl;
+    if (J1 >= n) break;
+    const int64_t J2 = J1 + NB < g.mn ? J1 + NB : (J1 < g.mn ? g.mn : n);
+    e = cudaEventRecord(ev_a, cs);                         // panel J done
+    if (e == cudaSuccess && have_rest) e = cudaStreamWaitEvent(cs, ev_b, 0);   // rest(J-1)
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
+    if (e != cudaSuccess) break;
+    if (J2 < n) {
+      rc2 = apply_block(J0, J1, J2, n, s);                 // rest(J)
+      if (rc2 != DDB_OK) break;
+      e = cudaEventRecord(ev_b, s);
+      have_rest = true;
+      if (e != cudaSuccess) break;
+    }
+    rc2 = apply_block(J0, J1, J1, J2, cs);                 // columns of block J+1
+    if (rc2 != DDB_OK || J1 >= g.mn) break;
+    rc2 = factor_outer(J1, J2 < g.mn ? J2 : g.mn);
   }
+  if (cs != nullptr) {
+    cudaError_t ej = cudaEventRecord(ev_a, cs);
+    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_a, 0);
+    if (e == cudaSuccess) e = ej;
+  }
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
   g_launches += nl;
   int hinfo = 0;
   if (e == cudaSuccess && rc2 == DDB_OK) {

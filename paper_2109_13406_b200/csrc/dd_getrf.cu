@@ -276,12 +276,14 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
   }
 }
 
-// Shared-memory panel: CTA c stages its rows [r0, r1) of the panel (all nb
-// columns) in shared memory for the whole factorization; only the pivot
-// row crosses CTAs (through g.rowbuf) -- per column: partial searches ->
-// barrier -> the owners of rows jp / j publish them -> barrier -> every CTA
-// scales and updates its own rows.  Falls back to the global-memory kernel
-// when a CTA's share would not fit (kSmemRowsMax rows).
+// Shared-memory panel, one grid barrier per column: CTA c stages its rows
+// [r0, r1) of the panel in shared memory for the whole factorization.  With
+// its partial pivot search each CTA publishes its candidate's whole panel row
+// (double-buffered by column parity), and the owner of row j publishes row j,
+// so after the single barrier every CTA has both rows of the interchange:
+// the winner's candidate row becomes row j, the old row j goes to row jp.
+// Falls back to the global-memory kernel when a CTA's share would not fit
+// (kSmemRowsMax rows).
 constexpr int kSmemRowsMax = 192;
 
 __global__ void __launch_bounds__(kPanelThreads)
@@ -290,6 +292,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   __shared__ PivKey best_s;
   __shared__ dd rec_s;
   __shared__ int use_rec_s, nonzero_s;
+  const int G = gridDim.x;
   const int64_t r0 = j0 + (int64_t)blockIdx.x * chunk;
   const int64_t r1 = r0 + chunk < g.m ? r0 + chunk : g.m;
   const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
@@ -305,9 +308,13 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     xl[r + c * ch] = g.a_lo[(r0 + r) + (j0 + c) * lda];
   }
   __syncthreads();
-  unsigned nbar = 0;
   auto owner = [&](int64_t row) { return (int)((row - j0) / chunk); };
-  auto local_search = [&](int jj) {
+  // global scratch, two parities: keys [2][G], candidate rows [2][G][2 nb],
+  // row j [2][2 nb]
+  auto cand = [&](int par, int c) { return g.rowbuf + ((size_t)par * G + c) * 2 * nb; };
+  auto jrow = [&](int par) { return g.rowbuf + (size_t)2 * G * 2 * nb + (size_t)par * 2 * nb; };
+  auto publish = [&](int jj) {        // search column jj, publish candidate (+ row j0+jj)
+    const int par = jj & 1;
     const int64_t j = j0 + jj;
     PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
     const int rs = r0 > j ? 0 : (int)(j - r0);
@@ -317,28 +324,43 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
       k = merge(k, y);
     }
     k = block_best(k);
+    const int slot = par * G + blockIdx.x;
     if (threadIdx.x == 0) {
-      g.part_ah[blockIdx.x] = k.ah;
-      g.part_al[blockIdx.x] = k.al;
-      g.part_h[blockIdx.x] = k.h;
-      g.part_l[blockIdx.x] = k.l;
-      g.part_idx[blockIdx.x] = k.idx;
-      g.part_nan[blockIdx.x] = k.nan;
+      g.part_ah[slot] = k.ah;
+      g.part_al[slot] = k.al;
+      g.part_h[slot] = k.h;
+      g.part_l[slot] = k.l;
+      g.part_idx[slot] = k.idx;
+      g.part_nan[slot] = k.nan;
+    }
+    if (k.idx >= 0) {
+      double* cr = cand(par, blockIdx.x);
+      const int rr = (int)(k.idx - r0);
+      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+        cr[c] = xh[rr + c * ch];
+        cr[nb + c] = xl[rr + c * ch];
+      }
+    }
+    if (owner(j) == (int)blockIdx.x) {
+      double* jr = jrow(par);
+      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+        jr[c] = xh[(j - r0) + c * ch];
+        jr[nb + c] = xl[(j - r0) + c * ch];
+      }
     }
   };
-  local_search(0);
-  double* pbh = g.rowbuf;                 // pivot row, then the displaced row j
-  double* pbl = g.rowbuf + nb;
-  double* sbh = g.rowbuf + 2 * nb;
-  double* sbl = g.rowbuf + 3 * nb;
+  publish(0);
+  unsigned nbar = 0;
   for (int jj = 0; jj < nb; ++jj) {
+    const int par = jj & 1;
     const int64_t j = j0 + jj;
-    grid_barrier(g.bar, gridDim.x * ++nbar);
+    grid_barrier(g.bar, G * ++nbar);
     if (threadIdx.x < 32) {
       PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
-      for (int c = threadIdx.x; c < (int)gridDim.x; c += 32) {
-        PivKey y{__ldcg(g.part_ah + c), __ldcg(g.part_al + c), __ldcg(g.part_h + c),
-                 __ldcg(g.part_l + c), __ldcg(g.part_idx + c), __ldcg(g.part_nan + c)};
+      for (int c = threadIdx.x; c < G; c += 32) {
+        const int slot = par * G + c;
+        PivKey y{__ldcg(g.part_ah + slot), __ldcg(g.part_al + slot), __ldcg(g.part_h + slot),
+                 __ldcg(g.part_l + slot), __ldcg(g.part_idx + slot), __ldcg(g.part_nan + slot)};
         k = merge(k, y);
       }
       for (int o = 16; o > 0; o >>= 1) k = merge(k, shfl_down(k, o));
@@ -354,20 +376,10 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     const int64_t jp = best_s.idx;
     // a NaN search keeps row j; otherwise the winner's value is the pivot
     const bool swapped = !best_s.nan && !(best_s.h == 0.0 && best_s.l == 0.0) && jp != j;
-    const int64_t prow = swapped ? jp : j;          // the row that ends at position j
-    if (owner(prow) == (int)blockIdx.x)
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-        pbh[c] = xh[(prow - r0) + c * ch];
-        pbl[c] = xl[(prow - r0) + c * ch];
-      }
-    if (swapped && owner(j) == (int)blockIdx.x)
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-        sbh[c] = xh[(j - r0) + c * ch];
-        sbl[c] = xl[(j - r0) + c * ch];
-      }
-    grid_barrier(g.bar, gridDim.x * ++nbar);
+    const double* src = swapped ? cand(par, owner(jp)) : jrow(par);
+    const double* jr = jrow(par);
     for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-      const double h = __ldcg(pbh + c), l = __ldcg(pbl + c);
+      const double h = __ldcg(src + c), l = __ldcg(src + nb + c);
       ph[c] = h;
       pl[c] = l;
       if (owner(j) == (int)blockIdx.x) {
@@ -375,8 +387,8 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
         xl[(j - r0) + c * ch] = l;
       }
       if (swapped && owner(jp) == (int)blockIdx.x) {
-        xh[(jp - r0) + c * ch] = __ldcg(sbh + c);
-        xl[(jp - r0) + c * ch] = __ldcg(sbl + c);
+        xh[(jp - r0) + c * ch] = __ldcg(jr + c);
+        xl[(jp - r0) + c * ch] = __ldcg(jr + nb + c);
       }
     }
     __syncthreads();
@@ -419,7 +431,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
       }
     }
     __syncthreads();
-    if (jj + 1 < nb) local_search(jj + 1);
+    if (jj + 1 < nb) publish(jj + 1);
   }
   for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
     const int r = t % nr, c = t / nr;
@@ -429,27 +441,70 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
 }
 
 // Apply the interchanges of steps [j0, j1) in order to columns [c0, c1).
+// The composed permutation of the touched rows (at most 2 (j1 - j0)) is
+// formed once per CTA in shared memory; each column is then one gather and
+// one scatter with independent loads.
+constexpr int kSwapMax = 128;    // touched rows of <= 64 steps (launch_getrf_laswp chunks)
+
 __global__ void __launch_bounds__(256)
 getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1) {
-  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= c1) return;
-  double* ah = g.a_hi + c * g.lda;
-  double* al = g.a_lo + c * g.lda;
-  for (int64_t j = j0; j < j1; ++j) {
-    const int64_t p = g.swap[j];
-    if (p == j) continue;
-    const double th = ah[j], tl = al[j];
-    ah[j] = ah[p];
-    al[j] = al[p];
-    ah[p] = th;
-    al[p] = tl;
+  __shared__ long long rows_s[kSwapMax];   // touched rows
+  __shared__ int src_s[kSwapMax];          // final content of rows_s[t] = old rows_s[src_s[t]]
+  __shared__ int nt_s;
+  if (threadIdx.x < 32) {                  // warp 0 composes the interchanges
+    const int lane = threadIdx.x;
+    int nt = 0;
+    auto find = [&](long long r) {          // index of row r in rows_s, appended if new
+      for (int base = 0; base < nt; base += 32) {
+        const int t = base + lane;
+        const unsigned hit = __ballot_sync(0xffffffffu, t < nt && rows_s[t] == r);
+        if (hit) return base + __ffs(hit) - 1;
+      }
+      if (lane == 0) {
+        rows_s[nt] = r;
+        src_s[nt] = nt;
+      }
+      __syncwarp();
+      return nt++;
+    };
+    for (int64_t j = j0; j < j1; ++j) {
+      const long long p = g.swap[j];
+      if (p == j) continue;
+      const int a = find(j), b = find(p);
+      if (lane == 0) {
+        const int t = src_s[a];
+        src_s[a] = src_s[b];
+        src_s[b] = t;
+      }
+      __syncwarp();
+    }
+    if (lane == 0) nt_s = nt;
+  }
+  __syncthreads();
+  const int nt = nt_s;
+  if (nt == 0) return;
+  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double* ah = g.a_hi + c * g.lda;
+    double* al = g.a_lo + c * g.lda;
+    double gh[kSwapMax], gl[kSwapMax];   // gather everything, then scatter
+    for (int t = 0; t < nt; ++t) {
+      gh[t] = ah[rows_s[src_s[t]]];
+      gl[t] = al[rows_s[src_s[t]]];
+    }
+    for (int t = 0; t < nt; ++t) {
+      ah[rows_s[t]] = gh[t];
+      al[rows_s[t]] = gl[t];
+    }
   }
 }
 
-// U12 = L11^-1 A12 for columns [c0, n): per column, rows r in [j0, j1):
-// a(r, c) += mul2(L(r, l), -U(l, c)) for l = j0 .. r-1 in order.
-__global__ void __launch_bounds__(128)
-getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0) {
+// U12 = L11^-1 A12 for columns [c0, c1): one warp per column, lane t holding
+// rows t and t + 32 of the block.  Step l: the owner finalises U(l, c) and
+// broadcasts it; every later row r gets a(r, c) += mul2(L(r, l), -U(l, c)) --
+// per element the reference's order (l ascending).
+__global__ void __launch_bounds__(256)
+getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0, int64_t c1) {
   extern __shared__ double sm[];
   double* lh = sm;
   double* ll = sm + nb * nb;
@@ -461,17 +516,26 @@ getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0) {
     }
   }
   __syncthreads();
-  const int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= g.n) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = c0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (c >= c1) return;                       // whole warps
   double* uh = g.a_hi + j0 + c * g.lda;
   double* ul = g.a_lo + j0 + c * g.lda;
-  for (int r = 1; r < nb; ++r) {
-    dd acc{uh[r], ul[r]};
-    for (int l = 0; l < r; ++l)
-      acc = add2_chk(acc, mul2_chk(dd{lh[r + l * nb], ll[r + l * nb]}, neg_(dd{uh[l], ul[l]})));
-    uh[r] = acc.h;
-    ul[r] = acc.l;
+  const int ra = lane, rb = lane + 32;
+  dd acc_a{0.0, 0.0}, acc_b{0.0, 0.0};
+  if (ra < nb) acc_a = dd{uh[ra], ul[ra]};
+  if (rb < nb) acc_b = dd{uh[rb], ul[rb]};
+  for (int l = 0; l < nb - 1; ++l) {
+    const dd own = l < 32 ? acc_a : acc_b;   // U(l, c) is final once its turn comes
+    dd u;
+    u.h = __shfl_sync(0xffffffffu, own.h, l & 31);
+    u.l = __shfl_sync(0xffffffffu, own.l, l & 31);
+    const dd nu = neg_(u);
+    if (ra > l && ra < nb) acc_a = add2_chk(acc_a, mul2_chk(dd{lh[ra + l * nb], ll[ra + l * nb]}, nu));
+    if (rb > l && rb < nb) acc_b = add2_chk(acc_b, mul2_chk(dd{lh[rb + l * nb], ll[rb + l * nb]}, nu));
   }
+  if (ra < nb) { uh[ra] = acc_a.h; ul[ra] = acc_a.l; }
+  if (rb < nb) { uh[rb] = acc_b.h; ul[rb] = acc_b.l; }
 }
 
 static int panel_grid(int64_t rows) {
@@ -530,12 +594,20 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
                                cudaStream_t s) {
   if (c1 <= c0) return cudaSuccess;
-  getrf_laswp_kernel<<<(unsigned)((c1 - c0 + 255) / 256), 256, 0, s>>>(g, j0, j1, c0, c1);
-  return cudaGetLastError();
+  int64_t grid = (c1 - c0 + 255) / 256;
+  if (grid > 148 * 8) grid = 148 * 8;
+  for (int64_t a = j0; a < j1; a += kSwapMax / 2) {      // <= 64 steps per launch, in order
+    const int64_t b = a + kSwapMax / 2 < j1 ? a + kSwapMax / 2 : j1;
+    getrf_laswp_kernel<<<(unsigned)grid, 256, 0, s>>>(g, a, b, c0, c1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
-cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, cudaStream_t s) {
-  if (g.n <= c0 || nb <= 1) return cudaSuccess;
+cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
+                              cudaStream_t s) {
+  if (c1 <= c0 || nb <= 1) return cudaSuccess;
   const size_t smem = 2 * sizeof(double) * (size_t)nb * nb;
   static thread_local int attr_dev = -1;
   int dev = 0;
@@ -544,7 +616,7 @@ cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0
     cudaFuncSetAttribute(getrf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_dev = dev;
   }
-  getrf_trsm_kernel<<<(unsigned)((g.n - c0 + 127) / 128), 128, smem, s>>>(g, j0, nb, c0);
+  getrf_trsm_kernel<<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, s>>>(g, j0, nb, c0, c1);
   return cudaGetLastError();
 }
 

@@ -146,13 +146,14 @@ struct GetrfArgs {
   long long* part_idx;
   int* part_nan;
   unsigned* bar;                // grid barrier counter
-  double* rowbuf;               // 4 x nb: the pivot row and the displaced row (hi, lo)
+  double* rowbuf;               // candidate rows and row j, two parities (dd_getrf.cu)
 };
 
 int getrf_max_panel_ctas();
 cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStream_t s);
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
                                cudaStream_t s);
-cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, cudaStream_t s);
+cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
+                              cudaStream_t s);
 
 }  // namespace ddb
