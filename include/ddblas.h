@@ -145,6 +145,19 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
 int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
                     int* info, int mode, void* stream);
 
+/* Solve with an LU factorization: mpkit.mplapack.Rgetrs (lu.py:117-145):
+ * op(A) X = B in place in B (n x nrhs), A and ipiv (host, n 1-based pivots)
+ * from ddb_rgetrf.  trans 'N': interchanges, then Rtrsm L,L,N,U and
+ * L,U,N,N; 'T' / 'C': Rtrsm L,U,T,N and L,L,T,U, then the interchanges in
+ * reverse.  Bit-identical to the reference in exact mode.  Returns 0 / the
+ * reference argument index (1 trans, 2 n, 3 nrhs, 5 lda, 8 ldb) / DDB_E*. */
+int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
+               int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
+               int mode, void* stream);
+int ddb_rgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
+                    int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
+                    int mode, void* stream);
+
 /* Cholesky: mpkit.mplapack.Rpotrf (mplapack/chol.py:21-65), dd, in place.
  * uplo 'L': A = L L^T, 'U': A = U^T U; only that triangle is read / written.
  * Blocked right-looking, two levels: outer block width nb (<= 0 = default
@@ -167,6 +180,7 @@ int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k
 int ddb_rsyrk_validate(char uplo, char trans, int64_t n, int64_t k, int64_t lda, int64_t ldc);
 int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda);
 int ddb_rgetrf_validate(int64_t m, int64_t n, int64_t lda);
+int ddb_rgetrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_t ldb);
 int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
                        int64_t lda, int64_t ldb);
 

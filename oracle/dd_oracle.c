@@ -881,3 +881,46 @@ int oracle_rgetrf(int64_t m, int64_t n, double *Ah, double *Al, int64_t lda, int
     free(coll);
     return 0;
 }
+
+/* Rgetrs (mplapack/lu.py:117-145): laswp (lu.py:61-65) + two Rtrsm calls.
+ * ipiv: 1-based pivot rows as Rgetrf returns them. */
+int oracle_getrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_t ldb) {
+    int t = upflag(trans);
+    if (t != 'N' && t != 'T' && t != 'C') return 1;
+    if (n < 0) return 2;
+    if (nrhs < 0) return 3;
+    if (lda < (n > 1 ? n : 1)) return 5;
+    if (ldb < (n > 1 ? n : 1)) return 8;
+    return 0;
+}
+
+static void laswp_dd(double *Bh, double *Bl, int64_t ldb, int64_t ncol, const int64_t *ipiv,
+                     int64_t np, int forward) {
+    for (int64_t s = 0; s < np; ++s) {
+        int64_t k = forward ? s : np - 1 - s, p = ipiv[k] - 1;
+        if (p == k) continue;
+        for (int64_t c = 0; c < ncol; ++c) {
+            double th = Bh[k + c * ldb], tl = Bl[k + c * ldb];
+            Bh[k + c * ldb] = Bh[p + c * ldb]; Bl[k + c * ldb] = Bl[p + c * ldb];
+            Bh[p + c * ldb] = th; Bl[p + c * ldb] = tl;
+        }
+    }
+}
+
+int oracle_rgetrs(char trans, int64_t n, int64_t nrhs, const double *Ah, const double *Al,
+                  int64_t lda, const int64_t *ipiv, int64_t nipiv, double *Bh, double *Bl,
+                  int64_t ldb) {
+    int rc = oracle_getrs_validate(trans, n, nrhs, lda, ldb);
+    if (rc) return rc;
+    if (n == 0 || nrhs == 0) return 0;
+    if (upflag(trans) == 'N') {
+        laswp_dd(Bh, Bl, ldb, nrhs, ipiv, nipiv, 1);
+        oracle_rtrsm('L', 'L', 'N', 'U', n, nrhs, 1.0, 0.0, Ah, Al, lda, Bh, Bl, ldb);
+        oracle_rtrsm('L', 'U', 'N', 'N', n, nrhs, 1.0, 0.0, Ah, Al, lda, Bh, Bl, ldb);
+    } else {
+        oracle_rtrsm('L', 'U', 'T', 'N', n, nrhs, 1.0, 0.0, Ah, Al, lda, Bh, Bl, ldb);
+        oracle_rtrsm('L', 'L', 'T', 'U', n, nrhs, 1.0, 0.0, Ah, Al, lda, Bh, Bl, ldb);
+        laswp_dd(Bh, Bl, ldb, nrhs, ipiv, nipiv, 0);
+    }
+    return 0;
+}

@@ -360,7 +360,45 @@ def run_case_getrf(case, store):
     store["cases"].append(case)
 
 
+def getrs_cases():
+    """Rgetrs (mplapack/lu.py:117-145) on an Rgetrf factorization: both
+    transposes, one and several right-hand sides, padded lds."""
+    cases = []
+    seed = 2100
+    for trans in ("N", "T", "C", "n"):
+        for n, nrhs, pad in ((1, 1, (0, 0)), (7, 3, (1, 2)), (33, 5, (0, 1)), (70, 2, (2, 0))):
+            if trans in "Cn" and n > 7:
+                continue
+            cases.append(dict(routine="Rgetrs", trans=trans, n=n, nrhs=nrhs, pad=pad, seed=seed))
+            seed += 1
+    cases.append(dict(routine="Rgetrs", trans="N", n=5, nrhs=0, pad=(0, 0), seed=seed))
+    return cases
+
+
+def run_case_getrs(case, store):
+    sys.path.insert(0, REF)
+    import mpkit.mpblas as mb
+    from mpkit.mplapack import Rgetrf, Rgetrs
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    n, nrhs = case["n"], case["nrhs"]
+    a = _matrix(mb, n, n, lds["lda"], (arrays["A_hi"], arrays["A_lo"]))
+    b = _matrix(mb, n, max(nrhs, 1), lds["ldb"], (arrays["B_hi"], arrays["B_lo"]))
+    with np.errstate(all="ignore"):
+        ipiv, info = Rgetrf(n, n, a, lds["lda"])
+        Rgetrs(case["trans"], n, nrhs, a, lds["lda"], ipiv, b, lds["ldb"])
+    case["ipiv"] = [int(p) for p in ipiv]
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    store["arrays"][f"c{cid}_out_hi"] = np.asarray(b.store[0], dtype=np.float64)
+    store["arrays"][f"c{cid}_out_lo"] = np.asarray(b.store[1], dtype=np.float64)
+    store["cases"].append(case)
+
+
 def run_case(mb, DDouble, case, store):
+    if case["routine"] == "Rgetrs":
+        return run_case_getrs(case, store)
     if case["routine"] == "Rtrsm":
         return run_case_trsm(case, store)
     if case["routine"] == "Rgetrf":
@@ -483,7 +521,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     store = {"cases": [], "arrays": {}}
     for case in (gemm_cases() + syrk_cases() + f64_cases() + complex_cases() + potrf_cases()
-                 + trsm_cases() + getrf_cases()):
+                 + trsm_cases() + getrf_cases() + getrs_cases()):
         run_case(mb, DDouble, case, store)
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
     with open(os.path.join(OUT, "cases.json"), "w") as f:

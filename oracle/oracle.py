@@ -85,6 +85,11 @@ def lib():
                                     ctypes.POINTER(ctypes.c_int64)]
         L.oracle_getrf_validate.restype = ctypes.c_int
         L.oracle_getrf_validate.argtypes = [_i64, _i64, _i64]
+        L.oracle_rgetrs.restype = ctypes.c_int
+        L.oracle_rgetrs.argtypes = [ctypes.c_char, _i64, _i64, _dp, _dp, _i64,
+                                    ctypes.POINTER(ctypes.c_int64), _i64, _dp, _dp, _i64]
+        L.oracle_getrs_validate.restype = ctypes.c_int
+        L.oracle_getrs_validate.argtypes = [ctypes.c_char] + [_i64] * 4
         L.oracle_div2.restype = None
         L.oracle_div2.argtypes = [ctypes.c_double] * 4 + [_dp]
         L.oracle_sqrt2.restype = None
@@ -193,6 +198,13 @@ def rgetrf(m, n, a_hi, a_lo, lda):
     info = ctypes.c_int64(0)
     rc = lib().oracle_rgetrf(m, n, _ptr(a_hi), _ptr(a_lo), lda, ipiv, ctypes.byref(info))
     return rc, [int(ipiv[i]) for i in range(mn)], int(info.value)
+
+
+def rgetrs(trans, n, nrhs, a_hi, a_lo, lda, ipiv, b_hi, b_lo, ldb):
+    """In-place solve with an Rgetrf factorization (mplapack/lu.py:117-145)."""
+    arr = (ctypes.c_int64 * max(1, len(ipiv)))(*ipiv)
+    return lib().oracle_rgetrs(_flag(trans), n, nrhs, _ptr(a_hi), _ptr(a_lo), lda, arr, len(ipiv),
+                               _ptr(b_hi), _ptr(b_lo), ldb)
 
 
 def div2(x, y):

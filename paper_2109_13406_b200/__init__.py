@@ -6,10 +6,10 @@ compute runs in hand-written sm_100a kernels (``csrc/``) behind the C ABI in
 """
 
 from .matrix import BlasError, DeviceMatrix, HostMatrix, to_dd
-from .lapack import PivotVector, Rgetrf, Rpotrf
+from .lapack import PivotVector, Rgetrf, Rgetrs, Rpotrf
 from .mpblas import Cgemm, Rgemm, Rsyrk, Rtrsm, default_mode
 
-__all__ = ["Rgemm", "Rsyrk", "Rtrsm", "Cgemm", "Rpotrf", "Rgetrf", "PivotVector", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
+__all__ = ["Rgemm", "Rsyrk", "Rtrsm", "Cgemm", "Rpotrf", "Rgetrf", "Rgetrs", "PivotVector", "BlasError", "DeviceMatrix", "HostMatrix", "to_dd",
            "default_mode", "flop_count"]
 
 

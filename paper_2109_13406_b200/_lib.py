@@ -28,7 +28,8 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_cgemm", "ddb_cgemm_host", "ddb_zgemm", "ddb_zgemm_host",
            "ddb_rpotrf", "ddb_rpotrf_host", "ddb_rpotrf_validate",
            "ddb_rtrsm", "ddb_rtrsm_host", "ddb_rtrsm_validate",
-           "ddb_rgetrf", "ddb_rgetrf_host", "ddb_rgetrf_validate")
+           "ddb_rgetrf", "ddb_rgetrf_host", "ddb_rgetrf_validate",
+           "ddb_rgetrs", "ddb_rgetrs_host", "ddb_rgetrs_validate")
 
 _lib = None
 
@@ -88,6 +89,14 @@ def load():
         f = getattr(L, name)
         f.restype = ctypes.c_int
         f.argtypes = lu
+    rs = [_c, _i64, _i64, _dp, _dp, _i64, ctypes.POINTER(ctypes.c_int64), _dp, _dp, _i64,
+          ctypes.c_int, _dp]
+    for name in ("ddb_rgetrs", "ddb_rgetrs_host"):
+        f = getattr(L, name)
+        f.restype = ctypes.c_int
+        f.argtypes = rs
+    L.ddb_rgetrs_validate.restype = ctypes.c_int
+    L.ddb_rgetrs_validate.argtypes = [_c] + [_i64] * 4
     L.ddb_rgetrf_validate.restype = ctypes.c_int
     L.ddb_rgetrf_validate.argtypes = [_i64, _i64, _i64]
     L.ddb_rpotrf_validate.restype = ctypes.c_int

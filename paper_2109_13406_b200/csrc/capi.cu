@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/ddblas.h"
 #include "internal.h"
@@ -897,6 +898,82 @@ int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t ld
   cudaError_t e = cudaMemcpyAsync(a_hi, A.p, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(a_lo, A.p + sa, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(e, "device to host copy");
+  return DDB_OK;
+}
+
+int ddb_rgetrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_t ldb) {
+  const int t = upflag(trans);
+  if (t != 'N' && t != 'T' && t != 'C') return 1;     // lu.py:123-125
+  if (n < 0) return 2;
+  if (nrhs < 0) return 3;
+  if (lda < (n > 1 ? n : 1)) return 5;
+  if (ldb < (n > 1 ? n : 1)) return 8;
+  return 0;
+}
+
+int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
+               int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
+               int mode, void* stream) {
+  const int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
+  if (rc) return rc;
+  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || (ipiv == nullptr && n > 0)) {
+    g_last_error = ipiv == nullptr ? "ipiv pointer is null" : "unknown mode";
+    return DDB_EINVAL;
+  }
+  if (n == 0 || nrhs == 0) return DDB_OK;             // lu.py:130-131
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  retain_pool_memory();
+  // laswp (lu.py:61-65) with the recorded pivots, as row interchanges of B
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, sizeof(long long) * (size_t)n, s);
+  if (e != cudaSuccess) return fail(e, "rgetrs workspace");
+  std::vector<long long> sw((size_t)n);
+  for (int64_t k = 0; k < n; ++k) sw[(size_t)k] = ipiv[k] - 1;
+  e = cudaMemcpyAsync(ws, sw.data(), sizeof(long long) * (size_t)n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // sw is a host temporary
+  GetrfArgs g{};
+  g.m = n; g.n = nrhs; g.mn = n; g.lda = ldb;
+  g.a_hi = b_hi; g.a_lo = b_lo;
+  g.swap = static_cast<long long*>(ws);
+  int r = DDB_OK;
+  const bool notr = upflag(trans) == 'N';
+  if (e == cudaSuccess && notr) {
+    e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 0);
+    if (e == cudaSuccess)
+      r = ddb_rtrsm('L', 'L', 'N', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+    if (e == cudaSuccess && r == DDB_OK)
+      r = ddb_rtrsm('L', 'U', 'N', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+  } else if (e == cudaSuccess) {
+    r = ddb_rtrsm('L', 'U', 'T', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+    if (r == DDB_OK)
+      r = ddb_rtrsm('L', 'L', 'T', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+    if (r == DDB_OK) e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 1);
+  }
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  if (r != DDB_OK) return r;
+  if (e != cudaSuccess) return fail(e, "rgetrs");
+  if (e2 != cudaSuccess) return fail(e2, "workspace free");
+  return DDB_OK;
+}
+
+int ddb_rgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
+                    int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
+                    int mode, void* stream) {
+  int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
+  if (rc) return rc;
+  if (n == 0 || nrhs == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t sa = span(n, n, lda), sb = span(n, nrhs, ldb);
+  DevBuf A, B;
+  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
+  if ((rc = stage_in(B, b_hi, b_lo, sb, s))) return rc;
+  rc = ddb_rgetrs(trans, n, nrhs, A.p, A.p + sa, lda, ipiv, B.p, B.p + sb, ldb, mode, stream);
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpyAsync(b_hi, B.p, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(b_lo, B.p + sb, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return fail(e, "device to host copy");
   return DDB_OK;

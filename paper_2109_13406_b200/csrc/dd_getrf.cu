@@ -447,7 +447,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
 constexpr int kSwapMax = 128;    // touched rows of <= 64 steps (launch_getrf_laswp chunks)
 
 __global__ void __launch_bounds__(256)
-getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1) {
+getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1, int reverse) {
   __shared__ long long rows_s[kSwapMax];   // touched rows
   __shared__ int src_s[kSwapMax];          // final content of rows_s[t] = old rows_s[src_s[t]]
   __shared__ int nt_s;
@@ -467,7 +467,8 @@ getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1) 
       __syncwarp();
       return nt++;
     };
-    for (int64_t j = j0; j < j1; ++j) {
+    for (int64_t s = j0; s < j1; ++s) {
+      const int64_t j = reverse ? j0 + j1 - 1 - s : s;
       const long long p = g.swap[j];
       if (p == j) continue;
       const int a = find(j), b = find(p);
@@ -592,13 +593,18 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
 }
 
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
-                               cudaStream_t s) {
+                               cudaStream_t s, int reverse) {
   if (c1 <= c0) return cudaSuccess;
   int64_t grid = (c1 - c0 + 255) / 256;
   if (grid > 148 * 8) grid = 148 * 8;
-  for (int64_t a = j0; a < j1; a += kSwapMax / 2) {      // <= 64 steps per launch, in order
-    const int64_t b = a + kSwapMax / 2 < j1 ? a + kSwapMax / 2 : j1;
-    getrf_laswp_kernel<<<(unsigned)grid, 256, 0, s>>>(g, a, b, c0, c1);
+  const int64_t step = kSwapMax / 2;                     // <= 64 steps per launch, in order
+  for (int64_t t = j0; t < j1; t += step) {
+    int64_t a = t, b = t + step < j1 ? t + step : j1;
+    if (reverse) {                                       // chunks from the end
+      b = j1 - (t - j0);
+      a = b - step > j0 ? b - step : j0;
+    }
+    getrf_laswp_kernel<<<(unsigned)grid, 256, 0, s>>>(g, a, b, c0, c1, reverse);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

@@ -152,7 +152,7 @@ struct GetrfArgs {
 int getrf_max_panel_ctas();
 cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStream_t s);
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
-                               cudaStream_t s);
+                               cudaStream_t s, int reverse = 0);
 cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
                               cudaStream_t s);
 

@@ -33,7 +33,7 @@ from . import _lib
 from .matrix import check_storage, require
 from .mpblas import _HostPlanes, _dev_ptr, _mode_code, _placement, _raise_rc
 
-__all__ = ["Rpotrf", "Rgetrf", "PivotVector"]
+__all__ = ["Rpotrf", "Rgetrf", "Rgetrs", "PivotVector"]
 
 
 class PivotVector:
@@ -132,3 +132,41 @@ def Rpotrf(uplo, n, a, lda=None, *, mode=None, nb=0):
     _raise_rc(routine, rc)
     ha.commit()
     return int(info.value)
+
+
+def Rgetrs(trans, n, nrhs, a, lda=None, ipiv=None, b=None, ldb=None, *, mode=None):
+    """Solve op(A)*X = B in place in B from an Rgetrf factorization
+    (mplapack/lu.py:117-145); returns 0.  mode as for Rtrsm."""
+    routine = "Rgetrs"
+    lda = a.ld if lda is None else lda
+    ldb = b.ld if (b is not None and ldb is None) else ldb
+    ok = isinstance(trans, str) and trans.upper() in ("N", "T", "C")   # lu.py:123-125
+    require(routine, ok, 1)
+    trans = trans.upper()
+    require(routine, n >= 0, 2)
+    require(routine, nrhs >= 0, 3)
+    require(routine, lda >= max(1, n), 5)
+    require(routine, ldb is not None and ldb >= max(1, n), 8)
+    if n == 0 or nrhs == 0:                                         # lu.py:130-131
+        return 0
+    if a.precision != "dd" or b.precision != "dd":
+        raise NotImplementedError(f"{routine}: only 'dd' is on the B200 path")
+    code = _mode_code(mode)
+    check_storage(b, n, nrhs, ldb)
+    piv = (ctypes.c_int64 * n)(*[int(p) for p in list(ipiv)[:n]])
+    L = _lib.load()
+    dev = _placement(routine, a, b)
+    if dev is not None:
+        import torch
+        with torch.cuda.device(dev):
+            stream = torch.cuda.current_stream(dev).cuda_stream
+            rc = L.ddb_rgetrs(trans.encode(), n, nrhs, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, piv,
+                              _dev_ptr(b, 0), _dev_ptr(b, 1), ldb, code, stream)
+        _raise_rc(routine, rc)
+        return 0
+    ha, hb = _HostPlanes(a.store), _HostPlanes(b.store)
+    rc = L.ddb_rgetrs_host(trans.encode(), n, nrhs, ha.ptr(0), ha.ptr(1), lda, piv, hb.ptr(0),
+                           hb.ptr(1), ldb, code, None)
+    _raise_rc(routine, rc)
+    hb.commit()
+    return 0

@@ -296,3 +296,32 @@ def test_rgetrf_early_exit_and_precision_gate():
     assert Rgetrf(3, 0, a) == (PivotVector(), 0)
     with pytest.raises(NotImplementedError):
         Rgetrf(3, 3, HostMatrix(3, 3, "f64"))
+
+
+@pytest.mark.parametrize("args,lds,idx", [(("X", 2, 1), {}, 1), (("N", -1, 1), {}, 2),
+                                          (("N", 2, -1), {}, 3), (("N", 3, 1), {"lda": 2}, 5),
+                                          (("T", 3, 1), {"ldb": 2}, 8)])
+def test_rgetrs_blas_error_indices(args, lds, idx):
+    """mplapack/lu.py:117-129, and the C ABI's validate agrees."""
+    from paper_2109_13406_b200 import Rgetrs
+    tr, n, nrhs = args
+    with pytest.raises(BlasError) as e:
+        Rgetrs(tr, n, nrhs, HostMatrix(4, 4), lds.get("lda", 4), [1, 2, 3, 4], HostMatrix(4, 4),
+               lds.get("ldb", 4))
+    assert e.value.index == idx and e.value.routine == "Rgetrs"
+    try:
+        L = _lib.load()
+    except _lib.LibraryMissing:
+        return
+    assert L.ddb_rgetrs_validate(tr.encode(), n, nrhs, lds.get("lda", 4), lds.get("ldb", 4)) == idx
+
+
+def test_rgetrs_missing_b_is_index_8_and_early_exit():
+    from paper_2109_13406_b200 import Rgetrs
+    with pytest.raises(BlasError) as e:
+        Rgetrs("N", 2, 1, HostMatrix(2, 2), 2, [1, 2], None, None)
+    assert e.value.index == 8
+    b = HostMatrix(3, 1)
+    b.store[0][:] = 5.0
+    assert Rgetrs("N", 3, 0, HostMatrix(3, 3), 3, [1, 2, 3], b, 3) == 0
+    assert np.all(b.store[0] == 5.0)

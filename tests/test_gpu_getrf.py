@@ -96,3 +96,46 @@ def test_rgetrf_fast_modes_close_to_exact(m, n, mode):
     diff = (gh - oh) + (gl - ol)
     scale = np.abs(oh).max()
     assert np.abs(diff).max() <= 1e-26 * scale, np.abs(diff).max() / scale
+
+
+SCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rgetrs"]
+
+
+@pytest.mark.parametrize("mode", ["exact", "reference"])
+@pytest.mark.parametrize("idx", range(len(SCASES)))
+def test_rgetrs_golden_bitwise(idx, mode):
+    """Rgetrf + Rgetrs on the GPU (lu.py:74-145) against the reference's output."""
+    import torch
+    from paper_2109_13406_b200 import Rgetrs
+    case, arr, out_hi, out_lo = SCASES[idx]
+    n, nrhs = case["n"], case["nrhs"]
+    a = DeviceMatrix(n, n, "dd", case["lda"], store=(torch.from_numpy(arr["A_hi"].copy()).cuda(),
+                                                      torch.from_numpy(arr["A_lo"].copy()).cuda()))
+    ipiv, info = Rgetrf(n, n, a, case["lda"], mode=mode)
+    assert list(ipiv) == case["ipiv"]
+    b = DeviceMatrix(n, max(nrhs, 1), "dd", case["ldb"],
+                     store=(torch.from_numpy(arr["B_hi"].copy()).cuda(),
+                            torch.from_numpy(arr["B_lo"].copy()).cuda()))
+    assert Rgetrs(case["trans"], n, nrhs, a, case["lda"], ipiv, b, case["ldb"], mode=mode) == 0
+    assert bits_equal(b.store[0].cpu().numpy(), out_hi), case
+    assert bits_equal(b.store[1].cpu().numpy(), out_lo), case
+
+
+@pytest.mark.parametrize("trans", ["N", "T"])
+def test_rgetrs_exact_matches_oracle_multiblock(trans):
+    import torch
+    from paper_2109_13406_b200 import Rgetrs
+    n, nrhs = 260, 17
+    ah, al = random_dd(n, n, n, 9, 1)
+    bh, bl = random_dd(n, nrhs, n, 9, 2)
+    a = DeviceMatrix(n, n, "dd", n, store=(torch.from_numpy(ah.copy()).cuda(),
+                                           torch.from_numpy(al.copy()).cuda()))
+    ipiv, _ = Rgetrf(n, n, a, n, mode="exact")
+    b = DeviceMatrix(n, nrhs, "dd", n, store=(torch.from_numpy(bh.copy()).cuda(),
+                                              torch.from_numpy(bl.copy()).cuda()))
+    Rgetrs(trans, n, nrhs, a, n, ipiv, b, n, mode="exact")
+    oh, ol = ah.copy(), al.copy()
+    _, oipiv, _ = oracle.rgetrf(n, n, oh, ol, n)
+    xh, xl = bh.copy(), bl.copy()
+    assert oracle.rgetrs(trans, n, nrhs, oh, ol, n, oipiv, xh, xl, n) == 0
+    assert bits_equal(b.store[0].cpu().numpy(), xh) and bits_equal(b.store[1].cpu().numpy(), xl)

@@ -20,6 +20,7 @@ CASES = [c for c in ALL if c[0]["routine"] in ("Rgemm", "Rsyrk")]
 PCASES = [c for c in ALL if c[0]["routine"] == "Rpotrf"]
 TCASES = [c for c in ALL if c[0]["routine"] == "Rtrsm"]
 LCASES = [c for c in ALL if c[0]["routine"] == "Rgetrf"]
+SCASES = [c for c in ALL if c[0]["routine"] == "Rgetrs"]
 CCASES = [c for c in ALL if c[0]["routine"] == "Cgemm"]
 
 
@@ -202,3 +203,18 @@ def test_oracle_trsm_validation_indices(args, idx):
                                       ((0, 0, 0), 4), ((0, 0, 1), 0)])
 def test_oracle_getrf_validation_indices(args, idx):
     assert oracle.lib().oracle_getrf_validate(*args) == idx
+
+
+@pytest.mark.parametrize("idx", range(len(SCASES)))
+def test_oracle_rgetrs_matches_reference_bitwise(idx):
+    """mplapack/lu.py:117-145 (after the oracle's Rgetrf) against the reference."""
+    case, arr, out_hi, out_lo = SCASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"]
+    n, nrhs = case["n"], case["nrhs"]
+    ah, al = arr["A_hi"].copy(), arr["A_lo"].copy()
+    rc, ipiv, info = oracle.rgetrf(n, n, ah, al, case["lda"])
+    assert rc == 0 and ipiv == case["ipiv"]
+    bh, bl = arr["B_hi"].copy(), arr["B_lo"].copy()
+    assert oracle.rgetrs(case["trans"], n, nrhs, ah, al, case["lda"], ipiv, bh, bl,
+                         case["ldb"]) == 0
+    assert bits_equal(bh, out_hi) and bits_equal(bl, out_lo), case
