@@ -431,6 +431,35 @@ int stage_in(DevBuf& b, const double* hi, const double* lo, int64_t n, cudaStrea
 
 }  // namespace
 
+namespace {
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Copy streams for the pipelined host entry point, one pair per host thread
+// and device.
+cudaError_t copy_streams(cudaStream_t* h2d, cudaStream_t* d2h) {
+  static thread_local cudaStream_t st[64][2] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  for (int i = 0; i < 2; ++i)
+    if (st[dev][i] == nullptr && (e = cudaStreamCreateWithFlags(&st[dev][i], cudaStreamNonBlocking)))
+      return e;
+  *h2d = st[dev][0];
+  *d2h = st[dev][1];
+  return cudaSuccess;
+}
+
+}  // namespace
+
 int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
                    double alpha_hi, double alpha_lo,
                    const double* a_hi, const double* a_lo, int64_t lda,
@@ -446,6 +475,81 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
   const int64_t sa = span(na ? m : k, na ? k : m, lda);
   const int64_t sb = span(nb ? k : n, nb ? n : k, ldb);
   const int64_t sc = span(m, n, ldc);
+  // Pipelined path (pinned host buffers, large n): C is done in column
+  // blocks; block b+1's B / C columns are copied in while block b computes
+  // and block b-1's C is copied out.  Each block is an ordinary ddb_rgemm
+  // call on its columns, so exact mode stays bit-identical.
+  static const int64_t pipe_env = [] {
+    const char* v = std::getenv("DDB_HOST_PIPELINE");
+    return v ? (int64_t)std::atoll(v) : (int64_t)-1;
+  }();
+  int64_t nblk = pipe_env >= 0 ? pipe_env : (n >= 2048 && (double)m * n * k >= 1e10 ? 4 : 0);
+  if (nblk > 1 && mode != MODE_REFERENCE && k > 0 && !is_zero(alpha_hi, alpha_lo) &&
+      is_pinned(a_hi) && is_pinned(b_hi) && is_pinned(c_hi)) {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaError_t e = copy_streams(&h2d, &d2h);
+    if (e != cudaSuccess) return fail(e, "copy streams");
+    DevBuf A, B, C;
+    retain_pool_memory();
+    A.s = B.s = C.s = s;
+    e = cudaMallocAsync(reinterpret_cast<void**>(&A.p), sizeof(double) * 2 * sa, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&B.p), sizeof(double) * 2 * sb, s);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&C.p), sizeof(double) * 2 * sc, s);
+    if (e != cudaSuccess) return fail(e, "host staging allocation");
+    const bool read_c = !is_zero(beta_hi, beta_lo);   // beta == 0: C is never read
+    cudaEvent_t ev0 = nullptr, ev_in = nullptr, ev_out = nullptr;
+    e = cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev0, s);             // allocations ready
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev0, 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(A.p, a_hi, sizeof(double) * sa, cudaMemcpyHostToDevice, h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(A.p + sa, a_lo, sizeof(double) * sa, cudaMemcpyHostToDevice, h2d);
+    const int64_t step = ((n + nblk - 1) / nblk + 63) / 64 * 64;
+    for (int64_t j0 = 0; j0 < n && e == cudaSuccess && rc == DDB_OK; j0 += step) {
+      const int64_t j1 = j0 + step < n ? j0 + step : n, w = j1 - j0;
+      // op(B)(:, j0:j1): columns j0.. of B ('N') or rows j0.. of B ('T')
+      for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl) {
+        const double* src = pl ? b_lo : b_hi;
+        double* dst = B.p + pl * sb;
+        if (nb)
+          e = cudaMemcpyAsync(dst + j0 * ldb, src + j0 * ldb,
+                              sizeof(double) * (size_t)span(k, w, ldb), cudaMemcpyHostToDevice, h2d);
+        else
+          e = cudaMemcpy2DAsync(dst + j0, sizeof(double) * ldb, src + j0, sizeof(double) * ldb,
+                                sizeof(double) * w, k, cudaMemcpyHostToDevice, h2d);
+        if (e == cudaSuccess && read_c)
+          e = cudaMemcpyAsync(C.p + pl * sc + j0 * ldc, (pl ? c_lo : c_hi) + j0 * ldc,
+                              sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyHostToDevice, h2d);
+      }
+      if (e == cudaSuccess) e = cudaEventRecord(ev_in, h2d);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in, 0);
+      if (e != cudaSuccess) break;
+      const double* bh = B.p + (nb ? j0 * ldb : j0);
+      const double* bl = B.p + sb + (nb ? j0 * ldb : j0);
+      rc = ddb_rgemm(transa, transb, m, w, k, alpha_hi, alpha_lo, A.p, A.p + sa, lda, bh, bl, ldb,
+                     beta_hi, beta_lo, C.p + j0 * ldc, C.p + sc + j0 * ldc, ldc, mode, stream);
+      if (rc != DDB_OK) break;
+      e = cudaEventRecord(ev_out, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev_out, 0);
+      for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl)
+        e = cudaMemcpyAsync((pl ? c_lo : c_hi) + j0 * ldc, C.p + pl * sc + j0 * ldc,
+                            sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyDeviceToHost, d2h);
+    }
+    // join the copy streams into `s` (the buffers are freed on `s`)
+    cudaError_t ej = cudaEventRecord(ev_out, d2h);
+    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_out, 0);
+    if (ej == cudaSuccess) ej = cudaEventRecord(ev_in, h2d);
+    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_in, 0);
+    if (ej == cudaSuccess) ej = cudaStreamSynchronize(s);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev_in) cudaEventDestroy(ev_in);
+    if (ev_out) cudaEventDestroy(ev_out);
+    if (rc != DDB_OK) return rc;
+    if (e != cudaSuccess) return fail(e, "pipelined host copy");
+    if (ej != cudaSuccess) return fail(ej, "pipelined host join");
+    return DDB_OK;
+  }
   DevBuf A, B, C;
   if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
   if ((rc = stage_in(B, b_hi, b_lo, sb, s))) return rc;

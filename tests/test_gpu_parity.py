@@ -532,3 +532,28 @@ def test_concurrent_calls_on_two_streams_from_two_threads():
     assert not errs, errs
     for mode in ("fast", "exact"):
         assert all(bits_equal(a, b) for a, b in zip(out[mode], refs[mode])), mode
+
+
+@pytest.mark.parametrize("ta,tb,beta", [("N", "N", 0.5), ("T", "T", 0.0), ("N", "T", 1.0)])
+def test_host_pipelined_path_matches_device_exact(ta, tb, beta):
+    """ddb_rgemm_host with pinned buffers and a large problem runs column
+    blocks with copies overlapped (capi.cu); exact mode must still be
+    bit-identical to the device-resident call."""
+    import torch
+    m, n, k = 640, 2048, 7680                   # m n k >= 1e10: the pipelined branch
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A, B, C = random_dd(nra, nca, nra, 4, 1), random_dd(nrb, ncb, nrb, 4, 2), random_dd(m, n, m, 4, 3)
+    hm = []
+    for (r, c, planes) in ((nra, nca, A), (nrb, ncb, B), (m, n, C)):
+        h = HostMatrix(r, c, "dd", r, pinned=True)
+        h.store[0][:] = planes[0]
+        h.store[1][:] = planes[1]
+        hm.append(h)
+    Rgemm(ta, tb, m, n, k, 1.5, hm[0], nra, hm[1], nrb, beta, hm[2], m, mode="exact")
+    c = dev(m, n, m, C)
+    Rgemm(ta, tb, m, n, k, 1.5, dev(nra, nca, nra, A), nra, dev(nrb, ncb, nrb, B), nrb, beta, c,
+          m, mode="exact")
+    torch.cuda.synchronize()
+    assert bits_equal(hm[2].store[0], c.store[0].cpu().numpy())
+    assert bits_equal(hm[2].store[1], c.store[1].cpu().numpy())
