@@ -17,172 +17,12 @@
 #include <vector>
 
 #include "../../include/ddblas.h"
+#include "host.h"
 #include "internal.h"
 
 using namespace ddb;
+using namespace ddb::host;
 
-namespace {
-
-thread_local std::string g_last_error;
-thread_local int g_last_route = -1;
-std::atomic<long long> g_launches{0};
-
-int fail(cudaError_t e, const char* what) {
-  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
-  return e == cudaErrorMemoryAllocation ? DDB_ENOMEM : DDB_ECUDA;
-}
-
-int upflag(char c) { return (c >= 'a' && c <= 'z') ? c - 32 : c; }
-bool is_zero(double h, double l) { return h == 0.0 && l == 0.0; }
-bool is_one(double h, double l) { return h == 1.0 && l == 0.0; }
-
-int bexp(double x) {
-  long long b;
-  std::memcpy(&b, &x, sizeof b);
-  return (int)((b >> 52) & 0x7ff);
-}
-// scalar safe-window test (same window as dd_prescan.cu)
-bool in_window(double h, double l) {
-  const int eh = bexp(h), el = bexp(l);
-  return !((h != 0.0 && eh < WIN_LO) || eh > WIN_HI || el > WIN_HI);
-}
-
-bool debug_sync() {
-  static const bool on = [] {
-    const char* v = std::getenv("DDB_DEBUG_SYNC");
-    return v != nullptr && v[0] != '\0' && v[0] != '0';
-  }();
-  return on;
-}
-
-// The per-call workspace and host staging buffers come from the device's
-// stream-ordered pool; keep freed blocks cached instead of returning them to
-// the driver at every synchronisation (release threshold = unlimited).
-void retain_pool_memory() {
-  static thread_local int done_mask = 0;   // bit per device id < 32
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 32 || (done_mask >> dev) & 1) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    unsigned long long thr = ~0ULL;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done_mask |= 1 << dev;
-}
-
-// Rpotrf's panel stream (highest priority), one per host thread and device.
-cudaError_t potrf_panel_stream(cudaStream_t* out) {
-  static thread_local cudaStream_t streams[64] = {};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev >= 64) return cudaErrorInvalidDevice;
-  if (streams[dev] == nullptr) {
-    int least = 0, greatest = 0;
-    e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (e == cudaSuccess)
-      e = cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, greatest);
-    if (e != cudaSuccess) return e;
-  }
-  *out = streams[dev];
-  return cudaSuccess;
-}
-
-// Runs one validated, non-trivial call: prescan -> tiled (gated on the
-// flag) -> reference-semantics kernel (gated on the opposite).
-int run(const GemmArgs& g0, int mode, cudaStream_t s) {
-  int nl = 0;
-  cudaError_t e;
-  GemmArgs g = g0;
-  {
-    static const int gm_env = [] {
-      const char* v = std::getenv("DDB_GROUP_M");
-      return v ? std::atoi(v) : 0;
-    }();
-    g.group_m = gm_env;
-  }
-  if (g.f64) {   // binary64: bit-exact tiled kernel for every input (no window)
-    if (g.alpha.h == 0.0 || g.k == 0 || mode == MODE_REFERENCE) {
-      e = launch_reference(g, nullptr, GATE_ALWAYS, s, &nl);
-      g_launches += nl;
-      if (e != cudaSuccess) return fail(e, "reference kernel launch");
-      g_last_route = 2;
-      return DDB_OK;
-    }
-    retain_pool_memory();
-    void* ws = nullptr;
-    e = cudaMallocAsync(&ws, 256, s);
-    if (e != cudaSuccess) return fail(e, "workspace allocation");
-    e = cudaMemsetAsync(ws, 0, 256, s);
-    g.kchunk = g.k;
-    if (e == cudaSuccess) e = launch_tiled(g, ALG_F64, nullptr, nullptr, static_cast<int*>(ws), s, &nl);
-    g_launches += nl;
-    cudaError_t e2 = cudaFreeAsync(ws, s);
-    if (e != cudaSuccess) return fail(e, "f64 kernel launch");
-    if (e2 != cudaSuccess) return fail(e2, "workspace free");
-    g_last_route = debug_sync() ? 4 : -1;
-    return DDB_OK;
-  }
-  const bool trivial_ref = mode == MODE_REFERENCE || is_zero(g.alpha.h, g.alpha.l) || g.k == 0;
-  bool scalars_ok = true;
-  if (mode == MODE_EXACT)
-    scalars_ok = in_window(g.alpha.h, g.alpha.l) && in_window(g.beta.h, g.beta.l);
-  if (trivial_ref || !scalars_ok) {
-    e = launch_reference(g, nullptr, GATE_ALWAYS, s, &nl);
-    g_launches += nl;
-    if (e != cudaSuccess) return fail(e, "reference kernel launch");
-    g_last_route = 2;
-    return DDB_OK;
-  }
-  retain_pool_memory();
-  const int alg = alg_for_mode(mode);
-  const int64_t nrow = g.m, ncol = g.n;
-  const size_t head = ((sizeof(int) * (size_t)(16 + nrow + ncol) + 255) / 256) * 256;
-  int64_t kchunk = g.k;
-  const int splits = choose_ksplit(g, alg, &kchunk);
-  g.kchunk = kchunk;
-  const size_t part_bytes = splits > 1 ? (size_t)splits * 2 * g.m * g.n * sizeof(double) : 0;
-  const size_t bnd_bytes = alg == ALG_CERT ? ((bound_workspace_bytes(g) + 255) / 256) * 256 : 0;
-  const size_t ws_bytes = head + bnd_bytes + part_bytes;
-  void* ws = nullptr;
-  e = cudaMallocAsync(&ws, ws_bytes, s);
-  if (e != cudaSuccess) return fail(e, "workspace allocation");
-  int* flag = static_cast<int*>(ws);
-  int* row_exp = flag + 16;
-  int* col_exp = g.syrk ? row_exp : row_exp + nrow;
-  const char* what = "dd kernel launch";
-  e = cudaMemsetAsync(ws, 0, head, s);
-  if (e == cudaSuccess) e = launch_prescan(g, alg, row_exp, col_exp, flag, s, &nl);
-  if (e == cudaSuccess && alg == ALG_CERT) {
-    char* bw = static_cast<char*>(ws) + head;
-    const size_t conv = ((2 * (size_t)g.m * g.k + 255) / 256) * 256 +
-                        (g.syrk ? 0 : ((2 * (size_t)g.k * g.n + 255) / 256) * 256);
-    float* bound = reinterpret_cast<float*>(bw + conv);
-    g.bound = bound;
-    g.bnd_fac = 1.0 + (double)g.k * 0x1p-20;
-    g.bnd_floor = (double)g.k * 0x1p-120;
-    e = launch_bound(g, row_exp, col_exp, bw, bound, s, &nl, &what);
-  }
-  if (splits > 1) g.part = reinterpret_cast<double*>(static_cast<char*>(ws) + head + bnd_bytes);
-  if (e == cudaSuccess) e = launch_tiled(g, alg, row_exp, col_exp, flag, s, &nl);
-  if (e == cudaSuccess && splits > 1) e = launch_splitk_reduce(g, splits, flag, s, &nl);
-  if (e == cudaSuccess) e = launch_reference(g, flag, GATE_IF_UNSAFE, s, &nl);
-  g_launches += nl;
-  int route = -1;
-  if (e == cudaSuccess && debug_sync()) {
-    int f = 0;
-    e = cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    route = f != ROUTE_SAFE ? 2 : (mode == MODE_EXACT ? 0 : (mode == MODE_FAST ? 1 : 3));
-  }
-  cudaError_t e2 = cudaFreeAsync(ws, s);
-  if (e != cudaSuccess) return fail(e, what);
-  if (e2 != cudaSuccess) return fail(e2, "workspace free");
-  g_last_route = route;
-  return DDB_OK;
-}
-
-}  // namespace
 
 extern "C" {
 
@@ -405,31 +245,6 @@ int ddb_zgemm(char transa, char transb, int64_t m, int64_t n, int64_t k, const d
 
 // ---- host-buffer entry points: stage operands through device memory ----
 
-namespace {
-
-int64_t span(int64_t nrow, int64_t ncol, int64_t ld) {
-  return (nrow <= 0 || ncol <= 0) ? 0 : (ncol - 1) * ld + nrow;
-}
-
-struct DevBuf {
-  double* p = nullptr;
-  cudaStream_t s = nullptr;
-  ~DevBuf() { if (p) cudaFreeAsync(p, s); }
-};
-
-int stage_in(DevBuf& b, const double* hi, const double* lo, int64_t n, cudaStream_t s) {
-  b.s = s;
-  retain_pool_memory();
-  if (n == 0) return DDB_OK;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b.p), sizeof(double) * 2 * n, s);
-  if (e != cudaSuccess) return fail(e, "host staging allocation");
-  e = cudaMemcpyAsync(b.p, hi, sizeof(double) * n, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(b.p + n, lo, sizeof(double) * n, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return fail(e, "host to device copy");
-  return DDB_OK;
-}
-
-}  // namespace
 
 namespace {
 
@@ -594,24 +409,6 @@ int ddb_rsyrk_host(char uplo, char trans, int64_t n, int64_t k,
   return DDB_OK;
 }
 
-namespace {
-int stage_in1(DevBuf& b, const double* x, int64_t n, cudaStream_t s) {
-  b.s = s;
-  retain_pool_memory();
-  if (n == 0) return DDB_OK;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&b.p), sizeof(double) * n, s);
-  if (e != cudaSuccess) return fail(e, "host staging allocation");
-  e = cudaMemcpyAsync(b.p, x, sizeof(double) * n, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return fail(e, "host to device copy");
-  return DDB_OK;
-}
-int stage_out1(double* x, const DevBuf& b, int64_t n, cudaStream_t s) {
-  cudaError_t e = cudaMemcpyAsync(x, b.p, sizeof(double) * n, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(e, "device to host copy");
-  return DDB_OK;
-}
-}  // namespace
 
 int ddb_dgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, double alpha,
                    const double* a, int64_t lda, const double* b, int64_t ldb, double beta,
@@ -698,611 +495,6 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
   rc = ddb_zgemm(transa, transb, m, n, k, alpha, A.p, lda, B.p, ldb, beta, C.p, ldc, stream);
   if (rc) return rc;
   return stage_out1(c, C, sc, s);
-}
-
-// ---- triangular solve (dd_trsm.cu) -------------------------------------------
-
-int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
-                       int64_t lda, int64_t ldb) {
-  const int sd = upflag(side), u = upflag(uplo), t = upflag(transa), d = upflag(diag);
-  if (sd != 'L' && sd != 'R') return 1;               // level23.py:296-299
-  if (u != 'U' && u != 'L') return 2;
-  if (t != 'N' && t != 'T' && t != 'C') return 3;
-  if (d != 'U' && d != 'N') return 4;
-  if (m < 0) return 5;                                // :300-301
-  if (n < 0) return 6;
-  const int64_t nrowa = sd == 'L' ? m : n;            // :302-304
-  if (lda < (nrowa > 1 ? nrowa : 1)) return 9;
-  if (ldb < (m > 1 ? m : 1)) return 11;
-  return 0;
-}
-
-int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
-              double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
-              int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream) {
-  const int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
-  if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM) {
-    g_last_error = "unknown mode";
-    return DDB_EINVAL;
-  }
-  if (m == 0 || n == 0) return DDB_OK;                // :306-307
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e;
-  if (is_zero(alpha_hi, alpha_lo)) {                  // :310-312: B = 0
-    e = cudaMemset2DAsync(b_hi, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
-    if (e == cudaSuccess) e = cudaMemset2DAsync(b_lo, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
-    return e == cudaSuccess ? DDB_OK : fail(e, "rtrsm zero fill");
-  }
-  const bool left = upflag(side) == 'L', upper = upflag(uplo) == 'U';
-  const bool notr = upflag(transa) == 'N', alpha_one = is_one(alpha_hi, alpha_lo);
-  const dd alpha{alpha_hi, alpha_lo};
-  // branch table (see dd_trsm.cu): production order, T orientation, finish,
-  // alpha placement, and whether the terms arrive in reverse order
-  TrsmArgs t{};
-  t.left = left;
-  t.unit = upflag(diag) == 'U';
-  t.fin_rec = !left;
-  int trans, init_scale, post_scale, rev_terms;
-  if (left && notr) {        t.rev = upper;  trans = 0; init_scale = !alpha_one; post_scale = 0; rev_terms = 0; }
-  else if (left) {           t.rev = !upper; trans = 1; init_scale = 1;          post_scale = 0; rev_terms = !upper; }
-  else if (notr) {           t.rev = !upper; trans = 1; init_scale = !alpha_one; post_scale = 0; rev_terms = !upper; }
-  else {                     t.rev = upper;  trans = 0; init_scale = 0; post_scale = !alpha_one; rev_terms = 0; }
-  t.p = left ? m : n;
-  t.q = left ? n : m;
-  t.ldw = t.p;
-  t.ldt = t.p;
-  retain_pool_memory();
-  const size_t wsz = (size_t)t.p * t.q, tsz = (size_t)t.p * t.p;
-  void* ws = nullptr;
-  e = cudaMallocAsync(&ws, sizeof(double) * 2 * (wsz + tsz + t.p), s);
-  if (e != cudaSuccess) return fail(e, "rtrsm workspace");
-  double* w = static_cast<double*>(ws);
-  t.w_hi = w; t.w_lo = w + wsz;
-  t.t_hi = w + 2 * wsz; t.t_lo = t.t_hi + tsz;
-  t.d_hi = t.t_lo + tsz; t.d_lo = t.d_hi + t.p;
-  int nl = 0, rc2 = DDB_OK;
-  e = launch_trsm_pack(t, b_hi, b_lo, ldb, init_scale, alpha, s);
-  ++nl;
-  if (e == cudaSuccess) { e = launch_trsm_coef(t, a_hi, a_lo, lda, trans, s); ++nl; }
-  const bool exact_order = mode == MODE_EXACT || mode == MODE_REFERENCE;
-  if (e == cudaSuccess && rev_terms && exact_order) {
-    e = launch_trsm_rev(t, s);
-    ++nl;
-  } else if (e == cudaSuccess) {
-    static const int64_t nb_env = [] {
-      const char* v = std::getenv("DDB_TRSM_NB");
-      return v ? (int64_t)std::atoll(v) : (int64_t)0;
-    }();
-    const int64_t nb = nb_env > 0 && nb_env <= 96 ? nb_env : 64;
-    for (int64_t r0 = 0; r0 < t.p && e == cudaSuccess && rc2 == DDB_OK; r0 += nb) {
-      const int64_t r1 = r0 + nb < t.p ? r0 + nb : t.p;
-      e = launch_trsm_block(t, r0, (int)(r1 - r0), s);
-      ++nl;
-      if (e != cudaSuccess || r1 >= t.p) break;
-      // W(r1:p, :) -= T(r1:p, r0:r1) W(r0:r1, :), terms in production order
-      GemmArgs g{};
-      g.ta = 0; g.tb = 0; g.syrk = 0;
-      g.m = t.p - r1; g.n = t.q; g.k = r1 - r0;
-      g.a_hi = t.t_hi + r1 + r0 * t.ldt; g.a_lo = t.t_lo + r1 + r0 * t.ldt; g.lda = t.ldt;
-      g.b_hi = t.w_hi + r0; g.b_lo = t.w_lo + r0; g.ldb = t.ldw;
-      g.c_hi = t.w_hi + r1; g.c_lo = t.w_lo + r1; g.ldc = t.ldw;
-      g.beta = dd{1.0, 0.0};
-      if (exact_order) { g.sub = 1; g.alpha = dd{1.0, 0.0}; }
-      else { g.sub = 0; g.alpha = dd{-1.0, 0.0}; }
-      rc2 = run(g, mode, s);
-    }
-  }
-  if (e == cudaSuccess && rc2 == DDB_OK) {
-    e = launch_trsm_unpack(t, b_hi, b_lo, ldb, post_scale, alpha, s);
-    ++nl;
-  }
-  g_launches += nl;
-  cudaError_t e2 = cudaFreeAsync(ws, s);
-  if (rc2 != DDB_OK) return rc2;
-  if (e != cudaSuccess) return fail(e, "rtrsm");
-  if (e2 != cudaSuccess) return fail(e2, "workspace free");
-  return DDB_OK;
-}
-
-int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
-                   double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
-                   int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream) {
-  int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
-  if (rc) return rc;
-  if (m == 0 || n == 0) return DDB_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t na = upflag(side) == 'L' ? m : n;
-  const int64_t sa = is_zero(alpha_hi, alpha_lo) ? 0 : span(na, na, lda);
-  const int64_t sb = span(m, n, ldb);
-  DevBuf A, B;
-  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
-  if ((rc = stage_in(B, b_hi, b_lo, sb, s))) return rc;
-  rc = ddb_rtrsm(side, uplo, transa, diag, m, n, alpha_hi, alpha_lo, A.p, A.p ? A.p + sa : nullptr,
-                 lda, B.p, B.p + sb, ldb, mode, stream);
-  if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync(b_hi, B.p, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(b_lo, B.p + sb, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(e, "device to host copy");
-  return DDB_OK;
-}
-
-// ---- LU with partial pivoting (dd_getrf.cu) -----------------------------------
-
-int ddb_rgetrf_validate(int64_t m, int64_t n, int64_t lda) {
-  if (m < 0) return 1;                                // lu.py:83-85
-  if (n < 0) return 2;
-  if (lda < (m > 1 ? m : 1)) return 4;
-  return 0;
-}
-
-int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
-               int* info, int mode, void* stream) {
-  const int rc = ddb_rgetrf_validate(m, n, lda);
-  if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr ||
-      (ipiv == nullptr && m > 0 && n > 0)) {
-    g_last_error = info == nullptr || ipiv == nullptr ? "ipiv / info pointer is null" : "unknown mode";
-    return DDB_EINVAL;
-  }
-  *info = 0;
-  if (m == 0 || n == 0) return DDB_OK;                // lu.py:86-87
-  static const int64_t nb_env = [] {
-    const char* v = std::getenv("DDB_GETRF_NB");
-    return v ? (int64_t)std::atoll(v) : (int64_t)0;
-  }();
-  const int64_t nbo = nb_env > 0 ? nb_env : 256;          // outer width
-  const int64_t ib = nbo < 64 ? nbo : 64;                  // inner (panel kernel) width
-  const int64_t nb = ib;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool_memory();
-  GetrfArgs g{};
-  g.m = m; g.n = n; g.mn = m < n ? m : n; g.lda = lda;
-  g.a_hi = a_hi; g.a_lo = a_lo;
-  const int G = getrf_max_panel_ctas();
-  // workspace: info, barrier | ipiv, swap (mn each) | G partial candidates
-  // partial candidates and rows: two parities (getrf_panel_smem_kernel)
-  const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
-                          2 * (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) +
-                          64 + sizeof(double) * (4 * (size_t)G + 4) * (size_t)nb + 64;
-  void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
-  if (e != cudaSuccess) return fail(e, "rgetrf workspace");
-  char* w = static_cast<char*>(ws);
-  g.info = reinterpret_cast<int*>(w);
-  g.bar = reinterpret_cast<unsigned*>(w + 64);
-  g.ipiv = reinterpret_cast<long long*>(w + 256);
-  g.swap = g.ipiv + g.mn;
-  double* pd = reinterpret_cast<double*>(g.swap + g.mn);
-  g.part_ah = pd; g.part_al = pd + 2 * G; g.part_h = pd + 4 * G; g.part_l = pd + 6 * G;
-  g.part_idx = reinterpret_cast<long long*>(pd + 8 * G);
-  g.part_nan = reinterpret_cast<int*>(g.part_idx + 2 * G);
-  g.rowbuf = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(g.part_nan + 2 * G) + 63) & ~static_cast<uintptr_t>(63));
-  int nl = 0, rc2 = DDB_OK;
-  e = cudaMemsetAsync(ws, 0, 256, s);
-  // Two block levels (outer NB = the trailing GEMM's depth, inner ib <= 64 =
-  // the panel kernel's width) and a lookahead: the next outer panel and the
-  // update of its columns run on the high-priority stream `cs` while the
-  // rest of the trailing update runs on the caller's stream (same scheme and
-  // ordering argument as Rpotrf).
-  const int64_t NB = nbo;
-  cudaStream_t cs = nullptr;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-  if (e == cudaSuccess) e = potrf_panel_stream(&cs);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
-  auto gemm = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t l0, int64_t l1,
-                  cudaStream_t st) -> int {   // A(r0:r1, c0:c1) += A(r0:r1, l0:l1) (-A(l0:l1, c0:c1))
-    if (r1 <= r0 || c1 <= c0 || l1 <= l0) return DDB_OK;
-    return ddb_rgemm('N', 'N', r1 - r0, c1 - c0, l1 - l0, -1.0, 0.0, a_hi + r0 + l0 * lda,
-                     a_lo + r0 + l0 * lda, lda, a_hi + l0 + c0 * lda, a_lo + l0 + c0 * lda, lda,
-                     1.0, 0.0, a_hi + r0 + c0 * lda, a_lo + r0 + c0 * lda, lda, mode,
-                     static_cast<void*>(st));
-  };
-  // block J's pending work on columns [c0, c1): interchanges, U12 (blocked
-  // by the inner width), trailing update of rows >= J1
-  auto apply_block = [&](int64_t J0, int64_t J1, int64_t c0, int64_t c1, cudaStream_t st) -> int {
-    if (c1 <= c0) return DDB_OK;
-    cudaError_t er = launch_getrf_laswp(g, J0, J1, c0, c1, st);
-    ++nl;
-    if (er != cudaSuccess) return fail(er, "rgetrf laswp");
-    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
-      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
-      if ((er = launch_getrf_trsm(g, i0, (int)(i1 - i0), c0, c1, st)) != cudaSuccess)
-        return fail(er, "rgetrf trsm");
-      ++nl;
-      const int r = gemm(i1, J1, c0, c1, i0, i1, st);
-      if (r != DDB_OK) return r;
-    }
-    return gemm(J1, m, c0, c1, J0, J1, st);
-  };
-  // factor the outer panel [J0, J1) (its columns only) on `cs`
-  auto factor_outer = [&](int64_t J0, int64_t J1) -> int {
-    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
-      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
-      cudaError_t er = launch_getrf_panel(g, i0, (int)(i1 - i0), cs);
-      ++nl;
-      if (er == cudaSuccess) { er = launch_getrf_laswp(g, i0, i1, J0, i0, cs); ++nl; }
-      if (er != cudaSuccess) return fail(er, "rgetrf panel");
-      if (i1 < J1) {
-        const int r = apply_block(i0, i1, i1, J1, cs);
-        if (r != DDB_OK) return r;
-      }
-    }
-    return DDB_OK;
-  };
-  if (e == cudaSuccess) e = cudaEventRecord(ev_a, s);
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_a, 0);
-  if (e == cudaSuccess) rc2 = factor_outer(0, NB < g.mn ? NB : g.mn);
-  bool have_rest = false;
-  for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
-    const int64_t J1 = J0 + NB < g.mn ? J0 + NB : g.mn;
-    // interchanges of block J on the factored columns to its left
-    if ((e = launch_getrf_laswp(g, J0, J1, 0, J0, cs)) != cudaSuccess) break;
-    ++nl;
-    if (J1 >= n) break;
-    const int64_t J2 = J1 + NB < g.mn ? J1 + NB : (J1 < g.mn ? g.mn : n);
-    e = cudaEventRecord(ev_a, cs);                         // panel J done
-    if (e == cudaSuccess && have_rest) e = cudaStreamWaitEvent(cs, ev_b, 0);   // rest(J-1)
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
-    if (e != cudaSuccess) break;
-    if (J2 < n) {
-      rc2 = apply_block(J0, J1, J2, n, s);                 // rest(J)
-      if (rc2 != DDB_OK) break;
-      e = cudaEventRecord(ev_b, s);
-      have_rest = true;
-      if (e != cudaSuccess) break;
-    }
-    rc2 = apply_block(J0, J1, J1, J2, cs);                 // columns of block J+1
-    if (rc2 != DDB_OK || J1 >= g.mn) break;
-    rc2 = factor_outer(J1, J2 < g.mn ? J2 : g.mn);
-  }
-  if (cs != nullptr) {
-    cudaError_t ej = cudaEventRecord(ev_a, cs);
-    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_a, 0);
-    if (e == cudaSuccess) e = ej;
-  }
-  if (ev_a) cudaEventDestroy(ev_a);
-  if (ev_b) cudaEventDestroy(ev_b);
-  g_launches += nl;
-  int hinfo = 0;
-  if (e == cudaSuccess && rc2 == DDB_OK) {
-    e = cudaMemcpyAsync(&hinfo, g.info, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(ipiv, g.ipiv, sizeof(long long) * g.mn, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  }
-  cudaError_t e2 = cudaFreeAsync(ws, s);
-  if (rc2 != DDB_OK) return rc2;
-  if (e != cudaSuccess) return fail(e, "rgetrf");
-  if (e2 != cudaSuccess) return fail(e2, "workspace free");
-  *info = hinfo;
-  return DDB_OK;
-}
-
-int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
-                    int* info, int mode, void* stream) {
-  int rc = ddb_rgetrf_validate(m, n, lda);
-  if (rc) return rc;
-  if (info == nullptr) {
-    g_last_error = "info pointer is null";
-    return DDB_EINVAL;
-  }
-  *info = 0;
-  if (m == 0 || n == 0) return DDB_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t sa = span(m, n, lda);
-  DevBuf A;
-  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
-  rc = ddb_rgetrf(m, n, A.p, A.p + sa, lda, ipiv, info, mode, stream);
-  if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync(a_hi, A.p, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(a_lo, A.p + sa, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(e, "device to host copy");
-  return DDB_OK;
-}
-
-int ddb_rgetrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_t ldb) {
-  const int t = upflag(trans);
-  if (t != 'N' && t != 'T' && t != 'C') return 1;     // lu.py:123-125
-  if (n < 0) return 2;
-  if (nrhs < 0) return 3;
-  if (lda < (n > 1 ? n : 1)) return 5;
-  if (ldb < (n > 1 ? n : 1)) return 8;
-  return 0;
-}
-
-int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
-               int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
-               int mode, void* stream) {
-  const int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
-  if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || (ipiv == nullptr && n > 0)) {
-    g_last_error = ipiv == nullptr ? "ipiv pointer is null" : "unknown mode";
-    return DDB_EINVAL;
-  }
-  if (n == 0 || nrhs == 0) return DDB_OK;             // lu.py:130-131
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool_memory();
-  // laswp (lu.py:61-65) with the recorded pivots, as row interchanges of B
-  void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, sizeof(long long) * (size_t)n, s);
-  if (e != cudaSuccess) return fail(e, "rgetrs workspace");
-  std::vector<long long> sw((size_t)n);
-  for (int64_t k = 0; k < n; ++k) sw[(size_t)k] = ipiv[k] - 1;
-  e = cudaMemcpyAsync(ws, sw.data(), sizeof(long long) * (size_t)n, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // sw is a host temporary
-  GetrfArgs g{};
-  g.m = n; g.n = nrhs; g.mn = n; g.lda = ldb;
-  g.a_hi = b_hi; g.a_lo = b_lo;
-  g.swap = static_cast<long long*>(ws);
-  int r = DDB_OK;
-  const bool notr = upflag(trans) == 'N';
-  if (e == cudaSuccess && notr) {
-    e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 0);
-    if (e == cudaSuccess)
-      r = ddb_rtrsm('L', 'L', 'N', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
-    if (e == cudaSuccess && r == DDB_OK)
-      r = ddb_rtrsm('L', 'U', 'N', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
-  } else if (e == cudaSuccess) {
-    r = ddb_rtrsm('L', 'U', 'T', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
-    if (r == DDB_OK)
-      r = ddb_rtrsm('L', 'L', 'T', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
-    if (r == DDB_OK) e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 1);
-  }
-  cudaError_t e2 = cudaFreeAsync(ws, s);
-  if (r != DDB_OK) return r;
-  if (e != cudaSuccess) return fail(e, "rgetrs");
-  if (e2 != cudaSuccess) return fail(e2, "workspace free");
-  return DDB_OK;
-}
-
-int ddb_rgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
-                    int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
-                    int mode, void* stream) {
-  int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
-  if (rc) return rc;
-  if (n == 0 || nrhs == 0) return DDB_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t sa = span(n, n, lda), sb = span(n, nrhs, ldb);
-  DevBuf A, B;
-  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
-  if ((rc = stage_in(B, b_hi, b_lo, sb, s))) return rc;
-  rc = ddb_rgetrs(trans, n, nrhs, A.p, A.p + sa, lda, ipiv, B.p, B.p + sb, ldb, mode, stream);
-  if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync(b_hi, B.p, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(b_lo, B.p + sb, sizeof(double) * sb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(e, "device to host copy");
-  return DDB_OK;
-}
-
-// ---- blocked Cholesky (dd_potrf.cu) ----------------------------------------
-
-int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {
-  const int u = upflag(uplo);
-  if (u != 'U' && u != 'L') return 1;                 // chol.py:24-26
-  if (n < 0) return 2;                                // chol.py:28
-  if (lda < (n > 1 ? n : 1)) return 4;                // chol.py:29
-  return 0;
-}
-
-int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
-               int mode, void* stream, int* info) {
-  const int rc = ddb_rpotrf_validate(uplo, n, lda);
-  if (rc) return rc;
-  if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr) {
-    g_last_error = info == nullptr ? "info pointer is null" : "unknown mode";
-    return DDB_EINVAL;
-  }
-  *info = 0;
-  if (n == 0) return DDB_OK;                          // chol.py:30-31
-  // two block levels: outer width NB (the trailing Rsyrk / Rgemm depth) and
-  // inner width ib <= kPotrfMaxNb (diagonal block in shared memory)
-  if (nb <= 0) {
-    static const int64_t nb_env = [] {
-      const char* v = std::getenv("DDB_POTRF_NB");
-      return v ? (int64_t)std::atoll(v) : (int64_t)0;
-    }();
-    nb = nb_env > 0 ? nb_env : 256;
-  }
-  const int64_t NB = nb;
-  const int64_t ib = nb < kPotrfMaxNb ? nb : kPotrfMaxNb;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  retain_pool_memory();
-  PotrfArgs p{};
-  p.n = n; p.lda = lda; p.upper = upflag(uplo) == 'U';
-  p.a_hi = a_hi; p.a_lo = a_lo;
-  // workspace: info | D, d0 (dd vectors), rec (ib dd) | backup ('L') or S
-  // ('U'), n x n dd | 'U': the inner transposed panel (n x ib) and two outer
-  // ones (n x NB; block J's is read by the trailing update while J+1's is
-  // written)
-  const size_t head = 256, vec = sizeof(double) * (size_t)n;
-  const size_t recb = ((sizeof(double) * 2 * (size_t)ib + 255) / 256) * 256;
-  const size_t full = sizeof(double) * (size_t)n * n;
-  const size_t t_in = p.upper ? (size_t)n * ib : 0, t_out = p.upper ? (size_t)n * NB : 0;
-  const size_t ws_bytes = head + 4 * vec + recb + 2 * full + sizeof(double) * 2 * (t_in + 2 * t_out);
-  void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
-  if (e != cudaSuccess) return fail(e, "workspace allocation");
-  char* w = static_cast<char*>(ws);
-  p.info = reinterpret_cast<int*>(w);
-  double* d = reinterpret_cast<double*>(w + head);
-  p.dh = d; p.dl = d + n;
-  double* d0h = d + 2 * n;
-  double* d0l = d + 3 * n;
-  p.d0_hi = d0h; p.d0_lo = d0l;
-  p.rec_hi = d + 4 * n; p.rec_lo = p.rec_hi + ib;
-  double* big = reinterpret_cast<double*>(w + head + 4 * vec + recb);
-  double* tin_h = big + 2 * (size_t)n * n;           // inner T: hi | lo
-  double* tin_l = tin_h + t_in;
-  double* tout_h = tin_l + t_in;                     // outer T: hi[2] | lo[2]
-  double* tout_l = tout_h + 2 * t_out;
-  int nl = 0;
-  e = cudaMemsetAsync(ws, 0, head + 2 * vec, s);
-  const size_t dpitch = sizeof(double) * (size_t)(lda + 1);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0h, 8, a_hi, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0l, 8, a_lo, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) {
-    if (p.upper) {
-      p.s_hi = big; p.s_lo = big + (size_t)n * n; p.lds = n;
-      e = cudaMemsetAsync(big, 0, 2 * full, s);
-    } else {
-      double* bh = big;
-      double* bl = big + (size_t)n * n;
-      p.b_hi = bh; p.b_lo = bl;
-      const size_t pitch = sizeof(double) * (size_t)lda, row = sizeof(double) * (size_t)n;
-      e = cudaMemcpy2DAsync(bh, row, a_hi, pitch, row, n, cudaMemcpyDeviceToDevice, s);
-      if (e == cudaSuccess) e = cudaMemcpy2DAsync(bl, row, a_lo, pitch, row, n, cudaMemcpyDeviceToDevice, s);
-    }
-  }
-  // Streams: the panel work (diagonal blocks, panels, inner updates and the
-  // lookahead update of the next block column) runs on a high-priority
-  // stream `cs`; the bulk trailing update of each outer block runs on the
-  // caller's stream `s`, overlapping the next panel.  Per element the
-  // contributions still arrive in block order: `cs` waits for rest(J-1)
-  // before update(J -> J+1), and rest(J) follows rest(J-1) on `s`.
-  int rc2 = DDB_OK;
-  cudaStream_t cs = nullptr;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
-  if (e == cudaSuccess) e = potrf_panel_stream(&cs);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
-  // trailing update of columns [c0, c1) (rows >= c0) by factor rows / columns
-  // [j0, j1):  'L': A(r, c) -= L(r, j0:j1) L(c, j0:j1)^T in place;
-  //            'U': S(r, c) += T(r) T(c)^T, T(x) = U(j0:j1, x)^T stored from
-  //                 column tb0 with leading dimension n - tb0
-  auto update = [&](int64_t j0, int64_t j1, int64_t c0, int64_t c1, const double* th,
-                    const double* tl, int64_t tb0, cudaStream_t st) -> int {
-    const int64_t kb = j1 - j0, wd = c1 - c0, below = n - c1;
-    void* sv = static_cast<void*>(st);
-    int r;
-    if (!p.upper) {
-      const double *lh = a_hi + j0 * lda, *ll = a_lo + j0 * lda;
-      r = ddb_rsyrk('L', 'N', wd, kb, -1.0, 0.0, lh + c0, ll + c0, lda, 1.0, 0.0,
-                    a_hi + c0 + c0 * lda, a_lo + c0 + c0 * lda, lda, mode, sv);
-      if (r == DDB_OK && below > 0)
-        r = ddb_rgemm('N', 'T', below, wd, kb, -1.0, 0.0, lh + c1, ll + c1, lda, lh + c0, ll + c0,
-                      lda, 1.0, 0.0, a_hi + c1 + c0 * lda, a_lo + c1 + c0 * lda, lda, mode, sv);
-    } else {
-      const int64_t ldt = n - tb0;
-      th -= tb0;
-      tl -= tb0;                                     // th[x] = T(x) for column x
-      r = ddb_rsyrk('L', 'N', wd, kb, 1.0, 0.0, th + c0, tl + c0, ldt, 1.0, 0.0,
-                    p.s_hi + c0 + c0 * n, p.s_lo + c0 + c0 * n, n, mode, sv);
-      if (r == DDB_OK && below > 0)
-        r = ddb_rgemm('N', 'T', below, wd, kb, 1.0, 0.0, th + c1, tl + c1, ldt, th + c0, tl + c0,
-                      ldt, 1.0, 0.0, p.s_hi + c1 + c0 * n, p.s_lo + c1 + c0 * n, n, mode, sv);
-    }
-    return r;
-  };
-  auto transpose = [&](int64_t j0, int64_t j1, double* th, double* tl) -> cudaError_t {
-    PotrfArgs q = p;
-    q.t_hi = th;
-    q.t_lo = tl;
-    ++nl;
-    return launch_potrf_transpose(q, j0, j1, (int)(j1 - j0), n - j1, cs);
-  };
-  // factor the outer panel [J0, J1): inner blocks, each followed by the
-  // update of the rest of the outer panel's columns
-  auto factor_outer = [&](int64_t J0, int64_t J1) -> int {
-    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
-      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
-      cudaError_t er = launch_potrf_diag(p, i0, i1, cs);
-      ++nl;
-      if (er == cudaSuccess && i1 < n) {
-        er = launch_potrf_panel(p, i0, (int)(i1 - i0), n - i1, cs);
-        ++nl;
-      }
-      if (er != cudaSuccess) return fail(er, "rpotrf panel");
-      if (i1 < J1) {
-        if (p.upper && (er = transpose(i0, i1, tin_h, tin_l)) != cudaSuccess)
-          return fail(er, "rpotrf transpose");
-        const int r = update(i0, i1, i1, J1, tin_h, tin_l, i1, cs);
-        if (r != DDB_OK) return r;
-      }
-    }
-    return DDB_OK;
-  };
-  if (e == cudaSuccess) e = cudaEventRecord(ev_a, s);      // workspace ready
-  if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_a, 0);
-  if (e == cudaSuccess) rc2 = factor_outer(0, NB < n ? NB : n);
-  bool have_rest = false;
-  for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
-    const int64_t J1 = J0 + NB < n ? J0 + NB : n;
-    if (J1 >= n) break;
-    const int64_t J2 = J1 + NB < n ? J1 + NB : n;
-    double* th = tout_h + ((J0 / NB) & 1) * t_out;
-    double* tl = tout_l + ((J0 / NB) & 1) * t_out;
-    if (p.upper) e = transpose(J0, J1, th, tl);
-    if (e == cudaSuccess) e = cudaEventRecord(ev_a, cs);    // panel J (+ T) done
-    if (e == cudaSuccess && have_rest) e = cudaStreamWaitEvent(cs, ev_b, 0);   // rest(J-1)
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
-    if (e != cudaSuccess) break;
-    if (J2 < n) {
-      rc2 = update(J0, J1, J2, n, th, tl, J1, s);           // rest(J)
-      if (rc2 != DDB_OK) break;
-      e = cudaEventRecord(ev_b, s);
-      have_rest = true;
-      if (e != cudaSuccess) break;
-    }
-    rc2 = update(J0, J1, J1, J2, th, tl, J1, cs);            // update(J -> J+1)
-    if (rc2 == DDB_OK) rc2 = factor_outer(J1, J2);
-  }
-  // join the panel stream back into `s`
-  if (cs != nullptr) {
-    cudaError_t ej = cudaEventRecord(ev_a, cs);
-    if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_a, 0);
-    if (e == cudaSuccess) e = ej;
-  }
-  if (ev_a) cudaEventDestroy(ev_a);
-  if (ev_b) cudaEventDestroy(ev_b);
-  if (e == cudaSuccess && rc2 == DDB_OK && !p.upper) {
-    e = launch_potrf_restore(p, s);
-    ++nl;
-  }
-  g_launches += nl;
-  int hinfo = 0;
-  if (e == cudaSuccess && rc2 == DDB_OK) {
-    e = cudaMemcpyAsync(&hinfo, p.info, sizeof(int), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  }
-  cudaError_t e2 = cudaFreeAsync(ws, s);
-  if (rc2 != DDB_OK) return rc2;
-  if (e != cudaSuccess) return fail(e, "rpotrf");
-  if (e2 != cudaSuccess) return fail(e2, "workspace free");
-  *info = hinfo;
-  return DDB_OK;
-}
-
-int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
-                    int mode, void* stream, int* info) {
-  int rc = ddb_rpotrf_validate(uplo, n, lda);
-  if (rc) return rc;
-  if (info == nullptr) {
-    g_last_error = "info pointer is null";
-    return DDB_EINVAL;
-  }
-  *info = 0;
-  if (n == 0) return DDB_OK;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const int64_t sa = span(n, n, lda);
-  DevBuf A;
-  if ((rc = stage_in(A, a_hi, a_lo, sa, s))) return rc;
-  rc = ddb_rpotrf(uplo, n, A.p, A.p + sa, lda, nb, mode, stream, info);
-  if (rc) return rc;
-  cudaError_t e = cudaMemcpyAsync(a_hi, A.p, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(a_lo, A.p + sa, sizeof(double) * sa, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(e, "device to host copy");
-  return DDB_OK;
 }
 
 }  // extern "C"
