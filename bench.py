@@ -133,6 +133,33 @@ def cpu_sample_rate(n, k, cols, threads):
     return 2.0 * m * cols * k / dt / 1e9, dt, f"Rgemm NN m={m} n={cols} k={k} (columns of the n={n} workload)"
 
 
+def cpu_lapack_rates(n=512):
+    """The reference's LAPACK consumers on the host (the bit-exact C port of
+    the unblocked algorithms, one core) at a sample size n: dd GFlops in the
+    reference bench's counting, for the rpotrf / rgetrf / rtrsm lines."""
+    from oracle import oracle
+    from paper_2109_13406_b200 import flop_count
+    from paper_2109_13406_b200.synth import random_dd, spd_dd
+    out = {}
+    h, l = spd_dd(n, n, seed=0)
+    t0 = time.perf_counter()
+    oracle.rpotrf("L", n, h, l, n)
+    out["rpotrf"] = flop_count("Rpotrf", n) / (time.perf_counter() - t0) / 1e9
+    h, l = random_dd(n, n, n, 0, 1)
+    t0 = time.perf_counter()
+    oracle.rgetrf(n, n, h, l, n)
+    out["rgetrf"] = flop_count("Rgetrf", n) / (time.perf_counter() - t0) / 1e9
+    ah, al = random_dd(n, n, n, 0, 4)
+    ah[:: n + 1] += 4.0
+    bh, bl = random_dd(n, n, n, 0, 5)
+    t0 = time.perf_counter()
+    oracle.rtrsm("L", "L", "N", "N", n, n, (1.5, 0.0), ah, al, n, bh, bl, n)
+    out["rtrsm"] = 1.0 * n ** 3 / (time.perf_counter() - t0) / 1e9
+    return {k: {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"n={n}, unblocked reference order (oracle/dd_oracle.c)"}
+            for k, v in out.items()}
+
+
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -286,6 +313,14 @@ def run_ours(args):
             extra["rpotrf"] = _rpotrf(n, dev, stream, mode)
             extra["rgetrf"] = _rgetrf(n, dev, stream, mode)
             extra["rtrsm"] = _rtrsm(n, dev, stream, mode)
+        if not distributed:
+            cpu_lp = cpu_lapack_rates()
+            for key in ("rpotrf", "rgetrf", "rtrsm"):
+                if key in extra:
+                    extra[key]["cpu_baseline"] = cpu_lp[key]
+                    # dd roof = measured DFMA peak / 20 fp64 flops per dd MAC x 2 dd flops
+                    roof = extra["roofline"]["peak"] * 1e3 / 10.0
+                    extra[key]["roofline_frac"] = extra[key]["value"] / roof
         cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, 16, 0)
         from oracle import oracle
         extra["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": oracle.max_threads(),
