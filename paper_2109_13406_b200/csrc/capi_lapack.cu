@@ -94,23 +94,35 @@ int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n
       const char* v = std::getenv("DDB_TRSM_NB");
       return v ? (int64_t)std::atoll(v) : (int64_t)0;
     }();
-    const int64_t nb = nb_env > 0 && nb_env <= 96 ? nb_env : 64;
-    for (int64_t r0 = 0; r0 < t.p && e == cudaSuccess && rc2 == DDB_OK; r0 += nb) {
-      const int64_t r1 = r0 + nb < t.p ? r0 + nb : t.p;
-      e = launch_trsm_block(t, r0, (int)(r1 - r0), s);
-      ++nl;
-      if (e != cudaSuccess || r1 >= t.p) break;
-      // W(r1:p, :) -= T(r1:p, r0:r1) W(r0:r1, :), terms in production order
+    // two levels: inner blocks of ib rows (diagonal solve + a GEMM over the
+    // rest of the outer block), then one GEMM of depth NB for all rows below
+    // the outer block -- per element the terms still arrive in production
+    // order
+    const int64_t ib = 64;
+    const int64_t NB = nb_env > 0 ? (nb_env < ib ? ib : nb_env) : 256;
+    // W(r0:r1, :) -= T(r0:r1, l0:l1) W(l0:l1, :)
+    auto update = [&](int64_t r0, int64_t r1, int64_t l0, int64_t l1) -> int {
+      if (r1 <= r0 || l1 <= l0) return DDB_OK;
       GemmArgs g{};
       g.ta = 0; g.tb = 0; g.syrk = 0;
-      g.m = t.p - r1; g.n = t.q; g.k = r1 - r0;
-      g.a_hi = t.t_hi + r1 + r0 * t.ldt; g.a_lo = t.t_lo + r1 + r0 * t.ldt; g.lda = t.ldt;
-      g.b_hi = t.w_hi + r0; g.b_lo = t.w_lo + r0; g.ldb = t.ldw;
-      g.c_hi = t.w_hi + r1; g.c_lo = t.w_lo + r1; g.ldc = t.ldw;
+      g.m = r1 - r0; g.n = t.q; g.k = l1 - l0;
+      g.a_hi = t.t_hi + r0 + l0 * t.ldt; g.a_lo = t.t_lo + r0 + l0 * t.ldt; g.lda = t.ldt;
+      g.b_hi = t.w_hi + l0; g.b_lo = t.w_lo + l0; g.ldb = t.ldw;
+      g.c_hi = t.w_hi + r0; g.c_lo = t.w_lo + r0; g.ldc = t.ldw;
       g.beta = dd{1.0, 0.0};
       if (exact_order) { g.sub = 1; g.alpha = dd{1.0, 0.0}; }
       else { g.sub = 0; g.alpha = dd{-1.0, 0.0}; }
-      rc2 = run(g, mode, s);
+      return run(g, mode, s);
+    };
+    for (int64_t o0 = 0; o0 < t.p && e == cudaSuccess && rc2 == DDB_OK; o0 += NB) {
+      const int64_t o1 = o0 + NB < t.p ? o0 + NB : t.p;
+      for (int64_t r0 = o0; r0 < o1 && e == cudaSuccess && rc2 == DDB_OK; r0 += ib) {
+        const int64_t r1 = r0 + ib < o1 ? r0 + ib : o1;
+        e = launch_trsm_block(t, r0, (int)(r1 - r0), s);
+        ++nl;
+        if (e == cudaSuccess) rc2 = update(r1, o1, r0, r1);
+      }
+      if (e == cudaSuccess && rc2 == DDB_OK) rc2 = update(o1, t.p, o0, o1);
     }
   }
   if (e == cudaSuccess && rc2 == DDB_OK) {
