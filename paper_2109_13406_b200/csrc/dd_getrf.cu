@@ -23,6 +23,8 @@
 // either way (lu.py:93-106).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace ddb {
@@ -581,6 +583,18 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
       cudaFuncSetAttribute(getrf_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            200 * 1024);
       attr_dev = dev;
+    }
+    // A cooperative launch guarantees co-residency but may wait for an idle
+    // device; with grid <= one CTA per SM an ordinary launch also completes
+    // (the other stream's CTAs always retire), and can overlap the trailing
+    // update (measured: no difference).  DDB_GETRF_COOP=0 selects it.
+    static const bool coop = [] {
+      const char* v = std::getenv("DDB_GETRF_COOP");
+      return v == nullptr || v[0] != '0';
+    }();
+    if (!coop) {
+      getrf_panel_smem_kernel<<<grid, kPanelThreads, smem, s>>>(ga, j0, nbv, chunk);
+      return cudaGetLastError();
     }
     void* args[] = {&ga, &j0, &nbv, &chunk};
     return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(getrf_panel_smem_kernel),
