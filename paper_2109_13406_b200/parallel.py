@@ -108,14 +108,36 @@ def _slab(store, start, length):
     return store[0][start:start + length], store[1][start:start + length]
 
 
+def _k_chunks(k, kchunks, tile=TILE):
+    """[l0, l1) boundaries of kchunks nearly equal k-panels (tile multiples)."""
+    kchunks = max(1, min(kchunks, -(-k // tile) if k else 1))
+    out = []
+    for c in range(kchunks):
+        l0 = (k * c // kchunks) // tile * tile if c else 0
+        l1 = (k * (c + 1) // kchunks) // tile * tile if c + 1 < kchunks else k
+        if l1 > l0:
+            out.append((l0, l1))
+    return out or [(0, k)]
+
+
 def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=None,
-                  compute=None):
+                  compute=None, kchunks=None):
     """C <- alpha op(A) op(B) + beta C with C split by column blocks over ranks.
 
     On the root, ``a``/``b``/``c`` are the full operands (leading dimensions
     tight: lda = rows); on the other ranks they are ignored (None).  Returns
     nothing; on the root C holds the result (bitwise equal to ``Rgemm`` in
-    exact mode)."""
+    exact mode).
+
+    The k dimension is streamed in ``kchunks`` panels: panel c+1 of op(A)
+    (broadcast) and of each rank's op(B) columns (point-to-point) is in
+    flight on NCCL's stream while panel c computes, each panel an Rgemm with
+    beta = 1 after the first.  For transa = 'N' that is the reference's own
+    per-element sequence (beta-scale C, then c += a_il * (alpha b_lj) for l
+    ascending, level23.py:120-125), so exact mode stays bitwise; for
+    transa = 'T' the reference sums from zero and combines once, so exact
+    mode keeps a single panel there (fast modes chunk either way)."""
+    from .mpblas import default_mode
     ops = _Ops(group)
     compute = functools.partial(Rgemm, _check_storage=False) if compute is None else compute
     m, n, k = plan.m, plan.n, plan.k
@@ -125,43 +147,27 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
     lda = max(1, nra)
     be = to_dd(beta)
     beta_zero = be[0] == 0.0 and be[1] == 0.0
-
-    # 1. op(A) to every rank
-    if rank == 0:
-        a_store = (a.store[0][:lda * nca], a.store[1][:lda * nca])
-    else:
-        a_store = plan.buf("A", lda * nca)
-    ops.bcast(a_store[0])
-    ops.bcast(a_store[1])
-    A = DeviceMatrix(nra, nca, "dd", lda, store=a_store)
-
-    # 2. B and C column slabs to their owners
+    exact_like = (default_mode() if mode is None else mode) in ("exact", "reference")
+    if kchunks is None:
+        kchunks = 4 if k >= 4096 and (ta == "N" or not exact_like) else 1
+    if ta != "N" and exact_like:
+        kchunks = 1
+    panels = _k_chunks(k, kchunks)
     j0, j1 = plan.blocks[rank]
     nb = j1 - j0
-    ldb_loc = max(1, k) if tb == "N" else max(1, nb)
+
+    # 1. C column slabs to their owners (only read when beta != 0)
     sends, recvs = [], []
     if rank == 0:
-        for r in range(1, world):
-            r0, r1 = plan.blocks[r]
-            if r1 == r0:
-                continue
-            if tb == "N":
-                bs = _slab(b.store, r0 * k, (r1 - r0) * k)
-            else:   # rows r0:r1 of the stored n x k matrix, packed column-major
-                bs = tuple(p[:n * k].view(k, n)[:, r0:r1].contiguous().view(-1) for p in b.store)
-            sends += [ops.send(bs[0], r, group), ops.send(bs[1], r, group)]
-            if not beta_zero:
-                cs = _slab(c.store, r0 * m, (r1 - r0) * m)
-                sends += [ops.send(cs[0], r, group), ops.send(cs[1], r, group)]
-        if tb == "N":
-            b_loc = _slab(b.store, j0 * k, nb * k)
-        else:
-            b_loc = tuple(p[:n * k].view(k, n)[:, j0:j1].contiguous().view(-1) for p in b.store)
         c_loc = _slab(c.store, j0 * m, nb * m)
+        if not beta_zero:
+            for r in range(1, world):
+                r0, r1 = plan.blocks[r]
+                if r1 > r0:
+                    cs = _slab(c.store, r0 * m, (r1 - r0) * m)
+                    sends += [ops.send(cs[0], r, group), ops.send(cs[1], r, group)]
     elif nb:
-        b_loc = plan.buf("B", nb * k)
         c_loc = plan.buf("C", nb * m)
-        recvs += [ops.recv(b_loc[0], 0, group), ops.recv(b_loc[1], 0, group)]
         if not beta_zero:
             recvs += [ops.recv(c_loc[0], 0, group), ops.recv(c_loc[1], 0, group)]
         else:
@@ -169,14 +175,81 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
             c_loc[1].zero_()
     ops.exchange(sends + recvs)
 
-    # 3. local slab
-    if nb:
-        nrb_loc, ncb_loc = (k, nb) if tb == "N" else (nb, k)
-        B = DeviceMatrix(nrb_loc, ncb_loc, "dd", ldb_loc, store=b_loc)
-        C = DeviceMatrix(m, nb, "dd", max(1, m), store=c_loc)
-        compute(ta, tb, m, nb, k, alpha, A, lda, B, ldb_loc, beta, C, max(1, m), mode=mode)
+    # 2. k-panels: communication of panel c+1 overlaps the compute of panel c
+    def a_panel(idx, l0, l1):
+        """(store, ld) of op(A)(:, l0:l1): a slice of A ('N') or packed rows ('T')."""
+        if ta == "N":
+            if rank == 0:
+                st = _slab(a.store, l0 * lda, (l1 - l0) * lda)
+            else:
+                full = plan.buf("A", lda * nca)
+                st = _slab(full, l0 * lda, (l1 - l0) * lda)
+            return st, lda
+        kc = l1 - l0
+        if rank == 0:
+            st = tuple(p[:lda * nca].view(nca, lda)[:, l0:l1].contiguous().view(-1)
+                       for p in a.store)
+        else:
+            st = plan.buf(f"A{idx}", kc * nca)
+        return st, max(1, kc)
 
-    # 4. slabs back to the root
+    def b_panel(idx, l0, l1, r0, r1, store=None):
+        """op(B)(l0:l1, r0:r1) packed column-major; (store, ld)."""
+        kc, w = l1 - l0, r1 - r0
+        if store is not None:            # the root packs from the full B
+            if tb == "N":
+                st = tuple(p[:k * n].view(n, k)[r0:r1, l0:l1].contiguous().view(-1)
+                           for p in store)
+            else:
+                st = tuple(p[:n * k].view(k, n)[l0:l1, r0:r1].contiguous().view(-1)
+                           for p in store)
+        else:
+            st = plan.buf(f"B{idx}", kc * w)
+        return st, (max(1, kc) if tb == "N" else max(1, w))
+
+    def issue(idx):
+        """Start panel idx's transfers; returns (waitables, local A, local B)."""
+        l0, l1 = panels[idx]
+        a_st, a_ld = a_panel(idx, l0, l1)
+        works = [dist.broadcast(a_st[0], src=0, group=group, async_op=True),
+                 dist.broadcast(a_st[1], src=0, group=group, async_op=True)]
+        p2p = []
+        b_loc = None
+        if rank == 0:
+            for r in range(world):
+                r0, r1 = plan.blocks[r]
+                if r1 == r0:
+                    continue
+                st, ld = b_panel(idx, l0, l1, r0, r1, store=b.store)
+                if r == 0:
+                    b_loc = (st, ld)
+                else:
+                    p2p += [ops.send(st[0], r, group), ops.send(st[1], r, group)]
+        elif nb:
+            st, ld = b_panel(idx, l0, l1, j0, j1)
+            b_loc = (st, ld)
+            p2p += [ops.recv(st[0], 0, group), ops.recv(st[1], 0, group)]
+        if p2p:
+            works += dist.batch_isend_irecv(p2p)
+        return works, (a_st, a_ld), b_loc
+
+    pending = issue(0)
+    for idx, (l0, l1) in enumerate(panels):
+        works, (a_st, a_ld), b_loc = pending
+        if idx + 1 < len(panels):
+            pending = issue(idx + 1)
+        for w_ in works:
+            w_.wait()
+        if nb:
+            kc = l1 - l0
+            A = DeviceMatrix(*((m, kc) if ta == "N" else (kc, m)), "dd", a_ld, store=a_st)
+            (b_st, b_ld) = b_loc
+            B = DeviceMatrix(*((kc, nb) if tb == "N" else (nb, kc)), "dd", b_ld, store=b_st)
+            C = DeviceMatrix(m, nb, "dd", max(1, m), store=c_loc)
+            compute(ta, tb, m, nb, kc, alpha, A, a_ld, B, b_ld, beta if idx == 0 else 1.0, C,
+                    max(1, m), mode=mode)
+
+    # 3. slabs back to the root
     sends, recvs = [], []
     if rank == 0:
         for r in range(1, world):

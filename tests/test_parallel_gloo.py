@@ -59,7 +59,7 @@ def _worker(rank, world, port, case, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         if case[0] == "gemm":
-            _, ta, tb, m, n, k, beta = case
+            _, ta, tb, m, n, k, beta, kchunks, mode = (case + (None, None))[:9]
             nra, nca = (m, k) if ta == "N" else (k, m)
             nrb, ncb = (k, n) if tb == "N" else (n, k)
             if rank == 0:
@@ -67,7 +67,8 @@ def _worker(rank, world, port, case, q):
             else:
                 A = B = C = None
             plan = parallel.RgemmPlan(m, n, k, world, rank, torch.device("cpu"))
-            parallel.rgemm_columns(plan, ta, tb, 1.5, A, B, beta, C, compute=oracle_gemm)
+            parallel.rgemm_columns(plan, ta, tb, 1.5, A, B, beta, C, compute=oracle_gemm,
+                                   kchunks=kchunks, mode=mode)
             if rank == 0:
                 q.put((C.store[0].numpy().copy(), C.store[1].numpy().copy()))
         else:
@@ -112,6 +113,33 @@ def test_rgemm_columns_bitwise_equal_single_process(ta, tb, beta):
     oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra, B[0], B[1], nrb, to_dd(beta),
                  ch, cl, m)
     assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+@pytest.mark.parametrize("ta,tb,beta,mode", [("N", "N", 0.5, None), ("N", "T", 0.0, None),
+                                             ("T", "N", 0.5, "exact"), ("T", "T", 1.0, "exact")])
+def test_rgemm_columns_k_panels_bitwise(ta, tb, beta, mode):
+    """k streamed in 3 panels (transfers overlapped with compute): still the
+    single-process result bit for bit -- transa 'N' by the axpy order,
+    transa 'T' in exact mode because the panels are then suppressed."""
+    m, n, k = 66, 150, 200
+    got = _run(("gemm", ta, tb, m, n, k, beta, 3, mode))
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A = random_dd(nra, nca, nra, 3, 1)
+    B = random_dd(nrb, ncb, nrb, 3, 2)
+    ch, cl = (x.copy() for x in random_dd(m, n, m, 3, 3))
+    oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra, B[0], B[1], nrb, to_dd(beta),
+                 ch, cl, m)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+def test_k_chunks_cover():
+    for k in (1, 63, 64, 200, 4096, 8193):
+        for c in (1, 2, 3, 4, 8):
+            ch = parallel._k_chunks(k, c)
+            assert ch[0][0] == 0 and ch[-1][1] == k
+            assert all(a1 == b0 for (_, a1), (b0, _) in zip(ch, ch[1:]))
+            assert all(l1 > l0 for l0, l1 in ch)
 
 
 @pytest.mark.parametrize("up,tr", [("U", "N"), ("L", "N"), ("U", "T"), ("L", "T")])
