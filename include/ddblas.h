@@ -174,6 +174,27 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
 int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
                     int mode, void* stream, int* info);
 
+/* Single-process multi-GPU: operands and result on
+ * devices[0]; device i computes a column slab of C (Rgemm: equal slabs;
+ * Rsyrk: slabs of equal triangle area, each an Rsyrk diagonal block + an
+ * Rgemm rectangle) after peer copies of op(A) and its slab; slabs come back
+ * by peer copy.  Exact mode is bitwise equal to ddb_rgemm / ddb_rsyrk.  A
+ * device id may repeat.  Synchronous; returns as ddb_rgemm / ddb_rsyrk
+ * (DDB_EINVAL for an empty device list). */
+int ddb_rgemm_mgpu(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                   double alpha_hi, double alpha_lo,
+                   const double* a_hi, const double* a_lo, int64_t lda,
+                   const double* b_hi, const double* b_lo, int64_t ldb,
+                   double beta_hi, double beta_lo,
+                   double* c_hi, double* c_lo, int64_t ldc, int mode, int ndev,
+                   const int* devices);
+int ddb_rsyrk_mgpu(char uplo, char trans, int64_t n, int64_t k,
+                   double alpha_hi, double alpha_lo,
+                   const double* a_hi, const double* a_lo, int64_t lda,
+                   double beta_hi, double beta_lo,
+                   double* c_hi, double* c_lo, int64_t ldc, int mode, int ndev,
+                   const int* devices);
+
 /* Argument checks alone (no device work): reference index or 0. */
 int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
                        int64_t lda, int64_t ldb, int64_t ldc);

@@ -29,7 +29,8 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rpotrf", "ddb_rpotrf_host", "ddb_rpotrf_validate",
            "ddb_rtrsm", "ddb_rtrsm_host", "ddb_rtrsm_validate",
            "ddb_rgetrf", "ddb_rgetrf_host", "ddb_rgetrf_validate",
-           "ddb_rgetrs", "ddb_rgetrs_host", "ddb_rgetrs_validate")
+           "ddb_rgetrs", "ddb_rgetrs_host", "ddb_rgetrs_validate",
+           "ddb_rgemm_mgpu", "ddb_rsyrk_mgpu")
 
 _lib = None
 
@@ -101,6 +102,11 @@ def load():
     L.ddb_rgetrf_validate.argtypes = [_i64, _i64, _i64]
     L.ddb_rpotrf_validate.restype = ctypes.c_int
     L.ddb_rpotrf_validate.argtypes = [_c, _i64, _i64]
+    ip = ctypes.POINTER(ctypes.c_int)
+    L.ddb_rgemm_mgpu.restype = ctypes.c_int
+    L.ddb_rgemm_mgpu.argtypes = gemm_args[:-1] + [ctypes.c_int, ip]
+    L.ddb_rsyrk_mgpu.restype = ctypes.c_int
+    L.ddb_rsyrk_mgpu.argtypes = syrk_args[:-1] + [ctypes.c_int, ip]
     L.ddb_rgemm_validate.restype = ctypes.c_int
     L.ddb_rgemm_validate.argtypes = [_c, _c] + [_i64] * 6
     L.ddb_rsyrk_validate.restype = ctypes.c_int

@@ -557,3 +557,66 @@ def test_host_pipelined_path_matches_device_exact(ta, tb, beta):
     torch.cuda.synchronize()
     assert bits_equal(hm[2].store[0], c.store[0].cpu().numpy())
     assert bits_equal(hm[2].store[1], c.store[1].cpu().numpy())
+
+
+def _mgpu_devices(count):
+    import ctypes
+    return (ctypes.c_int * count)(*([0] * count))
+
+
+@pytest.mark.parametrize("ta,tb,beta,mode", [("N", "N", 0.5, "exact"), ("N", "T", 0.0, "exact"),
+                                             ("T", "N", 1.5, "exact"), ("T", "T", 0.5, "exact"),
+                                             ("N", "N", 0.5, "fast")])
+@pytest.mark.parametrize("ndev", [1, 3])
+def test_rgemm_mgpu_matches_single_call(ta, tb, beta, mode, ndev):
+    """ddb_rgemm_mgpu with the device list [0]*ndev: the column slabs, peer
+    copies and gathers of the multi-GPU entry point on one GPU; exact mode
+    bitwise equal to ddb_rgemm, fast mode within its bound of it."""
+    import torch
+    L = _lib.load()
+    m, n, k = 150, 333, 97
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A, B, C = random_dd(nra, nca, nra + 1, 6, 1), random_dd(nrb, ncb, nrb + 2, 6, 2), \
+        random_dd(m, n, m + 3, 6, 3)
+    d = [torch.from_numpy(np.ascontiguousarray(p)).cuda() for p in (*A, *B, *C)]
+    ref = [t.clone() for t in d[4:]]
+    code = _lib.MODES[mode]
+    rc = L.ddb_rgemm(ta.encode(), tb.encode(), m, n, k, 1.5, 0.0, d[0].data_ptr(), d[1].data_ptr(),
+                     nra + 1, d[2].data_ptr(), d[3].data_ptr(), nrb + 2, beta, 0.0,
+                     ref[0].data_ptr(), ref[1].data_ptr(), m + 3, code, None)
+    assert rc == 0
+    rc = L.ddb_rgemm_mgpu(ta.encode(), tb.encode(), m, n, k, 1.5, 0.0, d[0].data_ptr(),
+                          d[1].data_ptr(), nra + 1, d[2].data_ptr(), d[3].data_ptr(), nrb + 2, beta,
+                          0.0, d[4].data_ptr(), d[5].data_ptr(), m + 3, code, ndev,
+                          _mgpu_devices(ndev))
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    if mode == "exact":
+        assert bits_equal(d[4].cpu().numpy(), ref[0].cpu().numpy())
+        assert bits_equal(d[5].cpu().numpy(), ref[1].cpu().numpy())
+    else:
+        diff = (d[4] - ref[0]) + (d[5] - ref[1])
+        assert float(diff.abs().max()) <= 1e-28 * float(ref[0].abs().max())
+
+
+@pytest.mark.parametrize("up,tr", [("U", "N"), ("L", "N"), ("U", "T"), ("L", "T")])
+@pytest.mark.parametrize("ndev", [2, 4])
+def test_rsyrk_mgpu_matches_single_call(up, tr, ndev):
+    import torch
+    L = _lib.load()
+    n, k = 300, 41
+    nra, nca = (n, k) if tr == "N" else (k, n)
+    A, C = random_dd(nra, nca, nra, 7, 1), random_dd(n, n, n + 1, 7, 3)
+    d = [torch.from_numpy(np.ascontiguousarray(p)).cuda() for p in (*A, *C)]
+    ref = [t.clone() for t in d[2:]]
+    rc = L.ddb_rsyrk(up.encode(), tr.encode(), n, k, 1.5, 0.0, d[0].data_ptr(), d[1].data_ptr(),
+                     nra, 0.5, 0.0, ref[0].data_ptr(), ref[1].data_ptr(), n + 1, 0, None)
+    assert rc == 0
+    rc = L.ddb_rsyrk_mgpu(up.encode(), tr.encode(), n, k, 1.5, 0.0, d[0].data_ptr(),
+                          d[1].data_ptr(), nra, 0.5, 0.0, d[2].data_ptr(), d[3].data_ptr(), n + 1,
+                          0, ndev, _mgpu_devices(ndev))
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert bits_equal(d[2].cpu().numpy(), ref[0].cpu().numpy())
+    assert bits_equal(d[3].cpu().numpy(), ref[1].cpu().numpy())
