@@ -198,7 +198,8 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   // partial candidates and rows: two parities (getrf_panel_smem_kernel)
   const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
                           2 * (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) +
-                          64 + sizeof(double) * (4 * (size_t)G + 4) * (size_t)nb + 64;
+                          64 + sizeof(double) * (4 * (size_t)G + 4) * (size_t)nb + 64 +
+                          2 * (size_t)kPermBufBytes + 64;
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "rgetrf workspace");
@@ -213,6 +214,18 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   g.part_nan = reinterpret_cast<int*>(g.part_idx + 2 * G);
   g.rowbuf = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(g.part_nan + 2 * G) + 63) & ~static_cast<uintptr_t>(63));
+  // composed interchanges: one buffer per stream that applies them
+  PermBuf pbuf[2];
+  {
+    char* pp = reinterpret_cast<char*>(
+        (reinterpret_cast<uintptr_t>(g.rowbuf + (4 * (size_t)G + 4) * nb) + 63) &
+        ~static_cast<uintptr_t>(63));
+    for (int i = 0; i < 2; ++i, pp += kPermBufBytes) {
+      pbuf[i].rows = reinterpret_cast<long long*>(pp);
+      pbuf[i].src = reinterpret_cast<int*>(pp + 512 * 8);
+      pbuf[i].n = reinterpret_cast<int*>(pp + 512 * 12);
+    }
+  }
   int nl = 0, rc2 = DDB_OK;
   e = cudaMemsetAsync(ws, 0, 256, s);
   // Two block levels (outer NB = the trailing GEMM's depth, inner ib <= 64 =
@@ -238,7 +251,7 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   // by the inner width), trailing update of rows >= J1
   auto apply_block = [&](int64_t J0, int64_t J1, int64_t c0, int64_t c1, cudaStream_t st) -> int {
     if (c1 <= c0) return DDB_OK;
-    cudaError_t er = launch_getrf_laswp(g, J0, J1, c0, c1, st);
+    cudaError_t er = launch_getrf_laswp(g, J0, J1, c0, c1, st, 0, pbuf[st == cs ? 0 : 1]);
     ++nl;
     if (er != cudaSuccess) return fail(er, "rgetrf laswp");
     for (int64_t i0 = J0; i0 < J1; i0 += ib) {
@@ -257,7 +270,7 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
       const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
       cudaError_t er = launch_getrf_panel(g, i0, (int)(i1 - i0), cs);
       ++nl;
-      if (er == cudaSuccess) { er = launch_getrf_laswp(g, i0, i1, J0, i0, cs); ++nl; }
+      if (er == cudaSuccess) { er = launch_getrf_laswp(g, i0, i1, J0, i0, cs, 0, pbuf[0]); ++nl; }
       if (er != cudaSuccess) return fail(er, "rgetrf panel");
       if (i1 < J1) {
         const int r = apply_block(i0, i1, i1, J1, cs);
@@ -273,7 +286,7 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
     const int64_t J1 = J0 + NB < g.mn ? J0 + NB : g.mn;
     // interchanges of block J on the factored columns to its left
-    if ((e = launch_getrf_laswp(g, J0, J1, 0, J0, cs)) != cudaSuccess) break;
+    if ((e = launch_getrf_laswp(g, J0, J1, 0, J0, cs, 0, pbuf[0])) != cudaSuccess) break;
     ++nl;
     if (J1 >= n) break;
     const int64_t J2 = J1 + NB < g.mn ? J1 + NB : (J1 < g.mn ? g.mn : n);
@@ -363,7 +376,8 @@ int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const do
   retain_pool_memory();
   // laswp (lu.py:61-65) with the recorded pivots, as row interchanges of B
   void* ws = nullptr;
-  cudaError_t e = cudaMallocAsync(&ws, sizeof(long long) * (size_t)n, s);
+  const size_t swb = ((sizeof(long long) * (size_t)n + 255) / 256) * 256;
+  cudaError_t e = cudaMallocAsync(&ws, swb + kPermBufBytes, s);
   if (e != cudaSuccess) return fail(e, "rgetrs workspace");
   std::vector<long long> sw((size_t)n);
   for (int64_t k = 0; k < n; ++k) sw[(size_t)k] = ipiv[k] - 1;
@@ -373,10 +387,14 @@ int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const do
   g.m = n; g.n = nrhs; g.mn = n; g.lda = ldb;
   g.a_hi = b_hi; g.a_lo = b_lo;
   g.swap = static_cast<long long*>(ws);
+  PermBuf pb;
+  pb.rows = reinterpret_cast<long long*>(static_cast<char*>(ws) + swb);
+  pb.src = reinterpret_cast<int*>(static_cast<char*>(ws) + swb + 512 * 8);
+  pb.n = reinterpret_cast<int*>(static_cast<char*>(ws) + swb + 512 * 12);
   int r = DDB_OK;
   const bool notr = upflag(trans) == 'N';
   if (e == cudaSuccess && notr) {
-    e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 0);
+    e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 0, pb);
     if (e == cudaSuccess)
       r = ddb_rtrsm('L', 'L', 'N', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
     if (e == cudaSuccess && r == DDB_OK)
@@ -385,7 +403,7 @@ int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const do
     r = ddb_rtrsm('L', 'U', 'T', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
     if (r == DDB_OK)
       r = ddb_rtrsm('L', 'L', 'T', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
-    if (r == DDB_OK) e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 1);
+    if (r == DDB_OK) e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 1, pb);
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   if (r != DDB_OK) return r;

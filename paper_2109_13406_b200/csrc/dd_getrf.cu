@@ -442,63 +442,79 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   }
 }
 
-// Apply the interchanges of steps [j0, j1) in order to columns [c0, c1).
-// The composed permutation of the touched rows (at most 2 (j1 - j0)) is
-// formed once per CTA in shared memory; each column is then one gather and
-// one scatter with independent loads.
-constexpr int kSwapMax = 128;    // touched rows of <= 64 steps (launch_getrf_laswp chunks)
+// Row interchanges (laswp, lu.py:61-65) of steps [j0, j1), in order (or in
+// reverse), on columns [c0, c1).  getrf_perm_kernel (one warp) composes them
+// into a permutation of the touched rows -- the step rows [j0, j1) at fixed
+// slots, the other targets appended -- and getrf_apply_perm_kernel moves the
+// touched entries of a group of columns through shared memory: every load is
+// independent, then every store.
+constexpr int kPermSteps = 256;                 // steps per composition
+constexpr int kPermMax = 2 * kPermSteps;        // touched rows
+
+__global__ void __launch_bounds__(32)
+getrf_perm_kernel(GetrfArgs g, int64_t j0, int64_t j1, int reverse, PermBuf pb) {
+  const int lane = threadIdx.x;
+  const int nb = (int)(j1 - j0);
+  for (int t = lane; t < nb; t += 32) {
+    pb.rows[t] = j0 + t;
+    pb.src[t] = t;
+  }
+  __syncwarp();
+  int nt = nb;
+  auto find = [&](long long r) {
+    if (r >= j0 && r < j1) return (int)(r - j0);
+    for (int base = nb; base < nt; base += 32) {
+      const int t = base + lane;
+      const unsigned hit = __ballot_sync(0xffffffffu, t < nt && pb.rows[t] == r);
+      if (hit) return base + __ffs(hit) - 1;
+    }
+    if (lane == 0) {
+      pb.rows[nt] = r;
+      pb.src[nt] = nt;
+    }
+    __syncwarp();
+    return nt++;
+  };
+  for (int64_t s = j0; s < j1; ++s) {
+    const int64_t j = reverse ? j0 + j1 - 1 - s : s;
+    const long long p = g.swap[j];
+    if (p == j) continue;
+    const int a = find(j), b = find(p);
+    if (lane == 0) {
+      const int t = pb.src[a];
+      pb.src[a] = pb.src[b];
+      pb.src[b] = t;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) *pb.n = nt;
+}
+
+constexpr int kPermCols = 8;                    // columns per CTA
 
 __global__ void __launch_bounds__(256)
-getrf_laswp_kernel(GetrfArgs g, int64_t j0, int64_t j1, int64_t c0, int64_t c1, int reverse) {
-  __shared__ long long rows_s[kSwapMax];   // touched rows
-  __shared__ int src_s[kSwapMax];          // final content of rows_s[t] = old rows_s[src_s[t]]
-  __shared__ int nt_s;
-  if (threadIdx.x < 32) {                  // warp 0 composes the interchanges
-    const int lane = threadIdx.x;
-    int nt = 0;
-    auto find = [&](long long r) {          // index of row r in rows_s, appended if new
-      for (int base = 0; base < nt; base += 32) {
-        const int t = base + lane;
-        const unsigned hit = __ballot_sync(0xffffffffu, t < nt && rows_s[t] == r);
-        if (hit) return base + __ffs(hit) - 1;
-      }
-      if (lane == 0) {
-        rows_s[nt] = r;
-        src_s[nt] = nt;
-      }
-      __syncwarp();
-      return nt++;
-    };
-    for (int64_t s = j0; s < j1; ++s) {
-      const int64_t j = reverse ? j0 + j1 - 1 - s : s;
-      const long long p = g.swap[j];
-      if (p == j) continue;
-      const int a = find(j), b = find(p);
-      if (lane == 0) {
-        const int t = src_s[a];
-        src_s[a] = src_s[b];
-        src_s[b] = t;
-      }
-      __syncwarp();
+getrf_apply_perm_kernel(GetrfArgs g, PermBuf pb, int64_t c0, int64_t c1) {
+  extern __shared__ double sm[];
+  const int nt = *pb.n;
+  double* vh = sm;                              // [kPermCols][nt]
+  double* vl = sm + (size_t)kPermCols * nt;
+  for (int64_t cb = c0 + (int64_t)blockIdx.x * kPermCols; cb < c1;
+       cb += (int64_t)gridDim.x * kPermCols) {
+    const int ncol = (int)(c1 - cb < kPermCols ? c1 - cb : kPermCols);
+    for (int e = threadIdx.x; e < nt * ncol; e += blockDim.x) {
+      const int t = e % nt, c = e / nt;
+      const int64_t x = pb.rows[pb.src[t]] + (cb + c) * g.lda;
+      vh[c * nt + t] = g.a_hi[x];
+      vl[c * nt + t] = g.a_lo[x];
     }
-    if (lane == 0) nt_s = nt;
-  }
-  __syncthreads();
-  const int nt = nt_s;
-  if (nt == 0) return;
-  for (int64_t c = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < c1;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    double* ah = g.a_hi + c * g.lda;
-    double* al = g.a_lo + c * g.lda;
-    double gh[kSwapMax], gl[kSwapMax];   // gather everything, then scatter
-    for (int t = 0; t < nt; ++t) {
-      gh[t] = ah[rows_s[src_s[t]]];
-      gl[t] = al[rows_s[src_s[t]]];
+    __syncthreads();
+    for (int e = threadIdx.x; e < nt * ncol; e += blockDim.x) {
+      const int t = e % nt, c = e / nt;
+      const int64_t x = pb.rows[t] + (cb + c) * g.lda;
+      g.a_hi[x] = vh[c * nt + t];
+      g.a_lo[x] = vl[c * nt + t];
     }
-    for (int t = 0; t < nt; ++t) {
-      ah[rows_s[t]] = gh[t];
-      al[rows_s[t]] = gl[t];
-    }
+    __syncthreads();
   }
 }
 
@@ -607,20 +623,30 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
 }
 
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
-                               cudaStream_t s, int reverse) {
-  if (c1 <= c0) return cudaSuccess;
-  int64_t grid = (c1 - c0 + 255) / 256;
+                               cudaStream_t s, int reverse, const PermBuf& pb) {
+  if (c1 <= c0 || j1 <= j0) return cudaSuccess;
+  static thread_local int attr_dev = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr_dev != dev) {
+    cudaFuncSetAttribute(getrf_apply_perm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * sizeof(double) * kPermCols * kPermMax));
+    attr_dev = dev;
+  }
+  int64_t grid = (c1 - c0 + kPermCols - 1) / kPermCols;
   if (grid > 148 * 8) grid = 148 * 8;
-  const int64_t step = kSwapMax / 2;                     // <= 64 steps per launch, in order
-  for (int64_t t = j0; t < j1; t += step) {
-    int64_t a = t, b = t + step < j1 ? t + step : j1;
+  for (int64_t t = j0; t < j1; t += kPermSteps) {        // compositions in order
+    int64_t a = t, b = t + kPermSteps < j1 ? t + kPermSteps : j1;
     if (reverse) {                                       // chunks from the end
       b = j1 - (t - j0);
-      a = b - step > j0 ? b - step : j0;
+      a = b - kPermSteps > j0 ? b - kPermSteps : j0;
     }
-    getrf_laswp_kernel<<<(unsigned)grid, 256, 0, s>>>(g, a, b, c0, c1, reverse);
+    getrf_perm_kernel<<<1, 32, 0, s>>>(g, a, b, reverse, pb);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    const size_t smem = 2 * sizeof(double) * kPermCols * (size_t)(2 * (b - a));
+    getrf_apply_perm_kernel<<<(unsigned)grid, 256, smem, s>>>(g, pb, c0, c1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

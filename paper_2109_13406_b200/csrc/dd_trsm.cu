@@ -165,9 +165,12 @@ trsm_coef_kernel(TrsmArgs t, const double* __restrict__ ah, const double* __rest
   }
 }
 
-// Diagonal block [r0, r1) of the forward recurrence, one thread per vector;
-// the block of T in shared memory.
-__global__ void __launch_bounds__(128)
+// Diagonal block [r0, r0 + nb) of the forward recurrence (nb <= 64), one
+// warp per vector, lane t holding rows t and t + 32 of the block.  Step s:
+// the running value of row s is broadcast, finished (fin_s) and stored, and
+// every later row subtracts its term -- per element the terms arrive in
+// production order.  The block of T sits in shared memory.
+__global__ void __launch_bounds__(256)
 trsm_block_kernel(TrsmArgs t, int64_t r0, int nb) {
   extern __shared__ double sm[];
   double* th = sm;
@@ -180,17 +183,29 @@ trsm_block_kernel(TrsmArgs t, int64_t r0, int nb) {
     }
   }
   __syncthreads();
-  const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= t.q) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (v >= t.q) return;                      // whole warps
   double* wh = t.w_hi + v * t.ldw + r0;
   double* wl = t.w_lo + v * t.ldw + r0;
+  const int ra = lane, rb = lane + 32;
+  dd acc_a{0.0, 0.0}, acc_b{0.0, 0.0};
+  if (ra < nb) acc_a = dd{wh[ra], wl[ra]};
+  if (rb < nb) acc_b = dd{wh[rb], wl[rb]};
   for (int s = 0; s < nb; ++s) {
-    dd acc{wh[s], wl[s]};
-    for (int c = 0; c < s; ++c)
-      acc = add2_chk(acc, negd(mul2_chk(dd{th[s + c * nb], tl[s + c * nb]}, dd{wh[c], wl[c]})));
-    const dd x = trsm_fin(t, r0 + s, acc);
-    wh[s] = x.h;
-    wl[s] = x.l;
+    const dd own = s < 32 ? acc_a : acc_b;
+    dd val;
+    val.h = __shfl_sync(0xffffffffu, own.h, s & 31);
+    val.l = __shfl_sync(0xffffffffu, own.l, s & 31);
+    const dd x = trsm_fin(t, r0 + s, val);
+    if (lane == (s & 31)) {
+      wh[s] = x.h;
+      wl[s] = x.l;
+    }
+    if (ra > s && ra < nb)
+      acc_a = add2_chk(acc_a, negd(mul2_chk(dd{th[ra + s * nb], tl[ra + s * nb]}, x)));
+    if (rb > s && rb < nb)
+      acc_b = add2_chk(acc_b, negd(mul2_chk(dd{th[rb + s * nb], tl[rb + s * nb]}, x)));
   }
 }
 
@@ -246,7 +261,7 @@ cudaError_t launch_trsm_block(const TrsmArgs& t, int64_t r0, int nb, cudaStream_
     cudaFuncSetAttribute(trsm_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr_dev = dev;
   }
-  trsm_block_kernel<<<(unsigned)((t.q + 127) / 128), 128, smem, s>>>(t, r0, nb);
+  trsm_block_kernel<<<(unsigned)((t.q + 7) / 8), 256, smem, s>>>(t, r0, nb);
   return cudaGetLastError();
 }
 

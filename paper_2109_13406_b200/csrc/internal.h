@@ -136,6 +136,12 @@ cudaError_t launch_trsm_block(const TrsmArgs& t, int64_t r0, int nb, cudaStream_
 cudaError_t launch_trsm_rev(const TrsmArgs& t, cudaStream_t s);
 
 // LU with partial pivoting (dd_getrf.cu)
+struct PermBuf {                // a composed row interchange (laswp)
+  long long* rows;              // touched rows (512)
+  int* src;                     // row t receives the old content of rows[src[t]]
+  int* n;                       // number of touched rows
+};
+
 struct GetrfArgs {
   int64_t m, n, mn, lda;
   double *a_hi, *a_lo;
@@ -151,8 +157,9 @@ struct GetrfArgs {
 
 int getrf_max_panel_ctas();
 cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStream_t s);
+constexpr int kPermBufBytes = 512 * (8 + 4) + 64;     // one PermBuf's storage
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
-                               cudaStream_t s, int reverse = 0);
+                               cudaStream_t s, int reverse, const PermBuf& pb);
 cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
                               cudaStream_t s);
 
