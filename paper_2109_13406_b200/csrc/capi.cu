@@ -318,33 +318,59 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(ev0, s);             // allocations ready
     if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev0, 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(A.p, a_hi, sizeof(double) * sa, cudaMemcpyHostToDevice, h2d);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(A.p + sa, a_lo, sizeof(double) * sa, cudaMemcpyHostToDevice, h2d);
+    // Block 0 also streams k in panels, so that its first GEMM waits only for
+    // the first panel of op(A) (the rest of A arrives while it runs): beta
+    // applies to the first panel, 1 to the others -- for transa = 'N' the
+    // reference's own axpy order (exact mode stays bitwise), for 'T' only in
+    // the fast modes.  Later blocks find A resident and run full depth.
     const int64_t step = ((n + nblk - 1) / nblk + 63) / 64 * 64;
+    const int kch0 = (k >= 4096 && (na || mode != MODE_EXACT)) ? 4 : 1;
+    auto h2d_2d = [&](double* dst, const double* src, int64_t ld, int64_t rows, int64_t cols) {
+      return cudaMemcpy2DAsync(dst, sizeof(double) * ld, src, sizeof(double) * ld,
+                               sizeof(double) * rows, cols, cudaMemcpyHostToDevice, h2d);
+    };
     for (int64_t j0 = 0; j0 < n && e == cudaSuccess && rc == DDB_OK; j0 += step) {
       const int64_t j1 = j0 + step < n ? j0 + step : n, w = j1 - j0;
-      // op(B)(:, j0:j1): columns j0.. of B ('N') or rows j0.. of B ('T')
-      for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl) {
-        const double* src = pl ? b_lo : b_hi;
-        double* dst = B.p + pl * sb;
-        if (nb)
-          e = cudaMemcpyAsync(dst + j0 * ldb, src + j0 * ldb,
-                              sizeof(double) * (size_t)span(k, w, ldb), cudaMemcpyHostToDevice, h2d);
-        else
-          e = cudaMemcpy2DAsync(dst + j0, sizeof(double) * ldb, src + j0, sizeof(double) * ldb,
-                                sizeof(double) * w, k, cudaMemcpyHostToDevice, h2d);
-        if (e == cudaSuccess && read_c)
-          e = cudaMemcpyAsync(C.p + pl * sc + j0 * ldc, (pl ? c_lo : c_hi) + j0 * ldc,
-                              sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyHostToDevice, h2d);
+      const int kch = j0 == 0 ? kch0 : 1;
+      for (int c = 0; c < kch && e == cudaSuccess && rc == DDB_OK; ++c) {
+        const int64_t l0 = c == 0 ? 0 : (k * c / kch) / 64 * 64;
+        const int64_t l1 = c + 1 == kch ? k : (k * (c + 1) / kch) / 64 * 64, kc = l1 - l0;
+        for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl) {
+          const double* asrc = pl ? a_lo : a_hi;
+          const double* bsrc = pl ? b_lo : b_hi;
+          double* adst = A.p + pl * sa;
+          double* bdst = B.p + pl * sb;
+          if (j0 == 0)            // op(A)(:, l0:l1): columns of A ('N') or rows ('T')
+            e = na ? cudaMemcpyAsync(adst + l0 * lda, asrc + l0 * lda,
+                                     sizeof(double) * (size_t)span(m, kc, lda),
+                                     cudaMemcpyHostToDevice, h2d)
+                   : h2d_2d(adst + l0, asrc + l0, lda, kc, m);
+          if (e != cudaSuccess) break;
+          // op(B)(l0:l1, j0:j1): rows / columns of B
+          if (kch == 1)
+            e = nb ? cudaMemcpyAsync(bdst + j0 * ldb, bsrc + j0 * ldb,
+                                     sizeof(double) * (size_t)span(k, w, ldb),
+                                     cudaMemcpyHostToDevice, h2d)
+                   : h2d_2d(bdst + j0, bsrc + j0, ldb, w, k);
+          else
+            e = nb ? h2d_2d(bdst + l0 + j0 * ldb, bsrc + l0 + j0 * ldb, ldb, kc, w)
+                   : h2d_2d(bdst + j0 + l0 * ldb, bsrc + j0 + l0 * ldb, ldb, w, kc);
+          if (e == cudaSuccess && read_c && c == 0)
+            e = cudaMemcpyAsync(C.p + pl * sc + j0 * ldc, (pl ? c_lo : c_hi) + j0 * ldc,
+                                sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyHostToDevice,
+                                h2d);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in, h2d);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in, 0);
+        if (e != cudaSuccess) break;
+        const int64_t ao = na ? l0 * lda : l0;
+        const int64_t bo = nb ? l0 + j0 * ldb : j0 + l0 * ldb;
+        rc = ddb_rgemm(transa, transb, m, w, kc, alpha_hi, alpha_lo, A.p + ao, A.p + sa + ao, lda,
+                       B.p + bo, B.p + sb + bo, ldb, c == 0 ? beta_hi : 1.0,
+                       c == 0 ? beta_lo : 0.0, C.p + j0 * ldc, C.p + sc + j0 * ldc, ldc, mode,
+                       stream);
       }
-      if (e == cudaSuccess) e = cudaEventRecord(ev_in, h2d);
-      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in, 0);
-      if (e != cudaSuccess) break;
-      const double* bh = B.p + (nb ? j0 * ldb : j0);
-      const double* bl = B.p + sb + (nb ? j0 * ldb : j0);
-      rc = ddb_rgemm(transa, transb, m, w, k, alpha_hi, alpha_lo, A.p, A.p + sa, lda, bh, bl, ldb,
-                     beta_hi, beta_lo, C.p + j0 * ldc, C.p + sc + j0 * ldc, ldc, mode, stream);
-      if (rc != DDB_OK) break;
+      if (rc != DDB_OK || e != cudaSuccess) break;
       e = cudaEventRecord(ev_out, s);
       if (e == cudaSuccess) e = cudaStreamWaitEvent(d2h, ev_out, 0);
       for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl)
