@@ -139,3 +139,51 @@ def test_rgetrs_exact_matches_oracle_multiblock(trans):
     xh, xl = bh.copy(), bl.copy()
     assert oracle.rgetrs(trans, n, nrhs, oh, ol, n, oipiv, xh, xl, n) == 0
     assert bits_equal(b.store[0].cpu().numpy(), xh) and bits_equal(b.store[1].cpu().numpy(), xl)
+
+
+def test_rgetrf_tall_panel_global_fallback():
+    """m = 30000 rows: more than the shared-memory panel kernel stages per CTA
+    (192 x 148), so the panel runs in the global-memory kernel; bitwise vs
+    the oracle."""
+    m, n = 30000, 70
+    hi, lo = random_dd(m, n, m, 12, 1)
+    ipiv, info, gh, gl = run(m, n, m, hi, lo, "exact")
+    oh, ol = hi.copy(), lo.copy()
+    _, oipiv, oinfo = oracle.rgetrf(m, n, oh, ol, m)
+    assert ipiv == oipiv and info == oinfo
+    assert bits_equal(gh, oh) and bits_equal(gl, ol)
+
+
+def test_block_widths_from_env_bitwise():
+    """DDB_GETRF_NB / DDB_TRSM_NB (read once per process): ragged outer
+    blocks (100 = 64 + 36 inner) stay bit-identical to the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, torch, sys
+sys.path.insert(0, ".")
+from oracle import oracle
+from paper_2109_13406_b200 import DeviceMatrix, Rgetrf, Rtrsm
+from paper_2109_13406_b200.synth import random_dd
+n = 333
+hi, lo = random_dd(n, n, n, 5, 1)
+a = DeviceMatrix(n, n, "dd", n, store=(torch.from_numpy(hi.copy()).cuda(), torch.from_numpy(lo.copy()).cuda()))
+ipiv, info = Rgetrf(n, n, a, n, mode="exact")
+oh, ol = hi.copy(), lo.copy()
+_, oipiv, _ = oracle.rgetrf(n, n, oh, ol, n)
+assert list(ipiv) == oipiv
+assert np.array_equal(a.store[0].cpu().numpy(), oh) and np.array_equal(a.store[1].cpu().numpy(), ol)
+bh, bl = random_dd(n, 9, n, 5, 2)
+b = DeviceMatrix(n, 9, "dd", n, store=(torch.from_numpy(bh.copy()).cuda(), torch.from_numpy(bl.copy()).cuda()))
+Rtrsm("L", "U", "N", "N", n, 9, 1.5, a, n, b, n, mode="exact")
+xh, xl = bh.copy(), bl.copy()
+assert oracle.rtrsm("L", "U", "N", "N", n, 9, (1.5, 0.0), oh, ol, n, xh, xl, n) == 0
+assert np.array_equal(b.store[0].cpu().numpy(), xh) and np.array_equal(b.store[1].cpu().numpy(), xl)
+print("ok")
+'''
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, DDB_GETRF_NB="100", DDB_TRSM_NB="100")
+    out = subprocess.run([sys.executable, "-c", code], cwd=repo, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
