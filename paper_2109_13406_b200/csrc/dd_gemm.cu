@@ -21,6 +21,9 @@ cudaError_t launch_tiled_select(int, const GemmArgs&, const int*, const int*, co
 cudaError_t launch_tiled_f64(int, const GemmArgs&, const int*, const int*, const int*,
                              cudaStream_t);
 bool tma_eligible(const GemmArgs& g, int alg);
+cudaError_t launch_dd_transpose(const double* sh, const double* sl, int64_t lds, double* dh,
+                                double* dl, int64_t ldd, int64_t rows, int64_t cols,
+                                cudaStream_t s);
 cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,
                           const int* flag, cudaStream_t s);
 cudaError_t launch_tiled_cert(int, const GemmArgs&, const int*, const int*, const int*,
@@ -87,6 +90,10 @@ int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk) {
   double best = eff(tiles);
   int best_s = 1;
   int64_t best_chunk = g.k;
+  // a split costs partial sums (16 bytes x splits per element, written and
+  // reduced) and shorter k-loops per tile: only worth it against a real
+  // tail (e.g. 2048^2 x 65536: 3.5 waves), not to polish a 97 % wave fill
+  if (best >= 0.95) return 1;
   for (int s = 2; s <= 16; ++s) {
     int64_t chunk = (g.k + s - 1) / s;
     chunk = ((chunk + 31) / 32) * 32;
@@ -144,6 +151,44 @@ cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const i
     const cudaError_t e = launch_tma_nn(g, alg, row_exp, col_exp, flag, s);
     if (e != cudaErrorNotSupported) return e;
     cudaGetLastError();
+  }
+  // Fast-mode Rsyrk through the TMA kernel: 'N' (C = A A^T) needs op(B) =
+  // A^T k-major, 'T' (C = A^T A) needs op(A) = A^T m-major; one transposed
+  // copy of A (16 n k bytes, even leading dimension) makes it an NN call with
+  // the triangle skip.  Same per-element arithmetic as the tiled kernel.
+  if (cfg == 0 && g.syrk != 0 && (alg == ALG_CERT || alg == ALG_TWOSUM) &&
+      std::getenv("DDB_NO_TMA_SYRK") == nullptr) {
+    const int64_t n = g.m, k = g.k;
+    const bool tn = g.ta == 0;                       // trans 'N'
+    const int64_t ldt = tn ? ((k + 1) & ~int64_t(1)) : ((n + 1) & ~int64_t(1));
+    const int64_t cols = tn ? n : k;                 // of the transposed copy
+    double* tbuf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&tbuf), sizeof(double) * 2 * ldt * cols, s) ==
+        cudaSuccess) {
+      GemmArgs g2 = g;
+      double* th = tbuf;
+      double* tl = tbuf + ldt * cols;
+      cudaError_t e;
+      if (tn) {   // A (n x k) -> A^T (k x n): the B operand
+        e = launch_dd_transpose(g.a_hi, g.a_lo, g.lda, th, tl, ldt, n, k, s);
+        g2.tb = 0; g2.b_hi = th; g2.b_lo = tl; g2.ldb = ldt;
+      } else {    // A (k x n) -> A^T (n x k): the A operand
+        e = launch_dd_transpose(g.a_hi, g.a_lo, g.lda, th, tl, ldt, k, n, s);
+        g2.ta = 0; g2.a_hi = th; g2.a_lo = tl; g2.lda = ldt;
+      }
+      if (e == cudaSuccess && tma_eligible(g2, alg)) {
+        ++*nlaunch;
+        e = launch_tma_nn(g2, alg, row_exp, col_exp, flag, s);
+        cudaFreeAsync(tbuf, s);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+      } else {
+        cudaFreeAsync(tbuf, s);
+        if (e != cudaSuccess) return e;
+      }
+    } else {
+      cudaGetLastError();
+    }
   }
   switch (alg) {
     case ALG_TWOSUM: return launch_tiled_twosum(cfg, g, row_exp, col_exp, flag, s);

@@ -76,7 +76,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 // work on the same wave of tiles at nearly the same k (the wave's A / B panel
 // k-slices are read from DRAM once and shared through L2); the producer runs
 // ahead across unit boundaries, overlapping the epilogue with the next loads.
-template <int ALG>
+template <int ALG, int SYRK>
 __global__ void __launch_bounds__(NT, 1)
 dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                  const __grid_constant__ CUtensorMap mAl, const __grid_constant__ CUtensorMap mBh,
@@ -120,8 +120,22 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     ktiles = (int)((kend - kbeg + BK - 1) / BK);
   };
 
+  // Rsyrk (SYRK = 1 upper / 2 lower): units whose tile lies entirely in the
+  // other triangle are skipped by producer and consumers alike
+  auto skipped = [&](int u) {
+    if (SYRK == 0) return false;
+    int64_t i0, j0, kb;
+    int kt;
+    unit_origin(u, i0, j0, kb, kt);
+    return SYRK == 1 ? i0 > j0 + BN - 1 : i0 + BM - 1 < j0;
+  };
+  auto next_unit = [&](int u) {   // first unit >= u in this CTA's stride that is not skipped
+    while (u < units && skipped(u)) u += gridDim.x;
+    return u;
+  };
+
   // ---- producer state (thread 0): walks (unit, k-tile) items ahead ----
-  int p_unit = blockIdx.x, p_kt = 0, p_ktiles = 0;
+  int p_unit = next_unit(blockIdx.x), p_kt = 0, p_ktiles = 0;
   int64_t p_i0 = 0, p_j0 = 0, p_kbeg = 0;
   uint32_t p_item = 0;
   if (tid == 0 && p_unit < units) unit_origin(p_unit, p_i0, p_j0, p_kbeg, p_ktiles);
@@ -139,7 +153,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     ++p_item;
     if (++p_kt == p_ktiles) {
       p_kt = 0;
-      p_unit += gridDim.x;
+      p_unit = next_unit(p_unit + gridDim.x);
       if (p_unit < units) unit_origin(p_unit, p_i0, p_j0, p_kbeg, p_ktiles);
     }
     return true;
@@ -149,7 +163,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 
   const int tx = tid % 16, ty = tid / 16;
   uint32_t c_item = 0;
-  for (int u = blockIdx.x; u < units; u += gridDim.x) {
+  for (int u = next_unit(blockIdx.x); u < units; u = next_unit(u + gridDim.x)) {
     int64_t i0, j0, kbeg;
     int ktiles;
     unit_origin(u, i0, j0, kbeg, ktiles);
@@ -240,6 +254,8 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
         const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
         const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
         if (gi >= g.m || gj >= g.n) continue;
+        if (SYRK == 1 && gi > gj) continue;   // the uplo triangle only (level23.py:245-270)
+        if (SYRK == 2 && gi < gj) continue;
         double sx, ex;
         const double hv = ALG == ALG_CERT ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
         two_sum(hv, L[a][b], sx, ex);
@@ -293,10 +309,44 @@ static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 }  // namespace tma
 
+// dst (cols x rows, ld ldd) = src (rows x cols, ld lds)^T, both planes: the
+// operand of a TMA Rsyrk that must be k-major / m-major (launch_tiled)
+__global__ void __launch_bounds__(256)
+dd_transpose_kernel(const double* __restrict__ sh, const double* __restrict__ sl, int64_t lds,
+                    double* __restrict__ dh, double* __restrict__ dl, int64_t ldd, int64_t rows,
+                    int64_t cols) {
+  __shared__ double th[32][33], tl[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int64_t r = r0 + threadIdx.x, c = c0 + y;
+    if (r < rows && c < cols) {
+      th[y][threadIdx.x] = sh[r + c * lds];
+      tl[y][threadIdx.x] = sl[r + c * lds];
+    }
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int64_t c = c0 + threadIdx.x, r = r0 + y;
+    if (r < rows && c < cols) {
+      dh[c + r * ldd] = th[threadIdx.x][y];
+      dl[c + r * ldd] = tl[threadIdx.x][y];
+    }
+  }
+}
+
+cudaError_t launch_dd_transpose(const double* sh, const double* sl, int64_t lds, double* dh,
+                                double* dl, int64_t ldd, int64_t rows, int64_t cols,
+                                cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
+  dd_transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(sh, sl, lds, dh, dl, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
 bool tma_eligible(const GemmArgs& g, int alg) {
   if (std::getenv("DDB_NO_TMA") != nullptr) return false;
   if (!(alg == ALG_CERT || alg == ALG_TWOSUM)) return false;
-  if (g.syrk != 0 || g.ta != 0 || g.tb != 0 || g.f64) return false;
+  if (g.ta != 0 || g.tb != 0 || g.f64) return false;   // Rsyrk arrives here in NN form
   if ((g.lda & 1) || (g.ldb & 1)) return false;
   if (!tma::aligned16(g.a_hi) || !tma::aligned16(g.a_lo) || !tma::aligned16(g.b_hi) ||
       !tma::aligned16(g.b_lo))
@@ -321,7 +371,12 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
     return cudaErrorNotSupported;
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
-  auto kern = alg == ALG_CERT ? dd_tma_nn_kernel<ALG_CERT> : dd_tma_nn_kernel<ALG_TWOSUM>;
+  auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
+  auto kern = alg == ALG_CERT
+                  ? pick(dd_tma_nn_kernel<ALG_CERT, 0>, dd_tma_nn_kernel<ALG_CERT, 1>,
+                         dd_tma_nn_kernel<ALG_CERT, 2>)
+                  : pick(dd_tma_nn_kernel<ALG_TWOSUM, 0>, dd_tma_nn_kernel<ALG_TWOSUM, 1>,
+                         dd_tma_nn_kernel<ALG_TWOSUM, 2>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
