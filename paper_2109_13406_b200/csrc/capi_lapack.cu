@@ -199,7 +199,7 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
                           2 * (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) +
                           64 + sizeof(double) * (4 * (size_t)G + 4) * (size_t)nb + 64 +
-                          2 * (size_t)kPermBufBytes + 64;
+                          5 * (size_t)kPermBufBytes + 64;
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "rgetrf workspace");
@@ -215,12 +215,15 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   g.rowbuf = reinterpret_cast<double*>(
       (reinterpret_cast<uintptr_t>(g.part_nan + 2 * G) + 63) & ~static_cast<uintptr_t>(63));
   // composed interchanges: one buffer per stream that applies them
-  PermBuf pbuf[2];
+  // [0], [1]: scratch for the panel stream / the caller's stream; [2]: the
+  // current inner panel's; [3], [4]: the outer blocks' (by parity: block J's
+  // is read by rest(J) on the caller's stream while J+1's is formed)
+  PermBuf pbuf[5];
   {
     char* pp = reinterpret_cast<char*>(
         (reinterpret_cast<uintptr_t>(g.rowbuf + (4 * (size_t)G + 4) * nb) + 63) &
         ~static_cast<uintptr_t>(63));
-    for (int i = 0; i < 2; ++i, pp += kPermBufBytes) {
+    for (int i = 0; i < 5; ++i, pp += kPermBufBytes) {
       pbuf[i].rows = reinterpret_cast<long long*>(pp);
       pbuf[i].src = reinterpret_cast<int*>(pp + 512 * 8);
       pbuf[i].n = reinterpret_cast<int*>(pp + 512 * 12);
@@ -249,10 +252,19 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   };
   // block J's pending work on columns [c0, c1): interchanges, U12 (blocked
   // by the inner width), trailing update of rows >= J1
-  auto apply_block = [&](int64_t J0, int64_t J1, int64_t c0, int64_t c1, cudaStream_t st) -> int {
-    if (c1 <= c0) return DDB_OK;
-    cudaError_t er = launch_getrf_laswp(g, J0, J1, c0, c1, st, 0, pbuf[st == cs ? 0 : 1]);
+  // interchanges of steps [J0, J1) on columns [c0, c1): from a composition
+  // formed once per block (pre) or composed here
+  auto swap_cols = [&](int64_t J0, int64_t J1, int64_t c0, int64_t c1, cudaStream_t st,
+                       const PermBuf* pre) -> cudaError_t {
+    if (c1 <= c0) return cudaSuccess;
     ++nl;
+    if (pre != nullptr) return launch_getrf_apply(g, *pre, J1 - J0, c0, c1, st);
+    return launch_getrf_laswp(g, J0, J1, c0, c1, st, 0, pbuf[st == cs ? 0 : 1]);
+  };
+  auto apply_block = [&](int64_t J0, int64_t J1, int64_t c0, int64_t c1, cudaStream_t st,
+                         const PermBuf* pre) -> int {
+    if (c1 <= c0) return DDB_OK;
+    cudaError_t er = swap_cols(J0, J1, c0, c1, st, pre);
     if (er != cudaSuccess) return fail(er, "rgetrf laswp");
     for (int64_t i0 = J0; i0 < J1; i0 += ib) {
       const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
@@ -270,10 +282,11 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
       const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
       cudaError_t er = launch_getrf_panel(g, i0, (int)(i1 - i0), cs);
       ++nl;
-      if (er == cudaSuccess) { er = launch_getrf_laswp(g, i0, i1, J0, i0, cs, 0, pbuf[0]); ++nl; }
+      if (er == cudaSuccess) { er = launch_getrf_compose(g, i0, i1, 0, pbuf[2], cs); ++nl; }
+      if (er == cudaSuccess) er = swap_cols(i0, i1, J0, i0, cs, &pbuf[2]);
       if (er != cudaSuccess) return fail(er, "rgetrf panel");
       if (i1 < J1) {
-        const int r = apply_block(i0, i1, i1, J1, cs);
+        const int r = apply_block(i0, i1, i1, J1, cs, &pbuf[2]);
         if (r != DDB_OK) return r;
       }
     }
@@ -285,9 +298,15 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   bool have_rest = false;
   for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
     const int64_t J1 = J0 + NB < g.mn ? J0 + NB : g.mn;
-    // interchanges of block J on the factored columns to its left
-    if ((e = launch_getrf_laswp(g, J0, J1, 0, J0, cs, 0, pbuf[0])) != cudaSuccess) break;
-    ++nl;
+    // block J's interchanges, composed once; first on the factored columns
+    // to its left
+    const PermBuf* pre = nullptr;
+    if (J1 - J0 <= kPermStepsMax) {
+      pre = &pbuf[3 + (int)((J0 / NB) & 1)];
+      if ((e = launch_getrf_compose(g, J0, J1, 0, *pre, cs)) != cudaSuccess) break;
+      ++nl;
+    }
+    if ((e = swap_cols(J0, J1, 0, J0, cs, pre)) != cudaSuccess) break;
     if (J1 >= n) break;
     const int64_t J2 = J1 + NB < g.mn ? J1 + NB : (J1 < g.mn ? g.mn : n);
     e = cudaEventRecord(ev_a, cs);                         // panel J done
@@ -295,13 +314,13 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
     if (e != cudaSuccess) break;
     if (J2 < n) {
-      rc2 = apply_block(J0, J1, J2, n, s);                 // rest(J)
+      rc2 = apply_block(J0, J1, J2, n, s, pre);            // rest(J)
       if (rc2 != DDB_OK) break;
       e = cudaEventRecord(ev_b, s);
       have_rest = true;
       if (e != cudaSuccess) break;
     }
-    rc2 = apply_block(J0, J1, J1, J2, cs);                 // columns of block J+1
+    rc2 = apply_block(J0, J1, J1, J2, cs, pre);            // columns of block J+1
     if (rc2 != DDB_OK || J1 >= g.mn) break;
     rc2 = factor_outer(J1, J2 < g.mn ? J2 : g.mn);
   }

@@ -453,41 +453,58 @@ constexpr int kPermMax = 2 * kPermSteps;        // touched rows
 
 __global__ void __launch_bounds__(32)
 getrf_perm_kernel(GetrfArgs g, int64_t j0, int64_t j1, int reverse, PermBuf pb) {
-  const int lane = threadIdx.x;
+  // one thread composes (the steps are inherently sequential); the step rows
+  // [j0, j1) sit at fixed slots, other targets are found through a small
+  // open-addressing table in shared memory
+  constexpr int kHash = 1024;
+  __shared__ long long rows_s[kPermMax];
+  __shared__ int src_s[kPermMax];
+  __shared__ long long key_s[kHash];
+  __shared__ int slot_s[kHash];
+  __shared__ int nt_s;
   const int nb = (int)(j1 - j0);
-  for (int t = lane; t < nb; t += 32) {
-    pb.rows[t] = j0 + t;
-    pb.src[t] = t;
+  for (int t = threadIdx.x; t < kHash; t += blockDim.x) key_s[t] = -1;
+  for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+    rows_s[t] = j0 + t;
+    src_s[t] = t;
   }
   __syncwarp();
-  int nt = nb;
-  auto find = [&](long long r) {
-    if (r >= j0 && r < j1) return (int)(r - j0);
-    for (int base = nb; base < nt; base += 32) {
-      const int t = base + lane;
-      const unsigned hit = __ballot_sync(0xffffffffu, t < nt && pb.rows[t] == r);
-      if (hit) return base + __ffs(hit) - 1;
+  if (threadIdx.x == 0) {
+    int nt = nb;
+    auto find = [&](long long r) {
+      if (r >= j0 && r < j1) return (int)(r - j0);
+      unsigned h = (unsigned)(((unsigned long long)r * 0x9E3779B97F4A7C15ull) >> 54);   // 10 bits
+      while (true) {
+        const long long k = key_s[h];
+        if (k == r) return slot_s[h];
+        if (k < 0) {
+          key_s[h] = r;
+          slot_s[h] = nt;
+          rows_s[nt] = r;
+          src_s[nt] = nt;
+          return nt++;
+        }
+        h = (h + 1) & (kHash - 1);
+      }
+    };
+    for (int64_t s = j0; s < j1; ++s) {
+      const int64_t j = reverse ? j0 + j1 - 1 - s : s;
+      const long long p = g.swap[j];
+      if (p == j) continue;
+      const int a = find(j), b = find(p);
+      const int t = src_s[a];
+      src_s[a] = src_s[b];
+      src_s[b] = t;
     }
-    if (lane == 0) {
-      pb.rows[nt] = r;
-      pb.src[nt] = nt;
-    }
-    __syncwarp();
-    return nt++;
-  };
-  for (int64_t s = j0; s < j1; ++s) {
-    const int64_t j = reverse ? j0 + j1 - 1 - s : s;
-    const long long p = g.swap[j];
-    if (p == j) continue;
-    const int a = find(j), b = find(p);
-    if (lane == 0) {
-      const int t = pb.src[a];
-      pb.src[a] = pb.src[b];
-      pb.src[b] = t;
-    }
-    __syncwarp();
+    nt_s = nt;
   }
-  if (lane == 0) *pb.n = nt;
+  __syncwarp();
+  const int nt = nt_s;
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    pb.rows[t] = rows_s[t];
+    pb.src[t] = src_s[t];
+  }
+  if (threadIdx.x == 0) *pb.n = nt;
 }
 
 constexpr int kPermCols = 8;                    // columns per CTA
@@ -622,9 +639,15 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
                                      dim3(kPanelThreads), args, 0, s);
 }
 
-cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
-                               cudaStream_t s, int reverse, const PermBuf& pb) {
-  if (c1 <= c0 || j1 <= j0) return cudaSuccess;
+cudaError_t launch_getrf_compose(const GetrfArgs& g, int64_t j0, int64_t j1, int reverse,
+                                 const PermBuf& pb, cudaStream_t s) {
+  getrf_perm_kernel<<<1, 32, 0, s>>>(g, j0, j1, reverse, pb);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_getrf_apply(const GetrfArgs& g, const PermBuf& pb, int64_t nsteps, int64_t c0,
+                               int64_t c1, cudaStream_t s) {
+  if (c1 <= c0 || nsteps <= 0) return cudaSuccess;
   static thread_local int attr_dev = -1;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -635,18 +658,23 @@ cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64
   }
   int64_t grid = (c1 - c0 + kPermCols - 1) / kPermCols;
   if (grid > 148 * 8) grid = 148 * 8;
+  const size_t smem = 2 * sizeof(double) * kPermCols * (size_t)(2 * nsteps);
+  getrf_apply_perm_kernel<<<(unsigned)grid, 256, smem, s>>>(g, pb, c0, c1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
+                               cudaStream_t s, int reverse, const PermBuf& pb) {
+  if (c1 <= c0 || j1 <= j0) return cudaSuccess;
   for (int64_t t = j0; t < j1; t += kPermSteps) {        // compositions in order
     int64_t a = t, b = t + kPermSteps < j1 ? t + kPermSteps : j1;
     if (reverse) {                                       // chunks from the end
       b = j1 - (t - j0);
       a = b - kPermSteps > j0 ? b - kPermSteps : j0;
     }
-    getrf_perm_kernel<<<1, 32, 0, s>>>(g, a, b, reverse, pb);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_getrf_compose(g, a, b, reverse, pb, s);
+    if (e == cudaSuccess) e = launch_getrf_apply(g, pb, b - a, c0, c1, s);
     if (e != cudaSuccess) return e;
-    const size_t smem = 2 * sizeof(double) * kPermCols * (size_t)(2 * (b - a));
-    getrf_apply_perm_kernel<<<(unsigned)grid, 256, smem, s>>>(g, pb, c0, c1);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
   return cudaSuccess;
 }

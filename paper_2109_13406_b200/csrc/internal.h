@@ -160,6 +160,11 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
 constexpr int kPermBufBytes = 512 * (8 + 4) + 64;     // one PermBuf's storage
 cudaError_t launch_getrf_laswp(const GetrfArgs& g, int64_t j0, int64_t j1, int64_t c0, int64_t c1,
                                cudaStream_t s, int reverse, const PermBuf& pb);
+constexpr int kPermStepsMax = 256;                     // steps one composition may hold
+cudaError_t launch_getrf_compose(const GetrfArgs& g, int64_t j0, int64_t j1, int reverse,
+                                 const PermBuf& pb, cudaStream_t s);
+cudaError_t launch_getrf_apply(const GetrfArgs& g, const PermBuf& pb, int64_t nsteps, int64_t c0,
+                               int64_t c1, cudaStream_t s);
 cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
                               cudaStream_t s);
 
