@@ -195,6 +195,26 @@ int ddb_rsyrk_mgpu(char uplo, char trans, int64_t n, int64_t k,
                    double* c_hi, double* c_lo, int64_t ldc, int mode, int ndev,
                    const int* devices);
 
+/* The LAPACK consumers on the reference's binary64 ('f64') Matrix: one
+ * plane, the F64 backend's IEEE operations in the reference's order
+ * (bit-identical; no mode).  Arguments and returns as the dd versions. */
+int ddb_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
+              const double* a, int64_t lda, double* b, int64_t ldb, void* stream);
+int ddb_dtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                   double alpha, const double* a, int64_t lda, double* b, int64_t ldb,
+                   void* stream);
+int ddb_dgetrf(int64_t m, int64_t n, double* a, int64_t lda, int64_t* ipiv, int* info,
+               void* stream);
+int ddb_dgetrf_host(int64_t m, int64_t n, double* a, int64_t lda, int64_t* ipiv, int* info,
+                    void* stream);
+int ddb_dgetrs(char trans, int64_t n, int64_t nrhs, const double* a, int64_t lda,
+               const int64_t* ipiv, double* b, int64_t ldb, void* stream);
+int ddb_dgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a, int64_t lda,
+                    const int64_t* ipiv, double* b, int64_t ldb, void* stream);
+int ddb_dpotrf(char uplo, int64_t n, double* a, int64_t lda, int64_t nb, void* stream, int* info);
+int ddb_dpotrf_host(char uplo, int64_t n, double* a, int64_t lda, int64_t nb, void* stream,
+                    int* info);
+
 /* Argument checks alone (no device work): reference index or 0. */
 int ddb_rgemm_validate(char transa, char transb, int64_t m, int64_t n, int64_t k,
                        int64_t lda, int64_t ldb, int64_t ldc);

@@ -924,3 +924,170 @@ int oracle_rgetrs(char trans, int64_t n, int64_t nrhs, const double *Ah, const d
     }
     return 0;
 }
+
+/* ---- the LAPACK consumers on the F64 backend (elem.py:149-197): numpy
+ * binary64 + - * /, Python float scalars, math.sqrt -- same loop orders as
+ * the dd restatements above ---- */
+int oracle_dpotrf(char uplo, int64_t n, double *A, int64_t lda, int64_t *info) {
+    int rc = oracle_potrf_validate(uplo, n, lda);
+    if (rc) return rc;
+    *info = 0;
+    const int upper = upflag(uplo) == 'U';
+#define AT(i, j) A[(i) + (j) * lda]
+    for (int64_t j = 0; j < n; ++j) {
+        double dot = 0.0;
+        for (int64_t l = 0; l < j; ++l) {
+            double h = upper ? AT(l, j) : AT(j, l);
+            dot = dot + h * h;
+        }
+        double ajj = AT(j, j) - dot;
+        if (isnan(ajj) || ajj <= 0.0) { AT(j, j) = ajj; *info = j + 1; return 0; }
+        ajj = sqrt(ajj);
+        AT(j, j) = ajj;
+        if (j == n - 1) break;
+        double rec = 1.0 / ajj;
+        for (int64_t q = j + 1; q < n; ++q) {
+            if (upper) {
+                double temp = 0.0;
+                for (int64_t l = 0; l < j; ++l) temp = temp + AT(l, q) * AT(l, j);
+                AT(j, q) = rec * (AT(j, q) + (-temp));
+            } else {
+                double tail = AT(q, j);
+                for (int64_t l = 0; l < j; ++l) tail = tail + (-AT(j, l)) * AT(q, l);
+                AT(q, j) = rec * tail;
+            }
+        }
+    }
+#undef AT
+    return 0;
+}
+
+int oracle_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n, double alpha,
+                 const double *A, int64_t lda, double *B, int64_t ldb) {
+    int rc = oracle_trsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
+    if (rc) return rc;
+    if (m == 0 || n == 0) return 0;
+    const int left = upflag(side) == 'L', up = upflag(uplo) == 'U';
+    const int notr = upflag(transa) == 'N', nounit = upflag(diag) == 'N';
+#define A_(i, j) A[(i) + (j) * lda]
+#define B_(i, j) B[(i) + (j) * ldb]
+    if (alpha == 0.0) {
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < m; ++i) B_(i, j) = 0.0;
+        return 0;
+    }
+    const int alpha_one = alpha == 1.0;
+    if (left && notr) {
+        for (int64_t j = 0; j < n; ++j) {
+            if (!alpha_one)
+                for (int64_t i = 0; i < m; ++i) B_(i, j) = alpha * B_(i, j);
+            for (int64_t s = 0; s < m; ++s) {
+                int64_t kk = up ? m - 1 - s : s;
+                if (nounit) B_(kk, j) = B_(kk, j) / A_(kk, kk);
+                int64_t r0 = up ? 0 : kk + 1, r1 = up ? kk : m;
+                double x = B_(kk, j);
+                for (int64_t i = r0; i < r1; ++i) B_(i, j) = B_(i, j) - A_(i, kk) * x;
+            }
+        }
+    } else if (left) {
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t s = 0; s < m; ++s) {
+                int64_t i = up ? s : m - 1 - s;
+                double temp = alpha * B_(i, j);
+                int64_t k0 = up ? 0 : i + 1, k1 = up ? i : m;
+                for (int64_t kk = k0; kk < k1; ++kk) temp = temp - A_(kk, i) * B_(kk, j);
+                if (nounit) temp = temp / A_(i, i);
+                B_(i, j) = temp;
+            }
+    } else if (notr) {
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t s = 0; s < n; ++s) {
+                int64_t j = up ? s : n - 1 - s;
+                if (!alpha_one) B_(i, j) = alpha * B_(i, j);
+                int64_t k0 = up ? 0 : j + 1, k1 = up ? j : n;
+                for (int64_t kk = k0; kk < k1; ++kk) B_(i, j) = B_(i, j) - A_(kk, j) * B_(i, kk);
+                if (nounit) B_(i, j) = (1.0 / A_(j, j)) * B_(i, j);
+            }
+    } else {
+        for (int64_t i = 0; i < m; ++i)
+            for (int64_t s = 0; s < n; ++s) {
+                int64_t kk = up ? n - 1 - s : s;
+                if (nounit) B_(i, kk) = (1.0 / A_(kk, kk)) * B_(i, kk);
+                int64_t j0 = up ? 0 : kk + 1, j1 = up ? kk : n;
+                double x = B_(i, kk);
+                for (int64_t j = j0; j < j1; ++j) B_(i, j) = B_(i, j) - A_(j, kk) * x;
+                if (!alpha_one) B_(i, kk) = alpha * B_(i, kk);
+            }
+    }
+#undef A_
+#undef B_
+    return 0;
+}
+
+int oracle_dgetrf(int64_t m, int64_t n, double *A, int64_t lda, int64_t *ipiv, int64_t *info) {
+    int rc = oracle_getrf_validate(m, n, lda);
+    if (rc) return rc;
+    *info = 0;
+    int64_t mn = m < n ? m : n;
+    for (int64_t j = 0; j < mn; ++j) {
+        int64_t jp = j;             /* F64Backend.argmax_abs: first max, NaN -> 0 */
+        double mx = -1.0;
+        int nan = 0;
+        for (int64_t i = j; i < m; ++i) {
+            double a = fabs(A[i + j * lda]);
+            if (isnan(a)) { nan = 1; break; }
+            if (a > mx) { mx = a; jp = i; }
+        }
+        if (nan) jp = j;
+        ipiv[j] = jp + 1;
+        double piv = A[jp + j * lda];
+        if (piv != 0.0) {
+            if (jp != j)
+                for (int64_t c = 0; c < n; ++c) {
+                    double t = A[j + c * lda];
+                    A[j + c * lda] = A[jp + c * lda];
+                    A[jp + c * lda] = t;
+                }
+            if (j < m - 1) {
+                if (fabs(piv) >= 0x1p-1022) {
+                    double rec = 1.0 / piv;
+                    for (int64_t i = j + 1; i < m; ++i) A[i + j * lda] = rec * A[i + j * lda];
+                } else {
+                    for (int64_t i = j + 1; i < m; ++i) A[i + j * lda] = A[i + j * lda] / piv;
+                }
+            }
+        } else if (*info == 0) {
+            *info = j + 1;
+        }
+        if (j < mn - 1)
+            for (int64_t c = j + 1; c < n; ++c) {
+                double y = -A[j + c * lda];
+                for (int64_t i = j + 1; i < m; ++i) A[i + c * lda] = A[i + c * lda] + A[i + j * lda] * y;
+            }
+    }
+    return 0;
+}
+
+int oracle_dgetrs(char trans, int64_t n, int64_t nrhs, const double *A, int64_t lda,
+                  const int64_t *ipiv, int64_t nipiv, double *B, int64_t ldb) {
+    int rc = oracle_getrs_validate(trans, n, nrhs, lda, ldb);
+    if (rc) return rc;
+    if (n == 0 || nrhs == 0) return 0;
+    const int notr = upflag(trans) == 'N';
+    if (notr) {
+        for (int64_t k = 0; k < nipiv; ++k) {
+            int64_t p = ipiv[k] - 1;
+            if (p != k) for (int64_t c = 0; c < nrhs; ++c) { double t = B[k + c * ldb]; B[k + c * ldb] = B[p + c * ldb]; B[p + c * ldb] = t; }
+        }
+        oracle_dtrsm('L', 'L', 'N', 'U', n, nrhs, 1.0, A, lda, B, ldb);
+        oracle_dtrsm('L', 'U', 'N', 'N', n, nrhs, 1.0, A, lda, B, ldb);
+    } else {
+        oracle_dtrsm('L', 'U', 'T', 'N', n, nrhs, 1.0, A, lda, B, ldb);
+        oracle_dtrsm('L', 'L', 'T', 'U', n, nrhs, 1.0, A, lda, B, ldb);
+        for (int64_t s = 0; s < nipiv; ++s) {
+            int64_t k = nipiv - 1 - s, p = ipiv[k] - 1;
+            if (p != k) for (int64_t c = 0; c < nrhs; ++c) { double t = B[k + c * ldb]; B[k + c * ldb] = B[p + c * ldb]; B[p + c * ldb] = t; }
+        }
+    }
+    return 0;
+}

@@ -396,7 +396,102 @@ def run_case_getrs(case, store):
     store["cases"].append(case)
 
 
+def run_case_lapack_f64(mb, case, store):
+    sys.path.insert(0, REF)
+    from mpkit.mplapack import Rgetrf, Rgetrs, Rpotrf
+    arrays, lds = case_inputs(case)
+    case.update(lds)
+    r = case["routine"]
+    with np.errstate(all="ignore"):
+        if r == "Rpotrf":
+            n = case["n"]
+            a = _ref_matrix(mb, n, n, lds["lda"], arrays, "A", case)
+            case["info"] = int(Rpotrf(case["uplo"], n, a, lds["lda"]))
+            out = a
+        elif r == "Rtrsm":
+            m, n = case["m"], case["n"]
+            na = m if case["side"].upper() == "L" else n
+            alpha = TRSM_ALPHAS[case["alpha"]][0]
+            case["alpha_v"] = [alpha, 0.0]
+            a = _ref_matrix(mb, na, na, lds["lda"], arrays, "A", case)
+            b = _ref_matrix(mb, m, n, lds["ldb"], arrays, "B", case)
+            mb.Rtrsm(case["side"], case["uplo"], case["transa"], case["diag"], m, n, alpha, a,
+                     lds["lda"], b, lds["ldb"])
+            out = b
+        elif r == "Rgetrf":
+            m, n = case["m"], case["n"]
+            a = _ref_matrix(mb, m, n, lds["lda"], arrays, "A", case)
+            ipiv, info = Rgetrf(m, n, a, lds["lda"])
+            case["info"], case["ipiv"] = int(info), [int(p) for p in ipiv]
+            out = a
+        else:
+            n, nrhs = case["n"], case["nrhs"]
+            a = _ref_matrix(mb, n, n, lds["lda"], arrays, "A", case)
+            b = _ref_matrix(mb, n, nrhs, lds["ldb"], arrays, "B", case)
+            ipiv, info = Rgetrf(n, n, a, lds["lda"])
+            Rgetrs(case["trans"], n, nrhs, a, lds["lda"], ipiv, b, lds["ldb"])
+            case["ipiv"] = [int(p) for p in ipiv]
+            out = b
+    _store_out(store, case, arrays, out)
+
+
+def lapack_f64_cases():
+    """The LAPACK consumers on the reference's binary64 Matrix (F64 backend)."""
+    cases = []
+    seed = 2300
+    for uplo in ("L", "U"):
+        for n, sp in ((1, None), (7, None), (70, None), (40, "neg_pivot"), (12, "nan_pivot")):
+            c = dict(routine="Rpotrf", precision="f64", uplo=uplo, n=n, pad=(1,), seed=seed)
+            if sp:
+                c["special"] = sp
+            cases.append(c)
+            seed += 1
+    for side in ("L", "R"):
+        for uplo in ("U", "L"):
+            for ta in ("N", "T"):
+                for diag, al in (("N", "a15lo"), ("U", "a1")):
+                    cases.append(dict(routine="Rtrsm", precision="f64", side=side, uplo=uplo,
+                                      transa=ta, diag=diag, m=70 if side == "L" else 9,
+                                      n=9 if side == "L" else 70, pad=(1, 2), alpha=al,
+                                      seed=seed))
+                    seed += 1
+    cases.append(dict(routine="Rtrsm", precision="f64", side="L", uplo="U", transa="N", diag="N",
+                      m=6, n=5, pad=(0, 0), alpha="a0", seed=seed)); seed += 1
+    for m, n, sp in ((7, 7, None), (70, 70, None), (40, 17, None), (17, 40, None),
+                     (20, 20, "zero_col"), (30, 30, "ties"), (20, 20, "tiny_pivot"),
+                     (10, 10, "nan")):
+        c = dict(routine="Rgetrf", precision="f64", m=m, n=n, pad=(1,), seed=seed)
+        if sp:
+            c["special"] = sp
+        cases.append(c)
+        seed += 1
+    for trans in ("N", "T"):
+        for n, nrhs in ((7, 3), (70, 2)):
+            cases.append(dict(routine="Rgetrs", precision="f64", trans=trans, n=n, nrhs=nrhs,
+                              pad=(1, 1), seed=seed))
+            seed += 1
+    return cases
+
+
+def _ref_matrix(mb, rows, cols, ld, arrays, name, case):
+    if case.get("precision") == "f64":
+        return _f64_matrix(mb, rows, cols, ld, arrays[f"{name}_hi"])
+    return _matrix(mb, rows, cols, ld, (arrays[f"{name}_hi"], arrays[f"{name}_lo"]))
+
+
+def _store_out(store, case, arrays, mat):
+    cid = len(store["cases"])
+    case["id"] = cid
+    case["input_sha256"] = input_digest(arrays)
+    store["arrays"][f"c{cid}_out_hi"] = np.asarray(mat.store[0], dtype=np.float64)
+    store["arrays"][f"c{cid}_out_lo"] = (np.asarray(mat.store[1], dtype=np.float64)
+                                         if case.get("precision") != "f64" else np.zeros(0))
+    store["cases"].append(case)
+
+
 def run_case(mb, DDouble, case, store):
+    if case["routine"] in ("Rpotrf", "Rtrsm", "Rgetrf", "Rgetrs") and case.get("precision") == "f64":
+        return run_case_lapack_f64(mb, case, store)
     if case["routine"] == "Rgetrs":
         return run_case_getrs(case, store)
     if case["routine"] == "Rtrsm":
@@ -521,7 +616,7 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     store = {"cases": [], "arrays": {}}
     for case in (gemm_cases() + syrk_cases() + f64_cases() + complex_cases() + potrf_cases()
-                 + trsm_cases() + getrf_cases() + getrs_cases()):
+                 + trsm_cases() + getrf_cases() + getrs_cases() + lapack_f64_cases()):
         run_case(mb, DDouble, case, store)
     np.savez_compressed(os.path.join(OUT, "cases.npz"), **store["arrays"])
     with open(os.path.join(OUT, "cases.json"), "w") as f:

@@ -90,6 +90,18 @@ def lib():
                                     ctypes.POINTER(ctypes.c_int64), _i64, _dp, _dp, _i64]
         L.oracle_getrs_validate.restype = ctypes.c_int
         L.oracle_getrs_validate.argtypes = [ctypes.c_char] + [_i64] * 4
+        dp1 = _dp
+        L.oracle_dpotrf.restype = ctypes.c_int
+        L.oracle_dpotrf.argtypes = [ctypes.c_char, _i64, dp1, _i64, ctypes.POINTER(ctypes.c_int64)]
+        L.oracle_dtrsm.restype = ctypes.c_int
+        L.oracle_dtrsm.argtypes = [ctypes.c_char] * 4 + [_i64, _i64, ctypes.c_double, dp1, _i64,
+                                                         dp1, _i64]
+        L.oracle_dgetrf.restype = ctypes.c_int
+        L.oracle_dgetrf.argtypes = [_i64, _i64, dp1, _i64, ctypes.POINTER(ctypes.c_int64),
+                                    ctypes.POINTER(ctypes.c_int64)]
+        L.oracle_dgetrs.restype = ctypes.c_int
+        L.oracle_dgetrs.argtypes = [ctypes.c_char, _i64, _i64, dp1, _i64,
+                                    ctypes.POINTER(ctypes.c_int64), _i64, dp1, _i64]
         L.oracle_div2.restype = None
         L.oracle_div2.argtypes = [ctypes.c_double] * 4 + [_dp]
         L.oracle_sqrt2.restype = None
@@ -205,6 +217,31 @@ def rgetrs(trans, n, nrhs, a_hi, a_lo, lda, ipiv, b_hi, b_lo, ldb):
     arr = (ctypes.c_int64 * max(1, len(ipiv)))(*ipiv)
     return lib().oracle_rgetrs(_flag(trans), n, nrhs, _ptr(a_hi), _ptr(a_lo), lda, arr, len(ipiv),
                                _ptr(b_hi), _ptr(b_lo), ldb)
+
+
+def dpotrf(uplo, n, a, lda):
+    """binary64 Rpotrf (F64 backend); returns (rc, info)."""
+    info = ctypes.c_int64(0)
+    rc = lib().oracle_dpotrf(_flag(uplo), n, _ptr(a), lda, ctypes.byref(info))
+    return rc, int(info.value)
+
+
+def dtrsm(side, uplo, transa, diag, m, n, alpha, a, lda, b, ldb):
+    return lib().oracle_dtrsm(_flag(side), _flag(uplo), _flag(transa), _flag(diag), m, n,
+                              float(alpha), _ptr(a), lda, _ptr(b), ldb)
+
+
+def dgetrf(m, n, a, lda):
+    mn = max(0, min(m, n))
+    ipiv = (ctypes.c_int64 * max(1, mn))()
+    info = ctypes.c_int64(0)
+    rc = lib().oracle_dgetrf(m, n, _ptr(a), lda, ipiv, ctypes.byref(info))
+    return rc, [int(ipiv[i]) for i in range(mn)], int(info.value)
+
+
+def dgetrs(trans, n, nrhs, a, lda, ipiv, b, ldb):
+    arr = (ctypes.c_int64 * max(1, len(ipiv)))(*ipiv)
+    return lib().oracle_dgetrs(_flag(trans), n, nrhs, _ptr(a), lda, arr, len(ipiv), _ptr(b), ldb)
 
 
 def div2(x, y):

@@ -30,7 +30,9 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rtrsm", "ddb_rtrsm_host", "ddb_rtrsm_validate",
            "ddb_rgetrf", "ddb_rgetrf_host", "ddb_rgetrf_validate",
            "ddb_rgetrs", "ddb_rgetrs_host", "ddb_rgetrs_validate",
-           "ddb_rgemm_mgpu", "ddb_rsyrk_mgpu")
+           "ddb_rgemm_mgpu", "ddb_rsyrk_mgpu",
+           "ddb_dtrsm", "ddb_dtrsm_host", "ddb_dgetrf", "ddb_dgetrf_host",
+           "ddb_dgetrs", "ddb_dgetrs_host", "ddb_dpotrf", "ddb_dpotrf_host")
 
 _lib = None
 
@@ -98,6 +100,18 @@ def load():
         f.argtypes = rs
     L.ddb_rgetrs_validate.restype = ctypes.c_int
     L.ddb_rgetrs_validate.argtypes = [_c] + [_i64] * 4
+    i64p, ip_ = ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int)
+    f64sig = {
+        "ddb_dtrsm": [_c, _c, _c, _c, _i64, _i64, _d, _dp, _i64, _dp, _i64, _dp],
+        "ddb_dgetrf": [_i64, _i64, _dp, _i64, i64p, ip_, _dp],
+        "ddb_dgetrs": [_c, _i64, _i64, _dp, _i64, i64p, _dp, _i64, _dp],
+        "ddb_dpotrf": [_c, _i64, _dp, _i64, _i64, _dp, ip_],
+    }
+    for name, args in f64sig.items():
+        for nm in (name, name + "_host"):
+            f = getattr(L, nm)
+            f.restype = ctypes.c_int
+            f.argtypes = args
     L.ddb_rgetrf_validate.restype = ctypes.c_int
     L.ddb_rgetrf_validate.argtypes = [_i64, _i64, _i64]
     L.ddb_rpotrf_validate.restype = ctypes.c_int

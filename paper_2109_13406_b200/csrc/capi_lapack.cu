@@ -18,11 +18,33 @@
 using namespace ddb;
 using namespace ddb::host;
 
-extern "C" {
+namespace {
+
+// binary64 twins of the trailing-update calls (the 'f64' Matrix: one plane,
+// lo pointers alias hi and are ignored; the f64 GEMMs are bit-exact, so
+// mode does not apply)
+int gemm_any(bool f64, char ta, char tb, int64_t m, int64_t n, int64_t k, double alpha_hi,
+             double alpha_lo, const double* ah, const double* al, int64_t lda, const double* bh,
+             const double* bl, int64_t ldb, double beta_hi, double beta_lo, double* ch, double* cl,
+             int64_t ldc, int mode, void* st) {
+  if (f64) return ddb_dgemm(ta, tb, m, n, k, alpha_hi, ah, lda, bh, ldb, beta_hi, ch, ldc, st);
+  return ddb_rgemm(ta, tb, m, n, k, alpha_hi, alpha_lo, ah, al, lda, bh, bl, ldb, beta_hi, beta_lo,
+                   ch, cl, ldc, mode, st);
+}
+
+int syrk_any(bool f64, char uplo, char trans, int64_t n, int64_t k, double alpha_hi,
+             double alpha_lo, const double* ah, const double* al, int64_t lda, double beta_hi,
+             double beta_lo, double* ch, double* cl, int64_t ldc, int mode, void* st) {
+  if (f64) return ddb_dsyrk(uplo, trans, n, k, alpha_hi, ah, lda, beta_hi, ch, ldc, st);
+  return ddb_rsyrk(uplo, trans, n, k, alpha_hi, alpha_lo, ah, al, lda, beta_hi, beta_lo, ch, cl,
+                   ldc, mode, st);
+}
 
 // ---- triangular solve (dd_trsm.cu) -------------------------------------------
 
-int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+}  // namespace
+
+extern "C" int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
                        int64_t lda, int64_t ldb) {
   const int sd = upflag(side), u = upflag(uplo), t = upflag(transa), d = upflag(diag);
   if (sd != 'L' && sd != 'R') return 1;               // level23.py:296-299
@@ -37,9 +59,10 @@ int ddb_rtrsm_validate(char side, char uplo, char transa, char diag, int64_t m, 
   return 0;
 }
 
-int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
-              double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
-              int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream) {
+static int rtrsm_impl(bool f64, char side, char uplo, char transa, char diag, int64_t m,
+                      int64_t n, double alpha_hi, double alpha_lo, const double* a_hi,
+                      const double* a_lo, int64_t lda, double* b_hi, double* b_lo, int64_t ldb,
+                      int mode, void* stream) {
   const int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
   if (rc) return rc;
   if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM) {
@@ -51,7 +74,8 @@ int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n
   cudaError_t e;
   if (is_zero(alpha_hi, alpha_lo)) {                  // :310-312: B = 0
     e = cudaMemset2DAsync(b_hi, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
-    if (e == cudaSuccess) e = cudaMemset2DAsync(b_lo, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
+    if (e == cudaSuccess && !f64)
+      e = cudaMemset2DAsync(b_lo, sizeof(double) * ldb, 0, sizeof(double) * m, n, s);
     return e == cudaSuccess ? DDB_OK : fail(e, "rtrsm zero fill");
   }
   const bool left = upflag(side) == 'L', upper = upflag(uplo) == 'U';
@@ -60,6 +84,7 @@ int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n
   // branch table (see dd_trsm.cu): production order, T orientation, finish,
   // alpha placement, and whether the terms arrive in reverse order
   TrsmArgs t{};
+  t.f64 = f64;
   t.left = left;
   t.unit = upflag(diag) == 'U';
   t.fin_rec = !left;
@@ -85,7 +110,8 @@ int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n
   e = launch_trsm_pack(t, b_hi, b_lo, ldb, init_scale, alpha, s);
   ++nl;
   if (e == cudaSuccess) { e = launch_trsm_coef(t, a_hi, a_lo, lda, trans, s); ++nl; }
-  const bool exact_order = mode == MODE_EXACT || mode == MODE_REFERENCE;
+  // binary64 is always in the reference's order
+  const bool exact_order = f64 || mode == MODE_EXACT || mode == MODE_REFERENCE;
   if (e == cudaSuccess && rev_terms && exact_order) {
     e = launch_trsm_rev(t, s);
     ++nl;
@@ -110,7 +136,8 @@ int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n
       g.b_hi = t.w_hi + l0; g.b_lo = t.w_lo + l0; g.ldb = t.ldw;
       g.c_hi = t.w_hi + r0; g.c_lo = t.w_lo + r0; g.ldc = t.ldw;
       g.beta = dd{1.0, 0.0};
-      if (exact_order) { g.sub = 1; g.alpha = dd{1.0, 0.0}; }
+      g.f64 = f64;    // binary64: c + a (-1 x) == c - a x exactly, the plain f64 kernel
+      if (exact_order && !f64) { g.sub = 1; g.alpha = dd{1.0, 0.0}; }
       else { g.sub = 0; g.alpha = dd{-1.0, 0.0}; }
       return run(g, mode, s);
     };
@@ -137,7 +164,22 @@ int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n
   return DDB_OK;
 }
 
-int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+extern "C" int ddb_rtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                         double alpha_hi, double alpha_lo, const double* a_hi,
+                         const double* a_lo, int64_t lda, double* b_hi, double* b_lo,
+                         int64_t ldb, int mode, void* stream) {
+  return rtrsm_impl(false, side, uplo, transa, diag, m, n, alpha_hi, alpha_lo, a_hi, a_lo, lda,
+                    b_hi, b_lo, ldb, mode, stream);
+}
+
+extern "C" int ddb_dtrsm(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                         double alpha, const double* a, int64_t lda, double* b, int64_t ldb,
+                         void* stream) {
+  return rtrsm_impl(true, side, uplo, transa, diag, m, n, alpha, 0.0, a, a, lda, b, b, ldb,
+                    DDB_MODE_EXACT, stream);
+}
+
+extern "C" int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
                    double alpha_hi, double alpha_lo, const double* a_hi, const double* a_lo,
                    int64_t lda, double* b_hi, double* b_lo, int64_t ldb, int mode, void* stream) {
   int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
@@ -163,15 +205,15 @@ int ddb_rtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int6
 
 // ---- LU with partial pivoting (dd_getrf.cu) -----------------------------------
 
-int ddb_rgetrf_validate(int64_t m, int64_t n, int64_t lda) {
+extern "C" int ddb_rgetrf_validate(int64_t m, int64_t n, int64_t lda) {
   if (m < 0) return 1;                                // lu.py:83-85
   if (n < 0) return 2;
   if (lda < (m > 1 ? m : 1)) return 4;
   return 0;
 }
 
-int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
-               int* info, int mode, void* stream) {
+static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda,
+                       int64_t* ipiv, int* info, int mode, void* stream) {
   const int rc = ddb_rgetrf_validate(m, n, lda);
   if (rc) return rc;
   if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr ||
@@ -193,6 +235,7 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   GetrfArgs g{};
   g.m = m; g.n = n; g.mn = m < n ? m : n; g.lda = lda;
   g.a_hi = a_hi; g.a_lo = a_lo;
+  g.f64 = f64;
   const int G = getrf_max_panel_ctas();
   // workspace: info, barrier | ipiv, swap (mn each) | G partial candidates
   // partial candidates and rows: two parities (getrf_panel_smem_kernel)
@@ -245,7 +288,7 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   auto gemm = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t l0, int64_t l1,
                   cudaStream_t st) -> int {   // A(r0:r1, c0:c1) += A(r0:r1, l0:l1) (-A(l0:l1, c0:c1))
     if (r1 <= r0 || c1 <= c0 || l1 <= l0) return DDB_OK;
-    return ddb_rgemm('N', 'N', r1 - r0, c1 - c0, l1 - l0, -1.0, 0.0, a_hi + r0 + l0 * lda,
+    return gemm_any(f64, 'N', 'N', r1 - r0, c1 - c0, l1 - l0, -1.0, 0.0, a_hi + r0 + l0 * lda,
                      a_lo + r0 + l0 * lda, lda, a_hi + l0 + c0 * lda, a_lo + l0 + c0 * lda, lda,
                      1.0, 0.0, a_hi + r0 + c0 * lda, a_lo + r0 + c0 * lda, lda, mode,
                      static_cast<void*>(st));
@@ -347,7 +390,17 @@ int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   return DDB_OK;
 }
 
-int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
+extern "C" int ddb_rgetrf(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda,
+                          int64_t* ipiv, int* info, int mode, void* stream) {
+  return rgetrf_impl(false, m, n, a_hi, a_lo, lda, ipiv, info, mode, stream);
+}
+
+extern "C" int ddb_dgetrf(int64_t m, int64_t n, double* a, int64_t lda, int64_t* ipiv, int* info,
+                          void* stream) {
+  return rgetrf_impl(true, m, n, a, a, lda, ipiv, info, DDB_MODE_EXACT, stream);
+}
+
+extern "C" int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t* ipiv,
                     int* info, int mode, void* stream) {
   int rc = ddb_rgetrf_validate(m, n, lda);
   if (rc) return rc;
@@ -371,7 +424,7 @@ int ddb_rgetrf_host(int64_t m, int64_t n, double* a_hi, double* a_lo, int64_t ld
   return DDB_OK;
 }
 
-int ddb_rgetrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_t ldb) {
+extern "C" int ddb_rgetrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_t ldb) {
   const int t = upflag(trans);
   if (t != 'N' && t != 'T' && t != 'C') return 1;     // lu.py:123-125
   if (n < 0) return 2;
@@ -381,9 +434,9 @@ int ddb_rgetrs_validate(char trans, int64_t n, int64_t nrhs, int64_t lda, int64_
   return 0;
 }
 
-int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
-               int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
-               int mode, void* stream) {
+static int rgetrs_impl(bool f64, char trans, int64_t n, int64_t nrhs, const double* a_hi,
+                       const double* a_lo, int64_t lda, const int64_t* ipiv, double* b_hi,
+                       double* b_lo, int64_t ldb, int mode, void* stream) {
   const int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
   if (rc) return rc;
   if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || (ipiv == nullptr && n > 0)) {
@@ -405,6 +458,7 @@ int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const do
   GetrfArgs g{};
   g.m = n; g.n = nrhs; g.mn = n; g.lda = ldb;
   g.a_hi = b_hi; g.a_lo = b_lo;
+  g.f64 = f64;
   g.swap = static_cast<long long*>(ws);
   PermBuf pb;
   pb.rows = reinterpret_cast<long long*>(static_cast<char*>(ws) + swb);
@@ -415,13 +469,13 @@ int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const do
   if (e == cudaSuccess && notr) {
     e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 0, pb);
     if (e == cudaSuccess)
-      r = ddb_rtrsm('L', 'L', 'N', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+      r = rtrsm_impl(f64, 'L', 'L', 'N', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
     if (e == cudaSuccess && r == DDB_OK)
-      r = ddb_rtrsm('L', 'U', 'N', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+      r = rtrsm_impl(f64, 'L', 'U', 'N', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
   } else if (e == cudaSuccess) {
-    r = ddb_rtrsm('L', 'U', 'T', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+    r = rtrsm_impl(f64, 'L', 'U', 'T', 'N', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
     if (r == DDB_OK)
-      r = ddb_rtrsm('L', 'L', 'T', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
+      r = rtrsm_impl(f64, 'L', 'L', 'T', 'U', n, nrhs, 1.0, 0.0, a_hi, a_lo, lda, b_hi, b_lo, ldb, mode, stream);
     if (r == DDB_OK) e = launch_getrf_laswp(g, 0, n, 0, nrhs, s, 1, pb);
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
@@ -431,7 +485,18 @@ int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi, const do
   return DDB_OK;
 }
 
-int ddb_rgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
+extern "C" int ddb_rgetrs(char trans, int64_t n, int64_t nrhs, const double* a_hi,
+                          const double* a_lo, int64_t lda, const int64_t* ipiv, double* b_hi,
+                          double* b_lo, int64_t ldb, int mode, void* stream) {
+  return rgetrs_impl(false, trans, n, nrhs, a_hi, a_lo, lda, ipiv, b_hi, b_lo, ldb, mode, stream);
+}
+
+extern "C" int ddb_dgetrs(char trans, int64_t n, int64_t nrhs, const double* a, int64_t lda,
+                          const int64_t* ipiv, double* b, int64_t ldb, void* stream) {
+  return rgetrs_impl(true, trans, n, nrhs, a, a, lda, ipiv, b, b, ldb, DDB_MODE_EXACT, stream);
+}
+
+extern "C" int ddb_rgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a_hi, const double* a_lo,
                     int64_t lda, const int64_t* ipiv, double* b_hi, double* b_lo, int64_t ldb,
                     int mode, void* stream) {
   int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
@@ -454,7 +519,7 @@ int ddb_rgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a_hi, con
 
 // ---- blocked Cholesky (dd_potrf.cu) ----------------------------------------
 
-int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {
+extern "C" int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {
   const int u = upflag(uplo);
   if (u != 'U' && u != 'L') return 1;                 // chol.py:24-26
   if (n < 0) return 2;                                // chol.py:28
@@ -462,8 +527,8 @@ int ddb_rpotrf_validate(char uplo, int64_t n, int64_t lda) {
   return 0;
 }
 
-int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
-               int mode, void* stream, int* info) {
+static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda,
+                       int64_t nb, int mode, void* stream, int* info) {
   const int rc = ddb_rpotrf_validate(uplo, n, lda);
   if (rc) return rc;
   if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr) {
@@ -487,6 +552,7 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   retain_pool_memory();
   PotrfArgs p{};
   p.n = n; p.lda = lda; p.upper = upflag(uplo) == 'U';
+  p.f64 = f64;
   p.a_hi = a_hi; p.a_lo = a_lo;
   // workspace: info | D, d0 (dd vectors), rec (ib dd) | backup ('L') or S
   // ('U'), n x n dd | 'U': the inner transposed panel (n x ib) and two outer
@@ -517,7 +583,8 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   e = cudaMemsetAsync(ws, 0, head + 2 * vec, s);
   const size_t dpitch = sizeof(double) * (size_t)(lda + 1);
   if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0h, 8, a_hi, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpy2DAsync(d0l, 8, a_lo, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && !f64)
+    e = cudaMemcpy2DAsync(d0l, 8, a_lo, dpitch, 8, n, cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess) {
     if (p.upper) {
       p.s_hi = big; p.s_lo = big + (size_t)n * n; p.lds = n;
@@ -528,7 +595,8 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
       p.b_hi = bh; p.b_lo = bl;
       const size_t pitch = sizeof(double) * (size_t)lda, row = sizeof(double) * (size_t)n;
       e = cudaMemcpy2DAsync(bh, row, a_hi, pitch, row, n, cudaMemcpyDeviceToDevice, s);
-      if (e == cudaSuccess) e = cudaMemcpy2DAsync(bl, row, a_lo, pitch, row, n, cudaMemcpyDeviceToDevice, s);
+      if (e == cudaSuccess && !f64)
+        e = cudaMemcpy2DAsync(bl, row, a_lo, pitch, row, n, cudaMemcpyDeviceToDevice, s);
     }
   }
   // Streams: the panel work (diagonal blocks, panels, inner updates and the
@@ -554,19 +622,19 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
     int r;
     if (!p.upper) {
       const double *lh = a_hi + j0 * lda, *ll = a_lo + j0 * lda;
-      r = ddb_rsyrk('L', 'N', wd, kb, -1.0, 0.0, lh + c0, ll + c0, lda, 1.0, 0.0,
+      r = syrk_any(f64, 'L', 'N', wd, kb, -1.0, 0.0, lh + c0, ll + c0, lda, 1.0, 0.0,
                     a_hi + c0 + c0 * lda, a_lo + c0 + c0 * lda, lda, mode, sv);
       if (r == DDB_OK && below > 0)
-        r = ddb_rgemm('N', 'T', below, wd, kb, -1.0, 0.0, lh + c1, ll + c1, lda, lh + c0, ll + c0,
+        r = gemm_any(f64, 'N', 'T', below, wd, kb, -1.0, 0.0, lh + c1, ll + c1, lda, lh + c0, ll + c0,
                       lda, 1.0, 0.0, a_hi + c1 + c0 * lda, a_lo + c1 + c0 * lda, lda, mode, sv);
     } else {
       const int64_t ldt = n - tb0;
       th -= tb0;
       tl -= tb0;                                     // th[x] = T(x) for column x
-      r = ddb_rsyrk('L', 'N', wd, kb, 1.0, 0.0, th + c0, tl + c0, ldt, 1.0, 0.0,
+      r = syrk_any(f64, 'L', 'N', wd, kb, 1.0, 0.0, th + c0, tl + c0, ldt, 1.0, 0.0,
                     p.s_hi + c0 + c0 * n, p.s_lo + c0 + c0 * n, n, mode, sv);
       if (r == DDB_OK && below > 0)
-        r = ddb_rgemm('N', 'T', below, wd, kb, 1.0, 0.0, th + c1, tl + c1, ldt, th + c0, tl + c0,
+        r = gemm_any(f64, 'N', 'T', below, wd, kb, 1.0, 0.0, th + c1, tl + c1, ldt, th + c0, tl + c0,
                       ldt, 1.0, 0.0, p.s_hi + c1 + c0 * n, p.s_lo + c1 + c0 * n, n, mode, sv);
     }
     return r;
@@ -650,7 +718,17 @@ int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, in
   return DDB_OK;
 }
 
-int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
+extern "C" int ddb_rpotrf(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda,
+                          int64_t nb, int mode, void* stream, int* info) {
+  return rpotrf_impl(false, uplo, n, a_hi, a_lo, lda, nb, mode, stream, info);
+}
+
+extern "C" int ddb_dpotrf(char uplo, int64_t n, double* a, int64_t lda, int64_t nb, void* stream,
+                          int* info) {
+  return rpotrf_impl(true, uplo, n, a, a, lda, nb, DDB_MODE_EXACT, stream, info);
+}
+
+extern "C" int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t lda, int64_t nb,
                     int mode, void* stream, int* info) {
   int rc = ddb_rpotrf_validate(uplo, n, lda);
   if (rc) return rc;
@@ -674,4 +752,68 @@ int ddb_rpotrf_host(char uplo, int64_t n, double* a_hi, double* a_lo, int64_t ld
   return DDB_OK;
 }
 
-}  // extern "C"
+// ---- binary64 host-buffer entry points (one plane, staged) ------------------
+
+extern "C" int ddb_dtrsm_host(char side, char uplo, char transa, char diag, int64_t m, int64_t n,
+                              double alpha, const double* a, int64_t lda, double* b, int64_t ldb,
+                              void* stream) {
+  int rc = ddb_rtrsm_validate(side, uplo, transa, diag, m, n, lda, ldb);
+  if (rc) return rc;
+  if (m == 0 || n == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t na = upflag(side) == 'L' ? m : n;
+  const int64_t sa = alpha == 0.0 ? 0 : span(na, na, lda), sb = span(m, n, ldb);
+  DevBuf A, B;
+  if ((rc = stage_in1(A, a, sa, s)) || (rc = stage_in1(B, b, sb, s))) return rc;
+  rc = ddb_dtrsm(side, uplo, transa, diag, m, n, alpha, A.p, lda, B.p, ldb, stream);
+  return rc ? rc : stage_out1(b, B, sb, s);
+}
+
+extern "C" int ddb_dgetrf_host(int64_t m, int64_t n, double* a, int64_t lda, int64_t* ipiv,
+                               int* info, void* stream) {
+  int rc = ddb_rgetrf_validate(m, n, lda);
+  if (rc) return rc;
+  if (info == nullptr) {
+    g_last_error = "info pointer is null";
+    return DDB_EINVAL;
+  }
+  *info = 0;
+  if (m == 0 || n == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t sa = span(m, n, lda);
+  DevBuf A;
+  if ((rc = stage_in1(A, a, sa, s))) return rc;
+  rc = ddb_dgetrf(m, n, A.p, lda, ipiv, info, stream);
+  return rc ? rc : stage_out1(a, A, sa, s);
+}
+
+extern "C" int ddb_dgetrs_host(char trans, int64_t n, int64_t nrhs, const double* a, int64_t lda,
+                               const int64_t* ipiv, double* b, int64_t ldb, void* stream) {
+  int rc = ddb_rgetrs_validate(trans, n, nrhs, lda, ldb);
+  if (rc) return rc;
+  if (n == 0 || nrhs == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t sa = span(n, n, lda), sb = span(n, nrhs, ldb);
+  DevBuf A, B;
+  if ((rc = stage_in1(A, a, sa, s)) || (rc = stage_in1(B, b, sb, s))) return rc;
+  rc = ddb_dgetrs(trans, n, nrhs, A.p, lda, ipiv, B.p, ldb, stream);
+  return rc ? rc : stage_out1(b, B, sb, s);
+}
+
+extern "C" int ddb_dpotrf_host(char uplo, int64_t n, double* a, int64_t lda, int64_t nb,
+                               void* stream, int* info) {
+  int rc = ddb_rpotrf_validate(uplo, n, lda);
+  if (rc) return rc;
+  if (info == nullptr) {
+    g_last_error = "info pointer is null";
+    return DDB_EINVAL;
+  }
+  *info = 0;
+  if (n == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t sa = span(n, n, lda);
+  DevBuf A;
+  if ((rc = stage_in1(A, a, sa, s))) return rc;
+  rc = ddb_dpotrf(uplo, n, A.p, lda, nb, stream, info);
+  return rc ? rc : stage_out1(a, A, sa, s);
+}

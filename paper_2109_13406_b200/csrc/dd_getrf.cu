@@ -25,76 +25,11 @@
 
 #include <cstdlib>
 
-#include "internal.h"
+#include "lapack_num.cuh"
 
 namespace ddb {
 
 namespace {
-
-__device__ __forceinline__ dd neg_(dd x) { return dd{-x.h, -x.l}; }
-__device__ __forceinline__ bool fin(double x) { return finite_(x); }
-__device__ __forceinline__ dd canon(double h, double l) { return dd{h, fin(h) ? l : 0.0}; }
-
-__device__ dd add2_scal(dd x, dd y) {
-  const double s0 = dadd(x.h, y.h);
-  if (!fin(s0)) return dd{s0, 0.0};
-  const dd r = add2_chk(x, y);
-  return canon(r.h, r.l);
-}
-__device__ dd mul21_scal(dd x, double y) {
-  double p, e;
-  two_prod_dekker(x.h, y, p, e);
-  if (!(fin(p) && fin(e))) return canon(p, 0.0);
-  e = dadd(e, dmul(x.l, y));
-  double s, t;
-  quick_two_sum(p, e, s, t);
-  return canon(s, t);
-}
-// scalar _div2 (ddarith.py:113-131)
-__device__ dd div2_scal(dd x, dd y) {
-  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-  const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  if (y.h == 0.0) {
-    if (x.h == 0.0) return dd{qnan, 0.0};
-    return dd{copysign(inf, x.h) * copysign(1.0, y.h), 0.0};
-  }
-  if (!(fin(x.h) && fin(y.h))) {
-    if (!fin(y.h) && !isnan(y.h)) {
-      if (!fin(x.h) && !isnan(x.h)) return dd{qnan, 0.0};
-      return dd{dmul(copysign(0.0, x.h), copysign(1.0, y.h)), 0.0};
-    }
-    return canon(dmul(x.h, copysign(1.0, y.h)), 0.0);
-  }
-  const double q1 = x.h / y.h;
-  dd r = add2_scal(x, neg_(mul21_scal(y, q1)));
-  const double q2 = r.h / y.h;
-  r = add2_scal(r, neg_(mul21_scal(y, q2)));
-  const double q3 = r.h / y.h;
-  double a, b;
-  quick_two_sum(q1, q2, a, b);
-  return add2_scal(dd{a, b}, dd{q3, 0.0});
-}
-// vectorised _v_div2 (elem.py:93-117)
-__device__ dd vdiv2(dd x, dd y) {
-  if (y.h == 0.0 || !(fin(x.h) && fin(y.h))) return div2_scal(x, y);
-  auto m21 = [](dd yy, double q) {
-    double p, e;
-    two_prod_dekker(yy.h, q, p, e);
-    const bool bad = !(fin(p) && fin(e));
-    e = dadd(e, dmul(yy.l, q));
-    double s, t;
-    quick_two_sum(p, e, s, t);
-    return bad ? dd{p, 0.0} : dd{s, t};
-  };
-  const double q1 = x.h / y.h;
-  dd r = add2_chk(x, neg_(m21(y, q1)));
-  const double q2 = r.h / y.h;
-  r = add2_chk(r, neg_(m21(y, q2)));
-  const double q3 = r.h / y.h;
-  double a, b;
-  quick_two_sum(q1, q2, a, b);
-  return add2_chk(dd{a, b}, dd{q3, 0.0});
-}
 
 // pivot-search key: larger |hi| wins, then larger lo*sign(hi), then the
 // smaller row index; a NaN |hi| anywhere makes the search return its first
@@ -167,10 +102,12 @@ __device__ PivKey block_best(PivKey k) {
 }  // namespace
 
 // Panel [j0, j0 + nb) over rows [j0, m).  CTA c owns rows [r0c, r1c).
+template <class N>
 __global__ void __launch_bounds__(kPanelThreads)
 getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
+  using T = typename N::T;
   __shared__ PivKey best_s;
-  __shared__ dd piv_s, rec_s;
+  __shared__ T piv_s, rec_s;
   __shared__ int use_rec_s, nonzero_s;
   const int64_t rows = g.m - j0;
   const int64_t chunk = (rows + gridDim.x - 1) / gridDim.x;
@@ -183,8 +120,8 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
   auto local_search = [&](int64_t j) {
     PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
     for (int64_t i = (r0 > j ? r0 : j) + threadIdx.x; i < r1; i += blockDim.x) {
-      const double h = ldg_cg(ah + i + j * lda), l = ldg_cg(al + i + j * lda);
-      PivKey y{fabs(h), h < 0.0 ? -l : l, h, l, (long long)i, isnan(h) ? 1 : 0};
+      const T v = N::ldcg(ah, al, i + j * lda);
+      PivKey y{N::key_hi(v), N::key_lo(v), N::hi(v), N::lo(v), (long long)i, N::key_nan(v) ? 1 : 0};
       k = merge(k, y);
     }
     k = block_best(k);
@@ -210,22 +147,17 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
       }
       for (int o = 16; o > 0; o >>= 1) k = merge(k, shfl_down(k, o));
       if (threadIdx.x == 0) {
-        dd piv{k.h, k.l};
+        T piv = N::make(k.h, k.l);
         if (k.nan || k.idx < 0) {   // argmax_abs returns 0 -> the diagonal entry
           k.idx = j;
-          piv = dd{ldg_cg(ah + j + j * lda), ldg_cg(al + j + j * lda)};
+          piv = N::ldcg(ah, al, j + j * lda);
         }
         best_s = k;
         const int64_t jp = k.idx;
         piv_s = piv;
-        nonzero_s = !(piv.h == 0.0 && piv.l == 0.0);
-        // |pivot| >= safmin (lu.py:98): DDouble abs then _cmp2 order
-        dd ap = piv;
-        if (ap.h < 0.0 || (ap.h == 0.0 && ap.l < 0.0)) ap = neg_(ap);
-        const double sh = 0x1p-969, sl = -0x0.0000000000006p-1022;
-        // _cmp2(ap, safmin) >= 0, NaN included (ddarith.py:166-176)
-        use_rec_s = !(ap.h < sh) && (ap.h > sh || !(ap.l < sl));
-        if (nonzero_s && use_rec_s) rec_s = div2_scal(dd{1.0, 0.0}, piv);
+        nonzero_s = N::nonzero(piv);
+        use_rec_s = N::ge_safmin(piv);                     // |pivot| >= safmin (lu.py:98)
+        if (nonzero_s && use_rec_s) rec_s = N::sdiv(N::one(), piv);
         if (blockIdx.x == 0) {
           g.ipiv[j] = jp + 1;
           g.swap[j] = nonzero_s ? jp : j;
@@ -238,11 +170,9 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
     const bool nonzero = nonzero_s;
     if (blockIdx.x == 0 && nonzero && jp != j) {   // interchange within the panel
       for (int64_t c = j0 + threadIdx.x; c < jend; c += blockDim.x) {
-        const double th = ldg_cg(ah + j + c * lda), tl = ldg_cg(al + j + c * lda);
-        ah[j + c * lda] = ldg_cg(ah + jp + c * lda);
-        al[j + c * lda] = ldg_cg(al + jp + c * lda);
-        ah[jp + c * lda] = th;
-        al[jp + c * lda] = tl;
+        const T tj = N::ldcg(ah, al, j + c * lda);
+        N::st(ah, al, j + c * lda, N::ldcg(ah, al, jp + c * lda));
+        N::st(ah, al, jp + c * lda, tj);
       }
     }
     grid_barrier(g.bar, gridDim.x * ++nbar);
@@ -251,12 +181,10 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
     const int64_t lo_row = r0 > j + 1 ? r0 : j + 1;
     if (nonzero) {
       const bool use_rec = use_rec_s;
-      const dd rec = rec_s, piv = piv_s;
+      const T rec = rec_s, piv = piv_s;
       for (int64_t i = lo_row + threadIdx.x; i < r1; i += blockDim.x) {
-        const dd x{ldg_cg(ah + i + j * lda), ldg_cg(al + i + j * lda)};
-        const dd y = use_rec ? mul2_chk(rec, x) : vdiv2(x, piv);
-        ah[i + j * lda] = y.h;
-        al[i + j * lda] = y.l;
+        const T x = N::ldcg(ah, al, i + j * lda);
+        N::st(ah, al, i + j * lda, use_rec ? N::mul(rec, x) : N::vdiv(x, piv));
       }
     }
     __syncthreads();
@@ -265,12 +193,8 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
     if (ncol > 0 && nrow > 0 && j < g.mn - 1) {
       for (int64_t t = threadIdx.x; t < ncol * nrow; t += blockDim.x) {
         const int64_t i = lo_row + t % nrow, c = j + 1 + t / nrow;
-        const dd x{ldg_cg(ah + i + j * lda), ldg_cg(al + i + j * lda)};
-        const dd u{ldg_cg(ah + j + c * lda), ldg_cg(al + j + c * lda)};
-        const dd r = add2_chk(dd{ldg_cg(ah + i + c * lda), ldg_cg(al + i + c * lda)},
-                              mul2_chk(x, neg_(u)));
-        ah[i + c * lda] = r.h;
-        al[i + c * lda] = r.l;
+        const T x = N::ldcg(ah, al, i + j * lda), u = N::ldcg(ah, al, j + c * lda);
+        N::st(ah, al, i + c * lda, N::add(N::ldcg(ah, al, i + c * lda), N::mul(x, N::neg(u))));
       }
     }
     __syncthreads();
@@ -288,11 +212,13 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
 // (kSmemRowsMax rows).
 constexpr int kSmemRowsMax = 192;
 
+template <class N>
 __global__ void __launch_bounds__(kPanelThreads)
 getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
+  using T = typename N::T;
   extern __shared__ double sm[];
   __shared__ PivKey best_s;
-  __shared__ dd rec_s;
+  __shared__ T rec_s;
   __shared__ int use_rec_s, nonzero_s;
   const int G = gridDim.x;
   const int64_t r0 = j0 + (int64_t)blockIdx.x * chunk;
@@ -306,8 +232,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   const int64_t lda = g.lda;
   for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
     const int r = t % nr, c = t / nr;
-    xh[r + c * ch] = g.a_hi[(r0 + r) + (j0 + c) * lda];
-    xl[r + c * ch] = g.a_lo[(r0 + r) + (j0 + c) * lda];
+    N::st(xh, xl, r + c * ch, N::ld(g.a_hi, g.a_lo, (r0 + r) + (j0 + c) * lda));
   }
   __syncthreads();
   auto owner = [&](int64_t row) { return (int)((row - j0) / chunk); };
@@ -321,8 +246,9 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
     const int rs = r0 > j ? 0 : (int)(j - r0);
     for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) {
-      const double h = xh[r + jj * ch], l = xl[r + jj * ch];
-      PivKey y{fabs(h), h < 0.0 ? -l : l, h, l, (long long)(r0 + r), isnan(h) ? 1 : 0};
+      const T v = N::ld(xh, xl, r + jj * ch);
+      PivKey y{N::key_hi(v), N::key_lo(v), N::hi(v), N::lo(v), (long long)(r0 + r),
+               N::key_nan(v) ? 1 : 0};
       k = merge(k, y);
     }
     k = block_best(k);
@@ -338,17 +264,12 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     if (k.idx >= 0) {
       double* cr = cand(par, blockIdx.x);
       const int rr = (int)(k.idx - r0);
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-        cr[c] = xh[rr + c * ch];
-        cr[nb + c] = xl[rr + c * ch];
-      }
+      for (int c = threadIdx.x; c < nb; c += blockDim.x) N::st(cr, cr + nb, c, N::ld(xh, xl, rr + c * ch));
     }
     if (owner(j) == (int)blockIdx.x) {
       double* jr = jrow(par);
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-        jr[c] = xh[(j - r0) + c * ch];
-        jr[nb + c] = xl[(j - r0) + c * ch];
-      }
+      for (int c = threadIdx.x; c < nb; c += blockDim.x)
+        N::st(jr, jr + nb, c, N::ld(xh, xl, (j - r0) + c * ch));
     }
   };
   publish(0);
@@ -377,31 +298,22 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     __syncthreads();
     const int64_t jp = best_s.idx;
     // a NaN search keeps row j; otherwise the winner's value is the pivot
-    const bool swapped = !best_s.nan && !(best_s.h == 0.0 && best_s.l == 0.0) && jp != j;
+    const bool swapped = !best_s.nan && N::nonzero(N::make(best_s.h, best_s.l)) && jp != j;
     const double* src = swapped ? cand(par, owner(jp)) : jrow(par);
     const double* jr = jrow(par);
     for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-      const double h = __ldcg(src + c), l = __ldcg(src + nb + c);
-      ph[c] = h;
-      pl[c] = l;
-      if (owner(j) == (int)blockIdx.x) {
-        xh[(j - r0) + c * ch] = h;
-        xl[(j - r0) + c * ch] = l;
-      }
-      if (swapped && owner(jp) == (int)blockIdx.x) {
-        xh[(jp - r0) + c * ch] = __ldcg(jr + c);
-        xl[(jp - r0) + c * ch] = __ldcg(jr + nb + c);
-      }
+      const T v = N::ldcg(src, src + nb, c);
+      N::st(ph, pl, c, v);
+      if (owner(j) == (int)blockIdx.x) N::st(xh, xl, (j - r0) + c * ch, v);
+      if (swapped && owner(jp) == (int)blockIdx.x)
+        N::st(xh, xl, (jp - r0) + c * ch, N::ldcg(jr, jr + nb, c));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      const dd piv{ph[jj], pl[jj]};
-      nonzero_s = !(piv.h == 0.0 && piv.l == 0.0);
-      dd ap = piv;
-      if (ap.h < 0.0 || (ap.h == 0.0 && ap.l < 0.0)) ap = neg_(ap);
-      const double sh = 0x1p-969, sl = -0x0.0000000000006p-1022;
-      use_rec_s = !(ap.h < sh) && (ap.h > sh || !(ap.l < sl));   // _cmp2 >= 0
-      if (nonzero_s && use_rec_s) rec_s = div2_scal(dd{1.0, 0.0}, piv);
+      const T piv = N::ld(ph, pl, jj);
+      nonzero_s = N::nonzero(piv);
+      use_rec_s = N::ge_safmin(piv);                       // |pivot| >= safmin (lu.py:98)
+      if (nonzero_s && use_rec_s) rec_s = N::sdiv(N::one(), piv);
       if (blockIdx.x == 0) {
         g.ipiv[j] = jp + 1;
         g.swap[j] = swapped ? jp : j;
@@ -413,12 +325,10 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     const int rs = r0 > j + 1 ? 0 : (int)(j + 1 - r0);
     if (nonzero) {
       const bool use_rec = use_rec_s;
-      const dd rec = rec_s, piv{ph[jj], pl[jj]};
+      const T rec = rec_s, piv = N::ld(ph, pl, jj);
       for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) {
-        const dd x{xh[r + jj * ch], xl[r + jj * ch]};
-        const dd y = use_rec ? mul2_chk(rec, x) : vdiv2(x, piv);
-        xh[r + jj * ch] = y.h;
-        xl[r + jj * ch] = y.l;
+        const T x = N::ld(xh, xl, r + jj * ch);
+        N::st(xh, xl, r + jj * ch, use_rec ? N::mul(rec, x) : N::vdiv(x, piv));
       }
     }
     __syncthreads();
@@ -426,10 +336,9 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     if (ncol > 0 && nrow > 0 && j < g.mn - 1) {
       for (int t = threadIdx.x; t < ncol * nrow; t += blockDim.x) {
         const int r = rs + t % nrow, c = jj + 1 + t / nrow;
-        const dd x{xh[r + jj * ch], xl[r + jj * ch]};
-        const dd rr = add2_chk(dd{xh[r + c * ch], xl[r + c * ch]}, mul2_chk(x, neg_(dd{ph[c], pl[c]})));
-        xh[r + c * ch] = rr.h;
-        xl[r + c * ch] = rr.l;
+        const T x = N::ld(xh, xl, r + jj * ch);
+        N::st(xh, xl, r + c * ch,
+              N::add(N::ld(xh, xl, r + c * ch), N::mul(x, N::neg(N::ld(ph, pl, c)))));
       }
     }
     __syncthreads();
@@ -437,8 +346,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   }
   for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
     const int r = t % nr, c = t / nr;
-    g.a_hi[(r0 + r) + (j0 + c) * lda] = xh[r + c * ch];
-    g.a_lo[(r0 + r) + (j0 + c) * lda] = xl[r + c * ch];
+    N::st(g.a_hi, g.a_lo, (r0 + r) + (j0 + c) * lda, N::ld(xh, xl, r + c * ch));
   }
 }
 
@@ -522,14 +430,14 @@ getrf_apply_perm_kernel(GetrfArgs g, PermBuf pb, int64_t c0, int64_t c1) {
       const int t = e % nt, c = e / nt;
       const int64_t x = pb.rows[pb.src[t]] + (cb + c) * g.lda;
       vh[c * nt + t] = g.a_hi[x];
-      vl[c * nt + t] = g.a_lo[x];
+      if (!g.f64) vl[c * nt + t] = g.a_lo[x];
     }
     __syncthreads();
     for (int e = threadIdx.x; e < nt * ncol; e += blockDim.x) {
       const int t = e % nt, c = e / nt;
       const int64_t x = pb.rows[t] + (cb + c) * g.lda;
       g.a_hi[x] = vh[c * nt + t];
-      g.a_lo[x] = vl[c * nt + t];
+      if (!g.f64) g.a_lo[x] = vl[c * nt + t];
     }
     __syncthreads();
   }
@@ -539,39 +447,35 @@ getrf_apply_perm_kernel(GetrfArgs g, PermBuf pb, int64_t c0, int64_t c1) {
 // rows t and t + 32 of the block.  Step l: the owner finalises U(l, c) and
 // broadcasts it; every later row r gets a(r, c) += mul2(L(r, l), -U(l, c)) --
 // per element the reference's order (l ascending).
+template <class N>
 __global__ void __launch_bounds__(256)
 getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0, int64_t c1) {
+  using T = typename N::T;
   extern __shared__ double sm[];
   double* lh = sm;
   double* ll = sm + nb * nb;
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
     const int r = e % nb, l = e / nb;
-    if (l < r) {
-      lh[e] = g.a_hi[(j0 + r) + (j0 + l) * g.lda];
-      ll[e] = g.a_lo[(j0 + r) + (j0 + l) * g.lda];
-    }
+    if (l < r) N::st(lh, ll, e, N::ld(g.a_hi, g.a_lo, (j0 + r) + (j0 + l) * g.lda));
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t c = c0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   if (c >= c1) return;                       // whole warps
   double* uh = g.a_hi + j0 + c * g.lda;
-  double* ul = g.a_lo + j0 + c * g.lda;
+  double* ul = g.f64 ? nullptr : g.a_lo + j0 + c * g.lda;
   const int ra = lane, rb = lane + 32;
-  dd acc_a{0.0, 0.0}, acc_b{0.0, 0.0};
-  if (ra < nb) acc_a = dd{uh[ra], ul[ra]};
-  if (rb < nb) acc_b = dd{uh[rb], ul[rb]};
+  T acc_a = N::zero(), acc_b = N::zero();
+  if (ra < nb) acc_a = N::ld(uh, ul, ra);
+  if (rb < nb) acc_b = N::ld(uh, ul, rb);
   for (int l = 0; l < nb - 1; ++l) {
-    const dd own = l < 32 ? acc_a : acc_b;   // U(l, c) is final once its turn comes
-    dd u;
-    u.h = __shfl_sync(0xffffffffu, own.h, l & 31);
-    u.l = __shfl_sync(0xffffffffu, own.l, l & 31);
-    const dd nu = neg_(u);
-    if (ra > l && ra < nb) acc_a = add2_chk(acc_a, mul2_chk(dd{lh[ra + l * nb], ll[ra + l * nb]}, nu));
-    if (rb > l && rb < nb) acc_b = add2_chk(acc_b, mul2_chk(dd{lh[rb + l * nb], ll[rb + l * nb]}, nu));
+    // U(l, c) is final once its turn comes
+    const T nu = N::neg(N::shfl(l < 32 ? acc_a : acc_b, l & 31));
+    if (ra > l && ra < nb) acc_a = N::add(acc_a, N::mul(N::ld(lh, ll, ra + l * nb), nu));
+    if (rb > l && rb < nb) acc_b = N::add(acc_b, N::mul(N::ld(lh, ll, rb + l * nb), nu));
   }
-  if (ra < nb) { uh[ra] = acc_a.h; ul[ra] = acc_a.l; }
-  if (rb < nb) { uh[rb] = acc_b.h; ul[rb] = acc_b.l; }
+  if (ra < nb) N::st(uh, ul, ra, acc_a);
+  if (rb < nb) N::st(uh, ul, rb, acc_b);
 }
 
 static int panel_grid(int64_t rows) {
@@ -581,10 +485,13 @@ static int panel_grid(int64_t rows) {
   if (dev != cached_dev) {
     int sms = 0, per = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrf_panel_kernel, kPanelThreads, 0);
-    // the shared-memory variant at its largest share: also >= 1 CTA / SM
-    cudaFuncSetAttribute(getrf_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, getrf_panel_kernel<NumDD>, kPanelThreads,
+                                                  0);
+    // the shared-memory variants at their largest share: also >= 1 CTA / SM
+    cudaFuncSetAttribute(getrf_panel_smem_kernel<NumDD>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(getrf_panel_smem_kernel<NumF64>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cached_max = per > 0 ? sms : 1;                            // one CTA per SM
     cached_dev = dev;
   }
@@ -609,14 +516,6 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
   }
   if (chunk <= kSmemRowsMax) {
     const size_t smem = sizeof(double) * (2 * (size_t)chunk * nb + 2 * (size_t)nb);
-    static thread_local int attr_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (attr_dev != dev) {
-      cudaFuncSetAttribute(getrf_panel_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-      attr_dev = dev;
-    }
     // A cooperative launch guarantees co-residency but may wait for an idle
     // device; with grid <= one CTA per SM an ordinary launch also completes
     // (the other stream's CTAs always retire), and can overlap the trailing
@@ -625,18 +524,21 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
       const char* v = std::getenv("DDB_GETRF_COOP");
       return v == nullptr || v[0] != '0';
     }();
+    void* kern = g.f64 ? reinterpret_cast<void*>(getrf_panel_smem_kernel<NumF64>)
+                       : reinterpret_cast<void*>(getrf_panel_smem_kernel<NumDD>);
     if (!coop) {
-      getrf_panel_smem_kernel<<<grid, kPanelThreads, smem, s>>>(ga, j0, nbv, chunk);
+      if (g.f64) getrf_panel_smem_kernel<NumF64><<<grid, kPanelThreads, smem, s>>>(ga, j0, nbv, chunk);
+      else getrf_panel_smem_kernel<NumDD><<<grid, kPanelThreads, smem, s>>>(ga, j0, nbv, chunk);
       return cudaGetLastError();
     }
     void* args[] = {&ga, &j0, &nbv, &chunk};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(getrf_panel_smem_kernel),
-                                       dim3(grid), dim3(kPanelThreads), args, smem, s);
+    return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kPanelThreads), args, smem, s);
   }
   grid = panel_grid(rows);
   void* args[] = {&ga, &j0, &nbv};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(getrf_panel_kernel), dim3(grid),
-                                     dim3(kPanelThreads), args, 0, s);
+  void* kern = g.f64 ? reinterpret_cast<void*>(getrf_panel_kernel<NumF64>)
+                     : reinterpret_cast<void*>(getrf_panel_kernel<NumDD>);
+  return cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kPanelThreads), args, 0, s);
 }
 
 cudaError_t launch_getrf_compose(const GetrfArgs& g, int64_t j0, int64_t j1, int reverse,
@@ -687,10 +589,14 @@ cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(getrf_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(getrf_trsm_kernel<NumDD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(getrf_trsm_kernel<NumF64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr_dev = dev;
   }
-  getrf_trsm_kernel<<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, s>>>(g, j0, nb, c0, c1);
+  if (g.f64) getrf_trsm_kernel<NumF64><<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, s>>>(g, j0, nb, c0, c1);
+  else getrf_trsm_kernel<NumDD><<<(unsigned)((c1 - c0 + 7) / 8), 256, smem, s>>>(g, j0, nb, c0, c1);
   return cudaGetLastError();
 }
 

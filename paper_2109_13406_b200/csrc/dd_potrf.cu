@@ -39,91 +39,9 @@
 // lower form write in place; a backup copy is kept for that).
 // dd sqrt / div / sub are the reference's scalar forms (ddarith.py:79-163);
 // element-wise add / mul the vectorised ones (elem.py:54-78).
-#include "internal.h"
+#include "lapack_num.cuh"
 
 namespace ddb {
-
-namespace {
-
-__device__ __forceinline__ dd neg2(dd x) { return dd{-x.h, -x.l}; }
-
-__device__ __forceinline__ bool isfin(double x) { return finite_(x); }
-
-// _canon (ddarith.py:68-71)
-__device__ __forceinline__ dd canon(double h, double l) { return dd{h, isfin(h) ? l : 0.0}; }
-
-// scalar _add2 (ddarith.py:79-90): the element form plus the final _canon
-__device__ dd add2_s(dd x, dd y) {
-  const double s0 = dadd(x.h, y.h);
-  if (!isfin(s0)) return dd{s0, 0.0};
-  const dd r = add2_chk(x, y);
-  return canon(r.h, r.l);
-}
-
-// _mul21 (ddarith.py:103-110): dd * double
-__device__ dd mul21_s(dd x, double y) {
-  double p, e;
-  two_prod_dekker(x.h, y, p, e);
-  if (!(isfin(p) && isfin(e))) return canon(p, 0.0);
-  e = dadd(e, dmul(x.l, y));
-  double s, t;
-  quick_two_sum(p, e, s, t);
-  return canon(s, t);
-}
-
-// _div2 (ddarith.py:113-131)
-__device__ dd div2_s(dd x, dd y) {
-  if (y.h == 0.0) {
-    if (x.h == 0.0) return dd{__longlong_as_double(0x7ff8000000000000LL), 0.0};
-    return dd{copysign(__longlong_as_double(0x7ff0000000000000LL), x.h) * copysign(1.0, y.h), 0.0};
-  }
-  if (!(isfin(x.h) && isfin(y.h))) {
-    if (!isfin(y.h) && !isnan(y.h)) {
-      if (!isfin(x.h) && !isnan(x.h)) return dd{__longlong_as_double(0x7ff8000000000000LL), 0.0};
-      return dd{dmul(copysign(0.0, x.h), copysign(1.0, y.h)), 0.0};
-    }
-    return canon(dmul(x.h, copysign(1.0, y.h)), 0.0);
-  }
-  const double q1 = x.h / y.h;
-  dd r = add2_s(x, neg2(mul21_s(y, q1)));
-  const double q2 = r.h / y.h;
-  r = add2_s(r, neg2(mul21_s(y, q2)));
-  const double q3 = r.h / y.h;
-  double a, b;
-  quick_two_sum(q1, q2, a, b);
-  return add2_s(dd{a, b}, dd{q3, 0.0});
-}
-
-// _sqrt2 (ddarith.py:142-163): Newton correction on 1/sqrt(hi), with the
-// exact even-power pre-scaling for very large / small arguments
-__device__ dd sqrt2_s(dd v) {
-  if (v.h == 0.0 && v.l == 0.0) return dd{0.0, 0.0};
-  if (!isfin(v.h)) return dd{v.h, 0.0};
-  double h = v.h, l = v.l;
-  int shift = 0;
-  if (h >= 0x1p996) { h = dmul(h, 0x1p-106); l = dmul(l, 0x1p-106); shift = 53; }
-  else if (h <= 0x1p-996) { h = dmul(h, 0x1p106); l = dmul(l, 0x1p106); shift = -53; }
-  const double x = 1.0 / sqrt(h);
-  const double ax = dmul(h, x);
-  double p, e;
-  two_prod_dekker(ax, ax, p, e);
-  const dd r = add2_s(dd{h, l}, dd{-p, -e});
-  double s, e2;
-  quick_two_sum(ax, dmul(r.h, dmul(x, 0.5)), s, e2);
-  if (shift == 53) { s = dmul(s, 0x1p53); e2 = dmul(e2, 0x1p53); }
-  else if (shift == -53) { s = dmul(s, 0x1p-53); e2 = dmul(e2, 0x1p-53); }
-  return canon(s, e2);
-}
-
-// chol.py:42: _isnan(ajj) (float(ajj) = hi + lo) or ajj <= 0 (_cmp2 order)
-__device__ __forceinline__ bool bad_pivot(dd a) {
-  if (isnan(dadd(a.h, a.l))) return true;
-  if (a.h < 0.0) return true;
-  if (a.h > 0.0) return false;
-  return !(a.l > 0.0);
-}
-
-}  // namespace
 
 // Diagonal block [j0, j1) in one CTA, staged in shared memory, right-looking:
 // per column j the pivot (thread 0), the column inside the block, then the
@@ -131,10 +49,12 @@ __device__ __forceinline__ bool bad_pivot(dd a) {
 // l order.  X(q, c) (q > c) is the block entry the factor overwrites: A(q, c)
 // for 'L', A(c, q) for 'U'; for 'U' the running dot products S(q, c) are
 // staged too.  The reciprocals go to p.rec for the panel kernel.
+template <class N>
 __global__ void __launch_bounds__(512)
 potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
+  using T = typename N::T;
   extern __shared__ double sm[];
-  __shared__ dd rec_s;
+  __shared__ T rec_s;
   __shared__ int ok_s;
   if (*p.info != 0) return;
   const int64_t lda = p.lda, lds = p.lds;
@@ -151,56 +71,43 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
     const int q = t % nb, c = t / nb;
     if (q <= c) continue;
     const int64_t x = p.upper ? (j0 + c) + (j0 + q) * lda : (j0 + q) + (j0 + c) * lda;
-    xh[t] = p.a_hi[x];
-    xl[t] = p.a_lo[x];
-    if (p.upper) {
-      const int64_t y = (j0 + q) + (j0 + c) * lds;
-      sh[t] = p.s_hi[y];
-      sl[t] = p.s_lo[y];
-    }
+    N::st(xh, xl, t, N::ld(p.a_hi, p.a_lo, x));
+    if (p.upper) N::st(sh, sl, t, N::ld(p.s_hi, p.s_lo, (j0 + q) + (j0 + c) * lds));
   }
   for (int t = threadIdx.x; t < nb; t += blockDim.x) {
-    dh[t] = p.dh[j0 + t];
-    dl[t] = p.dl[j0 + t];
-    d0h[t] = p.d0_hi[j0 + t];
-    d0l[t] = p.d0_lo[j0 + t];
+    N::st(dh, dl, t, N::ld(p.dh, p.dl, j0 + t));
+    N::st(d0h, d0l, t, N::ld(p.d0_hi, p.d0_lo, j0 + t));
   }
   __syncthreads();
   // thread 0 computes pivot j+1 while warps 1.. run step j's trailing
   // update (pivot j+1 needs only D(j+1), final after step j's column phase)
   auto pivot = [&](int j) {
-    const dd ajj = add2_s(dd{d0h[j], d0l[j]}, neg2(dd{dh[j], dl[j]}));   // chol.py:41
+    const T ajj = N::ssub(N::ld(d0h, d0l, j), N::ld(dh, dl, j));   // chol.py:41
     const int64_t djj = (j0 + j) * (lda + 1);
-    ok_s = !bad_pivot(ajj);
+    ok_s = !N::bad_pivot(ajj);
     if (!ok_s) {
-      p.a_hi[djj] = ajj.h;
-      p.a_lo[djj] = ajj.l;
+      N::st(p.a_hi, p.a_lo, djj, ajj);
       *p.info = (int)(j0 + j + 1);
     } else {
-      const dd s = sqrt2_s(ajj);
-      p.a_hi[djj] = s.h;
-      p.a_lo[djj] = s.l;
-      const dd rec = div2_s(dd{1.0, 0.0}, s);
+      const T s = N::ssqrt(ajj);
+      N::st(p.a_hi, p.a_lo, djj, s);
+      const T rec = N::sdiv(N::one(), s);
       rec_s = rec;
-      p.rec_hi[j] = rec.h;
-      p.rec_lo[j] = rec.l;
+      N::st(p.rec_hi, p.rec_lo, j, rec);
     }
   };
   if (threadIdx.x == 0) pivot(0);
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
     if (!ok_s) break;
-    const dd rec = rec_s;
+    const T rec = rec_s;
     for (int q = j + 1 + threadIdx.x; q < nb; q += blockDim.x) {
       const int t = q + j * nb;
-      dd a{xh[t], xl[t]};
-      if (p.upper) a = add2_chk(a, neg2(dd{sh[t], sl[t]}));
-      const dd v = mul2_chk(rec, a);
-      xh[t] = v.h;
-      xl[t] = v.l;
-      const dd d = add2_chk(dd{dh[q], dl[q]}, mul2_chk(v, v));
-      dh[q] = d.h;
-      dl[q] = d.l;
+      T a = N::ld(xh, xl, t);
+      if (p.upper) a = N::add(a, N::neg(N::ld(sh, sl, t)));
+      const T v = N::mul(rec, a);
+      N::st(xh, xl, t, v);
+      N::st(dh, dl, q, N::add(N::ld(dh, dl, q), N::mul(v, v)));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -214,7 +121,7 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
       const int nthr = blockDim.x - 32;
       for (int base = threadIdx.x - 32; base < npairs; base += nthr * kB) {
         int xs[kB];
-        dd acc[kB], f1[kB], f2[kB];
+        T acc[kB], f1[kB], f2[kB];
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
           const int t = base + b * nthr;
@@ -227,17 +134,17 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
             const int qi = ci + 1 + (t - ci * (2 * rem - ci - 1) / 2);
             const int c = j + 1 + ci, q = j + 1 + qi;
             xs[b] = q + c * nb;
-            const dd vq{xh[q + j * nb], xl[q + j * nb]}, vc{xh[c + j * nb], xl[c + j * nb]};
-            if (!p.upper) { acc[b] = dd{xh[xs[b]], xl[xs[b]]}; f1[b] = neg2(vc); f2[b] = vq; }
-            else { acc[b] = dd{sh[xs[b]], sl[xs[b]]}; f1[b] = vq; f2[b] = vc; }
+            const T vq = N::ld(xh, xl, q + j * nb), vc = N::ld(xh, xl, c + j * nb);
+            if (!p.upper) { acc[b] = N::ld(xh, xl, xs[b]); f1[b] = N::neg(vc); f2[b] = vq; }
+            else { acc[b] = N::ld(sh, sl, xs[b]); f1[b] = vq; f2[b] = vc; }
           }
         }
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
           if (xs[b] < 0) continue;
-          const dd r = add2_chk(acc[b], mul2_chk(f1[b], f2[b]));
-          if (!p.upper) { xh[xs[b]] = r.h; xl[xs[b]] = r.l; }
-          else { sh[xs[b]] = r.h; sl[xs[b]] = r.l; }
+          const T r = N::add(acc[b], N::mul(f1[b], f2[b]));
+          if (!p.upper) N::st(xh, xl, xs[b], r);
+          else N::st(sh, sl, xs[b], r);
         }
       }
     }
@@ -250,8 +157,7 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
     const int q = t % nb, c = t / nb;
     if (q <= c) continue;
     const int64_t x = p.upper ? (j0 + c) + (j0 + q) * lda : (j0 + q) + (j0 + c) * lda;
-    p.a_hi[x] = xh[t];
-    p.a_lo[x] = xl[t];
+    N::st(p.a_hi, p.a_lo, x, N::ld(xh, xl, t));
   }
 }
 
@@ -266,9 +172,10 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
 constexpr int kPanelG = 32;          // lanes per row: one warp
 constexpr int kPanelThreads = 256;    // 8 rows per CTA
 
-template <int NPER>
+template <class N, int NPER>
 __global__ void __launch_bounds__(kPanelThreads)
 potrf_panel_kernel(PotrfArgs p, int64_t j0, int nb) {
+  using T = typename N::T;
   extern __shared__ double sm[];
   // a failure inside this block's diagonal part still leaves the columns
   // before it complete, as the reference does (chol.py:44-46)
@@ -291,62 +198,51 @@ potrf_panel_kernel(PotrfArgs p, int64_t j0, int nb) {
     const int c2 = t % nb, c = t / nb;
     if (c2 <= c) continue;
     const int64_t x = p.upper ? (j0 + c) + (j0 + c2) * lda : (j0 + c2) + (j0 + c) * lda;
-    th[off(c) + c2 - c - 1] = p.a_hi[x];
-    tl[off(c) + c2 - c - 1] = p.a_lo[x];
+    N::st(th, tl, off(c) + c2 - c - 1, N::ld(p.a_hi, p.a_lo, x));
   }
-  for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-    rh[c] = p.rec_hi[c];
-    rl[c] = p.rec_lo[c];
-  }
+  for (int c = threadIdx.x; c < nb; c += blockDim.x) N::st(rh, rl, c, N::ld(p.rec_hi, p.rec_lo, c));
   __syncthreads();
   const int lane = threadIdx.x % kPanelG;
   const int64_t q = j1 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPanelG;
   if (q >= p.n) return;                 // whole warps exit together
-  dd acc[NPER];
+  T acc[NPER];
 #pragma unroll
   for (int i = 0; i < NPER; ++i) {
     const int c = lane + kPanelG * i;
-    acc[i] = dd{0.0, 0.0};
+    acc[i] = N::zero();
     if (c < nb) {
       const int64_t x = p.upper ? q + (j0 + c) * lds : q + (j0 + c) * lda;
-      acc[i] = p.upper ? dd{p.s_hi[x], p.s_lo[x]} : dd{p.a_hi[x], p.a_lo[x]};
+      acc[i] = p.upper ? N::ld(p.s_hi, p.s_lo, x) : N::ld(p.a_hi, p.a_lo, x);
     }
   }
-  dd dq{0.0, 0.0};
-  if (lane == 0) dq = dd{p.dh[q], p.dl[q]};
+  T dq = N::zero();
+  if (lane == 0) dq = N::ld(p.dh, p.dl, q);
   for (int c = 0; c < ncols; ++c) {
     const int owner = c % kPanelG, ic = c / kPanelG;
-    dd v{0.0, 0.0};
+    T v = N::zero();
     if (lane == owner) {
-      dd a{0.0, 0.0};
+      T a = N::zero();
 #pragma unroll
       for (int i = 0; i < NPER; ++i)
         if (i == ic) a = acc[i];
-      const dd rec{rh[c], rl[c]};
+      const T rec = N::ld(rh, rl, c);
       const int64_t x = p.upper ? (j0 + c) + q * lda : q + (j0 + c) * lda;
-      if (p.upper) a = add2_chk(dd{p.a_hi[x], p.a_lo[x]}, neg2(a));
-      v = mul2_chk(rec, a);
-      p.a_hi[x] = v.h;
-      p.a_lo[x] = v.l;
+      if (p.upper) a = N::add(N::ld(p.a_hi, p.a_lo, x), N::neg(a));
+      v = N::mul(rec, a);
+      N::st(p.a_hi, p.a_lo, x, v);
     }
-    v.h = __shfl_sync(0xffffffffu, v.h, owner);
-    v.l = __shfl_sync(0xffffffffu, v.l, owner);
-    if (lane == 0) dq = add2_chk(dq, mul2_chk(v, v));
+    v = N::shfl(v, owner);
+    if (lane == 0) dq = N::add(dq, N::mul(v, v));
 #pragma unroll
     for (int i = 0; i < NPER; ++i) {
       const int c2 = lane + kPanelG * i;
       if (c2 > c && c2 < nb) {
-        const int o = off(c) + c2 - c - 1;
-        const dd t{th[o], tl[o]};
-        acc[i] = p.upper ? add2_chk(acc[i], mul2_chk(v, t))
-                         : add2_chk(acc[i], mul2_chk(neg2(t), v));
+        const T t = N::ld(th, tl, off(c) + c2 - c - 1);
+        acc[i] = p.upper ? N::add(acc[i], N::mul(v, t)) : N::add(acc[i], N::mul(N::neg(t), v));
       }
     }
   }
-  if (lane == 0) {
-    p.dh[q] = dq.h;
-    p.dl[q] = dq.l;
-  }
+  if (lane == 0) N::st(p.dh, p.dl, q, dq);
 }
 
 // T(r, l) = U(j0 + l, j1 + r), r < rows, l < nb  (ld = rows)
@@ -359,7 +255,7 @@ potrf_transpose_kernel(PotrfArgs p, int64_t j0, int64_t j1, int nb, int64_t rows
     if (r < rows && l < nb) {
       const int64_t x = (j0 + l) + (j1 + r) * p.lda;
       th[y][threadIdx.x] = p.a_hi[x];
-      tl[y][threadIdx.x] = p.a_lo[x];
+      if (!p.f64) tl[y][threadIdx.x] = p.a_lo[x];
     }
   }
   __syncthreads();
@@ -367,7 +263,7 @@ potrf_transpose_kernel(PotrfArgs p, int64_t j0, int64_t j1, int nb, int64_t rows
     const int64_t l = l0 + y, r = r0 + threadIdx.x;
     if (r < rows && l < nb) {
       p.t_hi[r + l * rows] = th[threadIdx.x][y];
-      p.t_lo[r + l * rows] = tl[threadIdx.x][y];
+      if (!p.f64) p.t_lo[r + l * rows] = tl[threadIdx.x][y];
     }
   }
 }
@@ -385,7 +281,7 @@ potrf_restore_kernel(PotrfArgs p) {
   for (int64_t c = f + blockIdx.y; c <= i && c < p.n; c += gridDim.y) {
     if (i == c && c == f) continue;
     p.a_hi[i + c * p.lda] = p.b_hi[i + c * p.n];
-    p.a_lo[i + c * p.lda] = p.b_lo[i + c * p.n];
+    if (!p.f64) p.a_lo[i + c * p.lda] = p.b_lo[i + c * p.n];
   }
 }
 
@@ -396,14 +292,18 @@ cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaSt
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(potrf_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(potrf_diag_kernel<NumDD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(potrf_diag_kernel<NumF64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
     attr_dev = dev;
   }
-  potrf_diag_kernel<<<1, 512, smem, s>>>(p, j0, nb);
+  if (p.f64) potrf_diag_kernel<NumF64><<<1, 512, smem, s>>>(p, j0, nb);
+  else potrf_diag_kernel<NumDD><<<1, 512, smem, s>>>(p, j0, nb);
   return cudaGetLastError();
 }
 
-template <int NPER>
+template <class N, int NPER>
 static cudaError_t panel_launch(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
                                 cudaStream_t s) {
   const size_t smem = sizeof(double) * ((size_t)nb * (nb - 1) + 2 * (size_t)nb);
@@ -411,13 +311,13 @@ static cudaError_t panel_launch(const PotrfArgs& p, int64_t j0, int nb, int64_t 
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(potrf_panel_kernel<NPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(potrf_panel_kernel<N, NPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_dev = dev;
   }
   const int64_t threads = rows * kPanelG;
-  potrf_panel_kernel<NPER><<<(unsigned)((threads + kPanelThreads - 1) / kPanelThreads),
-                             kPanelThreads, smem, s>>>(p, j0, nb);
+  potrf_panel_kernel<N, NPER><<<(unsigned)((threads + kPanelThreads - 1) / kPanelThreads),
+                                kPanelThreads, smem, s>>>(p, j0, nb);
   return cudaGetLastError();
 }
 
@@ -426,7 +326,8 @@ cudaError_t launch_potrf_panel(const PotrfArgs& p, int64_t j0, int nb, int64_t r
   if (rows <= 0) return cudaSuccess;
   const int nper = (nb + kPanelG - 1) / kPanelG;
   (void)nper;   // nb <= 64 = 2 * kPanelG
-  return panel_launch<2>(p, j0, nb, rows, s);
+  return p.f64 ? panel_launch<NumF64, 2>(p, j0, nb, rows, s)
+               : panel_launch<NumDD, 2>(p, j0, nb, rows, s);
 }
 
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,

@@ -97,6 +97,7 @@ cudaError_t launch_zgemm(const ZgemmArgs& g, cudaStream_t s);
 struct PotrfArgs {
   int64_t n, lda;
   int upper;
+  int f64;                      // binary64 matrix (one plane; the *_lo pointers unused)
   double *a_hi, *a_lo;
   const double *d0_hi, *d0_lo;  // original diagonal
   double *dh, *dl;              // pivot dot products accumulated so far
@@ -121,6 +122,7 @@ cudaError_t launch_potrf_restore(const PotrfArgs& p, cudaStream_t s);
 struct TrsmArgs {
   int64_t p, q;
   int left, rev, unit, fin_rec;
+  int f64;                      // binary64 (one plane; the *_lo pointers unused)
   double *w_hi, *w_lo; int64_t ldw;
   double *t_hi, *t_lo; int64_t ldt;
   double *d_hi, *d_lo;
@@ -144,6 +146,7 @@ struct PermBuf {                // a composed row interchange (laswp)
 
 struct GetrfArgs {
   int64_t m, n, mn, lda;
+  int f64;                      // binary64 (one plane; a_lo unused)
   double *a_hi, *a_lo;
   long long* ipiv;              // 1-based pivot rows (device)
   long long* swap;              // interchange actually applied at step j (j = none)

@@ -22,7 +22,9 @@ with the later entries as the reference leaves them.  Keywords:
 
 ``a`` is a dd ``DeviceMatrix`` (asynchronous up to the final info read) or a
 host matrix (``HostMatrix`` / the reference's Matrix; staged through HBM).
-Other precisions raise NotImplementedError; there is no CPU fallback.
+binary64 ('f64') matrices run the same algorithms in the F64 backend's IEEE
+arithmetic, bit-identical to the reference (``mode`` does not apply).  Other
+precisions raise NotImplementedError; there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -34,6 +36,18 @@ from .matrix import check_storage, require
 from .mpblas import _HostPlanes, _dev_ptr, _mode_code, _placement, _raise_rc
 
 __all__ = ["Rpotrf", "Rgetrf", "Rgetrs", "PivotVector"]
+
+
+def _precision(routine, *mats):
+    """True for the reference's binary64 Matrix ('f64'), False for 'dd'."""
+    tags = {m.precision for m in mats}
+    if len(tags) > 1:
+        raise ValueError(f"{routine}: mixed precisions {sorted(tags)}")
+    tag = tags.pop()
+    if tag not in ("dd", "f64"):
+        raise NotImplementedError(
+            f"{routine}: precision {tag!r} is not on the B200 path (only 'dd' and 'f64')")
+    return tag == "f64"
 
 
 class PivotVector:
@@ -74,9 +88,7 @@ def Rgetrf(m, n, a, lda=None, *, mode=None):
     require(routine, lda >= max(1, m), 4)
     if m == 0 or n == 0:                                            # lu.py:86-87
         return PivotVector(), 0
-    if a.precision != "dd":
-        raise NotImplementedError(
-            f"{routine}: precision {a.precision!r} is not on the B200 path (only 'dd')")
+    f64 = _precision(routine, a)
     code = _mode_code(mode)
     check_storage(a, m, n, lda)
     L = _lib.load()
@@ -88,13 +100,19 @@ def Rgetrf(m, n, a, lda=None, *, mode=None):
         import torch
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
-            rc = L.ddb_rgetrf(m, n, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, ipiv,
-                              ctypes.byref(info), code, stream)
+            if f64:
+                rc = L.ddb_dgetrf(m, n, _dev_ptr(a, 0), lda, ipiv, ctypes.byref(info), stream)
+            else:
+                rc = L.ddb_rgetrf(m, n, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, ipiv,
+                                  ctypes.byref(info), code, stream)
         _raise_rc(routine, rc)
     else:
-        ha = _HostPlanes(a.store)
-        rc = L.ddb_rgetrf_host(m, n, ha.ptr(0), ha.ptr(1), lda, ipiv, ctypes.byref(info), code,
-                               None)
+        ha = _HostPlanes(a.store, 1 if f64 else 2)
+        if f64:
+            rc = L.ddb_dgetrf_host(m, n, ha.ptr(0), lda, ipiv, ctypes.byref(info), None)
+        else:
+            rc = L.ddb_rgetrf_host(m, n, ha.ptr(0), ha.ptr(1), lda, ipiv, ctypes.byref(info),
+                                   code, None)
         _raise_rc(routine, rc)
         ha.commit()
     return PivotVector(ipiv[:]), int(info.value)
@@ -110,9 +128,7 @@ def Rpotrf(uplo, n, a, lda=None, *, mode=None, nb=0):
     require(routine, lda >= max(1, n), 4)                           # chol.py:29
     if n == 0:                                                      # chol.py:30-31
         return 0
-    if a.precision != "dd":
-        raise NotImplementedError(
-            f"{routine}: precision {a.precision!r} is not on the B200 path (only 'dd')")
+    f64 = _precision(routine, a)
     code = _mode_code(mode)
     check_storage(a, n, n, lda)
     L = _lib.load()
@@ -122,13 +138,20 @@ def Rpotrf(uplo, n, a, lda=None, *, mode=None, nb=0):
         import torch
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
-            rc = L.ddb_rpotrf(uplo.encode(), n, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, int(nb),
-                              code, stream, ctypes.byref(info))
+            if f64:
+                rc = L.ddb_dpotrf(uplo.encode(), n, _dev_ptr(a, 0), lda, int(nb), stream,
+                                  ctypes.byref(info))
+            else:
+                rc = L.ddb_rpotrf(uplo.encode(), n, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, int(nb),
+                                  code, stream, ctypes.byref(info))
         _raise_rc(routine, rc)
         return int(info.value)
-    ha = _HostPlanes(a.store)
-    rc = L.ddb_rpotrf_host(uplo.encode(), n, ha.ptr(0), ha.ptr(1), lda, int(nb), code, None,
-                           ctypes.byref(info))
+    ha = _HostPlanes(a.store, 1 if f64 else 2)
+    if f64:
+        rc = L.ddb_dpotrf_host(uplo.encode(), n, ha.ptr(0), lda, int(nb), None, ctypes.byref(info))
+    else:
+        rc = L.ddb_rpotrf_host(uplo.encode(), n, ha.ptr(0), ha.ptr(1), lda, int(nb), code, None,
+                               ctypes.byref(info))
     _raise_rc(routine, rc)
     ha.commit()
     return int(info.value)
@@ -149,8 +172,7 @@ def Rgetrs(trans, n, nrhs, a, lda=None, ipiv=None, b=None, ldb=None, *, mode=Non
     require(routine, ldb is not None and ldb >= max(1, n), 8)
     if n == 0 or nrhs == 0:                                         # lu.py:130-131
         return 0
-    if a.precision != "dd" or b.precision != "dd":
-        raise NotImplementedError(f"{routine}: only 'dd' is on the B200 path")
+    f64 = _precision(routine, a, b)
     code = _mode_code(mode)
     check_storage(b, n, nrhs, ldb)
     piv = (ctypes.c_int64 * n)(*[int(p) for p in list(ipiv)[:n]])
@@ -160,13 +182,21 @@ def Rgetrs(trans, n, nrhs, a, lda=None, ipiv=None, b=None, ldb=None, *, mode=Non
         import torch
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
-            rc = L.ddb_rgetrs(trans.encode(), n, nrhs, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, piv,
-                              _dev_ptr(b, 0), _dev_ptr(b, 1), ldb, code, stream)
+            if f64:
+                rc = L.ddb_dgetrs(trans.encode(), n, nrhs, _dev_ptr(a, 0), lda, piv,
+                                  _dev_ptr(b, 0), ldb, stream)
+            else:
+                rc = L.ddb_rgetrs(trans.encode(), n, nrhs, _dev_ptr(a, 0), _dev_ptr(a, 1), lda,
+                                  piv, _dev_ptr(b, 0), _dev_ptr(b, 1), ldb, code, stream)
         _raise_rc(routine, rc)
         return 0
-    ha, hb = _HostPlanes(a.store), _HostPlanes(b.store)
-    rc = L.ddb_rgetrs_host(trans.encode(), n, nrhs, ha.ptr(0), ha.ptr(1), lda, piv, hb.ptr(0),
-                           hb.ptr(1), ldb, code, None)
+    np_ = 1 if f64 else 2
+    ha, hb = _HostPlanes(a.store, np_), _HostPlanes(b.store, np_)
+    if f64:
+        rc = L.ddb_dgetrs_host(trans.encode(), n, nrhs, ha.ptr(0), lda, piv, hb.ptr(0), ldb, None)
+    else:
+        rc = L.ddb_rgetrs_host(trans.encode(), n, nrhs, ha.ptr(0), ha.ptr(1), lda, piv,
+                               hb.ptr(0), hb.ptr(1), ldb, code, None)
     _raise_rc(routine, rc)
     hb.commit()
     return 0

@@ -250,9 +250,8 @@ def Rtrsm(side, uplo, transa, diag, m, n, alpha, a, lda=None, b=None, ldb=None, 
     with fast-mode GEMM updates (dd accuracy, not bit-identical)."""
     routine = "Rtrsm"
     tag = same_precision(routine, a, b)
-    if tag != "dd":
-        raise NotImplementedError(
-            f"{routine}: precision {tag!r} is not on the B200 path (only 'dd')")
+    _precision_gate(routine, tag)
+    f64 = tag == "f64"
     lda, ldb = _ld_of(a, lda), _ld_of(b, ldb)
     side = _flag(routine, side, ("L", "R"), 1)
     uplo = _flag(routine, uplo, ("U", "L"), 2)
@@ -271,17 +270,25 @@ def Rtrsm(side, uplo, transa, diag, m, n, alpha, a, lda=None, b=None, ldb=None, 
     check_storage(b, m, n, ldb)
     L = _lib.load()
     dev = _placement(routine, a, b)
-    head = (side.encode(), uplo.encode(), transa.encode(), diag.encode(), m, n, al[0], al[1])
+    flags = (side.encode(), uplo.encode(), transa.encode(), diag.encode(), m, n)
     if dev is not None:
         import torch
         with torch.cuda.device(dev):
             stream = torch.cuda.current_stream(dev).cuda_stream
-            rc = L.ddb_rtrsm(*head, _dev_ptr(a, 0), _dev_ptr(a, 1), lda, _dev_ptr(b, 0),
-                             _dev_ptr(b, 1), ldb, code, stream)
+            if f64:
+                rc = L.ddb_dtrsm(*flags, al[0], _dev_ptr(a, 0), lda, _dev_ptr(b, 0), ldb, stream)
+            else:
+                rc = L.ddb_rtrsm(*flags, al[0], al[1], _dev_ptr(a, 0), _dev_ptr(a, 1), lda,
+                                 _dev_ptr(b, 0), _dev_ptr(b, 1), ldb, code, stream)
         _raise_rc(routine, rc)
         return
-    ha, hb = _HostPlanes(a.store), _HostPlanes(b.store)
-    rc = L.ddb_rtrsm_host(*head, ha.ptr(0), ha.ptr(1), lda, hb.ptr(0), hb.ptr(1), ldb, code, None)
+    np_ = 1 if f64 else 2
+    ha, hb = _HostPlanes(a.store, np_), _HostPlanes(b.store, np_)
+    if f64:
+        rc = L.ddb_dtrsm_host(*flags, al[0], ha.ptr(0), lda, hb.ptr(0), ldb, None)
+    else:
+        rc = L.ddb_rtrsm_host(*flags, al[0], al[1], ha.ptr(0), ha.ptr(1), lda, hb.ptr(0),
+                              hb.ptr(1), ldb, code, None)
     _raise_rc(routine, rc)
     hb.commit()
 

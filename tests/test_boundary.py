@@ -213,6 +213,7 @@ def test_rpotrf_early_exit_and_precision_gate():
     assert Rpotrf("U", 0, a, 1) == 0
     assert np.all(a.store[0] == 7.0)
     b = HostMatrix(3, 3, "f64")
+    b.precision = "qd"
     with pytest.raises(NotImplementedError):
         Rpotrf("L", 3, b)
 
@@ -266,10 +267,12 @@ def test_rtrsm_early_exit_and_precision_gate():
     Rtrsm("R", "L", "T", "U", 3, 0, 2.0, a, 3, b, 3)
     assert np.all(b.store[0] == 7.0)
     c = HostMatrix(3, 3, "f64")
-    with pytest.raises(NotImplementedError):
-        Rtrsm("L", "U", "N", "N", 3, 3, 1.0, c, 3, HostMatrix(3, 3, "f64"), 3)
     with pytest.raises(ValueError, match="mixed precisions"):
         Rtrsm("L", "U", "N", "N", 3, 3, 1.0, a, 3, c, 3)
+    q = HostMatrix(3, 3)
+    q.precision = "qd"
+    with pytest.raises(NotImplementedError):
+        Rtrsm("L", "U", "N", "N", 3, 3, 1.0, q, 3, q, 3)
 
 
 @pytest.mark.parametrize("args,idx", [((-1, 2, 2), 1), ((2, -1, 2), 2), ((3, 2, 2), 4),
@@ -294,8 +297,10 @@ def test_rgetrf_early_exit_and_precision_gate():
     ipiv, info = Rgetrf(0, 3, a, 3)
     assert ipiv == [] and info == 0 and isinstance(ipiv, PivotVector)
     assert Rgetrf(3, 0, a) == (PivotVector(), 0)
+    q = HostMatrix(3, 3)
+    q.precision = "qd"
     with pytest.raises(NotImplementedError):
-        Rgetrf(3, 3, HostMatrix(3, 3, "f64"))
+        Rgetrf(3, 3, q)
 
 
 @pytest.mark.parametrize("args,lds,idx", [(("X", 2, 1), {}, 1), (("N", -1, 1), {}, 2),

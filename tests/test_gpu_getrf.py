@@ -15,7 +15,7 @@ from paper_2109_13406_b200.synth import random_dd
 
 pytestmark = pytest.mark.gpu
 
-LCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rgetrf"]
+LCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rgetrf" and c[0].get("precision") != "f64"]
 
 
 def bits_equal(a, b):
@@ -98,7 +98,7 @@ def test_rgetrf_fast_modes_close_to_exact(m, n, mode):
     assert np.abs(diff).max() <= 1e-26 * scale, np.abs(diff).max() / scale
 
 
-SCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rgetrs"]
+SCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rgetrs" and c[0].get("precision") != "f64"]
 
 
 @pytest.mark.parametrize("mode", ["exact", "reference"])

@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 EPS_DD = float.fromhex("0x1.ffffffffffff9p-105")   # machine_params("dd").eps
 THRESHOLD = 30.0
 
-PCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rpotrf"]
+PCASES = [c for c in golden.load_cases() if c[0]["routine"] == "Rpotrf" and c[0].get("precision") != "f64"]
 
 
 def bits_equal(a, b):

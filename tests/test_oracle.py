@@ -17,10 +17,12 @@ def bits_equal(a, b):
 
 ALL = list(golden.load_cases())
 CASES = [c for c in ALL if c[0]["routine"] in ("Rgemm", "Rsyrk")]
-PCASES = [c for c in ALL if c[0]["routine"] == "Rpotrf"]
-TCASES = [c for c in ALL if c[0]["routine"] == "Rtrsm"]
-LCASES = [c for c in ALL if c[0]["routine"] == "Rgetrf"]
-SCASES = [c for c in ALL if c[0]["routine"] == "Rgetrs"]
+PCASES = [c for c in ALL if c[0]["routine"] == "Rpotrf" and c[0].get("precision") != "f64"]
+TCASES = [c for c in ALL if c[0]["routine"] == "Rtrsm" and c[0].get("precision") != "f64"]
+LCASES = [c for c in ALL if c[0]["routine"] == "Rgetrf" and c[0].get("precision") != "f64"]
+SCASES = [c for c in ALL if c[0]["routine"] == "Rgetrs" and c[0].get("precision") != "f64"]
+FCASES = [c for c in ALL if c[0]["routine"] in ("Rpotrf", "Rtrsm", "Rgetrf", "Rgetrs")
+          and c[0].get("precision") == "f64"]
 CCASES = [c for c in ALL if c[0]["routine"] == "Cgemm"]
 
 
@@ -218,3 +220,34 @@ def test_oracle_rgetrs_matches_reference_bitwise(idx):
     assert oracle.rgetrs(case["trans"], n, nrhs, ah, al, case["lda"], ipiv, bh, bl,
                          case["ldb"]) == 0
     assert bits_equal(bh, out_hi) and bits_equal(bl, out_lo), case
+
+
+@pytest.mark.parametrize("idx", range(len(FCASES)))
+def test_oracle_lapack_f64_matches_reference_bitwise(idx):
+    """Rpotrf / Rtrsm / Rgetrf / Rgetrs on the F64 backend, restated in C."""
+    case, arr, out_hi, _ = FCASES[idx]
+    assert golden.input_digest(arr) == case["input_sha256"]
+    r = case["routine"]
+    with np.errstate(all="ignore"):
+        if r == "Rpotrf":
+            a = arr["A_hi"].copy()
+            rc, info = oracle.dpotrf(case["uplo"], case["n"], a, case["lda"])
+            assert rc == 0 and info == case["info"]
+            got = a
+        elif r == "Rtrsm":
+            got = arr["B_hi"].copy()
+            assert oracle.dtrsm(case["side"], case["uplo"], case["transa"], case["diag"],
+                                case["m"], case["n"], case["alpha_v"][0], arr["A_hi"],
+                                case["lda"], got, case["ldb"]) == 0
+        elif r == "Rgetrf":
+            got = arr["A_hi"].copy()
+            rc, ipiv, info = oracle.dgetrf(case["m"], case["n"], got, case["lda"])
+            assert rc == 0 and ipiv == case["ipiv"] and info == case["info"]
+        else:
+            a = arr["A_hi"].copy()
+            _, ipiv, _ = oracle.dgetrf(case["n"], case["n"], a, case["lda"])
+            assert ipiv == case["ipiv"]
+            got = arr["B_hi"].copy()
+            assert oracle.dgetrs(case["trans"], case["n"], case["nrhs"], a, case["lda"], ipiv,
+                                 got, case["ldb"]) == 0
+    assert bits_equal(got, out_hi), case
