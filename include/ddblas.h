@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DDB_VERSION 100
+#define DDB_VERSION 120   /* 1.2: LAPACK consumers (dd + f64), multi-GPU C entry points */
 
 #define DDB_OK 0
 #define DDB_EINVAL (-1)   /* bad mode / internal argument */
