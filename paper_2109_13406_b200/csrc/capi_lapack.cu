@@ -100,18 +100,20 @@ static int rtrsm_impl(bool f64, char side, char uplo, char transa, char diag, in
   retain_pool_memory();
   const size_t wsz = (size_t)t.p * t.q, tsz = (size_t)t.p * t.p;
   void* ws = nullptr;
-  e = cudaMallocAsync(&ws, sizeof(double) * 2 * (wsz + tsz + t.p), s);
+  e = cudaMallocAsync(&ws, sizeof(double) * 2 * (wsz + tsz + 2 * t.p), s);
   if (e != cudaSuccess) return fail(e, "rtrsm workspace");
   double* w = static_cast<double*>(ws);
   t.w_hi = w; t.w_lo = w + wsz;
   t.t_hi = w + 2 * wsz; t.t_lo = t.t_hi + tsz;
   t.d_hi = t.t_lo + tsz; t.d_lo = t.d_hi + t.p;
+  t.r_hi = t.d_lo + t.p; t.r_lo = t.r_hi + t.p;
+  // binary64 is always in the reference's order
+  const bool exact_order = f64 || mode == MODE_EXACT || mode == MODE_REFERENCE;
+  t.rec_fast = !exact_order;
   int nl = 0, rc2 = DDB_OK;
   e = launch_trsm_pack(t, b_hi, b_lo, ldb, init_scale, alpha, s);
   ++nl;
   if (e == cudaSuccess) { e = launch_trsm_coef(t, a_hi, a_lo, lda, trans, s); ++nl; }
-  // binary64 is always in the reference's order
-  const bool exact_order = f64 || mode == MODE_EXACT || mode == MODE_REFERENCE;
   if (e == cudaSuccess && rev_terms && exact_order) {
     e = launch_trsm_rev(t, s);
     ++nl;

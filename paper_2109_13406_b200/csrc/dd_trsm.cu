@@ -32,12 +32,17 @@ namespace ddb {
 
 namespace {
 
+// fin_s: unit diagonal -> v; the R branches -> (one / A(s,s)) * v with the
+// reciprocal formed once per s by trsm_coef_kernel (be.div(one, aelt) then
+// be.mul, level23.py:361-362, :368-369 -- the same bits); the L branches ->
+// v / A(s,s) (be.div, :332) in the reference's order, or, in the fast
+// modes, the precomputed reciprocal times v (dd accuracy, one division per
+// s instead of one per element)
 template <class N>
 __device__ __forceinline__ typename N::T trsm_fin(const TrsmArgs& t, int64_t s, typename N::T v) {
   if (t.unit) return v;
-  const typename N::T d = N::ld(t.d_hi, t.d_lo, s);
-  if (t.fin_rec) return N::mul(N::vdiv(N::one(), d), v);   // be.div(one, A(j,j)) * B
-  return N::vdiv(v, d);                                     // be.div(B, A(k,k))
+  if (t.fin_rec || t.rec_fast) return N::mul(N::ld(t.r_hi, t.r_lo, s), v);
+  return N::vdiv(v, N::ld(t.d_hi, t.d_lo, s));
 }
 
 }  // namespace
@@ -92,8 +97,13 @@ trsm_coef_kernel(TrsmArgs t, const double* __restrict__ ah, const double* __rest
     if (c > s) continue;
     const int64_t os = t.rev ? t.p - 1 - s : s, oc = t.rev ? t.p - 1 - c : c;
     const int64_t x = trans ? oc + os * lda : os + oc * lda;
-    if (c == s) N::st(t.d_hi, t.d_lo, s, N::ld(ah, al, x));
-    else N::st(t.t_hi, t.t_lo, s + c * t.ldt, N::ld(ah, al, x));
+    if (c == s) {
+      const typename N::T d = N::ld(ah, al, x);
+      N::st(t.d_hi, t.d_lo, s, d);
+      if (!t.unit && (t.fin_rec || t.rec_fast)) N::st(t.r_hi, t.r_lo, s, N::vdiv(N::one(), d));
+    } else {
+      N::st(t.t_hi, t.t_lo, s + c * t.ldt, N::ld(ah, al, x));
+    }
   }
 }
 

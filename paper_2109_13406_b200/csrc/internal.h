@@ -126,6 +126,8 @@ struct TrsmArgs {
   double *w_hi, *w_lo; int64_t ldw;
   double *t_hi, *t_lo; int64_t ldt;
   double *d_hi, *d_lo;
+  double *r_hi, *r_lo;          // 1 / A(s,s) per s (the R branches; the L ones in fast modes)
+  int rec_fast;                 // fast modes: L branches finish with the reciprocal too
 };
 
 cudaError_t launch_trsm_pack(const TrsmArgs& t, const double* bh, const double* bl, int64_t ldb,
