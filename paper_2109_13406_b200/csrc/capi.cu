@@ -298,7 +298,8 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
     const char* v = std::getenv("DDB_HOST_PIPELINE");
     return v ? (int64_t)std::atoll(v) : (int64_t)-1;
   }();
-  int64_t nblk = pipe_env >= 0 ? pipe_env : (n >= 2048 && (double)m * n * k >= 1e10 ? 4 : 0);
+  int64_t nblk = pipe_env >= 0 ? pipe_env
+                              : (n >= 2048 && (double)m * n * k >= 1e10 ? (n >= 8192 ? 8 : 4) : 0);
   if (nblk > 1 && mode != MODE_REFERENCE && k > 0 && !is_zero(alpha_hi, alpha_lo) &&
       is_pinned(a_hi) && is_pinned(b_hi) && is_pinned(c_hi)) {
     cudaStream_t h2d = nullptr, d2h = nullptr;
