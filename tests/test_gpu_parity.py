@@ -620,3 +620,26 @@ def test_rsyrk_mgpu_matches_single_call(up, tr, ndev):
     torch.cuda.synchronize()
     assert bits_equal(d[2].cpu().numpy(), ref[0].cpu().numpy())
     assert bits_equal(d[3].cpu().numpy(), ref[1].cpu().numpy())
+
+
+@pytest.mark.parametrize("ta,tb", [("T", "N"), ("T", "T"), ("N", "N")])
+def test_host_pipelined_fast_within_bound(ta, tb):
+    """The pipelined host path streams the first column block's k in panels
+    (fast modes, any transa): still inside the certified bound."""
+    m, n, k = 512, 2048, 9728                   # m n k >= 1e10, k >= 4096: k-panels
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A, B, C = random_dd(nra, nca, nra, 8, 1), random_dd(nrb, ncb, nrb, 8, 2), random_dd(m, n, m, 8, 3)
+    hm = []
+    for (r, c, planes) in ((nra, nca, A), (nrb, ncb, B), (m, n, C)):
+        h = HostMatrix(r, c, "dd", r, pinned=True)
+        h.store[0][:] = planes[0]
+        h.store[1][:] = planes[1]
+        hm.append(h)
+    alpha, beta = (1.5, 2 ** -60), (0.5, 0.0)
+    Rgemm(ta, tb, m, n, k, _Scalar(alpha), hm[0], nra, hm[1], nrb, _Scalar(beta), hm[2], m,
+          mode="fast")
+    I, J = [0, 97, 255, 511], [0, 5, 300, 1023, 2047]      # J spans the first column block
+    vals, scales = exact.exact_entries(ta, tb, k, alpha, A[0], A[1], nra, B[0], B[1], nrb, beta,
+                                       C[0], C[1], m, I, J)
+    assert exact.error_ratios(hm[2].store[0], hm[2].store[1], m, I, J, vals, scales, k) < 0.25
