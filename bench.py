@@ -310,6 +310,7 @@ def run_ours(args):
             extra["modes"] = _modes(n, k, dev, stream, A, B, C, C0, mode)
             extra["f64"] = _f64(n, dev, stream)
             extra["cgemm"] = _cgemm(n // 2, dev, stream, mode)
+            extra["trans_sweep"] = _trans_sweep(n // 2, dev, stream, mode)
             extra["rpotrf"] = _rpotrf(n, dev, stream, mode)
             extra["rgetrf"] = _rgetrf(n, dev, stream, mode)
             extra["rtrsm"] = _rtrsm(n, dev, stream, mode)
@@ -427,6 +428,20 @@ def _f64(n, dev, stream):
     t = min(times)
     return {"workload": f"f64 Rgemm NN m=n=k={n}", "value": 2.0 * n ** 3 / t / 1e9,
             "unit": "GFlops (binary64)", "ms": t * 1e3}
+
+
+def _trans_sweep(n, dev, stream, mode):
+    """BASELINE configs[1]: Rgemm m = n = k over NN / NT / TN / TT."""
+    from paper_2109_13406_b200 import DeviceMatrix, Rgemm
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    mats = [DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, t, dev)) for t in (1, 2, 3)]
+    out = {"workload": f"dd Rgemm m=n=k={n}", "unit": UNIT, "mode": mode}
+    for ta in "NT":
+        for tb in "NT":
+            times = timed(lambda: Rgemm(ta, tb, n, n, n, ALPHA, mats[0], n, mats[1], n, BETA,
+                                        mats[2], n, mode=mode), 2, 1, stream)
+            out[ta + tb] = 2.0 * n ** 3 / min(times) / 1e9
+    return out
 
 
 def _cgemm(n, dev, stream, mode):

@@ -240,7 +240,11 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   // row j [2][2 nb]
   auto cand = [&](int par, int c) { return g.rowbuf + ((size_t)par * G + c) * 2 * nb; };
   auto jrow = [&](int par) { return g.rowbuf + (size_t)2 * G * 2 * nb + (size_t)par * 2 * nb; };
-  auto publish = [&](int jj) {        // search column jj, publish candidate (+ row j0+jj)
+  // search column jj, publish the candidate (+ row j0 + jj).  Columns > upd
+  // of the published rows are sent with step jj - 1's rank-1 update applied
+  // (the same add2 / mul2 the bulk update below performs on them later), so
+  // the CTA can arrive at the barrier before its bulk update.
+  auto publish = [&](int jj, int upd) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
     PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
@@ -261,23 +265,43 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
       g.part_idx[slot] = k.idx;
       g.part_nan[slot] = k.nan;
     }
-    if (k.idx >= 0) {
-      double* cr = cand(par, blockIdx.x);
-      const int rr = (int)(k.idx - r0);
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) N::st(cr, cr + nb, c, N::ld(xh, xl, rr + c * ch));
-    }
-    if (owner(j) == (int)blockIdx.x) {
-      double* jr = jrow(par);
-      for (int c = threadIdx.x; c < nb; c += blockDim.x)
-        N::st(jr, jr + nb, c, N::ld(xh, xl, (j - r0) + c * ch));
+    auto row_out = [&](double* out, int rr) {
+      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+        T v = N::ld(xh, xl, rr + c * ch);
+        if (c > upd) v = N::add(v, N::mul(N::ld(xh, xl, rr + (jj - 1) * ch), N::neg(N::ld(ph, pl, c))));
+        N::st(out, out + nb, c, v);
+      }
+    };
+    if (k.idx >= 0) row_out(cand(par, blockIdx.x), (int)(k.idx - r0));
+    if (owner(j) == (int)blockIdx.x) row_out(jrow(par), (int)(j - r0));
+  };
+  // arrive / wait halves of grid_barrier
+  auto arrive = [&]() {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(g.bar, 1u);
     }
   };
-  publish(0);
+  auto wait = [&](unsigned target) {
+    if (threadIdx.x == 0) {
+      while (true) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(g.bar) : "memory");
+        if (v >= target) break;
+        __nanosleep(20);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  };
+  publish(0, nb);
+  arrive();
   unsigned nbar = 0;
   for (int jj = 0; jj < nb; ++jj) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
-    grid_barrier(g.bar, G * ++nbar);
+    wait(G * ++nbar);
     if (threadIdx.x < 32) {
       PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
       for (int c = threadIdx.x; c < G; c += 32) {
@@ -301,16 +325,9 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     const bool swapped = !best_s.nan && N::nonzero(N::make(best_s.h, best_s.l)) && jp != j;
     const double* src = swapped ? cand(par, owner(jp)) : jrow(par);
     const double* jr = jrow(par);
-    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-      const T v = N::ldcg(src, src + nb, c);
-      N::st(ph, pl, c, v);
-      if (owner(j) == (int)blockIdx.x) N::st(xh, xl, (j - r0) + c * ch, v);
-      if (swapped && owner(jp) == (int)blockIdx.x)
-        N::st(xh, xl, (jp - r0) + c * ch, N::ldcg(jr, jr + nb, c));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const T piv = N::ld(ph, pl, jj);
+    // the pivot (entry jj of the pivot row) on the last warp, idle in the row fetch (nb <= 64)
+    if (threadIdx.x == blockDim.x - 1) {
+      const T piv = N::ldcg(src, src + nb, jj);
       nonzero_s = N::nonzero(piv);
       use_rec_s = N::ge_safmin(piv);                       // |pivot| >= safmin (lu.py:98)
       if (nonzero_s && use_rec_s) rec_s = N::sdiv(N::one(), piv);
@@ -319,6 +336,13 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
         g.swap[j] = swapped ? jp : j;
         if (!nonzero_s && *g.info == 0) *g.info = (int)(j + 1);
       }
+    }
+    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+      const T v = N::ldcg(src, src + nb, c);
+      N::st(ph, pl, c, v);
+      if (owner(j) == (int)blockIdx.x) N::st(xh, xl, (j - r0) + c * ch, v);
+      if (swapped && owner(jp) == (int)blockIdx.x)
+        N::st(xh, xl, (jp - r0) + c * ch, N::ldcg(jr, jr + nb, c));
     }
     __syncthreads();
     const bool nonzero = nonzero_s;
@@ -331,19 +355,23 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
         N::st(xh, xl, r + jj * ch, use_rec ? N::mul(rec, x) : N::vdiv(x, piv));
       }
     }
+    if (jj + 1 == nb) break;              // (j < mn - 1 holds below: the panel lies inside mn)
     __syncthreads();
-    const int ncol = nb - jj - 1, nrow = nr - rs;
-    if (ncol > 0 && nrow > 0 && j < g.mn - 1) {
-      for (int t = threadIdx.x; t < ncol * nrow; t += blockDim.x) {
-        const int r = rs + t % nrow, c = jj + 1 + t / nrow;
-        const T x = N::ld(xh, xl, r + jj * ch);
-        N::st(xh, xl, r + c * ch,
-              N::add(N::ld(xh, xl, r + c * ch), N::mul(x, N::neg(N::ld(ph, pl, c)))));
-      }
-    }
+    // column jj + 1 first: the next search needs it
+    auto upd = [&](int r, int c) {
+      const T x = N::ld(xh, xl, r + jj * ch);
+      N::st(xh, xl, r + c * ch, N::add(N::ld(xh, xl, r + c * ch), N::mul(x, N::neg(N::ld(ph, pl, c)))));
+    };
+    for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) upd(r, jj + 1);
     __syncthreads();
-    if (jj + 1 < nb) publish(jj + 1);
+    publish(jj + 1, jj + 1);
+    arrive();
+    // the rest of the rank-1 update overlaps the other CTAs' arrival
+    const int ncol = nb - jj - 2, nrow = nr - rs;
+    if (ncol > 0 && nrow > 0)
+      for (int t = threadIdx.x; t < ncol * nrow; t += blockDim.x) upd(rs + t % nrow, jj + 2 + t / nrow);
   }
+  __syncthreads();
   for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
     const int r = t % nr, c = t / nr;
     N::st(g.a_hi, g.a_lo, (r0 + r) + (j0 + c) * lda, N::ld(xh, xl, r + c * ch));
