@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/ddblas.h"
@@ -273,6 +274,21 @@ cudaError_t copy_streams(cudaStream_t* h2d, cudaStream_t* d2h) {
   return cudaSuccess;
 }
 
+// C(i, j) <- add2(C(i, j), T(i, j)): folds the first column block's early
+// k panels (accumulated in T while its C columns were still in flight) into C
+__global__ void __launch_bounds__(256)
+fold_block_kernel(int64_t m, int64_t w, double* __restrict__ ch, double* __restrict__ cl,
+                  int64_t ldc, const double* __restrict__ th, const double* __restrict__ tl) {
+  const int64_t total = m * w;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m, x = i + j * ldc;
+    const dd r = add2_chk(dd{ch[x], cl[x]}, dd{th[e], tl[e]});
+    ch[x] = r.h;
+    cl[x] = r.l;
+  }
+}
+
 }  // namespace
 
 int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
@@ -319,13 +335,35 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventRecord(ev0, s);             // allocations ready
     if (e == cudaSuccess) e = cudaStreamWaitEvent(h2d, ev0, 0);
+    // DDB_HOST_TRACE=1: timing events after every copy group / GEMM, printed
+    // to stderr at the end (ms from the start; development aid)
+    static const bool trace = std::getenv("DDB_HOST_TRACE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    cudaEvent_t t0ev = nullptr;
+    auto mark = [&](const std::string& what, cudaStream_t st) {
+      if (!trace) return;
+      cudaEvent_t ev;
+      if (cudaEventCreate(&ev) != cudaSuccess) return;
+      cudaEventRecord(ev, st);
+      tev.emplace_back(what, ev);
+    };
+    if (trace && cudaEventCreate(&t0ev) == cudaSuccess) cudaEventRecord(t0ev, s);
     // Block 0 also streams k in panels, so that its first GEMM waits only for
     // the first panel of op(A) (the rest of A arrives while it runs): beta
     // applies to the first panel, 1 to the others -- for transa = 'N' the
     // reference's own axpy order (exact mode stays bitwise), for 'T' only in
     // the fast modes.  Later blocks find A resident and run full depth.
     const int64_t step = ((n + nblk - 1) / nblk + 63) / 64 * 64;
-    const int kch0 = (k >= 4096 && (na || mode != MODE_EXACT)) ? 4 : 1;
+    const int kch0 = (k >= 4096 && (na || mode != MODE_EXACT)) ? (k >= 8192 ? 8 : 4) : 1;
+    // Fast modes also defer block 0's C columns: its early k panels
+    // accumulate into a scratch T (beta = 0, then 1), the last panel applies
+    // beta to C, and T is folded in with one add2 per element -- the first
+    // GEMM then waits only for one panel of A and B.
+    const bool defer_c = read_c && kch0 > 1 && mode != MODE_EXACT;
+    double* tbuf = nullptr;
+    const int64_t w0 = step < n ? step : n;
+    if (defer_c && e == cudaSuccess)
+      e = cudaMallocAsync(reinterpret_cast<void**>(&tbuf), sizeof(double) * 2 * m * w0, s);
     auto h2d_2d = [&](double* dst, const double* src, int64_t ld, int64_t rows, int64_t cols) {
       return cudaMemcpy2DAsync(dst, sizeof(double) * ld, src, sizeof(double) * ld,
                                sizeof(double) * rows, cols, cudaMemcpyHostToDevice, h2d);
@@ -356,20 +394,38 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
           else
             e = nb ? h2d_2d(bdst + l0 + j0 * ldb, bsrc + l0 + j0 * ldb, ldb, kc, w)
                    : h2d_2d(bdst + j0 + l0 * ldb, bsrc + j0 + l0 * ldb, ldb, w, kc);
-          if (e == cudaSuccess && read_c && c == 0)
+          if (e == cudaSuccess && read_c && c == (defer_c && j0 == 0 ? kch - 1 : 0))
             e = cudaMemcpyAsync(C.p + pl * sc + j0 * ldc, (pl ? c_lo : c_hi) + j0 * ldc,
                                 sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyHostToDevice,
                                 h2d);
         }
+        mark("h2d b" + std::to_string(j0 / step) + " c" + std::to_string(c), h2d);
         if (e == cudaSuccess) e = cudaEventRecord(ev_in, h2d);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in, 0);
         if (e != cudaSuccess) break;
         const int64_t ao = na ? l0 * lda : l0;
         const int64_t bo = nb ? l0 + j0 * ldb : j0 + l0 * ldb;
-        rc = ddb_rgemm(transa, transb, m, w, kc, alpha_hi, alpha_lo, A.p + ao, A.p + sa + ao, lda,
-                       B.p + bo, B.p + sb + bo, ldb, c == 0 ? beta_hi : 1.0,
-                       c == 0 ? beta_lo : 0.0, C.p + j0 * ldc, C.p + sc + j0 * ldc, ldc, mode,
-                       stream);
+        if (defer_c && j0 == 0 && c + 1 < kch) {   // early panels -> T (m x w, ld m)
+          rc = ddb_rgemm(transa, transb, m, w, kc, alpha_hi, alpha_lo, A.p + ao, A.p + sa + ao,
+                         lda, B.p + bo, B.p + sb + bo, ldb, c == 0 ? 0.0 : 1.0, 0.0, tbuf,
+                         tbuf + m * w, m, mode, stream);
+        } else {
+          const bool first = c == (defer_c && j0 == 0 ? kch - 1 : 0);
+          rc = ddb_rgemm(transa, transb, m, w, kc, alpha_hi, alpha_lo, A.p + ao, A.p + sa + ao,
+                         lda, B.p + bo, B.p + sb + bo, ldb, first ? beta_hi : 1.0,
+                         first ? beta_lo : 0.0, C.p + j0 * ldc, C.p + sc + j0 * ldc, ldc, mode,
+                         stream);
+          if (rc == DDB_OK && defer_c && j0 == 0) {
+            int64_t gb = (m * w + 255) / 256;
+            if (gb > 148 * 8) gb = 148 * 8;
+            fold_block_kernel<<<(unsigned)gb, 256, 0, s>>>(m, w, C.p, C.p + sc, ldc, tbuf, tbuf + m * w);
+            g_launches += 1;
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaFreeAsync(tbuf, s);
+            tbuf = nullptr;
+          }
+        }
+        mark("gemm b" + std::to_string(j0 / step) + " c" + std::to_string(c), s);
       }
       if (rc != DDB_OK || e != cudaSuccess) break;
       e = cudaEventRecord(ev_out, s);
@@ -377,13 +433,24 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
       for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl)
         e = cudaMemcpyAsync((pl ? c_lo : c_hi) + j0 * ldc, C.p + pl * sc + j0 * ldc,
                             sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyDeviceToHost, d2h);
+      mark("d2h b" + std::to_string(j0 / step), d2h);
     }
     // join the copy streams into `s` (the buffers are freed on `s`)
     cudaError_t ej = cudaEventRecord(ev_out, d2h);
     if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_out, 0);
     if (ej == cudaSuccess) ej = cudaEventRecord(ev_in, h2d);
     if (ej == cudaSuccess) ej = cudaStreamWaitEvent(s, ev_in, 0);
+    if (tbuf != nullptr) cudaFreeAsync(tbuf, s);
     if (ej == cudaSuccess) ej = cudaStreamSynchronize(s);
+    if (trace && t0ev != nullptr) {
+      for (auto& te : tev) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t0ev, te.second);
+        std::fprintf(stderr, "[ddb trace] %8.2f ms  %s\n", ms, te.first.c_str());
+        cudaEventDestroy(te.second);
+      }
+      cudaEventDestroy(t0ev);
+    }
     if (ev0) cudaEventDestroy(ev0);
     if (ev_in) cudaEventDestroy(ev_in);
     if (ev_out) cudaEventDestroy(ev_out);

@@ -534,13 +534,15 @@ def test_concurrent_calls_on_two_streams_from_two_threads():
         assert all(bits_equal(a, b) for a, b in zip(out[mode], refs[mode])), mode
 
 
-@pytest.mark.parametrize("ta,tb,beta", [("N", "N", 0.5), ("T", "T", 0.0), ("N", "T", 1.0)])
-def test_host_pipelined_path_matches_device_exact(ta, tb, beta):
+@pytest.mark.parametrize("ta,tb,beta,k", [("N", "N", 0.5, 7680), ("T", "T", 0.0, 7680),
+                                          ("N", "T", 1.0, 7680), ("N", "N", 0.5, 8704)])
+def test_host_pipelined_path_matches_device_exact(ta, tb, beta, k):
     """ddb_rgemm_host with pinned buffers and a large problem runs column
     blocks with copies overlapped (capi.cu); exact mode must still be
     bit-identical to the device-resident call."""
     import torch
-    m, n, k = 640, 2048, 7680                   # m n k >= 1e10: the pipelined branch
+    m, n = 640, 2048                            # m n k >= 1e10: the pipelined branch
+    # (k >= 8192: block 0 in 8 k panels)
     nra, nca = (m, k) if ta == "N" else (k, m)
     nrb, ncb = (k, n) if tb == "N" else (n, k)
     A, B, C = random_dd(nra, nca, nra, 4, 1), random_dd(nrb, ncb, nrb, 4, 2), random_dd(m, n, m, 4, 3)
