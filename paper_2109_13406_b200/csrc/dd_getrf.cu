@@ -212,12 +212,51 @@ getrf_panel_kernel(GetrfArgs g, int64_t j0, int nb) {
 // (kSmemRowsMax rows).
 constexpr int kSmemRowsMax = 192;
 
+// The shared-memory kernel's search key: argmax_abs's order (elem.py:246-259)
+// as integers -- |hi| by its bits (non-negative doubles order like their bit
+// patterns; a NaN |hi| sorts above +inf, so a NaN anywhere wins and is
+// recognised on the winner), then lo * sign(hi) through the order-preserving
+// map of signed doubles (after -0 -> +0: the reference compares with ==), then
+// the smaller row.  The pivot value itself is read from the winner's
+// published row, so the key is three words and a merge is integer compares.
+struct SKey {
+  unsigned long long ah, al;
+  long long idx;                         // kNoRow: empty
+};
+constexpr long long kNoRow = 0x7fffffffffffffffLL;
+__device__ __forceinline__ SKey skey_merge(const SKey& x, const SKey& y) {
+  const bool yb = y.ah != x.ah ? y.ah > x.ah : (y.al != x.al ? y.al > x.al : y.idx < x.idx);
+  return yb ? y : x;
+}
+__device__ __forceinline__ SKey skey_shfl_down(const SKey& k, int o) {
+  return SKey{__shfl_down_sync(0xffffffffu, k.ah, o), __shfl_down_sync(0xffffffffu, k.al, o),
+              __shfl_down_sync(0xffffffffu, k.idx, o)};
+}
+template <class N>
+__device__ __forceinline__ SKey skey_of(typename N::T v, long long idx) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(dadd(N::key_lo(v), 0.0));
+  b ^= (b >> 63) ? ~0ull : (1ull << 63);
+  return SKey{(unsigned long long)__double_as_longlong(N::key_hi(v)), b, idx};
+}
+// block-wide best (all threads get it); every thread passes its key
+__device__ __forceinline__ SKey skey_block_best(SKey k) {
+  __shared__ SKey red[kPanelThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) k = skey_merge(k, skey_shfl_down(k, o));
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
+  __syncthreads();
+  if (l == 0) red[w] = k;
+  __syncthreads();
+  SKey r = red[0];
+#pragma unroll
+  for (int i = 1; i < kPanelThreads / 32; ++i) r = skey_merge(r, red[i]);
+  return r;
+}
+
 template <class N>
 __global__ void __launch_bounds__(kPanelThreads)
 getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   using T = typename N::T;
   extern __shared__ double sm[];
-  __shared__ PivKey best_s;
   __shared__ T rec_s;
   __shared__ int use_rec_s, nonzero_s;
   const int G = gridDim.x;
@@ -247,23 +286,16 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   auto publish = [&](int jj, int upd) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
-    PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
+    SKey k{0ull, 0ull, kNoRow};
     const int rs = r0 > j ? 0 : (int)(j - r0);
-    for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) {
-      const T v = N::ld(xh, xl, r + jj * ch);
-      PivKey y{N::key_hi(v), N::key_lo(v), N::hi(v), N::lo(v), (long long)(r0 + r),
-               N::key_nan(v) ? 1 : 0};
-      k = merge(k, y);
-    }
-    k = block_best(k);
+    for (int r = rs + threadIdx.x; r < nr; r += blockDim.x)
+      k = skey_merge(k, skey_of<N>(N::ld(xh, xl, r + jj * ch), (long long)(r0 + r)));
+    k = skey_block_best(k);
     const int slot = par * G + blockIdx.x;
     if (threadIdx.x == 0) {
-      g.part_ah[slot] = k.ah;
-      g.part_al[slot] = k.al;
-      g.part_h[slot] = k.h;
-      g.part_l[slot] = k.l;
+      reinterpret_cast<unsigned long long*>(g.part_ah)[slot] = k.ah;
+      reinterpret_cast<unsigned long long*>(g.part_al)[slot] = k.al;
       g.part_idx[slot] = k.idx;
-      g.part_nan[slot] = k.nan;
     }
     auto row_out = [&](double* out, int rr) {
       for (int c = threadIdx.x; c < nb; c += blockDim.x) {
@@ -272,7 +304,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
         N::st(out, out + nb, c, v);
       }
     };
-    if (k.idx >= 0) row_out(cand(par, blockIdx.x), (int)(k.idx - r0));
+    if (k.idx != kNoRow) row_out(cand(par, blockIdx.x), (int)(k.idx - r0));
     if (owner(j) == (int)blockIdx.x) row_out(jrow(par), (int)(j - r0));
   };
   // arrive / wait halves of grid_barrier
@@ -302,27 +334,21 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
     wait(G * ++nbar);
-    if (threadIdx.x < 32) {
-      PivKey k{0.0, 0.0, 0.0, 0.0, -1, 0};
-      for (int c = threadIdx.x; c < G; c += 32) {
-        const int slot = par * G + c;
-        PivKey y{__ldcg(g.part_ah + slot), __ldcg(g.part_al + slot), __ldcg(g.part_h + slot),
-                 __ldcg(g.part_l + slot), __ldcg(g.part_idx + slot), __ldcg(g.part_nan + slot)};
-        k = merge(k, y);
-      }
-      for (int o = 16; o > 0; o >>= 1) k = merge(k, shfl_down(k, o));
-      if (threadIdx.x == 0) {
-        if (k.nan || k.idx < 0) {          // argmax_abs returns 0 -> the diagonal entry
-          k.idx = j;
-          k.nan = 1;
-        }
-        best_s = k;
-      }
+    // the G partial keys: one per thread, then a block reduction
+    SKey k{0ull, 0ull, kNoRow};
+    for (int c = threadIdx.x; c < G; c += blockDim.x) {
+      const int slot = par * G + c;
+      k = skey_merge(k, SKey{__ldcg(reinterpret_cast<const unsigned long long*>(g.part_ah) + slot),
+                             __ldcg(reinterpret_cast<const unsigned long long*>(g.part_al) + slot),
+                             __ldcg(g.part_idx + slot)});
     }
-    __syncthreads();
-    const int64_t jp = best_s.idx;
-    // a NaN search keeps row j; otherwise the winner's value is the pivot
-    const bool swapped = !best_s.nan && N::nonzero(N::make(best_s.h, best_s.l)) && jp != j;
+    k = skey_block_best(k);
+    // NaN |hi| (np.max propagates it: argmax_abs returns 0 -> the diagonal
+    // entry) or no candidate: row j stays
+    const bool nan = k.idx == kNoRow || isnan(__longlong_as_double((long long)k.ah));
+    const int64_t jp = nan ? j : k.idx;
+    // nonzero(pivot) from the key: |hi| != 0 or lo != 0 (+0 is the map's 1 << 63)
+    const bool swapped = !nan && (k.ah != 0ull || k.al != (1ull << 63)) && jp != j;
     const double* src = swapped ? cand(par, owner(jp)) : jrow(par);
     const double* jr = jrow(par);
     // the pivot (entry jj of the pivot row) on the last warp, idle in the row fetch (nb <= 64)
@@ -523,7 +549,14 @@ static int panel_grid(int64_t rows) {
     cached_max = per > 0 ? sms : 1;                            // one CTA per SM
     cached_dev = dev;
   }
-  int64_t want = (rows + 63) / 64;                            // >= 64 rows per CTA
+  // rows per CTA: the panel is latency-bound, so fewer, fuller CTAs leave
+  // more SMs to the trailing update it overlaps (env DDB_GETRF_ROWS)
+  static const int64_t per_cta = [] {
+    const char* v = std::getenv("DDB_GETRF_ROWS");
+    const int64_t r = v ? (int64_t)std::atoll(v) : 0;
+    return r > 0 ? r : (int64_t)64;
+  }();
+  int64_t want = (rows + per_cta - 1) / per_cta;
   if (want < 1) want = 1;
   return (int)(want < cached_max ? want : cached_max);
 }
