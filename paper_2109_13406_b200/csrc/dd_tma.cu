@@ -86,8 +86,9 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
   if (*flag != ROUTE_SAFE) return;   // dd_reference.cu handles this call
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  double* ring = reinterpret_cast<double*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align by an offset from the __shared__ array (an integer round trip of
+  // the pointer would lose its address space: generic LD instead of LDS)
+  double* ring = reinterpret_cast<double*>(smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + STAGES * STAGE_DOUBLES);
   uint64_t* empty = full + STAGES;
 
