@@ -190,6 +190,46 @@ cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const i
       cudaGetLastError();
     }
   }
+  // Fast-mode Rgemm with a transposed operand (NT / TN / TT): transposed
+  // copies of op(A) (m-major) and / or op(B) (k-major) -- 32 bytes of copy
+  // traffic per element against k or m MACs per element -- make it an NN call
+  // for the TMA kernel.  The fast modes' per-element arithmetic does not
+  // depend on the operand layout.
+  if (cfg == 0 && g.syrk == 0 && (g.ta != 0 || g.tb != 0) && (alg == ALG_CERT || alg == ALG_TWOSUM) &&
+      std::getenv("DDB_NO_TMA_TRANS") == nullptr) {
+    const int64_t lda2 = (g.m + 1) & ~int64_t(1), ldb2 = (g.k + 1) & ~int64_t(1);
+    const size_t na = g.ta ? 2 * (size_t)lda2 * g.k : 0, nbb = g.tb ? 2 * (size_t)ldb2 * g.n : 0;
+    double* tbuf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&tbuf), sizeof(double) * (na + nbb), s) ==
+        cudaSuccess) {
+      GemmArgs g2 = g;
+      cudaError_t e = cudaSuccess;
+      if (g.ta) {   // A stored k x m -> m x k
+        double* th = tbuf;
+        double* tl = th + na / 2;
+        e = launch_dd_transpose(g.a_hi, g.a_lo, g.lda, th, tl, lda2, g.k, g.m, s);
+        g2.ta = 0; g2.a_hi = th; g2.a_lo = tl; g2.lda = lda2;
+      }
+      if (e == cudaSuccess && g.tb) {   // B stored n x k -> k x n
+        double* th = tbuf + na;
+        double* tl = th + nbb / 2;
+        e = launch_dd_transpose(g.b_hi, g.b_lo, g.ldb, th, tl, ldb2, g.n, g.k, s);
+        g2.tb = 0; g2.b_hi = th; g2.b_lo = tl; g2.ldb = ldb2;
+      }
+      if (e == cudaSuccess && tma_eligible(g2, alg)) {
+        *nlaunch += (g.ta != 0) + (g.tb != 0);
+        e = launch_tma_nn(g2, alg, row_exp, col_exp, flag, s);
+        cudaFreeAsync(tbuf, s);
+        if (e != cudaErrorNotSupported) return e;
+        cudaGetLastError();
+      } else {
+        cudaFreeAsync(tbuf, s);
+        if (e != cudaSuccess) return e;
+      }
+    } else {
+      cudaGetLastError();
+    }
+  }
   switch (alg) {
     case ALG_TWOSUM: return launch_tiled_twosum(cfg, g, row_exp, col_exp, flag, s);
     case ALG_SELECT: return launch_tiled_select(cfg, g, row_exp, col_exp, flag, s);
