@@ -29,7 +29,7 @@ using tiled::anchor_of;
 using tiled::dbits;
 
 #ifndef DDB_TMA_UNROLL
-#define DDB_TMA_UNROLL 4   // 2-step bodies unrolled per loop trip (8 = the whole k-tile)
+#define DDB_TMA_UNROLL 2   // 2-step bodies unrolled per loop trip (8 = the whole k-tile; 2 measured best)
 #endif
 
 constexpr int kTmaUnroll = DDB_TMA_UNROLL;
