@@ -368,8 +368,23 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
       return cudaMemcpy2DAsync(dst, sizeof(double) * ld, src, sizeof(double) * ld,
                                sizeof(double) * rows, cols, cudaMemcpyHostToDevice, h2d);
     };
-    for (int64_t j0 = 0; j0 < n && e == cudaSuccess && rc == DDB_OK; j0 += step) {
-      const int64_t j1 = j0 + step < n ? j0 + step : n, w = j1 - j0;
+    // Block widths: block 0 = step (k-panelled), then blocks of 2 step (fewer
+    // calls: each re-scans A for the safe window and the bound), and a final
+    // block of step / 4 so that the un-overlapped last copy-out is short.
+    std::vector<int64_t> bounds{0};
+    {
+      int64_t j = step < n ? step : n;
+      bounds.push_back(j);
+      const int64_t tail = step / 4 >= 64 ? step / 4 / 64 * 64 : 0;
+      const int64_t mid_end = n - tail > j ? n - tail : n;
+      while (j < mid_end) {
+        j = j + 2 * step < mid_end ? j + 2 * step : mid_end;
+        bounds.push_back(j);
+      }
+      if (j < n) bounds.push_back(n);
+    }
+    for (size_t bi = 0; bi + 1 < bounds.size() && e == cudaSuccess && rc == DDB_OK; ++bi) {
+      const int64_t j0 = bounds[bi], j1 = bounds[bi + 1], w = j1 - j0;
       const int kch = j0 == 0 ? kch0 : 1;
       for (int c = 0; c < kch && e == cudaSuccess && rc == DDB_OK; ++c) {
         const int64_t l0 = c == 0 ? 0 : (k * c / kch) / 64 * 64;
@@ -399,7 +414,7 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
                                 sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyHostToDevice,
                                 h2d);
         }
-        mark("h2d b" + std::to_string(j0 / step) + " c" + std::to_string(c), h2d);
+        mark("h2d b" + std::to_string(bi) + " c" + std::to_string(c), h2d);
         if (e == cudaSuccess) e = cudaEventRecord(ev_in, h2d);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_in, 0);
         if (e != cudaSuccess) break;
@@ -425,7 +440,7 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
             tbuf = nullptr;
           }
         }
-        mark("gemm b" + std::to_string(j0 / step) + " c" + std::to_string(c), s);
+        mark("gemm b" + std::to_string(bi) + " c" + std::to_string(c), s);
       }
       if (rc != DDB_OK || e != cudaSuccess) break;
       e = cudaEventRecord(ev_out, s);
@@ -433,7 +448,7 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
       for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl)
         e = cudaMemcpyAsync((pl ? c_lo : c_hi) + j0 * ldc, C.p + pl * sc + j0 * ldc,
                             sizeof(double) * (size_t)span(m, w, ldc), cudaMemcpyDeviceToHost, d2h);
-      mark("d2h b" + std::to_string(j0 / step), d2h);
+      mark("d2h b" + std::to_string(bi), d2h);
     }
     // join the copy streams into `s` (the buffers are freed on `s`)
     cudaError_t ej = cudaEventRecord(ev_out, d2h);
