@@ -293,13 +293,29 @@ def run_ours(args):
         kernel_t = t if not distributed else t_local
         achieved = 20.0 * n * n * k / kernel_t / 1e12 / (world if distributed else 1)
         prof = _profile_traffic()
+        ipm = {"fast": 7.5, "exact": 29, "twosum": 12.375}[mode]
+        traffic = prof.get("dram_bytes_per_launch")
+        try:
+            with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+                hbm_peak = float(json.load(f)["hbm_gbs"])
+        except Exception:
+            hbm_peak = None
         extra["roofline"] = {
             "bound": "fp64", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
             "frac": achieved * 1e12 / peak,
             "traffic": prof.get("dram_bytes_per_launch"),
             "convention": "20 fp64 flops per dd MAC (north star); peak = live DFMA probe",
             "algorithmic_bytes": 16.0 * (2 * n * k + 2 * n * n),
-            "fp64_instr_per_mac": {"fast": 7.5, "exact": 29, "twosum": 12.375}[mode],
+            "fp64_instr_per_mac": ipm,
+            # the hardware fraction: FP64 instructions actually issued per second
+            # over the pipe's lane rate (peak / 2, FMA = 2 flops); ncu's
+            # sm__pipe_fp64_cycles_active is the same quantity for the kernel alone
+            "fp64_pipe_frac": ipm * n * n * k / kernel_t / (world if distributed else 1)
+                              / (peak / 2.0),
+            # achieved DRAM bandwidth of the dominant kernel (ncu bytes / step time)
+            # against the measured copy bandwidth
+            "hbm_gbs": (traffic / kernel_t / 1e9) if traffic and not distributed else None,
+            "hbm_peak_gbs": hbm_peak,
         }
     if rank == 0 and not args.quick:
         # ---- e2e through the public API with pinned host buffers ----
