@@ -13,6 +13,12 @@
 //     tiled kernels exit at once and the reference-semantics kernel
 //     (dd_reference.cu) computes the call, so every input is handled with
 //     the reference's own inf / nan / overflow behaviour.
+//     In the fast modes (canon != 0) a word is also unsafe when it is not a
+//     normalised dd, |lo| > 2^-53 |hi| (e.g. hi = 0, lo != 0): their error
+//     analyses bound the lo * hi terms by the hi * hi ones (dd_tiled.cuh),
+//     and the certified bound is built from |hi| alone (dd_bound.cu).  The
+//     reference's own operations only ever produce normalised values; such
+//     hand-made inputs get the reference semantics instead.
 //
 // Traffic: 16 B per scanned element (hi + lo), coalesced along the
 // contiguous (column-major) dimension; one block = 32 rows x 64 columns.
@@ -28,7 +34,7 @@ __global__ void __launch_bounds__(256)
 prescan_kernel(const double* __restrict__ hi, const double* __restrict__ lo, int64_t ld,
                int64_t rows, int64_t cols, int* __restrict__ out_row,
                int* __restrict__ out_col, int* __restrict__ flag, int tri,
-               int64_t col_off) {
+               int64_t col_off, int canon) {
   __shared__ int srow[8][33];
   const int x = threadIdx.x, y = threadIdx.y;
   const int64_t r = (int64_t)blockIdx.x * 32 + x;
@@ -47,6 +53,8 @@ prescan_kernel(const double* __restrict__ hi, const double* __restrict__ lo, int
       const double l = lo[r + c * ld];
       const int eh = bexp(h), el = bexp(l);
       bad |= (h != 0.0 && eh < WIN_LO) || eh > WIN_HI || el > WIN_HI;
+      // h * 2^-53 is exact inside the window (|h| >= 2^-300)
+      bad |= canon && fabs(l) > fabs(h) * 0x1p-53;
       e = eh;
     }
     rmax = max(rmax, e);
@@ -72,7 +80,7 @@ prescan_kernel(const double* __restrict__ hi, const double* __restrict__ lo, int
 
 static cudaError_t scan(const double* hi, const double* lo, int64_t ld, int64_t rows,
                         int64_t cols, int* out_row, int* out_col, int* flag,
-                        cudaStream_t s, int* nlaunch, int tri = 0) {
+                        cudaStream_t s, int* nlaunch, int canon, int tri = 0) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   const int64_t gx = (rows + 31) / 32, gy_total = (cols + 63) / 64;
   // gridDim.y is limited to 65535: split very wide matrices into column slabs
@@ -83,7 +91,7 @@ static cudaError_t scan(const double* hi, const double* lo, int64_t ld, int64_t 
     prescan_kernel<<<grid, block, 0, s>>>(hi + cbase * ld, lo + cbase * ld, ld, rows,
                                           cols - cbase, out_row,
                                           out_col ? out_col + cbase : nullptr, flag, tri,
-                                          cbase);
+                                          cbase, canon);
     ++*nlaunch;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -97,26 +105,28 @@ cudaError_t launch_prescan(const GemmArgs& g, int alg, int* row_exp, int* col_ex
                            int* flag, cudaStream_t s, int* nlaunch) {
   // only the certified-anchor algorithm consumes the exponent maxima
   const bool fast = alg == ALG_CERT;
+  // the fast algorithms' error analyses assume normalised dd operands
+  const int canon = alg == ALG_CERT || alg == ALG_TWOSUM;
   cudaError_t e;
   // op(A) is m x k: stored m x k (N) or k x m (T)
   if (g.ta == 0)
-    e = scan(g.a_hi, g.a_lo, g.lda, g.m, g.k, fast ? row_exp : nullptr, nullptr, flag, s, nlaunch);
+    e = scan(g.a_hi, g.a_lo, g.lda, g.m, g.k, fast ? row_exp : nullptr, nullptr, flag, s, nlaunch, canon);
   else
-    e = scan(g.a_hi, g.a_lo, g.lda, g.k, g.m, nullptr, fast ? row_exp : nullptr, flag, s, nlaunch);
+    e = scan(g.a_hi, g.a_lo, g.lda, g.k, g.m, nullptr, fast ? row_exp : nullptr, flag, s, nlaunch, canon);
   if (e != cudaSuccess) return e;
   if (g.syrk == 0) {
     // op(B) is k x n: stored k x n (N) or n x k (T)
     if (g.tb == 0)
-      e = scan(g.b_hi, g.b_lo, g.ldb, g.k, g.n, nullptr, fast ? col_exp : nullptr, flag, s, nlaunch);
+      e = scan(g.b_hi, g.b_lo, g.ldb, g.k, g.n, nullptr, fast ? col_exp : nullptr, flag, s, nlaunch, canon);
     else
-      e = scan(g.b_hi, g.b_lo, g.ldb, g.n, g.k, fast ? col_exp : nullptr, nullptr, flag, s, nlaunch);
+      e = scan(g.b_hi, g.b_lo, g.ldb, g.n, g.k, fast ? col_exp : nullptr, nullptr, flag, s, nlaunch, canon);
     if (e != cudaSuccess) return e;
   }
   // The exact kernel's axpy form (transa = 'N') starts its unchecked
   // accumulation from beta*C, so C must be in the window too.
   if (alg == ALG_EXACT && g.ta == 0 && !(g.beta.h == 0.0 && g.beta.l == 0.0)) {
     // Rsyrk: only the uplo triangle is ever read (level23.py:245-246)
-    e = scan(g.c_hi, g.c_lo, g.ldc, g.m, g.n, nullptr, nullptr, flag, s, nlaunch, g.syrk);
+    e = scan(g.c_hi, g.c_lo, g.ldc, g.m, g.n, nullptr, nullptr, flag, s, nlaunch, 0, g.syrk);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

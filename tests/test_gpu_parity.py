@@ -202,6 +202,33 @@ def test_tiled_route_taken_for_in_window_inputs():
     assert _lib.last_route() == 2
 
 
+@pytest.mark.parametrize("mode", ["fast", "twosum"])
+@pytest.mark.parametrize("where", ["A", "B"])
+@pytest.mark.parametrize("kind", ["hi_zero", "lo_big"])
+def test_non_normalised_operands_take_reference_route(mode, where, kind):
+    """A hand-made dd with |lo| > 2^-53 |hi| (hi = 0, lo != 0, or lo of the
+    order of hi) is outside the fast algorithms' error analysis: the call is
+    routed to the reference-semantics kernel and matches mode='reference'."""
+    m, n, k = 96, 80, 70
+    A = [x.copy() for x in random_dd(m, k, m, 31, 1)]
+    B = [x.copy() for x in random_dd(k, n, k, 31, 2)]
+    C = random_dd(m, n, m, 31, 3)
+    X = A if where == "A" else B
+    if kind == "hi_zero":
+        X[0][5], X[1][5] = 0.0, 1e-3
+    else:
+        X[1][7] = 0.75 * X[0][7]
+    outs = []
+    for md in (mode, "reference"):
+        a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
+        Rgemm("N", "N", m, n, k, _Scalar((1.5, 0.0)), a, m, b, k, _Scalar((0.5, 0.0)), c, m,
+              mode=md)
+        outs.append((c.store[0].cpu().numpy(), c.store[1].cpu().numpy()))
+        if md == mode:
+            assert _lib.last_route() == 2
+    assert bits_equal(outs[0][0], outs[1][0]) and bits_equal(outs[0][1], outs[1][1])
+
+
 # ---- larger shapes against the C oracle (bitwise, exact mode) -------------
 
 SHAPES = [(300, 260, 200, 3, 1, 5), (129, 65, 17, 0, 0, 0), (1, 1, 1, 0, 0, 0),
