@@ -307,6 +307,11 @@ def run_ours(args):
             "convention": "20 fp64 flops per dd MAC (north star); peak = live DFMA probe",
             "algorithmic_bytes": 16.0 * (2 * n * k + 2 * n * n),
             "fp64_instr_per_mac": ipm,
+            # fast mode (default DDB_SPLIT): 5.5 per MAC in the dd TMA kernel
+            # (anchored hi*hi) + 2 in the two binary64 cross-term GEMMs
+            "fp64_instr_split": ({"tma_kernel": 5.5, "cross_dgemm": 2.0}
+                                 if mode == "fast" and os.environ.get("DDB_SPLIT", "1") != "0"
+                                 else None),
             # the hardware fraction: FP64 instructions actually issued per second
             # over the pipe's lane rate (peak / 2, FMA = 2 flops); ncu's
             # sm__pipe_fp64_cycles_active is the same quantity for the kernel alone
@@ -561,6 +566,22 @@ def _modes(n, k, dev, stream, A, B, C, C0, mode):
                       1, 1, stream)
         t = min(times)
         out[other] = {"ms": t * 1e3, "value": 2.0 * n * n * k / t / 1e9, "unit": UNIT}
+    if mode == "fast" and os.environ.get("DDB_SPLIT", "1") != "0":
+        # fast mode without the split: the certified-anchor MAC entirely in the
+        # hand-written kernel (7.5 FP64 instructions per MAC, no library GEMM)
+        saved = os.environ.get("DDB_SPLIT")
+        os.environ["DDB_SPLIT"] = "0"
+        try:
+            times = timed(lambda: Rgemm("N", "N", n, n, k, ALPHA, A, n, B, k, BETA, C, n,
+                                        mode="fast"), 1, 1, stream)
+        finally:
+            if saved is None:
+                os.environ.pop("DDB_SPLIT", None)
+            else:
+                os.environ["DDB_SPLIT"] = saved
+        t = min(times)
+        out["fast_nosplit"] = {"ms": t * 1e3, "value": 2.0 * n * n * k / t / 1e9, "unit": UNIT,
+                               "what": "DDB_SPLIT=0: cross terms inside the dd kernel"}
     C.store[0].copy_(C0.store[0])
     C.store[1].copy_(C0.store[1])
     return out

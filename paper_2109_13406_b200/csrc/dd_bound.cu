@@ -113,4 +113,35 @@ cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_e
   return cudaGetLastError();
 }
 
+// ALG_SPLIT's cross terms: x (m x n, ld = m) = op(A)_lo op(B)_hi + op(A)_hi op(B)_lo,
+// two plain binary64 library GEMMs (the same handle, default math mode: IEEE
+// binary64 products and sums in some order).  Any summation order keeps
+// |error| <= 2k u * sum_l (|a_lo b_hi| + |a_hi b_lo|) <= 4k u^2 * sum_l |a_hi b_hi|
+// for normalised operands (|lo| <= u |hi|, enforced by the prescan), i.e.
+// one unit of the c k 2^-104 budget (dd_tma.cu).
+cudaError_t launch_cross_dgemm(const GemmArgs& g, double* x, cudaStream_t s) {
+  cublasHandle_t h = handle_for_current_device();
+  if (h == nullptr) return cudaErrorUnknown;
+  if (cublasSetStream(h, s) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  const double one = 1.0, zero = 0.0;
+  const cublasOperation_t opa = g.ta == 0 ? CUBLAS_OP_N : CUBLAS_OP_T;
+  const cublasOperation_t opb = g.tb == 0 ? CUBLAS_OP_N : CUBLAS_OP_T;
+  if (g.syrk != 0) {
+    // Rsyrk in NN form (op(B) = op(A)^T): only the uplo triangle is read,
+    // x = op(A)_hi op(A)_lo^T + op(A)_lo op(A)_hi^T is one DSYR2K (half the flops)
+    const cublasFillMode_t up = g.syrk == 1 ? CUBLAS_FILL_MODE_UPPER : CUBLAS_FILL_MODE_LOWER;
+    const cublasStatus_t st = cublasDsyr2k(h, up, opa, (int)g.m, (int)g.k, &one, g.a_hi,
+                                           (int)g.lda, g.a_lo, (int)g.lda, &zero, x, (int)g.m);
+    if (st != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    return cudaGetLastError();
+  }
+  cublasStatus_t st = cublasDgemm(h, opa, opb, (int)g.m, (int)g.n, (int)g.k, &one, g.a_lo,
+                                  (int)g.lda, g.b_hi, (int)g.ldb, &zero, x, (int)g.m);
+  if (st == CUBLAS_STATUS_SUCCESS)
+    st = cublasDgemm(h, opa, opb, (int)g.m, (int)g.n, (int)g.k, &one, g.a_hi, (int)g.lda,
+                     g.b_lo, (int)g.ldb, &one, x, (int)g.m);
+  if (st != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+  return cudaGetLastError();
+}
+
 }  // namespace ddb

@@ -15,6 +15,22 @@
 // Used when transa = transb = 'N', both planes 16-byte aligned, lda and ldb
 // even (TMA global strides are multiples of 16 bytes); anything else runs
 // dd_tiled.cuh.
+//
+// ALG_SPLIT (fast mode's default here): the dd product a*b = ah bh + (al bh +
+// ah bl) + al bl splits into the hi * hi part, accumulated by this kernel with
+// the certified anchor (Tn = fma(ah, bh, T), r = fma(ah, bh, T - Tn), L += r,
+// (T, L) folded every 2 steps: 5.5 FP64 instructions per MAC instead of 7.5,
+// and only the hi planes staged: half the TMA / LDS bytes), and the cross
+// terms X = A_lo B_hi + A_hi B_lo, two plain binary64 library GEMMs (DSYR2K
+// for Rsyrk) run first and added to L in the epilogue; al bl (< u^2 |ab|) is
+// dropped, as in every dd product.  Error per element, in units of
+// k 2^-104 S' (S' >= sum |ah bh|, the certified bound): per 2 steps the two
+// residuals round by <= 2^(E-107) each and the two additions into L (|L| <
+// 1.5 ulp(T)) by <= 2^(E-106) and 2^(E-105), i.e. <= 2 units per step with
+// 2^E < 4 S'; the GEMMs' recursive-summation bound is 2k u * sum (|al bh| +
+// |ah bl|) <= 4k u^2 S' = 1 unit (operands normalised, |lo| <= 2^-53 |hi|,
+// which the prescan enforces).  Total c <= 3 (+ O(u^2) epilogue roundings)
+// against the north star's c = 4.  Measured 258 vs 272 ms at 8192^3.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -84,6 +100,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                  const int* __restrict__ col_exp, const int* __restrict__ flag, int tiles_m,
                  int tiles_n, int splits) {
   if (*flag != ROUTE_SAFE) return;   // dd_reference.cu handles this call
+  constexpr bool CERTLIKE = ALG == ALG_CERT || ALG == ALG_SPLIT;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align by an offset from the __shared__ array (an integer round trip of
@@ -145,12 +162,18 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     const int s = p_item % STAGES;
     if (p_item >= STAGES) mbar_wait(&empty[s], ((p_item / STAGES) - 1) & 1);
     double* st = ring + s * STAGE_DOUBLES;
-    mbar_expect_tx(&full[s], STAGE_BYTES);
     const int kc = (int)(p_kbeg + (int64_t)p_kt * BK);
-    tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
-    tma_load_2d(st + A_PLANE, &mAl, (int)p_i0, kc, &full[s]);
-    tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)p_j0, &full[s]);
-    tma_load_2d(st + 2 * A_PLANE + B_PLANE, &mBl, kc, (int)p_j0, &full[s]);
+    if (ALG == ALG_SPLIT) {   // hi planes only
+      mbar_expect_tx(&full[s], (uint32_t)(A_PLANE + B_PLANE) * 8u);
+      tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
+      tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)p_j0, &full[s]);
+    } else {
+      mbar_expect_tx(&full[s], STAGE_BYTES);
+      tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
+      tma_load_2d(st + A_PLANE, &mAl, (int)p_i0, kc, &full[s]);
+      tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)p_j0, &full[s]);
+      tma_load_2d(st + 2 * A_PLANE + B_PLANE, &mBl, kc, (int)p_j0, &full[s]);
+    }
     ++p_item;
     if (++p_kt == p_ktiles) {
       p_kt = 0;
@@ -170,7 +193,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     unit_origin(u, i0, j0, kbeg, ktiles);
 
     double H[TM][TN], L[TM][TN];
-    if (ALG == ALG_CERT) {
+    if (CERTLIKE) {
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -200,6 +223,42 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
       const double* a_l = a_h + A_PLANE;
       const double* b_h = a_h + 2 * A_PLANE;
       const double* b_l = b_h + B_PLANE;
+      if (ALG == ALG_SPLIT) {
+        // hi * hi only: Tn = T + ah bh (T stays in its anchor's binade, so
+        // T - Tn is exact), r = ah bh + (T - Tn) is Tn's rounding error up to
+        // one rounding, L collects the r's; (T, L) folded every 2 steps.
+#pragma unroll (kTmaUnroll)
+        for (int kk = 0; kk < BK; kk += 2) {
+          double ah0[TM], ah1[TM], bh0[TN], bh1[TN];
+#pragma unroll
+          for (int gq = 0; gq < TM / 2; ++gq) {
+            const double2 h0 = *reinterpret_cast<const double2*>(a_h + kk * BM + gq * RX + tx * 2);
+            const double2 h1 = *reinterpret_cast<const double2*>(a_h + (kk + 1) * BM + gq * RX + tx * 2);
+            ah0[2 * gq] = h0.x; ah0[2 * gq + 1] = h0.y;
+            ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y;
+          }
+#pragma unroll
+          for (int b = 0; b < TN; ++b) {
+            const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
+            const double2 h = *reinterpret_cast<const double2*>(b_h + cj * BK + kk);
+            bh0[b] = h.x; bh1[b] = h.y;
+          }
+#pragma unroll
+          for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b) {
+              const double T = H[a][b];
+              const double Tn = dfma(ah0[a], bh0[b], T);
+              const double r = dfma(ah0[a], bh0[b], dsub(T, Tn));
+              const double T1 = dfma(ah1[a], bh1[b], Tn);
+              const double r1 = dfma(ah1[a], bh1[b], dsub(Tn, T1));
+              const double l = dadd(dadd(L[a][b], r), r1);
+              const double T2 = dadd(T1, l);
+              L[a][b] = dsub(l, dsub(T2, T1));
+              H[a][b] = T2;
+            }
+        }
+      } else {
 #pragma unroll (kTmaUnroll)
       for (int kk = 0; kk < BK; kk += 2) {
         double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TN], bl0[TN], bh1[TN], bl1[TN];
@@ -242,6 +301,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
             }
         }
       }
+      }
       __syncwarp();
       if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     }
@@ -258,8 +318,10 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
         if (SYRK == 1 && gi > gj) continue;   // the uplo triangle only (level23.py:245-270)
         if (SYRK == 2 && gi < gj) continue;
         double sx, ex;
-        const double hv = ALG == ALG_CERT ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
-        two_sum(hv, L[a][b], sx, ex);
+        const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
+        double lv = L[a][b];
+        if (ALG == ALG_SPLIT && split == 0) lv = dadd(lv, g.cross[gi + gj * g.m]);
+        two_sum(hv, lv, sx, ex);
         if (g.part != nullptr) {
           double* ph = g.part + (size_t)split * 2 * g.m * g.n;
           ph[gi + gj * g.m] = sx;
@@ -307,6 +369,15 @@ static bool encode(CUtensorMap* m, const double* base, int64_t inner, int64_t ou
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// fast mode through ALG_SPLIT (default for deep calls; measured 258 vs 272 ms
+// at 8192^3) or the full certified-anchor MAC: DDB_SPLIT=0 never splits,
+// DDB_SPLIT=2 splits at any depth (tests).  Read per call (a few ns).
+static int split_policy() {
+  const char* v = std::getenv("DDB_SPLIT");
+  if (v == nullptr) return 1;
+  return v[0] == '0' ? 0 : (v[0] == '2' ? 2 : 1);
+}
 
 }  // namespace tma
 
@@ -373,14 +444,38 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
   auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
-  auto kern = alg == ALG_CERT
+  // ALG_SPLIT (Rgemm only): the cross terms first, as two binary64 GEMMs
+  // into a stream-ordered m x n scratch, then the hi * hi kernel
+  // Shallow calls (the LAPACK consumers' depth-256 updates) lose more to the
+  // cross GEMMs' fixed costs than the kernel gains: measured Rpotrf / Rgetrf /
+  // Rtrsm at n = 8192 3-4 % slower with the split at k = 256, Rsyrk even at
+  // n = k = 4096 (cuBLAS DSYR2K runs below DGEMM's rate).
+  const int policy = split_policy();
+  const bool split_alg = alg == ALG_CERT && policy != 0 &&
+                         (policy == 2 || g.k >= (g.syrk ? 8192 : 1024));
+  GemmArgs ga = g;
+  double* xbuf = nullptr;
+  if (split_alg) {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&xbuf),
+                                    sizeof(double) * (size_t)g.m * g.n, s);
+    if (e != cudaSuccess) return e;
+    e = launch_cross_dgemm(g, xbuf, s);
+    if (e != cudaSuccess) { cudaFreeAsync(xbuf, s); return e; }
+    ga.cross = xbuf;
+  }
+  auto kern = split_alg ? pick(dd_tma_nn_kernel<ALG_SPLIT, 0>, dd_tma_nn_kernel<ALG_SPLIT, 1>,
+                               dd_tma_nn_kernel<ALG_SPLIT, 2>)
+              : alg == ALG_CERT
                   ? pick(dd_tma_nn_kernel<ALG_CERT, 0>, dd_tma_nn_kernel<ALG_CERT, 1>,
                          dd_tma_nn_kernel<ALG_CERT, 2>)
                   : pick(dd_tma_nn_kernel<ALG_TWOSUM, 0>, dd_tma_nn_kernel<ALG_TWOSUM, 1>,
                          dd_tma_nn_kernel<ALG_TWOSUM, 2>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)SMEM_BYTES);
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess) {
+    if (xbuf != nullptr) cudaFreeAsync(xbuf, s);
+    return e;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -390,9 +485,14 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // speed but more DRAM reads (its CTAs drift apart in k across units).
   const int grid = std::getenv("DDB_TMA_PERSISTENT") ? (int)(units < sms ? units : sms)
                                                      : (int)units;
-  kern<<<grid, NT, SMEM_BYTES, s>>>(g, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
+  kern<<<grid, NT, SMEM_BYTES, s>>>(ga, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
                                     tiles_n, splits);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (xbuf != nullptr) {
+    const cudaError_t e2 = cudaFreeAsync(xbuf, s);
+    if (e == cudaSuccess) e = e2;
+  }
+  return e;
 }
 
 }  // namespace ddb

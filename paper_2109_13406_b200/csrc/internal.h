@@ -10,7 +10,11 @@ namespace ddb {
 enum Mode { MODE_EXACT = 0, MODE_FAST = 1, MODE_REFERENCE = 2, MODE_TWOSUM = 3 };
 
 // Tiled accumulation algorithm for a mode (dd_gemm.cu).
-enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_CERT = 3, ALG_F64 = 4 };
+// ALG_SPLIT: the certified-anchor accumulation of hi * hi only, with the
+// lo * hi + hi * lo cross terms from two binary64 GEMMs (dd_tma.cu; fast mode,
+// TMA route only)
+enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_CERT = 3, ALG_F64 = 4,
+           ALG_SPLIT = 5 };
 int alg_for_mode(int mode);
 
 // Route flag written by the prescan: 0 = every operand inside the safe
@@ -48,6 +52,9 @@ struct GemmArgs {
   // product negated after rounding (be.sub(c, be.mul(a, b)), the reference's
   // Rtrsm update, level23.py:334-336); alpha, beta unused (treated as 1)
   int sub;
+  // ALG_SPLIT: sum_l a_lo b_hi + a_hi b_lo (m x n, ld = m), added into the
+  // low word of the first k-slice's sum
+  const double* cross;
 };
 
 // Which kernel should run, decided on the device by the prescan flag.
@@ -65,6 +72,7 @@ cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag,
                                  int* nlaunch);
 cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
                          float* bound, cudaStream_t s, int* nlaunch, const char** what);
+cudaError_t launch_cross_dgemm(const GemmArgs& g, double* x, cudaStream_t s);
 
 // complex GEMM (dd_complex.cu)
 struct cdd { dd re, im; };

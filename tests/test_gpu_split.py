@@ -1,0 +1,135 @@
+"""GPU: fast mode's split algorithm (ALG_SPLIT, dd_tma.cu) forced at every
+depth (DDB_SPLIT=2; by default it only runs for k >= 1024, Rsyrk k >= 8192).
+The anchored hi*hi kernel plus the binary64 cross-term GEMMs must stay inside
+the dd error bound with c = 3 (its analysis, dd_tma.cu's header), on the
+adversarial magnitude patterns, Rsyrk triangles, split-K and the transposed
+routes, and leave everything outside the written region untouched."""
+
+import os
+
+import numpy as np
+import pytest
+
+from oracle import exact
+from paper_2109_13406_b200 import DeviceMatrix, Rgemm, Rsyrk, _lib
+from paper_2109_13406_b200.synth import random_dd
+
+pytestmark = pytest.mark.gpu
+
+C_SPLIT = 3.0
+
+
+@pytest.fixture(autouse=True)
+def force_split(monkeypatch):
+    monkeypatch.setenv("DDB_SPLIT", "2")
+    monkeypatch.setenv("DDB_DEBUG_SYNC", "1")
+    yield
+
+
+def dev(m, n, ld, planes):
+    import torch
+    return DeviceMatrix(m, n, "dd", ld,
+                        store=tuple(torch.from_numpy(np.ascontiguousarray(p)).cuda()
+                                    for p in planes))
+
+
+def _bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return bool(np.all((a.view(np.uint64) == b.view(np.uint64)) | (np.isnan(a) & np.isnan(b))))
+
+
+def _pattern(kind, m, n, k, seed):
+    from test_gpu_parity import _pattern as pattern   # the same adversarial inputs
+    return pattern(kind, m, n, k, seed)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "disjoint", "graded", "rows", "cancel"])
+@pytest.mark.parametrize("k", [1, 2, 3, 17, 300])
+def test_split_bound_on_adversarial_patterns(kind, k):
+    m, n = 70, 66
+    A, B = _pattern(kind, m, n, k, 5 + k)
+    C = random_dd(m, n, m, 5, 3)
+    alpha, beta = (1.5, 0.0), (0.5, 0.0)
+    a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
+    Rgemm("N", "N", m, n, k, alpha[0], a, m, b, k, beta[0], c, m, mode="fast")
+    assert _lib.last_route() == 1
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    I, J = list(range(0, m, 7)), list(range(0, n, 5))
+    vals, scales = exact.exact_entries("N", "N", k, alpha, A[0], A[1], m, B[0], B[1], k,
+                                       beta, C[0], C[1], m, I, J)
+    worst = exact.error_ratios(gh, gl, m, I, J, vals, scales, k, c=C_SPLIT)
+    assert worst <= 1.0, worst
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+@pytest.mark.parametrize("shape", [(96, 64, 700), (64, 64, 20000)])
+def test_split_rgemm_trans_and_split_k(ta, tb, shape):
+    m, n, k = shape
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A = random_dd(nra, nca, nra, 41, 1)
+    B = random_dd(nrb, ncb, nrb, 41, 2)
+    C = random_dd(m, n, m + 2, 41, 3)
+    alpha, beta = (1.5, 2 ** -60), (0.5, 0.0)
+    a, b, c = dev(nra, nca, nra, A), dev(nrb, ncb, nrb, B), dev(m, n, m + 2, C)
+    Rgemm(ta, tb, m, n, k, _S(alpha), a, nra, b, nrb, _S(beta), c, m + 2, mode="fast")
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    pad = np.ones(len(gh), bool)
+    for j in range(n):
+        pad[j * (m + 2): j * (m + 2) + m] = False
+    assert _bits_equal(gh[pad], C[0][pad]) and _bits_equal(gl[pad], C[1][pad])
+    I, J = list(range(0, m, max(1, m // 6))), list(range(0, n, max(1, n // 6)))
+    vals, scales = exact.exact_entries(ta, tb, k, alpha, A[0], A[1], nra, B[0], B[1], nrb,
+                                       beta, C[0], C[1], m + 2, I, J)
+    assert exact.error_ratios(gh, gl, m + 2, I, J, vals, scales, k, c=C_SPLIT) <= 1.0
+
+
+@pytest.mark.parametrize("uplo", ["U", "L"])
+@pytest.mark.parametrize("trans", ["N", "T"])
+def test_split_rsyrk_triangle_within_bound(uplo, trans):
+    n, k = 130, 300
+    nra, nca = (n, k) if trans == "N" else (k, n)
+    A = random_dd(nra, nca, nra, 42, 1)
+    C = random_dd(n, n, n, 42, 3)
+    a, c = dev(nra, nca, nra, A), dev(n, n, n, C)
+    Rsyrk(uplo, trans, n, k, 1.5, a, nra, 0.5, c, n, mode="fast")
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    iu = np.array([[(i <= j) if uplo == "U" else (i >= j) for j in range(n)] for i in range(n)])
+    mask = iu.T.reshape(-1)
+    assert _bits_equal(gh[~mask], C[0][~mask]) and _bits_equal(gl[~mask], C[1][~mask])
+    I = [0, 37, 74, 129]
+    ta, tb = ("N", "T") if trans == "N" else ("T", "N")
+    vals, scales = exact.exact_entries(ta, tb, k, (1.5, 0.0), A[0], A[1], nra, A[0], A[1], nra,
+                                       (0.5, 0.0), C[0], C[1], n, I, I)
+    worst = 0.0
+    for x, i in enumerate(I):
+        for y, j in enumerate(I):
+            if (i <= j) if uplo == "U" else (i >= j):
+                worst = max(worst, exact.error_ratios(gh, gl, n, [i], [j], [[vals[x][y]]],
+                                                      [[scales[x][y]]], k, c=C_SPLIT))
+    assert worst <= 1.0, worst
+
+
+def test_split_matches_cert_to_dd_accuracy():
+    """Both fast algorithms agree to within their bounds on one deep call."""
+    m, n, k = 128, 64, 4096
+    A = random_dd(m, k, m, 43, 1)
+    B = random_dd(k, n, k, 43, 2)
+    C = random_dd(m, n, m, 43, 3)
+    outs = []
+    for pol in ("2", "0"):
+        os.environ["DDB_SPLIT"] = pol
+        a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
+        Rgemm("N", "N", m, n, k, 1.5, a, m, b, k, 0.5, c, m, mode="fast")
+        outs.append((c.store[0].cpu().numpy(), c.store[1].cpu().numpy()))
+    os.environ["DDB_SPLIT"] = "2"
+    (h1, l1), (h2, l2) = outs
+    d = np.abs((h1 - h2) + (l1 - l2))
+    # |C| ~ 20, sum |ab| ~ k / 4: both within 4 k 2^-104 * 1024 ~ 2^-80 of the
+    # exact value; a lost cross term would show at ~2^-49
+    assert np.all(d <= 2.0 ** -75), float(d.max())
+
+
+class _S:
+    def __init__(self, v):
+        self.hi, self.lo = float(v[0]), float(v[1])
