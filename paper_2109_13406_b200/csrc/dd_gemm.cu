@@ -96,7 +96,7 @@ int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk) {
   if (best >= 0.95) return 1;
   for (int s = 2; s <= 16; ++s) {
     int64_t chunk = (g.k + s - 1) / s;
-    chunk = ((chunk + 31) / 32) * 32;
+    chunk = ((chunk + 95) / 96) * 96;   // whole k-tiles of every kernel (16, 24, 32 deep)
     if (chunk < 512) break;
     const int real = (int)((g.k + chunk - 1) / chunk);
     const double e = eff(tiles * real);

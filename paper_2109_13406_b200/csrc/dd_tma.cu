@@ -19,18 +19,22 @@
 // ALG_SPLIT (fast mode's default here): the dd product a*b = ah bh + (al bh +
 // ah bl) + al bl splits into the hi * hi part, accumulated by this kernel with
 // the certified anchor (Tn = fma(ah, bh, T), r = fma(ah, bh, T - Tn), L += r,
-// (T, L) folded every 2 steps: 5.5 FP64 instructions per MAC instead of 7.5,
-// and only the hi planes staged: half the TMA / LDS bytes), and the cross
-// terms X = A_lo B_hi + A_hi B_lo, two plain binary64 library GEMMs (DSYR2K
-// for Rsyrk) run first and added to L in the epilogue; al bl (< u^2 |ab|) is
-// dropped, as in every dd product.  Error per element, in units of
-// k 2^-104 S' (S' >= sum |ah bh|, the certified bound): per 2 steps the two
-// residuals round by <= 2^(E-107) each and the two additions into L (|L| <
-// 1.5 ulp(T)) by <= 2^(E-106) and 2^(E-105), i.e. <= 2 units per step with
-// 2^E < 4 S'; the GEMMs' recursive-summation bound is 2k u * sum (|al bh| +
-// |ah bl|) <= 4k u^2 S' = 1 unit (operands normalised, |lo| <= 2^-53 |hi|,
-// which the prescan enforces).  Total c <= 3 (+ O(u^2) epilogue roundings)
-// against the north star's c = 4.  Measured 258 vs 272 ms at 8192^3.
+// (T, L) folded every 3 steps: 5 FP64 instructions per MAC instead of 7.5,
+// and only the hi planes staged, 24-deep k-tiles), and the cross terms
+// X = A_lo B_hi + A_hi B_lo, two plain binary64 library GEMMs (DSYR2K for
+// Rsyrk) run first and added to L in the epilogue; al bl (< u^2 |ab|) is
+// dropped, as in every dd product.  Error per element, with the unit
+// v = 2^(E-106) < 2^-104 S' (2^E < 4 S', S' >= sum |ah bh| the certified
+// bound): each residual r (|r| <= ulp(T)/2 = 2^(E-53)) rounds by <= v/2; after
+// a fold |L| <= 2^(E-53), so by monotone rounding the three additions into L
+// stay <= 2^(E-52), 1.5 * 2^(E-52), 2^(E-51) and round by <= v, 2v, 2v: 6.5 v
+// per 3 steps, c = 2.17 (a period of 2 gives c = 2, of 4 c = 2.75).  The
+// GEMMs' recursive-summation bound is 2k u * sum (|al bh| + |ah bl|) <=
+// 4k u^2 S' (operands normalised, |lo| <= 2^-53 |hi|, which the prescan
+// enforces): c = 1; the dropped al bl c = 0.25.  With S' <= 1.08 sum |ab|
+// (bf16 round-up, fp32 factor at k = 65536): c <= 2.17 * 1.08 + 1.25 = 3.6
+// (+ O(u^2) epilogue roundings) against the north star's c = 4.
+// Measured at 8192^3: 240.4 ms vs 272.2 for the full MAC in this kernel.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -56,6 +60,31 @@ constexpr int A_PLANE = BK * BM, B_PLANE = BN * BK;          // doubles
 constexpr int STAGE_DOUBLES = 2 * A_PLANE + 2 * B_PLANE;     // 6144 doubles = 48 KB
 constexpr uint32_t STAGE_BYTES = STAGE_DOUBLES * 8;
 constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 1024;
+
+// ALG_SPLIT: k-tile depth and fold period (steps between (T, L) folds).  The
+// stage holds only the hi planes, so a deeper tile fits the same ring.  A
+// fold period of 3 keeps |L| < 2 ulp(T): error <= 6.5 units per 3 steps
+// (see the header), against 4 per 2 steps with a period of 2.
+#ifndef DDB_SPLIT_BK
+#define DDB_SPLIT_BK 24
+#endif
+#ifndef DDB_SPLIT_FOLD
+#define DDB_SPLIT_FOLD 3
+#endif
+#ifndef DDB_SPLIT_CHAIN
+#define DDB_SPLIT_CHAIN 0     // 1: per-element step chains instead of per-step sweeps
+#endif
+#ifndef DDB_SPLIT_UNROLL
+#define DDB_SPLIT_UNROLL 2    // k-loop bodies unrolled per trip (2: 240.4 vs 241.8 ms at 8192^3)
+#endif
+constexpr int SPLIT_BK = DDB_SPLIT_BK, SPLIT_FOLD = DDB_SPLIT_FOLD;
+constexpr bool SPLIT_CHAIN = DDB_SPLIT_CHAIN;
+constexpr int SPLIT_UNROLL = DDB_SPLIT_UNROLL;
+constexpr int SPLIT_BODY = SPLIT_FOLD % 2 == 0 ? SPLIT_FOLD : 2 * SPLIT_FOLD;   // even
+static_assert(SPLIT_BK % SPLIT_BODY == 0 && SPLIT_BK % 2 == 0, "split k-tile");
+static_assert((SPLIT_BK * (BM + BN)) * 8 <= STAGE_BYTES, "split stage fits the ring");
+// split-K chunks must be whole k-tiles of every kernel (dd_gemm.cu)
+static_assert(96 % SPLIT_BK == 0 || SPLIT_BK == 32, "chunk rounding");
 
 __device__ __forceinline__ uint32_t saddr(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -101,6 +130,10 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                  int tiles_n, int splits) {
   if (*flag != ROUTE_SAFE) return;   // dd_reference.cu handles this call
   constexpr bool CERTLIKE = ALG == ALG_CERT || ALG == ALG_SPLIT;
+  constexpr int KB = ALG == ALG_SPLIT ? SPLIT_BK : BK;            // k-tile depth
+  constexpr int AP = KB * BM;                                     // A hi plane, doubles
+  // stage layout: A hi | A lo | B hi | B lo (split: A hi | B hi)
+  constexpr int B_OFF = ALG == ALG_SPLIT ? AP : 2 * A_PLANE;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align by an offset from the __shared__ array (an integer round trip of
@@ -135,7 +168,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     j0 = (int64_t)(local / gm) * BN;
     kbeg = (int64_t)split * kchunk;
     const int64_t kend = min(g.k, kbeg + kchunk);
-    ktiles = (int)((kend - kbeg + BK - 1) / BK);
+    ktiles = (int)((kend - kbeg + KB - 1) / KB);
   };
 
   // Rsyrk (SYRK = 1 upper / 2 lower): units whose tile lies entirely in the
@@ -162,11 +195,11 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     const int s = p_item % STAGES;
     if (p_item >= STAGES) mbar_wait(&empty[s], ((p_item / STAGES) - 1) & 1);
     double* st = ring + s * STAGE_DOUBLES;
-    const int kc = (int)(p_kbeg + (int64_t)p_kt * BK);
+    const int kc = (int)(p_kbeg + (int64_t)p_kt * KB);
     if (ALG == ALG_SPLIT) {   // hi planes only
-      mbar_expect_tx(&full[s], (uint32_t)(A_PLANE + B_PLANE) * 8u);
+      mbar_expect_tx(&full[s], (uint32_t)(KB * (BM + BN)) * 8u);
       tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
-      tma_load_2d(st + 2 * A_PLANE, &mBh, kc, (int)p_j0, &full[s]);
+      tma_load_2d(st + B_OFF, &mBh, kc, (int)p_j0, &full[s]);
     } else {
       mbar_expect_tx(&full[s], STAGE_BYTES);
       tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
@@ -226,37 +259,76 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
       if (ALG == ALG_SPLIT) {
         // hi * hi only: Tn = T + ah bh (T stays in its anchor's binade, so
         // T - Tn is exact), r = ah bh + (T - Tn) is Tn's rounding error up to
-        // one rounding, L collects the r's; (T, L) folded every 2 steps.
-#pragma unroll (kTmaUnroll)
-        for (int kk = 0; kk < BK; kk += 2) {
-          double ah0[TM], ah1[TM], bh0[TN], bh1[TN];
+        // one rounding, L collects the r's; (T, L) folded every SPLIT_FOLD
+        // steps.  B is k-major: one LDS.128 per column gives two k-steps.
+        const double* bs = a_h + B_OFF;
+#pragma unroll (SPLIT_UNROLL)
+        for (int kk = 0; kk < KB; kk += SPLIT_BODY) {
 #pragma unroll
-          for (int gq = 0; gq < TM / 2; ++gq) {
-            const double2 h0 = *reinterpret_cast<const double2*>(a_h + kk * BM + gq * RX + tx * 2);
-            const double2 h1 = *reinterpret_cast<const double2*>(a_h + (kk + 1) * BM + gq * RX + tx * 2);
-            ah0[2 * gq] = h0.x; ah0[2 * gq + 1] = h0.y;
-            ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y;
-          }
+          for (int pq = 0; pq < SPLIT_BODY; pq += 2) {
+            double ah0[TM], ah1[TM], bh0[TN], bh1[TN];
 #pragma unroll
-          for (int b = 0; b < TN; ++b) {
-            const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
-            const double2 h = *reinterpret_cast<const double2*>(b_h + cj * BK + kk);
-            bh0[b] = h.x; bh1[b] = h.y;
-          }
-#pragma unroll
-          for (int a = 0; a < TM; ++a)
+            for (int gq = 0; gq < TM / 2; ++gq) {
+              const double2 h0 =
+                  *reinterpret_cast<const double2*>(a_h + (kk + pq) * BM + gq * RX + tx * 2);
+              const double2 h1 =
+                  *reinterpret_cast<const double2*>(a_h + (kk + pq + 1) * BM + gq * RX + tx * 2);
+              ah0[2 * gq] = h0.x; ah0[2 * gq + 1] = h0.y;
+              ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y;
+            }
 #pragma unroll
             for (int b = 0; b < TN; ++b) {
-              const double T = H[a][b];
-              const double Tn = dfma(ah0[a], bh0[b], T);
-              const double r = dfma(ah0[a], bh0[b], dsub(T, Tn));
-              const double T1 = dfma(ah1[a], bh1[b], Tn);
-              const double r1 = dfma(ah1[a], bh1[b], dsub(Tn, T1));
-              const double l = dadd(dadd(L[a][b], r), r1);
-              const double T2 = dadd(T1, l);
-              L[a][b] = dsub(l, dsub(T2, T1));
-              H[a][b] = T2;
+              const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
+              const double2 h = *reinterpret_cast<const double2*>(bs + cj * KB + kk + pq);
+              bh0[b] = h.x; bh1[b] = h.y;
             }
+            if (SPLIT_CHAIN) {   // per element: both steps of the pair (and its folds)
+#pragma unroll
+              for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) {
+                  double T = H[a][b], l = L[a][b];
+#pragma unroll
+                  for (int q = 0; q < 2; ++q) {
+                    const double av = q ? ah1[a] : ah0[a], bv = q ? bh1[b] : bh0[b];
+                    const double Tn = dfma(av, bv, T);
+                    l = dadd(l, dfma(av, bv, dsub(T, Tn)));
+                    T = Tn;
+                    if ((pq + q + 1) % SPLIT_FOLD == 0) {
+                      const double T2 = dadd(T, l);
+                      l = dsub(l, dsub(T2, T));
+                      T = T2;
+                    }
+                  }
+                  H[a][b] = T;
+                  L[a][b] = l;
+                }
+            } else {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+#pragma unroll
+              for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TN; ++b) {
+                  const double av = q ? ah1[a] : ah0[a], bv = q ? bh1[b] : bh0[b];
+                  const double T = H[a][b];
+                  const double Tn = dfma(av, bv, T);
+                  L[a][b] = dadd(L[a][b], dfma(av, bv, dsub(T, Tn)));
+                  H[a][b] = Tn;
+                }
+              if ((pq + q + 1) % SPLIT_FOLD == 0) {
+#pragma unroll
+                for (int a = 0; a < TM; ++a)
+#pragma unroll
+                  for (int b = 0; b < TN; ++b) {
+                    const double T2 = dadd(H[a][b], L[a][b]);
+                    L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
+                    H[a][b] = T2;
+                  }
+              }
+            }
+            }
+          }
         }
       } else {
 #pragma unroll (kTmaUnroll)
@@ -436,23 +508,22 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // 256 bytes doubled the DRAM reads (ncu, round 1), so B uses 128-byte lines.
   const CUtensorMapL2promotion pa = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   const CUtensorMapL2promotion pb = CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
-  if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, BK, pa) ||
-      !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, BK, pa) ||
-      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, BK, BN, pb) ||
-      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, BK, BN, pb))
+  // ALG_SPLIT: the cross terms first, as two binary64 GEMMs into a
+  // stream-ordered m x n scratch, then the hi * hi kernel.  Shallow calls (the
+  // LAPACK consumers' depth-256 updates) lose more to the cross GEMMs' fixed
+  // costs than the kernel gains: measured Rpotrf / Rgetrf / Rtrsm at n = 8192
+  // 1-3 % slower with the split at k = 256; Rsyrk n = k = 4096 4.5 % faster.
+  const int policy = split_policy();
+  const bool split_alg = alg == ALG_CERT && policy != 0 && (policy == 2 || g.k >= 1024);
+  const uint32_t kb = split_alg ? SPLIT_BK : BK;
+  if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, kb, pa) ||
+      !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, kb, pa) ||
+      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, kb, BN, pb) ||
+      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, kb, BN, pb))
     return cudaErrorNotSupported;
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
   auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
-  // ALG_SPLIT (Rgemm only): the cross terms first, as two binary64 GEMMs
-  // into a stream-ordered m x n scratch, then the hi * hi kernel
-  // Shallow calls (the LAPACK consumers' depth-256 updates) lose more to the
-  // cross GEMMs' fixed costs than the kernel gains: measured Rpotrf / Rgetrf /
-  // Rtrsm at n = 8192 3-4 % slower with the split at k = 256, Rsyrk even at
-  // n = k = 4096 (cuBLAS DSYR2K runs below DGEMM's rate).
-  const int policy = split_policy();
-  const bool split_alg = alg == ALG_CERT && policy != 0 &&
-                         (policy == 2 || g.k >= (g.syrk ? 8192 : 1024));
   GemmArgs ga = g;
   double* xbuf = nullptr;
   if (split_alg) {

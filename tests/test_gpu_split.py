@@ -1,7 +1,8 @@
 """GPU: fast mode's split algorithm (ALG_SPLIT, dd_tma.cu) forced at every
-depth (DDB_SPLIT=2; by default it only runs for k >= 1024, Rsyrk k >= 8192).
+depth (DDB_SPLIT=2; by default it only runs for k >= 1024).
 The anchored hi*hi kernel plus the binary64 cross-term GEMMs must stay inside
-the dd error bound with c = 3 (its analysis, dd_tma.cu's header), on the
+the dd error bound (analysed worst case c <= 3.6, dd_tma.cu's header; tested
+here with the tighter c = 3), on the
 adversarial magnitude patterns, Rsyrk triangles, split-K and the transposed
 routes, and leave everything outside the written region untouched."""
 
