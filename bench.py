@@ -133,6 +133,18 @@ def cpu_sample_rate(n, k, cols, threads):
     return 2.0 * m * cols * k / dt / 1e9, dt, f"Rgemm NN m={m} n={cols} k={k} (columns of the n={n} workload)"
 
 
+def cpu_sample_cols(n, k, seconds):
+    """Columns of the n x n x k workload that take about `seconds` on the
+    host cores, from a 16-column probe: a bounded sample (the whole-workload
+    CPU run would take hours), rounded to a multiple of the thread count."""
+    from oracle import oracle
+    threads = max(1, oracle.max_threads())
+    _, dt, _ = cpu_sample_rate(n, k, 16, 0)
+    cols = int(16 * seconds / max(dt, 1e-3))
+    cols = max(threads, (cols // threads) * threads)
+    return min(cols, n)
+
+
 def cpu_lapack_rates(n=512):
     """The reference's LAPACK consumers on the host (the bit-exact C port of
     the unblocked algorithms, one core) at a sample size n: dd GFlops in the
@@ -167,7 +179,7 @@ def run_reference_arm(args):
     from oracle import oracle
     threads = oracle.max_threads()
     n = args.n
-    cols = max(threads, 8)
+    cols = cpu_sample_cols(n, n, 2.0)
     for _ in range(args.warmup):
         cpu_sample_rate(n, n, cols, threads)
     rates, secs = [], []
@@ -345,7 +357,7 @@ def run_ours(args):
                     # dd roof = measured DFMA peak / 20 fp64 flops per dd MAC x 2 dd flops
                     roof = extra["roofline"]["peak"] * 1e3 / 10.0
                     extra[key]["roofline_frac"] = extra[key]["value"] / roof
-        cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, 16, 0)
+        cpu_rate, cpu_s, desc = cpu_sample_rate(n, k, cpu_sample_cols(n, k, 10.0), 0)
         from oracle import oracle
         extra["cpu_baseline"] = {"value": cpu_rate, "unit": UNIT, "cores": oracle.max_threads(),
                                  "kind": "port", "sample": desc, "seconds": cpu_s}
