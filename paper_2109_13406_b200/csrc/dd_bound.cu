@@ -119,6 +119,30 @@ cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_e
 // |error| <= 2k u * sum_l (|a_lo b_hi| + |a_hi b_lo|) <= 4k u^2 * sum_l |a_hi b_hi|
 // for normalised operands (|lo| <= u |hi|, enforced by the prescan), i.e.
 // one unit of the c k 2^-104 budget (dd_tma.cu).
+// x(i, j) += x(j, i) on the uplo triangle (diagonal: 2 x(i, i)), in place: a
+// tile of the triangle reads only its mirror tile in the other triangle, which
+// no block writes, and the diagonal tiles stage the mirror in shared memory
+// before any write.  Turns Y = op(A)_hi op(A)_lo^T into the Rsyrk cross term
+// Y + Y^T.  HBM-bound: 16 bytes read + 8 written per triangle element.
+__global__ void __launch_bounds__(256)
+sym_fold_kernel(double* __restrict__ x, int64_t n, int upper) {
+  const int64_t bi = blockIdx.x, bj = blockIdx.y;       // tile row / tile column
+  if (upper ? bi > bj : bi < bj) return;
+  __shared__ double t[32][33];
+  const int64_t r0 = bi * 32, c0 = bj * 32;
+  // mirror tile: rows c0.., columns r0.. ; t[c][r] = x(c0 + c, r0 + r)^T staged
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int64_t mr = c0 + threadIdx.x, mc = r0 + y;
+    if (mr < n && mc < n) t[threadIdx.x][y] = x[mr + mc * n];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += 8) {
+    const int64_t i = r0 + threadIdx.x, j = c0 + y;
+    if (i < n && j < n && (upper ? i <= j : i >= j))
+      x[i + j * n] = x[i + j * n] + t[y][threadIdx.x];
+  }
+}
+
 cudaError_t launch_cross_dgemm(const GemmArgs& g, double* x, cudaStream_t s) {
   cublasHandle_t h = handle_for_current_device();
   if (h == nullptr) return cudaErrorUnknown;
@@ -127,12 +151,19 @@ cudaError_t launch_cross_dgemm(const GemmArgs& g, double* x, cudaStream_t s) {
   const cublasOperation_t opa = g.ta == 0 ? CUBLAS_OP_N : CUBLAS_OP_T;
   const cublasOperation_t opb = g.tb == 0 ? CUBLAS_OP_N : CUBLAS_OP_T;
   if (g.syrk != 0) {
-    // Rsyrk in NN form (op(B) = op(A)^T): only the uplo triangle is read,
-    // x = op(A)_hi op(A)_lo^T + op(A)_lo op(A)_hi^T is one DSYR2K (half the flops)
-    const cublasFillMode_t up = g.syrk == 1 ? CUBLAS_FILL_MODE_UPPER : CUBLAS_FILL_MODE_LOWER;
-    const cublasStatus_t st = cublasDsyr2k(h, up, opa, (int)g.m, (int)g.k, &one, g.a_hi,
-                                           (int)g.lda, g.a_lo, (int)g.lda, &zero, x, (int)g.m);
+    // Rsyrk in NN form (op(B) = op(A)^T): only the uplo triangle is read.
+    // x = op(A)_hi op(A)_lo^T + op(A)_lo op(A)_hi^T = Y + Y^T with
+    // Y = op(A)_hi op(A)_lo^T: one full DGEMM (DMMA tensor cores, 30.8 ms at
+    // n = k = 8192) and an in-place triangle fold, instead of cuBLAS DSYR2K
+    // (same flops, but a SIMT kernel: 40.5 ms).  The fold adds one rounding
+    // to two length-k sums: the 2k u bound above still holds.
+    const cublasOperation_t opt = g.ta == 0 ? CUBLAS_OP_T : CUBLAS_OP_N;
+    const cublasStatus_t st = cublasDgemm(h, opa, opt, (int)g.m, (int)g.m, (int)g.k, &one,
+                                          g.a_hi, (int)g.lda, g.a_lo, (int)g.lda, &zero, x,
+                                          (int)g.m);
     if (st != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    const unsigned tiles = (unsigned)((g.m + 31) / 32);
+    sym_fold_kernel<<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(x, g.m, g.syrk == 1);
     return cudaGetLastError();
   }
   cublasStatus_t st = cublasDgemm(h, opa, opb, (int)g.m, (int)g.n, (int)g.k, &one, g.a_lo,

@@ -21,9 +21,9 @@
 // the certified anchor (Tn = fma(ah, bh, T), r = fma(ah, bh, T - Tn), L += r,
 // (T, L) folded every 3 steps: 5 FP64 instructions per MAC instead of 7.5,
 // and only the hi planes staged, 24-deep k-tiles), and the cross terms
-// X = A_lo B_hi + A_hi B_lo, two plain binary64 library GEMMs (DSYR2K for
-// Rsyrk) run first and added to L in the epilogue; al bl (< u^2 |ab|) is
-// dropped, as in every dd product.  Error per element, with the unit
+// X = A_lo B_hi + A_hi B_lo, two plain binary64 library GEMMs (for Rsyrk
+// one DGEMM + a triangle fold, dd_bound.cu) run first and added to L in the
+// epilogue; al bl (< u^2 |ab|) is dropped, as in every dd product.  Error per element, with the unit
 // v = 2^(E-106) < 2^-104 S' (2^E < 4 S', S' >= sum |ah bh| the certified
 // bound): each residual r (|r| <= ulp(T)/2 = 2^(E-53)) rounds by <= v/2; after
 // a fold |L| <= 2^(E-53), so by monotone rounding the three additions into L
