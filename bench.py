@@ -346,6 +346,8 @@ def run_ours(args):
             extra["f64"] = _f64(n, dev, stream)
             extra["cgemm"] = _cgemm(n // 2, dev, stream, mode)
             extra["trans_sweep"] = _trans_sweep(n // 2, dev, stream, mode)
+            extra["syrk_sweep"] = _syrk_sweep(n // 2, dev, stream, mode)
+            extra["deep_k"] = _deep_k(n // 4, 8 * n, dev, stream, mode)
             extra["rpotrf"] = _rpotrf(n, dev, stream, mode)
             extra["rgetrf"] = _rgetrf(n, dev, stream, mode)
             extra["rtrsm"] = _rtrsm(n, dev, stream, mode)
@@ -477,6 +479,35 @@ def _trans_sweep(n, dev, stream, mode):
                                         mats[2], n, mode=mode), 2, 1, stream)
             out[ta + tb] = 2.0 * n ** 3 / min(times) / 1e9
     return out
+
+
+def _syrk_sweep(n, dev, stream, mode):
+    """BASELINE configs[2]: Rsyrk n = k over uplo U / L x trans N / T."""
+    from paper_2109_13406_b200 import DeviceMatrix, Rsyrk, flop_count
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    A = DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, 1, dev))
+    C = DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, 3, dev))
+    out = {"workload": f"dd Rsyrk n=k={n}", "unit": UNIT, "mode": mode}
+    for uplo in "UL":
+        for tr in "NT":
+            times = timed(lambda: Rsyrk(uplo, tr, n, n, ALPHA, A, n, BETA, C, n, mode=mode),
+                          2, 1, stream)
+            out[uplo + tr] = flop_count("Rsyrk", n, k=n) / min(times) / 1e9
+    return out
+
+
+def _deep_k(m, k, dev, stream, mode):
+    """BASELINE configs[3]: Rgemm NN m = n, deep k (accumulation depth)."""
+    from paper_2109_13406_b200 import DeviceMatrix, Rgemm
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    A = DeviceMatrix(m, k, "dd", m, store=hashed_dd_device(m, k, 0, 1, dev))
+    B = DeviceMatrix(k, m, "dd", k, store=hashed_dd_device(k, m, 0, 2, dev))
+    C = DeviceMatrix(m, m, "dd", m, store=hashed_dd_device(m, m, 0, 3, dev))
+    times = timed(lambda: Rgemm("N", "N", m, m, k, ALPHA, A, m, B, k, BETA, C, m, mode=mode),
+                  2, 1, stream)
+    t = min(times)
+    return {"workload": f"dd Rgemm NN m=n={m} k={k}", "value": 2.0 * m * m * k / t / 1e9,
+            "unit": UNIT, "ms": t * 1e3, "mode": mode}
 
 
 def _cgemm(n, dev, stream, mode):
