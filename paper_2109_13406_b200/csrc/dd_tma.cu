@@ -77,12 +77,16 @@ constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 10
 #ifndef DDB_SPLIT_UNROLL
 #define DDB_SPLIT_UNROLL 2    // k-loop bodies unrolled per trip (2: 240.4 vs 241.8 ms at 8192^3)
 #endif
+#ifndef DDB_SPLIT_TN
+#define DDB_SPLIT_TN 4        // split kernel: columns per thread (tile width SPLIT_TN / 2 * 32)
+#endif
 constexpr int SPLIT_BK = DDB_SPLIT_BK, SPLIT_FOLD = DDB_SPLIT_FOLD;
+constexpr int SPLIT_TN = DDB_SPLIT_TN, SPLIT_BN = SPLIT_TN / 2 * RY;
 constexpr bool SPLIT_CHAIN = DDB_SPLIT_CHAIN;
 constexpr int SPLIT_UNROLL = DDB_SPLIT_UNROLL;
 constexpr int SPLIT_BODY = SPLIT_FOLD % 2 == 0 ? SPLIT_FOLD : 2 * SPLIT_FOLD;   // even
 static_assert(SPLIT_BK % SPLIT_BODY == 0 && SPLIT_BK % 2 == 0, "split k-tile");
-static_assert((SPLIT_BK * (BM + BN)) * 8 <= STAGE_BYTES, "split stage fits the ring");
+static_assert((SPLIT_BK * (BM + SPLIT_BN)) * 8 <= STAGE_BYTES, "split stage fits the ring");
 // split-K chunks must be whole k-tiles of every kernel (dd_gemm.cu)
 static_assert(96 % SPLIT_BK == 0 || SPLIT_BK == 32, "chunk rounding");
 
@@ -134,6 +138,8 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
   constexpr int AP = KB * BM;                                     // A hi plane, doubles
   // stage layout: A hi | A lo | B hi | B lo (split: A hi | B hi)
   constexpr int B_OFF = ALG == ALG_SPLIT ? AP : 2 * A_PLANE;
+  // per-thread columns / tile width (split: SPLIT_TN, the hi planes leave room)
+  constexpr int TNK = ALG == ALG_SPLIT ? SPLIT_TN : TN, BNK = TNK / 2 * RY;
 
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // align by an offset from the __shared__ array (an integer round trip of
@@ -165,7 +171,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     const int gm = min(tiles_m - first_m, GM_);
     const int local = tile % group_size;
     i0 = (int64_t)(first_m + local % gm) * BM;
-    j0 = (int64_t)(local / gm) * BN;
+    j0 = (int64_t)(local / gm) * BNK;
     kbeg = (int64_t)split * kchunk;
     const int64_t kend = min(g.k, kbeg + kchunk);
     ktiles = (int)((kend - kbeg + KB - 1) / KB);
@@ -178,7 +184,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     int64_t i0, j0, kb;
     int kt;
     unit_origin(u, i0, j0, kb, kt);
-    return SYRK == 1 ? i0 > j0 + BN - 1 : i0 + BM - 1 < j0;
+    return SYRK == 1 ? i0 > j0 + BNK - 1 : i0 + BM - 1 < j0;
   };
   auto next_unit = [&](int u) {   // first unit >= u in this CTA's stride that is not skipped
     while (u < units && skipped(u)) u += gridDim.x;
@@ -197,7 +203,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     double* st = ring + s * STAGE_DOUBLES;
     const int kc = (int)(p_kbeg + (int64_t)p_kt * KB);
     if (ALG == ALG_SPLIT) {   // hi planes only
-      mbar_expect_tx(&full[s], (uint32_t)(KB * (BM + BN)) * 8u);
+      mbar_expect_tx(&full[s], (uint32_t)(KB * (BM + BNK)) * 8u);
       tma_load_2d(st, &mAh, (int)p_i0, kc, &full[s]);
       tma_load_2d(st + B_OFF, &mBh, kc, (int)p_j0, &full[s]);
     } else {
@@ -225,12 +231,12 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     int ktiles;
     unit_origin(u, i0, j0, kbeg, ktiles);
 
-    double H[TM][TN], L[TM][TN];
+    double H[TM][TNK], L[TM][TNK];
     if (CERTLIKE) {
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
-        for (int b = 0; b < TN; ++b) {
+        for (int b = 0; b < TNK; ++b) {
           const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
           const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
           const bool in = gi < g.m && gj < g.n;
@@ -245,7 +251,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
-        for (int b = 0; b < TN; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
+        for (int b = 0; b < TNK; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
     }
 
     for (int kt = 0; kt < ktiles; ++kt, ++c_item) {
@@ -266,7 +272,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
         for (int kk = 0; kk < KB; kk += SPLIT_BODY) {
 #pragma unroll
           for (int pq = 0; pq < SPLIT_BODY; pq += 2) {
-            double ah0[TM], ah1[TM], bh0[TN], bh1[TN];
+            double ah0[TM], ah1[TM], bh0[TNK], bh1[TNK];
 #pragma unroll
             for (int gq = 0; gq < TM / 2; ++gq) {
               const double2 h0 =
@@ -277,7 +283,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
               ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y;
             }
 #pragma unroll
-            for (int b = 0; b < TN; ++b) {
+            for (int b = 0; b < TNK; ++b) {
               const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
               const double2 h = *reinterpret_cast<const double2*>(bs + cj * KB + kk + pq);
               bh0[b] = h.x; bh1[b] = h.y;
@@ -286,7 +292,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 #pragma unroll
               for (int a = 0; a < TM; ++a)
 #pragma unroll
-                for (int b = 0; b < TN; ++b) {
+                for (int b = 0; b < TNK; ++b) {
                   double T = H[a][b], l = L[a][b];
 #pragma unroll
                   for (int q = 0; q < 2; ++q) {
@@ -309,7 +315,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 #pragma unroll
               for (int a = 0; a < TM; ++a)
 #pragma unroll
-                for (int b = 0; b < TN; ++b) {
+                for (int b = 0; b < TNK; ++b) {
                   const double av = q ? ah1[a] : ah0[a], bv = q ? bh1[b] : bh0[b];
                   const double T = H[a][b];
                   const double Tn = dfma(av, bv, T);
@@ -320,7 +326,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 #pragma unroll
                 for (int a = 0; a < TM; ++a)
 #pragma unroll
-                  for (int b = 0; b < TN; ++b) {
+                  for (int b = 0; b < TNK; ++b) {
                     const double T2 = dadd(H[a][b], L[a][b]);
                     L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
                     H[a][b] = T2;
@@ -333,7 +339,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
       } else {
 #pragma unroll (kTmaUnroll)
       for (int kk = 0; kk < BK; kk += 2) {
-        double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TN], bl0[TN], bh1[TN], bl1[TN];
+        double ah0[TM], al0[TM], ah1[TM], al1[TM], bh0[TNK], bl0[TNK], bh1[TNK], bl1[TNK];
 #pragma unroll
         for (int gq = 0; gq < TM / 2; ++gq) {
           const double2 h0 = *reinterpret_cast<const double2*>(a_h + kk * BM + gq * RX + tx * 2);
@@ -344,19 +350,19 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
           ah1[2 * gq] = h1.x; ah1[2 * gq + 1] = h1.y; al1[2 * gq] = l1.x; al1[2 * gq + 1] = l1.y;
         }
 #pragma unroll
-        for (int b = 0; b < TN; ++b) {   // k-major B: (kk, kk+1) of column cj in one LDS
+        for (int b = 0; b < TNK; ++b) {   // k-major B: (kk, kk+1) of column cj in one LDS
           const int cj = (b >> 1) * RY + ty * 2 + (b & 1);
           const double2 h = *reinterpret_cast<const double2*>(b_h + cj * BK + kk);
           const double2 l = *reinterpret_cast<const double2*>(b_l + cj * BK + kk);
           bh0[b] = h.x; bh1[b] = h.y; bl0[b] = l.x; bl1[b] = l.y;
         }
-        tiled::mac_step<ALG, TM, TN>(H, L, ah0, al0, bh0, bl0);
-        tiled::mac_step<ALG, TM, TN>(H, L, ah1, al1, bh1, bl1);
+        tiled::mac_step<ALG, TM, TNK>(H, L, ah0, al0, bh0, bl0);
+        tiled::mac_step<ALG, TM, TNK>(H, L, ah1, al1, bh1, bl1);
         if (ALG == ALG_CERT) {
 #pragma unroll
           for (int a = 0; a < TM; ++a)
 #pragma unroll
-            for (int b = 0; b < TN; ++b) {
+            for (int b = 0; b < TNK; ++b) {
               const double T2 = dadd(H[a][b], L[a][b]);
               L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
               H[a][b] = T2;
@@ -365,7 +371,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 #pragma unroll
           for (int a = 0; a < TM; ++a)
 #pragma unroll
-            for (int b = 0; b < TN; ++b) {
+            for (int b = 0; b < TNK; ++b) {
               double sx, ex;
               quick_two_sum(H[a][b], L[a][b], sx, ex);
               H[a][b] = sx;
@@ -383,7 +389,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 #pragma unroll
     for (int a = 0; a < TM; ++a)
 #pragma unroll
-      for (int b = 0; b < TN; ++b) {
+      for (int b = 0; b < TNK; ++b) {
         const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
         const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
         if (gi >= g.m || gj >= g.n) continue;
@@ -516,12 +522,13 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   const int policy = split_policy();
   const bool split_alg = alg == ALG_CERT && policy != 0 && (policy == 2 || g.k >= 1024);
   const uint32_t kb = split_alg ? SPLIT_BK : BK;
+  const uint32_t bn = split_alg ? SPLIT_BN : BN;
   if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, kb, pa) ||
       !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, kb, pa) ||
-      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, kb, BN, pb) ||
-      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, kb, BN, pb))
+      !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, kb, bn, pb) ||
+      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, kb, bn, pb))
     return cudaErrorNotSupported;
-  const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
+  const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + bn - 1) / bn);
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
   auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
   GemmArgs ga = g;
