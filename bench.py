@@ -420,8 +420,9 @@ def _e2e(n, k, mode, distributed, world, rank, dev):
             dist.barrier()
         t0 = time.perf_counter()
         if distributed:
-            parallel.rgemm_host_columns("N", "N", n, n, k, ALPHA, *(hm if hm else (None,) * 3),
-                                        BETA, world, rank, dev, mode=mode)
+            a, b, c = hm if hm else (None,) * 3
+            parallel.rgemm_host_columns("N", "N", n, n, k, ALPHA, a, b, BETA, c, world, rank, dev,
+                                        mode=mode)
         else:
             Rgemm("N", "N", n, n, k, ALPHA, hm[0], n, hm[1], k, BETA, hm[2], n, mode=mode)
         torch.cuda.synchronize()

@@ -339,15 +339,20 @@ def rsyrk_columns(n, k, world, rank, device, uplo, trans, alpha, a, beta, c, mod
 
 
 def rgemm_host_columns(transa, transb, m, n, k, alpha, a, b, beta, c, world, rank, device,
-                       mode=None, group=None):
+                       mode=None, group=None, compute=None):
     """End-to-end variant: host (numpy) operands on the root are staged to its
-    GPU, the column-split Rgemm runs, and C is copied back to the host."""
+    GPU, the column-split Rgemm runs, and C is copied back to the host.
+    Argument order as Rgemm's (alpha, a, b, beta, c); a, b, c are HostMatrix
+    on rank 0 and None elsewhere."""
     plan = RgemmPlan(m, n, k, world, rank, device)
     if rank == 0:
         A, B, C = (DeviceMatrix.from_host(x, device) for x in (a, b, c))
     else:
         A = B = C = None
-    rgemm_columns(plan, transa, transb, alpha, A, B, beta, C, mode=mode, group=group)
+    rgemm_columns(plan, transa, transb, alpha, A, B, beta, C, mode=mode, group=group,
+                  compute=compute)
     if rank == 0:
-        c.store[0][:] = C.store[0].cpu().numpy()
-        c.store[1][:] = C.store[1].cpu().numpy()
+        # straight into the caller's (pinned) planes: one DMA per plane, no
+        # pageable temporary
+        for dst, src in zip(c.store, C.store):
+            torch.from_numpy(dst).copy_(src)

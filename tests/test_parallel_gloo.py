@@ -71,6 +71,24 @@ def _worker(rank, world, port, case, q):
                                    kchunks=kchunks, mode=mode)
             if rank == 0:
                 q.put((C.store[0].numpy().copy(), C.store[1].numpy().copy()))
+        elif case[0] == "host":
+            from paper_2109_13406_b200 import HostMatrix
+            _, m, n, k = case
+            hm = None
+            if rank == 0:
+                hm = []
+                for rows, cols, tag in ((m, k, 1), (k, n, 2), (m, n, 3)):
+                    h = HostMatrix(rows, cols, "dd", rows)
+                    hi, lo = random_dd(rows, cols, rows, 5, tag)
+                    h.store[0][:] = hi
+                    h.store[1][:] = lo
+                    hm.append(h)
+            a, b, c = hm if hm else (None,) * 3
+            # the bench's e2e call (bench.py _e2e), argument order as Rgemm's
+            parallel.rgemm_host_columns("N", "N", m, n, k, 1.5, a, b, 0.5, c, world, rank,
+                                        torch.device("cpu"), compute=oracle_gemm)
+            if rank == 0:
+                q.put((np.array(c.store[0]), np.array(c.store[1])))
         else:
             _, up, tr, n, k = case
             nra, nca = (n, k) if tr == "N" else (k, n)
@@ -111,6 +129,19 @@ def test_rgemm_columns_bitwise_equal_single_process(ta, tb, beta):
     B = random_dd(nrb, ncb, nrb, 3, 2)
     ch, cl = (x.copy() for x in random_dd(m, n, m, 3, 3))
     oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra, B[0], B[1], nrb, to_dd(beta),
+                 ch, cl, m)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+def test_rgemm_host_columns_bitwise_equal_single_process():
+    """The end-to-end multi-rank entry (host buffers on rank 0) the bench's
+    N > 1 e2e leg calls: the single-process result bit for bit."""
+    m, n, k = 64, 90, 40
+    got = _run(("host", m, n, k))
+    A = random_dd(m, k, m, 5, 1)
+    B = random_dd(k, n, k, 5, 2)
+    ch, cl = (x.copy() for x in random_dd(m, n, m, 5, 3))
+    oracle.rgemm("N", "N", m, n, k, (1.5, 0.0), A[0], A[1], m, B[0], B[1], k, (0.5, 0.0),
                  ch, cl, m)
     assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
 
