@@ -437,7 +437,10 @@ def _e2e(n, k, mode, distributed, world, rank, dev):
         t = float(tt.item())
     return {"value": 2.0 * n * n * k / t / 1e9, "unit": UNIT,
             "h2d_bytes_per_step": 16 * (n * k + k * n + n * n), "d2h_bytes_per_step": 16 * n * n,
-            "ms_per_step": t * 1e3, "host_buffers": "pinned numpy planes, ddb_rgemm_host"}
+            "ms_per_step": t * 1e3,
+            "host_buffers": "pinned numpy planes, " + (
+                "parallel.rgemm_host_columns (staged on the root, then column-split)"
+                if distributed else "ddb_rgemm_host")}
 
 
 def _rsyrk(n, k, mode, dev, stream, steps):
