@@ -239,6 +239,24 @@ int ddb_last_route(void);
  * bench's roofline denominator. */
 double ddb_fp64_peak_probe(void* stream);
 
+/* Diagnostic: the split algorithm's cross terms alone (device pointers,
+ * asynchronous on `stream`): X (m x n, ld = m) = A_lo*B_hi + A_hi*B_lo, NN,
+ * on the hand-written DMMA kernel.  Planes 16-byte aligned, lda / ldb even.
+ * tri: 0 all tiles, 1 / 2 only tiles meeting the upper / lower triangle. */
+int ddb_cross_terms(int64_t m, int64_t n, int64_t k, const double* a_hi, const double* a_lo,
+                    int64_t lda, const double* b_hi, const double* b_lo, int64_t ldb, double* x,
+                    int tri, void* stream);
+
+/* Diagnostic: the fast mode's certified magnitude bound alone (device
+ * pointers, synchronous).  row_exp (m) / col_exp (n): biased exponent maxima
+ * of op(A) rows / op(B) columns; abf (m x kp) / bbf (n x kp), kp = k rounded
+ * up to 8, may be NULL: |hi| * 2^(1022 - exp) rounded up to bf16, K-major;
+ * s_out (m x n, ld = m): abf * bbf^T in fp32 on the tcgen05 kernel. */
+int ddb_abs_bound(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                  const double* a_hi, int64_t lda, const double* b_hi, int64_t ldb,
+                  int* row_exp, int* col_exp, float* s_out, uint16_t* abf, uint16_t* bbf,
+                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -606,4 +606,81 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
   return stage_out1(c, C, sc, s);
 }
 
+// ---- diagnostics: the fast mode's building blocks in isolation --------------
+
+// X (m x n, ld = m) = A_lo B_hi + A_hi B_lo on the hand-written DMMA kernel
+// (dd_cross.cu).  NN operands: 16-byte aligned planes, even lda / ldb.
+// tri: 0 every tile, 1 / 2 only tiles meeting the upper / lower triangle.
+int ddb_cross_terms(int64_t m, int64_t n, int64_t k, const double* a_hi, const double* a_lo,
+                    int64_t lda, const double* b_hi, const double* b_lo, int64_t ldb, double* x,
+                    int tri, void* stream) {
+  if (m < 0 || n < 0 || k < 0 || lda < (m > 1 ? m : 1) || ldb < (k > 1 ? k : 1) || tri < 0 ||
+      tri > 2)
+    return DDB_EINVAL;
+  if (m == 0 || n == 0) return DDB_OK;
+  GemmArgs g{};
+  g.m = m; g.n = n; g.k = k;
+  g.a_hi = a_hi; g.a_lo = a_lo; g.lda = lda;
+  g.b_hi = b_hi; g.b_lo = b_lo; g.ldb = ldb;
+  g.syrk = tri;
+  int nl = 0;
+  cudaError_t e = launch_cross_dmma(g, x, static_cast<cudaStream_t>(stream), &nl);
+  g_launches += nl;
+  if (e == cudaErrorNotSupported) {
+    g_last_error = "ddb_cross_terms: operands not TMA-eligible (alignment / odd ld)";
+    return DDB_EINVAL;
+  }
+  if (e != cudaSuccess) return fail(e, "cross-term kernel launch");
+  return DDB_OK;
+}
+
+// The certified magnitude bound alone (dd_bound.cu): the prescan's exponent
+// maxima of op(A) rows / op(B) columns (row_exp m, col_exp n), the scaled
+// rounded-up bf16 magnitudes K-major (abf m x kp, bbf n x kp, kp = k rounded
+// up to 8; may be NULL) and S = abf * bbf^T in fp32 (m x n, ld = m), as the
+// tcgen05 kernel computes it.  Device pointers; synchronous.
+int ddb_abs_bound(char transa, char transb, int64_t m, int64_t n, int64_t k,
+                  const double* a_hi, int64_t lda, const double* b_hi, int64_t ldb,
+                  int* row_exp, int* col_exp, float* s_out, uint16_t* abf, uint16_t* bbf,
+                  void* stream) {
+  int rc = ddb_rgemm_validate(transa, transb, m, n, k, lda, ldb, m > 1 ? m : 1);
+  if (rc) return rc;
+  if (m == 0 || n == 0 || k == 0) return DDB_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GemmArgs g{};
+  g.ta = upflag(transa) == 'N' ? 0 : 1;
+  g.tb = upflag(transb) == 'N' ? 0 : 1;
+  g.m = m; g.n = n; g.k = k;
+  g.a_hi = a_hi; g.a_lo = a_hi; g.lda = lda;   // lo planes only feed the window test
+  g.b_hi = b_hi; g.b_lo = b_hi; g.ldb = ldb;
+  retain_pool_memory();
+  const size_t head = route_ws_bytes(m, n, 0);
+  const size_t bb = (bound_workspace_bytes(g) + 255) / 256 * 256;
+  void* ws = nullptr;
+  cudaError_t e = cudaMallocAsync(&ws, head + bb, s);
+  if (e != cudaSuccess) return fail(e, "workspace allocation");
+  const RouteWs r = route_ws_carve(ws, m, n, 0);
+  int nl = 0;
+  const char* what = "bound";
+  e = cudaMemsetAsync(ws, 0, head, s);
+  if (e == cudaSuccess) e = launch_prescan(g, ALG_EXACT, r, s, &nl);
+  char* bw = static_cast<char*>(ws) + head;
+  float* bound = bound_carve(g, bw);
+  if (e == cudaSuccess) e = launch_bound(g, r.rmax, r.cmax, bw, bound, s, &nl, &what);
+  g_launches += nl;
+  const int64_t kp = (k + 7) / 8 * 8;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(row_exp, r.rmax, sizeof(int) * m, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(col_exp, r.cmax, sizeof(int) * n, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(s_out, bound, sizeof(float) * m * n, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && abf != nullptr)
+    e = cudaMemcpyAsync(abf, bw, 2 * (size_t)m * kp, cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess && bbf != nullptr)
+    e = cudaMemcpyAsync(bbf, bw + (2 * (size_t)m * kp + 1023) / 1024 * 1024, 2 * (size_t)n * kp,
+                        cudaMemcpyDeviceToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFreeAsync(ws, s);
+  if (e != cudaSuccess) return fail(e, what);
+  return DDB_OK;
+}
+
 }  // extern "C"

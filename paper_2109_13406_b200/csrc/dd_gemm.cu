@@ -112,13 +112,13 @@ int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk) {
 
 __global__ void __launch_bounds__(256)
 splitk_reduce_kernel(GemmArgs g, int splits, const int* __restrict__ flag) {
-  if (*flag != ROUTE_SAFE) return;
   const int64_t i = (int64_t)blockIdx.x * 32 + threadIdx.x;
   if (i >= g.m) return;
   const size_t plane = (size_t)g.m * g.n;
   for (int64_t j = (int64_t)blockIdx.y * 8 + threadIdx.y; j < g.n; j += (int64_t)gridDim.y * 8) {
     if (g.syrk == 1 && i > j) continue;
     if (g.syrk == 2 && i < j) continue;
+    if (elem_class(g, i, j) == EC_REF) continue;   // dd_reference.cu writes it
     const size_t pi = i + j * g.m;
     dd acc{g.part[pi], g.part[plane + pi]};
     for (int z = 1; z < splits; ++z) {
@@ -140,6 +140,20 @@ cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag,
   splitk_reduce_kernel<<<grid, block, 0, s>>>(g, splits, flag);
   ++*nlaunch;
   return cudaGetLastError();
+}
+
+// Fast mode: the EC_WIDE elements (dd_prescan.cu) by the TwoSum accumulation
+// on the cp.async tiled kernel (any layout, no transposed copies); its CTAs
+// exit at once unless their tile may hold one, and the whole launch when the
+// call has none (flag[1] + flag[2] <= wide_lim).
+cudaError_t launch_wide_fallback(const GemmArgs& g, cudaStream_t s, int* nlaunch) {
+  if (g.m <= 0 || g.n <= 0 || g.wide_lim <= 0) return cudaSuccess;
+  GemmArgs gw = g;
+  gw.only_wide = 1;
+  gw.cross = nullptr;
+  gw.bound = nullptr;
+  ++*nlaunch;
+  return launch_tiled_twosum(0, gw, nullptr, nullptr, g.flag, s);
 }
 
 cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,

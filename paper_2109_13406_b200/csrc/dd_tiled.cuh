@@ -241,7 +241,6 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   constexpr int RX = 2 * C::NX, RY = 2 * C::NY;   // row / column group strides
   constexpr int STAGES = C::STAGES, ASTR = C::ASTR, BSTR = C::BSTR;
   constexpr int A_STAGE = C::A_STAGE, B_STAGE = C::B_STAGE;
-  if (*flag != ROUTE_SAFE) return;  // dd_reference.cu handles this call
 
   // grouped raster over the tile grid
   const int bid = blockIdx.x;
@@ -254,6 +253,8 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
   const int64_t i0 = (int64_t)bm * BM, j0 = (int64_t)bn * BN;
   if (SYRK == 1 && i0 > j0 + BN - 1) return;   // tile entirely below the diagonal
   if (SYRK == 2 && i0 + BM - 1 < j0) return;   // tile entirely above the diagonal
+  // TwoSum fallback launch (fast mode): only tiles that may hold EC_WIDE elements
+  if (g.only_wide && !tile_maybe_wide(g, i0, j0, BM, BN)) return;
 
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
@@ -479,6 +480,7 @@ dd_tiled_kernel(GemmArgs g, const int* __restrict__ row_exp, const int* __restri
       if (gi >= g.m || gj >= g.n) continue;
       if (SYRK == 1 && gi > gj) continue;
       if (SYRK == 2 && gi < gj) continue;
+      if (!elem_mine(g, gi, gj)) continue;   // routed elsewhere (internal.h: elem_class)
       const int64_t ci = gi + gj * g.ldc;
       if (ALG == ALG_F64) {    // level23.py:120-149 with the F64 backend (elem.py:149-197)
         if (TA == 0) {

@@ -40,6 +40,7 @@
 #include <cstdlib>
 
 #include "dd_tiled.cuh"
+#include "tma_util.cuh"
 
 namespace ddb {
 namespace tma {
@@ -90,36 +91,6 @@ static_assert((SPLIT_BK * (BM + SPLIT_BN)) * 8 <= STAGE_BYTES, "split stage fits
 // split-K chunks must be whole k-tiles of every kernel (dd_gemm.cu)
 static_assert(96 % SPLIT_BK == 0 || SPLIT_BK == 32, "chunk rounding");
 
-__device__ __forceinline__ uint32_t saddr(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(saddr(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(saddr(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}\n" ::"r"(saddr(b)), "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(saddr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar))
-      : "memory");
-}
-
 // Work unit = one (tile, k-slice).  PERSISTENT: gridDim.x CTAs (one per SM)
 // walk the units u = blockIdx.x + i * gridDim.x in raster order, so all SMs
 // work on the same wave of tiles at nearly the same k (the wave's A / B panel
@@ -132,7 +103,6 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                  const __grid_constant__ CUtensorMap mBl, const int* __restrict__ row_exp,
                  const int* __restrict__ col_exp, const int* __restrict__ flag, int tiles_m,
                  int tiles_n, int splits) {
-  if (*flag != ROUTE_SAFE) return;   // dd_reference.cu handles this call
   constexpr bool CERTLIKE = ALG == ALG_CERT || ALG == ALG_SPLIT;
   constexpr int KB = ALG == ALG_SPLIT ? SPLIT_BK : BK;            // k-tile depth
   constexpr int AP = KB * BM;                                     // A hi plane, doubles
@@ -395,6 +365,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
         if (gi >= g.m || gj >= g.n) continue;
         if (SYRK == 1 && gi > gj) continue;   // the uplo triangle only (level23.py:245-270)
         if (SYRK == 2 && gi < gj) continue;
+        if (!elem_mine(g, gi, gj)) continue;   // routed elsewhere (internal.h: elem_class)
         double sx, ex;
         const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
         double lv = L[a][b];
@@ -413,37 +384,6 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
         g.c_lo[ci] = out.l;
       }
   }
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
-typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                             const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                             const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeFn encode_fn() {
-  static EncodeFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (EncodeFn) nullptr;
-    return reinterpret_cast<EncodeFn>(p);
-  }();
-  return fn;
-}
-
-static bool encode(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t ld,
-                   uint32_t box_inner, uint32_t box_outer, CUtensorMapL2promotion promo) {
-  EncodeFn fn = encode_fn();
-  if (fn == nullptr) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  const cuuint32_t box[2] = {box_inner, box_outer};
-  const cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -520,24 +460,37 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // costs than the kernel gains: measured Rpotrf / Rgetrf / Rtrsm at n = 8192
   // 1-3 % slower with the split at k = 256; Rsyrk n = k = 4096 4.5 % faster.
   const int policy = split_policy();
-  const bool split_alg = alg == ALG_CERT && policy != 0 && (policy == 2 || g.k >= 1024);
+  bool split_alg = alg == ALG_CERT && policy != 0 && (policy == 2 || g.k >= 1024);
+  double* xbuf = nullptr;
+  if (split_alg &&
+      cudaMallocAsync(reinterpret_cast<void**>(&xbuf), sizeof(double) * (size_t)g.m * g.n, s) !=
+          cudaSuccess) {
+    // no room for the m x n cross-term scratch: the certified full MAC
+    // needs none (same error bound, ~13 % slower)
+    cudaGetLastError();
+    xbuf = nullptr;
+    split_alg = false;
+  }
   const uint32_t kb = split_alg ? SPLIT_BK : BK;
   const uint32_t bn = split_alg ? SPLIT_BN : BN;
   if (!encode(&mAh, g.a_hi, g.m, g.k, g.lda, BM, kb, pa) ||
       !encode(&mAl, g.a_lo, g.m, g.k, g.lda, BM, kb, pa) ||
       !encode(&mBh, g.b_hi, g.k, g.n, g.ldb, kb, bn, pb) ||
-      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, kb, bn, pb))
+      !encode(&mBl, g.b_lo, g.k, g.n, g.ldb, kb, bn, pb)) {
+    if (xbuf != nullptr) cudaFreeAsync(xbuf, s);
     return cudaErrorNotSupported;
+  }
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + bn - 1) / bn);
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
   auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
   GemmArgs ga = g;
-  double* xbuf = nullptr;
   if (split_alg) {
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&xbuf),
-                                    sizeof(double) * (size_t)g.m * g.n, s);
-    if (e != cudaSuccess) return e;
-    e = launch_cross_dgemm(g, xbuf, s);
+    // the cross terms first: hand-written DMMA kernel (dd_cross.cu), or the
+    // library DGEMMs for an A/B measurement (DDB_CROSS=cublas)
+    int nl = 0;
+    const char* v = std::getenv("DDB_CROSS");
+    cudaError_t e = (v != nullptr && v[0] == 'c') ? launch_cross_dgemm(g, xbuf, s)
+                                                  : launch_cross_dmma(g, xbuf, s, &nl);
     if (e != cudaSuccess) { cudaFreeAsync(xbuf, s); return e; }
     ga.cross = xbuf;
   }

@@ -81,8 +81,10 @@ cudaError_t panel_stream(cudaStream_t* out) {
   return cudaSuccess;
 }
 
-// Runs one validated, non-trivial call: prescan -> tiled (gated on the
-// flag) -> reference-semantics kernel (gated on the opposite).
+// Runs one validated, non-trivial call: prescan (+ route summary) -> [fast:
+// bound] -> the mode's tiled kernel (EC_FAST elements) -> [fast: TwoSum
+// fallback for EC_WIDE elements] -> [split-K reduce] -> reference-semantics
+// kernel for the EC_REF elements (exits at once when there are none).
 int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   int nl = 0;
   cudaError_t e;
@@ -102,17 +104,10 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
       g_last_route = 2;
       return DDB_OK;
     }
-    retain_pool_memory();
-    void* ws = nullptr;
-    e = cudaMallocAsync(&ws, 256, s);
-    if (e != cudaSuccess) return fail(e, "workspace allocation");
-    e = cudaMemsetAsync(ws, 0, 256, s);
     g.kchunk = g.k;
-    if (e == cudaSuccess) e = launch_tiled(g, ALG_F64, nullptr, nullptr, static_cast<int*>(ws), s, &nl);
+    e = launch_tiled(g, ALG_F64, nullptr, nullptr, nullptr, s, &nl);
     g_launches += nl;
-    cudaError_t e2 = cudaFreeAsync(ws, s);
     if (e != cudaSuccess) return fail(e, "f64 kernel launch");
-    if (e2 != cudaSuccess) return fail(e2, "workspace free");
     g_last_route = debug_sync() ? 4 : -1;
     return DDB_OK;
   }
@@ -128,9 +123,13 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
     return DDB_OK;
   }
   retain_pool_memory();
-  const int alg = alg_for_mode(mode);
+  int alg = alg_for_mode(mode);
+  // The certified bound's accumulation factor (1 + k 2^-21, below) keeps
+  // S' <= 1.11 sum |ab| up to k = 2^17; deeper calls take the TwoSum MAC,
+  // whose error bound holds at any depth.
+  if (alg == ALG_CERT && g.k > kCertMaxK) alg = ALG_TWOSUM;
   const int64_t nrow = g.m, ncol = g.n;
-  const size_t head = ((sizeof(int) * (size_t)(16 + nrow + ncol) + 255) / 256) * 256;
+  const size_t head = route_ws_bytes(nrow, ncol, g.syrk);
   int64_t kchunk = g.k;
   const int splits = choose_ksplit(g, alg, &kchunk);
   g.kchunk = kchunk;
@@ -140,33 +139,37 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   void* ws = nullptr;
   e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "workspace allocation");
-  int* flag = static_cast<int*>(ws);
-  int* row_exp = flag + 16;
-  int* col_exp = g.syrk ? row_exp : row_exp + nrow;
+  const RouteWs r = route_ws_carve(ws, nrow, ncol, g.syrk);
   const char* what = "dd kernel launch";
   e = cudaMemsetAsync(ws, 0, head, s);
-  if (e == cudaSuccess) e = launch_prescan(g, alg, row_exp, col_exp, flag, s, &nl);
+  if (e == cudaSuccess) e = launch_prescan(g, alg, r, s, &nl);
+  g.rsp = r.rsp; g.csp = r.csp; g.rsb = r.rsb; g.csb = r.csb; g.flag = r.flag;
+  g.bad_rows = r.bad_rows; g.bad_cols = r.bad_cols;
+  g.wide_lim = alg == ALG_CERT ? wide_limit(g.k) : 0;
   if (e == cudaSuccess && alg == ALG_CERT) {
     char* bw = static_cast<char*>(ws) + head;
-    const size_t conv = ((2 * (size_t)g.m * g.k + 255) / 256) * 256 +
-                        (g.syrk ? 0 : ((2 * (size_t)g.k * g.n + 255) / 256) * 256);
-    float* bound = reinterpret_cast<float*>(bw + conv);
+    float* bound = bound_carve(g, bw);
     g.bound = bound;
-    g.bnd_fac = 1.0 + (double)g.k * 0x1p-20;
+    g.bnd_fac = 1.0 + (double)g.k * 0x1p-21;
     g.bnd_floor = (double)g.k * 0x1p-120;
-    e = launch_bound(g, row_exp, col_exp, bw, bound, s, &nl, &what);
+    e = launch_bound(g, r.rmax, r.cmax, bw, bound, s, &nl, &what);
   }
   if (splits > 1) g.part = reinterpret_cast<double*>(static_cast<char*>(ws) + head + bnd_bytes);
-  if (e == cudaSuccess) e = launch_tiled(g, alg, row_exp, col_exp, flag, s, &nl);
-  if (e == cudaSuccess && splits > 1) e = launch_splitk_reduce(g, splits, flag, s, &nl);
-  if (e == cudaSuccess) e = launch_reference(g, flag, GATE_IF_UNSAFE, s, &nl);
+  if (e == cudaSuccess) e = launch_tiled(g, alg, r.rmax, r.cmax, r.flag, s, &nl);
+  if (e == cudaSuccess && alg == ALG_CERT) e = launch_wide_fallback(g, s, &nl);
+  if (e == cudaSuccess && splits > 1) e = launch_splitk_reduce(g, splits, r.flag, s, &nl);
+  if (e == cudaSuccess) e = launch_reference(g, r.flag, GATE_IF_UNSAFE, s, &nl);
   g_launches += nl;
   int route = -1;
   if (e == cudaSuccess && debug_sync()) {
-    int f = 0;
-    e = cudaMemcpyAsync(&f, flag, sizeof f, cudaMemcpyDeviceToHost, s);
+    // 0 exact, 1 fast, 3 twosum; 2 = some elements took the reference
+    // kernel, 5 = some took the TwoSum fallback (fast mode)
+    int f[3] = {0, 0, 0};
+    e = cudaMemcpyAsync(f, r.flag, sizeof f, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    route = f != ROUTE_SAFE ? 2 : (mode == MODE_EXACT ? 0 : (mode == MODE_FAST ? 1 : 3));
+    route = f[0] != ROUTE_SAFE ? 2
+            : (g.wide_lim > 0 && f[1] + f[2] > g.wide_lim) ? 5
+            : (mode == MODE_EXACT ? 0 : (alg == ALG_CERT ? 1 : 3));
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   if (e != cudaSuccess) return fail(e, what);

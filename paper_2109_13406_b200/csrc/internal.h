@@ -18,10 +18,33 @@ enum Alg { ALG_EXACT = 0, ALG_TWOSUM = 1, ALG_SELECT = 2, ALG_CERT = 3, ALG_F64 
 int alg_for_mode(int mode);
 
 // Route flag written by the prescan: 0 = every operand inside the safe
-// window (tiled kernels run), nonzero = some value outside it (non-finite,
-// |x| > 2**301, or a nonzero hi word below 2**-300): the tiled kernels exit
-// and the reference-semantics kernel runs instead.
+// window, nonzero = some value outside it (non-finite, |x| > 2**301, or a
+// nonzero hi word below 2**-300).  Routing is per element (dd_prescan.cu):
+// the prescan marks every op(A) row / op(B) column holding such a word, the
+// tiled kernels skip the elements in those rows / columns and the
+// reference-semantics kernel computes exactly those.
 enum RouteFlag { ROUTE_SAFE = 0, ROUTE_UNSAFE = 1 };
+
+// Per-element route classes (elem_class below).
+//   EC_FAST: the mode's tiled kernel (fast, exact or twosum);
+//   EC_WIDE: fast modes only, the element's row and column exponent spreads
+//            (max / min nonzero |hi|) are too wide for the certified bound to
+//            be tight (dd_bound.cu): the TwoSum accumulation computes it;
+//   EC_REF:  a word outside the safe window in its row or column: the
+//            reference-semantics kernel (dd_reference.cu) computes it.
+// Certified-anchor (fast) accumulation: deepest k it accepts, and the
+// spread limit for EC_WIDE (dd_bound.cu derives both): an element whose row
+// and column exponent spreads sum above 112 - ceil(log2 k) takes TwoSum.
+constexpr int64_t kCertMaxK = int64_t(1) << 17;
+inline int wide_limit(int64_t k) {
+  int lg = 0;
+  while ((int64_t(1) << lg) < k) ++lg;
+  return 112 - lg;
+}
+
+enum ElemClass { EC_FAST = 0, EC_WIDE = 1, EC_REF = 2 };
+constexpr int SPREAD_BAD = 1 << 20;      // spread value of a row / column holding an unsafe word
+constexpr int ROUTE_BLK = 32;            // rows / columns per block maximum (rsb / csb)
 
 // Safe window in biased-exponent terms (see dd_prescan.cu).
 constexpr int WIN_LO = 1023 - 300;   // hi words: zero or biased exp >= WIN_LO
@@ -55,24 +78,73 @@ struct GemmArgs {
   // ALG_SPLIT: sum_l a_lo b_hi + a_hi b_lo (m x n, ld = m), added into the
   // low word of the first k-slice's sum
   const double* cross;
+  // per-element routing (dd_prescan.cu, route_summary_kernel): exponent
+  // spread of op(A) row i / op(B) column j (SPREAD_BAD: holds an unsafe
+  // word), and their maxima over blocks of ROUTE_BLK rows / columns (unsafe
+  // rows excluded).  nullptr: no routing (every element EC_FAST).
+  const int *rsp, *csp, *rsb, *csb;
+  int wide_lim;     // fast modes: spread sum above which an element is EC_WIDE (0: never)
+  int only_wide;    // TwoSum fallback launch: compute / store EC_WIDE elements only
+  const int* flag;  // [0] any unsafe word, [1] max row spread, [2] max column spread,
+                    // [3] / [4] number of unsafe rows / columns (listed in bad_rows / bad_cols)
+  const int *bad_rows, *bad_cols;
 };
+
+__device__ __forceinline__ int elem_class(const GemmArgs& g, int64_t i, int64_t j) {
+  if (g.rsp == nullptr) return EC_FAST;
+  const int v = g.rsp[i] + g.csp[j];
+  if (v >= SPREAD_BAD) return EC_REF;
+  return (g.wide_lim > 0 && v > g.wide_lim) ? EC_WIDE : EC_FAST;
+}
+
+// The element class a kernel instance writes: the fallback launch writes the
+// EC_WIDE elements, every other launch the EC_FAST ones.
+__device__ __forceinline__ bool elem_mine(const GemmArgs& g, int64_t i, int64_t j) {
+  return elem_class(g, i, j) == (g.only_wide ? EC_WIDE : EC_FAST);
+}
+
+// Fallback launch: can the tile [i0, i0 + bm) x [j0, j0 + bn) hold an
+// EC_WIDE element?  Block maxima only (a superset test; stores re-check).
+__device__ __forceinline__ bool tile_maybe_wide(const GemmArgs& g, int64_t i0, int64_t j0,
+                                                int bm, int bn) {
+  if (g.flag[1] + g.flag[2] <= g.wide_lim) return false;    // no wide element in the call
+  int rm = 0, cm = 0;
+  const int64_t i1 = i0 + bm - 1 < g.m - 1 ? i0 + bm - 1 : g.m - 1;
+  const int64_t j1 = j0 + bn - 1 < g.n - 1 ? j0 + bn - 1 : g.n - 1;
+  const int64_t ib1 = i1 / ROUTE_BLK, jb1 = j1 / ROUTE_BLK;
+  for (int64_t b = i0 / ROUTE_BLK; b <= ib1; ++b) rm = max(rm, g.rsb[b]);
+  for (int64_t b = j0 / ROUTE_BLK; b <= jb1; ++b) cm = max(cm, g.csb[b]);
+  return rm + cm > g.wide_lim;
+}
 
 // Which kernel should run, decided on the device by the prescan flag.
 enum Gate { GATE_ALWAYS = 0, GATE_IF_SAFE = 1, GATE_IF_UNSAFE = 2 };
 
-cudaError_t launch_prescan(const GemmArgs& g, int alg, int* row_exp, int* col_exp,
-                           int* flag, cudaStream_t s, int* nlaunch);
+// Route workspace carved from one zeroed block (dd_prescan.cu)
+struct RouteWs {
+  int* flag;                    // 16 ints
+  int *rmax, *rneg, *cmax, *cneg;   // per op(A) row / op(B) column (Rsyrk: c* == r*)
+  int *rsp, *csp, *rsb, *csb;
+  int *bad_rows, *bad_cols;     // the unsafe rows / columns, flag[3] / flag[4] of them
+};
+size_t route_ws_bytes(int64_t m, int64_t n, int syrk);
+RouteWs route_ws_carve(void* base, int64_t m, int64_t n, int syrk);
+cudaError_t launch_prescan(const GemmArgs& g, int alg, const RouteWs& r, cudaStream_t s,
+                           int* nlaunch);
+cudaError_t launch_wide_fallback(const GemmArgs& g, cudaStream_t s, int* nlaunch);
 cudaError_t launch_reference(const GemmArgs& g, const int* flag, int gate, cudaStream_t s,
                              int* nlaunch);
 cudaError_t launch_tiled(const GemmArgs& g, int alg, const int* row_exp, const int* col_exp,
                          const int* flag, cudaStream_t s, int* nlaunch);
 size_t bound_workspace_bytes(const GemmArgs& g);
+float* bound_carve(const GemmArgs& g, void* ws);   // the fp32 bound inside the workspace
 int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk);
 cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag, cudaStream_t s,
                                  int* nlaunch);
 cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
                          float* bound, cudaStream_t s, int* nlaunch, const char** what);
 cudaError_t launch_cross_dgemm(const GemmArgs& g, double* x, cudaStream_t s);
+cudaError_t launch_cross_dmma(const GemmArgs& g, double* x, cudaStream_t s, int* nlaunch);
 
 // complex GEMM (dd_complex.cu)
 struct cdd { dd re, im; };

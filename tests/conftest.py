@@ -7,6 +7,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
 
+# the library reads DDB_DEBUG_SYNC once: GPU tests inspect ddb_last_route()
+os.environ.setdefault("DDB_DEBUG_SYNC", "1")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

@@ -53,7 +53,7 @@ def test_split_bound_on_adversarial_patterns(kind, k):
     alpha, beta = (1.5, 0.0), (0.5, 0.0)
     a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
     Rgemm("N", "N", m, n, k, alpha[0], a, m, b, k, beta[0], c, m, mode="fast")
-    assert _lib.last_route() == 1
+    assert _lib.last_route() in (1, 5)   # 5: some elements took the TwoSum fallback
     gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
     I, J = list(range(0, m, 7)), list(range(0, n, 5))
     vals, scales = exact.exact_entries("N", "N", k, alpha, A[0], A[1], m, B[0], B[1], k,
