@@ -57,7 +57,73 @@ def parse():
     p.add_argument("--quick", action="store_true", help="skip the secondary measurements")
     p.add_argument("--force-dist", action="store_true",
                    help="use the distributed (NCCL) path even with one rank (testing)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="TEST HOOK: launcher / ranks / timing / JSON plumbing only, on the CPU "
+                        "(gloo, a stand-in numpy step); never a measurement")
     return p.parse_args()
+
+
+# --------------------------------------------------------------------------
+# N > 1 without torchrun: re-launch this script with one rank per GPU
+
+def self_launch(args):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: re-exec under
+    torch.distributed.run with N local ranks on 127.0.0.1 and return its exit
+    code.  Refuses (exit 2) when fewer than N GPUs are visible, so a request
+    for N GPUs never reports n_gpus = 1."""
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but only {have} "
+                              "CUDA device(s) visible", "n_gpus": have}), flush=True)
+            return 2
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """TEST HOOK (--dry-run): the multi-rank plumbing of run_ours on the CPU --
+    gloo process group, barrier + max-over-ranks timing, rank 0's JSON line --
+    with a stand-in numpy step instead of the GPU kernels."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    if world > 1:
+        dist.init_process_group("gloo")
+    x = np.random.default_rng(rank).standard_normal((128, 128))
+    step = lambda: x @ x  # noqa: E731  (stand-in work, not a measurement)
+    for _ in range(args.warmup):
+        step()
+    if world > 1:
+        dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                          "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+                          "dry_run": True, "data": "stand-in CPU step (test hook)"}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # --------------------------------------------------------------------------
@@ -300,42 +366,53 @@ def run_ours(args):
 
     extra = {}
     if rank == 0:
-        # ---- roofline of the dominant kernel (tiled dd GEMM) ----
+        # ---- roofline: the FP64 pipe (DFMA + DMMA share it) ----
         peak = _lib.fp64_peak_probe()        # DFMA lane-ops/s * 2, measured live
         kernel_t = t if not distributed else t_local
-        achieved = 20.0 * n * n * k / kernel_t / 1e12 / (world if distributed else 1)
+        share = world if distributed else 1
+        macs = float(n) * n * k / share
         prof = _profile_traffic()
+        fp64 = _profile_fp64_step()
         split_on = mode == "fast" and os.environ.get("DDB_SPLIT", "1") != "0"
-        # FP64-pipe instructions per dd MAC: fast = 5 in the dd kernel + 2 in
-        # the cross-term GEMMs (split, default) or 7.5 in the dd kernel alone
-        ipm = 7.0 if split_on else {"fast": 7.5, "exact": 29, "twosum": 12.375}[mode]
         traffic = prof.get("dram_bytes_per_launch")
         try:
             with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
                 hbm_peak = float(json.load(f)["hbm_gbs"])
         except Exception:
             hbm_peak = None
+        lane_peak = peak / 2.0                   # FP64 FMA lane-ops per second
+        # the hardware fraction of the whole step: FP64-pipe lane operations
+        # issued per step (ncu: 32 x sm__inst_executed_pipe_fp64 + 256 x
+        # DMMA.8x8x4 instructions, summed over every launch of one step,
+        # profiles/r2_fp64_step.json) / step time / the pipe's lane rate
+        lane_ops = None
+        if fp64 and fp64.get("n") == n and fp64.get("mode") == mode and not distributed:
+            lane_ops = fp64["fp64_lane_ops_per_step"]
+        hw_frac = lane_ops / kernel_t / lane_peak if lane_ops else None
+        dd_conv = 20.0 * macs / kernel_t / 1e12          # the north star's convention
         extra["roofline"] = {
-            "bound": "fp64", "achieved": achieved, "peak": peak / 1e12, "unit": "TFLOP/s",
-            "frac": achieved * 1e12 / peak,
-            "traffic": prof.get("dram_bytes_per_launch"),
+            "bound": "fp64", "unit": "TFLOP/s",
+            "achieved": (2.0 * lane_ops / kernel_t / 1e12) if lane_ops else None,
+            "peak": peak / 1e12,
+            "frac": hw_frac,
+            "frac_source": ("ncu FP64-pipe lane ops per step (profiles/r2_fp64_step.json) / "
+                            "CUDA-event step time / live DFMA peak") if hw_frac else None,
+            "traffic": traffic,
+            "frac_dd_convention": dd_conv * 1e12 / peak,
+            "achieved_dd_convention": dd_conv,
             "convention": "20 fp64 flops per dd MAC (north star); peak = live DFMA probe",
+            "fp64_instr_per_mac_measured": (lane_ops / macs) if lane_ops else None,
+            "fp64_instr_split": ({"tma_kernel_hi_hi": 5.0, "cross_dmma": 2.0}
+                                 if split_on else None),
             "algorithmic_bytes": 16.0 * (2 * n * k + 2 * n * n),
-            "fp64_instr_per_mac": ipm,
-            # fast mode (default DDB_SPLIT): 5 per MAC in the dd TMA kernel
-            # (anchored hi*hi, fold every 3 steps) + 2 in the two binary64
-            # cross-term GEMMs
-            "fp64_instr_split": ({"tma_kernel": 5.0, "cross_dgemm": 2.0} if split_on else None),
-            # the hardware fraction: FP64 instructions actually issued per second
-            # over the pipe's lane rate (peak / 2, FMA = 2 flops); ncu's
-            # sm__pipe_fp64_cycles_active is the same quantity for the kernel alone
-            "fp64_pipe_frac": ipm * n * n * k / kernel_t / (world if distributed else 1)
-                              / (peak / 2.0),
             # achieved DRAM bandwidth of the dominant kernel (ncu bytes / step time)
             # against the measured copy bandwidth
             "hbm_gbs": (traffic / kernel_t / 1e9) if traffic and not distributed else None,
             "hbm_peak_gbs": hbm_peak,
         }
+        if not distributed:
+            # accuracy of the timed result (checker, outside the timed region)
+            extra["accuracy"] = _accuracy(n, k, A, B, C0, C, mode)
     if rank == 0 and not args.quick:
         # ---- e2e through the public API with pinned host buffers ----
         extra["e2e"] = _e2e(n, k, mode, distributed, world, rank, dev)
@@ -351,6 +428,7 @@ def run_ours(args):
             extra["rpotrf"] = _rpotrf(n, dev, stream, mode)
             extra["rgetrf"] = _rgetrf(n, dev, stream, mode)
             extra["rtrsm"] = _rtrsm(n, dev, stream, mode)
+        extra["config5"] = _config5(mode, dev, stream, distributed, world, rank)
         if not distributed:
             cpu_lp = cpu_lapack_rates()
             for key in ("rpotrf", "rgetrf", "rtrsm"):
@@ -365,6 +443,7 @@ def run_ours(args):
                                  "kind": "port", "sample": desc, "seconds": cpu_s}
     elif distributed and not args.quick:
         _e2e(n, k, mode, distributed, world, rank, dev)
+        _config5(mode, dev, stream, distributed, world, rank)
 
     if rank == 0:
         line = {
@@ -385,6 +464,58 @@ def run_ours(args):
     if distributed:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _profile_fp64_step():
+    """FP64-pipe lane operations of one step (every launch), from the ncu
+    capture committed under profiles/ (scripts/fp64_step.py)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "r2_fp64_step.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def _accuracy(n, k, A, B, C0, C, mode, rows=8, cols=8):
+    """Error of sampled entries of the timed result against exact rationals
+    (oracle/exact.py: the CHECKER, run after the timed region; 8 x 8 entries,
+    full k), with mpmath at 240 bits on two of them.  Returns the max of
+    |err| / (4 k 2^-104 (|alpha| sum|ab| + |beta| |c|)) and of |err| / |C|."""
+    import numpy as np
+    from oracle import exact
+    g = np.random.default_rng(12345)
+    I = sorted(g.choice(n, rows, replace=False).tolist())
+    J = sorted(g.choice(n, cols, replace=False).tolist())
+    ah = np.stack([A.store[0][i::n][:k].cpu().numpy() for i in I])
+    al = np.stack([A.store[1][i::n][:k].cpu().numpy() for i in I])
+    bh = np.stack([B.store[0][j * k:(j + 1) * k].cpu().numpy() for j in J])
+    bl = np.stack([B.store[1][j * k:(j + 1) * k].cpu().numpy() for j in J])
+    ch0 = np.array([[float(C0.store[0][i + j * n]) for j in J] for i in I])
+    cl0 = np.array([[float(C0.store[1][i + j * n]) for j in J] for i in I])
+    gh = np.array([[float(C.store[0][i + j * n]) for j in J] for i in I])
+    gl = np.array([[float(C.store[1][i + j * n]) for j in J] for i in I])
+    # the sampled sub-problem, rows I of op(A) (ld = rows) and columns J of op(B)
+    R, Q = len(I), len(J)
+    vals, scales = exact.exact_entries(
+        "N", "N", k, (ALPHA, 0.0), ah.T.reshape(-1), al.T.reshape(-1), R,
+        bh.reshape(-1), bl.reshape(-1), k, (BETA, 0.0), ch0.T.reshape(-1), cl0.T.reshape(-1), R,
+        list(range(R)), list(range(Q)))
+    ratio = exact.error_ratios(gh.T.reshape(-1), gl.T.reshape(-1), R, list(range(R)),
+                               list(range(Q)), vals, scales, k, c=4.0)
+    from fractions import Fraction
+    rel = 0.0
+    for x in range(R):
+        for y in range(Q):
+            v = vals[x][y]
+            err = abs(Fraction(gh[x, y]) + Fraction(gl[x, y]) - v)
+            if v != 0:
+                rel = max(rel, float(err / abs(v)))
+    mp = [float(exact.mp_check(vals[x][x], gh[x, x], gl[x, x])) for x in range(2)]
+    return {"entries": R * Q, "k": k, "mode": mode, "max_err_over_bound": ratio,
+            "bound": "4 k 2^-104 (|alpha| sum|a b| + |beta| |c|)",
+            "max_rel_err": rel, "rel_bound_k_2^-104": k * 2.0 ** -104,
+            "mpmath240_abs_err_first2": mp,
+            "checker": "oracle/exact.py (exact rationals; mpmath 240-bit cross-check)"}
 
 
 def _profile_traffic():
@@ -441,6 +572,60 @@ def _e2e(n, k, mode, distributed, world, rank, dev):
             "host_buffers": "pinned numpy planes, " + (
                 "parallel.rgemm_host_columns (staged on the root, then column-split)"
                 if distributed else "ddb_rgemm_host")}
+
+
+def _config5(mode, dev, stream, distributed, world, rank, n=32768):
+    """BASELINE configs[4]: Rgemm NN and Rsyrk U/N at n = k = 32768 (48 GiB /
+    32 GiB of operands), one timed call each (~15 s / ~8 s on one B200; the
+    kernels are already warm from the n = 8192 legs); at N > 1 through the
+    column-split NCCL path (A broadcast in k-panels, B / C slabs P2P)."""
+    import torch
+    from paper_2109_13406_b200 import DeviceMatrix, Rgemm, Rsyrk, flop_count
+    from paper_2109_13406_b200 import parallel
+    from paper_2109_13406_b200.synth import hashed_dd_device
+    out = {"workload": f"dd Rgemm NN and Rsyrk U/N at n=k={n}", "unit": UNIT, "mode": mode,
+           "n_gpus": world, "steps": 1}
+    mats = None
+    if rank == 0 or not distributed:
+        mats = [DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, t, dev))
+                for t in (1, 2, 3)]
+    A, B, C = mats if mats else (None,) * 3
+
+    def sync_time(fn):
+        if distributed:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3
+        if distributed:
+            import torch.distributed as dist
+            tt = torch.tensor([t], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    if distributed:
+        plan = parallel.RgemmPlan(n, n, n, world, rank, dev)
+        t = sync_time(lambda: parallel.rgemm_columns(plan, "N", "N", ALPHA, A, B, BETA, C,
+                                                     mode=mode))
+        del plan
+    else:
+        t = sync_time(lambda: Rgemm("N", "N", n, n, n, ALPHA, A, n, B, n, BETA, C, n, mode=mode))
+    out["rgemm"] = {"value": 2.0 * n ** 3 / t / 1e9, "ms": t * 1e3}
+    if distributed:
+        t = sync_time(lambda: parallel.rsyrk_columns(n, n, world, rank, dev, "U", "N", ALPHA, A,
+                                                     BETA, C, mode=mode))
+    else:
+        t = sync_time(lambda: Rsyrk("U", "N", n, n, ALPHA, A, n, BETA, C, n, mode=mode))
+    out["rsyrk"] = {"value": flop_count("Rsyrk", n, k=n) / t / 1e9, "ms": t * 1e3}
+    del A, B, C, mats
+    torch.cuda.empty_cache()
+    return out
 
 
 def _rsyrk(n, k, mode, dev, stream, steps):
@@ -638,6 +823,11 @@ def _modes(n, k, dev, stream, A, B, C, C0, mode):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+    if args.dry_run:
+        run_dry(args)
+        return
     if args.impl == "reference":
         run_reference_arm(args)
         return

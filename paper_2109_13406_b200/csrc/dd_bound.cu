@@ -37,8 +37,6 @@
 // written per element) plus ~0.8 ms of tensor-core time.
 #include <cuda_bf16.h>
 
-#include <cstdlib>
-
 #include "internal.h"
 #include "tma_util.cuh"
 
@@ -261,18 +259,9 @@ float* bound_carve(const GemmArgs& g, void* ws) {
                                   ((2 * a + 1023) / 1024 + (2 * b + 1023) / 1024) * 1024);
 }
 
-cudaError_t launch_bound_cublas(const GemmArgs& g, const int* row_exp, const int* col_exp,
-                                void* ws, float* bound, cudaStream_t s, int* nlaunch,
-                                const char** what);
-
 // Fills bound (m x n, ld = m, fp32) from the operands and the prescan maxima.
 cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
                          float* bound, cudaStream_t s, int* nlaunch, const char** what) {
-  {
-    const char* v = std::getenv("DDB_BOUND");   // measurement override: the library GEMM
-    if (v != nullptr && v[0] == 'c')
-      return launch_bound_cublas(g, row_exp, col_exp, ws, bound, s, nlaunch, what);
-  }
   const int64_t kp = kpad(g.k);
   __nv_bfloat16* abf = static_cast<__nv_bfloat16*>(ws);
   __nv_bfloat16* bbf =

@@ -6,7 +6,7 @@
 // one binary64 GEMM of depth 2k: every k-tile stages the four operand tiles
 // (A_lo, A_hi: 128 x 16, B_hi, B_lo: 16 x 128) with TMA (cp.async.bulk.tensor,
 // 128-byte swizzle) into a 3-stage ring guarded by transaction-counted
-// mbarriers, and 8 warps accumulate their 64 x 32 sub-tiles with
+// mbarriers (one producer warp), and 8 warps accumulate their 64 x 32 sub-tiles with
 // mma.sync.m16n8k4.f64 (DMMA): per k4 step a warp loads 8 + 4 fragment
 // doubles and issues 2 x 16 DMMA (each 512 multiply-adds).  DMMA shares the
 // FP64 pipe with DFMA (same 64 FMA / clk / SM), so the bound is the FP64
@@ -34,7 +34,12 @@ namespace cross {
 
 using namespace tma;
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, NT = 256;
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3;
+// 8 consumer warps (two warpgroups) + one producer warpgroup whose first
+// lane issues the TMA loads; setmaxnreg moves the producer's registers to
+// the consumers (40 / 232 per thread against 168 at launch)
+constexpr int NCW = 8, NT = 32 * (NCW + 4);
+constexpr int REG_CONSUMER = 232, REG_PRODUCER = 40;
 constexpr int WM = 64, WN = 32;                    // warp tile (2 x 4 warps)
 constexpr int MT = WM / 16, NTL = WN / 8;          // m16 / n8 tiles per warp
 constexpr uint32_t A_TILE = BM * BK * 8;           // 16 KB per plane
@@ -84,7 +89,7 @@ cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NT / 32);
+      mbar_init(&empty[s], NCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -92,26 +97,29 @@ cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant
   __syncthreads();
 
   const int ktiles = (int)((k + BK - 1) / BK);
-  int p_kt = 0;
-  auto produce = [&]() {   // thread 0: the next k-tile into its stage
-    if (p_kt >= ktiles) return;
-    const int s = p_kt % STAGES;
-    if (p_kt >= STAGES) mbar_wait(&empty[s], ((p_kt / STAGES) - 1) & 1);
-    unsigned char* st = ring_g + (size_t)s * STAGE_BYTES;
-    const int kc = p_kt * BK;
-    mbar_expect_tx(&full[s], STAGE_BYTES);
+  if (warp >= NCW) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_PRODUCER));
+    // ---- TMA producer: one lane walks the k-tiles ahead of the consumers ----
+    if (warp == NCW && lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+        unsigned char* st = ring_g + (size_t)s * STAGE_BYTES;
+        const int kc = kt * BK;
+        mbar_expect_tx(&full[s], STAGE_BYTES);
 #pragma unroll
-    for (int b = 0; b < BM / 16; ++b) {
-      tma_load_2d(st + b * 2048, &mAl, (int)i0 + 16 * b, kc, &full[s]);
-      tma_load_2d(st + A_TILE + b * 2048, &mAh, (int)i0 + 16 * b, kc, &full[s]);
+        for (int b = 0; b < BM / 16; ++b) {
+          tma_load_2d(st + b * 2048, &mAl, (int)i0 + 16 * b, kc, &full[s]);
+          tma_load_2d(st + A_TILE + b * 2048, &mAh, (int)i0 + 16 * b, kc, &full[s]);
+        }
+        tma_load_2d(st + 2 * A_TILE, &mBh, kc, (int)j0, &full[s]);
+        tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, kc, (int)j0, &full[s]);
+      }
     }
-    tma_load_2d(st + 2 * A_TILE, &mBh, kc, (int)j0, &full[s]);
-    tma_load_2d(st + 2 * A_TILE + B_TILE, &mBl, kc, (int)j0, &full[s]);
-    ++p_kt;
-  };
-  if (tid == 0)
-    for (int i = 0; i < STAGES - 1; ++i) produce();
+    return;
+  }
 
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_CONSUMER));
   const int wm = warp & 1, wn = warp >> 1;
   const int g = lane >> 2, tig = lane & 3;
   double acc[MT][NTL][4];
@@ -128,7 +136,6 @@ cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant
 
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % STAGES;
-    if (tid == 0) produce();
     mbar_wait(&full[s], (kt / STAGES) & 1);
     const uint32_t st = ring + (uint32_t)s * STAGE_BYTES;
 #pragma unroll

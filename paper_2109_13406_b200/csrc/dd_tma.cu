@@ -485,12 +485,9 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
   GemmArgs ga = g;
   if (split_alg) {
-    // the cross terms first: hand-written DMMA kernel (dd_cross.cu), or the
-    // library DGEMMs for an A/B measurement (DDB_CROSS=cublas)
+    // the cross terms first: hand-written DMMA kernel (dd_cross.cu)
     int nl = 0;
-    const char* v = std::getenv("DDB_CROSS");
-    cudaError_t e = (v != nullptr && v[0] == 'c') ? launch_cross_dgemm(g, xbuf, s)
-                                                  : launch_cross_dmma(g, xbuf, s, &nl);
+    cudaError_t e = launch_cross_dmma(g, xbuf, s, &nl);
     if (e != cudaSuccess) { cudaFreeAsync(xbuf, s); return e; }
     ga.cross = xbuf;
   }
