@@ -55,7 +55,15 @@ using tiled::dbits;
 
 constexpr int kTmaUnroll = DDB_TMA_UNROLL;
 constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
-constexpr int NT = 256;       // 8 warps; thread 0 doubles as the TMA producer
+constexpr int NT = 256;       // 8 consumer warps
+#ifndef DDB_TMA_WS
+#define DDB_TMA_WS 1          // 1: a separate producer warpgroup issues the TMA loads
+#endif
+// DDB_TMA_WS = 1: warps 8..11 form a producer warpgroup (one lane issues every
+// TMA load; setmaxnreg hands its registers to the consumers, 24 / 240 per
+// thread); 0: thread 0 of consumer warp 0 doubles as the producer
+constexpr int NTK = NT + (DDB_TMA_WS ? 128 : 0);
+constexpr int REG_CONSUMER = 240, REG_PRODUCER = 24;
 constexpr int TM = 8, TN = 4, RX = 32, RY = 32;
 constexpr int A_PLANE = BK * BM, B_PLANE = BN * BK;          // doubles
 constexpr int STAGE_DOUBLES = 2 * A_PLANE + 2 * B_PLANE;     // 6144 doubles = 48 KB
@@ -97,7 +105,7 @@ static_assert(96 % SPLIT_BK == 0 || SPLIT_BK == 32, "chunk rounding");
 // k-slices are read from DRAM once and shared through L2); the producer runs
 // ahead across unit boundaries, overlapping the epilogue with the next loads.
 template <int ALG, int SYRK>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NTK, 1)
 dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                  const __grid_constant__ CUtensorMap mAl, const __grid_constant__ CUtensorMap mBh,
                  const __grid_constant__ CUtensorMap mBl, const int* __restrict__ row_exp,
@@ -165,7 +173,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
   int p_unit = next_unit(blockIdx.x), p_kt = 0, p_ktiles = 0;
   int64_t p_i0 = 0, p_j0 = 0, p_kbeg = 0;
   uint32_t p_item = 0;
-  if (tid == 0 && p_unit < units) unit_origin(p_unit, p_i0, p_j0, p_kbeg, p_ktiles);
+  if (tid == (DDB_TMA_WS ? NT : 0) && p_unit < units) unit_origin(p_unit, p_i0, p_j0, p_kbeg, p_ktiles);
   auto produce_next = [&]() {   // issue the next item if any; false when exhausted
     if (p_unit >= units) return false;
     const int s = p_item % STAGES;
@@ -191,8 +199,17 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     }
     return true;
   };
-  if (tid == 0)
+  if (DDB_TMA_WS) {
+    if (tid >= NT) {   // producer warpgroup
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_PRODUCER));
+      if (tid == NT)
+        while (produce_next()) {}
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(REG_CONSUMER));
+  } else if (tid == 0) {
     for (int i = 0; i < STAGES - 1; ++i) produce_next();
+  }
 
   const int tx = tid % 16, ty = tid / 16;
   uint32_t c_item = 0;
@@ -226,7 +243,7 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 
     for (int kt = 0; kt < ktiles; ++kt, ++c_item) {
       const int s = c_item % STAGES;
-      if (tid == 0) produce_next();
+      if (!DDB_TMA_WS && tid == 0) produce_next();
       mbar_wait(&full[s], (c_item / STAGES) & 1);
       const double* a_h = ring + s * STAGE_DOUBLES;
       const double* a_l = a_h + A_PLANE;
@@ -513,7 +530,7 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // speed but more DRAM reads (its CTAs drift apart in k across units).
   const int grid = std::getenv("DDB_TMA_PERSISTENT") ? (int)(units < sms ? units : sms)
                                                      : (int)units;
-  kern<<<grid, NT, SMEM_BYTES, s>>>(ga, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
+  kern<<<grid, NTK, SMEM_BYTES, s>>>(ga, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
                                     tiles_n, splits);
   e = cudaGetLastError();
   if (xbuf != nullptr) {

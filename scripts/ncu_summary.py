@@ -14,6 +14,10 @@ KEYS = [
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active (% of peak)"),
     ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 inst executed (% of peak)"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active",
+     "DMMA (FP64 tensor subpipe) inst executed (% of peak)"),
+    ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active (% of elapsed)"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active (%)"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active (% of 64)"),
     ("launch__registers_per_thread", "registers / thread"),

@@ -208,3 +208,29 @@ def test_hashed_operands_device_equals_host():
     jj = np.arange(100 * 50) // 100
     eh, el = hashed_entries(5, 2, ii, jj)
     assert bits_equal(h.cpu().numpy(), eh) and bits_equal(l.cpu().numpy(), el)
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast", "twosum"])
+def test_mpmath_240bit_cross_check_config1_and_deep_k(mode):
+    """The mpmath 240-bit oracle (oracle/exact.py mp_check), as the reference's
+    acceptance test does (test_acceptance.py:361-415): for sampled entries of
+    configs[0] (256^3) and of a deep-k call, the 240-bit error of the GPU
+    result agrees with the exact-rational error and is inside the dd bound
+    (c = 4; exact mode is bitwise the reference's, whose own error is far
+    inside it)."""
+    from fractions import Fraction
+    for (m, n, k, seed) in ((256, 256, 256, 0), (64, 64, 20000, 9)):
+        A, B, C = random_dd(m, k, m, seed, 1), random_dd(k, n, k, seed, 2), random_dd(m, n, m, seed, 3)
+        c = dev(m, n, C)
+        Rgemm("N", "N", m, n, k, 1.5, dev(m, k, A), m, dev(k, n, B), k, 0.5, c, m, mode=mode)
+        gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+        I, J = [0, 7, m - 1], [1, 33, n - 1]
+        vals, scales = exact.exact_entries("N", "N", k, ALPHA, A[0], A[1], m, B[0], B[1], k,
+                                           BETA, C[0], C[1], m, I, J)
+        for x, i in enumerate(I):
+            for y, j in enumerate(J):
+                h, l = float(gh[i + j * m]), float(gl[i + j * m])
+                mp_err = float(exact.mp_check(vals[x][y], h, l))
+                fr_err = float(abs(Fraction(h) + Fraction(l) - vals[x][y]))
+                assert abs(mp_err - fr_err) <= 1e-60 * max(1.0, abs(float(vals[x][y])))
+                assert mp_err <= 4 * k * 2.0 ** -104 * scales[x][y]

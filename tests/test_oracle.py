@@ -251,3 +251,23 @@ def test_oracle_lapack_f64_matches_reference_bitwise(idx):
             assert oracle.dgetrs(case["trans"], case["n"], case["nrhs"], a, case["lda"], ipiv,
                                  got, case["ldb"]) == 0
     assert bits_equal(got, out_hi), case
+
+
+def test_oracle_reproduces_the_reference_pins():
+    """The C oracle against the pins generated by running the reference
+    (oracle/gen_pins.py): integer instance, Hilbert n = 2 product, and the
+    thread-count-invariance operands."""
+    import os
+    pins = np.load(os.path.join(os.path.dirname(__file__), "golden", "pins.npz"))
+    for pre, (m, n, k, al, be) in {"int": (3, 3, 3, 3.0, -2.0), "tc": (8, 8, 8, 0.75, -0.5)}.items():
+        ch, cl = pins[pre + "_c_hi"].copy(), pins[pre + "_c_lo"].copy()
+        assert oracle.rgemm("N", "N", m, n, k, (al, 0.0), pins[pre + "_a_hi"], pins[pre + "_a_lo"],
+                            m, pins[pre + "_b_hi"], pins[pre + "_b_lo"], k, (be, 0.0), ch, cl,
+                            m) == 0
+        assert np.array_equal(ch.view(np.uint64), pins[pre + "_out_hi"].view(np.uint64))
+        assert np.array_equal(cl.view(np.uint64), pins[pre + "_out_lo"].view(np.uint64))
+    ch, cl = np.zeros(4), np.zeros(4)
+    assert oracle.rgemm("N", "N", 2, 2, 2, (1.0, 0.0), pins["hil_inv_hi"], pins["hil_inv_lo"], 2,
+                        pins["hil_a_hi"], pins["hil_a_lo"], 2, (0.0, 0.0), ch, cl, 2) == 0
+    assert np.array_equal(ch.view(np.uint64), pins["hil_prod_hi"].view(np.uint64))
+    assert np.array_equal(cl.view(np.uint64), pins["hil_prod_lo"].view(np.uint64))
