@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DDB_VERSION 120   /* 1.2: LAPACK consumers (dd + f64), multi-GPU C entry points */
+#define DDB_VERSION 130   /* 1.3: per-element routing, no library GEMMs, diagnostics */
 
 #define DDB_OK 0
 #define DDB_EINVAL (-1)   /* bad mode / internal argument */
@@ -43,9 +43,21 @@ extern "C" {
 #define DDB_ENOMEM (-3)   /* device allocation failed */
 
 /* mode: DDB_MODE_EXACT     bit-identical to the reference (29 FP64 instr / MAC)
- *       DDB_MODE_FAST      certified-anchor accumulation (7.5 FP64 instr / MAC
- *                          + a bf16 tensor-core bound GEMM), error
- *                          <= c*k*2^-104*sum|a*b| (c = 4) for every input
+ *       DDB_MODE_FAST      certified-anchor accumulation: hi*hi in the
+ *                          hand-written DFMA kernel (5 FP64 instr / MAC) + the
+ *                          cross terms A_lo*B_hi + A_hi*B_lo on a hand-written
+ *                          DMMA kernel (2 / MAC) + a bf16 tcgen05 bound GEMM
+ *                          (k >= 1024; shallower calls: 7.5 / MAC in one
+ *                          kernel).  Error <= c*k*2^-104*(|alpha| sum|a*b| +
+ *                          |beta||c|), c = 4, for every input in the safe
+ *                          window: elements whose row / column exponent
+ *                          spreads exceed 112 - ceil(log2 k) and calls with
+ *                          k > 2^17 take the TwoSum accumulation instead,
+ *                          elements whose op(A) row / op(B) column holds a
+ *                          value outside the window (inf, nan, |x| >= 2^301,
+ *                          0 < |hi| < 2^-300, non-normalised dd) take the
+ *                          reference-semantics kernel (bit-exact there).
+ *                          Not bitwise equal to the reference elsewhere.
  *       DDB_MODE_REFERENCE one thread per element, checked arithmetic (debug)
  *       DDB_MODE_TWOSUM    TwoSum dd accumulation, same bound, no bound GEMM
  *                          (12.4 FP64 instr / MAC) */

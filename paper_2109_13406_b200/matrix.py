@@ -230,6 +230,15 @@ class DeviceMatrix:
         return DeviceMatrix(self.m, self.n, self.precision, self.ld,
                             store=tuple(p.clone() for p in self.store))
 
+    def packed(self):
+        """This matrix with a tight leading dimension (ld = max(1, m)): self
+        when it already is, else a packed copy of the m x n values."""
+        if self.ld == max(1, self.m):
+            return self
+        store = tuple(p[:self.ld * self.n].view(self.n, self.ld)[:, :self.m].contiguous().view(-1)
+                      if self.n else p[:0].clone() for p in self.store)
+        return DeviceMatrix(self.m, self.n, self.precision, max(1, self.m), store=store)
+
     def __repr__(self):
         return (f"DeviceMatrix({self.m}x{self.n}, ld={self.ld}, precision={self.precision!r}, "
                 f"device={self.device})")

@@ -13,9 +13,19 @@ plus one keyword, ``mode``:
   "fast"   (default; env ``DDBLAS_MODE`` overrides) certified-anchor dd
            accumulation on the FP64 pipe, componentwise error
            <= c*k*2**-104*(|alpha| sum|a*b| + |beta||c|), c = 4 -- the
-           north-star tolerance -- for every input
+           north-star tolerance -- for every input: elements whose row /
+           column exponent spreads are too wide for the certified bound
+           (and calls with k > 2**17) take the TwoSum accumulation, elements
+           whose op(A) row / op(B) column holds an inf / nan / out-of-window
+           value take the reference-semantics kernel.  Not bitwise equal to
+           the reference: of the reference's own pins it keeps the integer
+           instance (test_acceptance.py:121-139) but not the Hilbert n = 2
+           residual of exactly (2**-106, 0) (test_acceptance.py:298-305),
+           which it meets only to the dd bound (tests/test_gpu_pins.py)
   "twosum" the same bound with TwoSum accumulation (no bound GEMM; slower)
-  "exact"  bit-identical to the reference's result
+  "exact"  bit-identical to the reference's result (every reference pin);
+           the mode to select (``mode="exact"`` or DDBLAS_MODE=exact) when a
+           drop-in must reproduce the reference bit for bit
   "reference"  the one-thread-per-element checked kernel (debugging)
 
 C is updated in place; A and B are read only; nothing is returned.
@@ -99,7 +109,7 @@ class _HostPlanes:
         return self.planes[i].ctypes.data
 
     def commit(self):
-        for dst, src in zip(self.src[:2], self.planes):
+        for dst, src in zip(self.src[:len(self.planes)], self.planes):
             if dst is not src:
                 dst[...] = src
 

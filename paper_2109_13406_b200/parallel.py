@@ -124,10 +124,11 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
                   compute=None, kchunks=None):
     """C <- alpha op(A) op(B) + beta C with C split by column blocks over ranks.
 
-    On the root, ``a``/``b``/``c`` are the full operands (leading dimensions
-    tight: lda = rows); on the other ranks they are ignored (None).  Returns
-    nothing; on the root C holds the result (bitwise equal to ``Rgemm`` in
-    exact mode).
+    On the root, ``a``/``b``/``c`` are the full operands; padded leading
+    dimensions are packed first (C's result is copied back into the padded
+    storage, its padding untouched); on the other ranks they are ignored
+    (None).  Returns nothing; on the root C holds the result (bitwise equal
+    to ``Rgemm`` in exact mode).
 
     The k dimension is streamed in ``kchunks`` panels: panel c+1 of op(A)
     (broadcast) and of each rank's op(B) columns (point-to-point) is in
@@ -155,6 +156,12 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
     panels = _k_chunks(k, kchunks)
     j0, j1 = plan.blocks[rank]
     nb = j1 - j0
+    c_user = None
+    if rank == 0:
+        # the slabs below assume tight leading dimensions: pack padded operands
+        a, b = a.packed(), b.packed()
+        if c.ld != max(1, m):
+            c_user, c = c, c.packed()
 
     # 1. C column slabs to their owners (only read when beta != 0)
     sends, recvs = [], []
@@ -261,6 +268,9 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
     elif nb:
         sends += [ops.send(c_loc[0], 0, group), ops.send(c_loc[1], 0, group)]
     ops.exchange(sends + recvs)
+    if c_user is not None:   # back into the caller's padded storage
+        for dst, src in zip(c_user.store, c.store):
+            dst[:c_user.ld * n].view(n, c_user.ld)[:, :m].copy_(src[:m * n].view(n, m))
 
 
 def rsyrk_columns(n, k, world, rank, device, uplo, trans, alpha, a, beta, c, mode=None,
@@ -285,6 +295,11 @@ def rsyrk_columns(n, k, world, rank, device, uplo, trans, alpha, a, beta, c, mod
                           torch.empty(numel, dtype=torch.float64, device=device))
         return bufs[name]
 
+    c_user = None
+    if rank == 0:   # the slabs below assume tight leading dimensions
+        a = a.packed()
+        if c.ld != max(1, n):
+            c_user, c = c, c.packed()
     a_store = (a.store[0][:lda * nca], a.store[1][:lda * nca]) if rank == 0 else buf("A", lda * nca)
     ops.bcast(a_store[0])
     ops.bcast(a_store[1])
@@ -336,6 +351,9 @@ def rsyrk_columns(n, k, world, rank, device, uplo, trans, alpha, a, beta, c, mod
     elif nb:
         sends += [ops.send(c_loc[0], 0, group), ops.send(c_loc[1], 0, group)]
     ops.exchange(sends + recvs)
+    if c_user is not None:   # back into the caller's padded storage
+        for dst, src in zip(c_user.store, c.store):
+            dst[:c_user.ld * n].view(n, c_user.ld)[:, :n].copy_(src[:n * n].view(n, n))
 
 
 def rgemm_host_columns(transa, transb, m, n, k, alpha, a, b, beta, c, world, rank, device,

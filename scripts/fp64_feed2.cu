@@ -1,0 +1,174 @@
+// fp64_feed2.cu -- microbenchmark: the split kernel's MAC mix (8 x 4 micro-
+// tile, 256 threads, 1 CTA / SM) fed from shared memory with different load
+// schedules, against the register-only ceiling (fp64_warps.cu: 99.4 %).
+//   V 0: pair-buffered (the kernel's schedule: both steps' operands loaded,
+//        the next pair's loads hoisted by the compiler)      -> ~246 registers
+//   V 1: per step: A 4 x LDS.128 + B 4 x LDS.64 right before the step
+//   V 2: per pair, B k-pairs (4 x LDS.128) once, A per step (4 x LDS.128)
+//   V 3: as V 2, with __launch_bounds__(256, 1) and a register cap of 200
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_feed2 fp64_feed2.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int TM = 8, TN = 4, KB = 24, BM = 128, BN = 64;
+
+__device__ __forceinline__ void step(double (&T)[TM][TN], double (&L)[TM][TN], const double (&a)[TM],
+                                     const double (&b)[TN]) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const double t = T[i][j];
+      const double tn = __fma_rn(a[i], b[j], t);
+      L[i][j] = __dadd_rn(L[i][j], __fma_rn(a[i], b[j], __dsub_rn(t, tn)));
+      T[i][j] = tn;
+    }
+}
+__device__ __forceinline__ void fold(double (&T)[TM][TN], double (&L)[TM][TN]) {
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const double t2 = __dadd_rn(T[i][j], L[i][j]);
+      L[i][j] = __dsub_rn(L[i][j], __dsub_rn(t2, T[i][j]));
+      T[i][j] = t2;
+    }
+}
+
+template <int V>
+__global__ void __launch_bounds__(256, 1) feed(double* out, int iters) {
+  extern __shared__ __align__(16) double sm[];   // A [KB][BM] | B [BN][KB]
+  double* sa = sm;
+  double* sb = sm + KB * BM;
+  for (int i = threadIdx.x; i < KB * (BM + BN); i += 256) sm[i] = 1.0 + (i & 127) * 1e-9;
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double T[TM][TN], L[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) { T[i][j] = 1.5; L[i][j] = 0.0; }
+  auto lda = [&](int k, double (&a)[TM]) {
+#pragma unroll
+    for (int g = 0; g < TM / 2; ++g) {
+      const double2 h = *reinterpret_cast<const double2*>(sa + k * BM + g * 32 + tx * 2);
+      a[2 * g] = h.x;
+      a[2 * g + 1] = h.y;
+    }
+  };
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 2
+    for (int kk = 0; kk < KB; kk += 6) {
+#pragma unroll
+      for (int pq = 0; pq < 6; pq += 2) {
+        const int k = kk + pq;
+        if (V == 0) {
+          double a0[TM], a1[TM], b0[TN], b1[TN];
+          lda(k, a0);
+          lda(k + 1, a1);
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            const int cj = (j >> 1) * 32 + ty * 2 + (j & 1);
+            const double2 h = *reinterpret_cast<const double2*>(sb + cj * KB + k);
+            b0[j] = h.x;
+            b1[j] = h.y;
+          }
+          step(T, L, a0, b0);
+          if ((pq + 1) % 3 == 0) fold(T, L);
+          step(T, L, a1, b1);
+          if ((pq + 2) % 3 == 0) fold(T, L);
+        } else if (V == 1) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double a[TM], b[TN];
+            lda(k + q, a);
+#pragma unroll
+            for (int j = 0; j < TN; ++j) b[j] = sb[((j >> 1) * 32 + ty * 2 + (j & 1)) * KB + k + q];
+            step(T, L, a, b);
+            if ((pq + q + 1) % 3 == 0) fold(T, L);
+          }
+        } else {
+          double b0[TN], b1[TN];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) {
+            const int cj = (j >> 1) * 32 + ty * 2 + (j & 1);
+            const double2 h = *reinterpret_cast<const double2*>(sb + cj * KB + k);
+            b0[j] = h.x;
+            b1[j] = h.y;
+          }
+          double a[TM];
+          lda(k, a);
+          step(T, L, a, b0);
+          if ((pq + 1) % 3 == 0) fold(T, L);
+          lda(k + 1, a);
+          step(T, L, a, b1);
+          if ((pq + 2) % 3 == 0) fold(T, L);
+        }
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) s += T[i][j] + L[i][j];
+  if (s == 12345.0) out[0] = s;
+}
+
+__global__ void burn(double* out, int iters) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = __fma_rn(x[i], 0.999999, 1e-9);
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 12345.0) out[0] = s;
+}
+
+template <class K>
+float timeit(K launch) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 4; ++r) {
+    cudaEventRecord(e0);
+    launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (r && ms < best) best = ms;
+  }
+  return best;
+}
+
+template <int V>
+void one(int sms, double* out, double peak) {
+  const size_t smem = sizeof(double) * KB * (BM + BN);
+  cudaFuncSetAttribute(feed<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int its = 500;
+  const float ms = timeit([&] { feed<V><<<sms, 256, smem>>>(out, its); });
+  // per KB steps and element: 4 FP64 per step + 3 per fold (KB / 3 folds)
+  const double lane = (double)sms * 256 * its * TM * TN * (KB * 4.0 + KB / 3 * 3.0);
+  printf("V %d: %.1f %% of the pipe (%s)\n", V, 100.0 * lane / (ms * 1e-3) / peak,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  double* out;
+  cudaMalloc(&out, 8);
+  const int it = 20000;
+  const float ref = timeit([&] { burn<<<sms * 4, 256>>>(out, it); });
+  const double peak = (double)sms * 4 * 256 * it * 8 / (ref * 1e-3);
+  printf("burn: %.3f T lane-op/s\n", peak / 1e12);
+  one<0>(sms, out, peak);
+  one<1>(sms, out, peak);
+  one<2>(sms, out, peak);
+  return 0;
+}

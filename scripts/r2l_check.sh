@@ -1,0 +1,28 @@
+set -u
+mkdir -p gpurun_out
+cat > /tmp/syrk16.py <<'PY'
+import sys, torch
+sys.path.insert(0, ".")
+from paper_2109_13406_b200 import DeviceMatrix, Rsyrk, Rgemm, flop_count
+from paper_2109_13406_b200.synth import hashed_dd_device
+n = int(sys.argv[1]); what = sys.argv[2]
+A = DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, 1, "cuda"))
+C = DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, 3, "cuda"))
+B = DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, 2, "cuda")) if what == "gemm" else None
+for it in range(2):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    if what == "gemm":
+        Rgemm("N", "N", n, n, n, 1.5, A, n, B, n, 0.5, C, n)
+        f = 2.0 * n ** 3
+    else:
+        Rsyrk("U", "N", n, n, 1.5, A, n, 0.5, C, n)
+        f = flop_count("Rsyrk", n, k=n)
+    e1.record(); torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3
+    print(what, n, f"{t*1e3:.1f} ms {f/t/1e9:.1f} dd GFlops")
+PY
+python /tmp/syrk16.py 16384 syrk && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2l_syrk16.csv python /tmp/syrk16.py 16384 syrk > /dev/null 2>&1
+python /tmp/syrk16.py 16384 gemm
+python /tmp/syrk16.py 8192 syrk

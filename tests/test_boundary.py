@@ -181,7 +181,7 @@ def test_library_exports_every_header_symbol():
                          text=True).stdout
     for name in declared:
         assert re.search(rf"\bT {name}$", out, re.M), name
-    assert _lib.load().ddb_version() == 120
+    assert _lib.load().ddb_version() == 130
 
 
 POTRF_BAD = [(("X", 2), {}, 1), (("UU", 2), {}, 1), ((3, 2), {}, 1), (("U", -1), {}, 2),

@@ -48,9 +48,10 @@ def _free_port():
     return p
 
 
-def _cpu_mat(rows, cols, seed, tag):
-    hi, lo = random_dd(rows, cols, rows, seed, tag)
-    return DeviceMatrix(rows, cols, "dd", max(1, rows),
+def _cpu_mat(rows, cols, seed, tag, pad=0):
+    ld = max(1, rows) + pad
+    hi, lo = random_dd(rows, cols, ld, seed, tag)
+    return DeviceMatrix(rows, cols, "dd", ld,
                         store=(torch.from_numpy(hi.copy()), torch.from_numpy(lo.copy())))
 
 
@@ -58,12 +59,14 @@ def _worker(rank, world, port, case, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        if case[0] == "gemm":
+        if case[0] in ("gemm", "gemm_pad"):
+            pad = 3 if case[0] == "gemm_pad" else 0
             _, ta, tb, m, n, k, beta, kchunks, mode = (case + (None, None))[:9]
             nra, nca = (m, k) if ta == "N" else (k, m)
             nrb, ncb = (k, n) if tb == "N" else (n, k)
             if rank == 0:
-                A, B, C = _cpu_mat(nra, nca, 3, 1), _cpu_mat(nrb, ncb, 3, 2), _cpu_mat(m, n, 3, 3)
+                A, B, C = (_cpu_mat(nra, nca, 3, 1, pad), _cpu_mat(nrb, ncb, 3, 2, pad),
+                           _cpu_mat(m, n, 3, 3, pad))
             else:
                 A = B = C = None
             plan = parallel.RgemmPlan(m, n, k, world, rank, torch.device("cpu"))
@@ -90,10 +93,11 @@ def _worker(rank, world, port, case, q):
             if rank == 0:
                 q.put((np.array(c.store[0]), np.array(c.store[1])))
         else:
-            _, up, tr, n, k = case
+            _, up, tr, n, k = case[:5]
+            pad = case[5] if len(case) > 5 else 0
             nra, nca = (n, k) if tr == "N" else (k, n)
             if rank == 0:
-                A, C = _cpu_mat(nra, nca, 4, 1), _cpu_mat(n, n, 4, 3)
+                A, C = _cpu_mat(nra, nca, 4, 1, pad), _cpu_mat(n, n, 4, 3, pad)
             else:
                 A = C = None
             parallel.rsyrk_columns(n, k, world, rank, torch.device("cpu"), up, tr, 1.5, A, 0.5, C,
@@ -161,6 +165,34 @@ def test_rgemm_columns_k_panels_bitwise(ta, tb, beta, mode):
     ch, cl = (x.copy() for x in random_dd(m, n, m, 3, 3))
     oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra, B[0], B[1], nrb, to_dd(beta),
                  ch, cl, m)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("T", "T")])
+def test_rgemm_columns_padded_leading_dimensions(ta, tb):
+    """lda / ldb / ldc = rows + 3 on the root: the operands are packed for the
+    slabs and C comes back into its padded storage, padding untouched --
+    bitwise the single-process result on the same padded layout."""
+    m, n, k = 70, 150, 33
+    got = _run(("gemm_pad", ta, tb, m, n, k, 0.5))
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A = random_dd(nra, nca, nra + 3, 3, 1)
+    B = random_dd(nrb, ncb, nrb + 3, 3, 2)
+    ch, cl = (x.copy() for x in random_dd(m, n, m + 3, 3, 3))
+    oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra + 3, B[0], B[1], nrb + 3,
+                 (0.5, 0.0), ch, cl, m + 3)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+@pytest.mark.parametrize("up,tr", [("U", "N"), ("L", "T")])
+def test_rsyrk_columns_padded_leading_dimensions(up, tr):
+    n, k = 120, 17
+    got = _run(("syrk", up, tr, n, k, 2))
+    nra, nca = (n, k) if tr == "N" else (k, n)
+    A = random_dd(nra, nca, nra + 2, 4, 1)
+    ch, cl = (x.copy() for x in random_dd(n, n, n + 2, 4, 3))
+    oracle.rsyrk(up, tr, n, k, (1.5, 0.0), A[0], A[1], nra + 2, (0.5, 0.0), ch, cl, n + 2)
     assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
 
 
