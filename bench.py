@@ -576,15 +576,15 @@ def _e2e(n, k, mode, distributed, world, rank, dev):
 
 def _config5(mode, dev, stream, distributed, world, rank, n=32768):
     """BASELINE configs[4]: Rgemm NN and Rsyrk U/N at n = k = 32768 (48 GiB /
-    32 GiB of operands), one timed call each (~15 s / ~8 s on one B200; the
-    kernels are already warm from the n = 8192 legs); at N > 1 through the
+    32 GiB of operands), one warm-up and one timed call each (~15 s / ~8 s on
+    one B200); at N > 1 through the
     column-split NCCL path (A broadcast in k-panels, B / C slabs P2P)."""
     import torch
     from paper_2109_13406_b200 import DeviceMatrix, Rgemm, Rsyrk, flop_count
     from paper_2109_13406_b200 import parallel
     from paper_2109_13406_b200.synth import hashed_dd_device
     out = {"workload": f"dd Rgemm NN and Rsyrk U/N at n=k={n}", "unit": UNIT, "mode": mode,
-           "n_gpus": world, "steps": 1}
+           "n_gpus": world, "steps": 1, "warmup": 1}
     mats = None
     if rank == 0 or not distributed:
         mats = [DeviceMatrix(n, n, "dd", n, store=hashed_dd_device(n, n, 0, t, dev))
@@ -592,6 +592,7 @@ def _config5(mode, dev, stream, distributed, world, rank, n=32768):
     A, B, C = mats if mats else (None,) * 3
 
     def sync_time(fn):
+        fn()   # one warm-up call: the first call at a new size grows the workspace pools
         if distributed:
             import torch.distributed as dist
             dist.barrier()
