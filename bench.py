@@ -529,19 +529,58 @@ def _profile_traffic():
         return {}
 
 
+def _shm_room(nbytes):
+    try:
+        st = os.statvfs("/dev/shm")
+        return st.f_bavail * st.f_frsize > nbytes * 1.1
+    except OSError:
+        return False
+
+
 def _e2e(n, k, mode, distributed, world, rank, dev):
+    """The same Rgemm through the public API from pinned HOST planes, host
+    copies inside the timed region.  N = 1: ddb_rgemm_host (copies pipelined
+    with the kernels).  N > 1: every rank runs that host entry on its column
+    slab, reading A / its B columns and writing its C columns through its OWN
+    PCIe link from host planes in shared memory (parallel.rgemm_host_shared);
+    without room in /dev/shm, rank 0 stages everything and the slabs go over
+    NCCL (parallel.rgemm_host_columns)."""
     import torch
     from paper_2109_13406_b200 import HostMatrix, Rgemm
     from paper_2109_13406_b200 import parallel
+    from paper_2109_13406_b200.matrix import SharedHostMatrix
     from paper_2109_13406_b200.synth import random_dd
+    dims = ((n, k, 1), (k, n, 2), (n, n, 3))
+    shared = False
     hm = []
-    if rank == 0:
-        for rows, cols, tag in ((n, k, 1), (k, n, 2), (n, n, 3)):
-            m = HostMatrix(rows, cols, "dd", rows, pinned=True)
+    if distributed:
+        import torch.distributed as dist
+        flag = [_shm_room(16 * (n * k + k * n + n * n))] if rank == 0 else [None]
+        dist.broadcast_object_list(flag, src=0)
+        shared = bool(flag[0])
+    if shared:
+        names = [None] * 3
+        if rank == 0:
+            for rows, cols, tag in dims:
+                m_ = SharedHostMatrix(rows, cols, "dd", rows, create=True)
+                hi, lo = random_dd(rows, cols, rows, 0, tag)
+                m_.store[0][:] = hi
+                m_.store[1][:] = lo
+                hm.append(m_)
+            names = [x.name for x in hm]
+        dist.broadcast_object_list(names, src=0)
+        if rank != 0:
+            hm = [SharedHostMatrix(rows, cols, "dd", rows, name=nm)
+                  for (rows, cols, _), nm in zip(dims, names)]
+        for x in hm:
+            x.pin()                      # page-lock this rank's mapping (setup)
+    elif rank == 0:
+        for rows, cols, tag in dims:
+            m_ = HostMatrix(rows, cols, "dd", rows, pinned=True)
             hi, lo = random_dd(rows, cols, rows, 0, tag)
-            m.store[0][:] = hi
-            m.store[1][:] = lo
-            hm.append(m)
+            m_.store[0][:] = hi
+            m_.store[1][:] = lo
+            hm.append(m_)
     steps = 2
     times = []
     for it in range(steps + 1):
@@ -550,7 +589,10 @@ def _e2e(n, k, mode, distributed, world, rank, dev):
             import torch.distributed as dist
             dist.barrier()
         t0 = time.perf_counter()
-        if distributed:
+        if shared:
+            parallel.rgemm_host_shared("N", "N", n, n, k, ALPHA, hm[0], hm[1], BETA, hm[2],
+                                       world, rank, mode=mode)
+        elif distributed:
             a, b, c = hm if hm else (None,) * 3
             parallel.rgemm_host_columns("N", "N", n, n, k, ALPHA, a, b, BETA, c, world, rank, dev,
                                         mode=mode)
@@ -566,12 +608,23 @@ def _e2e(n, k, mode, distributed, world, rank, dev):
         tt = torch.tensor([t], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = float(tt.item())
+        dist.barrier()
+    if shared:
+        for x in hm:
+            x.close()
+    w = n // max(1, world)
     return {"value": 2.0 * n * n * k / t / 1e9, "unit": UNIT,
-            "h2d_bytes_per_step": 16 * (n * k + k * n + n * n), "d2h_bytes_per_step": 16 * n * n,
+            "h2d_bytes_per_step": 16 * (n * k + k * n + n * n) + (16 * n * k * (world - 1)
+                                                                   if shared else 0),
+            "d2h_bytes_per_step": 16 * n * n,
             "ms_per_step": t * 1e3,
-            "host_buffers": "pinned numpy planes, " + (
-                "parallel.rgemm_host_columns (staged on the root, then column-split)"
-                if distributed else "ddb_rgemm_host")}
+            "host_buffers": ("shared-memory host planes, pinned per rank; every rank runs "
+                             "ddb_rgemm_host on its column slab over its own PCIe link "
+                             "(parallel.rgemm_host_shared)" if shared else
+                             "pinned numpy planes, " + (
+                                 "parallel.rgemm_host_columns (staged on the root, then "
+                                 "column-split)" if distributed else "ddb_rgemm_host")),
+            "per_rank_slab_columns": w if distributed else n}
 
 
 def _config5(mode, dev, stream, distributed, world, rank, n=32768):

@@ -251,6 +251,12 @@ int ddb_last_route(void);
  * bench's roofline denominator. */
 double ddb_fp64_peak_probe(void* stream);
 
+/* Page-lock / release an existing host range (portable), so the *_host entry
+ * points copy from / to it by DMA; used for host buffers shared between
+ * processes (one process per GPU staging its own slab, parallel.py). */
+int ddb_host_register(void* ptr, int64_t bytes);
+int ddb_host_unregister(void* ptr);
+
 /* Diagnostic: the split algorithm's cross terms alone (device pointers,
  * asynchronous on `stream`): X (m x n, ld = m) = A_lo*B_hi + A_hi*B_lo, NN,
  * on the hand-written DMMA kernel.  Planes 16-byte aligned, lda / ldb even.

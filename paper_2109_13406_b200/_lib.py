@@ -33,7 +33,7 @@ EXPORTS = ("ddb_rgemm", "ddb_rsyrk", "ddb_rgemm_host", "ddb_rsyrk_host",
            "ddb_rgemm_mgpu", "ddb_rsyrk_mgpu",
            "ddb_dtrsm", "ddb_dtrsm_host", "ddb_dgetrf", "ddb_dgetrf_host",
            "ddb_dgetrs", "ddb_dgetrs_host", "ddb_dpotrf", "ddb_dpotrf_host",
-           "ddb_cross_terms", "ddb_abs_bound")
+           "ddb_cross_terms", "ddb_abs_bound", "ddb_host_register", "ddb_host_unregister")
 
 _lib = None
 
@@ -133,6 +133,10 @@ def load():
     L.ddb_last_route.restype = ctypes.c_int
     L.ddb_fp64_peak_probe.restype = ctypes.c_double
     L.ddb_fp64_peak_probe.argtypes = [_dp]
+    L.ddb_host_register.restype = ctypes.c_int
+    L.ddb_host_register.argtypes = [_dp, _i64]
+    L.ddb_host_unregister.restype = ctypes.c_int
+    L.ddb_host_unregister.argtypes = [_dp]
     L.ddb_abs_bound.restype = ctypes.c_int
     L.ddb_abs_bound.argtypes = [_c, _c, _i64, _i64, _i64, _dp, _i64, _dp, _i64, _dp, _dp, _dp,
                                 _dp, _dp, _dp]

@@ -683,4 +683,27 @@ int ddb_abs_bound(char transa, char transb, int64_t m, int64_t n, int64_t k,
   return DDB_OK;
 }
 
+// Page-lock an existing host range (e.g. a shared-memory mapping that several
+// processes stage from, parallel.rgemm_host_shared) so copies from / to it are
+// DMA at full link speed; portable across devices.  Pair with
+// ddb_host_unregister.
+int ddb_host_register(void* ptr, int64_t bytes) {
+  if (ptr == nullptr || bytes <= 0) return DDB_EINVAL;
+  const cudaError_t e = cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterPortable);
+  if (e == cudaErrorHostMemoryAlreadyRegistered) {
+    cudaGetLastError();
+    return DDB_OK;
+  }
+  return e == cudaSuccess ? DDB_OK : fail(e, "cudaHostRegister");
+}
+
+int ddb_host_unregister(void* ptr) {
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e == cudaErrorHostMemoryNotRegistered) {
+    cudaGetLastError();
+    return DDB_OK;
+  }
+  return e == cudaSuccess ? DDB_OK : fail(e, "cudaHostUnregister");
+}
+
 }  // extern "C"

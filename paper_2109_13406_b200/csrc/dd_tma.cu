@@ -63,7 +63,10 @@ constexpr int NT = 256;       // 8 consumer warps
 // TMA load; setmaxnreg hands its registers to the consumers, 24 / 240 per
 // thread); 0: thread 0 of consumer warp 0 doubles as the producer
 constexpr int NTK = NT + (DDB_TMA_WS ? 128 : 0);
-constexpr int REG_CONSUMER = 240, REG_PRODUCER = 24;
+#ifndef DDB_TMA_REGC
+#define DDB_TMA_REGC 240      // consumer registers per thread after setmaxnreg
+#endif
+constexpr int REG_CONSUMER = DDB_TMA_REGC, REG_PRODUCER = 24;
 constexpr int TM = 8, TN = 4, RX = 32, RY = 32;
 constexpr int A_PLANE = BK * BM, B_PLANE = BN * BK;          // doubles
 constexpr int STAGE_DOUBLES = 2 * A_PLANE + 2 * B_PLANE;     // 6144 doubles = 48 KB

@@ -189,6 +189,54 @@ class HostMatrix:
         return f"HostMatrix({self.m}x{self.n}, ld={self.ld}, precision={self.precision!r})"
 
 
+class SharedHostMatrix(HostMatrix):
+    """HostMatrix whose planes live in POSIX shared memory, so that every
+    process of a one-process-per-GPU job maps the same host buffer and copies
+    its own part over its own PCIe link (parallel.rgemm_host_shared).
+
+    The creator (``create=True``) allocates; the others attach by ``name``.
+    ``pin()`` page-locks this process's mapping through the library
+    (``ddb_host_register``) so the host entry points copy by DMA."""
+
+    def __init__(self, m, n, precision="dd", ld=None, name=None, create=False):
+        from multiprocessing import shared_memory
+        ld = max(1, m) if ld is None else ld
+        if ld < max(1, m) or m < 0 or n < 0:
+            raise ValueError("bad shared matrix shape")
+        self.m, self.n, self.ld, self.precision = m, n, ld, precision
+        planes = _planes(precision)
+        dt = np.dtype(_plane_dtype(precision))
+        self._plane_bytes = ld * n * dt.itemsize
+        nbytes = max(1, planes * self._plane_bytes)
+        self._shm = shared_memory.SharedMemory(name=name, create=create, size=nbytes)
+        self.name = self._shm.name
+        self._owner = create
+        self._pinned = False
+        self.store = tuple(np.ndarray((ld * n,), dtype=dt, buffer=self._shm.buf,
+                                      offset=i * self._plane_bytes) for i in range(planes))
+
+    def pin(self):
+        from . import _lib
+        if not self._pinned and self._plane_bytes:
+            rc = _lib.load().ddb_host_register(self.store[0].ctypes.data,
+                                               len(self.store) * self._plane_bytes)
+            if rc != 0:
+                raise RuntimeError(f"ddb_host_register: {_lib.last_error()}")
+            self._pinned = True
+        return self
+
+    def close(self):
+        """Unpin, unmap, and (creator) unlink the shared segment."""
+        if self._pinned:
+            from . import _lib
+            _lib.load().ddb_host_unregister(self.store[0].ctypes.data)
+            self._pinned = False
+        self.store = ()
+        self._shm.close()
+        if self._owner:
+            self._shm.unlink()
+
+
 class DeviceMatrix:
     """m x n dd matrix resident in HBM: ``store = (hi, lo)`` torch float64
     CUDA tensors of length ``ld*n`` in the reference's column-major layout."""

@@ -33,7 +33,7 @@ import math
 import torch
 import torch.distributed as dist
 
-from .matrix import DeviceMatrix, to_dd
+from .matrix import DeviceMatrix, HostMatrix, SharedHostMatrix, to_dd
 from .mpblas import Rgemm, Rsyrk
 
 TILE = 64   # column boundaries are multiples of the kernel's BN
@@ -150,7 +150,9 @@ def rgemm_columns(plan, transa, transb, alpha, a, b, beta, c, mode=None, group=N
     beta_zero = be[0] == 0.0 and be[1] == 0.0
     exact_like = (default_mode() if mode is None else mode) in ("exact", "reference")
     if kchunks is None:
-        kchunks = 4 if k >= 4096 and (ta == "N" or not exact_like) else 1
+        # panels exist to overlap the broadcast of op(A) with compute; one
+        # rank has nothing to overlap (each panel is a separate kernel call)
+        kchunks = 4 if world > 1 and k >= 4096 and (ta == "N" or not exact_like) else 1
     if ta != "N" and exact_like:
         kchunks = 1
     panels = _k_chunks(k, kchunks)
@@ -374,3 +376,32 @@ def rgemm_host_columns(transa, transb, m, n, k, alpha, a, b, beta, c, world, ran
         # pageable temporary
         for dst, src in zip(c.store, C.store):
             torch.from_numpy(dst).copy_(src)
+
+
+def rgemm_host_shared(transa, transb, m, n, k, alpha, a, b, beta, c, world, rank, mode=None,
+                      group=None, compute=None):
+    """End-to-end multi-rank Rgemm from / to SHARED host buffers: every rank
+    runs the host entry point (``ddb_rgemm_host``: copies pipelined with the
+    kernels) on its column slab J_r of C, reading op(A) and its op(B) columns
+    and writing its C columns through its OWN GPU and PCIe link -- no
+    collective on the data path, and no rank's link carries another's slab.
+
+    ``a``, ``b``, ``c`` are ``SharedHostMatrix`` objects mapped (and pinned)
+    in every rank.  The per-element operation sequence is the single call's,
+    so exact mode is bitwise equal to ``Rgemm``.  Returns after every rank's
+    slab is back in ``c`` (a barrier)."""
+    compute = functools.partial(Rgemm, _check_storage=False) if compute is None else compute
+    ta, tb = transa.upper(), transb.upper()
+    j0, j1 = column_split(n, world)[rank]
+    w = j1 - j0
+    if w > 0:
+        nra, nca = (m, k) if ta == "N" else (k, m)
+        # op(B)(:, J): columns J of B ('N', offset j0 * ldb) or rows J ('T', offset j0)
+        boff = j0 * b.ld if tb == "N" else j0
+        bv = HostMatrix.from_planes(k if tb == "N" else w, w if tb == "N" else k,
+                                    *(p[boff:] for p in b.store), ld=b.ld)
+        cv = HostMatrix.from_planes(m, w, *(p[j0 * c.ld:] for p in c.store), ld=c.ld)
+        compute(ta, tb, m, w, k, alpha, a, a.ld, bv, b.ld, beta, cv, c.ld, mode=mode)
+    if dist.is_initialized():
+        dist.barrier(group=group)
+

@@ -40,6 +40,15 @@ def oracle_syrk(up, tr, n, k, alpha, a, lda, beta, c, ldc, mode=None):
     assert rc == 0
 
 
+def oracle_gemm_np(ta, tb, m, n, k, alpha, a, lda, b, ldb, beta, c, ldc, mode=None):
+    """compute callable on host (numpy) matrices, writing C in place."""
+    rc = oracle.rgemm(ta, tb, m, n, k, to_dd(alpha), np.ascontiguousarray(a.store[0]),
+                      np.ascontiguousarray(a.store[1]), lda, np.ascontiguousarray(b.store[0]),
+                      np.ascontiguousarray(b.store[1]), ldb, to_dd(beta), c.store[0], c.store[1],
+                      ldc, threads=1)
+    assert rc == 0
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -74,6 +83,34 @@ def _worker(rank, world, port, case, q):
                                    kchunks=kchunks, mode=mode)
             if rank == 0:
                 q.put((C.store[0].numpy().copy(), C.store[1].numpy().copy()))
+        elif case[0] == "shared":
+            from paper_2109_13406_b200.matrix import SharedHostMatrix
+            _, ta, tb, m, n, k, pad = case
+            nra, nca = (m, k) if ta == "N" else (k, m)
+            nrb, ncb = (k, n) if tb == "N" else (n, k)
+            dims = ((nra, nca, 1), (nrb, ncb, 2), (m, n, 3))
+            names = [None, None, None]
+            mats = []
+            if rank == 0:
+                for rows, cols, tag in dims:
+                    sm = SharedHostMatrix(rows, cols, "dd", rows + pad, create=True)
+                    hi, lo = random_dd(rows, cols, rows + pad, 6, tag)
+                    sm.store[0][:] = hi
+                    sm.store[1][:] = lo
+                    mats.append(sm)
+                names = [x.name for x in mats]
+            dist.broadcast_object_list(names, src=0)
+            if rank != 0:
+                mats = [SharedHostMatrix(rows, cols, "dd", rows + pad, name=nm)
+                        for (rows, cols, _), nm in zip(dims, names)]
+            a, b, c = mats
+            parallel.rgemm_host_shared(ta, tb, m, n, k, 1.5, a, b, 0.5, c, world, rank,
+                                       compute=oracle_gemm_np)
+            if rank == 0:
+                q.put((np.array(c.store[0]), np.array(c.store[1])))
+            dist.barrier()
+            for x in mats:
+                x.close()
         elif case[0] == "host":
             from paper_2109_13406_b200 import HostMatrix
             _, m, n, k = case
@@ -147,6 +184,23 @@ def test_rgemm_host_columns_bitwise_equal_single_process():
     ch, cl = (x.copy() for x in random_dd(m, n, m, 5, 3))
     oracle.rgemm("N", "N", m, n, k, (1.5, 0.0), A[0], A[1], m, B[0], B[1], k, (0.5, 0.0),
                  ch, cl, m)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
+@pytest.mark.parametrize("ta,tb,pad", [("N", "N", 0), ("T", "T", 3), ("N", "T", 1)])
+def test_rgemm_host_shared_bitwise_equal_single_process(ta, tb, pad):
+    """The per-rank host entry (every rank stages its own slab from shared
+    host memory through its own link, no collective on the data path):
+    the single-process result bit for bit, padding untouched."""
+    m, n, k = 70, 150, 33
+    got = _run(("shared", ta, tb, m, n, k, pad))
+    nra, nca = (m, k) if ta == "N" else (k, m)
+    nrb, ncb = (k, n) if tb == "N" else (n, k)
+    A = random_dd(nra, nca, nra + pad, 6, 1)
+    B = random_dd(nrb, ncb, nrb + pad, 6, 2)
+    ch, cl = (x.copy() for x in random_dd(m, n, m + pad, 6, 3))
+    oracle.rgemm(ta, tb, m, n, k, (1.5, 0.0), A[0], A[1], nra + pad, B[0], B[1], nrb + pad,
+                 (0.5, 0.0), ch, cl, m + pad)
     assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
 
 
