@@ -609,7 +609,8 @@ int ddb_zgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k, co
 // ---- diagnostics: the fast mode's building blocks in isolation --------------
 
 // X (m x n, ld = m) = A_lo B_hi + A_hi B_lo on the hand-written DMMA kernel
-// (dd_cross.cu).  NN operands: 16-byte aligned planes, even lda / ldb.
+// (dd_cross.cu), with the production split-K policy.  NN operands: 16-byte
+// aligned planes, even lda / ldb.
 // tri: 0 every tile, 1 / 2 only tiles meeting the upper / lower triangle.
 int ddb_cross_terms(int64_t m, int64_t n, int64_t k, const double* a_hi, const double* a_lo,
                     int64_t lda, const double* b_hi, const double* b_lo, int64_t ldb, double* x,
@@ -624,7 +625,19 @@ int ddb_cross_terms(int64_t m, int64_t n, int64_t k, const double* a_hi, const d
   g.b_hi = b_hi; g.b_lo = b_lo; g.ldb = ldb;
   g.syrk = tri;
   int nl = 0;
-  cudaError_t e = launch_cross_dmma(g, x, static_cast<cudaStream_t>(stream), &nl);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the production policy: k-slices when the tile grid underfills the GPU,
+  // reduced in slice order into x (the slices need (S - 1) m n scratch)
+  int64_t kchunk = k;
+  const int slices = cross_kslices(g, &kchunk);
+  double* xs = x;
+  cudaError_t e = cudaSuccess;
+  if (slices > 1) e = cudaMallocAsync(reinterpret_cast<void**>(&xs), sizeof(double) * slices * m * n, s);
+  if (e == cudaSuccess) e = launch_cross_dmma(g, xs, s, &nl, slices, kchunk);
+  if (e == cudaSuccess && slices > 1) {
+    e = cudaMemcpyAsync(x, xs, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, s);
+    cudaFreeAsync(xs, s);
+  }
   g_launches += nl;
   if (e == cudaErrorNotSupported) {
     g_last_error = "ddb_cross_terms: operands not TMA-eligible (alignment / odd ld)";

@@ -26,6 +26,8 @@
 // The B fragment loads are conflict-free (2 wavefronts per LDS.64), the A
 // ones 4 wavefronts; at one warp-k4-step per 128 SM cycles that is ~40 of the
 // 128 available wavefront slots.
+#include <cmath>
+
 #include "internal.h"
 #include "tma_util.cuh"
 
@@ -67,7 +69,12 @@ __global__ void __launch_bounds__(NT, 1)
 cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant__ CUtensorMap mAh,
                   const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
                   double* __restrict__ x, int64_t m, int64_t n, int64_t k, int tiles_m,
-                  int tiles_n) {
+                  int tiles_n, int64_t kchunk) {
+  // split-K: blockIdx.y = k-slice z over [z kchunk, (z + 1) kchunk), its sum
+  // to plane z of x (m x n each; cross_reduce_kernel adds the planes in order)
+  const int64_t kz0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t kz1 = kz0 + kchunk < k ? kz0 + kchunk : k;
+  x += (size_t)blockIdx.y * m * n;
   // grouped raster over the tile grid (L2 reuse of the A / B panels)
   const int bid = blockIdx.x;
   const int group_size = GROUP_M * tiles_n;
@@ -96,7 +103,7 @@ cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant
   }
   __syncthreads();
 
-  const int ktiles = (int)((k + BK - 1) / BK);
+  const int ktiles = (int)((kz1 - kz0 + BK - 1) / BK);   // kchunk is a multiple of BK
   if (warp >= NCW) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(REG_PRODUCER));
     // ---- TMA producer: one lane walks the k-tiles ahead of the consumers ----
@@ -105,7 +112,7 @@ cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant
         const int s = kt % STAGES;
         if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
         unsigned char* st = ring_g + (size_t)s * STAGE_BYTES;
-        const int kc = kt * BK;
+        const int kc = (int)(kz0 + (int64_t)kt * BK);
         mbar_expect_tx(&full[s], STAGE_BYTES);
 #pragma unroll
         for (int b = 0; b < BM / 16; ++b) {
@@ -183,7 +190,59 @@ cross_dmma_kernel(const __grid_constant__ CUtensorMap mAl, const __grid_constant
 
 // X = A_lo B_hi + A_hi B_lo for an NN-form call (16-byte aligned planes, even
 // lda / ldb: tma_eligible); cudaErrorNotSupported when a map cannot be made.
-cudaError_t launch_cross_dmma(const GemmArgs& g, double* x, cudaStream_t s, int* nlaunch) {
+// x_0 += x_1 + ... + x_{S-1} in slice order (deterministic for a given shape)
+__global__ void __launch_bounds__(256)
+cross_reduce_kernel(double* __restrict__ x, int64_t mn, int slices) {
+  for (int64_t i = (int64_t)blockIdx.x * 256 + threadIdx.x; i < mn;
+       i += (int64_t)gridDim.x * 256) {
+    double v = x[i];
+    for (int z = 1; z < slices; ++z) v = __dadd_rn(v, x[(size_t)z * mn + i]);
+    x[i] = v;
+  }
+}
+
+// k-slices for the cross kernel: the tile grid alone can leave the last wave
+// mostly empty (m = n = 2048: 256 tiles = 1.7 waves on 148 SMs); splitting k
+// into S slices (each >= 1024 deep, a multiple of BK) multiplies the work
+// units.  S = 1 unless it buys > 3 % of wave efficiency.
+int cross_kslices(const GemmArgs& g, int64_t* kchunk) {
+  using namespace cross;
+  *kchunk = g.k;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t tm = (g.m + BM - 1) / BM, tn = (g.n + BN - 1) / BN;
+  int64_t tiles = 0;
+  if (g.syrk == 0) {
+    tiles = tm * tn;
+  } else {
+    for (int64_t j = 0; j < tn; ++j)
+      for (int64_t i = 0; i < tm; ++i)
+        if (g.syrk == 1 ? i * BM <= j * BN + BN - 1 : i * BM + BM - 1 >= j * BN) ++tiles;
+  }
+  auto eff = [&](int64_t t) {
+    const double w = (double)t / sms;
+    return w / std::ceil(w);
+  };
+  double best = eff(tiles);
+  int best_s = 1;
+  for (int sl = 2; sl <= 8; ++sl) {
+    int64_t chunk = (g.k + sl - 1) / sl;
+    chunk = (chunk + BK - 1) / BK * BK;
+    if (chunk < 1024) break;
+    const int real = (int)((g.k + chunk - 1) / chunk);
+    const double e = eff(tiles * real);
+    if (e > best + 0.03) {
+      best = e;
+      best_s = real;
+      *kchunk = chunk;
+    }
+  }
+  if (best_s == 1) *kchunk = g.k;
+  return best_s;
+}
+
+cudaError_t launch_cross_dmma(const GemmArgs& g, double* x, cudaStream_t s, int* nlaunch,
+                              int slices, int64_t kchunk) {
   using namespace cross;
   alignas(64) CUtensorMap mAl, mAh, mBh, mBl;
   const auto dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
@@ -200,8 +259,16 @@ cudaError_t launch_cross_dmma(const GemmArgs& g, double* x, cudaStream_t s, int*
                                        (int)SMEM_BYTES);
   if (e != cudaSuccess) return e;
   const int tiles_m = (int)((g.m + BM - 1) / BM), tiles_n = (int)((g.n + BN - 1) / BN);
-  kern<<<tiles_m * tiles_n, NT, SMEM_BYTES, s>>>(mAl, mAh, mBh, mBl, x, g.m, g.n, g.k, tiles_m,
-                                                 tiles_n);
+  if (slices < 1) { slices = 1; kchunk = g.k; }
+  kern<<<dim3(tiles_m * tiles_n, slices), NT, SMEM_BYTES, s>>>(mAl, mAh, mBh, mBl, x, g.m, g.n,
+                                                               g.k, tiles_m, tiles_n, kchunk);
+  ++*nlaunch;
+  e = cudaGetLastError();
+  if (e != cudaSuccess || slices == 1) return e;
+  const int64_t mn = g.m * g.n;
+  int64_t blocks = (mn + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  cross_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>(x, mn, slices);
   ++*nlaunch;
   return cudaGetLastError();
 }

@@ -143,7 +143,9 @@ cudaError_t launch_splitk_reduce(const GemmArgs& g, int splits, const int* flag,
                                  int* nlaunch);
 cudaError_t launch_bound(const GemmArgs& g, const int* row_exp, const int* col_exp, void* ws,
                          float* bound, cudaStream_t s, int* nlaunch, const char** what);
-cudaError_t launch_cross_dmma(const GemmArgs& g, double* x, cudaStream_t s, int* nlaunch);
+int cross_kslices(const GemmArgs& g, int64_t* kchunk);
+cudaError_t launch_cross_dmma(const GemmArgs& g, double* x, cudaStream_t s, int* nlaunch,
+                              int slices = 1, int64_t kchunk = 0);
 
 // complex GEMM (dd_complex.cu)
 struct cdd { dd re, im; };
