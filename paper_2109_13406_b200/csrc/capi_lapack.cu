@@ -539,16 +539,23 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
   }
   *info = 0;
   if (n == 0) return DDB_OK;                          // chol.py:30-31
-  // two block levels: outer width NB (the trailing Rsyrk / Rgemm depth) and
+  // three block levels: outer width NB (the depth of the bulk trailing
+  // Rsyrk / Rgemm: 1024 reaches the split algorithm's k >= 1024 regime),
+  // middle width MB (the depth of the updates inside an outer panel) and
   // inner width ib <= kPotrfMaxNb (diagonal block in shared memory)
   if (nb <= 0) {
     static const int64_t nb_env = [] {
       const char* v = std::getenv("DDB_POTRF_NB");
       return v ? (int64_t)std::atoll(v) : (int64_t)0;
     }();
-    nb = nb_env > 0 ? nb_env : 256;
+    // 1024-deep outer panels pay off once the bulk trailing update dominates
+    // the panel chain: n = 16384 fast 531 -> 470 ms; n = 8192 98.6 -> 101.5
+    // ms (the longer outer panels lengthen the lookahead's critical path),
+    // and exact mode gains nothing from depth
+    nb = nb_env > 0 ? nb_env : (n >= 12288 && mode != DDB_MODE_EXACT ? 1024 : 256);
   }
   const int64_t NB = nb;
+  const int64_t MB = NB > 256 ? 256 : NB;
   const int64_t ib = nb < kPotrfMaxNb ? nb : kPotrfMaxNb;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   retain_pool_memory();
@@ -564,7 +571,9 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
   const size_t recb = ((sizeof(double) * 2 * (size_t)ib + 255) / 256) * 256;
   const size_t full = sizeof(double) * (size_t)n * n;
   const size_t t_in = p.upper ? (size_t)n * ib : 0, t_out = p.upper ? (size_t)n * NB : 0;
-  const size_t ws_bytes = head + 4 * vec + recb + 2 * full + sizeof(double) * 2 * (t_in + 2 * t_out);
+  const size_t t_mid = p.upper && MB < NB ? (size_t)n * MB : 0;
+  const size_t ws_bytes =
+      head + 4 * vec + recb + 2 * full + sizeof(double) * 2 * (t_in + 2 * t_out + t_mid);
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "workspace allocation");
@@ -581,6 +590,8 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
   double* tin_l = tin_h + t_in;
   double* tout_h = tin_l + t_in;                     // outer T: hi[2] | lo[2]
   double* tout_l = tout_h + 2 * t_out;
+  double* tmid_h = tout_l + 2 * t_out;               // middle T: hi | lo
+  double* tmid_l = tmid_h + t_mid;
   int nl = 0;
   e = cudaMemsetAsync(ws, 0, head + 2 * vec, s);
   const size_t dpitch = sizeof(double) * (size_t)(lda + 1);
@@ -648,9 +659,9 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
     ++nl;
     return launch_potrf_transpose(q, j0, j1, (int)(j1 - j0), n - j1, cs);
   };
-  // factor the outer panel [J0, J1): inner blocks, each followed by the
-  // update of the rest of the outer panel's columns
-  auto factor_outer = [&](int64_t J0, int64_t J1) -> int {
+  // factor the middle panel [J0, J1): inner blocks, each followed by the
+  // update of the rest of the middle panel's columns
+  auto factor_mid = [&](int64_t J0, int64_t J1) -> int {
     for (int64_t i0 = J0; i0 < J1; i0 += ib) {
       const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
       cudaError_t er = launch_potrf_diag(p, i0, i1, cs);
@@ -664,6 +675,24 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
         if (p.upper && (er = transpose(i0, i1, tin_h, tin_l)) != cudaSuccess)
           return fail(er, "rpotrf transpose");
         const int r = update(i0, i1, i1, J1, tin_h, tin_l, i1, cs);
+        if (r != DDB_OK) return r;
+      }
+    }
+    return DDB_OK;
+  };
+  // factor the outer panel [J0, J1): middle panels, each followed by the
+  // update (depth MB) of the rest of the outer panel's columns.  Every
+  // element still receives its updates in pivot-block order.
+  auto factor_outer = [&](int64_t J0, int64_t J1) -> int {
+    for (int64_t m0 = J0; m0 < J1; m0 += MB) {
+      const int64_t m1 = m0 + MB < J1 ? m0 + MB : J1;
+      int r = factor_mid(m0, m1);
+      if (r != DDB_OK) return r;
+      if (m1 < J1) {
+        cudaError_t er = cudaSuccess;
+        if (p.upper && (er = transpose(m0, m1, tmid_h, tmid_l)) != cudaSuccess)
+          return fail(er, "rpotrf transpose");
+        r = update(m0, m1, m1, J1, tmid_h, tmid_l, m1, cs);
         if (r != DDB_OK) return r;
       }
     }

@@ -109,7 +109,8 @@ def test_rpotrf_golden_fast_modes(idx, mode):
 
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
-@pytest.mark.parametrize("n,nb", [(700, 0), (1000, 100), (900, 48), (650, 130)])
+@pytest.mark.parametrize("n,nb", [(700, 0), (1000, 100), (900, 48), (650, 130), (1100, 600),
+                                  (1300, 520)])
 def test_rpotrf_exact_matches_oracle(uplo, n, nb):
     """Multi-block sizes, default and odd block widths: bitwise vs the C
     oracle (the reference's order, pinned by the golden tests)."""
@@ -123,7 +124,8 @@ def test_rpotrf_exact_matches_oracle(uplo, n, nb):
 
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
-def test_rpotrf_late_failure_restores_trailing(uplo):
+@pytest.mark.parametrize("nb", [64, 300])
+def test_rpotrf_late_failure_restores_trailing(uplo, nb):
     """A failing pivot deep in a multi-block run: info, A(j,j) and every
     entry the reference leaves untouched match the oracle bit for bit."""
     n, ld = 600, 600
@@ -134,7 +136,7 @@ def test_rpotrf_late_failure_restores_trailing(uplo):
     rc, oinfo = oracle.rpotrf(uplo, n, oh, ol, ld)
     assert oinfo == j + 1
     for mode in ("exact", "fast"):
-        info, gh, gl = run(uplo, n, ld, hi, lo, mode, 64)
+        info, gh, gl = run(uplo, n, ld, hi, lo, mode, nb)
         assert info == j + 1
         if mode == "exact":
             assert bits_equal(gh, oh) and bits_equal(gl, ol)
@@ -147,8 +149,8 @@ def test_rpotrf_late_failure_restores_trailing(uplo):
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("mode", ["fast", "twosum", "exact"])
-def test_rpotrf_large_residual(uplo, mode):
-    n = 2500
+@pytest.mark.parametrize("n", [2500, 4500])
+def test_rpotrf_large_residual(uplo, mode, n):
     hi, lo = spd_dd(n, n, seed=11)
     info, gh, gl = run(uplo, n, n, hi, lo, mode)
     assert info == 0
