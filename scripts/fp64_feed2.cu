@@ -5,7 +5,9 @@
 //        the next pair's loads hoisted by the compiler)      -> ~246 registers
 //   V 1: per step: A 4 x LDS.128 + B 4 x LDS.64 right before the step
 //   V 2: per pair, B k-pairs (4 x LDS.128) once, A per step (4 x LDS.128)
-//   V 3: as V 2, with __launch_bounds__(256, 1) and a register cap of 200
+//   V 3: operands regenerated every step by integer ops (no loads)
+//   V 4: loop-invariant operands in this loop structure
+//   V 5 / V 6: V 0 / V 4 with the k-loop body not unrolled (6 steps of code)
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fp64_feed2 fp64_feed2.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -57,12 +59,12 @@ __global__ void __launch_bounds__(256, 1) feed(double* out, int iters) {
     }
   };
   for (int it = 0; it < iters; ++it) {
-#pragma unroll 2
+#pragma unroll (V >= 5 ? 1 : 2)
     for (int kk = 0; kk < KB; kk += 6) {
 #pragma unroll
       for (int pq = 0; pq < 6; pq += 2) {
         const int k = kk + pq;
-        if (V == 0) {
+        if (V == 0 || V == 5) {
           double a0[TM], a1[TM], b0[TN], b1[TN];
           lda(k, a0);
           lda(k + 1, a1);
@@ -84,6 +86,32 @@ __global__ void __launch_bounds__(256, 1) feed(double* out, int iters) {
             lda(k + q, a);
 #pragma unroll
             for (int j = 0; j < TN; ++j) b[j] = sb[((j >> 1) * 32 + ty * 2 + (j & 1)) * KB + k + q];
+            step(T, L, a, b);
+            if ((pq + q + 1) % 3 == 0) fold(T, L);
+          }
+        } else if (V == 3) {
+          // operands change every step but come from integer-pipe ops, not loads
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double a[TM], b[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+              a[i] = __longlong_as_double(0x3FF0000000000000LL + (((long long)(k + q) * 977 + i * 131 + tx) & 0xFFFFF));
+#pragma unroll
+            for (int j = 0; j < TN; ++j)
+              b[j] = __longlong_as_double(0x3FE0000000000000LL + (((long long)(k + q) * 733 + j * 89 + ty) & 0xFFFFF));
+            step(T, L, a, b);
+            if ((pq + q + 1) % 3 == 0) fold(T, L);
+          }
+        } else if (V == 4 || V == 6) {
+          // loop-invariant operands (the register-only ceiling, same loop structure)
+          double a[TM], b[TN];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) a[i] = 1.0 + i * 1e-7 + tx * 1e-9;
+#pragma unroll
+          for (int j = 0; j < TN; ++j) b[j] = 0.5 + j * 1e-7 + ty * 1e-9;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
             step(T, L, a, b);
             if ((pq + q + 1) % 3 == 0) fold(T, L);
           }
@@ -170,5 +198,9 @@ int main() {
   one<0>(sms, out, peak);
   one<1>(sms, out, peak);
   one<2>(sms, out, peak);
+  one<3>(sms, out, peak);
+  one<4>(sms, out, peak);
+  one<5>(sms, out, peak);
+  one<6>(sms, out, peak);
   return 0;
 }
