@@ -204,6 +204,26 @@ def test_rgemm_host_shared_bitwise_equal_single_process(ta, tb, pad):
     assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
 
 
+@pytest.mark.parametrize("world", [3, 4])
+def test_rgemm_and_rsyrk_columns_wider_worlds(world):
+    """World sizes 3 and 4 (uneven column / triangle slabs, k-panels): still
+    the single-process result bit for bit."""
+    m, n, k = 70, 200, 130
+    got = _run(("gemm", "N", "T", m, n, k, 0.5, 3, None), world=world)
+    A = random_dd(m, k, m, 3, 1)
+    B = random_dd(n, k, n, 3, 2)
+    ch, cl = (x.copy() for x in random_dd(m, n, m, 3, 3))
+    oracle.rgemm("N", "T", m, n, k, (1.5, 0.0), A[0], A[1], m, B[0], B[1], n, (0.5, 0.0),
+                 ch, cl, m)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+    nn, kk = 230, 19
+    got = _run(("syrk", "L", "N", nn, kk), world=world)
+    A = random_dd(nn, kk, nn, 4, 1)
+    ch, cl = (x.copy() for x in random_dd(nn, nn, nn, 4, 3))
+    oracle.rsyrk("L", "N", nn, kk, (1.5, 0.0), A[0], A[1], nn, (0.5, 0.0), ch, cl, nn)
+    assert np.array_equal(got[0], ch) and np.array_equal(got[1], cl)
+
+
 @pytest.mark.parametrize("ta,tb,beta,mode", [("N", "N", 0.5, None), ("N", "T", 0.0, None),
                                              ("T", "N", 0.5, "exact"), ("T", "T", 1.0, "exact")])
 def test_rgemm_columns_k_panels_bitwise(ta, tb, beta, mode):
