@@ -6,8 +6,10 @@
 // planes) through shared memory by a 3-stage cp.async pipeline.  8-byte
 // copies handle any lda / ldb / alignment / transpose: each double lands in
 // its k-major smem slot, so every trans variant reads smem identically with
-// 16-byte LDS.  Tensor cores are not used: tcgen05 has no fp64 kind and DMMA
-// rounds away the per-product error terms dd needs.
+// 16-byte LDS.  The dd MAC stays on the FP64 pipe: tcgen05 has no fp64 kind
+// and DMMA rounds away the per-product error terms dd needs (the fast mode's
+// auxiliary cross-term and bound GEMMs do use DMMA / tcgen05: dd_cross.cu,
+// dd_bound.cu).
 //
 // Accumulation algorithms (template ALG), per output element:
 //

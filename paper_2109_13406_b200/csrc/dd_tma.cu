@@ -21,20 +21,23 @@
 // the certified anchor (Tn = fma(ah, bh, T), r = fma(ah, bh, T - Tn), L += r,
 // (T, L) folded every 3 steps: 5 FP64 instructions per MAC instead of 7.5,
 // and only the hi planes staged, 24-deep k-tiles), and the cross terms
-// X = A_lo B_hi + A_hi B_lo, two plain binary64 library GEMMs (for Rsyrk
-// one DGEMM + a triangle fold, dd_bound.cu) run first and added to L in the
-// epilogue; al bl (< u^2 |ab|) is dropped, as in every dd product.  Error per element, with the unit
-// v = 2^(E-106) < 2^-104 S' (2^E < 4 S', S' >= sum |ah bh| the certified
-// bound): each residual r (|r| <= ulp(T)/2 = 2^(E-53)) rounds by <= v/2; after
-// a fold |L| <= 2^(E-53), so by monotone rounding the three additions into L
-// stay <= 2^(E-52), 1.5 * 2^(E-52), 2^(E-51) and round by <= v, 2v, 2v: 6.5 v
-// per 3 steps, c = 2.17 (a period of 2 gives c = 2, of 4 c = 2.75).  The
-// GEMMs' recursive-summation bound is 2k u * sum (|al bh| + |ah bl|) <=
-// 4k u^2 S' (operands normalised, |lo| <= 2^-53 |hi|, which the prescan
-// enforces): c = 1; the dropped al bl c = 0.25.  With S' <= 1.08 sum |ab|
-// (bf16 round-up, fp32 factor at k = 65536): c <= 2.17 * 1.08 + 1.25 = 3.6
-// (+ O(u^2) epilogue roundings) against the north star's c = 4.
-// Measured at 8192^3: 240.4 ms vs 272.2 for the full MAC in this kernel.
+// X = A_lo B_hi + A_hi B_lo, computed first by the hand-written DMMA kernel
+// (dd_cross.cu; for Rsyrk on the triangle tiles only) and added to L in the
+// epilogue; al bl (< u^2 |ab|) is dropped, as in every dd product.  Error per
+// element, with the unit v = 2^(E-106) < 2^-104 S' (2^E < 4 S', S' >= sum
+// |ah bh| the certified bound): each residual r (|r| <= ulp(T)/2 =
+// 2^(E-53)) rounds by <= v/2; after a fold |L| <= 2^(E-53), so by monotone
+// rounding the three additions into L stay <= 2^(E-52), 1.5 * 2^(E-52),
+// 2^(E-51) and round by <= v, 2v, 2v: 6.5 v per 3 steps, c = 2.17 rho with
+// rho = S' / sum|ab| (a period of 2 gives 2 rho, of 4 2.75 rho).  The cross
+// sums' recursive-summation bound is 2k u * sum (|al bh| + |ah bl|) <=
+// 4k u^2 sum|ab| (operands normalised, |lo| <= 2^-53 |hi|, which the prescan
+// enforces): c = 1; the dropped al bl c = 0.25.  rho <= 1.11 for every
+// element the routing leaves here (dd_bound.cu: k <= 2^17 and row + column
+// exponent spreads within 112 - ceil(log2 k); wider elements take the TwoSum
+// fallback), so c <= 2.17 * 1.11 + 1.25 = 3.66 (+ O(u^2) epilogue roundings)
+// against the north star's c = 4.
+// Measured at 8192^3: 177 ms for this kernel + 60.5 ms of cross terms.
 #include <cuda.h>
 
 #include <cstdlib>
