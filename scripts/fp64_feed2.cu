@@ -89,6 +89,25 @@ __global__ void __launch_bounds__(256, 1) feed(double* out, int iters) {
             step(T, L, a, b);
             if ((pq + q + 1) % 3 == 0) fold(T, L);
           }
+        } else if (V == 7) {
+          // warp-uniform B: all 32 lanes of a warp share its 4 columns (rows
+          // spread over the lanes), so b can live in uniform registers
+          const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double a[TM], b[TN];
+#pragma unroll
+            for (int g = 0; g < TM / 2; ++g) {
+              const double2 h = *reinterpret_cast<const double2*>(sa + (k + q) * BM + (g * 64 + lane * 2) % BM);
+              a[2 * g] = h.x;
+              a[2 * g + 1] = h.y;
+            }
+#pragma unroll
+            for (int j = 0; j < TN; ++j)
+              b[j] = __shfl_sync(0xffffffffu, sb[(w * TN + j) * KB + k + q], 0);
+            step(T, L, a, b);
+            if ((pq + q + 1) % 3 == 0) fold(T, L);
+          }
         } else if (V == 3) {
           // operands change every step but come from integer-pipe ops, not loads
 #pragma unroll
@@ -202,5 +221,6 @@ int main() {
   one<4>(sms, out, peak);
   one<5>(sms, out, peak);
   one<6>(sms, out, peak);
+  one<7>(sms, out, peak);
   return 0;
 }
