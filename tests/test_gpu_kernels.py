@@ -152,3 +152,29 @@ def test_bound_with_spread_magnitudes():
     A, B, re, ce, Af, Bf, S = _bound("N", "N", 200, 160, 300, 5, spread=60.0)
     exact = Af @ Bf.T
     assert bool((S * (1 + 300 * 2.0 ** -21) + 300 * 2.0 ** -120 >= exact).all())
+
+
+@pytest.mark.parametrize("m,n,k", [(129, 257, 3), (1000, 64, 4096), (200, 130, 77)])
+def test_cross_and_bound_stay_inside_their_outputs(m, n, k):
+    """Guard zones after the m x n outputs of both diagnostics stay untouched
+    (the kernels' ragged-edge masks; split-K scratch is separate)."""
+    import torch
+    lda, ldb = m + (m & 1), k + (k & 1)
+    ah, al = _planes(m, k, lda, 9)
+    bh, bl = _planes(k, n, ldb, 10)
+    guard = 4096
+    x = torch.full((m * n + guard,), 12345.0, device="cuda", dtype=torch.float64)
+    rc = _lib.load().ddb_cross_terms(m, n, k, _ptr(ah), _ptr(al), lda, _ptr(bh), _ptr(bl), ldb,
+                                     _ptr(x), 0, None)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert bool((x[m * n:] == 12345.0).all()) and bool(torch.isfinite(x[:m * n]).all())
+    s = torch.full((m * n + guard,), 7.0, device="cuda", dtype=torch.float32)
+    re = torch.zeros(m + 64, device="cuda", dtype=torch.int32)
+    ce = torch.zeros(n + 64, device="cuda", dtype=torch.int32)
+    rc = _lib.load().ddb_abs_bound(b"N", b"N", m, n, k, _ptr(ah), lda, _ptr(bh), ldb, _ptr(re),
+                                   _ptr(ce), _ptr(s), None, None, None)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert bool((s[m * n:] == 7.0).all()) and bool((s[:m * n] >= 0).all())
+    assert bool((re[m:] == 0).all()) and bool((ce[n:] == 0).all())
