@@ -354,7 +354,14 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
     // reference's own axpy order (exact mode stays bitwise), for 'T' only in
     // the fast modes.  Later blocks find A resident and run full depth.
     const int64_t step = ((n + nblk - 1) / nblk + 63) / 64 * 64;
-    const int kch0 = (k >= 4096 && (na || mode != MODE_EXACT)) ? (k >= 8192 ? 8 : 4) : 1;
+    // (block 0's time ~ A_copy / P + compute + P * per-call cost; at
+    // k = 8192, P = 4 / 6 / 8 measured within 0.5 %; DDB_HOST_KPANELS overrides)
+    static const int kp_env = [] {
+      const char* v = std::getenv("DDB_HOST_KPANELS");
+      return v ? std::atoi(v) : 0;
+    }();
+    const int kch0 = (k >= 4096 && (na || mode != MODE_EXACT))
+                         ? (kp_env > 0 ? kp_env : (k >= 8192 ? 8 : 4)) : 1;
     // Fast modes also defer block 0's C columns: its early k panels
     // accumulate into a scratch T (beta = 0, then 1), the last panel applies
     // beta to C, and T is folded in with one add2 per element -- the first

@@ -392,7 +392,8 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
         double sx, ex;
         const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
         double lv = L[a][b];
-        if (ALG == ALG_SPLIT && split == 0) lv = dadd(lv, g.cross[gi + gj * g.m]);
+        if (ALG == ALG_SPLIT && split == 0 && g.cross != nullptr)
+          lv = dadd(lv, g.cross[gi + gj * g.m]);
         two_sum(hv, lv, sx, ex);
         if (g.part != nullptr) {
           double* ph = g.part + (size_t)split * 2 * g.m * g.n;
@@ -421,6 +422,41 @@ static int split_policy() {
 }
 
 }  // namespace tma
+
+// The concurrent split schedule's last step: C += alpha * X on the EC_FAST
+// elements (the uplo triangle for Rsyrk), X the cross terms (ld = m).  One
+// checked dd multiply and add per element (two roundings below 2^-104 |C|),
+// HBM-bound: ~40 bytes per element.
+__global__ void __launch_bounds__(256)
+cross_add_kernel(GemmArgs g, const double* __restrict__ x) {
+  const int64_t total = g.m * g.n, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int64_t i = t % g.m, j = t / g.m;
+    if (g.syrk == 1 && i > j) continue;
+    if (g.syrk == 2 && i < j) continue;
+    if (elem_class(g, i, j) != EC_FAST) continue;
+    const int64_t ci = i + j * g.ldc;
+    const dd out = add2_chk(dd{g.c_hi[ci], g.c_lo[ci]}, mul2_chk(g.alpha, dd{x[t], 0.0}));
+    g.c_hi[ci] = out.h;
+    g.c_lo[ci] = out.l;
+  }
+}
+
+// Second stream per host thread and device: the split schedule's cross
+// terms run there concurrently with the hi * hi kernel.
+static cudaError_t aux_stream(cudaStream_t* out) {
+  static thread_local cudaStream_t streams[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  if (streams[dev] == nullptr) {
+    e = cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+  }
+  *out = streams[dev];
+  return cudaSuccess;
+}
 
 // dst (cols x rows, ld ldd) = src (rows x cols, ld lds)^T, both planes: the
 // operand of a TMA Rsyrk that must be k-major / m-major (launch_tiled)
@@ -509,12 +545,36 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   const int splits = g.kchunk >= g.k ? 1 : (int)((g.k + g.kchunk - 1) / g.kchunk);
   auto pick = [&](auto c0, auto c1, auto c2) { return g.syrk == 1 ? c1 : (g.syrk == 2 ? c2 : c0); };
   GemmArgs ga = g;
+  // Concurrent schedule (no split-K): the cross-term kernel runs on a second
+  // stream alongside the hi * hi kernel -- each kernel's last partial wave
+  // is filled by the other's CTAs -- and a final HBM-bound pass adds
+  // alpha * X to C.  With split-K the partial sums take X in slice 0 instead
+  // (cross first, then the kernel).  DDB_CROSS_SERIAL=1: always the latter.
+  static const bool cross_serial = std::getenv("DDB_CROSS_SERIAL") != nullptr;
+  const bool concurrent = split_alg && splits == 1 && !cross_serial;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (split_alg) {
-    // the cross terms first: hand-written DMMA kernel (dd_cross.cu)
     int nl = 0;
-    cudaError_t e = launch_cross_dmma(g, xbuf, s, &nl, xslices, xchunk);
-    if (e != cudaSuccess) { cudaFreeAsync(xbuf, s); return e; }
-    ga.cross = xbuf;
+    cudaError_t e = cudaSuccess;
+    if (concurrent) {
+      e = aux_stream(&s2);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_fork, s);   // operands + xbuf ready
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s2, ev_fork, 0);
+      if (e == cudaSuccess) e = launch_cross_dmma(g, xbuf, s2, &nl, xslices, xchunk);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_join, s2);
+    } else {
+      e = launch_cross_dmma(g, xbuf, s, &nl, xslices, xchunk);
+      ga.cross = xbuf;
+    }
+    if (e != cudaSuccess) {
+      if (ev_fork) cudaEventDestroy(ev_fork);
+      if (ev_join) cudaEventDestroy(ev_join);
+      cudaFreeAsync(xbuf, s);
+      return e;
+    }
   }
   auto kern = split_alg ? pick(dd_tma_nn_kernel<ALG_SPLIT, 0>, dd_tma_nn_kernel<ALG_SPLIT, 1>,
                                dd_tma_nn_kernel<ALG_SPLIT, 2>)
@@ -541,6 +601,18 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   kern<<<grid, NTK, SMEM_BYTES, s>>>(ga, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
                                     tiles_n, splits);
   e = cudaGetLastError();
+  if (concurrent) {
+    const cudaError_t ej = cudaStreamWaitEvent(s, ev_join, 0);
+    if (e == cudaSuccess) e = ej;
+    if (e == cudaSuccess) {
+      int64_t blocks = (g.m * g.n + 255) / 256;
+      if (blocks > 16 * (int64_t)sms) blocks = 16 * (int64_t)sms;
+      cross_add_kernel<<<(unsigned)blocks, 256, 0, s>>>(ga, xbuf);
+      e = cudaGetLastError();
+    }
+    cudaEventDestroy(ev_fork);
+    cudaEventDestroy(ev_join);
+  }
   if (xbuf != nullptr) {
     const cudaError_t e2 = cudaFreeAsync(xbuf, s);
     if (e == cudaSuccess) e = e2;
