@@ -273,3 +273,22 @@ def test_one_nan_in_a_large_call_costs_little():
     assert bits_equal(cc.store[0][4321::n].cpu().numpy(), ref_c.store[0].cpu().numpy())
     assert bits_equal(cc.store[1][4321::n].cpu().numpy(), ref_c.store[1].cpu().numpy())
     assert torch.isfinite(cc.store[0][4322::n]).all()
+
+
+@pytest.mark.parametrize("k,s", [(65536, 48), (65536, 49), (131072, 47), (131072, 48)])
+def test_spread_at_the_limit_deep_k(monkeypatch, k, s):
+    """Right at the wide limit (2s = 112 - ceil(log2 k) stays on the certified
+    path, 2s + 2 takes the fallback) and at the deepest certified k, where the
+    accumulation factor (1 + k 2^-21) and the floor k 2^-120 are largest: the
+    split kernel must still be inside the c = 4 bound."""
+    monkeypatch.setenv("DDB_SPLIT", "2")
+    m, n = 24, 20
+    A, B = spread_operands(m, n, k, s, 77 + s)
+    C = random_dd(m, n, m, 5, 3)
+    alpha, beta = (1.5, 0.0), (0.5, 0.0)
+    a, b, c = dev(m, k, m, A), dev(k, n, k, B), dev(m, n, m, C)
+    Rgemm("N", "N", m, n, k, alpha[0], a, m, b, k, beta[0], c, m, mode="fast")
+    lim = 112 - int(np.ceil(np.log2(k)))
+    assert _lib.last_route() == (5 if 2 * s > lim else 1)
+    worst = _ratio(c, m, n, k, A, B, alpha, beta, C, [0, 7, 23], [0, 5, 19])
+    assert worst <= 1.0, worst
