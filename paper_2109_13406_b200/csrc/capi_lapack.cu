@@ -563,35 +563,40 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
   p.n = n; p.lda = lda; p.upper = upflag(uplo) == 'U';
   p.f64 = f64;
   p.a_hi = a_hi; p.a_lo = a_lo;
-  // workspace: info | D, d0 (dd vectors), rec (ib dd) | backup ('L') or S
-  // ('U'), n x n dd | 'U': the inner transposed panel (n x ib) and two outer
-  // ones (n x NB; block J's is read by the trailing update while J+1's is
-  // written)
+  // workspace: info | D, d0 (dd vectors), rec (MB dd: the middle panel's
+  // reciprocals) | backup ('L') or S ('U'), n x n dd | 'U': the middle
+  // diagonal block transposed (MB x MB), the middle transposed panel (n x
+  // MB, 3 levels only) and two outer ones (n x NB; block J's is read by the trailing update
+  // while J+1's is written)
   const size_t head = 256, vec = sizeof(double) * (size_t)n;
-  const size_t recb = ((sizeof(double) * 2 * (size_t)ib + 255) / 256) * 256;
+  const size_t recb = ((sizeof(double) * 2 * (size_t)MB + 255) / 256) * 256;
   const size_t full = sizeof(double) * (size_t)n * n;
-  const size_t t_in = p.upper ? (size_t)n * ib : 0, t_out = p.upper ? (size_t)n * NB : 0;
+  const size_t t_out = p.upper ? (size_t)n * NB : 0;
   const size_t t_mid = p.upper && MB < NB ? (size_t)n * MB : 0;
+  const size_t t_dg = p.upper ? (size_t)MB * MB : 0;
   const size_t ws_bytes =
-      head + 4 * vec + recb + 2 * full + sizeof(double) * 2 * (t_in + 2 * t_out + t_mid);
+      head + 4 * vec + recb + 2 * full + sizeof(double) * 2 * (2 * t_out + t_mid + t_dg);
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
   if (e != cudaSuccess) return fail(e, "workspace allocation");
   char* w = static_cast<char*>(ws);
   p.info = reinterpret_cast<int*>(w);
+  unsigned* pmask = reinterpret_cast<unsigned*>(w + 64);   // kPotrfMaxPanel / 32 words
   double* d = reinterpret_cast<double*>(w + head);
   p.dh = d; p.dl = d + n;
   double* d0h = d + 2 * n;
   double* d0l = d + 3 * n;
   p.d0_hi = d0h; p.d0_lo = d0l;
-  p.rec_hi = d + 4 * n; p.rec_lo = p.rec_hi + ib;
+  double* rec_h = d + 4 * n;
+  double* rec_l = rec_h + MB;
+  p.rec_hi = rec_h; p.rec_lo = rec_l;
   double* big = reinterpret_cast<double*>(w + head + 4 * vec + recb);
-  double* tin_h = big + 2 * (size_t)n * n;           // inner T: hi | lo
-  double* tin_l = tin_h + t_in;
-  double* tout_h = tin_l + t_in;                     // outer T: hi[2] | lo[2]
+  double* tout_h = big + 2 * (size_t)n * n;          // outer T: hi[2] | lo[2]
   double* tout_l = tout_h + 2 * t_out;
   double* tmid_h = tout_l + 2 * t_out;               // middle T: hi | lo
   double* tmid_l = tmid_h + t_mid;
+  double* tdg_h = tmid_l + t_mid;                    // 'U' diagonal block, transposed
+  double* tdg_l = tdg_h + t_dg;
   int nl = 0;
   e = cudaMemsetAsync(ws, 0, head + 2 * vec, s);
   const size_t dpitch = sizeof(double) * (size_t)(lda + 1);
@@ -659,24 +664,51 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
     ++nl;
     return launch_potrf_transpose(q, j0, j1, (int)(j1 - j0), n - j1, cs);
   };
-  // factor the middle panel [J0, J1): inner blocks, each followed by the
-  // update of the rest of the middle panel's columns
+  // factor the middle panel [J0, J1) (width <= 256): its diagonal block by
+  // inner blocks (diagonal kernel, the block's rows below the inner block,
+  // the update of the rest of the diagonal block), then every row below the
+  // middle panel against all of its columns in one potrf_rows_kernel launch
+  // -- per element the same products in the same l order as the blocked
+  // Rsyrk / Rgemm updates (exact mode stays bitwise)
   auto factor_mid = [&](int64_t J0, int64_t J1) -> int {
+    const int64_t sa = p.upper ? lda : 1, sb = p.upper ? 1 : lda;   // P(c2, c) strides in A
     for (int64_t i0 = J0; i0 < J1; i0 += ib) {
       const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
-      cudaError_t er = launch_potrf_diag(p, i0, i1, cs);
+      PotrfArgs q = p;
+      q.rec_hi = rec_h + (i0 - J0);
+      q.rec_lo = rec_l + (i0 - J0);
+      cudaError_t er = launch_potrf_diag(q, i0, i1, cs);
       ++nl;
-      if (er == cudaSuccess && i1 < n) {
-        er = launch_potrf_panel(p, i0, (int)(i1 - i0), n - i1, cs);
-        ++nl;
+      if (er == cudaSuccess && i1 < J1) {
+        const size_t o = (size_t)i0 + (size_t)i0 * lda;
+        const double* al = f64 ? nullptr : a_lo + o;
+        er = launch_potrf_rows(q, i0, (int)(i1 - i0), i1, J1, a_hi + o, al, sa, sb, q.rec_hi,
+                               q.rec_lo, nullptr, cs);
+        if (er == cudaSuccess) er = launch_potrf_blockupd(p, i0, i1, J1, cs);
+        nl += 2;
       }
       if (er != cudaSuccess) return fail(er, "rpotrf panel");
-      if (i1 < J1) {
-        if (p.upper && (er = transpose(i0, i1, tin_h, tin_l)) != cudaSuccess)
-          return fail(er, "rpotrf transpose");
-        const int r = update(i0, i1, i1, J1, tin_h, tin_l, i1, cs);
-        if (r != DDB_OK) return r;
+    }
+    if (J1 < n) {
+      const int wd = (int)(J1 - J0);
+      const double *ph, *pl;
+      int64_t sr = 1, sc = lda;
+      cudaError_t er = cudaSuccess;
+      if (p.upper) {                 // P(c2, c) = U(J0 + c, J0 + c2), read coalesced
+        PotrfArgs q = p;
+        q.t_hi = tdg_h;
+        q.t_lo = tdg_l;
+        er = launch_potrf_transpose(q, J0, J0, wd, wd, cs);
+        ++nl;
+        ph = tdg_h; pl = f64 ? nullptr : tdg_l; sc = wd;
+      } else {
+        const size_t o = (size_t)J0 + (size_t)J0 * lda;
+        ph = a_hi + o; pl = f64 ? nullptr : a_lo + o;
       }
+      if (er == cudaSuccess)
+        er = launch_potrf_rows(p, J0, wd, J1, n, ph, pl, sr, sc, rec_h, rec_l, pmask, cs);
+      nl += f64 ? 1 : 2;
+      if (er != cudaSuccess) return fail(er, "rpotrf panel");
     }
     return DDB_OK;
   };

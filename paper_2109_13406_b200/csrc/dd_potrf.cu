@@ -161,88 +161,205 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
   }
 }
 
-// Panel below ('L': rows q >= j1) / right of ('U': columns q >= j1) the
-// diagonal block.  Each q is independent: a group of G lanes owns it, lane t
-// holding the accumulators of block columns c = j0 + t + G*i.  Step c: the
-// owner finalises entry c (rec_c * acc, or rec_c * (A - acc) for 'U'),
-// broadcasts it, and every lane extends its later columns by one product --
-// the reference's per-element order (chol.py:50-64), with NPER independent
-// chains per lane.  The block's factor (strictly-lower part, transposed for
-// 'U') and the reciprocals sit in shared memory.
-constexpr int kPanelG = 32;          // lanes per row: one warp
-constexpr int kPanelThreads = 256;    // 8 rows per CTA
+// Factor rows below a factored diagonal block.  Rows q in [q0, q1) ('U':
+// columns of U) against the w <= 32 * NPER columns [j0, j0 + w): each q is an
+// independent recurrence, one warp per q, lane t holding the accumulators of
+// columns c = t + 32 i ("chain" i).  Step c: entry c is finalised (rec_c *
+// acc, or rec_c * (A - acc) for 'U'), broadcast, and every lane extends its
+// later columns by one product -- the reference's per-element order
+// (chol.py:50-64) and the same operation sequence the blocked path's Rsyrk /
+// Rgemm updates apply, so one launch covers a whole (up to 256-wide) panel.
+// The diagonal block's factor P(c2, c) = L(j0 + c2, j0 + c) ('U': U(j0 + c,
+// j0 + c2)) is read at ph[c2 * sr + c * sc] through L1 (the w x w block is
+// L2-resident) one step ahead of its use; the reciprocals sit in shared
+// memory.  The steps run in 32-step segments, one per chain, unrolled over
+// the chains: in segment s chains < s are finished and compiled out, chains >
+// s are fully live, so a 256-wide panel keeps ~89 % of the lanes busy with no
+// per-chain predicates.  Every lane forms rec_c * acc on its own chain-s
+// accumulator and the owner's is broadcast (no divergent owner branch).
+// Arithmetic (MODE): the check-free forms are bit-identical to the checked
+// ones inside the safe window (lapack_num.cuh: NumDD::win); RK_FAST when every
+// P row this warp reads is inside it (pmask, potrf_psafe_kernel) and so are
+// the starting accumulators and D -- then only the broadcast value is checked
+// per step; RK_CHECK checks every P entry at use (no mask: the narrow inner
+// panels); RK_SLOW the checked forms throughout.
+constexpr int kRowsThreads = 256;    // 8 rows per CTA
+#ifndef DDB_ROWS_MINB
+#define DDB_ROWS_MINB 2      // CTAs per SM the register allocation targets (2: 128 registers; 86.8 vs 89.4 ms)
+#endif
+#ifndef DDB_ROWS_SEL
+#define DDB_ROWS_SEL 0       // 1: the ordered-Fast2Sum add (fewer FP64 ops, more selects; 86.8 vs 86.0 ms)
+#endif
+enum RowsMode { RK_SLOW = 0, RK_CHECK = 1, RK_FAST = 2 };
 
-template <class N, int NPER>
-__global__ void __launch_bounds__(kPanelThreads)
-potrf_panel_kernel(PotrfArgs p, int64_t j0, int nb) {
+template <class N>
+__device__ __forceinline__ typename N::T rfadd(typename N::T x, typename N::T y) {
+  return DDB_ROWS_SEL ? N::fadd(x, y) : N::fadd2(x, y);
+}
+
+template <class N, int NPER, bool UP, int MODE>
+__device__ __forceinline__ void rows_steps(const PotrfArgs& p, int64_t j0, int w, int ncols, int64_t q,
+                                           const double* __restrict__ ph, const double* __restrict__ pl,
+                                           int sr, int sc, const typename N::T* rec_s,
+                                           typename N::T (&acc)[NPER], const typename N::T (&au)[NPER],
+                                           typename N::T& dq) {
   using T = typename N::T;
-  extern __shared__ double sm[];
-  // a failure inside this block's diagonal part still leaves the columns
-  // before it complete, as the reference does (chol.py:44-46)
-  int ncols = nb;
-  const int inf = *p.info;
-  if (inf != 0) {
-    if (inf - 1 < j0) return;
-    ncols = (int)(inf - 1 - j0);
-  }
-  const int64_t lda = p.lda, lds = p.lds;
-  const int64_t j1 = j0 + nb;
-  // packed strictly-lower triangle: T(c2, c) (c < c2) at off(c) + c2 - c - 1
-  const int ntri = nb * (nb - 1) / 2;
-  double* th = sm;
-  double* tl = sm + ntri;
-  double* rh = sm + 2 * ntri;
-  double* rl = rh + nb;
-  auto off = [nb](int c) { return c * (2 * nb - c - 1) / 2; };
-  for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
-    const int c2 = t % nb, c = t / nb;
-    if (c2 <= c) continue;
-    const int64_t x = p.upper ? (j0 + c) + (j0 + c2) * lda : (j0 + c2) + (j0 + c) * lda;
-    N::st(th, tl, off(c) + c2 - c - 1, N::ld(p.a_hi, p.a_lo, x));
-  }
-  for (int c = threadIdx.x; c < nb; c += blockDim.x) N::st(rh, rl, c, N::ld(p.rec_hi, p.rec_lo, c));
-  __syncthreads();
-  const int lane = threadIdx.x % kPanelG;
-  const int64_t q = j1 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPanelG;
-  if (q >= p.n) return;                 // whole warps exit together
-  T acc[NPER];
+  const int lane = threadIdx.x & 31;
+  const int64_t lda = p.lda;
+  T tn[NPER];
 #pragma unroll
-  for (int i = 0; i < NPER; ++i) {
-    const int c = lane + kPanelG * i;
-    acc[i] = N::zero();
-    if (c < nb) {
-      const int64_t x = p.upper ? q + (j0 + c) * lds : q + (j0 + c) * lda;
-      acc[i] = p.upper ? N::ld(p.s_hi, p.s_lo, x) : N::ld(p.a_hi, p.a_lo, x);
-    }
-  }
-  T dq = N::zero();
-  if (lane == 0) dq = N::ld(p.dh, p.dl, q);
-  for (int c = 0; c < ncols; ++c) {
-    const int owner = c % kPanelG, ic = c / kPanelG;
-    T v = N::zero();
-    if (lane == owner) {
-      T a = N::zero();
+  for (int i = 0; i < NPER; ++i) tn[i] = N::zero();
+  int off = lane * sr;                       // P(lane + 32 i, c) at off + 32 i sr
+  auto fetch = [&](int s) {                  // chains >= s of the step at column offset off
 #pragma unroll
-      for (int i = 0; i < NPER; ++i)
-        if (i == ic) a = acc[i];
-      const T rec = N::ld(rh, rl, c);
-      const int64_t x = p.upper ? (j0 + c) + q * lda : q + (j0 + c) * lda;
-      if (p.upper) a = N::add(N::ld(p.a_hi, p.a_lo, x), N::neg(a));
-      v = N::mul(rec, a);
-      N::st(p.a_hi, p.a_lo, x, v);
-    }
-    v = N::shfl(v, owner);
-    if (lane == 0) dq = N::add(dq, N::mul(v, v));
+    for (int i = 0; i < NPER; ++i)
+      if (i >= s && lane + 32 * i < w) tn[i] = N::ldg(ph, pl, off + 32 * i * sr);
+  };
+  if (ncols > 0) fetch(0);
 #pragma unroll
-    for (int i = 0; i < NPER; ++i) {
-      const int c2 = lane + kPanelG * i;
-      if (c2 > c && c2 < nb) {
-        const T t = N::ld(th, tl, off(c) + c2 - c - 1);
-        acc[i] = p.upper ? N::add(acc[i], N::mul(v, t)) : N::add(acc[i], N::mul(N::neg(t), v));
+  for (int s = 0; s < NPER; ++s) {
+    if (32 * s >= ncols) break;
+    const int cend = min(32, ncols - 32 * s);
+    for (int cc = 0; cc < cend; ++cc) {
+      const int c = 32 * s + cc;
+      T t[NPER];
+#pragma unroll
+      for (int i = s; i < NPER; ++i) t[i] = tn[i];
+      off += sc;
+      if (c + 1 < ncols) fetch(cc + 1 < 32 ? s : s + 1);
+      // finalise entry c: every lane forms it from its own chain-s
+      // accumulator, the owner's (lane cc) is broadcast and stored
+      const T a = UP ? N::add(au[s], N::neg(acc[s])) : acc[s];
+      const T v = N::shfl(N::mul(rec_s[c], a), cc);
+      if (lane == cc) N::st(p.a_hi, p.a_lo, UP ? (j0 + c) + q * lda : q + (j0 + c) * lda, v);
+      // extend the later columns.  Lanes whose chain-s column is already
+      // final (c2 <= c) and lanes past w update too: those accumulators are
+      // never read again, so no per-lane predicate is needed
+      if (MODE != RK_SLOW && N::win(v)) {           // warp-uniform
+        dq = rfadd<N>(dq, N::fmul(v, v));
+#pragma unroll
+        for (int i = s; i < NPER; ++i) {
+          if (MODE == RK_CHECK && !N::win(t[i]))
+            acc[i] = UP ? N::add(acc[i], N::mul(v, t[i])) : N::add(acc[i], N::mul(N::neg(t[i]), v));
+          else
+            acc[i] = UP ? rfadd<N>(acc[i], N::fmul(v, t[i])) : rfadd<N>(acc[i], N::fmul(N::neg(t[i]), v));
+        }
+      } else {
+        dq = N::add(dq, N::mul(v, v));
+#pragma unroll
+        for (int i = s; i < NPER; ++i)
+          acc[i] = UP ? N::add(acc[i], N::mul(v, t[i])) : N::add(acc[i], N::mul(N::neg(t[i]), v));
       }
     }
   }
+}
+
+template <class N, int NPER, bool UP>
+__global__ void __launch_bounds__(kRowsThreads, DDB_ROWS_MINB)
+potrf_rows_kernel(PotrfArgs p, int64_t j0, int w, int64_t q0, int64_t q1,
+                  const double* __restrict__ ph, const double* __restrict__ pl, int sr, int sc,
+                  const double* __restrict__ rh, const double* __restrict__ rl,
+                  const unsigned* __restrict__ pmask) {
+  using T = typename N::T;
+  __shared__ T rec_s[32 * NPER];
+  // a failure inside the diagonal block still leaves the columns before it
+  // complete, as the reference does (chol.py:44-46)
+  int ncols = w;
+  const int inf = *p.info;
+  if (inf != 0) {
+    if (inf - 1 < j0) return;
+    ncols = (int)min((int64_t)w, inf - 1 - j0);
+  }
+  for (int c = threadIdx.x; c < w; c += blockDim.x) rec_s[c] = N::ld(rh, rl, c);
+  __syncthreads();
+  const int64_t lda = p.lda, lds = p.lds;
+  const int lane = threadIdx.x & 31;
+  const int64_t q = q0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (q >= q1) return;                  // whole warps exit together
+  T acc[NPER], au[NPER];
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int c = lane + 32 * i;
+    acc[i] = N::zero();
+    au[i] = N::zero();
+    if (c < w) {
+      acc[i] = UP ? N::ld(p.s_hi, p.s_lo, q + (j0 + c) * lds) : N::ld(p.a_hi, p.a_lo, q + (j0 + c) * lda);
+      if (UP) au[i] = N::ld(p.a_hi, p.a_lo, (j0 + c) + q * lda);    // 'U': A(j0 + c, q)
+      ok &= N::win(acc[i]);
+      if (pmask != nullptr) ok &= (pmask[i] >> lane & 1u) != 0;
+    }
+  }
+  // D(q), the running pivot dot product, kept by every lane (same value)
+  T dq = N::ld(p.dh, p.dl, q);
+  ok &= N::win(dq);
+  const bool all_ok = __all_sync(0xffffffffu, ok);
+  if (N::kF64 || !all_ok)
+    rows_steps<N, NPER, UP, RK_SLOW>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
+  else if (pmask == nullptr)
+    rows_steps<N, NPER, UP, RK_CHECK>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
+  else
+    rows_steps<N, NPER, UP, RK_FAST>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
   if (lane == 0) N::st(p.dh, p.dl, q, dq);
+}
+
+// Window mask of the w x w factor block P (potrf_rows_kernel): bit r % 32 of
+// mask[r / 32] set when every P(r, c), c < r, is inside the safe window.  One
+// warp per row, 32 rows per CTA.
+__global__ void __launch_bounds__(1024)
+potrf_psafe_kernel(const double* __restrict__ ph, const double* __restrict__ pl, int w, int sr,
+                   int sc, unsigned* __restrict__ mask) {
+  const int lane = threadIdx.x & 31, r = blockIdx.x * 32 + threadIdx.x / 32;
+  bool ok = true;
+  if (r < w)
+    for (int c = lane; c < r; c += 32) ok &= NumDD::win(NumDD::ldg(ph, pl, (int64_t)r * sr + (int64_t)c * sc));
+  ok = __all_sync(0xffffffffu, ok);
+  __shared__ unsigned word;
+  if (threadIdx.x == 0) word = 0;
+  __syncthreads();
+  if (lane == 0 && ok) atomicOr(&word, 1u << (threadIdx.x / 32));
+  __syncthreads();
+  if (threadIdx.x == 0) mask[blockIdx.x] = word;
+}
+
+// Trailing update of the diagonal block [i1, j1)^2 by the factored inner
+// block [i0, i1) (<= 64 columns): entries i1 <= c < q < j1, one thread each,
+// products in l order -- what Rsyrk('L', 'N') applies there in the blocked
+// path ('L': A(q, c) += (-L(c, l)) L(q, l) in place; 'U': S(q, c) += U(l, q)
+// U(l, c)).  The CTA's 32 rows and 8 columns of the inner block's factor are
+// staged in shared memory first.  Diagonal entries are not updated: pivots
+// come from D.
+template <class N>
+__global__ void __launch_bounds__(256)
+potrf_blockupd_kernel(PotrfArgs p, int64_t i0, int64_t i1, int64_t j1) {
+  using T = typename N::T;
+  __shared__ T fq[kPotrfMaxNb][33], fc[kPotrfMaxNb][8];
+  if (*p.info != 0) return;
+  const int64_t qb = i1 + (int64_t)blockIdx.x * 32, cb = i1 + (int64_t)blockIdx.y * 8;
+  if (cb >= qb + 31) return;                       // tile strictly above the diagonal
+  const int kb = (int)(i1 - i0);
+  const int64_t lda = p.lda;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // F(x, l) = L(x, i0 + l) ('L') / U(i0 + l, x) ('U')
+  auto f = [&](int64_t x, int l) {
+    return p.upper ? N::ld(p.a_hi, p.a_lo, (i0 + l) + x * lda) : N::ld(p.a_hi, p.a_lo, x + (i0 + l) * lda);
+  };
+  for (int l = ty; l < kb; l += 8) {
+    if (qb + tx < j1) fq[l][tx] = f(qb + tx, l);
+    if (tx < 8 && cb + tx < j1) fc[l][tx] = f(cb + tx, l);
+  }
+  __syncthreads();
+  const int64_t q = qb + tx, c = cb + ty;
+  if (q >= j1 || c >= q) return;
+  if (!p.upper) {
+    T acc = N::ld(p.a_hi, p.a_lo, q + c * lda);
+    for (int l = 0; l < kb; ++l) acc = N::add(acc, N::mul(N::neg(fc[l][ty]), fq[l][tx]));
+    N::st(p.a_hi, p.a_lo, q + c * lda, acc);
+  } else {
+    T acc = N::ld(p.s_hi, p.s_lo, q + c * p.lds);
+    for (int l = 0; l < kb; ++l) acc = N::add(acc, N::mul(fq[l][tx], fc[l][ty]));
+    N::st(p.s_hi, p.s_lo, q + c * p.lds, acc);
+  }
 }
 
 // T(r, l) = U(j0 + l, j1 + r), r < rows, l < nb  (ld = rows)
@@ -304,30 +421,54 @@ cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaSt
 }
 
 template <class N, int NPER>
-static cudaError_t panel_launch(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
-                                cudaStream_t s) {
-  const size_t smem = sizeof(double) * ((size_t)nb * (nb - 1) + 2 * (size_t)nb);
-  static thread_local int attr_dev = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (attr_dev != dev) {
-    cudaFuncSetAttribute(potrf_panel_kernel<N, NPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr_dev = dev;
-  }
-  const int64_t threads = rows * kPanelG;
-  potrf_panel_kernel<N, NPER><<<(unsigned)((threads + kPanelThreads - 1) / kPanelThreads),
-                                kPanelThreads, smem, s>>>(p, j0, nb);
+static cudaError_t rows_launch(const PotrfArgs& p, int64_t j0, int w, int64_t q0, int64_t q1,
+                               const double* ph, const double* pl, int sr, int sc,
+                               const double* rh, const double* rl, const unsigned* pmask,
+                               cudaStream_t s) {
+  const int64_t threads = (q1 - q0) * 32;
+  const unsigned grid = (unsigned)((threads + kRowsThreads - 1) / kRowsThreads);
+  if (p.upper)
+    potrf_rows_kernel<N, NPER, true><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc,
+                                                                   rh, rl, pmask);
+  else
+    potrf_rows_kernel<N, NPER, false><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc,
+                                                                    rh, rl, pmask);
   return cudaGetLastError();
 }
 
-cudaError_t launch_potrf_panel(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
-                               cudaStream_t s) {
-  if (rows <= 0) return cudaSuccess;
-  const int nper = (nb + kPanelG - 1) / kPanelG;
-  (void)nper;   // nb <= 64 = 2 * kPanelG
-  return p.f64 ? panel_launch<NumF64, 2>(p, j0, nb, rows, s)
-               : panel_launch<NumDD, 2>(p, j0, nb, rows, s);
+template <class N>
+static cudaError_t rows_dispatch(const PotrfArgs& p, int64_t j0, int w, int64_t q0, int64_t q1,
+                                 const double* ph, const double* pl, int sr, int sc,
+                                 const double* rh, const double* rl, const unsigned* pmask,
+                                 cudaStream_t s) {
+  if (w <= 64) return rows_launch<N, 2>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask, s);
+  if (w <= 128) return rows_launch<N, 4>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask, s);
+  return rows_launch<N, 8>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask, s);
+}
+
+cudaError_t launch_potrf_rows(const PotrfArgs& p, int64_t j0, int w, int64_t q0, int64_t q1,
+                              const double* ph, const double* pl, int64_t sr, int64_t sc,
+                              const double* rh, const double* rl, unsigned* pmask, cudaStream_t s) {
+  if (q1 <= q0 || w <= 0) return cudaSuccess;
+  // P offsets are 32-bit: the w x w block spans < 2^31 elements
+  if (w > kPotrfMaxPanel || (w - 1) * (sr + sc) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  if (pmask != nullptr && !p.f64) {
+    potrf_psafe_kernel<<<(w + 31) / 32, 1024, 0, s>>>(ph, pl, w, (int)sr, (int)sc, pmask);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return p.f64 ? rows_dispatch<NumF64>(p, j0, w, q0, q1, ph, pl, (int)sr, (int)sc, rh, rl, nullptr, s)
+               : rows_dispatch<NumDD>(p, j0, w, q0, q1, ph, pl, (int)sr, (int)sc, rh, rl, pmask, s);
+}
+
+cudaError_t launch_potrf_blockupd(const PotrfArgs& p, int64_t i0, int64_t i1, int64_t j1,
+                                  cudaStream_t s) {
+  const int64_t m = j1 - i1;
+  if (m <= 1) return cudaSuccess;
+  dim3 grid((unsigned)((m + 31) / 32), (unsigned)((m + 7) / 8));
+  if (p.f64) potrf_blockupd_kernel<NumF64><<<grid, dim3(32, 8), 0, s>>>(p, i0, i1, j1);
+  else potrf_blockupd_kernel<NumDD><<<grid, dim3(32, 8), 0, s>>>(p, i0, i1, j1);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,

@@ -186,14 +186,21 @@ struct PotrfArgs {
   int64_t lds;
   double *t_hi, *t_lo;          // upper: the transposed panel U12^T
   const double *b_hi, *b_lo;    // lower: backup of the input (ld = n)
-  double *rec_hi, *rec_lo;      // the current block's pivot reciprocals
+  double *rec_hi, *rec_lo;      // the current inner block's pivot reciprocals
   int* info;                    // device: first failing pivot + 1, or 0
 };
 
-constexpr int kPotrfMaxNb = 64;
+constexpr int kPotrfMaxNb = 64;       // diagonal block (shared memory)
+constexpr int kPotrfMaxPanel = 256;   // columns per potrf_rows_kernel launch
 cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaStream_t s);
-cudaError_t launch_potrf_panel(const PotrfArgs& p, int64_t j0, int nb, int64_t rows,
-                               cudaStream_t s);
+// rows [q0, q1) against the factored w-column block at j0 (dd_potrf.cu);
+// pmask (w / 32 words of scratch, or null): check the block against the safe
+// window once up front instead of per step
+cudaError_t launch_potrf_rows(const PotrfArgs& p, int64_t j0, int w, int64_t q0, int64_t q1,
+                              const double* ph, const double* pl, int64_t sr, int64_t sc,
+                              const double* rh, const double* rl, unsigned* pmask, cudaStream_t s);
+cudaError_t launch_potrf_blockupd(const PotrfArgs& p, int64_t i0, int64_t i1, int64_t j1,
+                                  cudaStream_t s);
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,
                                    int64_t rows, cudaStream_t s);
 cudaError_t launch_potrf_restore(const PotrfArgs& p, cudaStream_t s);

@@ -120,7 +120,22 @@ struct NumDD {
   __device__ static T ldcg(const double* h, const double* l, int64_t i) {
     return dd{__ldcg(h + i), __ldcg(l + i)};
   }
+  __device__ static T ldg(const double* h, const double* l, int64_t i) {
+    return dd{__ldg(h + i), __ldg(l + i)};
+  }
   __device__ static void st(double* h, double* l, int64_t i, T v) { h[i] = v.h; l[i] = v.l; }
+  // the prescan's safe window (dd_prescan.cu): hi zero or 2^-300 <= |hi| <
+  // 2^301, lo finite below 2^301.  For operands inside it (and accumulators
+  // that started inside it and took at most a few thousand such products)
+  // fadd / fmul are bit-identical to add / mul (dd_arith.cuh)
+  __device__ static bool win(T x) {
+    const int eh = (int)((__double_as_longlong(x.h) >> 52) & 0x7ff);
+    const int el = (int)((__double_as_longlong(x.l) >> 52) & 0x7ff);
+    return (eh >= WIN_LO || (__double_as_longlong(x.h) << 1) == 0) && eh <= WIN_HI && el <= WIN_HI;
+  }
+  __device__ static T fadd(T x, T y) { return add2_nc_sel(x, y); }
+  __device__ static T fadd2(T x, T y) { return add2_nc(x, y); }
+  __device__ static T fmul(T x, T y) { return mul2_nc(x, y); }
   __device__ static T zero() { return dd{0.0, 0.0}; }
   __device__ static T one() { return dd{1.0, 0.0}; }
   __device__ static T neg(T x) { return lap::neg2(x); }
@@ -161,7 +176,12 @@ struct NumF64 {
   static constexpr bool kF64 = true;
   __device__ static T ld(const double* h, const double*, int64_t i) { return h[i]; }
   __device__ static T ldcg(const double* h, const double*, int64_t i) { return __ldcg(h + i); }
+  __device__ static T ldg(const double* h, const double*, int64_t i) { return __ldg(h + i); }
   __device__ static void st(double* h, double*, int64_t i, T v) { h[i] = v; }
+  __device__ static bool win(T) { return true; }
+  __device__ static T fadd(T x, T y) { return dadd(x, y); }
+  __device__ static T fadd2(T x, T y) { return dadd(x, y); }
+  __device__ static T fmul(T x, T y) { return dmul(x, y); }
   __device__ static T zero() { return 0.0; }
   __device__ static T one() { return 1.0; }
   __device__ static T neg(T x) { return -x; }
