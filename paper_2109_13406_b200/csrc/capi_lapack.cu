@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -41,6 +42,41 @@ int syrk_any(bool f64, char uplo, char trans, int64_t n, int64_t k, double alpha
 }
 
 // ---- triangular solve (dd_trsm.cu) -------------------------------------------
+
+// DDB_LAPACK_TRACE=1: a CUDA-event timeline of a blocked driver's streams,
+// printed to stderr when the call finishes (diagnostics only: timing events)
+struct Trace {
+  bool on = false;
+  cudaEvent_t t0 = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<const char*> what;
+  std::vector<int64_t> tag;
+  explicit Trace(cudaStream_t s) {
+    const char* v = std::getenv("DDB_LAPACK_TRACE");
+    on = v != nullptr && v[0] == '1';
+    if (on && cudaEventCreate(&t0) == cudaSuccess) cudaEventRecord(t0, s);
+  }
+  void mark(const char* w, int64_t j, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    ev.push_back(e);
+    what.push_back(w);
+    tag.push_back(j);
+  }
+  ~Trace() {
+    if (!on) return;
+    for (size_t i = 0; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventSynchronize(ev[i]);
+      cudaEventElapsedTime(&ms, t0, ev[i]);
+      std::fprintf(stderr, "trace %9.3f %-12s %lld\n", ms, what[i], (long long)tag[i]);
+      cudaEventDestroy(ev[i]);
+    }
+    cudaEventDestroy(t0);
+  }
+};
 
 }  // namespace
 
@@ -617,6 +653,7 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
         e = cudaMemcpy2DAsync(bl, row, a_lo, pitch, row, n, cudaMemcpyDeviceToDevice, s);
     }
   }
+  Trace tr(s);
   // Streams: the panel work (diagonal blocks, panels, inner updates and the
   // lookahead update of the next block column) runs on a high-priority
   // stream `cs`; the bulk trailing update of each outer block runs on the
@@ -689,6 +726,7 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
       }
       if (er != cudaSuccess) return fail(er, "rpotrf panel");
     }
+    tr.mark("diagblk_done", J0, cs);
     if (J1 < n) {
       const int wd = (int)(J1 - J0);
       const double *ph, *pl;
@@ -733,6 +771,7 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
   if (e == cudaSuccess) e = cudaEventRecord(ev_a, s);      // workspace ready
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_a, 0);
   if (e == cudaSuccess) rc2 = factor_outer(0, NB < n ? NB : n);
+  tr.mark("panel_done", 0, cs);
   bool have_rest = false;
   for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
     const int64_t J1 = J0 + NB < n ? J0 + NB : n;
@@ -746,14 +785,19 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
     if (e != cudaSuccess) break;
     if (J2 < n) {
+      tr.mark("rest_start", J0, s);
       rc2 = update(J0, J1, J2, n, th, tl, J1, s);           // rest(J)
       if (rc2 != DDB_OK) break;
+      tr.mark("rest_done", J0, s);
       e = cudaEventRecord(ev_b, s);
       have_rest = true;
       if (e != cudaSuccess) break;
     }
+    tr.mark("upd_start", J0, cs);
     rc2 = update(J0, J1, J1, J2, th, tl, J1, cs);            // update(J -> J+1)
+    tr.mark("upd_done", J0, cs);
     if (rc2 == DDB_OK) rc2 = factor_outer(J1, J2);
+    tr.mark("panel_done", J1, cs);
   }
   // join the panel stream back into `s`
   if (cs != nullptr) {

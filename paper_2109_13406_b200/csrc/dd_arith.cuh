@@ -63,6 +63,17 @@ __device__ __forceinline__ void two_prod_fma(double a, double b, double& p, doub
   e = dfma(a, b, -p);
 }
 
+// Dekker's product with the FMA residual where the two agree bit for bit:
+// both factors non-zero with 2^-300 <= |x| < 2^301 (biased exponents 723 ..
+// 1323), so no split product under- or overflows and both residuals are the
+// exact a*b - p (+0 when zero).  Elsewhere Dekker's, as the reference.
+__device__ __forceinline__ void two_prod_g(double a, double b, double& p, double& e) {
+  const unsigned ea = (unsigned)((__double_as_longlong(a) >> 52) & 0x7ff) - 723u;
+  const unsigned eb = (unsigned)((__double_as_longlong(b) >> 52) & 0x7ff) - 723u;
+  if (ea <= 600u && eb <= 600u) two_prod_fma(a, b, p, e);
+  else two_prod_dekker(a, b, p, e);
+}
+
 // elem.py:54-66 (accurate add; only s0 = xh + yh is checked)
 __device__ __forceinline__ dd add2_chk(dd x, dd y) {
   double s0 = dadd(x.h, y.h);
@@ -80,7 +91,7 @@ __device__ __forceinline__ dd add2_chk(dd x, dd y) {
 // elem.py:69-78
 __device__ __forceinline__ dd mul2_chk(dd x, dd y) {
   double p, e;
-  two_prod_dekker(x.h, y.h, p, e);
+  two_prod_g(x.h, y.h, p, e);
   bool bad = !(finite_(p) && finite_(e));
   e = dadd(e, dadd(dmul(x.h, y.l), dmul(x.l, y.h)));
   double rh, rl;

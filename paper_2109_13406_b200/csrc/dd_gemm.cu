@@ -5,6 +5,7 @@
 //                            DDB_FAST_ALG=twosum|select overrides, for measurement)
 //   twosum   -> ALG_TWOSUM  (error-bounded without the bound GEMM)
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -69,7 +70,7 @@ static int sm_count() {
 // mostly empty (e.g. m = n = 2048, k = 65536: 512 tiles on 148 SMs).
 int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk) {
   *kchunk = g.k;
-  if (alg == ALG_EXACT || g.k < 1024) return 1;
+  if (alg == ALG_EXACT || g.k < 192) return 1;
   const int bm = tile_cfg() == 1 ? 64 : 128, bn = 64;
   const int64_t tm = (g.m + bm - 1) / bm, tn = (g.n + bn - 1) / bn;
   int64_t tiles = 0;
@@ -83,6 +84,23 @@ int choose_ksplit(const GemmArgs& g, int alg, int64_t* kchunk) {
       }
   }
   const int sms = sm_count();
+  // latency regime (the LAPACK consumers' narrow updates): under half a wave
+  // of tiles, so one tile's k-loop is the whole call -- cut k into up to
+  // sms / tiles slices of >= 96 (Rpotrf n = 8192: 256 x 256 x 256 updates)
+  if (tiles * 2 <= sms) {
+    const int64_t want = std::min<int64_t>(sms / std::max<int64_t>(tiles, 1), (g.k + 95) / 96);
+    if (want >= 2) {
+      int64_t chunk = (g.k + want - 1) / want;
+      chunk = ((chunk + 95) / 96) * 96;
+      const int real = (int)((g.k + chunk - 1) / chunk);
+      if (real >= 2) {
+        *kchunk = chunk;
+        return real;
+      }
+    }
+    return 1;
+  }
+  if (g.k < 1024) return 1;
   auto eff = [&](int64_t t) {
     const double waves = (double)t / sms;
     return waves / std::ceil(waves);

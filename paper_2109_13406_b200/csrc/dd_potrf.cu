@@ -49,13 +49,27 @@ namespace ddb {
 // l order.  X(q, c) (q > c) is the block entry the factor overwrites: A(q, c)
 // for 'L', A(c, q) for 'U'; for 'U' the running dot products S(q, c) are
 // staged too.  The reciprocals go to p.rec for the panel kernel.
+// The pivot chain (thread 0: sqrt and reciprocal, the reference's scalar
+// forms) is the kernel's critical path, so the trailing updates run on the
+// warps of the other three SM sub-partitions (warp w on w % 4) and leave
+// warp 0's FP64 pipe to it; while the block stays inside the safe window
+// (checked at load, then every new column value) they use the check-free
+// forms, bit-identical there.
+#ifdef DDB_DIAG_TIMING
+// diagnostics build only: per-step clock64 stamps of the last diagonal block
+__device__ long long g_diag_t[64][5];
+#define DIAG_T(j, k) (g_diag_t[j][k] = clock64())
+#else
+#define DIAG_T(j, k) ((void)0)
+#endif
+
 template <class N>
 __global__ void __launch_bounds__(512)
 potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
   using T = typename N::T;
   extern __shared__ double sm[];
   __shared__ T rec_s;
-  __shared__ int ok_s;
+  __shared__ int ok_s, nc_s;
   if (*p.info != 0) return;
   const int64_t lda = p.lda, lds = p.lds;
   const int sq = nb * nb;
@@ -67,17 +81,29 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
   double* dl = dh + nb;
   double* d0h = dl + nb;
   double* d0l = d0h + nb;
+  bool win = true;
   for (int t = threadIdx.x; t < sq; t += blockDim.x) {
     const int q = t % nb, c = t / nb;
     if (q <= c) continue;
     const int64_t x = p.upper ? (j0 + c) + (j0 + q) * lda : (j0 + q) + (j0 + c) * lda;
-    N::st(xh, xl, t, N::ld(p.a_hi, p.a_lo, x));
-    if (p.upper) N::st(sh, sl, t, N::ld(p.s_hi, p.s_lo, (j0 + q) + (j0 + c) * lds));
+    const T xv = N::ld(p.a_hi, p.a_lo, x);
+    N::st(xh, xl, t, xv);
+    win &= N::win(xv);
+    if (p.upper) {
+      const T sv = N::ld(p.s_hi, p.s_lo, (j0 + q) + (j0 + c) * lds);
+      N::st(sh, sl, t, sv);
+      win &= N::win(sv);
+    }
   }
   for (int t = threadIdx.x; t < nb; t += blockDim.x) {
-    N::st(dh, dl, t, N::ld(p.dh, p.dl, j0 + t));
+    const T dv = N::ld(p.dh, p.dl, j0 + t);
+    N::st(dh, dl, t, dv);
     N::st(d0h, d0l, t, N::ld(p.d0_hi, p.d0_lo, j0 + t));
+    win &= N::win(dv);
   }
+  if (threadIdx.x == 0) nc_s = 1;
+  win = __syncthreads_and(win) && !N::kF64;
+  if (threadIdx.x == 0) nc_s = win;
   __syncthreads();
   // thread 0 computes pivot j+1 while warps 1.. run step j's trailing
   // update (pivot j+1 needs only D(j+1), final after step j's column phase)
@@ -100,6 +126,7 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
     if (!ok_s) break;
+    if (threadIdx.x == 0) DIAG_T(j, 0);
     const T rec = rec_s;
     for (int q = j + 1 + threadIdx.x; q < nb; q += blockDim.x) {
       const int t = q + j * nb;
@@ -107,19 +134,27 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
       if (p.upper) a = N::add(a, N::neg(N::ld(sh, sl, t)));
       const T v = N::mul(rec, a);
       N::st(xh, xl, t, v);
-      N::st(dh, dl, q, N::add(N::ld(dh, dl, q), N::mul(v, v)));
+      const bool f = nc_s && N::win(v);
+      if (!f) nc_s = 0;
+      const T d = N::ld(dh, dl, q);
+      N::st(dh, dl, q, f ? N::fadd2(d, N::fmul(v, v)) : N::add(d, N::mul(v, v)));
     }
     __syncthreads();
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) {
+      DIAG_T(j, 1);
       if (j + 1 < nb) pivot(j + 1);
-    } else if (threadIdx.x >= 32) {
+      DIAG_T(j, 2);
+    } else if ((warp & 3) != 0) {
       // pairs (q, c), j < c < q < nb, enumerated column by column; batches
       // of kB independent updates (operands gathered before any store)
       const int rem = nb - j - 1;
       const int npairs = rem * (rem - 1) / 2;
       constexpr int kB = 4;
-      const int nthr = blockDim.x - 32;
-      for (int base = threadIdx.x - 32; base < npairs; base += nthr * kB) {
+      const int nthr = (nw - (nw + 3) / 4) * 32;                  // warps not on sub-partition 0
+      const int me = (warp - warp / 4 - 1) * 32 + (threadIdx.x & 31);
+      const bool fast = nc_s;
+      for (int base = me; base < npairs; base += nthr * kB) {
         int xs[kB];
         T acc[kB], f1[kB], f2[kB];
 #pragma unroll
@@ -142,13 +177,15 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
           if (xs[b] < 0) continue;
-          const T r = N::add(acc[b], N::mul(f1[b], f2[b]));
+          const T r = fast ? N::fadd2(acc[b], N::fmul(f1[b], f2[b])) : N::add(acc[b], N::mul(f1[b], f2[b]));
           if (!p.upper) N::st(xh, xl, xs[b], r);
           else N::st(sh, sl, xs[b], r);
         }
       }
+      if (threadIdx.x == 32) DIAG_T(j, 3);
     }
     __syncthreads();
+    if (threadIdx.x == 0) DIAG_T(j, 4);
   }
   // write the block back ('U': the untouched part is written back unchanged;
   // 'L': entries the reference would not have touched yet are restored from
@@ -401,6 +438,12 @@ potrf_restore_kernel(PotrfArgs p) {
     if (!p.f64) p.a_lo[i + c * p.lda] = p.b_lo[i + c * p.n];
   }
 }
+
+#ifdef DDB_DIAG_TIMING
+extern "C" int ddb_debug_diag_timing(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_diag_t, sizeof(g_diag_t));
+}
+#endif
 
 cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaStream_t s) {
   const int nb = (int)(j1 - j0);

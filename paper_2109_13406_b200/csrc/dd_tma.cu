@@ -377,36 +377,96 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
       if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     }
 
-    // epilogue (as dd_tiled.cuh's fast modes)
+    // epilogue (as dd_tiled.cuh's fast modes).  The routing words, the cross
+    // terms and C are loaded for all of the thread's elements before any
+    // arithmetic, so their global round trips overlap instead of running one
+    // element after another (that serial chain was ~30 % of a tile at k = 256)
     const int split = u / tiles;
+    int rsv[TM], csv[TNK];
+#pragma unroll
+    for (int a = 0; a < TM; ++a) {
+      const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+      rsv[a] = g.rsp != nullptr && gi < g.m ? g.rsp[gi] : 0;
+    }
+#pragma unroll
+    for (int b = 0; b < TNK; ++b) {
+      const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+      csv[b] = g.rsp != nullptr && gj < g.n ? g.csp[gj] : 0;
+    }
+    uint64_t mine = 0;   // bit a * TNK + b: this launch writes the element
 #pragma unroll
     for (int a = 0; a < TM; ++a)
 #pragma unroll
       for (int b = 0; b < TNK; ++b) {
         const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
         const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-        if (gi >= g.m || gj >= g.n) continue;
-        if (SYRK == 1 && gi > gj) continue;   // the uplo triangle only (level23.py:245-270)
-        if (SYRK == 2 && gi < gj) continue;
-        if (!elem_mine(g, gi, gj)) continue;   // routed elsewhere (internal.h: elem_class)
-        double sx, ex;
-        const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
-        double lv = L[a][b];
-        if (ALG == ALG_SPLIT && split == 0 && g.cross != nullptr)
-          lv = dadd(lv, g.cross[gi + gj * g.m]);
-        two_sum(hv, lv, sx, ex);
-        if (g.part != nullptr) {
+        bool ok = gi < g.m && gj < g.n;
+        if (SYRK == 1) ok &= gi <= gj;   // the uplo triangle only (level23.py:245-270)
+        if (SYRK == 2) ok &= gi >= gj;
+        if (g.rsp != nullptr) {          // elem_mine (internal.h) on the preloaded words
+          const int v = rsv[a] + csv[b];
+          const int cls = v >= SPREAD_BAD ? EC_REF : (g.wide_lim > 0 && v > g.wide_lim ? EC_WIDE : EC_FAST);
+          ok &= cls == (g.only_wide ? EC_WIDE : EC_FAST);
+        }
+        mine |= ok ? uint64_t(1) << (a * TNK + b) : uint64_t(0);
+      }
+    if (ALG == ALG_SPLIT && split == 0 && g.cross != nullptr) {
+#pragma unroll
+      for (int a = 0; a < TM; ++a) {
+        double xv[TNK];
+#pragma unroll
+        for (int b = 0; b < TNK; ++b) {
+          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+          xv[b] = (mine >> (a * TNK + b) & 1) ? g.cross[gi + gj * g.m] : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < TNK; ++b) L[a][b] = dadd(L[a][b], xv[b]);
+      }
+    }
+    if (g.part != nullptr) {
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TNK; ++b) {
+          if (!(mine >> (a * TNK + b) & 1)) continue;
+          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+          double sx, ex;
+          const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
+          two_sum(hv, L[a][b], sx, ex);
           double* ph = g.part + (size_t)split * 2 * g.m * g.n;
           ph[gi + gj * g.m] = sx;
           ph[(size_t)g.m * g.n + gi + gj * g.m] = ex;
-          continue;
         }
+      continue;
+    }
+    // C in batches of one row pair's TNK elements (registers: H and L stay live)
+#pragma unroll
+    for (int a = 0; a < TM; ++a) {
+      double ch[TNK], cl[TNK];
+#pragma unroll
+      for (int b = 0; b < TNK; ++b) {
+        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+        const bool m = mine >> (a * TNK + b) & 1;
+        ch[b] = m ? g.c_hi[gi + gj * g.ldc] : 0.0;
+        cl[b] = m ? g.c_lo[gi + gj * g.ldc] : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < TNK; ++b) {
+        if (!(mine >> (a * TNK + b) & 1)) continue;
+        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+        double sx, ex;
+        const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
+        two_sum(hv, L[a][b], sx, ex);
         const int64_t ci = gi + gj * g.ldc;
-        const dd out = add2_chk(mul2_chk(g.alpha, dd{sx, ex}),
-                                scale_beta(g.beta, dd{g.c_hi[ci], g.c_lo[ci]}));
+        const dd out = add2_chk(mul2_chk(g.alpha, dd{sx, ex}), scale_beta(g.beta, dd{ch[b], cl[b]}));
         g.c_hi[ci] = out.h;
         g.c_lo[ci] = out.l;
       }
+    }
   }
 }
 

@@ -34,7 +34,7 @@ static __device__ dd add2_s(dd x, dd y) {
 // _mul21 (ddarith.py:103-110): dd * double
 static __device__ dd mul21_s(dd x, double y) {
   double p, e;
-  two_prod_dekker(x.h, y, p, e);
+  two_prod_g(x.h, y, p, e);
   if (!(isfin(p) && isfin(e))) return canon(p, 0.0);
   e = dadd(e, dmul(x.l, y));
   double s, t;
@@ -79,7 +79,7 @@ static __device__ dd sqrt2_s(dd v) {
   const double x = 1.0 / sqrt(h);
   const double ax = dmul(h, x);
   double p, e;
-  two_prod_dekker(ax, ax, p, e);
+  two_prod_g(ax, ax, p, e);
   const dd r = add2_s(dd{h, l}, dd{-p, -e});
   double s, e2;
   quick_two_sum(ax, dmul(r.h, dmul(x, 0.5)), s, e2);
@@ -92,7 +92,7 @@ static __device__ dd sqrt2_s(dd v) {
 // the scalar _div2
 static __device__ dd v_mul21(dd y, double q) {
   double p, e;
-  two_prod_dekker(y.h, q, p, e);
+  two_prod_g(y.h, q, p, e);
   const bool bad = !(isfin(p) && isfin(e));
   e = dadd(e, dmul(y.l, q));
   double s, t;

@@ -1,0 +1,7 @@
+python scripts/syrk_k.py 8192 256
+python scripts/syrk_k.py 4096 256
+python scripts/syrk_k.py 8192 64
+python scripts/shape_time.py 7680 256 256 fast N T
+python scripts/shape_time.py 2048 256 256 fast N T
+python scripts/shape_time.py 8192 8192 8192 fast
+python scripts/potrf_time.py 8192 256,512 fast
