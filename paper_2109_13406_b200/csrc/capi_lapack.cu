@@ -323,6 +323,7 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
   if (e == cudaSuccess) e = panel_stream(&cs);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_a, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_b, cudaEventDisableTiming);
+  Trace tr(s);
   auto gemm = [&](int64_t r0, int64_t r1, int64_t c0, int64_t c1, int64_t l0, int64_t l1,
                   cudaStream_t st) -> int {   // A(r0:r1, c0:c1) += A(r0:r1, l0:l1) (-A(l0:l1, c0:c1))
     if (r1 <= r0 || c1 <= c0 || l1 <= l0) return DDB_OK;
@@ -363,6 +364,7 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
       const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
       cudaError_t er = launch_getrf_panel(g, i0, (int)(i1 - i0), cs);
       ++nl;
+      tr.mark("ipanel_done", i0, cs);
       if (er == cudaSuccess) { er = launch_getrf_compose(g, i0, i1, 0, pbuf[2], cs); ++nl; }
       if (er == cudaSuccess) er = swap_cols(i0, i1, J0, i0, cs, &pbuf[2]);
       if (er != cudaSuccess) return fail(er, "rgetrf panel");
@@ -370,12 +372,14 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
         const int r = apply_block(i0, i1, i1, J1, cs, &pbuf[2]);
         if (r != DDB_OK) return r;
       }
+      tr.mark("iapply_done", i0, cs);
     }
     return DDB_OK;
   };
   if (e == cudaSuccess) e = cudaEventRecord(ev_a, s);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_a, 0);
   if (e == cudaSuccess) rc2 = factor_outer(0, NB < g.mn ? NB : g.mn);
+  tr.mark("panel_done", 0, cs);
   bool have_rest = false;
   for (int64_t J0 = 0; e == cudaSuccess && rc2 == DDB_OK; J0 += NB) {
     const int64_t J1 = J0 + NB < g.mn ? J0 + NB : g.mn;
@@ -395,15 +399,20 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev_a, 0);
     if (e != cudaSuccess) break;
     if (J2 < n) {
+      tr.mark("rest_start", J0, s);
       rc2 = apply_block(J0, J1, J2, n, s, pre);            // rest(J)
       if (rc2 != DDB_OK) break;
+      tr.mark("rest_done", J0, s);
       e = cudaEventRecord(ev_b, s);
       have_rest = true;
       if (e != cudaSuccess) break;
     }
+    tr.mark("upd_start", J0, cs);
     rc2 = apply_block(J0, J1, J1, J2, cs, pre);            // columns of block J+1
+    tr.mark("upd_done", J0, cs);
     if (rc2 != DDB_OK || J1 >= g.mn) break;
     rc2 = factor_outer(J1, J2 < g.mn ? J2 : g.mn);
+    tr.mark("panel_done", J1, cs);
   }
   if (cs != nullptr) {
     cudaError_t ej = cudaEventRecord(ev_a, cs);

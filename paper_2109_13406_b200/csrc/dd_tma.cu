@@ -225,26 +225,34 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
     unit_origin(u, i0, j0, kbeg, ktiles);
 
     double H[TM][TNK], L[TM][TNK];
-    if (CERTLIKE) {
 #pragma unroll
-      for (int a = 0; a < TM; ++a)
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TNK; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
+    if (CERTLIKE) {
+      // anchors row pair by row pair, shifted in from H[TM - 1]: a rolled
+      // loop keeps the kernel's code small (a short-k tile runs its prologue
+      // and epilogue once, and fully unrolled they missed the instruction
+      // cache: ~2x the tile time at k = 64)
+#pragma unroll 1
+      for (int a = 0; a < TM; ++a) {
+#pragma unroll
+        for (int i = 0; i + 1 < TM; ++i)
+#pragma unroll
+          for (int b = 0; b < TNK; ++b) H[i][b] = H[i + 1][b];
+        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+        const int er = gi < g.m ? row_exp[gi] : 0;
 #pragma unroll
         for (int b = 0; b < TNK; ++b) {
-          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
           const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
           const bool in = gi < g.m && gj < g.n;
           const float sb = in ? g.bound[gi + gj * g.m] : 0.f;
-          const int er = gi < g.m ? row_exp[gi] : 0, ec = gj < g.n ? col_exp[gj] : 0;
+          const int ec = gj < g.n ? col_exp[gj] : 0;
           const double sd = dfma((double)sb, g.bnd_fac, g.bnd_floor);
           const int es = (int)((dbits(sd) >> 52) & 0x7ff);
-          H[a][b] = anchor_from_bexp(es + er + ec - 2042);
-          L[a][b] = 0.0;
+          H[TM - 1][b] = anchor_from_bexp(es + er + ec - 2042);
         }
-    } else {
-#pragma unroll
-      for (int a = 0; a < TM; ++a)
-#pragma unroll
-        for (int b = 0; b < TNK; ++b) { H[a][b] = 0.0; L[a][b] = 0.0; }
+      }
     }
 
     for (int kt = 0; kt < ktiles; ++kt, ++c_item) {
@@ -377,95 +385,68 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
       if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     }
 
-    // epilogue (as dd_tiled.cuh's fast modes).  The routing words, the cross
-    // terms and C are loaded for all of the thread's elements before any
-    // arithmetic, so their global round trips overlap instead of running one
-    // element after another (that serial chain was ~30 % of a tile at k = 256)
+    // epilogue (as dd_tiled.cuh's fast modes), one row pair at a time from
+    // H[0] / L[0], the rest shifted down after it (rolled: see the prologue).
+    // Per row pair the routing words, the cross terms and C are loaded for
+    // its TNK elements before any arithmetic, so the global round trips
+    // overlap instead of running one element after another.
     const int split = u / tiles;
-    int rsv[TM], csv[TNK];
-#pragma unroll
-    for (int a = 0; a < TM; ++a) {
-      const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-      rsv[a] = g.rsp != nullptr && gi < g.m ? g.rsp[gi] : 0;
-    }
+    int csv[TNK];
 #pragma unroll
     for (int b = 0; b < TNK; ++b) {
       const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
       csv[b] = g.rsp != nullptr && gj < g.n ? g.csp[gj] : 0;
     }
-    uint64_t mine = 0;   // bit a * TNK + b: this launch writes the element
-#pragma unroll
-    for (int a = 0; a < TM; ++a)
+#pragma unroll 1
+    for (int a = 0; a < TM; ++a) {
+      const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
+      const int rsv = g.rsp != nullptr && gi < g.m ? g.rsp[gi] : 0;
+      bool mine[TNK];
+      double xv[TNK], ch[TNK], cl[TNK];
 #pragma unroll
       for (int b = 0; b < TNK; ++b) {
-        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
         const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
         bool ok = gi < g.m && gj < g.n;
         if (SYRK == 1) ok &= gi <= gj;   // the uplo triangle only (level23.py:245-270)
         if (SYRK == 2) ok &= gi >= gj;
         if (g.rsp != nullptr) {          // elem_mine (internal.h) on the preloaded words
-          const int v = rsv[a] + csv[b];
+          const int v = rsv + csv[b];
           const int cls = v >= SPREAD_BAD ? EC_REF : (g.wide_lim > 0 && v > g.wide_lim ? EC_WIDE : EC_FAST);
           ok &= cls == (g.only_wide ? EC_WIDE : EC_FAST);
         }
-        mine |= ok ? uint64_t(1) << (a * TNK + b) : uint64_t(0);
+        mine[b] = ok;
+        const bool x = ALG == ALG_SPLIT && split == 0 && g.cross != nullptr && ok;
+        xv[b] = x ? g.cross[gi + gj * g.m] : 0.0;
+        const bool c = ok && g.part == nullptr;
+        ch[b] = c ? g.c_hi[gi + gj * g.ldc] : 0.0;
+        cl[b] = c ? g.c_lo[gi + gj * g.ldc] : 0.0;
       }
-    if (ALG == ALG_SPLIT && split == 0 && g.cross != nullptr) {
 #pragma unroll
-      for (int a = 0; a < TM; ++a) {
-        double xv[TNK];
-#pragma unroll
-        for (int b = 0; b < TNK; ++b) {
-          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-          xv[b] = (mine >> (a * TNK + b) & 1) ? g.cross[gi + gj * g.m] : 0.0;
-        }
-#pragma unroll
-        for (int b = 0; b < TNK; ++b) L[a][b] = dadd(L[a][b], xv[b]);
-      }
-    }
-    if (g.part != nullptr) {
-#pragma unroll
-      for (int a = 0; a < TM; ++a)
-#pragma unroll
-        for (int b = 0; b < TNK; ++b) {
-          if (!(mine >> (a * TNK + b) & 1)) continue;
-          const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-          const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-          double sx, ex;
-          const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
-          two_sum(hv, L[a][b], sx, ex);
+      for (int b = 0; b < TNK; ++b) {
+        if (!mine[b]) continue;
+        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+        double sx, ex;
+        const double hv = CERTLIKE ? dsub(H[0][b], anchor_of(H[0][b])) : H[0][b];
+        const double lv = ALG == ALG_SPLIT ? dadd(L[0][b], xv[b]) : L[0][b];
+        two_sum(hv, lv, sx, ex);
+        if (g.part != nullptr) {
           double* ph = g.part + (size_t)split * 2 * g.m * g.n;
           ph[gi + gj * g.m] = sx;
           ph[(size_t)g.m * g.n + gi + gj * g.m] = ex;
+          continue;
         }
-      continue;
-    }
-    // C in batches of one row pair's TNK elements (registers: H and L stay live)
-#pragma unroll
-    for (int a = 0; a < TM; ++a) {
-      double ch[TNK], cl[TNK];
-#pragma unroll
-      for (int b = 0; b < TNK; ++b) {
-        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-        const bool m = mine >> (a * TNK + b) & 1;
-        ch[b] = m ? g.c_hi[gi + gj * g.ldc] : 0.0;
-        cl[b] = m ? g.c_lo[gi + gj * g.ldc] : 0.0;
-      }
-#pragma unroll
-      for (int b = 0; b < TNK; ++b) {
-        if (!(mine >> (a * TNK + b) & 1)) continue;
-        const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-        double sx, ex;
-        const double hv = CERTLIKE ? dsub(H[a][b], anchor_of(H[a][b])) : H[a][b];
-        two_sum(hv, L[a][b], sx, ex);
         const int64_t ci = gi + gj * g.ldc;
         const dd out = add2_chk(mul2_chk(g.alpha, dd{sx, ex}), scale_beta(g.beta, dd{ch[b], cl[b]}));
         g.c_hi[ci] = out.h;
         g.c_lo[ci] = out.l;
       }
+#pragma unroll
+      for (int i = 0; i + 1 < TM; ++i)
+#pragma unroll
+        for (int b = 0; b < TNK; ++b) {
+          H[i][b] = H[i + 1][b];
+          L[i][b] = L[i + 1][b];
+        }
     }
   }
 }
