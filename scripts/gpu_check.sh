@@ -20,3 +20,11 @@ $CMD > gpurun_out/${TAG}_quick.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum,sm__inst_executed_pipe_fp64.sum,sm__inst_executed_pipe_tensor_subpipe_dmma.sum \
     --clock-control none --csv --log-file gpurun_out/${TAG}_fp64_step.csv $CMD > gpurun_out/${TAG}_ncu.log 2>&1
 echo "ncu rc=$?"
+# ncu --set full of the hi*hi kernel alone (serial schedule: ncu cannot replay
+# it beside the concurrent cross-term stream)
+export DDB_CROSS_SERIAL=1
+CMD1="python bench.py --steps 1 --warmup 0 --quick"
+$CMD1 > gpurun_out/${TAG}_serial.log 2>&1 && \
+ncu --set full --clock-control none --import-source on -k regex:"dd_tma_nn" -c 1 \
+    -o gpurun_out/${TAG}_main $CMD1 > gpurun_out/${TAG}_ncu_main.log 2>&1
+echo "ncu main rc=$?"
