@@ -124,6 +124,30 @@ def test_rpotrf_exact_matches_oracle(uplo, n, nb):
 
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("nb", [0, 100])
+def test_rpotrf_out_of_window_rows_exact_matches_oracle(uplo, nb):
+    """D A D with a few 2^+-350 scales: factor entries far outside the safe
+    window in some rows / columns, so the row-recurrence kernel's warps, the
+    window mask of its factor block and the diagonal kernel's check-free
+    updates all take their checked fallbacks -- still bitwise vs the oracle."""
+    n = 700
+    ld = n + 1
+    hi, lo = spd_dd(n, ld, seed=91)
+    d = np.ones(n)
+    for i, e in ((5, 350), (300, 350), (450, -350), (650, -350), (257, 320)):
+        d[i] = 2.0 ** e
+    for c in range(n):
+        sl = slice(c * ld, c * ld + n)
+        hi[sl] *= d * d[c]        # exact: powers of two
+        lo[sl] *= d * d[c]
+    info, gh, gl = run(uplo, n, ld, hi, lo, "exact", nb)
+    oh, ol = hi.copy(), lo.copy()
+    rc, oinfo = oracle.rpotrf(uplo, n, oh, ol, ld)
+    assert rc == 0 and info == oinfo == 0
+    assert bits_equal(gh, oh) and bits_equal(gl, ol)
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("nb", [64, 300])
 def test_rpotrf_late_failure_restores_trailing(uplo, nb):
     """A failing pivot deep in a multi-block run: info, A(j,j) and every
