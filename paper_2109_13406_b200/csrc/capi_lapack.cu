@@ -287,6 +287,8 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
   char* w = static_cast<char*>(ws);
   g.info = reinterpret_cast<int*>(w);
   g.bar = reinterpret_cast<unsigned*>(w + 64);
+  // window masks of the U12 kernel's L block, one per stream (8 words each)
+  unsigned* lmask[2] = {reinterpret_cast<unsigned*>(w + 128), reinterpret_cast<unsigned*>(w + 192)};
   g.ipiv = reinterpret_cast<long long*>(w + 256);
   g.swap = g.ipiv + g.mn;
   double* pd = reinterpret_cast<double*>(g.swap + g.mn);
@@ -348,13 +350,21 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
     if (c1 <= c0) return DDB_OK;
     cudaError_t er = swap_cols(J0, J1, c0, c1, st, pre);
     if (er != cudaSuccess) return fail(er, "rgetrf laswp");
-    for (int64_t i0 = J0; i0 < J1; i0 += ib) {
-      const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
-      if ((er = launch_getrf_trsm(g, i0, (int)(i1 - i0), c0, c1, st)) != cudaSuccess)
-        return fail(er, "rgetrf trsm");
-      ++nl;
-      const int r = gemm(i1, J1, c0, c1, i0, i1, st);
-      if (r != DDB_OK) return r;
+    if (J1 - J0 > ib && J1 - J0 <= 256) {
+      // the whole block row's U12 in one launch (per element the same
+      // products in the same order as the inner trsm / Rgemm sequence below)
+      er = launch_getrf_u12(g, J0, (int)(J1 - J0), c0, c1, lmask[st == cs ? 0 : 1], st);
+      nl += f64 ? 1 : 2;
+      if (er != cudaSuccess) return fail(er, "rgetrf u12");
+    } else {
+      for (int64_t i0 = J0; i0 < J1; i0 += ib) {
+        const int64_t i1 = i0 + ib < J1 ? i0 + ib : J1;
+        if ((er = launch_getrf_trsm(g, i0, (int)(i1 - i0), c0, c1, st)) != cudaSuccess)
+          return fail(er, "rgetrf trsm");
+        ++nl;
+        const int r = gemm(i1, J1, c0, c1, i0, i1, st);
+        if (r != DDB_OK) return r;
+      }
     }
     return gemm(J1, m, c0, c1, J0, J1, st);
   };

@@ -532,6 +532,105 @@ getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0, int64_t c1) {
   if (rb < nb) N::st(uh, ul, rb, acc_b);
 }
 
+// U12 of a block row in one launch: columns c in [c0, c1) of rows [j0, j0 +
+// w) (w <= 256) after the block's interchanges, U(l, c) = A(l, c) - sum_{t <
+// l} L(l, t) U(t, c) with the products in t order -- the same operation
+// sequence as getrf_trsm_kernel per inner block plus the alpha = -1 Rgemm
+// between inner blocks (add2(acc, mul2(L, -U)) per element, t ascending), so
+// exact mode stays bitwise.  One warp per column, lane t holding rows t + 32
+// i (chains); step l finalises entry l (unit diagonal: no scaling),
+// broadcasts it, and every lane extends its later rows -- lanes whose row is
+// already final update dead accumulators, so there are no per-lane
+// predicates.  L is read through L1 one step ahead; the check-free forms run
+// while the step is inside the safe window (mask: L block rows, from
+// launch_window_mask; the starting column; each broadcast value).
+template <class N, int NPER>
+__global__ void __launch_bounds__(256)
+getrf_u12_kernel(GetrfArgs g, int64_t j0, int w, int64_t c0, int64_t c1,
+                 const unsigned* __restrict__ lmask) {
+  using T = typename N::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = c0 + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (c >= c1) return;                       // whole warps
+  const int64_t lda = g.lda;
+  double* uh = g.a_hi + j0 + c * lda;
+  double* ul = g.f64 ? nullptr : g.a_lo + j0 + c * lda;
+  const double* lh = g.a_hi + j0 + j0 * lda;  // L(j0 + r, j0 + t) at r + t * lda
+  const double* ll = g.f64 ? nullptr : g.a_lo + j0 + j0 * lda;
+  T acc[NPER];
+  bool ok = !N::kF64 && lmask != nullptr;
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) {
+    const int r = lane + 32 * i;
+    acc[i] = N::zero();
+    if (r < w) {
+      acc[i] = N::ld(uh, ul, r);
+      ok &= N::win(acc[i]) && (lmask[i] >> lane & 1u) != 0;
+    }
+  }
+  const bool fast_ok = __all_sync(0xffffffffu, ok);
+  T tn[NPER];
+#pragma unroll
+  for (int i = 0; i < NPER; ++i) tn[i] = N::zero();
+  auto fetch = [&](int t, int s) {           // L(r, t) for chains >= s
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      if (i >= s && lane + 32 * i < w) tn[i] = N::ldg(lh, ll, (int64_t)(lane + 32 * i) + (int64_t)t * lda);
+  };
+  if (w > 1) fetch(0, 0);
+#pragma unroll
+  for (int s = 0; s < NPER; ++s) {
+    if (32 * s >= w) break;
+    const int tend = min(32, w - 32 * s);
+    for (int tt = 0; tt < tend; ++tt) {
+      const int t = 32 * s + tt;
+      T lv[NPER];
+#pragma unroll
+      for (int i = s; i < NPER; ++i) lv[i] = tn[i];
+      if (t + 1 < w) fetch(t + 1, tt + 1 < 32 ? s : s + 1);
+      const T u = N::shfl(acc[s], tt);       // U(j0 + t, c): final
+      if (lane == tt) N::st(uh, ul, t, u);
+      const T nu = N::neg(u);
+      if (fast_ok && N::win(u)) {            // warp-uniform
+#pragma unroll
+        for (int i = s; i < NPER; ++i) acc[i] = N::fadd2(acc[i], N::fmul(lv[i], nu));
+      } else {
+#pragma unroll
+        for (int i = s; i < NPER; ++i) acc[i] = N::add(acc[i], N::mul(lv[i], nu));
+      }
+    }
+  }
+}
+
+template <class N, int NPER>
+static cudaError_t u12_launch(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
+                              const unsigned* lmask, cudaStream_t s) {
+  const int64_t threads = (c1 - c0) * 32;
+  getrf_u12_kernel<N, NPER><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, j0, w, c0, c1, lmask);
+  return cudaGetLastError();
+}
+
+template <class N>
+static cudaError_t u12_dispatch(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
+                                const unsigned* lmask, cudaStream_t s) {
+  if (w <= 64) return u12_launch<N, 2>(g, j0, w, c0, c1, lmask, s);
+  if (w <= 128) return u12_launch<N, 4>(g, j0, w, c0, c1, lmask, s);
+  return u12_launch<N, 8>(g, j0, w, c0, c1, lmask, s);
+}
+
+cudaError_t launch_getrf_u12(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
+                             unsigned* lmask, cudaStream_t s) {
+  if (c1 <= c0 || w <= 0) return cudaSuccess;
+  if (w > 256) return cudaErrorInvalidValue;
+  if (!g.f64) {
+    const cudaError_t e = launch_window_mask(g.a_hi + j0 + j0 * g.lda, g.a_lo + j0 + j0 * g.lda, w, 1,
+                                             g.lda, lmask, s);
+    if (e != cudaSuccess) return e;
+  }
+  return g.f64 ? u12_dispatch<NumF64>(g, j0, w, c0, c1, nullptr, s)
+               : u12_dispatch<NumDD>(g, j0, w, c0, c1, lmask, s);
+}
+
 static int panel_grid(int64_t rows) {
   static thread_local int cached_dev = -1, cached_max = 0;
   int dev = 0;

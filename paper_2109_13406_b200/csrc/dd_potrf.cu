@@ -496,12 +496,19 @@ cudaError_t launch_potrf_rows(const PotrfArgs& p, int64_t j0, int w, int64_t q0,
   // P offsets are 32-bit: the w x w block spans < 2^31 elements
   if (w > kPotrfMaxPanel || (w - 1) * (sr + sc) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   if (pmask != nullptr && !p.f64) {
-    potrf_psafe_kernel<<<(w + 31) / 32, 1024, 0, s>>>(ph, pl, w, (int)sr, (int)sc, pmask);
-    const cudaError_t e = cudaGetLastError();
+    const cudaError_t e = launch_window_mask(ph, pl, w, sr, sc, pmask, s);
     if (e != cudaSuccess) return e;
   }
   return p.f64 ? rows_dispatch<NumF64>(p, j0, w, q0, q1, ph, pl, (int)sr, (int)sc, rh, rl, nullptr, s)
                : rows_dispatch<NumDD>(p, j0, w, q0, q1, ph, pl, (int)sr, (int)sc, rh, rl, pmask, s);
+}
+
+cudaError_t launch_window_mask(const double* ph, const double* pl, int w, int64_t sr, int64_t sc,
+                               unsigned* mask, cudaStream_t s) {
+  if (w <= 0) return cudaSuccess;
+  if ((w - 1) * (sr + sc) >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+  potrf_psafe_kernel<<<(w + 31) / 32, 1024, 0, s>>>(ph, pl, w, (int)sr, (int)sc, mask);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_potrf_blockupd(const PotrfArgs& p, int64_t i0, int64_t i1, int64_t j1,

@@ -260,5 +260,13 @@ cudaError_t launch_getrf_apply(const GetrfArgs& g, const PermBuf& pb, int64_t ns
                                int64_t c1, cudaStream_t s);
 cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
                               cudaStream_t s);
+// U12 of rows [j0, j0 + w) (w <= 256), columns [c0, c1), in one launch;
+// lmask: 8 words of scratch (dd_getrf.cu)
+cudaError_t launch_getrf_u12(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
+                             unsigned* lmask, cudaStream_t s);
+// bit r % 32 of mask[r / 32]: row r of the w x w block P (P(r, c) at
+// ph[r * sr + c * sc], c < r) is inside the safe window (dd_potrf.cu)
+cudaError_t launch_window_mask(const double* ph, const double* pl, int w, int64_t sr, int64_t sc,
+                               unsigned* mask, cudaStream_t s);
 
 }  // namespace ddb
