@@ -279,7 +279,7 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
   // partial candidates and rows: two parities (getrf_panel_smem_kernel)
   const size_t ws_bytes = 256 + sizeof(long long) * 2 * (size_t)g.mn +
                           2 * (size_t)G * (4 * sizeof(double) + sizeof(long long) + sizeof(int)) +
-                          64 + sizeof(double) * (4 * (size_t)G + 4) * (size_t)nb + 64 +
+                          64 + sizeof(double) * (4 * (size_t)G + 4) * ((size_t)nb + 1) + 64 +
                           5 * (size_t)kPermBufBytes + 64;
   void* ws = nullptr;
   cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
@@ -304,7 +304,7 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
   PermBuf pbuf[5];
   {
     char* pp = reinterpret_cast<char*>(
-        (reinterpret_cast<uintptr_t>(g.rowbuf + (4 * (size_t)G + 4) * nb) + 63) &
+        (reinterpret_cast<uintptr_t>(g.rowbuf + (4 * (size_t)G + 4) * (nb + 1)) + 63) &
         ~static_cast<uintptr_t>(63));
     for (int i = 0; i < 5; ++i, pp += kPermBufBytes) {
       pbuf[i].rows = reinterpret_cast<long long*>(pp);

@@ -252,68 +252,121 @@ __device__ __forceinline__ SKey skey_block_best(SKey k) {
   return r;
 }
 
+__device__ __forceinline__ void named_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kPanelThreads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kPanelThreads) : "memory");
+}
+constexpr int kPanelMaxNb = 64;          // panel width (the driver's inner block)
+
+#ifdef DDB_DIAG_TIMING
+// diagnostics build only: per-step clock64 stamps of CTA 0 in the last panel
+__device__ long long g_panel_t[64][8];
+#define PANEL_T(jj, k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_panel_t[jj][k] = clock64(); } while (0)
+extern "C" int ddb_debug_panel_timing(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_panel_t, sizeof(g_panel_t));
+}
+#else
+#define PANEL_T(jj, k) ((void)0)
+#endif
+
 template <class N>
 __global__ void __launch_bounds__(kPanelThreads)
 getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   using T = typename N::T;
   extern __shared__ double sm[];
   __shared__ T rec_s;
-  __shared__ int use_rec_s, nonzero_s;
+  __shared__ int flags_s;                // bit 0 nonzero pivot, bit 1 |pivot| >= safmin
   const int G = gridDim.x;
   const int64_t r0 = j0 + (int64_t)blockIdx.x * chunk;
   const int64_t r1 = r0 + chunk < g.m ? r0 + chunk : g.m;
   const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
-  const int ch = (int)chunk;
-  double* xh = sm;                       // rows x nb, ld = chunk
+  const int ch = (int)chunk | 1;         // odd row stride: a row read across lanes is conflict-free
+  double* xh = sm;                       // rows x nb, ld = ch
   double* xl = sm + (size_t)ch * nb;
-  double* ph = xl + (size_t)ch * nb;     // the pivot row (nb)
-  double* pl = ph + nb;
+  // the pivot rows of two consecutive steps (step jj's at parity jj & 1)
+  auto prow_h = [&](int par) { return xl + (size_t)ch * nb + (size_t)par * 2 * nb; };
+  auto prow_l = [&](int par) { return prow_h(par) + nb; };
   const int64_t lda = g.lda;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
     const int r = t % nr, c = t / nr;
     N::st(xh, xl, r + c * ch, N::ld(g.a_hi, g.a_lo, (r0 + r) + (j0 + c) * lda));
   }
   __syncthreads();
   auto owner = [&](int64_t row) { return (int)((row - j0) / chunk); };
-  // global scratch, two parities: keys [2][G], candidate rows [2][G][2 nb],
-  // row j [2][2 nb]
-  auto cand = [&](int par, int c) { return g.rowbuf + ((size_t)par * G + c) * 2 * nb; };
-  auto jrow = [&](int par) { return g.rowbuf + (size_t)2 * G * 2 * nb + (size_t)par * 2 * nb; };
-  // search column jj, publish the candidate (+ row j0 + jj).  Columns > upd
-  // of the published rows are sent with step jj - 1's rank-1 update applied
-  // (the same add2 / mul2 the bulk update below performs on them later), so
+  auto mine = [&](int64_t row) { return row >= r0 && row < r1; };
+  auto first_row = [&](int64_t j) { return r0 > j ? 0 : (int)(j - r0); };   // local rows >= j
+  // global scratch, two parities: keys [2][G], candidate rows [2][G][2 nb +
+  // 2], row j [2][2 nb + 2]: hi row | lo row | the reciprocal of the row's
+  // entry in the column searched (formed speculatively by the publisher)
+  const size_t RS = 2 * (size_t)nb + 2;
+  auto cand = [&](int par, int c) { return g.rowbuf + ((size_t)par * G + c) * RS; };
+  auto jrow = [&](int par) { return g.rowbuf + (size_t)2 * G * RS + (size_t)par * RS; };
+  // step jj's rank-1 update of x(r, c) (check-free inside the safe window)
+  auto upd = [&](int r, int c, int jj) {
+    const T x = N::ld(xh, xl, r + jj * ch), a = N::ld(xh, xl, r + c * ch);
+    const T pc = N::ld(prow_h(jj & 1), prow_l(jj & 1), c);
+    const T out = N::win(x) && N::win(a) && N::win(pc) ? N::fadd2(a, N::fmul(x, N::neg(pc)))
+                                                       : N::add(a, N::mul(x, N::neg(pc)));
+    N::st(xh, xl, r + c * ch, out);
+  };
+  // warps 1 / 2: the reciprocal of the candidate's / row j's pivot-column
+  // entry (the reference's scalar _div2, needed only when the entry is a
+  // non-zero >= safmin), in the shadow of warp 0's row output
+  auto spec_rec = [&](double* out, int rr, int jj) {
+    if (lane != 0) return;
+    const T v = N::ld(xh, xl, rr + jj * ch);
+    T rec = N::zero();
+    if (N::nonzero(v) && N::ge_safmin(v)) rec = N::sdiv(N::one(), v);
+    N::st(out + 2 * nb, out + 2 * nb + 1, 0, rec);
+  };
+  // search column jj (warps 0 and 1 alike), publish the candidate (+ row j0
+  // + jj).  Columns > u of the published rows carry step jj - 1's rank-1
+  // update (the same operations the bulk update performs on them later), so
   // the CTA can arrive at the barrier before its bulk update.
-  auto publish = [&](int jj, int upd) {
+  auto publish = [&](int jj, int u) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
+    if (warp == 2) {
+      if (mine(j)) spec_rec(jrow(par), (int)(j - r0), jj);
+      return;
+    }
     SKey k{0ull, 0ull, kNoRow};
-    const int rs = r0 > j ? 0 : (int)(j - r0);
-    for (int r = rs + threadIdx.x; r < nr; r += blockDim.x)
+    for (int r = first_row(j) + lane; r < nr; r += 32)
       k = skey_merge(k, skey_of<N>(N::ld(xh, xl, r + jj * ch), (long long)(r0 + r)));
-    k = skey_block_best(k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+      k = skey_merge(k, SKey{__shfl_xor_sync(0xffffffffu, k.ah, o), __shfl_xor_sync(0xffffffffu, k.al, o),
+                             __shfl_xor_sync(0xffffffffu, k.idx, o)});
+    if (warp == 1) {
+      if (k.idx != kNoRow) spec_rec(cand(par, blockIdx.x), (int)(k.idx - r0), jj);
+      return;
+    }
     const int slot = par * G + blockIdx.x;
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       reinterpret_cast<unsigned long long*>(g.part_ah)[slot] = k.ah;
       reinterpret_cast<unsigned long long*>(g.part_al)[slot] = k.al;
       g.part_idx[slot] = k.idx;
     }
     auto row_out = [&](double* out, int rr) {
-      for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+      for (int c = lane; c < nb; c += 32) {
         T v = N::ld(xh, xl, rr + c * ch);
-        if (c > upd) v = N::add(v, N::mul(N::ld(xh, xl, rr + (jj - 1) * ch), N::neg(N::ld(ph, pl, c))));
+        if (c > u) {
+          const T pc = N::ld(prow_h((jj - 1) & 1), prow_l((jj - 1) & 1), c);
+          v = N::add(v, N::mul(N::ld(xh, xl, rr + (jj - 1) * ch), N::neg(pc)));
+        }
         N::st(out, out + nb, c, v);
       }
     };
     if (k.idx != kNoRow) row_out(cand(par, blockIdx.x), (int)(k.idx - r0));
-    if (owner(j) == (int)blockIdx.x) row_out(jrow(par), (int)(j - r0));
+    if (mine(j)) row_out(jrow(par), (int)(j - r0));
   };
-  // arrive / wait halves of grid_barrier
+  // split grid barrier: release-add after the CTA's writes, acquire-poll
   auto arrive = [&]() {
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(g.bar, 1u);
-    }
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(g.bar) : "memory");
   };
   auto wait = [&](unsigned target) {
     if (threadIdx.x == 0) {
@@ -323,79 +376,129 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
         if (v >= target) break;
         __nanosleep(20);
       }
-      __threadfence();
     }
     __syncthreads();
   };
-  publish(0, nb);
+  if (warp < 3) publish(0, nb);
   arrive();
   unsigned nbar = 0;
   for (int jj = 0; jj < nb; ++jj) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
+    PANEL_T(jj, 0);
     wait(G * ++nbar);
-    // the G partial keys: one per thread, then a block reduction
-    SKey k{0ull, 0ull, kNoRow};
-    for (int c = threadIdx.x; c < G; c += blockDim.x) {
-      const int slot = par * G + c;
-      k = skey_merge(k, SKey{__ldcg(reinterpret_cast<const unsigned long long*>(g.part_ah) + slot),
-                             __ldcg(reinterpret_cast<const unsigned long long*>(g.part_al) + slot),
-                             __ldcg(g.part_idx + slot)});
-    }
-    k = skey_block_best(k);
-    // NaN |hi| (np.max propagates it: argmax_abs returns 0 -> the diagonal
-    // entry) or no candidate: row j stays
-    const bool nan = k.idx == kNoRow || isnan(__longlong_as_double((long long)k.ah));
-    const int64_t jp = nan ? j : k.idx;
-    // nonzero(pivot) from the key: |hi| != 0 or lo != 0 (+0 is the map's 1 << 63)
-    const bool swapped = !nan && (k.ah != 0ull || k.al != (1ull << 63)) && jp != j;
-    const double* src = swapped ? cand(par, owner(jp)) : jrow(par);
-    const double* jr = jrow(par);
-    // the pivot (entry jj of the pivot row) on the last warp, idle in the row fetch (nb <= 64)
-    if (threadIdx.x == blockDim.x - 1) {
-      const T piv = N::ldcg(src, src + nb, jj);
-      nonzero_s = N::nonzero(piv);
-      use_rec_s = N::ge_safmin(piv);                       // |pivot| >= safmin (lu.py:98)
-      if (nonzero_s && use_rec_s) rec_s = N::sdiv(N::one(), piv);
-      if (blockIdx.x == 0) {
-        g.ipiv[j] = jp + 1;
-        g.swap[j] = swapped ? jp : j;
-        if (!nonzero_s && *g.info == 0) *g.info = (int)(j + 1);
+    PANEL_T(jj, 1);
+    if (warp == 0) {
+      // merge the G partial keys, fetch the pivot row (and row j) and the
+      // publisher's reciprocal; the rows go into x only once the other warps
+      // have finished step jj - 1's deferred bulk update (named barrier 1)
+      SKey k{0ull, 0ull, kNoRow};
+      for (int c = lane; c < G; c += 32) {
+        const int slot = par * G + c;
+        k = skey_merge(k, SKey{__ldcg(reinterpret_cast<const unsigned long long*>(g.part_ah) + slot),
+                               __ldcg(reinterpret_cast<const unsigned long long*>(g.part_al) + slot),
+                               __ldcg(g.part_idx + slot)});
       }
-    }
-    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
-      const T v = N::ldcg(src, src + nb, c);
-      N::st(ph, pl, c, v);
-      if (owner(j) == (int)blockIdx.x) N::st(xh, xl, (j - r0) + c * ch, v);
-      if (swapped && owner(jp) == (int)blockIdx.x)
-        N::st(xh, xl, (jp - r0) + c * ch, N::ldcg(jr, jr + nb, c));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        k = skey_merge(k, SKey{__shfl_xor_sync(0xffffffffu, k.ah, o), __shfl_xor_sync(0xffffffffu, k.al, o),
+                               __shfl_xor_sync(0xffffffffu, k.idx, o)});
+      // NaN |hi| (np.max propagates it: argmax_abs returns 0 -> the diagonal
+      // entry) or no candidate: row j stays
+      const bool nan = k.idx == kNoRow || isnan(__longlong_as_double((long long)k.ah));
+      const int64_t jp = nan ? j : k.idx;
+      // nonzero(pivot) from the key: |hi| != 0 or lo != 0 (+0 is the map's 1 << 63)
+      const bool swapped = !nan && (k.ah != 0ull || k.al != (1ull << 63)) && jp != j;
+      const double* src = swapped ? cand(par, owner(jp)) : jrow(par);
+      const double* jr = jrow(par);
+      const bool own_j = mine(j), own_jp = swapped && mine(jp);
+      constexpr int kMaxPer = (kPanelMaxNb + 31) / 32;
+      T v[kMaxPer], o[kMaxPer];
+#pragma unroll
+      for (int i = 0; i < kMaxPer; ++i) {
+        const int c = lane + 32 * i;
+        v[i] = o[i] = N::zero();
+        if (c < nb) {
+          v[i] = N::ldcg(src, src + nb, c);
+          if (own_jp) o[i] = N::ldcg(jr, jr + nb, c);
+        }
+      }
+      T piv = N::zero(), rec = N::zero();
+      if (lane == 0) {
+        piv = N::ldcg(src, src + nb, jj);
+        rec = N::ldcg(src + 2 * nb, src + 2 * nb + 1, 0);
+      }
+      named_sync(1);
+#pragma unroll
+      for (int i = 0; i < kMaxPer; ++i) {
+        const int c = lane + 32 * i;
+        if (c < nb) {
+          N::st(prow_h(par), prow_l(par), c, v[i]);
+          if (own_j) N::st(xh, xl, (j - r0) + c * ch, v[i]);
+          if (own_jp) N::st(xh, xl, (jp - r0) + c * ch, o[i]);
+        }
+      }
+      if (lane == 0) {
+        const bool nz = N::nonzero(piv), ur = N::ge_safmin(piv);     // lu.py:98
+        flags_s = (nz ? 1 : 0) | (ur ? 2 : 0);
+        if (nz && ur) rec_s = rec;             // = _div2(1, piv), formed by the publisher
+        if (blockIdx.x == 0) {
+          g.ipiv[j] = jp + 1;
+          g.swap[j] = swapped ? jp : j;
+          if (!nz && *g.info == 0) *g.info = (int)(j + 1);
+        }
+      }
+      PANEL_T(jj, 2);
+    } else {
+      // step jj - 1's bulk update of columns >= jj + 2 (column jj + 1 was
+      // done before the barrier), 64 rows x 7 column phases
+      if (jj > 0) {
+        const int t = threadIdx.x - 32, rr = t % 32, cc = t / 32;
+        const int rs = first_row(j), pj = (jj - 1) & 1;
+        for (int r = rs + rr; r < nr; r += 32) {
+          const T x = N::ld(xh, xl, r + (jj - 1) * ch);
+          const bool wx = N::win(x);
+          for (int c = jj + 2 + cc; c < nb; c += (kPanelThreads - 32) / 32) {
+            const T a = N::ld(xh, xl, r + c * ch), pc = N::ld(prow_h(pj), prow_l(pj), c);
+            // mul2(x, -p): the sign moves between the factors exactly
+            const T out = wx && N::win(a) && N::win(pc) ? N::fadd2(a, N::fmul(x, N::neg(pc)))
+                                                        : N::add(a, N::mul(x, N::neg(pc)));
+            N::st(xh, xl, r + c * ch, out);
+          }
+        }
+      }
+      named_arrive(1);
     }
     __syncthreads();
-    const bool nonzero = nonzero_s;
-    const int rs = r0 > j + 1 ? 0 : (int)(j + 1 - r0);
-    if (nonzero) {
-      const bool use_rec = use_rec_s;
-      const T rec = rec_s, piv = N::ld(ph, pl, jj);
-      for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) {
-        const T x = N::ld(xh, xl, r + jj * ch);
-        N::st(xh, xl, r + jj * ch, use_rec ? N::mul(rec, x) : N::vdiv(x, piv));
+    PANEL_T(jj, 3);
+    const int flags = flags_s;
+    const int rs = first_row(j + 1);
+    // this thread's row (chunk <= kSmemRowsMax < kPanelThreads): scale
+    // column jj, then step jj's update of column jj + 1 (the next search)
+    {
+      const int r = rs + threadIdx.x;
+      if (r < nr) {
+        T x = N::ld(xh, xl, r + jj * ch);
+        if (flags & 1) {
+          x = (flags & 2) ? N::mul(rec_s, x) : N::vdiv(x, N::ld(prow_h(par), prow_l(par), jj));
+          N::st(xh, xl, r + jj * ch, x);
+        }
+        if (jj + 1 < nb) upd(r, jj + 1, jj);
       }
     }
     if (jj + 1 == nb) break;              // (j < mn - 1 holds below: the panel lies inside mn)
     __syncthreads();
-    // column jj + 1 first: the next search needs it
-    auto upd = [&](int r, int c) {
-      const T x = N::ld(xh, xl, r + jj * ch);
-      N::st(xh, xl, r + c * ch, N::add(N::ld(xh, xl, r + c * ch), N::mul(x, N::neg(N::ld(ph, pl, c)))));
-    };
-    for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) upd(r, jj + 1);
-    __syncthreads();
-    publish(jj + 1, jj + 1);
+    PANEL_T(jj, 4);
+    if (warp < 3) publish(jj + 1, jj + 1);
+    PANEL_T(jj, 5);
     arrive();
-    // the rest of the rank-1 update overlaps the other CTAs' arrival
-    const int ncol = nb - jj - 2, nrow = nr - rs;
-    if (ncol > 0 && nrow > 0)
-      for (int t = threadIdx.x; t < ncol * nrow; t += blockDim.x) upd(rs + t % nrow, jj + 2 + t / nrow);
+    PANEL_T(jj, 6);
+    // column jj + 2 of step jj's update now (the next step's first update
+    // needs it); the other columns go to the other warps in the shadow of
+    // the next step's key merge (the deferral keeps every element's update
+    // order: step jj before step jj + 1)
+    if (jj + 2 < nb)
+      for (int r = rs + threadIdx.x; r < nr; r += blockDim.x) upd(r, jj + 2, jj);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < nr * nb; t += blockDim.x) {
@@ -674,8 +777,8 @@ cudaError_t launch_getrf_panel(const GetrfArgs& g, int64_t j0, int nb, cudaStrea
     chunk = rows < 32 ? rows : 32;
     grid = (int)((rows + chunk - 1) / chunk);
   }
-  if (chunk <= kSmemRowsMax) {
-    const size_t smem = sizeof(double) * (2 * (size_t)chunk * nb + 2 * (size_t)nb);
+  if (chunk <= kSmemRowsMax && nb <= kPanelMaxNb) {
+    const size_t smem = sizeof(double) * (2 * (size_t)(chunk | 1) * nb + 4 * (size_t)nb);
     // A cooperative launch guarantees co-residency but may wait for an idle
     // device; with grid <= one CTA per SM an ordinary launch also completes
     // (the other stream's CTAs always retire), and can overlap the trailing
