@@ -238,19 +238,6 @@ __device__ __forceinline__ SKey skey_of(typename N::T v, long long idx) {
   b ^= (b >> 63) ? ~0ull : (1ull << 63);
   return SKey{(unsigned long long)__double_as_longlong(N::key_hi(v)), b, idx};
 }
-// block-wide best (all threads get it); every thread passes its key
-__device__ __forceinline__ SKey skey_block_best(SKey k) {
-  __shared__ SKey red[kPanelThreads / 32];
-  for (int o = 16; o > 0; o >>= 1) k = skey_merge(k, skey_shfl_down(k, o));
-  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-  __syncthreads();
-  if (l == 0) red[w] = k;
-  __syncthreads();
-  SKey r = red[0];
-#pragma unroll
-  for (int i = 1; i < kPanelThreads / 32; ++i) r = skey_merge(r, red[i]);
-  return r;
-}
 
 __device__ __forceinline__ void named_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kPanelThreads) : "memory");

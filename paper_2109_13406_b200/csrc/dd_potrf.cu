@@ -25,12 +25,14 @@
 //   * upper: temp accumulates from ZERO, so the trailing updates go to a
 //     separate accumulator S (lower-stored, S(jj, j) for U(j, jj)) by
 //     Rsyrk('L', 'N', alpha = 1, beta = 1) on T = U12^T;
-//   * per block: potrf_diag_kernel factors the diagonal block in one CTA
-//     (right-looking, a barrier per column; the pivots are the only serial
-//     chain), potrf_panel_kernel the rows below it ('U': the columns right of
-//     it), each row an independent sequence over the block's columns run by
-//     a group of lanes; block width <= 64 (the diagonal block lives in
-//     shared memory).
+//   * per middle panel (<= 256 columns): its diagonal block by 64-column
+//     inner blocks -- potrf_diag_kernel factors the inner diagonal block in
+//     one CTA (right-looking, a barrier per column; the pivots are the only
+//     serial chain), potrf_rows_kernel the diagonal block's rows below it,
+//     potrf_blockupd_kernel the rest of the diagonal block -- then every row
+//     below the panel ('U': column right of it) in one potrf_rows_kernel
+//     launch against all of the panel's columns, each row an independent
+//     sequence run by a warp.
 // So in exact mode (Rsyrk exact) the factor is bit-identical to the
 // reference for operands inside the safe window; fast / twosum modes differ
 // only by their Rsyrk accumulation.  On failure the device info is set,
