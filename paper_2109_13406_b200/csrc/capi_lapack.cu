@@ -617,6 +617,7 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
   PotrfArgs p{};
   p.n = n; p.lda = lda; p.upper = upflag(uplo) == 'U';
   p.f64 = f64;
+  p.fastacc = !f64 && (mode == DDB_MODE_FAST || mode == DDB_MODE_TWOSUM);
   p.a_hi = a_hi; p.a_lo = a_lo;
   // workspace: info | D, d0 (dd vectors), rec (MB dd: the middle panel's
   // reciprocals) | backup ('L') or S ('U'), n x n dd | 'U': the middle

@@ -229,7 +229,29 @@ constexpr int kRowsThreads = 256;    // 8 rows per CTA
 #ifndef DDB_ROWS_SEL
 #define DDB_ROWS_SEL 0       // 1: the ordered-Fast2Sum add (fewer FP64 ops, more selects; 86.8 vs 86.0 ms)
 #endif
-enum RowsMode { RK_SLOW = 0, RK_CHECK = 1, RK_FAST = 2 };
+enum RowsMode { RK_SLOW = 0, RK_CHECK = 1, RK_FAST = 2, RK_TWOSUM = 3 };
+
+// RK_TWOSUM (fast / twosum modes): the accumulators are unnormalised (H, L)
+// pairs -- per product p = xh yh, its FMA residual and the cross terms go to
+// L together with TwoSum(H, p)'s error: 13 FP64 operations instead of the
+// exact-order add2(mul2()) 29, the TwoSum mode's error bound (every rounding
+// lands in L, |L| ~ u |H|).  Normalised when an entry is finalised.
+__device__ __forceinline__ dd ts_mac(dd acc, dd x, dd y) {
+  const double p = dmul(x.h, y.h);
+  const double e = dfma(x.h, y.h, -p);
+  const double c = dfma(x.h, y.l, dmul(x.l, y.h));
+  double s, err;
+  two_sum(acc.h, p, s, err);
+  return dd{s, dadd(acc.l, dadd(err, dadd(e, c)))};
+}
+__device__ __forceinline__ dd ts_norm(dd a) {
+  double s, e;
+  quick_two_sum(a.h, a.l, s, e);
+  return dd{s, e};
+}
+// binary64 instantiations never select RK_TWOSUM (fastacc is dd only)
+__device__ __forceinline__ double ts_mac(double acc, double x, double y) { return dadd(acc, dmul(x, y)); }
+__device__ __forceinline__ double ts_norm(double a) { return a; }
 
 template <class N>
 __device__ __forceinline__ typename N::T rfadd(typename N::T x, typename N::T y) {
@@ -268,12 +290,28 @@ __device__ __forceinline__ void rows_steps(const PotrfArgs& p, int64_t j0, int w
       if (c + 1 < ncols) fetch(cc + 1 < 32 ? s : s + 1);
       // finalise entry c: every lane forms it from its own chain-s
       // accumulator, the owner's (lane cc) is broadcast and stored
-      const T a = UP ? N::add(au[s], N::neg(acc[s])) : acc[s];
+      T as = acc[s];
+      if constexpr (MODE == RK_TWOSUM) as = ts_norm(as);
+      const T a = UP ? N::add(au[s], N::neg(as)) : as;
       const T v = N::shfl(N::mul(rec_s[c], a), cc);
       if (lane == cc) N::st(p.a_hi, p.a_lo, UP ? (j0 + c) + q * lda : q + (j0 + c) * lda, v);
       // extend the later columns.  Lanes whose chain-s column is already
       // final (c2 <= c) and lanes past w update too: those accumulators are
       // never read again, so no per-lane predicate is needed
+      if constexpr (MODE == RK_TWOSUM) {
+        if (N::win(v)) {                              // warp-uniform
+          dq = ts_mac(dq, v, v);
+#pragma unroll
+          for (int i = s; i < NPER; ++i) acc[i] = UP ? ts_mac(acc[i], v, t[i]) : ts_mac(acc[i], N::neg(t[i]), v);
+        } else {                                      // checked forms on normalised values
+          dq = N::add(ts_norm(dq), N::mul(v, v));
+#pragma unroll
+          for (int i = s; i < NPER; ++i)
+            acc[i] = UP ? N::add(ts_norm(acc[i]), N::mul(v, t[i]))
+                        : N::add(ts_norm(acc[i]), N::mul(N::neg(t[i]), v));
+        }
+        continue;
+      }
       if (MODE != RK_SLOW && N::win(v)) {           // warp-uniform
         dq = rfadd<N>(dq, N::fmul(v, v));
 #pragma unroll
@@ -337,7 +375,10 @@ potrf_rows_kernel(PotrfArgs p, int64_t j0, int w, int64_t q0, int64_t q1,
     rows_steps<N, NPER, UP, RK_SLOW>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
   else if (pmask == nullptr)
     rows_steps<N, NPER, UP, RK_CHECK>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
-  else
+  else if (p.fastacc) {
+    rows_steps<N, NPER, UP, RK_TWOSUM>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
+    dq = ts_norm(dq);
+  } else
     rows_steps<N, NPER, UP, RK_FAST>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
   if (lane == 0) N::st(p.dh, p.dl, q, dq);
 }

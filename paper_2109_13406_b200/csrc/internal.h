@@ -187,6 +187,7 @@ struct PotrfArgs {
   double *t_hi, *t_lo;          // upper: the transposed panel U12^T
   const double *b_hi, *b_lo;    // lower: backup of the input (ld = n)
   double *rec_hi, *rec_lo;      // the current inner block's pivot reciprocals
+  int fastacc;                  // fast / twosum modes: TwoSum accumulation in the panel rows
   int* info;                    // device: first failing pivot + 1, or 0
 };
 
