@@ -274,6 +274,7 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
   g.m = m; g.n = n; g.mn = m < n ? m : n; g.lda = lda;
   g.a_hi = a_hi; g.a_lo = a_lo;
   g.f64 = f64;
+  g.fastacc = !f64 && (mode == DDB_MODE_FAST || mode == DDB_MODE_TWOSUM);
   const int G = getrf_max_panel_ctas();
   // workspace: info, barrier | ipiv, swap (mn each) | G partial candidates
   // partial candidates and rows: two parities (getrf_panel_smem_kernel)

@@ -634,7 +634,25 @@ getrf_trsm_kernel(GetrfArgs g, int64_t j0, int nb, int64_t c0, int64_t c1) {
 // predicates.  L is read through L1 one step ahead; the check-free forms run
 // while the step is inside the safe window (mask: L block rows, from
 // launch_window_mask; the starting column; each broadcast value).
-template <class N, int NPER>
+// TwoSum accumulation (fast / twosum modes, as potrf_rows_kernel's
+// RK_TWOSUM): unnormalised (H, L), 13 FP64 operations per product
+__device__ __forceinline__ dd ts_mac(dd acc, dd x, dd y) {
+  const double p = dmul(x.h, y.h);
+  const double e = dfma(x.h, y.h, -p);
+  const double c = dfma(x.h, y.l, dmul(x.l, y.h));
+  double s, err;
+  two_sum(acc.h, p, s, err);
+  return dd{s, dadd(acc.l, dadd(err, dadd(e, c)))};
+}
+__device__ __forceinline__ dd ts_norm(dd a) {
+  double s, e;
+  quick_two_sum(a.h, a.l, s, e);
+  return dd{s, e};
+}
+__device__ __forceinline__ double ts_mac(double acc, double x, double y) { return dadd(acc, dmul(x, y)); }
+__device__ __forceinline__ double ts_norm(double a) { return a; }
+
+template <class N, int NPER, bool TS>
 __global__ void __launch_bounds__(256)
 getrf_u12_kernel(GetrfArgs g, int64_t j0, int w, int64_t c0, int64_t c1,
                  const unsigned* __restrict__ lmask) {
@@ -659,6 +677,7 @@ getrf_u12_kernel(GetrfArgs g, int64_t j0, int w, int64_t c0, int64_t c1,
     }
   }
   const bool fast_ok = __all_sync(0xffffffffu, ok);
+  const bool ts = TS && fast_ok;             // TwoSum only on an all-in-window column
   T tn[NPER];
 #pragma unroll
   for (int i = 0; i < NPER; ++i) tn[i] = N::zero();
@@ -678,10 +697,18 @@ getrf_u12_kernel(GetrfArgs g, int64_t j0, int w, int64_t c0, int64_t c1,
 #pragma unroll
       for (int i = s; i < NPER; ++i) lv[i] = tn[i];
       if (t + 1 < w) fetch(t + 1, tt + 1 < 32 ? s : s + 1);
-      const T u = N::shfl(acc[s], tt);       // U(j0 + t, c): final
+      T as = acc[s];
+      if (ts) as = ts_norm(as);
+      const T u = N::shfl(as, tt);           // U(j0 + t, c): final
       if (lane == tt) N::st(uh, ul, t, u);
       const T nu = N::neg(u);
-      if (fast_ok && N::win(u)) {            // warp-uniform
+      if (ts && N::win(u)) {                 // fast modes: TwoSum accumulation
+#pragma unroll
+        for (int i = s; i < NPER; ++i) acc[i] = ts_mac(acc[i], lv[i], nu);
+      } else if (ts) {
+#pragma unroll
+        for (int i = s; i < NPER; ++i) acc[i] = N::add(ts_norm(acc[i]), N::mul(lv[i], nu));
+      } else if (fast_ok && N::win(u)) {     // warp-uniform
 #pragma unroll
         for (int i = s; i < NPER; ++i) acc[i] = N::fadd2(acc[i], N::fmul(lv[i], nu));
       } else {
@@ -696,7 +723,9 @@ template <class N, int NPER>
 static cudaError_t u12_launch(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
                               const unsigned* lmask, cudaStream_t s) {
   const int64_t threads = (c1 - c0) * 32;
-  getrf_u12_kernel<N, NPER><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(g, j0, w, c0, c1, lmask);
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  if (g.fastacc) getrf_u12_kernel<N, NPER, true><<<grid, 256, 0, s>>>(g, j0, w, c0, c1, lmask);
+  else getrf_u12_kernel<N, NPER, false><<<grid, 256, 0, s>>>(g, j0, w, c0, c1, lmask);
   return cudaGetLastError();
 }
 

@@ -247,6 +247,7 @@ struct GetrfArgs {
   int* part_nan;
   unsigned* bar;                // grid barrier counter
   double* rowbuf;               // candidate rows and row j, two parities (dd_getrf.cu)
+  int fastacc;                  // fast / twosum modes: TwoSum accumulation in the U12 kernel
 };
 
 int getrf_max_panel_ctas();
