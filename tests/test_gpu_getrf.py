@@ -84,6 +84,31 @@ def test_rgetrf_exact_matches_oracle_multipanel(m, n, special):
     assert bits_equal(gh, oh) and bits_equal(gl, ol)
 
 
+def test_rgetrf_out_of_window_rows_exact_matches_oracle():
+    """Rows / columns scaled by 2^+-350: the panel's check-free updates and
+    the U12 kernel's window mask fall back to the checked forms on them --
+    still bitwise vs the oracle across several 256-column blocks."""
+    m = n = 600
+    ld = m + 1
+    hi, lo = _inputs(m, n, ld, seed=99)
+    rs = np.ones(m)
+    cs = np.ones(n)
+    for i, e in ((3, 350), (290, -350), (411, 330)):
+        rs[i] = 2.0 ** e
+    for j, e in ((7, -340), (300, 350), (520, -300)):
+        cs[j] = 2.0 ** e
+    for c in range(n):
+        sl = slice(c * ld, c * ld + m)
+        hi[sl] *= rs * cs[c]       # exact: powers of two
+        lo[sl] *= rs * cs[c]
+    ipiv, info, gh, gl = run(m, n, ld, hi, lo, "exact")
+    oh, ol = hi.copy(), lo.copy()
+    rc, oipiv, oinfo = oracle.rgetrf(m, n, oh, ol, ld)
+    assert rc == 0
+    assert ipiv == oipiv and info == oinfo
+    assert bits_equal(gh, oh) and bits_equal(gl, ol)
+
+
 @pytest.mark.parametrize("mode", ["fast", "twosum"])
 @pytest.mark.parametrize("m,n", [(320, 320), (500, 200), (200, 500)])
 def test_rgetrf_fast_modes_close_to_exact(m, n, mode):
