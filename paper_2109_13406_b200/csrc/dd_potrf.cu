@@ -59,7 +59,7 @@ namespace ddb {
 // forms, bit-identical there.
 #ifdef DDB_DIAG_TIMING
 // diagnostics build only: per-step clock64 stamps of the last diagonal block
-__device__ long long g_diag_t[64][5];
+__device__ long long g_diag_t[64][8];
 #define DIAG_T(j, k) (g_diag_t[j][k] = clock64())
 #else
 #define DIAG_T(j, k) ((void)0)
@@ -113,15 +113,18 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
     const T ajj = N::ssub(N::ld(d0h, d0l, j), N::ld(dh, dl, j));   // chol.py:41
     const int64_t djj = (j0 + j) * (lda + 1);
     ok_s = !N::bad_pivot(ajj);
+    DIAG_T(j, 5);
     if (!ok_s) {
       N::st(p.a_hi, p.a_lo, djj, ajj);
       *p.info = (int)(j0 + j + 1);
     } else {
       const T s = N::ssqrt(ajj);
       N::st(p.a_hi, p.a_lo, djj, s);
+      DIAG_T(j, 6);
       const T rec = N::sdiv(N::one(), s);
       rec_s = rec;
       N::st(p.rec_hi, p.rec_lo, j, rec);
+      DIAG_T(j, 7);
     }
   };
   if (threadIdx.x == 0) pivot(0);
