@@ -560,7 +560,25 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // costs than the kernel gains: measured Rpotrf / Rgetrf / Rtrsm at n = 8192
   // 1-3 % slower with the split at k = 256; Rsyrk n = k = 4096 4.5 % faster.
   const int policy = split_policy();
-  bool split_alg = alg == ALG_CERT && policy != 0 && (policy == 2 || g.k >= 1024);
+  int dev0 = 0, sms0 = 148;
+  cudaGetDevice(&dev0);
+  cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+  // shallow but wide calls (the LAPACK consumers' depth-256 bulk updates:
+  // k >= 256 and >= 2 waves of split tiles) split too, on the serial
+  // schedule: 7936 x 7680 x 256 takes 8.47 ms split vs 9.06 ms certified
+  // (the concurrent schedule's extra C pass, 8.79 ms, does not pay at this
+  // depth); Rgetrf n = 8192 153.8 -> 145.6 ms, Rpotrf 80.0 -> 75.2 ms
+  const int64_t big_tiles = ((g.m + BM - 1) / BM) * ((g.n + SPLIT_BN - 1) / SPLIT_BN);
+  static const int sw_k = [] {
+    const char* v = std::getenv("DDB_SHALLOW_SPLIT_K");
+    return v ? std::atoi(v) : 256;
+  }();
+  static const int sw_t = [] {
+    const char* v = std::getenv("DDB_SHALLOW_SPLIT_WAVES");
+    return v ? std::atoi(v) : 2;
+  }();
+  const bool shallow_wide = g.k >= sw_k && g.k < 1024 && big_tiles >= sw_t * (int64_t)sms0;
+  bool split_alg = alg == ALG_CERT && policy != 0 && (policy == 2 || g.k >= 1024 || shallow_wide);
   double* xbuf = nullptr;
   int64_t xchunk = g.k;
   const int xslices = split_alg ? cross_kslices(g, &xchunk) : 1;
@@ -592,7 +610,7 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // alpha * X to C.  With split-K the partial sums take X in slice 0 instead
   // (cross first, then the kernel).  DDB_CROSS_SERIAL=1: always the latter.
   static const bool cross_serial = std::getenv("DDB_CROSS_SERIAL") != nullptr;
-  const bool concurrent = split_alg && splits == 1 && !cross_serial;
+  const bool concurrent = split_alg && splits == 1 && !cross_serial && !shallow_wide;
   cudaStream_t s2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   if (split_alg) {

@@ -160,3 +160,37 @@ def test_split_rsyrk_full_triangle_matches_cert(uplo, trans):
 class _S:
     def __init__(self, v):
         self.hi, self.lo = float(v[0]), float(v[1])
+
+
+@pytest.mark.parametrize("kind", ["uniform", "graded", "cancel"])
+@pytest.mark.parametrize("syrk", [False, True])
+def test_shallow_wide_default_policy_split_serial(monkeypatch, kind, syrk):
+    """The default policy (no DDB_SPLIT) splits shallow wide calls (256 <= k
+    < 1024, >= 2 waves of tiles: the LAPACK consumers' bulk updates) on the
+    serial schedule: inside the bound; Rsyrk leaves the other triangle
+    untouched."""
+    monkeypatch.delenv("DDB_SPLIT", raising=False)
+    m = n = 2048
+    k = 300
+    A, B = _pattern(kind, m, n, k, 11)
+    C = random_dd(m, n, m, 6, 3)
+    alpha, beta = (1.5, 0.0), (0.5, 0.0)
+    a, c = dev(m, k, m, A), dev(m, n, m, C)
+    if syrk:
+        Rsyrk("L", "N", n, k, alpha[0], a, m, beta[0], c, m, mode="fast")
+        tb, Bp, ldb = "T", A, m
+        I, J = list(range(1031, m, 97)), list(range(0, 1024, 89))   # all i >= j
+    else:
+        Rgemm("N", "N", m, n, k, alpha[0], a, m, dev(k, n, k, B), k, beta[0], c, m, mode="fast")
+        tb, Bp, ldb = "N", B, k
+        I, J = list(range(3, m, 97)), list(range(0, n, 89))
+    assert _lib.last_route() in (1, 5)
+    gh, gl = c.store[0].cpu().numpy(), c.store[1].cpu().numpy()
+    vals, scales = exact.exact_entries("N", tb, k, alpha, A[0], A[1], m, Bp[0], Bp[1], ldb,
+                                       beta, C[0], C[1], m, I, J)
+    worst = exact.error_ratios(gh, gl, m, I, J, vals, scales, k, c=C_SPLIT)
+    assert worst <= 1.0, worst
+    if syrk:
+        r, cc = np.meshgrid(np.arange(m), np.arange(n), indexing="ij")
+        upper = (r < cc).T.reshape(-1)     # column-major flat index
+        assert _bits_equal(gh[upper], C[0][upper]) and _bits_equal(gl[upper], C[1][upper])
