@@ -367,6 +367,11 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
         if (r != DDB_OK) return r;
       }
     }
+    if (J1 - J0 <= ib && c1 - c0 <= 256 && m > J1) {   // an inner panel's update: one lean launch
+      er = launch_getrf_inner_upd(g, J0, (int)(J1 - J0), J1, m, c0, c1, st);
+      ++nl;
+      return er == cudaSuccess ? DDB_OK : fail(er, "rgetrf inner update");
+    }
     return gemm(J1, m, c0, c1, J0, J1, st);
   };
   // factor the outer panel [J0, J1) (its columns only) on `cs`

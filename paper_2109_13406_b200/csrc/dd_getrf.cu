@@ -719,6 +719,80 @@ getrf_u12_kernel(GetrfArgs g, int64_t j0, int w, int64_t c0, int64_t c1,
   }
 }
 
+// The inner panels' trailing update inside an outer block row, A(r, c) +=
+// L(r, l) (-U(l, c)) for rows [r0, r1), columns [c0, c1) (<= 256), l < kb
+// (<= 64), as one lean launch instead of an Rgemm call (~10 launches of
+// routing / bound / split machinery around a k = 64 tile that the TMA kernel
+// runs in ~66 us).  CTA: 128 rows (one per thread) x 8 columns, the 8 x kb
+// slice of U staged in shared memory with a window flag.  Per element the
+// products arrive in l order: exact mode the check-free add2(mul2(L, -U))
+// inside the safe window (bit-identical to the checked forms and to the
+// alpha = -1 Rgemm it replaces), the checked forms otherwise; fast / twosum
+// modes the TwoSum accumulation (ts_mac) inside the window.
+template <class N, bool TS>
+__global__ void __launch_bounds__(128)
+getrf_inner_upd_kernel(GetrfArgs g, int64_t l0, int kb, int64_t r0, int64_t r1, int64_t c0,
+                       int64_t c1) {
+  using T = typename N::T;
+  constexpr int CW = 8;
+  __shared__ T us[kPanelMaxNb][CW];
+  __shared__ int uok;
+  const int64_t lda = g.lda;
+  const int64_t cb = c0 + (int64_t)blockIdx.y * CW;
+  if (threadIdx.x == 0) uok = 1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < kb * CW; e += blockDim.x) {
+    const int l = e % kb, cc = e / kb;
+    T u = N::zero();
+    if (cb + cc < c1) u = N::ld(g.a_hi, g.a_lo, (l0 + l) + (cb + cc) * lda);
+    us[l][cc] = N::neg(u);
+    if (!N::win(u)) uok = 0;
+  }
+  __syncthreads();
+  const int64_t r = r0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  T acc[CW];
+  bool ok = uok != 0 && !N::kF64;
+#pragma unroll
+  for (int cc = 0; cc < CW; ++cc) {
+    acc[cc] = N::zero();
+    if (cb + cc < c1) {
+      acc[cc] = N::ld(g.a_hi, g.a_lo, r + (cb + cc) * lda);
+      ok &= N::win(acc[cc]);
+    }
+  }
+  T ln = N::ld(g.a_hi, g.a_lo, r + l0 * lda);
+  for (int l = 0; l < kb; ++l) {
+    const T lv = ln;
+    if (l + 1 < kb) ln = N::ld(g.a_hi, g.a_lo, r + (l0 + l + 1) * lda);
+    if (ok && N::win(lv)) {
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc)
+        acc[cc] = TS ? ts_mac(acc[cc], lv, us[l][cc]) : N::fadd2(acc[cc], N::fmul(lv, us[l][cc]));
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc) {
+        const T a = TS ? ts_norm(acc[cc]) : acc[cc];
+        acc[cc] = N::add(a, N::mul(lv, us[l][cc]));
+      }
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < CW; ++cc)
+    if (cb + cc < c1) N::st(g.a_hi, g.a_lo, r + (cb + cc) * lda, TS ? ts_norm(acc[cc]) : acc[cc]);
+}
+
+cudaError_t launch_getrf_inner_upd(const GetrfArgs& g, int64_t l0, int kb, int64_t r0, int64_t r1,
+                                   int64_t c0, int64_t c1, cudaStream_t s) {
+  if (r1 <= r0 || c1 <= c0 || kb <= 0) return cudaSuccess;
+  if (kb > kPanelMaxNb) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((r1 - r0 + 127) / 128), (unsigned)((c1 - c0 + 7) / 8));
+  if (g.f64) getrf_inner_upd_kernel<NumF64, false><<<grid, 128, 0, s>>>(g, l0, kb, r0, r1, c0, c1);
+  else if (g.fastacc) getrf_inner_upd_kernel<NumDD, true><<<grid, 128, 0, s>>>(g, l0, kb, r0, r1, c0, c1);
+  else getrf_inner_upd_kernel<NumDD, false><<<grid, 128, 0, s>>>(g, l0, kb, r0, r1, c0, c1);
+  return cudaGetLastError();
+}
+
 template <class N, int NPER>
 static cudaError_t u12_launch(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
                               const unsigned* lmask, cudaStream_t s) {

@@ -262,6 +262,10 @@ cudaError_t launch_getrf_apply(const GetrfArgs& g, const PermBuf& pb, int64_t ns
                                int64_t c1, cudaStream_t s);
 cudaError_t launch_getrf_trsm(const GetrfArgs& g, int64_t j0, int nb, int64_t c0, int64_t c1,
                               cudaStream_t s);
+// A(r, c) += L(r, l) (-U(l, c)), rows [r0, r1), columns [c0, c1), l in [l0,
+// l0 + kb), kb <= 64: the inner panels' update (dd_getrf.cu)
+cudaError_t launch_getrf_inner_upd(const GetrfArgs& g, int64_t l0, int kb, int64_t r0, int64_t r1,
+                                   int64_t c0, int64_t c1, cudaStream_t s);
 // U12 of rows [j0, j0 + w) (w <= 256), columns [c0, c1), in one launch;
 // lmask: 8 words of scratch (dd_getrf.cu)
 cudaError_t launch_getrf_u12(const GetrfArgs& g, int64_t j0, int w, int64_t c0, int64_t c1,
