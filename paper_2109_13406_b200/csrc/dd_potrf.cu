@@ -334,7 +334,10 @@ __device__ __forceinline__ void rows_steps(const PotrfArgs& p, int64_t j0, int w
   }
 }
 
-template <class N, int NPER, bool UP>
+// FA: the fast / twosum modes' instantiation (RK_TWOSUM on the masked
+// panel), else the exact modes' (RK_FAST): one accumulation form per
+// kernel keeps its code and register use down
+template <class N, int NPER, bool UP, bool FA>
 __global__ void __launch_bounds__(kRowsThreads, DDB_ROWS_MINB)
 potrf_rows_kernel(PotrfArgs p, int64_t j0, int w, int64_t q0, int64_t q1,
                   const double* __restrict__ ph, const double* __restrict__ pl, int sr, int sc,
@@ -378,7 +381,7 @@ potrf_rows_kernel(PotrfArgs p, int64_t j0, int w, int64_t q0, int64_t q1,
     rows_steps<N, NPER, UP, RK_SLOW>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
   else if (pmask == nullptr)
     rows_steps<N, NPER, UP, RK_CHECK>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
-  else if (p.fastacc) {
+  else if constexpr (FA) {
     rows_steps<N, NPER, UP, RK_TWOSUM>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
     dq = ts_norm(dq);
   } else
@@ -516,12 +519,14 @@ static cudaError_t rows_launch(const PotrfArgs& p, int64_t j0, int w, int64_t q0
                                cudaStream_t s) {
   const int64_t threads = (q1 - q0) * 32;
   const unsigned grid = (unsigned)((threads + kRowsThreads - 1) / kRowsThreads);
-  if (p.upper)
-    potrf_rows_kernel<N, NPER, true><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc,
-                                                                   rh, rl, pmask);
-  else
-    potrf_rows_kernel<N, NPER, false><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc,
-                                                                    rh, rl, pmask);
+  const bool fa = p.fastacc && pmask != nullptr;
+  if (p.upper) {
+    if (fa) potrf_rows_kernel<N, NPER, true, true><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask);
+    else potrf_rows_kernel<N, NPER, true, false><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask);
+  } else {
+    if (fa) potrf_rows_kernel<N, NPER, false, true><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask);
+    else potrf_rows_kernel<N, NPER, false, false><<<grid, kRowsThreads, 0, s>>>(p, j0, w, q0, q1, ph, pl, sr, sc, rh, rl, pmask);
+  }
   return cudaGetLastError();
 }
 
