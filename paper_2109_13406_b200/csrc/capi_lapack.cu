@@ -703,6 +703,22 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
     const int64_t kb = j1 - j0, wd = c1 - c0, below = n - c1;
     void* sv = static_cast<void*>(st);
     int r;
+    // fast modes, a narrow block column with few rows: one lean launch
+    static const int64_t lean_rows = [] {
+      const char* v = std::getenv("DDB_POTRF_LEAN_ROWS");
+      return v ? (int64_t)std::atoll(v) : (int64_t)3072;
+    }();
+    if (p.fastacc && kb <= 256 && wd <= 256 && n - c0 <= lean_rows) {
+      cudaError_t er;
+      if (!p.upper)
+        er = launch_potrf_lean_upd(a_hi + j0 * lda, a_lo + j0 * lda, lda, (int)kb, -1.0, a_hi, a_lo,
+                                   lda, c0, n, c0, (int)wd, p.info, st);
+      else
+        er = launch_potrf_lean_upd(th - tb0, tl - tb0, n - tb0, (int)kb, 1.0, p.s_hi, p.s_lo, n, c0,
+                                   n, c0, (int)wd, p.info, st);
+      ++nl;
+      return er == cudaSuccess ? DDB_OK : fail(er, "rpotrf update");
+    }
     if (!p.upper) {
       const double *lh = a_hi + j0 * lda, *ll = a_lo + j0 * lda;
       r = syrk_any(f64, 'L', 'N', wd, kb, -1.0, 0.0, lh + c0, ll + c0, lda, 1.0, 0.0,

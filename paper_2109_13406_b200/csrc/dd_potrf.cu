@@ -448,6 +448,76 @@ potrf_blockupd_kernel(PotrfArgs p, int64_t i0, int64_t i1, int64_t j1) {
   }
 }
 
+// Fast / twosum modes, late in the factorization: the lookahead update of
+// the next (<= 256-column) block column as one lean launch instead of an
+// Rsyrk and an Rgemm call (each ~10 launches of routing / bound / split
+// machinery: ~0.12 ms apiece for a few microseconds of work).  C(r, c) +=
+// sgn F(c, l) F(r, l), l < kb, for rows [r0, r1) and columns [c0, c0 + wd),
+// c <= r; F(x, l) at fh[x + l ldf].  CTA: 128 rows (one per thread) x 8
+// columns with the columns' F(c, :) slice in shared memory; the TwoSum
+// accumulation while the operands are inside the safe window, the checked
+// dd forms otherwise.
+__global__ void __launch_bounds__(128)
+potrf_lean_upd_kernel(const double* __restrict__ fh, const double* __restrict__ fl, int64_t ldf,
+                      int kb, double sgn, double* __restrict__ ch, double* __restrict__ cl,
+                      int64_t ldc, int64_t r0, int64_t r1, int64_t c0, int wd,
+                      const int* __restrict__ info) {
+  constexpr int CW = 8, KMAX = 256;
+  __shared__ dd fs[KMAX][CW];
+  __shared__ int fok;
+  if (*info != 0) return;                    // a failed factorization: the restore pass owns the rest
+  const int64_t cb = c0 + (int64_t)blockIdx.y * CW;
+  const int64_t rbase = r0 + (int64_t)blockIdx.x * blockDim.x;
+  if (rbase + blockDim.x - 1 < cb) return;   // the whole tile lies above the diagonal
+  if (threadIdx.x == 0) fok = 1;
+  __syncthreads();
+  for (int e = threadIdx.x; e < kb * CW; e += blockDim.x) {
+    const int l = e / CW, cc = e % CW;
+    dd f{0.0, 0.0};
+    if (cb + cc < c0 + wd) f = NumDD::ld(fh, fl, cb + cc + (int64_t)l * ldf);
+    fs[l][cc] = dd{sgn * f.h, sgn * f.l};
+    if (!NumDD::win(f)) fok = 0;
+  }
+  __syncthreads();
+  const int64_t r = rbase + threadIdx.x;
+  if (r >= r1) return;
+  dd acc[CW];
+  bool ok = fok != 0;
+#pragma unroll
+  for (int cc = 0; cc < CW; ++cc) {
+    acc[cc] = dd{0.0, 0.0};
+    if (cb + cc < c0 + wd && cb + cc <= r) {
+      acc[cc] = NumDD::ld(ch, cl, r + (cb + cc) * ldc);
+      ok &= NumDD::win(acc[cc]);
+    }
+  }
+  dd fn = NumDD::ld(fh, fl, r);
+  for (int l = 0; l < kb; ++l) {
+    const dd fr = fn;
+    if (l + 1 < kb) fn = NumDD::ld(fh, fl, r + (int64_t)(l + 1) * ldf);
+    if (ok && NumDD::win(fr)) {
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc) acc[cc] = ts_mac(acc[cc], fs[l][cc], fr);
+    } else {
+#pragma unroll
+      for (int cc = 0; cc < CW; ++cc) acc[cc] = NumDD::add(ts_norm(acc[cc]), NumDD::mul(fs[l][cc], fr));
+    }
+  }
+#pragma unroll
+  for (int cc = 0; cc < CW; ++cc)
+    if (cb + cc < c0 + wd && cb + cc <= r) NumDD::st(ch, cl, r + (cb + cc) * ldc, ts_norm(acc[cc]));
+}
+
+cudaError_t launch_potrf_lean_upd(const double* fh, const double* fl, int64_t ldf, int kb, double sgn,
+                                  double* ch, double* cl, int64_t ldc, int64_t r0, int64_t r1,
+                                  int64_t c0, int wd, const int* info, cudaStream_t s) {
+  if (r1 <= r0 || wd <= 0 || kb <= 0) return cudaSuccess;
+  if (kb > 256) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)((r1 - r0 + 127) / 128), (unsigned)((wd + 7) / 8));
+  potrf_lean_upd_kernel<<<grid, 128, 0, s>>>(fh, fl, ldf, kb, sgn, ch, cl, ldc, r0, r1, c0, wd, info);
+  return cudaGetLastError();
+}
+
 // T(r, l) = U(j0 + l, j1 + r), r < rows, l < nb  (ld = rows)
 __global__ void __launch_bounds__(256)
 potrf_transpose_kernel(PotrfArgs p, int64_t j0, int64_t j1, int nb, int64_t rows) {

@@ -202,6 +202,11 @@ cudaError_t launch_potrf_rows(const PotrfArgs& p, int64_t j0, int w, int64_t q0,
                               const double* rh, const double* rl, unsigned* pmask, cudaStream_t s);
 cudaError_t launch_potrf_blockupd(const PotrfArgs& p, int64_t i0, int64_t i1, int64_t j1,
                                   cudaStream_t s);
+// fast modes: C(r, c) += sgn F(c, l) F(r, l), rows [r0, r1), columns [c0, c0
+// + wd) with c <= r, l < kb <= 256 (dd_potrf.cu)
+cudaError_t launch_potrf_lean_upd(const double* fh, const double* fl, int64_t ldf, int kb, double sgn,
+                                  double* ch, double* cl, int64_t ldc, int64_t r0, int64_t r1,
+                                  int64_t c0, int wd, const int* info, cudaStream_t s);
 cudaError_t launch_potrf_transpose(const PotrfArgs& p, int64_t j0, int64_t j1, int nb,
                                    int64_t rows, cudaStream_t s);
 cudaError_t launch_potrf_restore(const PotrfArgs& p, cudaStream_t s);
