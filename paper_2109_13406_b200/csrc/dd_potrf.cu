@@ -65,7 +65,52 @@ __device__ long long g_diag_t[64][8];
 #define DIAG_T(j, k) ((void)0)
 #endif
 
-template <class N>
+// RK_TWOSUM (fast / twosum modes): the accumulators are unnormalised (H, L)
+// pairs -- per product p = xh yh, its FMA residual and the cross terms go to
+// L together with TwoSum(H, p)'s error: 13 FP64 operations instead of the
+// exact-order add2(mul2()) 29, the TwoSum mode's error bound (every rounding
+// lands in L, |L| ~ u |H|).  Normalised when an entry is finalised.
+__device__ __forceinline__ dd ts_mac(dd acc, dd x, dd y) {
+  const double p = dmul(x.h, y.h);
+  const double e = dfma(x.h, y.h, -p);
+  const double c = dfma(x.h, y.l, dmul(x.l, y.h));
+  double s, err;
+  two_sum(acc.h, p, s, err);
+  return dd{s, dadd(acc.l, dadd(err, dadd(e, c)))};
+}
+__device__ __forceinline__ dd ts_norm(dd a) {
+  double s, e;
+  quick_two_sum(a.h, a.l, s, e);
+  return dd{s, e};
+}
+// binary64 instantiations never select RK_TWOSUM (fastacc is dd only)
+__device__ __forceinline__ double ts_mac(double acc, double x, double y) { return dadd(acc, dmul(x, y)); }
+__device__ __forceinline__ double ts_norm(double a) { return a; }
+
+// Fast / twosum modes (FA): the pivot's square root and reciprocal by one
+// Newton correction each on the IEEE sqrt / reciprocal of the high word
+// (dd-accurate; ~500 instead of ~2100 cycles of the reference's scalar
+// forms), the trailing update with the TwoSum accumulation (entries stay
+// unnormalised until their column is finalised); both inside the safe
+// window only, the exact forms otherwise.
+__device__ __forceinline__ dd fast_sqrt_dd(dd a) {
+  const double y = __dsqrt_rn(a.h);
+  const double r = dadd(dfma(-y, y, a.h), a.l);
+  double s, e;
+  quick_two_sum(y, __ddiv_rn(r, dmul(2.0, y)), s, e);
+  return dd{s, e};
+}
+__device__ __forceinline__ dd fast_rec_dd(dd s) {
+  const double r0 = __drcp_rn(s.h);
+  const double e = dsub(dfma(-s.h, r0, 1.0), dmul(s.l, r0));
+  double h, l;
+  quick_two_sum(r0, dmul(r0, e), h, l);
+  return dd{h, l};
+}
+__device__ __forceinline__ double fast_sqrt_dd(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ double fast_rec_dd(double s) { return __ddiv_rn(1.0, s); }
+
+template <class N, bool FA>
 __global__ void __launch_bounds__(512)
 potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
   using T = typename N::T;
@@ -110,7 +155,9 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
   // thread 0 computes pivot j+1 while warps 1.. run step j's trailing
   // update (pivot j+1 needs only D(j+1), final after step j's column phase)
   auto pivot = [&](int j) {
-    const T ajj = N::ssub(N::ld(d0h, d0l, j), N::ld(dh, dl, j));   // chol.py:41
+    const T d0 = N::ld(d0h, d0l, j), dj = N::ld(dh, dl, j);
+    const bool fa = FA && nc_s && N::win(d0) && N::win(dj);
+    const T ajj = fa ? N::fadd2(d0, N::neg(dj)) : N::ssub(d0, dj);   // chol.py:41
     const int64_t djj = (j0 + j) * (lda + 1);
     ok_s = !N::bad_pivot(ajj);
     DIAG_T(j, 5);
@@ -118,10 +165,11 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
       N::st(p.a_hi, p.a_lo, djj, ajj);
       *p.info = (int)(j0 + j + 1);
     } else {
-      const T s = N::ssqrt(ajj);
+      const bool fs = fa && N::win(ajj);
+      const T s = fs ? fast_sqrt_dd(ajj) : N::ssqrt(ajj);
       N::st(p.a_hi, p.a_lo, djj, s);
       DIAG_T(j, 6);
-      const T rec = N::sdiv(N::one(), s);
+      const T rec = fs ? fast_rec_dd(s) : N::sdiv(N::one(), s);
       rec_s = rec;
       N::st(p.rec_hi, p.rec_lo, j, rec);
       DIAG_T(j, 7);
@@ -136,7 +184,8 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
     for (int q = j + 1 + threadIdx.x; q < nb; q += blockDim.x) {
       const int t = q + j * nb;
       T a = N::ld(xh, xl, t);
-      if (p.upper) a = N::add(a, N::neg(N::ld(sh, sl, t)));
+      if (FA && !p.upper) a = ts_norm(a);            // TwoSum-accumulated entry
+      if (p.upper) a = N::add(a, N::neg(FA ? ts_norm(N::ld(sh, sl, t)) : N::ld(sh, sl, t)));
       const T v = N::mul(rec, a);
       N::st(xh, xl, t, v);
       const bool f = nc_s && N::win(v);
@@ -182,7 +231,10 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
 #pragma unroll
         for (int b = 0; b < kB; ++b) {
           if (xs[b] < 0) continue;
-          const T r = fast ? N::fadd2(acc[b], N::fmul(f1[b], f2[b])) : N::add(acc[b], N::mul(f1[b], f2[b]));
+          T r;
+          if (FA && fast) r = ts_mac(acc[b], f1[b], f2[b]);
+          else if (fast) r = N::fadd2(acc[b], N::fmul(f1[b], f2[b]));
+          else r = N::add(FA ? ts_norm(acc[b]) : acc[b], N::mul(f1[b], f2[b]));
           if (!p.upper) N::st(xh, xl, xs[b], r);
           else N::st(sh, sl, xs[b], r);
         }
@@ -234,27 +286,6 @@ constexpr int kRowsThreads = 256;    // 8 rows per CTA
 #endif
 enum RowsMode { RK_SLOW = 0, RK_CHECK = 1, RK_FAST = 2, RK_TWOSUM = 3 };
 
-// RK_TWOSUM (fast / twosum modes): the accumulators are unnormalised (H, L)
-// pairs -- per product p = xh yh, its FMA residual and the cross terms go to
-// L together with TwoSum(H, p)'s error: 13 FP64 operations instead of the
-// exact-order add2(mul2()) 29, the TwoSum mode's error bound (every rounding
-// lands in L, |L| ~ u |H|).  Normalised when an entry is finalised.
-__device__ __forceinline__ dd ts_mac(dd acc, dd x, dd y) {
-  const double p = dmul(x.h, y.h);
-  const double e = dfma(x.h, y.h, -p);
-  const double c = dfma(x.h, y.l, dmul(x.l, y.h));
-  double s, err;
-  two_sum(acc.h, p, s, err);
-  return dd{s, dadd(acc.l, dadd(err, dadd(e, c)))};
-}
-__device__ __forceinline__ dd ts_norm(dd a) {
-  double s, e;
-  quick_two_sum(a.h, a.l, s, e);
-  return dd{s, e};
-}
-// binary64 instantiations never select RK_TWOSUM (fastacc is dd only)
-__device__ __forceinline__ double ts_mac(double acc, double x, double y) { return dadd(acc, dmul(x, y)); }
-__device__ __forceinline__ double ts_norm(double a) { return a; }
 
 template <class N>
 __device__ __forceinline__ typename N::T rfadd(typename N::T x, typename N::T y) {
@@ -571,14 +602,17 @@ cudaError_t launch_potrf_diag(const PotrfArgs& p, int64_t j0, int64_t j1, cudaSt
   int dev = 0;
   cudaGetDevice(&dev);
   if (attr_dev != dev) {
-    cudaFuncSetAttribute(potrf_diag_kernel<NumDD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(potrf_diag_kernel<NumDD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    cudaFuncSetAttribute(potrf_diag_kernel<NumF64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(potrf_diag_kernel<NumDD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    cudaFuncSetAttribute(potrf_diag_kernel<NumF64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
     attr_dev = dev;
   }
-  if (p.f64) potrf_diag_kernel<NumF64><<<1, 512, smem, s>>>(p, j0, nb);
-  else potrf_diag_kernel<NumDD><<<1, 512, smem, s>>>(p, j0, nb);
+  if (p.f64) potrf_diag_kernel<NumF64, false><<<1, 512, smem, s>>>(p, j0, nb);
+  else if (p.fastacc) potrf_diag_kernel<NumDD, true><<<1, 512, smem, s>>>(p, j0, nb);
+  else potrf_diag_kernel<NumDD, false><<<1, 512, smem, s>>>(p, j0, nb);
   return cudaGetLastError();
 }
 
