@@ -175,6 +175,38 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
       DIAG_T(j, 7);
     }
   };
+  // trailing-update ownership: every strictly-lower entry (q, c) of the
+  // block belongs to one thread of the warps off sub-partition 0 for the
+  // whole kernel and lives in its registers -- per step j the owner adds the
+  // product of column j's entries (c > j) and stores the entry once, when
+  // its column is next (c = j + 1).  No per-step index arithmetic and no
+  // shared-memory read-modify-write of the accumulators.
+  constexpr int kE = 6;                    // 6 x 384 >= 2016 entries (nb <= 64)
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const bool owner = (warp & 3) != 0;
+  const int nthr = (nw - (nw + 3) / 4) * 32;                  // warps not on sub-partition 0
+  const int me = (warp - warp / 4 - 1) * 32 + (threadIdx.x & 31);
+  int eq[kE], ec[kE];
+  T eacc[kE];
+  {
+    const int npairs = nb * (nb - 1) / 2;
+#pragma unroll
+    for (int k = 0; k < kE; ++k) {
+      const int t = me + k * nthr;
+      eq[k] = -1;
+      ec[k] = nb;
+      eacc[k] = N::zero();
+      if (owner && t < npairs) {
+        // column c of pair t, column-major over the strictly-lower triangle
+        int ci = (int)((2.0f * nb - 1.0f - sqrtf((2.0f * nb - 1.0f) * (2.0f * nb - 1.0f) - 8.0f * t)) * 0.5f);
+        while (ci > 0 && ci * (2 * nb - ci - 1) / 2 > t) --ci;
+        while ((ci + 1) * (2 * nb - ci - 2) / 2 <= t) ++ci;
+        eq[k] = ci + 1 + (t - ci * (2 * nb - ci - 1) / 2);
+        ec[k] = ci;
+        eacc[k] = p.upper ? N::ld(sh, sl, eq[k] + ec[k] * nb) : N::ld(xh, xl, eq[k] + ec[k] * nb);
+      }
+    }
+  }
   if (threadIdx.x == 0) pivot(0);
   __syncthreads();
   for (int j = 0; j < nb; ++j) {
@@ -194,49 +226,28 @@ potrf_diag_kernel(PotrfArgs p, int64_t j0, int nb) {
       N::st(dh, dl, q, f ? N::fadd2(d, N::fmul(v, v)) : N::add(d, N::mul(v, v)));
     }
     __syncthreads();
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (threadIdx.x == 0) {
       DIAG_T(j, 1);
       if (j + 1 < nb) pivot(j + 1);
       DIAG_T(j, 2);
-    } else if ((warp & 3) != 0) {
-      // pairs (q, c), j < c < q < nb, enumerated column by column; batches
-      // of kB independent updates (operands gathered before any store)
-      const int rem = nb - j - 1;
-      const int npairs = rem * (rem - 1) / 2;
-      constexpr int kB = 4;
-      const int nthr = (nw - (nw + 3) / 4) * 32;                  // warps not on sub-partition 0
-      const int me = (warp - warp / 4 - 1) * 32 + (threadIdx.x & 31);
+    } else if (owner) {
       const bool fast = nc_s;
-      for (int base = me; base < npairs; base += nthr * kB) {
-        int xs[kB];
-        T acc[kB], f1[kB], f2[kB];
 #pragma unroll
-        for (int b = 0; b < kB; ++b) {
-          const int t = base + b * nthr;
-          xs[b] = -1;
-          if (t < npairs) {
-            // column ci (0-based within the rem trailing columns) of pair t
-            int ci = (int)((2.0f * rem - 1.0f - sqrtf((2.0f * rem - 1.0f) * (2.0f * rem - 1.0f) - 8.0f * t)) * 0.5f);
-            while (ci > 0 && ci * (2 * rem - ci - 1) / 2 > t) --ci;
-            while ((ci + 1) * (2 * rem - ci - 2) / 2 <= t) ++ci;
-            const int qi = ci + 1 + (t - ci * (2 * rem - ci - 1) / 2);
-            const int c = j + 1 + ci, q = j + 1 + qi;
-            xs[b] = q + c * nb;
-            const T vq = N::ld(xh, xl, q + j * nb), vc = N::ld(xh, xl, c + j * nb);
-            if (!p.upper) { acc[b] = N::ld(xh, xl, xs[b]); f1[b] = N::neg(vc); f2[b] = vq; }
-            else { acc[b] = N::ld(sh, sl, xs[b]); f1[b] = vq; f2[b] = vc; }
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < kB; ++b) {
-          if (xs[b] < 0) continue;
-          T r;
-          if (FA && fast) r = ts_mac(acc[b], f1[b], f2[b]);
-          else if (fast) r = N::fadd2(acc[b], N::fmul(f1[b], f2[b]));
-          else r = N::add(FA ? ts_norm(acc[b]) : acc[b], N::mul(f1[b], f2[b]));
-          if (!p.upper) N::st(xh, xl, xs[b], r);
-          else N::st(sh, sl, xs[b], r);
+      for (int k = 0; k < kE; ++k) {
+        if (ec[k] <= j) continue;              // entry final (or none)
+        const int q = eq[k], c = ec[k];
+        const T vq = N::ld(xh, xl, q + j * nb), vc = N::ld(xh, xl, c + j * nb);
+        T f1, f2;
+        if (!p.upper) { f1 = N::neg(vc); f2 = vq; }
+        else { f1 = vq; f2 = vc; }
+        T r;
+        if (FA && fast) r = ts_mac(eacc[k], f1, f2);
+        else if (fast) r = N::fadd2(eacc[k], N::fmul(f1, f2));
+        else r = N::add(FA ? ts_norm(eacc[k]) : eacc[k], N::mul(f1, f2));
+        eacc[k] = r;
+        if (c == j + 1) {                       // its column is next: hand it over
+          if (!p.upper) N::st(xh, xl, q + c * nb, r);
+          else N::st(sh, sl, q + c * nb, r);
         }
       }
       if (threadIdx.x == 32) DIAG_T(j, 3);

@@ -16,7 +16,7 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 h0, l0 = spd_device(n)
 for _ in range(2):
     a = DeviceMatrix(n, n, "dd", n, store=(h0.clone(), l0.clone()))
-    assert Rpotrf("L", n, a, n, mode="fast", nb=64) == 0
+    assert Rpotrf("L", n, a, n, mode=os.environ.get("DIAG_MODE", "fast"), nb=64) == 0
 torch.cuda.synchronize()
 lib = ctypes.CDLL(os.environ["DDBLAS_LIB"])
 buf = np.zeros((64, 8), dtype=np.int64)
