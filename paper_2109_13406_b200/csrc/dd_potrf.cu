@@ -462,9 +462,12 @@ __global__ void __launch_bounds__(256)
 potrf_blockupd_kernel(PotrfArgs p, int64_t i0, int64_t i1, int64_t j1) {
   using T = typename N::T;
   __shared__ T fq[kPotrfMaxNb][33], fc[kPotrfMaxNb][8];
+  __shared__ int fok;
   if (*p.info != 0) return;
   const int64_t qb = i1 + (int64_t)blockIdx.x * 32, cb = i1 + (int64_t)blockIdx.y * 8;
   if (cb >= qb + 31) return;                       // tile strictly above the diagonal
+  if (threadIdx.x == 0 && threadIdx.y == 0) fok = !N::kF64;
+  __syncthreads();
   const int kb = (int)(i1 - i0);
   const int64_t lda = p.lda;
   const int tx = threadIdx.x, ty = threadIdx.y;
@@ -472,22 +475,29 @@ potrf_blockupd_kernel(PotrfArgs p, int64_t i0, int64_t i1, int64_t j1) {
   auto f = [&](int64_t x, int l) {
     return p.upper ? N::ld(p.a_hi, p.a_lo, (i0 + l) + x * lda) : N::ld(p.a_hi, p.a_lo, x + (i0 + l) * lda);
   };
+  bool ok = true;
   for (int l = ty; l < kb; l += 8) {
-    if (qb + tx < j1) fq[l][tx] = f(qb + tx, l);
-    if (tx < 8 && cb + tx < j1) fc[l][tx] = f(cb + tx, l);
+    if (qb + tx < j1) { fq[l][tx] = f(qb + tx, l); ok &= N::win(fq[l][tx]); }
+    if (tx < 8 && cb + tx < j1) { fc[l][tx] = f(cb + tx, l); ok &= N::win(fc[l][tx]); }
   }
+  if (!ok) fok = 0;
   __syncthreads();
   const int64_t q = qb + tx, c = cb + ty;
   if (q >= j1 || c >= q) return;
-  if (!p.upper) {
-    T acc = N::ld(p.a_hi, p.a_lo, q + c * lda);
-    for (int l = 0; l < kb; ++l) acc = N::add(acc, N::mul(N::neg(fc[l][ty]), fq[l][tx]));
-    N::st(p.a_hi, p.a_lo, q + c * lda, acc);
-  } else {
-    T acc = N::ld(p.s_hi, p.s_lo, q + c * p.lds);
-    for (int l = 0; l < kb; ++l) acc = N::add(acc, N::mul(fq[l][tx], fc[l][ty]));
-    N::st(p.s_hi, p.s_lo, q + c * p.lds, acc);
+  // inside the safe window: the check-free forms (exact: bit-identical) or,
+  // in the fast / twosum modes, the TwoSum accumulation
+  T acc = !p.upper ? N::ld(p.a_hi, p.a_lo, q + c * lda) : N::ld(p.s_hi, p.s_lo, q + c * p.lds);
+  const bool fast = fok && N::win(acc);
+  for (int l = 0; l < kb; ++l) {
+    const T f1 = !p.upper ? N::neg(fc[l][ty]) : fq[l][tx];
+    const T f2 = !p.upper ? fq[l][tx] : fc[l][ty];
+    if (fast && p.fastacc) acc = ts_mac(acc, f1, f2);
+    else if (fast) acc = N::fadd2(acc, N::fmul(f1, f2));
+    else acc = N::add(acc, N::mul(f1, f2));
   }
+  if (fast && p.fastacc) acc = ts_norm(acc);
+  if (!p.upper) N::st(p.a_hi, p.a_lo, q + c * lda, acc);
+  else N::st(p.s_hi, p.s_lo, q + c * p.lds, acc);
 }
 
 // Fast / twosum modes, late in the factorization: the lookahead update of
