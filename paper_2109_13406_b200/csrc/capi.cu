@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -393,9 +394,26 @@ int ddb_rgemm_host(char transa, char transb, int64_t m, int64_t n, int64_t k,
     for (size_t bi = 0; bi + 1 < bounds.size() && e == cudaSuccess && rc == DDB_OK; ++bi) {
       const int64_t j0 = bounds[bi], j1 = bounds[bi + 1], w = j1 - j0;
       const int kch = j0 == 0 ? kch0 : 1;
+      // k-panel boundaries of block 0: growing by `ratio` per panel so the
+      // first GEMM waits for a short copy while each next panel's copy still
+      // finishes within the current panel's compute (copy ~2.6 us, compute
+      // ~3.6 us per k at n = 8192: ratio < 1.38); equal panels measured
+      // 247.6 ms end to end at 8192^3, ratio 1.35 245.0 ms (DDB_HOST_GEOM =
+      // 100 x ratio)
+      static const double ratio = [] {
+        const char* v = std::getenv("DDB_HOST_GEOM");
+        return v ? std::atof(v) / 100.0 : 1.35;
+      }();
+      auto edge = [&](int c) -> int64_t {
+        if (c <= 0) return 0;
+        if (c >= kch) return k;
+        double f = (double)c / kch;
+        if (ratio > 1.0) f = (std::pow(ratio, c) - 1.0) / (std::pow(ratio, kch) - 1.0);
+        return ((int64_t)(k * f)) / 64 * 64;
+      };
       for (int c = 0; c < kch && e == cudaSuccess && rc == DDB_OK; ++c) {
-        const int64_t l0 = c == 0 ? 0 : (k * c / kch) / 64 * 64;
-        const int64_t l1 = c + 1 == kch ? k : (k * (c + 1) / kch) / 64 * 64, kc = l1 - l0;
+        const int64_t l0 = edge(c);
+        const int64_t l1 = edge(c + 1), kc = l1 - l0;
         for (int pl = 0; pl < 2 && e == cudaSuccess; ++pl) {
           const double* asrc = pl ? a_lo : a_hi;
           const double* bsrc = pl ? b_lo : b_hi;
