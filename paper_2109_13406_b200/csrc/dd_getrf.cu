@@ -316,8 +316,25 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
   auto publish = [&](int jj, int u) {
     const int par = jj & 1;
     const int64_t j = j0 + jj;
+    auto row_out = [&](double* out, int rr) {
+      for (int c = lane; c < nb; c += 32) {
+        T v = N::ld(xh, xl, rr + c * ch);
+        if (c > u) {
+          const T pc = N::ld(prow_h((jj - 1) & 1), prow_l((jj - 1) & 1), c);
+          const T x = N::ld(xh, xl, rr + (jj - 1) * ch);
+          // check-free inside the window: bit-identical to the checked forms
+          v = N::win(v) && N::win(x) && N::win(pc) ? N::fadd2(v, N::fmul(x, N::neg(pc)))
+                                                   : N::add(v, N::mul(x, N::neg(pc)));
+        }
+        N::st(out, out + nb, c, v);
+      }
+    };
     if (warp == 2) {
       if (mine(j)) spec_rec(jrow(par), (int)(j - r0), jj);
+      return;
+    }
+    if (warp == 3) {                           // row j (no search needed)
+      if (mine(j)) row_out(jrow(par), (int)(j - r0));
       return;
     }
     SKey k{0ull, 0ull, kNoRow};
@@ -337,18 +354,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
       reinterpret_cast<unsigned long long*>(g.part_al)[slot] = k.al;
       g.part_idx[slot] = k.idx;
     }
-    auto row_out = [&](double* out, int rr) {
-      for (int c = lane; c < nb; c += 32) {
-        T v = N::ld(xh, xl, rr + c * ch);
-        if (c > u) {
-          const T pc = N::ld(prow_h((jj - 1) & 1), prow_l((jj - 1) & 1), c);
-          v = N::add(v, N::mul(N::ld(xh, xl, rr + (jj - 1) * ch), N::neg(pc)));
-        }
-        N::st(out, out + nb, c, v);
-      }
-    };
     if (k.idx != kNoRow) row_out(cand(par, blockIdx.x), (int)(k.idx - r0));
-    if (mine(j)) row_out(jrow(par), (int)(j - r0));
   };
   // split grid barrier: release-add after the CTA's writes, acquire-poll
   auto arrive = [&]() {
@@ -366,7 +372,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     }
     __syncthreads();
   };
-  if (warp < 3) publish(0, nb);
+  if (warp < 4) publish(0, nb);
   arrive();
   unsigned nbar = 0;
   for (int jj = 0; jj < nb; ++jj) {
@@ -476,7 +482,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
     if (jj + 1 == nb) break;              // (j < mn - 1 holds below: the panel lies inside mn)
     __syncthreads();
     PANEL_T(jj, 4);
-    if (warp < 3) publish(jj + 1, jj + 1);
+    if (warp < 4) publish(jj + 1, jj + 1);
     PANEL_T(jj, 5);
     arrive();
     PANEL_T(jj, 6);
