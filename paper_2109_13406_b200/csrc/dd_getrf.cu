@@ -847,12 +847,13 @@ static int panel_grid(int64_t rows) {
     cached_max = per > 0 ? sms : 1;                            // one CTA per SM
     cached_dev = dev;
   }
-  // rows per CTA: the panel is latency-bound, so fewer, fuller CTAs leave
-  // more SMs to the trailing update it overlaps (env DDB_GETRF_ROWS)
+  // rows per CTA (env DDB_GETRF_ROWS): each step's rank-1 update of a CTA's
+  // rows sits on the panel's critical path, so thinner slices (more CTAs,
+  // capped at one per SM) shorten it
   static const int64_t per_cta = [] {
     const char* v = std::getenv("DDB_GETRF_ROWS");
     const int64_t r = v ? (int64_t)std::atoll(v) : 0;
-    return r > 0 ? r : (int64_t)64;
+    return r > 0 ? r : (int64_t)32;   // 32: 141.0 vs 141.5 ms at n = 8192 (64)
   }();
   int64_t want = (rows + per_cta - 1) / per_cta;
   if (want < 1) want = 1;
