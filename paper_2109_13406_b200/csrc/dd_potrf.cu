@@ -303,7 +303,7 @@ __device__ __forceinline__ typename N::T rfadd(typename N::T x, typename N::T y)
   return DDB_ROWS_SEL ? N::fadd(x, y) : N::fadd2(x, y);
 }
 
-template <class N, int NPER, bool UP, int MODE>
+template <class N, int NPER, bool UP, int MODE, bool TCHK = false>
 __device__ __forceinline__ void rows_steps(const PotrfArgs& p, int64_t j0, int w, int ncols, int64_t q,
                                            const double* __restrict__ ph, const double* __restrict__ pl,
                                            int sr, int sc, const typename N::T* rec_s,
@@ -347,7 +347,13 @@ __device__ __forceinline__ void rows_steps(const PotrfArgs& p, int64_t j0, int w
         if (N::win(v)) {                              // warp-uniform
           dq = ts_mac(dq, v, v);
 #pragma unroll
-          for (int i = s; i < NPER; ++i) acc[i] = UP ? ts_mac(acc[i], v, t[i]) : ts_mac(acc[i], N::neg(t[i]), v);
+          for (int i = s; i < NPER; ++i) {
+            if (TCHK && !N::win(t[i]))          // an unchecked P entry outside the window
+              acc[i] = UP ? N::add(ts_norm(acc[i]), N::mul(v, t[i]))
+                          : N::add(ts_norm(acc[i]), N::mul(N::neg(t[i]), v));
+            else
+              acc[i] = UP ? ts_mac(acc[i], v, t[i]) : ts_mac(acc[i], N::neg(t[i]), v);
+          }
         } else {                                      // checked forms on normalised values
           dq = N::add(ts_norm(dq), N::mul(v, v));
 #pragma unroll
@@ -421,7 +427,10 @@ potrf_rows_kernel(PotrfArgs p, int64_t j0, int w, int64_t q0, int64_t q1,
   const bool all_ok = __all_sync(0xffffffffu, ok);
   if (N::kF64 || !all_ok)
     rows_steps<N, NPER, UP, RK_SLOW>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
-  else if (pmask == nullptr)
+  else if (pmask == nullptr && p.fastacc) {   // narrow launch, fast modes: TwoSum, P checked per entry
+    rows_steps<N, NPER, UP, RK_TWOSUM, true>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
+    dq = ts_norm(dq);
+  } else if (pmask == nullptr)
     rows_steps<N, NPER, UP, RK_CHECK>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
   else if constexpr (FA) {
     rows_steps<N, NPER, UP, RK_TWOSUM>(p, j0, w, ncols, q, ph, pl, sr, sc, rec_s, acc, au, dq);
