@@ -611,11 +611,12 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
       const char* v = std::getenv("DDB_POTRF_NB");
       return v ? (int64_t)std::atoll(v) : (int64_t)0;
     }();
-    // 1024-deep outer panels pay off once the bulk trailing update dominates
-    // the panel chain: n = 16384 fast 531 -> 470 ms; n = 8192 98.6 -> 101.5
-    // ms (the longer outer panels lengthen the lookahead's critical path),
-    // and exact mode gains nothing from depth
-    nb = nb_env > 0 ? nb_env : (n >= 12288 && mode != DDB_MODE_EXACT ? 1024 : 256);
+    // deeper outer panels pay off once the bulk trailing update dominates
+    // the panel chain; exact mode gains nothing from depth.  Fast modes at
+    // n = 8192: 256 -> 70.7 ms, 384 -> 69.0 ms, 512 -> 69.4 ms
+    // (n = 4096: 256 best, 16.6 vs 17.9 ms; n = 16384: 384 ... 1024 alike)
+    const bool fastm = mode != DDB_MODE_EXACT && mode != DDB_MODE_REFERENCE;
+    nb = nb_env > 0 ? nb_env : (fastm && n >= 12288 ? 1024 : (fastm && n >= 6144 ? 384 : 256));
   }
   const int64_t NB = nb;
   const int64_t MB = NB > 256 ? 256 : NB;
