@@ -520,11 +520,13 @@ getrf_perm_kernel(GetrfArgs g, int64_t j0, int64_t j1, int reverse, PermBuf pb) 
   __shared__ long long key_s[kHash];
   __shared__ int slot_s[kHash];
   __shared__ int nt_s;
+  __shared__ long long swap_s[kPermSteps];
   const int nb = (int)(j1 - j0);
   for (int t = threadIdx.x; t < kHash; t += blockDim.x) key_s[t] = -1;
   for (int t = threadIdx.x; t < nb; t += blockDim.x) {
     rows_s[t] = j0 + t;
     src_s[t] = t;
+    swap_s[t] = g.swap[j0 + t];        // all steps' targets in one coalesced read
   }
   __syncwarp();
   if (threadIdx.x == 0) {
@@ -547,7 +549,7 @@ getrf_perm_kernel(GetrfArgs g, int64_t j0, int64_t j1, int reverse, PermBuf pb) 
     };
     for (int64_t s = j0; s < j1; ++s) {
       const int64_t j = reverse ? j0 + j1 - 1 - s : s;
-      const long long p = g.swap[j];
+      const long long p = swap_s[j - j0];
       if (p == j) continue;
       const int a = find(j), b = find(p);
       const int t = src_s[a];
