@@ -110,7 +110,7 @@ def test_rgetrf_out_of_window_rows_exact_matches_oracle():
 
 
 @pytest.mark.parametrize("mode", ["fast", "twosum"])
-@pytest.mark.parametrize("m,n", [(320, 320), (500, 200), (200, 500)])
+@pytest.mark.parametrize("m,n", [(320, 320), (500, 200), (200, 500), (1600, 1600)])
 def test_rgetrf_fast_modes_close_to_exact(m, n, mode):
     ld = m
     hi, lo = _inputs(m, n, ld, seed=3)

@@ -172,6 +172,21 @@ def test_rpotrf_late_failure_restores_trailing(uplo, nb):
 
 
 @pytest.mark.parametrize("uplo", ["L", "U"])
+@pytest.mark.parametrize("mode", ["fast", "twosum"])
+def test_rpotrf_default_blocking_large_n_residual(uplo, mode):
+    """n = 6400: the fast modes' default outer width 384 (three block levels:
+    256- and 128-column middle panels, the lean lookahead kernel late in the
+    factorization, TwoSum accumulation in the row kernels and the diagonal
+    kernel's Newton pivots) -- inside the reference's acceptance residual."""
+    n = 6400
+    hi, lo = spd_dd(n, n, seed=23)
+    info, gh, gl = run(uplo, n, n, hi, lo, mode)
+    assert info == 0
+    r = residual_ratio(uplo, n, n, hi, lo, gh, gl)
+    assert r < THRESHOLD, r
+
+
+@pytest.mark.parametrize("uplo", ["L", "U"])
 @pytest.mark.parametrize("mode", ["fast", "twosum", "exact"])
 @pytest.mark.parametrize("n", [2500, 4500])
 def test_rpotrf_large_residual(uplo, mode, n):
