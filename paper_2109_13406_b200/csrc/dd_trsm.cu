@@ -32,6 +32,24 @@ namespace ddb {
 
 namespace {
 
+// TwoSum accumulation (fast modes, as dd_potrf.cu / dd_getrf.cu): unnormalised
+// (H, L), 13 FP64 operations per product
+__device__ __forceinline__ dd ts_mac(dd acc, dd x, dd y) {
+  const double p = dmul(x.h, y.h);
+  const double e = dfma(x.h, y.h, -p);
+  const double c = dfma(x.h, y.l, dmul(x.l, y.h));
+  double s, err;
+  two_sum(acc.h, p, s, err);
+  return dd{s, dadd(acc.l, dadd(err, dadd(e, c)))};
+}
+__device__ __forceinline__ dd ts_norm(dd a) {
+  double s, e;
+  quick_two_sum(a.h, a.l, s, e);
+  return dd{s, e};
+}
+__device__ __forceinline__ double ts_mac(double acc, double x, double y) { return dadd(acc, dmul(x, y)); }
+__device__ __forceinline__ double ts_norm(double a) { return a; }
+
 // fin_s: unit diagonal -> v; the R branches -> (one / A(s,s)) * v with the
 // reciprocal formed once per s by trsm_coef_kernel (be.div(one, aelt) then
 // be.mul, level23.py:361-362, :368-369 -- the same bits); the L branches ->
@@ -117,12 +135,21 @@ __global__ void __launch_bounds__(256)
 trsm_block_kernel(TrsmArgs t, int64_t r0, int nb) {
   using T = typename N::T;
   extern __shared__ double sm[];
+  __shared__ int tok;
   double* th = sm;
   double* tl = sm + nb * nb;
+  if (threadIdx.x == 0) tok = !N::kF64;
+  __syncthreads();
+  bool ok = true;
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
     const int s = e % nb, c = e / nb;
-    if (c < s) N::st(th, tl, e, N::ld(t.t_hi, t.t_lo, (r0 + s) + (r0 + c) * t.ldt));
+    if (c < s) {
+      const T tv = N::ld(t.t_hi, t.t_lo, (r0 + s) + (r0 + c) * t.ldt);
+      N::st(th, tl, e, tv);
+      ok &= N::win(tv);
+    }
   }
+  if (!ok) tok = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
@@ -133,12 +160,25 @@ trsm_block_kernel(TrsmArgs t, int64_t r0, int nb) {
   T acc_a = N::zero(), acc_b = N::zero();
   if (ra < nb) acc_a = N::ld(wh, wl, ra);
   if (rb < nb) acc_b = N::ld(wh, wl, rb);
+  // inside the safe window (T block, this vector's start, each x): the
+  // check-free forms, bit-identical to the checked ones; in the fast modes
+  // the TwoSum accumulation (the products enter unrounded, dd accuracy)
+  const bool blk_ok = __all_sync(0xffffffffu, tok && N::win(acc_a) && N::win(acc_b));
+  const bool ts = blk_ok && t.rec_fast;
   for (int s = 0; s < nb; ++s) {
-    const T val = N::shfl(s < 32 ? acc_a : acc_b, s & 31);
+    T val = N::shfl(s < 32 ? acc_a : acc_b, s & 31);
+    if (ts) val = ts_norm(val);
     const T x = trsm_fin<N>(t, r0 + s, val);
     if (lane == (s & 31)) N::st(wh, wl, s, x);
-    if (ra > s && ra < nb) acc_a = N::add(acc_a, N::neg(N::mul(N::ld(th, tl, ra + s * nb), x)));
-    if (rb > s && rb < nb) acc_b = N::add(acc_b, N::neg(N::mul(N::ld(th, tl, rb + s * nb), x)));
+    const bool f = blk_ok && N::win(x);          // warp-uniform
+    auto step = [&](T acc, int r) -> T {
+      const T tv = N::ld(th, tl, r + s * nb);
+      if (f && ts) return ts_mac(acc, N::neg(tv), x);
+      if (f) return N::fadd2(acc, N::neg(N::fmul(tv, x)));
+      return N::add(ts ? ts_norm(acc) : acc, N::neg(N::mul(tv, x)));
+    };
+    if (ra > s && ra < nb) acc_a = step(acc_a, ra);
+    if (rb > s && rb < nb) acc_b = step(acc_b, rb);
   }
 }
 
