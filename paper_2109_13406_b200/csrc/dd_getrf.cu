@@ -421,6 +421,7 @@ getrf_panel_smem_kernel(GetrfArgs g, int64_t j0, int nb, int64_t chunk) {
         piv = N::ldcg(src, src + nb, jj);
         rec = N::ldcg(src + 2 * nb, src + 2 * nb + 1, 0);
       }
+      PANEL_T(jj, 7);
       named_sync(1);
 #pragma unroll
       for (int i = 0; i < kMaxPer; ++i) {

@@ -27,3 +27,6 @@ d = np.diff(t, axis=1)
 names = [n for n in os.environ.get("PANEL_NAMES", "wait,keys,row+rec,scale+upd,publish,arrive").split(",")]
 print("mean cycles per step:", ", ".join(f"{nm} {v:.0f}" for nm, v in zip(names, d.mean(axis=0))))
 print("step (k0 -> next k0): %.0f cycles" % np.diff(buf[:63, 0]).mean())
+if os.environ.get("PANEL_K7"):
+    print("warp 0 keys + row fetch (k1 -> k7): %.0f, waiting for the bulk (k7 -> k2): %.0f" % (
+        (buf[1:63, 7] - buf[1:63, 1]).mean(), (buf[1:63, 2] - buf[1:63, 7]).mean()))
