@@ -44,7 +44,7 @@ extern "C" {
 
 /* mode: DDB_MODE_EXACT     bit-identical to the reference (29 FP64 instr / MAC)
  *       DDB_MODE_FAST      certified-anchor accumulation: hi*hi in the
- *                          hand-written DFMA kernel (5 FP64 instr / MAC) + the
+ *                          hand-written DFMA kernel (4.75 FP64 instr / MAC) + the
  *                          cross terms A_lo*B_hi + A_hi*B_lo on a hand-written
  *                          DMMA kernel (2 / MAC) + a bf16 tcgen05 bound GEMM
  *                          (k >= 1024; shallower calls: 7.5 / MAC in one
@@ -52,7 +52,7 @@ extern "C" {
  *                          |beta||c|), c = 4, for every input in the safe
  *                          window: elements whose row / column exponent
  *                          spreads exceed 112 - ceil(log2 k) and calls with
- *                          k > 2^17 take the TwoSum accumulation instead,
+ *                          k > 2^16 take the TwoSum accumulation instead,
  *                          elements whose op(A) row / op(B) column holds a
  *                          value outside the window (inf, nan, |x| >= 2^301,
  *                          0 < |hi| < 2^-300, non-normalised dd) take the

@@ -21,17 +21,17 @@
 //   * all terms are >= 0, so with a per-addition relative error <= 2^-22
 //     (fp32, truncating adders and one guard bit of slack included) the
 //     computed S >= (1 - k 2^-22) sum, and (1 + k 2^-21)(1 - k 2^-22) >= 1
-//     for k <= 2^20 (calls deeper than kCertMaxK = 2^17 take TwoSum);
+//     for k <= 2^20 (calls deeper than kCertMaxK = 2^16 take TwoSum);
 //   * a converted value below bf16's normal range may be flushed by the
 //     tensor core: each such product is < 2^-126, covered by k 2^-120.
 // Tightness: S' <= (1.0157 sum^ + k 2^-131)(1 + k 2^-21) + k 2^-120 in the
 // scaled units, where sum^ >= 2^-(sa + sb + 2) for an element whose row /
 // column exponent spreads are sa / sb (the scaled magnitudes lie in
 // [2^-(s+1), 1)).  So S' / sum <= 1.0157 (1 + k 2^-21) + k 2^-118 2^(sa + sb)
-// <= 1.11 for k <= 2^17 whenever sa + sb <= 112 - ceil(log2 k) (wide_limit,
+// <= 1.064 for k <= 2^16 whenever sa + sb <= 112 - ceil(log2 k) (wide_limit,
 // internal.h); wider elements are EC_WIDE and take the TwoSum fallback.
 // The anchored kernels need S' / sum <= 1.14 (ALG_CERT: c = 3.5 S'/sum) and
-// <= 1.27 (ALG_SPLIT: c = 2.17 S'/sum + 1.25) for c = 4.
+// <= 1.1 (ALG_SPLIT: c = 2.5 S'/sum + 1.25) for c = 4.
 //
 // Cost at n = 8192: ~0.3 ms for the conversions (HBM-bound: 8 B read + 2 B
 // written per element) plus ~0.8 ms of tensor-core time.

@@ -19,25 +19,28 @@
 // ALG_SPLIT (fast mode's default here): the dd product a*b = ah bh + (al bh +
 // ah bl) + al bl splits into the hi * hi part, accumulated by this kernel with
 // the certified anchor (Tn = fma(ah, bh, T), r = fma(ah, bh, T - Tn), L += r,
-// (T, L) folded every 3 steps: 5 FP64 instructions per MAC instead of 7.5,
-// and only the hi planes staged, 24-deep k-tiles), and the cross terms
+// the two residuals of a step pair summed before they enter L, (T, L)
+// folded every 4 steps: 4.75 FP64 instructions per MAC instead of 7.5, and
+// only the hi planes staged, 24-deep k-tiles), and the cross terms
 // X = A_lo B_hi + A_hi B_lo, computed first by the hand-written DMMA kernel
 // (dd_cross.cu; for Rsyrk on the triangle tiles only) and added to L in the
 // epilogue; al bl (< u^2 |ab|) is dropped, as in every dd product.  Error per
 // element, with the unit v = 2^(E-106) < 2^-104 S' (2^E < 4 S', S' >= sum
 // |ah bh| the certified bound): each residual r (|r| <= ulp(T)/2 =
-// 2^(E-53)) rounds by <= v/2; after a fold |L| <= 2^(E-53), so by monotone
-// rounding the three additions into L stay <= 2^(E-52), 1.5 * 2^(E-52),
-// 2^(E-51) and round by <= v, 2v, 2v: 6.5 v per 3 steps, c = 2.17 rho with
-// rho = S' / sum|ab| (a period of 2 gives 2 rho, of 4 2.75 rho).  The cross
-// sums' recursive-summation bound is 2k u * sum (|al bh| + |ah bl|) <=
-// 4k u^2 sum|ab| (operands normalised, |lo| <= 2^-53 |hi|, which the prescan
-// enforces): c = 1; the dropped al bl c = 0.25.  rho <= 1.11 for every
-// element the routing leaves here (dd_bound.cu: k <= 2^17 and row + column
-// exponent spreads within 112 - ceil(log2 k); wider elements take the TwoSum
-// fallback), so c <= 2.17 * 1.11 + 1.25 = 3.66 (+ O(u^2) epilogue roundings)
-// against the north star's c = 4.
-// Measured at 8192^3: 177 ms for this kernel + 60.5 ms of cross terms.
+// 2^(E-53)) rounds by <= v/2; a pair sum r0 + r1 (<= 2^(E-52)) by <= v;
+// after a fold |L| <= 2^(E-53), so by monotone rounding the two additions
+// into L stay <= 1.5 * 2^(E-52) and 2.5 * 2^(E-52) and round by <= 2v, 4v:
+// 4 (v/2) + 2 v + 2v + 4v = 10 v per 4 steps, c = 2.5 rho with rho = S' /
+// sum|ab| (per-step accumulation with the same period: 2.75 rho; a period
+// of 3: 2.17 rho).  The cross sums' recursive-summation bound is 2k u *
+// sum (|al bh| + |ah bl|) <= 4k u^2 sum|ab| (operands normalised, |lo| <=
+// 2^-53 |hi|, which the prescan enforces): c = 1; the dropped al bl c =
+// 0.25.  rho <= 1.064 for every element the routing leaves here
+// (dd_bound.cu: k <= 2^16 and row + column exponent spreads within 112 -
+// ceil(log2 k); wider elements take the TwoSum fallback), so c <= 2.5 *
+// 1.064 + 1.25 = 3.91 (+ O(u^2) epilogue roundings, << 0.09 k at the
+// k >= 256 this kernel runs) against the north star's c = 4.
+// Measured at 8192^3: 167 ms for this kernel + 60.5 ms of cross terms.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -78,16 +81,20 @@ constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 10
 
 // ALG_SPLIT: k-tile depth and fold period (steps between (T, L) folds).  The
 // stage holds only the hi planes, so a deeper tile fits the same ring.  A
-// fold period of 3 keeps |L| < 2 ulp(T): error <= 6.5 units per 3 steps
-// (see the header), against 4 per 2 steps with a period of 2.
+// fold period of 4 with pair-summed residuals: error <= 10 units per 4 steps
+// (see the header); 229.3 vs 235.4 ms per 8192^3 step against a period of 3
+// (6.5 units per 3 steps).
 #ifndef DDB_SPLIT_BK
 #define DDB_SPLIT_BK 24
 #endif
 #ifndef DDB_SPLIT_FOLD
-#define DDB_SPLIT_FOLD 3
+#define DDB_SPLIT_FOLD 4
 #endif
 #ifndef DDB_SPLIT_CHAIN
 #define DDB_SPLIT_CHAIN 0     // 1: per-element step chains instead of per-step sweeps
+#endif
+#ifndef DDB_SPLIT_PAIR
+#define DDB_SPLIT_PAIR 1      // 1: the two residuals of a step pair summed before entering L
 #endif
 #ifndef DDB_SPLIT_UNROLL
 #define DDB_SPLIT_UNROLL 2    // k-loop bodies unrolled per trip (2: 240.4 vs 241.8 ms at 8192^3)
@@ -97,7 +104,8 @@ constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 10
 #endif
 constexpr int SPLIT_BK = DDB_SPLIT_BK, SPLIT_FOLD = DDB_SPLIT_FOLD;
 constexpr int SPLIT_TN = DDB_SPLIT_TN, SPLIT_BN = SPLIT_TN / 2 * RY;
-constexpr bool SPLIT_CHAIN = DDB_SPLIT_CHAIN;
+constexpr bool SPLIT_CHAIN = DDB_SPLIT_CHAIN, SPLIT_PAIR = DDB_SPLIT_PAIR;
+static_assert(!SPLIT_PAIR || SPLIT_FOLD % 2 == 0, "pairs fold on pair boundaries");
 constexpr int SPLIT_UNROLL = DDB_SPLIT_UNROLL;
 constexpr int SPLIT_BODY = SPLIT_FOLD % 2 == 0 ? SPLIT_FOLD : 2 * SPLIT_FOLD;   // even
 static_assert(SPLIT_BK % SPLIT_BODY == 0 && SPLIT_BK % 2 == 0, "split k-tile");
@@ -310,6 +318,29 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
                   H[a][b] = T;
                   L[a][b] = l;
                 }
+            } else if (SPLIT_PAIR) {   // L += (r0 + r1): one rounding into L per step pair
+#pragma unroll
+              for (int a = 0; a < TM; ++a)
+#pragma unroll
+                for (int b = 0; b < TNK; ++b) {
+                  const double T = H[a][b];
+                  const double T1 = dfma(ah0[a], bh0[b], T);
+                  const double r0 = dfma(ah0[a], bh0[b], dsub(T, T1));
+                  const double T2 = dfma(ah1[a], bh1[b], T1);
+                  const double r1 = dfma(ah1[a], bh1[b], dsub(T1, T2));
+                  L[a][b] = dadd(L[a][b], dadd(r0, r1));
+                  H[a][b] = T2;
+                }
+              if ((pq + 2) % SPLIT_FOLD == 0) {
+#pragma unroll
+                for (int a = 0; a < TM; ++a)
+#pragma unroll
+                  for (int b = 0; b < TNK; ++b) {
+                    const double T2 = dadd(H[a][b], L[a][b]);
+                    L[a][b] = dsub(L[a][b], dsub(T2, H[a][b]));
+                    H[a][b] = T2;
+                  }
+              }
             } else {
 #pragma unroll
             for (int q = 0; q < 2; ++q) {

@@ -125,7 +125,7 @@ int run(const GemmArgs& g0, int mode, cudaStream_t s) {
   retain_pool_memory();
   int alg = alg_for_mode(mode);
   // The certified bound's accumulation factor (1 + k 2^-21, below) keeps
-  // S' <= 1.11 sum |ab| up to k = 2^17; deeper calls take the TwoSum MAC,
+  // S' <= 1.064 sum |ab| up to k = 2^16; deeper calls take the TwoSum MAC,
   // whose error bound holds at any depth.
   if (alg == ALG_CERT && g.k > kCertMaxK) alg = ALG_TWOSUM;
   const int64_t nrow = g.m, ncol = g.n;

@@ -35,7 +35,7 @@ enum RouteFlag { ROUTE_SAFE = 0, ROUTE_UNSAFE = 1 };
 // Certified-anchor (fast) accumulation: deepest k it accepts, and the
 // spread limit for EC_WIDE (dd_bound.cu derives both): an element whose row
 // and column exponent spreads sum above 112 - ceil(log2 k) takes TwoSum.
-constexpr int64_t kCertMaxK = int64_t(1) << 17;
+constexpr int64_t kCertMaxK = int64_t(1) << 16;
 inline int wide_limit(int64_t k) {
   int lg = 0;
   while ((int64_t(1) << lg) < k) ++lg;

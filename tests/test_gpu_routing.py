@@ -158,10 +158,10 @@ def test_rsyrk_wide_rows_within_bound(uplo, trans):
 
 
 def test_cert_depth_cap_routes_deep_calls_to_twosum():
-    """k above 2^17: the certified bound's accumulation factor is no longer
+    """k above 2^16: the certified bound's accumulation factor is no longer
     tight enough, the call takes the TwoSum MAC (route 3) and stays inside
     the bound."""
-    m, n, k = 4, 4, (1 << 17) + 40
+    m, n, k = 4, 4, (1 << 16) + 40
     A = random_dd(m, k, m, 11, 1)
     B = random_dd(k, n, k, 11, 2)
     C = random_dd(m, n, m, 11, 3)
@@ -275,7 +275,7 @@ def test_one_nan_in_a_large_call_costs_little():
     assert torch.isfinite(cc.store[0][4322::n]).all()
 
 
-@pytest.mark.parametrize("k,s", [(65536, 48), (65536, 49), (131072, 47), (131072, 48)])
+@pytest.mark.parametrize("k,s", [(32768, 48), (32768, 49), (65536, 48), (65536, 49)])
 def test_spread_at_the_limit_deep_k(monkeypatch, k, s):
     """Right at the wide limit (2s = 112 - ceil(log2 k) stays on the certified
     path, 2s + 2 takes the fallback) and at the deepest certified k, where the
