@@ -21,7 +21,7 @@
 // the certified anchor (Tn = fma(ah, bh, T), r = fma(ah, bh, T - Tn), L += r,
 // the two residuals of a step pair summed before they enter L, (T, L)
 // folded every 4 steps: 4.75 FP64 instructions per MAC instead of 7.5, and
-// only the hi planes staged, 24-deep k-tiles), and the cross terms
+// only the hi planes staged, 32-deep k-tiles), and the cross terms
 // X = A_lo B_hi + A_hi B_lo, computed first by the hand-written DMMA kernel
 // (dd_cross.cu; for Rsyrk on the triangle tiles only) and added to L in the
 // epilogue; al bl (< u^2 |ab|) is dropped, as in every dd product.  Error per
@@ -85,7 +85,7 @@ constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * 8 + 10
 // (see the header); 229.3 vs 235.4 ms per 8192^3 step against a period of 3
 // (6.5 units per 3 steps).
 #ifndef DDB_SPLIT_BK
-#define DDB_SPLIT_BK 24
+#define DDB_SPLIT_BK 32      // 32 x (128 + 64) doubles = the ring's 48 KB stage (24: 229.3 vs 228.8 ms)
 #endif
 #ifndef DDB_SPLIT_FOLD
 #define DDB_SPLIT_FOLD 4
