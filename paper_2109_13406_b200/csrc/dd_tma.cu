@@ -242,23 +242,48 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
       // loop keeps the kernel's code small (a short-k tile runs its prologue
       // and epilogue once, and fully unrolled they missed the instruction
       // cache: ~2x the tile time at k = 64)
-#pragma unroll 1
+      // (every bound word and row exponent is loaded up front -- one round
+      // trip instead of one per row -- parked in L and H[.][0] and shifted
+      // out row by row, which leaves L zero again; 227.8 vs 228.7 ms at
+      // 8192^3.  An L2 prefetch of C and the cross terms by the producer
+      // warp before the epilogue cost 9 ms there and was dropped.)
+      int ec[TNK];
+#pragma unroll
+      for (int b = 0; b < TNK; ++b) {
+        const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
+        ec[b] = gj < g.n ? col_exp[gj] : 0;
+      }
+#pragma unroll
       for (int a = 0; a < TM; ++a) {
-#pragma unroll
-        for (int i = 0; i + 1 < TM; ++i)
-#pragma unroll
-          for (int b = 0; b < TNK; ++b) H[i][b] = H[i + 1][b];
         const int64_t gi = i0 + (a >> 1) * RX + tx * 2 + (a & 1);
-        const int er = gi < g.m ? row_exp[gi] : 0;
+        H[a][0] = gi < g.m ? (double)row_exp[gi] : 0.0;
 #pragma unroll
         for (int b = 0; b < TNK; ++b) {
           const int64_t gj = j0 + (b >> 1) * RY + ty * 2 + (b & 1);
-          const bool in = gi < g.m && gj < g.n;
-          const float sb = in ? g.bound[gi + gj * g.m] : 0.f;
-          const int ec = gj < g.n ? col_exp[gj] : 0;
-          const double sd = dfma((double)sb, g.bnd_fac, g.bnd_floor);
+          L[a][b] = gi < g.m && gj < g.n ? (double)g.bound[gi + gj * g.m] : 0.0;
+        }
+      }
+#pragma unroll 1
+      for (int a = 0; a < TM; ++a) {
+        const int er = (int)H[0][0];
+        double anc[TNK];
+#pragma unroll
+        for (int b = 0; b < TNK; ++b) {
+          const double sd = dfma(L[0][b], g.bnd_fac, g.bnd_floor);
           const int es = (int)((dbits(sd) >> 52) & 0x7ff);
-          H[TM - 1][b] = anchor_from_bexp(es + er + ec - 2042);
+          anc[b] = anchor_from_bexp(es + er + ec[b] - 2042);
+        }
+#pragma unroll
+        for (int i = 0; i + 1 < TM; ++i)
+#pragma unroll
+          for (int b = 0; b < TNK; ++b) {
+            H[i][b] = H[i + 1][b];
+            L[i][b] = L[i + 1][b];
+          }
+#pragma unroll
+        for (int b = 0; b < TNK; ++b) {
+          H[TM - 1][b] = anc[b];
+          L[TM - 1][b] = 0.0;
         }
       }
     }
