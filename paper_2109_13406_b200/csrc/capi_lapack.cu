@@ -256,6 +256,7 @@ static int rgetrf_impl(bool f64, int64_t m, int64_t n, double* a_hi, double* a_l
                        int64_t* ipiv, int* info, int mode, void* stream) {
   const int rc = ddb_rgetrf_validate(m, n, lda);
   if (rc) return rc;
+  NoPersistScope no_persist;   // trailing updates beside the panel stream
   if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr ||
       (ipiv == nullptr && m > 0 && n > 0)) {
     g_last_error = info == nullptr || ipiv == nullptr ? "ipiv / info pointer is null" : "unknown mode";
@@ -596,6 +597,7 @@ static int rpotrf_impl(bool f64, char uplo, int64_t n, double* a_hi, double* a_l
                        int64_t nb, int mode, void* stream, int* info) {
   const int rc = ddb_rpotrf_validate(uplo, n, lda);
   if (rc) return rc;
+  NoPersistScope no_persist;   // trailing updates beside the panel stream
   if (mode < DDB_MODE_EXACT || mode > DDB_MODE_TWOSUM || info == nullptr) {
     g_last_error = info == nullptr ? "info pointer is null" : "unknown mode";
     return DDB_EINVAL;

@@ -539,6 +539,8 @@ dd_tma_nn_kernel(GemmArgs g, const __grid_constant__ CUtensorMap mAh,
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+thread_local int g_no_persist = 0;   // > 0 inside a NoPersistScope
+
 // fast mode through ALG_SPLIT (default for deep calls; measured 258 vs 272 ms
 // at 8192^3) or the full certified-anchor MAC: DDB_SPLIT=0 never splits,
 // DDB_SPLIT=2 splits at any depth (tests).  Read per call (a few ns).
@@ -549,6 +551,9 @@ static int split_policy() {
 }
 
 }  // namespace tma
+
+NoPersistScope::NoPersistScope(bool on) : on_(on) { tma::g_no_persist += on ? 1 : 0; }
+NoPersistScope::~NoPersistScope() { tma::g_no_persist -= on_ ? 1 : 0; }
 
 // The concurrent split schedule's last step: C += alpha * X on the EC_FAST
 // elements (the uplo triangle for Rsyrk), X the cross terms (ld = m).  One
@@ -738,11 +743,21 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t units = (int64_t)tiles_m * tiles_n * splits;
-  // Default: one CTA per unit (the hardware scheduler backfills SMs).  The
-  // persistent walk (one CTA per SM, DDB_TMA_PERSISTENT=1) measured the same
-  // speed but more DRAM reads (its CTAs drift apart in k across units).
-  const int grid = std::getenv("DDB_TMA_PERSISTENT") ? (int)(units < sms ? units : sms)
-                                                     : (int)units;
+  // Default: the persistent walk, one CTA per SM (the producer runs ahead
+  // across unit boundaries, so a unit's prologue / epilogue overlaps the
+  // next unit's loads: 8192 x 7936 x 256 in 8.00 vs 8.53 ms, 8192^3 226.2 vs
+  // 227.4, Rtrsm 8192 152.7 vs 157.1), except for Rsyrk (the skipped
+  // triangle leaves the strided walk unbalanced: n = 4096 3875 vs 4350 dd
+  // GFlops) and inside Rpotrf / Rgetrf (NoPersistScope), whose
+  // high-priority panel stream needs SMs to free up while a trailing update
+  // runs (Rgetrf 142.7 vs 137.3 ms persistent).  DDB_TMA_PERSISTENT=0 / 1
+  // forces one CTA per unit / the walk everywhere.
+  static const int penv = [] {
+    const char* v = std::getenv("DDB_TMA_PERSISTENT");
+    return v ? (v[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool persist = penv == 1 || (penv < 0 && tma::g_no_persist == 0 && g.syrk == 0);
+  const int grid = persist ? (int)(units < sms ? units : sms) : (int)units;
   kern<<<grid, NTK, SMEM_BYTES, s>>>(ga, mAh, mAl, mBh, mBl, row_exp, col_exp, flag, tiles_m,
                                     tiles_n, splits);
   e = cudaGetLastError();

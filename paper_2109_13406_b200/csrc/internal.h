@@ -35,6 +35,15 @@ enum RouteFlag { ROUTE_SAFE = 0, ROUTE_UNSAFE = 1 };
 // Certified-anchor (fast) accumulation: deepest k it accepts, and the
 // spread limit for EC_WIDE (dd_bound.cu derives both): an element whose row
 // and column exponent spreads sum above 112 - ceil(log2 k) takes TwoSum.
+// The TMA GEMM walks its tiles with one persistent CTA per SM, except while
+// a NoPersistScope is alive on the calling host thread (Rpotrf / Rgetrf:
+// their panel stream must find SMs freeing up during a trailing update).
+struct NoPersistScope {
+  explicit NoPersistScope(bool on = true);
+  ~NoPersistScope();
+  bool on_;
+};
+
 constexpr int64_t kCertMaxK = int64_t(1) << 16;
 inline int wide_limit(int64_t k) {
   int lg = 0;
