@@ -750,7 +750,9 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // triangle leaves the strided walk unbalanced: n = 4096 3875 vs 4350 dd
   // GFlops) and inside Rpotrf / Rgetrf (NoPersistScope), whose
   // high-priority panel stream needs SMs to free up while a trailing update
-  // runs (Rgetrf 142.7 vs 137.3 ms persistent).  DDB_TMA_PERSISTENT=0 / 1
+  // runs (Rgetrf 142.7 vs 137.3 ms persistent; a walk over 148 - R SMs
+  // leaving R to the panel stream did worse still: R = 8 / 16 / 32 gave
+  // 144.8 / 147.3 / 151.7 ms).  DDB_TMA_PERSISTENT=0 / 1
   // forces one CTA per unit / the walk everywhere.
   static const int penv = [] {
     const char* v = std::getenv("DDB_TMA_PERSISTENT");
