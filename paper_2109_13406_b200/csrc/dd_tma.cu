@@ -746,9 +746,10 @@ cudaError_t launch_tma_nn(const GemmArgs& g, int alg, const int* row_exp, const 
   // Default: the persistent walk, one CTA per SM (the producer runs ahead
   // across unit boundaries, so a unit's prologue / epilogue overlaps the
   // next unit's loads: 8192 x 7936 x 256 in 8.00 vs 8.53 ms, 8192^3 226.2 vs
-  // 227.4, Rtrsm 8192 152.7 vs 157.1), except for Rsyrk (the skipped
-  // triangle leaves the strided walk unbalanced: n = 4096 3875 vs 4350 dd
-  // GFlops) and inside Rpotrf / Rgetrf (NoPersistScope), whose
+  // 227.4, Rtrsm 8192 152.7 vs 157.1), except for Rsyrk (n = 4096 3875 vs
+  // 4350 dd GFlops; a walk over the triangle's tiles only, evenly spread,
+  // did no better: 18.1 vs 15.9 ms) and inside Rpotrf / Rgetrf
+  // (NoPersistScope), whose
   // high-priority panel stream needs SMs to free up while a trailing update
   // runs (Rgetrf 142.7 vs 137.3 ms persistent; a walk over 148 - R SMs
   // leaving R to the panel stream did worse still: R = 8 / 16 / 32 gave
