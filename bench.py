@@ -320,6 +320,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     distributed = world > 1 or args.force_dist
     if distributed:
+        # one CTA per tile in the GEMMs (read at the library's first launch):
+        # the k-panel broadcasts' NCCL kernels need SMs while a panel's GEMM
+        # runs, which the persistent walk would hold until it ends
+        os.environ.setdefault("DDB_TMA_PERSISTENT", "0")
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")

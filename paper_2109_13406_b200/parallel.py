@@ -23,6 +23,11 @@ Data movement (operands start on rank 0, the root, and C ends there):
 
 The compute callable is injectable so the host logic is testable on CPU with
 the gloo backend (tests/test_parallel_gloo.py); the default is the CUDA path.
+
+Set ``DDB_TMA_PERSISTENT=0`` before the first GEMM of a process that overlaps
+these broadcasts with compute (bench.py does): the library's default
+persistent tile walk holds every SM until a GEMM ends, and NCCL's kernels
+need SMs to run beside it.
 """
 
 from __future__ import annotations
