@@ -75,7 +75,7 @@ constexpr int NT = 256;       // 8 consumer warps
 // thread); 0: thread 0 of consumer warp 0 doubles as the producer
 constexpr int NTK = NT + (DDB_TMA_WS ? 128 : 0);
 #ifndef DDB_TMA_REGC
-#define DDB_TMA_REGC 208      // consumer registers per thread after setmaxnreg (240: 240.1 ms at 8192^3, 208: 238.8)
+#define DDB_TMA_REGC 240      // consumer registers per thread after setmaxnreg (final kernel: 240 225.8 ms at 8192^3, 224 226.6, 208 226.2, 184 237.4 with spills)
 #endif
 constexpr int REG_CONSUMER = DDB_TMA_REGC, REG_PRODUCER = 24;
 constexpr int TM = 8, TN = 4, RX = 32, RY = 32;
